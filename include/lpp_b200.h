@@ -1,0 +1,152 @@
+/* lpp_b200.h — C ABI of the B200-native LPP-SGD hot path.
+ *
+ * This is the drop-in boundary that replaces the reference's only native
+ * component, the CPython module `asyncsgd._atomics`
+ * (/root/reference/pkg/src/asyncsgd/_atomics.c:394-412), and the numpy
+ * work the engine does around it (engine.py:199-229, 343-355, 418-421).
+ *
+ * Conventions (mirroring _atomics.c:1-7 and :20-39):
+ *   - plain pointers and sizes only; no torch / CUDA types in signatures
+ *     (streams are passed as `void*` = cudaStream_t);
+ *   - the caller owns every buffer it passes in; functions never keep them;
+ *   - every function returns 0 on success and a negative LPP_E* code on
+ *     error; lpp_last_error() returns the thread-local message of the most
+ *     recent failure (the reference raises ValueError/IndexError instead);
+ *   - device functions are asynchronous on the given stream; they are safe
+ *     to call concurrently from many host threads on different streams;
+ *   - element order inside one call is unspecified (the GPU has no
+ *     "ascending" order), but every element update is a single atomic
+ *     read-modify-write in atomic modes, so concurrent updates at the same
+ *     index are never lost, and every 32-bit element is read/written
+ *     untorn (_atomics.c:58-74 guarantees the same for fp64).
+ */
+#ifndef LPP_B200_H
+#define LPP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LPP_ABI_VERSION 1
+
+/* error codes */
+#define LPP_OK 0
+#define LPP_E_VALUE -1   /* bad size / alignment / argument  (ref: ValueError) */
+#define LPP_E_INDEX -2   /* index or range out of bounds     (ref: IndexError) */
+#define LPP_E_CUDA -3    /* CUDA runtime error                                */
+#define LPP_E_NOMEM -4   /* allocation failed                                 */
+
+/* apply modes (K1/K2, K4) */
+#define LPP_MODE_PLAIN 0 /* ld/st read-modify-write: Hogwild "classic", may lose
+                            concurrent updates; for single-writer use only     */
+#define LPP_MODE_RED 1   /* red.global.add.v4.f32: element-atomic, default      */
+#define LPP_MODE_BULK 2  /* cp.reduce.async.bulk .add.f32 from shared memory   */
+
+int lpp_abi_version(void);
+const char* lpp_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* host atomics (K6) — replace _atomics.{load,store,fetch_add}_i64     */
+/* (_atomics.c:125-183).  Operate on caller-owned host int64 cells,    */
+/* e.g. numpy buffers or a POSIX shared-memory control block.          */
+/* Memory order: acquire loads, release stores, acq_rel RMW.           */
+int64_t lpp_atomic_load_i64(const int64_t* p);
+void lpp_atomic_store_i64(int64_t* p, int64_t v);
+int64_t lpp_atomic_fetch_add_i64(int64_t* p, int64_t delta);
+/* returns 1 if *p was `expected` and is now `desired`, else 0 */
+int lpp_atomic_cas_i64(int64_t* p, int64_t expected, int64_t desired);
+/* Spin (with exponential back-off sleeps up to max_sleep_us) until
+ * *p >= target; returns the value seen, or INT64_MIN if *abort_flag != 0
+ * first (abort_flag may be NULL).  Releases no locks: call from a thread
+ * that may block (the Python binding drops the GIL around it). */
+int64_t lpp_atomic_wait_ge_i64(const int64_t* p, int64_t target,
+                               const int64_t* abort_flag, int max_sleep_us);
+
+/* ------------------------------------------------------------------ */
+/* arenas: flat fp32 parameter vectors in device memory (a1)           */
+/* replace ParamStore.values (paramstore.py:59-77)                     */
+typedef struct lpp_arena* lpp_arena_t;
+
+/* cudaMalloc'd, 256-byte aligned, zero-filled, IPC-exportable */
+int lpp_arena_create(int device, size_t n_elems, lpp_arena_t* out);
+int lpp_arena_destroy(lpp_arena_t arena);
+float* lpp_arena_data(lpp_arena_t arena);
+size_t lpp_arena_size(lpp_arena_t arena);
+int lpp_arena_device(lpp_arena_t arena);
+
+/* Multi-process peer mapping (one process per GPU, NVLink P2P).
+ * export writes LPP_IPC_HANDLE_BYTES bytes to handle_out. */
+#define LPP_IPC_HANDLE_BYTES 64
+int lpp_arena_export_ipc(lpp_arena_t arena, void* handle_out);
+int lpp_ipc_open(int device, const void* handle, float** ptr_out);
+int lpp_ipc_close(int device, float* ptr);
+/* Single-process peer access: device `device` may load/store/red into
+ * memory of `peer`.  Returns 0 if enabled (or already enabled). */
+int lpp_enable_peer_access(int device, int peer);
+int lpp_can_access_peer(int device, int peer, int* out);
+
+/* ------------------------------------------------------------------ */
+/* K1/K2 apply — replaces ParamStore.sub_assign -> accum_cas_f64        */
+/* (paramstore.py:121-136, _atomics.c:312-344; call site engine.py:355)*/
+/*
+ *   for e in [0, n):
+ *     g' = g[e] + wd * x[e]                (wd != 0 only)
+ *     m[e] = mu * m[e] + g'                (mu != 0 only; m is per-stream)
+ *     x[e] += -(lr * (mu != 0 ? m[e] : g'))  atomically per element
+ *
+ * x, g and m are already offset to the block start (x = arena + lo).
+ * lr: if lr_dev != NULL the learning rate is *lr_dev (device scalar, so a
+ * captured CUDA graph can replay with a fresh value), else `lr`.
+ * x, g, m must share the same address alignment modulo 16 bytes.
+ */
+int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float lr,
+                  const float* lr_dev, float mu, float wd, int mode,
+                  void* stream);
+
+/* Reference-shaped accumulate: dst[start + e] += scale * delta[e],
+ * e in [0, n), with dst of length dst_len (range-checked like
+ * _atomics.c:328-333).  fp32 mirror of accum_cas_f64. */
+int lpp_accum(float* dst, size_t dst_len, size_t start, const float* delta,
+              size_t n, float scale, int mode, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* K3 snapshot — replaces ParamStore.snapshot -> snapshot_f64           */
+/* (paramstore.py:97-117, _atomics.c:186-215; call site engine.py:343) */
+/* out[e] = src[e] for e in [0, n), per-element untorn loads.           */
+int lpp_snapshot(const float* src, float* out, size_t n, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* K4 averaging — replaces _averager_body's snapshot + _MeanAllReduce   */
+/* + add_assign(mean - snap) (engine.py:199-229, 418-421).              */
+/*
+ * Owner-computes over the shard [lo, hi) of Q arenas (arenas[q] is the
+ * base of worker q's arena; remote ones are peer / IPC mappings):
+ *   v_q  = arenas[q][e]                        (q = 0..Q-1, loads)
+ *   mean = (((v_0 + v_1) + v_2) + ...) / Q     (fixed order, as np.mean(axis=0))
+ *   arenas[q][e] += mean - v_q                 (atomic per element, mode RED;
+ *                                               plain store of mean-correction
+ *                                               in mode PLAIN)
+ *   mean_out[e - lo] = mean                    (mean_out may be NULL)
+ * Updaters may keep writing the arenas concurrently: their updates are
+ * preserved (the correction is added, not stored).  Q <= LPP_MAX_WORKERS.
+ * `arenas` is a HOST array of Q device pointers.
+ */
+#define LPP_MAX_WORKERS 8
+int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t hi,
+                      float* mean_out, int mode, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* utilities */
+/* Write a buffer of n_bytes (>= L2 size to flush it) on the stream. */
+int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream);
+/* number of SMs of `device` */
+int lpp_sm_count(int device, int* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LPP_B200_H */

@@ -1,0 +1,180 @@
+"""ctypes binding of the C-ABI CUDA library ``lib/liblpp_b200.so``.
+
+The library is the product: there is no CPU fallback.  Importing this
+module fails loudly (ImportError) when the library has not been built, and
+every call that returns a non-zero status raises, mirroring the reference's
+exception contract for ``asyncsgd._atomics`` (``_atomics.c:26-36`` ValueError,
+``:76-84,328-333`` IndexError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+LIB_PATH = LIB_DIR / "liblpp_b200.so"
+
+MODE_PLAIN = 0
+MODE_RED = 1
+MODE_BULK = 2
+MODES = {"plain": MODE_PLAIN, "red": MODE_RED, "bulk": MODE_BULK}
+MAX_WORKERS = 8
+IPC_HANDLE_BYTES = 64
+
+E_VALUE, E_INDEX, E_CUDA, E_NOMEM = -1, -2, -3, -4
+
+
+class LppError(RuntimeError):
+    """A CUDA-side failure reported through the C ABI."""
+
+
+def _load() -> ctypes.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the CUDA extension is required; there is no CPU fallback)"
+        )
+    return ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+
+
+lib = _load()
+
+_c = ctypes
+_size = _c.c_size_t
+_vp = _c.c_void_p
+_i64p = _c.POINTER(_c.c_int64)
+
+_SIGS = {
+    "lpp_abi_version": (_c.c_int, []),
+    "lpp_last_error": (_c.c_char_p, []),
+    "lpp_atomic_load_i64": (_c.c_int64, [_vp]),
+    "lpp_atomic_store_i64": (None, [_vp, _c.c_int64]),
+    "lpp_atomic_fetch_add_i64": (_c.c_int64, [_vp, _c.c_int64]),
+    "lpp_atomic_cas_i64": (_c.c_int, [_vp, _c.c_int64, _c.c_int64]),
+    "lpp_atomic_wait_ge_i64": (_c.c_int64, [_vp, _c.c_int64, _vp, _c.c_int]),
+    "lpp_arena_create": (_c.c_int, [_c.c_int, _size, _c.POINTER(_vp)]),
+    "lpp_arena_destroy": (_c.c_int, [_vp]),
+    "lpp_arena_data": (_vp, [_vp]),
+    "lpp_arena_size": (_size, [_vp]),
+    "lpp_arena_device": (_c.c_int, [_vp]),
+    "lpp_arena_export_ipc": (_c.c_int, [_vp, _vp]),
+    "lpp_ipc_open": (_c.c_int, [_c.c_int, _vp, _c.POINTER(_vp)]),
+    "lpp_ipc_close": (_c.c_int, [_c.c_int, _vp]),
+    "lpp_enable_peer_access": (_c.c_int, [_c.c_int, _c.c_int]),
+    "lpp_can_access_peer": (_c.c_int, [_c.c_int, _c.c_int, _c.POINTER(_c.c_int)]),
+    "lpp_apply_sgd": (
+        _c.c_int,
+        [_vp, _vp, _vp, _size, _c.c_float, _vp, _c.c_float, _c.c_float, _c.c_int, _vp],
+    ),
+    "lpp_accum": (_c.c_int, [_vp, _size, _size, _vp, _size, _c.c_float, _c.c_int, _vp]),
+    "lpp_snapshot": (_c.c_int, [_vp, _vp, _size, _vp]),
+    "lpp_average_shard": (
+        _c.c_int,
+        [_c.POINTER(_vp), _c.c_int, _size, _size, _vp, _c.c_int, _vp],
+    ),
+    "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
+    "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def last_error() -> str:
+    msg = lib.lpp_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str) -> None:
+    if status == 0:
+        return
+    msg = f"{what}: {last_error()}"
+    if status == E_VALUE:
+        raise ValueError(msg)
+    if status == E_INDEX:
+        raise IndexError(msg)
+    if status == E_NOMEM:
+        raise MemoryError(msg)
+    raise LppError(msg)
+
+
+# ---------------------------------------------------------------------------
+# host atomics on numpy int64 cells (K6)
+
+
+def _cell_ptr(buf: np.ndarray, i: int) -> int:
+    if buf.dtype != np.int64 or not buf.flags.c_contiguous:
+        raise ValueError("counter buffer must be C-contiguous int64")
+    if not 0 <= i < buf.shape[0]:
+        raise IndexError(f"index {i} out of range [0, {buf.shape[0]})")
+    return buf.ctypes.data + 8 * i
+
+
+def atomic_load(buf: np.ndarray, i: int = 0) -> int:
+    return int(lib.lpp_atomic_load_i64(_cell_ptr(buf, i)))
+
+
+def atomic_store(buf: np.ndarray, i: int, v: int) -> None:
+    lib.lpp_atomic_store_i64(_cell_ptr(buf, i), int(v))
+
+
+def atomic_fetch_add(buf: np.ndarray, i: int, delta: int) -> int:
+    return int(lib.lpp_atomic_fetch_add_i64(_cell_ptr(buf, i), int(delta)))
+
+
+def atomic_cas(buf: np.ndarray, i: int, expected: int, desired: int) -> bool:
+    return bool(lib.lpp_atomic_cas_i64(_cell_ptr(buf, i), int(expected), int(desired)))
+
+
+def atomic_wait_ge(buf: np.ndarray, i: int, target: int, abort: np.ndarray | None = None,
+                   abort_i: int = 0, max_sleep_us: int = 200) -> int | None:
+    """Block (GIL released) until buf[i] >= target; None if aborted."""
+    ap = _cell_ptr(abort, abort_i) if abort is not None else None
+    v = int(lib.lpp_atomic_wait_ge_i64(_cell_ptr(buf, i), int(target), ap, int(max_sleep_us)))
+    return None if v == -(2**63) else v
+
+
+# ---------------------------------------------------------------------------
+# device-side wrappers (raw pointers; the torch layer lives in arena.py)
+
+
+def sm_count(device: int) -> int:
+    out = _c.c_int(0)
+    check(lib.lpp_sm_count(int(device), _c.byref(out)), "sm_count")
+    return out.value
+
+
+def apply_sgd(x_ptr: int, g_ptr: int, m_ptr: int | None, n: int, lr: float,
+              lr_dev_ptr: int | None, mu: float, wd: float, mode: int, stream: int) -> None:
+    check(
+        lib.lpp_apply_sgd(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, stream),
+        "apply_sgd",
+    )
+
+
+def accum(dst_ptr: int, dst_len: int, start: int, delta_ptr: int, n: int, scale: float,
+          mode: int, stream: int) -> None:
+    check(lib.lpp_accum(dst_ptr, dst_len, start, delta_ptr, n, scale, mode, stream), "accum")
+
+
+def snapshot(src_ptr: int, out_ptr: int, n: int, stream: int) -> None:
+    check(lib.lpp_snapshot(src_ptr, out_ptr, n, stream), "snapshot")
+
+
+def average_shard(arena_ptrs, lo: int, hi: int, mean_out_ptr: int | None, mode: int,
+                  stream: int) -> None:
+    q = len(arena_ptrs)
+    table = (_vp * max(q, 1))(*arena_ptrs)
+    check(lib.lpp_average_shard(table, q, lo, hi, mean_out_ptr, mode, stream), "average_shard")
+
+
+def l2_flush(ptr: int, nbytes: int, stream: int) -> None:
+    check(lib.lpp_l2_flush(ptr, nbytes, stream), "l2_flush")

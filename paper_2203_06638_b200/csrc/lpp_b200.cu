@@ -1,0 +1,726 @@
+// lpp_b200.cu — sm_100a kernels and the C ABI declared in include/lpp_b200.h.
+//
+// Kernels (ids from SURVEY.md §2):
+//   K1/K2  k_apply / k_apply_bulk : Hogwild SGD apply into the shared arena,
+//          replaces ParamStore.sub_assign -> _atomics.accum_cas_f64
+//          (paramstore.py:121-136, _atomics.c:312-344, call site engine.py:355)
+//   K3     k_snapshot             : replica refresh,
+//          replaces ParamStore.snapshot -> snapshot_f64 (_atomics.c:186-215)
+//   K4     k_average              : owner-computes in-place model averaging,
+//          replaces _averager_body + _MeanAllReduce + add_assign(mean - snap)
+//          (engine.py:199-229, 418-421)
+//   K6     host atomics           : _atomics.{load,store,fetch_add}_i64
+//          (_atomics.c:125-183)
+//
+// All of them are HBM- (or NVLink-) bound streaming kernels: 128-bit
+// vectorised, grid-stride with several independent 16-byte loads in flight
+// per thread, grid sized in multiples of the SM count.  Element-atomic
+// updates use the sm_90+ vector reduction red.global.add.v4.f32 (SASS
+// REDG.E.ADD.F32x4) or the bulk-async reduction cp.reduce.async.bulk
+// .add.f32 (SASS UBLKRED) issued from shared memory.
+
+#include "../../include/lpp_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <thread>
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local char g_err[512] = "";
+
+static int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                      \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      return set_err(LPP_E_CUDA, "%s failed: %s", #expr,                    \
+                     cudaGetErrorString(e_));                               \
+  } while (0)
+
+#define LAUNCH_CHECK(name)                                                  \
+  do {                                                                      \
+    cudaError_t e_ = cudaGetLastError();                                    \
+    if (e_ != cudaSuccess)                                                  \
+      return set_err(LPP_E_CUDA, "%s launch failed: %s", name,              \
+                     cudaGetErrorString(e_));                               \
+  } while (0)
+
+extern "C" int lpp_abi_version(void) { return LPP_ABI_VERSION; }
+extern "C" const char* lpp_last_error(void) { return g_err; }
+
+// ---------------------------------------------------------------------------
+// K6: host atomics on caller-owned int64 cells
+
+extern "C" int64_t lpp_atomic_load_i64(const int64_t* p) {
+  return __atomic_load_n(p, __ATOMIC_ACQUIRE);
+}
+extern "C" void lpp_atomic_store_i64(int64_t* p, int64_t v) {
+  __atomic_store_n(p, v, __ATOMIC_RELEASE);
+}
+extern "C" int64_t lpp_atomic_fetch_add_i64(int64_t* p, int64_t delta) {
+  return __atomic_fetch_add(p, delta, __ATOMIC_ACQ_REL);
+}
+extern "C" int lpp_atomic_cas_i64(int64_t* p, int64_t expected, int64_t desired) {
+  return __atomic_compare_exchange_n(p, &expected, desired, 0, __ATOMIC_ACQ_REL,
+                                     __ATOMIC_ACQUIRE)
+             ? 1
+             : 0;
+}
+extern "C" int64_t lpp_atomic_wait_ge_i64(const int64_t* p, int64_t target,
+                                          const int64_t* abort_flag,
+                                          int max_sleep_us) {
+  int spins = 0;
+  int sleep_us = 1;
+  for (;;) {
+    int64_t v = __atomic_load_n(p, __ATOMIC_ACQUIRE);
+    if (v >= target) return v;
+    if (abort_flag && __atomic_load_n(abort_flag, __ATOMIC_ACQUIRE) != 0)
+      return INT64_MIN;
+    if (++spins < 64) continue;
+    std::this_thread::sleep_for(std::chrono::microseconds(sleep_us));
+    if (sleep_us < max_sleep_us) sleep_us *= 2;
+    if (sleep_us > max_sleep_us) sleep_us = max_sleep_us > 0 ? max_sleep_us : 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+static int sm_count_cached(int device) {
+  static std::atomic<int> cache[64];
+  if (device < 0 || device >= 64) return 148;
+  int v = cache[device].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0)
+    n = 148;
+  cache[device].store(n, std::memory_order_relaxed);
+  return n;
+}
+
+static int current_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return sm_count_cached(dev);
+}
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;       // independent 16-byte loads in flight per thread
+constexpr int kBlocksPerSM = 8;  // 8 x 256 threads = 2048 = full SM occupancy
+
+static unsigned grid_for(size_t nvec, int sms) {
+  size_t want = (nvec + kThreads - 1) / kThreads;
+  size_t cap = (size_t)sms * kBlocksPerSM;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (unsigned)want;
+}
+
+// number of leading scalar elements before p is 16-byte aligned
+static inline size_t head_elems(const void* p, size_t n) {
+  size_t mis = ((uintptr_t)p & 15u);
+  size_t h = mis ? (16u - mis) / 4u : 0u;
+  return h < n ? h : n;
+}
+
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+// L2-coherent loads for data other agents may be writing concurrently
+__device__ __forceinline__ float4 ld_cg4(const float* p) {
+  return __ldcg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
+
+// The per-element SGD arithmetic, written with explicit round-to-nearest
+// intrinsics so that ptxas cannot contract it into FMAs; oracle/apply_ref.c
+// restates exactly this sequence.
+template <bool WD, bool MOM>
+__device__ __forceinline__ float sgd_delta(float g, float x, float& m, float lr, float mu,
+                                           float wd) {
+  float gp = g;
+  if (WD) gp = __fadd_rn(gp, __fmul_rn(wd, x));
+  if (MOM) {
+    float mm = __fadd_rn(__fmul_rn(mu, m), gp);
+    m = mm;
+    gp = mm;
+  }
+  return -__fmul_rn(lr, gp);
+}
+
+// ---------------------------------------------------------------------------
+// K1/K2: apply (modes PLAIN and RED)
+
+template <int MODE, bool WD, bool MOM>
+__global__ void __launch_bounds__(kThreads)
+    k_apply(float* x, const float* __restrict__ g, float* m, size_t n, size_t head,
+            size_t nvec, float lr, const float* __restrict__ lr_dev, float mu, float wd) {
+  if (lr_dev) lr = *lr_dev;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float* xb = x + head;
+  const float* gb = g + head;
+  float* mb = MOM ? m + head : nullptr;
+
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * kUnroll) {
+    float4 gr[kUnroll], xr[kUnroll], mr[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+        gr[u] = __ldg(reinterpret_cast<const float4*>(gb) + i);
+        if (WD || MODE == LPP_MODE_PLAIN) xr[u] = ld_cg4(xb + 4 * i);
+        if (MOM) mr[u] = reinterpret_cast<const float4*>(mb)[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+        float4 d;
+        d.x = sgd_delta<WD, MOM>(gr[u].x, xr[u].x, mr[u].x, lr, mu, wd);
+        d.y = sgd_delta<WD, MOM>(gr[u].y, xr[u].y, mr[u].y, lr, mu, wd);
+        d.z = sgd_delta<WD, MOM>(gr[u].z, xr[u].z, mr[u].z, lr, mu, wd);
+        d.w = sgd_delta<WD, MOM>(gr[u].w, xr[u].w, mr[u].w, lr, mu, wd);
+        if (MOM) reinterpret_cast<float4*>(mb)[i] = mr[u];
+        if (MODE == LPP_MODE_PLAIN) {
+          float4 o;
+          o.x = __fadd_rn(xr[u].x, d.x);
+          o.y = __fadd_rn(xr[u].y, d.y);
+          o.z = __fadd_rn(xr[u].z, d.z);
+          o.w = __fadd_rn(xr[u].w, d.w);
+          __stcg(reinterpret_cast<float4*>(xb) + i, o);
+        } else {
+          red_add_v4(xb + 4 * i, d);
+        }
+      }
+    }
+  }
+  // scalar head [0, head) and tail [head + 4*nvec, n): first block only
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      float xv = (WD || MODE == LPP_MODE_PLAIN) ? ld_cg(x + e) : 0.f;
+      float mv = MOM ? m[e] : 0.f;
+      float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
+      if (MOM) m[e] = mv;
+      if (MODE == LPP_MODE_PLAIN)
+        __stcg(x + e, __fadd_rn(xv, d));
+      else
+        red_add_f32(x + e, d);
+    }
+  }
+}
+
+// K1/K2 mode BULK: the CTA computes a 16 KB tile of deltas into shared memory
+// and one thread hands it to the bulk-copy engine as an element-wise atomic
+// add (cp.reduce.async.bulk .add.f32), STAGES tiles in flight per CTA.
+constexpr int kBulkTileV = kThreads * 4;  // float4 per tile (16 KB)
+constexpr int kBulkStages = 3;
+
+template <bool WD, bool MOM>
+__global__ void __launch_bounds__(kThreads)
+    k_apply_bulk(float* x, const float* __restrict__ g, float* m, size_t n, size_t head,
+                 size_t nvec, float lr, const float* __restrict__ lr_dev, float mu,
+                 float wd) {
+  extern __shared__ __align__(128) float4 s_tile[];  // kBulkStages * kBulkTileV
+  if (lr_dev) lr = *lr_dev;
+  float* xb = x + head;
+  const float4* gb = reinterpret_cast<const float4*>(g + head);
+  float4* mb = MOM ? reinterpret_cast<float4*>(m + head) : nullptr;
+  const size_t ntiles = (nvec + kBulkTileV - 1) / kBulkTileV;
+  int stage = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (threadIdx.x == 0)
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kBulkStages - 1) : "memory");
+    __syncthreads();
+    const size_t base = t * kBulkTileV;
+    const int cnt = (int)((nvec - base) < (size_t)kBulkTileV ? (nvec - base) : kBulkTileV);
+    float4* buf = s_tile + stage * kBulkTileV;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int j = threadIdx.x + u * kThreads;
+      if (j < cnt) {
+        float4 gv = __ldg(gb + base + j);
+        float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (WD) xv = ld_cg4(xb + 4 * (base + j));
+        if (MOM) mv = mb[base + j];
+        float4 d;
+        d.x = sgd_delta<WD, MOM>(gv.x, xv.x, mv.x, lr, mu, wd);
+        d.y = sgd_delta<WD, MOM>(gv.y, xv.y, mv.y, lr, mu, wd);
+        d.z = sgd_delta<WD, MOM>(gv.z, xv.z, mv.z, lr, mu, wd);
+        d.w = sgd_delta<WD, MOM>(gv.w, xv.w, mv.w, lr, mu, wd);
+        if (MOM) mb[base + j] = mv;
+        buf[j] = d;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t saddr = (uint32_t)__cvta_generic_to_shared(buf);
+      asm volatile(
+          "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+              xb + 4 * base),
+          "r"(saddr), "r"(cnt * 16)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    stage = (stage + 1) % kBulkStages;
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      float xv = WD ? ld_cg(x + e) : 0.f;
+      float mv = MOM ? m[e] : 0.f;
+      float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
+      if (MOM) m[e] = mv;
+      red_add_f32(x + e, d);
+    }
+  }
+}
+
+template <int MODE, bool WD, bool MOM>
+static void launch_apply_t(float* x, const float* g, float* m, size_t n, size_t head,
+                           size_t nvec, float lr, const float* lr_dev, float mu, float wd,
+                           cudaStream_t st) {
+  int sms = current_sms();
+  if (MODE == LPP_MODE_BULK) {
+    size_t ntiles = (nvec + kBulkTileV - 1) / kBulkTileV;
+    size_t cap = (size_t)sms * 4;  // 3 x 16 KB smem per CTA -> 4 CTAs/SM
+    unsigned grid = (unsigned)(ntiles < cap ? (ntiles ? ntiles : 1) : cap);
+    size_t smem = (size_t)kBulkStages * kBulkTileV * sizeof(float4);
+    k_apply_bulk<WD, MOM><<<grid, kThreads, smem, st>>>(x, g, m, n, head, nvec, lr, lr_dev,
+                                                       mu, wd);
+  } else {
+    k_apply<MODE, WD, MOM><<<grid_for(nvec, sms), kThreads, 0, st>>>(x, g, m, n, head, nvec,
+                                                                    lr, lr_dev, mu, wd);
+  }
+}
+
+template <int MODE>
+static void launch_apply_mode(float* x, const float* g, float* m, size_t n, size_t head,
+                              size_t nvec, float lr, const float* lr_dev, float mu, float wd,
+                              cudaStream_t st) {
+  bool WD = wd != 0.f, MOM = mu != 0.f;
+  if (WD && MOM)
+    launch_apply_t<MODE, true, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+  else if (WD)
+    launch_apply_t<MODE, true, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+  else if (MOM)
+    launch_apply_t<MODE, false, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+  else
+    launch_apply_t<MODE, false, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+}
+
+extern "C" int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float lr,
+                             const float* lr_dev, float mu, float wd, int mode,
+                             void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!x || !g) return set_err(LPP_E_VALUE, "apply_sgd: null x or g");
+  if (mu != 0.f && !m) return set_err(LPP_E_VALUE, "apply_sgd: momentum needs a buffer");
+  if (mode < LPP_MODE_PLAIN || mode > LPP_MODE_BULK)
+    return set_err(LPP_E_VALUE, "apply_sgd: unknown mode %d", mode);
+  if (((uintptr_t)x & 3u) || ((uintptr_t)g & 3u) || (m && ((uintptr_t)m & 3u)))
+    return set_err(LPP_E_VALUE, "apply_sgd: buffers must be 4-byte aligned");
+  if ((((uintptr_t)x ^ (uintptr_t)g) & 15u) || (m && (((uintptr_t)x ^ (uintptr_t)m) & 15u)))
+    return set_err(LPP_E_VALUE,
+                   "apply_sgd: x, g, m must share their alignment modulo 16 bytes");
+  size_t head = head_elems(x, n);
+  size_t nvec = (n - head) / 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (mode) {
+    case LPP_MODE_PLAIN:
+      launch_apply_mode<LPP_MODE_PLAIN>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      break;
+    case LPP_MODE_RED:
+      launch_apply_mode<LPP_MODE_RED>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      break;
+    default:
+      launch_apply_mode<LPP_MODE_BULK>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      break;
+  }
+  LAUNCH_CHECK("apply_sgd");
+  return LPP_OK;
+}
+
+// reference-shaped accumulate: dst[start+e] += scale*delta[e]
+__global__ void __launch_bounds__(kThreads)
+    k_accum(float* d, const float* __restrict__ s, size_t n, size_t head, size_t nvec,
+            float scale, int mode) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (size_t i = tid; i < nvec; i += stride) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(s + head) + i);
+    v.x = __fmul_rn(scale, v.x);
+    v.y = __fmul_rn(scale, v.y);
+    v.z = __fmul_rn(scale, v.z);
+    v.w = __fmul_rn(scale, v.w);
+    if (mode == LPP_MODE_PLAIN) {
+      float4 o = ld_cg4(d + head + 4 * i);
+      o.x = __fadd_rn(o.x, v.x);
+      o.y = __fadd_rn(o.y, v.y);
+      o.z = __fadd_rn(o.z, v.z);
+      o.w = __fadd_rn(o.w, v.w);
+      __stcg(reinterpret_cast<float4*>(d + head) + i, o);
+    } else {
+      red_add_v4(d + head + 4 * i, v);
+    }
+  }
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      float v = __fmul_rn(scale, s[e]);
+      if (mode == LPP_MODE_PLAIN)
+        __stcg(d + e, __fadd_rn(ld_cg(d + e), v));
+      else
+        red_add_f32(d + e, v);
+    }
+  }
+}
+
+extern "C" int lpp_accum(float* dst, size_t dst_len, size_t start, const float* delta,
+                         size_t n, float scale, int mode, void* stream) {
+  if (start > dst_len || n > dst_len - start)
+    return set_err(LPP_E_INDEX, "update range out of bounds");
+  if (n == 0) return LPP_OK;
+  if (!dst || !delta) return set_err(LPP_E_VALUE, "accum: null buffer");
+  if (mode != LPP_MODE_PLAIN && mode != LPP_MODE_RED)
+    return set_err(LPP_E_VALUE, "accum: mode must be PLAIN or RED");
+  float* d = dst + start;
+  if (((uintptr_t)d ^ (uintptr_t)delta) & 15u) {
+    // mismatched alignment: scalar path (treat everything as head)
+    k_accum<<<grid_for((n + 3) / 4, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
+        d, delta, n, n, 0, scale, mode);
+  } else {
+    size_t head = head_elems(d, n);
+    size_t nvec = (n - head) / 4;
+    k_accum<<<grid_for(nvec, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
+        d, delta, n, head, nvec, scale, mode);
+  }
+  LAUNCH_CHECK("accum");
+  return LPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3: snapshot (replica refresh)
+
+__global__ void __launch_bounds__(kThreads)
+    k_snapshot(const float* src, float* __restrict__ out, size_t n, size_t head, size_t nvec) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float* sb = src + head;
+  float4* ob = reinterpret_cast<float4*>(out + head);
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * kUnroll) {
+    float4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) r[u] = ld_cg4(sb + 4 * i);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) ob[i] = r[u];
+    }
+  }
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      out[e] = ld_cg(src + e);
+    }
+  }
+}
+
+extern "C" int lpp_snapshot(const float* src, float* out, size_t n, void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!src || !out) return set_err(LPP_E_VALUE, "snapshot: null buffer");
+  size_t head, nvec;
+  if (((uintptr_t)src ^ (uintptr_t)out) & 15u) {
+    head = n;
+    nvec = 0;
+  } else {
+    head = head_elems(src, n);
+    nvec = (n - head) / 4;
+  }
+  k_snapshot<<<grid_for(nvec ? nvec : 1, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
+      src, out, n, head, nvec);
+  LAUNCH_CHECK("snapshot");
+  return LPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K4: owner-computes averaging over a shard of Q arenas
+
+struct ArenaTable {
+  float* p[LPP_MAX_WORKERS];
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads)
+    k_average(ArenaTable t, int Q, size_t lo, size_t n, size_t head, size_t nvec,
+              float* __restrict__ mean_out) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float fq = (float)Q;
+  constexpr int U = 2;  // 2 x Q independent 16-byte loads in flight
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * U) {
+    float4 v[U][LPP_MAX_WORKERS];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+#pragma unroll
+        for (int q = 0; q < LPP_MAX_WORKERS; ++q)
+          if (q < Q) v[u][q] = ld_cg4(t.p[q] + lo + head + 4 * i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+        float4 s = v[u][0];
+#pragma unroll
+        for (int q = 1; q < LPP_MAX_WORKERS; ++q) {
+          if (q < Q) {
+            s.x = __fadd_rn(s.x, v[u][q].x);
+            s.y = __fadd_rn(s.y, v[u][q].y);
+            s.z = __fadd_rn(s.z, v[u][q].z);
+            s.w = __fadd_rn(s.w, v[u][q].w);
+          }
+        }
+        float4 mean;
+        mean.x = __fdiv_rn(s.x, fq);
+        mean.y = __fdiv_rn(s.y, fq);
+        mean.z = __fdiv_rn(s.z, fq);
+        mean.w = __fdiv_rn(s.w, fq);
+#pragma unroll
+        for (int q = 0; q < LPP_MAX_WORKERS; ++q) {
+          if (q < Q) {
+            float4 c;
+            c.x = __fsub_rn(mean.x, v[u][q].x);
+            c.y = __fsub_rn(mean.y, v[u][q].y);
+            c.z = __fsub_rn(mean.z, v[u][q].z);
+            c.w = __fsub_rn(mean.w, v[u][q].w);
+            float* dst = t.p[q] + lo + head + 4 * i;
+            if (MODE == LPP_MODE_PLAIN) {
+              float4 o;
+              o.x = __fadd_rn(v[u][q].x, c.x);
+              o.y = __fadd_rn(v[u][q].y, c.y);
+              o.z = __fadd_rn(v[u][q].z, c.z);
+              o.w = __fadd_rn(v[u][q].w, c.w);
+              __stcg(reinterpret_cast<float4*>(dst), o);
+            } else {
+              red_add_v4(dst, c);
+            }
+          }
+        }
+        if (mean_out) reinterpret_cast<float4*>(mean_out + head)[i] = mean;
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      float vv[LPP_MAX_WORKERS];
+#pragma unroll
+      for (int q = 0; q < LPP_MAX_WORKERS; ++q)
+        if (q < Q) vv[q] = ld_cg(t.p[q] + lo + e);
+      float s = vv[0];
+#pragma unroll
+      for (int q = 1; q < LPP_MAX_WORKERS; ++q)
+        if (q < Q) s = __fadd_rn(s, vv[q]);
+      float mean = __fdiv_rn(s, fq);
+#pragma unroll
+      for (int q = 0; q < LPP_MAX_WORKERS; ++q) {
+        if (q < Q) {
+          float c = __fsub_rn(mean, vv[q]);
+          if (MODE == LPP_MODE_PLAIN)
+            __stcg(t.p[q] + lo + e, __fadd_rn(vv[q], c));
+          else
+            red_add_f32(t.p[q] + lo + e, c);
+        }
+      }
+      if (mean_out) mean_out[e] = mean;
+    }
+  }
+}
+
+extern "C" int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t hi,
+                                 float* mean_out, int mode, void* stream) {
+  if (Q < 1 || Q > LPP_MAX_WORKERS)
+    return set_err(LPP_E_VALUE, "average_shard: Q=%d outside [1, %d]", Q, LPP_MAX_WORKERS);
+  if (hi < lo) return set_err(LPP_E_INDEX, "average_shard: hi < lo");
+  if (!arenas) return set_err(LPP_E_VALUE, "average_shard: null arena table");
+  if (mode != LPP_MODE_PLAIN && mode != LPP_MODE_RED)
+    return set_err(LPP_E_VALUE, "average_shard: mode must be PLAIN or RED");
+  size_t n = hi - lo;
+  if (n == 0) return LPP_OK;
+  ArenaTable t;
+  memset(&t, 0, sizeof(t));
+  for (int q = 0; q < Q; ++q) {
+    if (!arenas[q]) return set_err(LPP_E_VALUE, "average_shard: null arena %d", q);
+    if (((uintptr_t)arenas[q] ^ (uintptr_t)arenas[0]) & 15u)
+      return set_err(LPP_E_VALUE, "average_shard: arenas must share 16-byte alignment");
+    t.p[q] = arenas[q];
+  }
+  if (mean_out && ((((uintptr_t)mean_out) ^ (uintptr_t)(arenas[0] + lo)) & 15u))
+    return set_err(LPP_E_VALUE, "average_shard: mean_out alignment must match the shard");
+  size_t head = head_elems(arenas[0] + lo, n);
+  size_t nvec = (n - head) / 4;
+  unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
+  if (mode == LPP_MODE_PLAIN)
+    k_average<LPP_MODE_PLAIN><<<grid, kThreads, 0, (cudaStream_t)stream>>>(t, Q, lo, n, head,
+                                                                          nvec, mean_out);
+  else
+    k_average<LPP_MODE_RED><<<grid, kThreads, 0, (cudaStream_t)stream>>>(t, Q, lo, n, head,
+                                                                        nvec, mean_out);
+  LAUNCH_CHECK("average_shard");
+  return LPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// arenas + peer mapping
+
+struct lpp_arena {
+  float* ptr;
+  size_t n;
+  int device;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+extern "C" int lpp_arena_create(int device, size_t n_elems, lpp_arena_t* out) {
+  if (!out) return set_err(LPP_E_VALUE, "arena_create: null out");
+  *out = nullptr;
+  DeviceGuard guard(device);
+  float* p = nullptr;
+  size_t bytes = (n_elems ? n_elems : 1) * sizeof(float);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess)
+    return set_err(LPP_E_NOMEM, "arena_create: cudaMalloc(%zu) failed: %s", bytes,
+                   cudaGetErrorString(e));
+  e = cudaMemset(p, 0, bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return set_err(LPP_E_CUDA, "arena_create: memset failed: %s", cudaGetErrorString(e));
+  }
+  lpp_arena* a = new lpp_arena{p, n_elems, device};
+  *out = a;
+  return LPP_OK;
+}
+
+extern "C" int lpp_arena_destroy(lpp_arena_t a) {
+  if (!a) return LPP_OK;
+  DeviceGuard guard(a->device);
+  cudaError_t e = cudaFree(a->ptr);
+  delete a;
+  if (e != cudaSuccess)
+    return set_err(LPP_E_CUDA, "arena_destroy: %s", cudaGetErrorString(e));
+  return LPP_OK;
+}
+
+extern "C" float* lpp_arena_data(lpp_arena_t a) { return a ? a->ptr : nullptr; }
+extern "C" size_t lpp_arena_size(lpp_arena_t a) { return a ? a->n : 0; }
+extern "C" int lpp_arena_device(lpp_arena_t a) { return a ? a->device : -1; }
+
+extern "C" int lpp_arena_export_ipc(lpp_arena_t a, void* handle_out) {
+  if (!a || !handle_out) return set_err(LPP_E_VALUE, "export_ipc: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == LPP_IPC_HANDLE_BYTES, "ipc handle size");
+  DeviceGuard guard(a->device);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, a->ptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return LPP_OK;
+}
+
+extern "C" int lpp_ipc_open(int device, const void* handle, float** ptr_out) {
+  if (!handle || !ptr_out) return set_err(LPP_E_VALUE, "ipc_open: null argument");
+  DeviceGuard guard(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr_out = (float*)p;
+  return LPP_OK;
+}
+
+extern "C" int lpp_ipc_close(int device, float* ptr) {
+  DeviceGuard guard(device);
+  CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return LPP_OK;
+}
+
+extern "C" int lpp_can_access_peer(int device, int peer, int* out) {
+  if (!out) return set_err(LPP_E_VALUE, "can_access_peer: null out");
+  CUDA_TRY(cudaDeviceCanAccessPeer(out, device, peer));
+  return LPP_OK;
+}
+
+extern "C" int lpp_enable_peer_access(int device, int peer) {
+  if (device == peer) return LPP_OK;
+  DeviceGuard guard(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return LPP_OK;
+  }
+  if (e != cudaSuccess)
+    return set_err(LPP_E_CUDA, "enable_peer_access(%d -> %d): %s", device, peer,
+                   cudaGetErrorString(e));
+  return LPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// utilities
+
+extern "C" int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream) {
+  if (!scratch) return set_err(LPP_E_VALUE, "l2_flush: null scratch");
+  CUDA_TRY(cudaMemsetAsync(scratch, 0x5a, n_bytes, (cudaStream_t)stream));
+  return LPP_OK;
+}
+
+extern "C" int lpp_sm_count(int device, int* out) {
+  if (!out) return set_err(LPP_E_VALUE, "sm_count: null out");
+  CUDA_TRY(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device));
+  return LPP_OK;
+}

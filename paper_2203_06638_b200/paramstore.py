@@ -1,0 +1,164 @@
+"""Arena-backed shared parameter store with the reference ``ParamStore`` API.
+
+Drop-in for ``asyncsgd.paramstore`` (``/root/reference/pkg/src/asyncsgd/paramstore.py``):
+
+* ``AtomicCounter`` (``paramstore.py:19-39``): a host int64 cell updated
+  with the C ABI's acquire/release/acq_rel atomics (K6); the cell can live
+  in a numpy array or in a POSIX shared-memory control block (multi-process
+  groups).
+* ``ParamStore`` (``paramstore.py:59-136``): ``values`` is an fp32 device
+  arena (``Arena``) instead of an fp64 numpy vector; ``snapshot`` is K3,
+  ``sub_assign``/``add_assign`` are K1 (``lpp_accum``) — element-atomic
+  device reductions, so concurrent updates from many CUDA streams are never
+  lost (``_atomics.c:58-74``).  Device ops are asynchronous on the current
+  torch stream (or the ``stream=`` given); ``read``/``write`` synchronise.
+
+Not yet implemented: write tags (``track_writes=True``, K5 in SURVEY §2).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .arena import Arena, stream_ptr
+
+
+class AtomicCounter:
+    """A shared int64 with atomic fetch-and-add (``paramstore.py:19-39``)."""
+
+    __slots__ = ("_cell", "_i")
+
+    def __init__(self, initial: int = 0, cell: np.ndarray | None = None, index: int = 0):
+        if cell is None:
+            cell = np.array([initial], dtype=np.int64)
+            index = 0
+        else:
+            N.atomic_store(cell, index, initial)
+        self._cell = cell
+        self._i = index
+
+    def read_and_inc(self) -> int:
+        return N.atomic_fetch_add(self._cell, self._i, 1)
+
+    def read(self) -> int:
+        return N.atomic_load(self._cell, self._i)
+
+    def add(self, delta: int) -> int:
+        return N.atomic_fetch_add(self._cell, self._i, delta)
+
+    def store(self, value: int) -> None:
+        N.atomic_store(self._cell, self._i, value)
+
+    def cas(self, expected: int, desired: int) -> bool:
+        return N.atomic_cas(self._cell, self._i, expected, desired)
+
+    def wait_ge(self, target: int, abort: "AtomicCounter | None" = None) -> int | None:
+        """Block without the GIL until the value is >= target (None: aborted)."""
+        if abort is None:
+            return N.atomic_wait_ge(self._cell, self._i, target)
+        return N.atomic_wait_ge(self._cell, self._i, target, abort._cell, abort._i)
+
+
+@dataclass(frozen=True)
+class Snapshot:
+    """Per-element copy of a store (``paramstore.py:42-56``); values on device."""
+
+    values: torch.Tensor
+    order: int
+    tags: np.ndarray | None = None
+    tag_indices: np.ndarray | None = None
+
+
+def _as_device_f32(delta, device: int) -> torch.Tensor:
+    t = torch.as_tensor(delta)
+    if t.dim() != 1:
+        t = t.reshape(-1)
+    return t.to(device=f"cuda:{device}", dtype=torch.float32).contiguous()
+
+
+class ParamStore:
+    """One worker's shared arena plus its two shared counters."""
+
+    def __init__(self, initial, track_writes: bool = False, device: int | None = None,
+                 mode: str = "red"):
+        arr = torch.as_tensor(np.asarray(initial) if not torch.is_tensor(initial) else initial)
+        if arr.dim() != 1:
+            raise ValueError("parameter vector must be one-dimensional")
+        if track_writes:
+            raise NotImplementedError("write tags (K5) are not implemented on the GPU path yet")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self.dim = int(arr.shape[0])
+        self.arena = Arena(self.dim, self.device)
+        if self.dim:
+            self.arena.tensor.copy_(arr.to(torch.float32))
+        self.mode = N.MODES[mode]
+        self.sample_counter = AtomicCounter(0)
+        self.update_order_counter = AtomicCounter(0)
+        self.tags = None
+
+    @property
+    def values(self) -> torch.Tensor:
+        return self.arena.tensor
+
+    # -- element access ---------------------------------------------------
+
+    def read(self, index: int) -> float:
+        if not 0 <= index < self.dim:
+            raise IndexError(f"index {index} out of range [0, {self.dim})")
+        return float(self.arena.tensor[index].item())
+
+    def write(self, index: int, value: float) -> None:
+        if not 0 <= index < self.dim:
+            raise IndexError(f"index {index} out of range [0, {self.dim})")
+        self.arena.tensor[index] = value
+        torch.cuda.synchronize(self.device)
+
+    # -- counters -----------------------------------------------------------
+
+    def read_and_inc(self) -> int:
+        return self.sample_counter.read_and_inc()
+
+    def claim_update_order(self) -> int:
+        return self.update_order_counter.read_and_inc() + 1
+
+    # -- snapshots (K3) -----------------------------------------------------
+
+    def snapshot(self, tag_indices=None, out: torch.Tensor | None = None,
+                 stream: torch.cuda.Stream | None = None) -> Snapshot:
+        order = self.sample_counter.read()
+        if out is None:
+            out = torch.empty(self.dim, dtype=torch.float32, device=f"cuda:{self.device}")
+        elif out.numel() != self.dim or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError("snapshot out must be a contiguous fp32 vector of the store's length")
+        if self.dim:
+            N.snapshot(self.arena.ptr, out.data_ptr(), self.dim, stream_ptr(stream))
+        return Snapshot(out, order)
+
+    # -- range updates (K1) -------------------------------------------------
+
+    def sub_assign(self, start: int, delta, stamp: int = 0,
+                   stream: torch.cuda.Stream | None = None) -> None:
+        self._accum(start, delta, -1.0, stream)
+
+    def add_assign(self, start: int, delta, stamp: int = 0,
+                   stream: torch.cuda.Stream | None = None) -> None:
+        self._accum(start, delta, 1.0, stream)
+
+    def _accum(self, start: int, delta, scale: float, stream) -> None:
+        d = _as_device_f32(delta, self.device)
+        n = d.numel()
+        if start < 0 or start + n > self.dim:
+            raise IndexError("update range out of bounds")
+        mode = self.mode if self.mode != N.MODE_BULK else N.MODE_RED
+        N.accum(self.arena.ptr, self.dim, int(start), d.data_ptr(), n, scale, mode,
+                stream_ptr(stream))
+        if stream is not None:
+            # `d` may be a temporary of the current stream: keep its block
+            # reserved until the kernel on `stream` has consumed it
+            d.record_stream(stream)

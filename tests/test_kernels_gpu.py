@@ -1,0 +1,249 @@
+"""K1-K4 parity on the GPU: every kernel vs the C oracle (oracle/apply_ref.c)
+on the same seeded inputs — bit-exact, since each element is written by one
+thread in one fixed operation order — plus the reference's store worked
+examples and its concurrency stress oracles (test_paramstore.py:63-270)
+ported to CUDA streams."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def N():
+    from paper_2203_06638_b200 import _native
+
+    return _native
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import native
+
+    return native
+
+
+def _cuda(a):
+    return torch.from_numpy(a).cuda()
+
+
+SIZES = [0, 1, 3, 4, 5, 17, 1023, 4096 + 3, 100_003, 1_000_001]
+
+
+@pytest.mark.parametrize("mode", ["plain", "red", "bulk"])
+@pytest.mark.parametrize("mu,wd", [(0.0, 0.0), (0.9, 0.0), (0.0, 5e-4), (0.9, 5e-4)])
+def test_apply_sgd_bitexact_vs_oracle(N, orc, mode, mu, wd):
+    from paper_2203_06638_b200.arena import Arena
+
+    gen = np.random.default_rng(17)
+    for n in SIZES:
+        for off in (0, 1, 2, 3):
+            total = n + off + 5
+            x = gen.normal(size=total).astype(np.float32)
+            g = (1e-2 * gen.normal(size=total)).astype(np.float32)
+            m = gen.normal(size=total).astype(np.float32)
+            lr = np.float32(0.0375)
+            ax, ag, am = Arena(total, 0), Arena(total, 0), Arena(total, 0)
+            ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g)), am.tensor.copy_(_cuda(m))
+            N.apply_sgd(ax.ptr + 4 * off, ag.ptr + 4 * off, am.ptr + 4 * off if mu else None, n,
+                        float(lr), None, mu, wd, N.MODES[mode], 0)
+            torch.cuda.synchronize()
+            xo, mo = x.copy(), m.copy()
+            if n:
+                xv, mv = xo[off:off + n].copy(), mo[off:off + n].copy()
+                orc.apply_sgd(xv, g[off:off + n].copy(), mv if mu else None, float(lr), mu, wd)
+                xo[off:off + n] = xv
+                mo[off:off + n] = mv
+            got = ax.tensor.cpu().numpy()
+            assert np.array_equal(got, xo), (mode, n, off)
+            if mu:
+                assert np.array_equal(am.tensor.cpu().numpy(), mo), (mode, n, off)
+            for a in (ax, ag, am):
+                a.close()
+
+
+def test_apply_sgd_lr_from_device_scalar(N, orc):
+    from paper_2203_06638_b200.arena import Arena
+
+    n = 4099
+    gen = np.random.default_rng(3)
+    x = gen.normal(size=n).astype(np.float32)
+    g = gen.normal(size=n).astype(np.float32)
+    ax, ag = Arena(n, 0), Arena(n, 0)
+    ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g))
+    lr_dev = torch.tensor([0.125], device="cuda")
+    N.apply_sgd(ax.ptr, ag.ptr, None, n, 99.0, lr_dev.data_ptr(), 0.0, 0.0, N.MODE_RED, 0)
+    torch.cuda.synchronize()
+    orc.apply_sgd(x, g, None, 0.125)
+    assert np.array_equal(ax.tensor.cpu().numpy(), x)
+
+
+def test_apply_sgd_rejects_bad_arguments(N):
+    from paper_2203_06638_b200.arena import Arena
+
+    a = Arena(64, 0)
+    with pytest.raises(ValueError):
+        N.apply_sgd(a.ptr, a.ptr + 4, None, 8, 0.1, None, 0.0, 0.0, N.MODE_RED, 0)  # misaligned pair
+    with pytest.raises(ValueError):
+        N.apply_sgd(a.ptr, a.ptr, None, 8, 0.1, None, 0.9, 0.0, N.MODE_RED, 0)  # momentum w/o buffer
+    with pytest.raises(ValueError):
+        N.apply_sgd(a.ptr, a.ptr, None, 8, 0.1, None, 0.0, 0.0, 7, 0)
+
+
+def test_store_worked_examples(golden_scalars):
+    from paper_2203_06638_b200.paramstore import ParamStore
+
+    st = ParamStore(np.array([1.0, 2.0, 3.0, 4.0]))
+    st.sub_assign(1, np.array([-10.0, -20.0]))
+    assert st.values.cpu().tolist() == golden_scalars["paramstore"]["sub_assign"]
+    st2 = ParamStore(np.array([2.0, 4.0]))
+    st2.add_assign(0, np.array([-1.0, 1.0]))
+    assert st2.values.cpu().tolist() == golden_scalars["paramstore"]["add_assign"]
+    st3 = ParamStore(np.array([1.0, 2.0, 3.0]))
+    st3.sub_assign(0, np.zeros(3))
+    assert st3.values.cpu().tolist() == [1.0, 2.0, 3.0]
+    with pytest.raises(IndexError):
+        ParamStore(np.zeros(4)).sub_assign(3, np.array([1.0, 1.0]))
+    with pytest.raises(IndexError):
+        ParamStore(np.zeros(4)).add_assign(-1, np.array([1.0]))
+    with pytest.raises(ValueError):
+        ParamStore(np.zeros((2, 2)))
+
+
+def test_store_counters_and_snapshot():
+    from paper_2203_06638_b200.paramstore import ParamStore
+
+    st = ParamStore(np.array([1.0, 2.0, 3.0]))
+    assert st.read_and_inc() == 0 and st.read_and_inc() == 1
+    snap = st.snapshot()
+    assert snap.order == 2 and snap.values.cpu().tolist() == [1.0, 2.0, 3.0]
+    st.write(0, 9.0)
+    assert snap.values[0].item() == 1.0 and st.read(0) == 9.0
+    assert st.claim_update_order() == 1 and st.claim_update_order() == 2
+    assert ParamStore(np.zeros(0)).snapshot().values.shape == (0,)
+
+
+@pytest.mark.parametrize("n", [1, 5, 1024, 1_000_003])
+def test_snapshot_exact_and_misaligned(N, n):
+    from paper_2203_06638_b200.arena import Arena
+
+    src = Arena(n + 8, 0)
+    src.tensor.copy_(torch.randn(n + 8, device="cuda"))
+    for so, do in ((0, 0), (1, 1), (3, 3), (1, 2)):
+        out = torch.full((n + 8,), -7.0, device="cuda")
+        N.snapshot(src.ptr + 4 * so, out.data_ptr() + 4 * do, n, 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out[do:do + n], src.tensor[so:so + n])
+        assert bool((out[:do] == -7.0).all()) and bool((out[do + n:] == -7.0).all())
+
+
+@pytest.mark.parametrize("Q", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("mode", ["plain", "red"])
+def test_average_shard_bitexact_vs_oracle(N, orc, Q, mode):
+    from paper_2203_06638_b200.arena import Arena
+
+    gen = np.random.default_rng(Q)
+    n = 50_001
+    xs = [gen.normal(size=n).astype(np.float32) for _ in range(Q)]
+    arenas = [Arena(n, 0) for _ in range(Q)]
+    for a, x in zip(arenas, xs):
+        a.tensor.copy_(_cuda(x))
+    for lo, hi in ((0, n), (1, 777), (3, n - 2), (10_000, 10_001)):
+        mean_dev = torch.zeros(hi - lo + 4, device="cuda")
+        # mean_out must share the shard's alignment: offset by lo % 4
+        off = lo % 4
+        N.average_shard([a.ptr for a in arenas], lo, hi, mean_dev.data_ptr() + 4 * off,
+                        N.MODES[mode], 0)
+        torch.cuda.synchronize()
+        mean_ref = np.zeros(hi - lo, dtype=np.float32)
+        orc.average(xs, lo, hi, mean_ref)
+        for a, x in zip(arenas, xs):
+            assert np.array_equal(a.tensor.cpu().numpy(), x), (Q, mode, lo, hi)
+        assert np.array_equal(mean_dev[off:off + hi - lo].cpu().numpy(), mean_ref)
+
+
+def test_average_conserves_the_worker_mean(N):
+    """Sum over workers of the per-round corrections is ~0 (test_engine.py:152-166),
+    at fp32 tolerance Q * |x| * eps."""
+    from paper_2203_06638_b200.arena import Arena
+
+    Q, n = 4, 200_000
+    arenas = [Arena(n, 0) for _ in range(Q)]
+    for a in arenas:
+        a.tensor.copy_(torch.randn(n, device="cuda"))
+    before = torch.stack([a.tensor.clone() for a in arenas])
+    N.average_shard([a.ptr for a in arenas], 0, n, None, N.MODE_RED, 0)
+    torch.cuda.synchronize()
+    after = torch.stack([a.tensor for a in arenas])
+    total = (after - before).sum(0)
+    assert float(total.abs().max()) <= Q * 4 * 1.2e-7 * float(before.abs().max())
+    # Q=1 averaging is an exact no-op (test_engine.py:169-182)
+    N.average_shard([arenas[0].ptr], 0, n, None, N.MODE_RED, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(arenas[0].tensor, after[0])
+
+
+def test_no_lost_updates_across_streams(N):
+    """K streams hammer the same elements with +1 (test_paramstore.py:320-344):
+    the red path must land every update exactly."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, K, ops = 4096 + 3, 8, 60
+    x = Arena(n, 0)
+    g = torch.full((n,), -1.0, device="cuda")  # x += -(lr * g) = +1 per op
+    streams = [torch.cuda.Stream() for _ in range(K)]
+    torch.cuda.synchronize()
+    for s in streams:
+        for _ in range(ops):
+            N.apply_sgd(x.ptr, g.data_ptr(), None, n, 1.0, None, 0.0, 0.0, N.MODE_RED, s.cuda_stream)
+    torch.cuda.synchronize()
+    assert bool((x.tensor == float(K * ops)).all())
+    # bulk-async reductions are element-atomic too
+    y = Arena(n, 0)
+    for s in streams:
+        for _ in range(ops):
+            N.apply_sgd(y.ptr, g.data_ptr(), None, n, 1.0, None, 0.0, 0.0, N.MODE_BULK, s.cuda_stream)
+    torch.cuda.synchronize()
+    assert bool((y.tensor == float(K * ops)).all())
+
+
+def test_concurrent_disjoint_updates_all_land():
+    """test_paramstore.py:347-361, on two CUDA streams."""
+    from paper_2203_06638_b200.paramstore import ParamStore
+
+    st = ParamStore(np.arange(4, dtype=np.float64))
+    ops = 400
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a = torch.tensor([1.0, 2.0], device="cuda")
+    b = torch.tensor([1.0, 3.0], device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(ops):
+        st.add_assign(0, a, stream=s1)
+        st.sub_assign(2, b, stream=s2)
+    torch.cuda.synchronize()
+    assert st.values.cpu().tolist() == [0 + ops, 1 + 2 * ops, 2 - ops, 3 - 3 * ops]
+
+
+def test_snapshot_elements_are_written_values(N):
+    """Snapshot membership under concurrent writers (test_paramstore.py:221-251):
+    writers add exact integers; every snapshot element must be a value the
+    element actually held (an integer in range), never a torn mix."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, rounds = 1 << 16, 40
+    x = Arena(n, 0)
+    g = torch.full((n,), -1.0, device="cuda")
+    ws, rs = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty(n, device="cuda") for _ in range(rounds)]
+    torch.cuda.synchronize()
+    for r in range(rounds):
+        N.apply_sgd(x.ptr, g.data_ptr(), None, n, 1.0, None, 0.0, 0.0, N.MODE_RED, ws.cuda_stream)
+        N.snapshot(x.ptr, outs[r].data_ptr(), n, rs.cuda_stream)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert bool((o == o.round()).all()) and float(o.min()) >= 0 and float(o.max()) <= rounds

@@ -1,0 +1,135 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol
+include/lpp_b200.h declares, and its host atomics (K6, the replacement of
+_atomics.{load,store,fetch_add}_i64) keep the reference's counter contract
+under real thread contention (test_paramstore.py:133-183)."""
+
+from __future__ import annotations
+
+import re
+import subprocess
+import threading
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2203_06638_b200 import _native as N
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _declared_symbols() -> set[str]:
+    text = (ROOT / "include" / "lpp_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(lpp_[a-z0-9_]+)\s*\(", text))
+
+
+def test_library_exports_every_declared_symbol():
+    declared = _declared_symbols()
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", str(N.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (lpp_[a-z0-9_]+)$", out, flags=re.M))
+    assert declared <= exported, declared - exported
+    assert declared == set(N.EXPORTED), declared ^ set(N.EXPORTED)
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(N.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_abi_version_and_error_channel():
+    assert N.lib.lpp_abi_version() == 1
+    with pytest.raises(IndexError):
+        # range check happens before any device work
+        N.accum(0, 4, 3, 0, 2, 1.0, N.MODE_RED, 0)
+
+
+def test_counter_semantics():
+    from paper_2203_06638_b200.paramstore import AtomicCounter
+
+    c = AtomicCounter(0)
+    assert c.read_and_inc() == 0 and c.read_and_inc() == 1 and c.read() == 2
+    c = AtomicCounter(5)
+    assert c.add(3) == 5 and c.read() == 8
+    c.store(-2)
+    assert c.read() == -2
+    assert c.cas(-2, 7) and not c.cas(-2, 9) and c.read() == 7
+
+
+def _run_threads(bodies):
+    gate = threading.Barrier(len(bodies))
+
+    def wrap(fn):
+        def run():
+            gate.wait()
+            fn()
+        return run
+
+    ts = [threading.Thread(target=wrap(b)) for b in bodies]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+
+
+def test_concurrent_claims_are_unique():
+    from paper_2203_06638_b200.paramstore import AtomicCounter
+
+    c = AtomicCounter(0)
+    got = [[] for _ in range(16)]
+
+    def claim(i):
+        def body():
+            for _ in range(2000):
+                got[i].append(c.read_and_inc())
+        return body
+
+    _run_threads([claim(i) for i in range(16)])
+    flat = sorted(v for g in got for v in g)
+    assert flat == list(range(16 * 2000))
+
+
+def test_cas_elects_exactly_one_opener_per_round():
+    cell = np.zeros(1, dtype=np.int64)
+    wins = [0] * 8
+
+    def body(i):
+        def run():
+            for r in range(500):
+                # everyone tries to open round r+1 from r; exactly one wins
+                while N.atomic_load(cell, 0) < r:
+                    pass
+                if N.atomic_cas(cell, 0, r, r + 1):
+                    wins[i] += 1
+        return run
+
+    _run_threads([body(i) for i in range(8)])
+    assert sum(wins) == 500 and N.atomic_load(cell, 0) == 500
+
+
+def test_wait_ge_returns_and_aborts():
+    cell = np.zeros(2, dtype=np.int64)
+    seen = []
+
+    def waiter():
+        seen.append(N.atomic_wait_ge(cell, 0, 3))
+
+    t = threading.Thread(target=waiter)
+    t.start()
+    for _ in range(3):
+        N.atomic_fetch_add(cell, 0, 1)
+    t.join(5)
+    assert seen == [3]
+    N.atomic_store(cell, 1, 1)
+    assert N.atomic_wait_ge(cell, 0, 100, abort=cell, abort_i=1) is None
+
+
+def test_counter_checks_buffer_type_and_range():
+    with pytest.raises(ValueError):
+        N.atomic_load(np.zeros(1, dtype=np.float64), 0)
+    with pytest.raises(IndexError):
+        N.atomic_load(np.zeros(1, dtype=np.int64), 1)
