@@ -1,0 +1,885 @@
+"""LPP-SGD / LAP-SGD engine on B200, plus the MB-SGD / PL-SGD baselines.
+
+Drop-in for ``asyncsgd.engine`` (``/root/reference/pkg/src/asyncsgd/engine.py``):
+the same ``RunConfig`` (engine.py:34-72, same validation messages),
+``run_experiment(cfg) -> RunResult`` (engine.py:637-642), ``UpdateRecord``,
+``AveragerStamp``, ``MetricsRow``.  The execution model is B200-native:
+
+* worker q = one GPU (or, in-process, one arena on a device) holding the
+  shared fp32 arena x_q (``ParamStore``);
+* updater r of worker q = one CUDA stream driven by one host thread; each
+  step claims slot s from the host atomic counter C^q (engine.py:336),
+  picks lr and the PASSM+ block (engine.py:337-342), then enqueues
+  K3 snapshot -> captured fwd/bwd graph of that block -> K1/K2 apply on its
+  stream (engine.py:343-355).  Updaters never block on the averager;
+  in-flight steps per stream are bounded (``in_flight``) so the slot
+  counter tracks device progress;
+* averager of worker q = one host thread + a high-priority stream.  Round
+  opening follows engine.py:394-412 (any worker's trigger opens the round
+  for all, CAS-elected), and each round is one K4 launch over the shard
+  this worker OWNS, which reads the shard from all Q arenas (peer / NVLink)
+  and adds ``mean - v_q`` into every arena in place (engine.py:418-421)
+  while updaters keep writing.  Averagers (never updaters) exchange one
+  final-flag vote per round so that they stop on the same unanimous round
+  (engine.py:452-453).
+
+``schedule="serialized"`` runs the canonical deterministic interleaving
+(oracle/schedule.py) with the very same step and round kernels;
+it is the parity mode.
+
+Multi-process groups (one process per GPU) attach through
+``paper_2203_06638_b200.group`` (IPC arena mapping + a shared-memory
+control block); in one process, Q workers may share one device (used by the
+parity tests) or spread over the visible devices.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .arena import Arena, enable_peer_access
+from .objectives import ArenaObjective
+from .paramstore import AtomicCounter, ParamStore
+from .partition import Block, BlockChoice, BlockPartition, SelectionReason, select_block
+from .schedules import LrSchedule, SyncScheme, lr_at, sync_every
+from .step import StepProgram
+
+ALGOS = ("mb_sgd", "pl_sgd", "lap_sgd", "lpp_sgd")
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    algo: str
+    objective: ArenaObjective
+    partition: BlockPartition
+    lr: LrSchedule
+    sync: SyncScheme
+    budget: int
+    warm_start_budget: int
+    workers: int = 2
+    updaters: int = 4
+    batch_size: int = 32
+    seed: int = 0
+    eval_interval: int = 0
+    record_mode: str = "light"
+    tag_sample: int = 16
+    quiescent: bool = False
+    epoch_partition: bool = False
+    round_budget: int | None = None
+    # --- B200 extensions (defaults keep the reference's semantics) ---
+    schedule: str = "async"          # "async" | "serialized" (canonical parity schedule)
+    momentum: float = 0.0            # per-stream momentum buffers (paper: 0.9)
+    weight_decay: float = 0.0
+    apply_mode: str = "red"          # "red" | "bulk" | "plain" (plain may lose updates)
+    sampling: str = "host"           # "host": reference rng stream, H2D per step; "device": in-graph
+    devices: tuple[int, ...] | None = None   # in-process worker -> device map
+    use_graphs: bool = True
+    in_flight: int = 2
+    evaluate: bool = True            # compute the initial/final MetricsRow losses
+
+    def __post_init__(self):
+        if self.algo not in ALGOS:
+            raise ValueError(f"unknown algorithm {self.algo!r}")
+        if self.algo in ("mb_sgd", "pl_sgd") and self.updaters != 1:
+            raise ValueError(f"{self.algo} is sequential per worker; set updaters=1")
+        if self.record_mode not in ("off", "light", "full"):
+            raise ValueError(f"unknown record mode {self.record_mode!r}")
+        if self.workers < 1 or self.updaters < 1 or self.batch_size < 1:
+            raise ValueError("workers, updaters, batch_size must be positive")
+        if self.budget < 1:
+            raise ValueError("budget must be positive")
+        if self.algo == "lpp_sgd" and self.partition.num_blocks < self.updaters:
+            raise ValueError("need at least one block per updater")
+        if self.round_budget is not None:
+            if self.algo in ("mb_sgd", "pl_sgd"):
+                raise ValueError("round_budget applies to asynchronous runs only")
+            if self.round_budget < 1:
+                raise ValueError("round_budget must be positive")
+        if self.schedule not in ("async", "serialized"):
+            raise ValueError(f"unknown schedule {self.schedule!r}")
+        if self.apply_mode not in N.MODES:
+            raise ValueError(f"unknown apply mode {self.apply_mode!r}")
+        if self.sampling not in ("host", "device"):
+            raise ValueError(f"unknown sampling {self.sampling!r}")
+        if self.epoch_partition:
+            raise ValueError("epoch_partition sampling is not implemented on the GPU path yet")
+        if self.workers > N.MAX_WORKERS:
+            raise ValueError(f"at most {N.MAX_WORKERS} workers per averaging group")
+
+
+@dataclass(slots=True)
+class UpdateRecord:
+    worker: int
+    rank: int
+    s: int
+    u: int
+    k_claim: int
+    block_id: int
+    reason: str
+    lr: float
+    flops: int
+    backward_flops: int
+    clean: bool | None
+    tag_indices: np.ndarray | None = None
+    tags: np.ndarray | None = None
+    grad: np.ndarray | None = None
+    snapshot: np.ndarray | None = None
+
+
+@dataclass(slots=True)
+class AveragerStamp:
+    worker: int
+    round: int
+    u: int
+    s_cur: int
+    k_delta: int
+    wall_ms: float
+    snapshot: np.ndarray | None = None
+    mean: np.ndarray | None = None
+
+
+@dataclass(frozen=True)
+class MetricsRow:
+    algo: str
+    seed: int
+    wall_ms: float
+    samples: int
+    round: int
+    train_loss: float
+    grad_norm_sq: float
+    flops: int
+    p_hat: float
+
+    CSV_HEADER = "algo,seed,wall_ms,samples,round,train_loss,grad_norm_sq,flops,p_hat"
+
+    def as_csv(self) -> str:
+        return ",".join([self.algo, str(self.seed), repr(self.wall_ms), str(self.samples),
+                         str(self.round), repr(self.train_loss), repr(self.grad_norm_sq),
+                         str(self.flops), repr(self.p_hat)])
+
+
+@dataclass
+class RunResult:
+    config: RunConfig
+    metrics: list[MetricsRow]
+    final_values: np.ndarray
+    x0: np.ndarray
+    wall_ms: float
+    flops: int
+    p_hat: float
+    counter_finals: list[int]
+    updates: list[UpdateRecord] = field(default_factory=list)
+    stamps: list[AveragerStamp] = field(default_factory=list)
+    device_ms: float = 0.0           # CUDA-event time of the run (first launch -> drain)
+    apply_timing: tuple = ()          # (launches, total apply ms, algorithmic bytes) if timed
+
+
+# ---------------------------------------------------------------------------
+# round control block (host int64 cells; shared memory for multi-process)
+
+
+class RoundControl:
+    """Cells shared by a group's averagers.
+
+    layout: [0] round_calls  [1] stop  [2] abort  [3] drained workers
+            [8 : 8+R]        per-round vote count
+            [8+R : 8+2R]     per-round final-vote count
+    """
+
+    HEADER = 8
+
+    def __init__(self, workers: int, max_rounds: int, buf: np.ndarray | None = None):
+        self.workers = workers
+        self.max_rounds = max_rounds
+        n = self.HEADER + 2 * (max_rounds + 2)
+        if buf is None:
+            buf = np.zeros(n, dtype=np.int64)
+        if buf.shape[0] < n:
+            raise ValueError("control buffer too small")
+        self.buf = buf
+        self.round_calls = _Cell(buf, 0)
+        self.stop = _Cell(buf, 1)
+        self.abort = _Cell(buf, 2)
+        self.drained = _Cell(buf, 3)
+
+    @staticmethod
+    def nbytes(max_rounds: int) -> int:
+        return 8 * (RoundControl.HEADER + 2 * (max_rounds + 2))
+
+    def vote(self, r: int, final: bool) -> None:
+        if r > self.max_rounds:
+            raise RuntimeError("averaging round budget of the control block exceeded")
+        if final:
+            N.atomic_fetch_add(self.buf, self.HEADER + self.max_rounds + 2 + r, 1)
+        N.atomic_fetch_add(self.buf, self.HEADER + r, 1)
+
+    def wait_votes(self, r: int) -> bool | None:
+        """Wait (GIL released) until all workers voted in round r; unanimous-final?"""
+        got = N.atomic_wait_ge(self.buf, self.HEADER + r, self.workers, self.buf, 2)
+        if got is None:
+            return None
+        return N.atomic_load(self.buf, self.HEADER + self.max_rounds + 2 + r) == self.workers
+
+
+class _Cell:
+    """An AtomicCounter-like view of one cell (no initial store)."""
+
+    __slots__ = ("_b", "_i")
+
+    def __init__(self, buf, i):
+        self._b, self._i = buf, i
+
+    def read(self):
+        return N.atomic_load(self._b, self._i)
+
+    def add(self, d):
+        return N.atomic_fetch_add(self._b, self._i, d)
+
+    def store(self, v):
+        N.atomic_store(self._b, self._i, v)
+
+    def cas(self, e, d):
+        return N.atomic_cas(self._b, self._i, e, d)
+
+
+def shard_bounds(dim: int, workers: int) -> list[tuple[int, int]]:
+    """Owner shards [lo, hi), boundaries rounded to 4 elements (16 bytes)."""
+    cuts = [0]
+    for q in range(1, workers):
+        c = (dim * q // workers) // 4 * 4
+        cuts.append(max(cuts[-1], min(c, dim)))
+    cuts.append(dim)
+    return [(cuts[q], cuts[q + 1]) for q in range(workers)]
+
+
+# ---------------------------------------------------------------------------
+# workers
+
+
+class _Worker:
+    def __init__(self, engine: "_Engine", q: int, device: int, x0: torch.Tensor):
+        cfg = engine.cfg
+        self.q = q
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.store = ParamStore(x0, device=device, mode=cfg.apply_mode)
+        self.exited = AtomicCounter(0)
+        self.last_avg_stamp = AtomicCounter(0)
+        self.synced_at = AtomicCounter(0)
+        d = engine.dim
+        U = cfg.updaters
+        with torch.cuda.device(device):
+            self.streams = [torch.cuda.Stream(device=device) for _ in range(U)]
+            self.avg_stream = torch.cuda.Stream(device=device, priority=-1)
+        self.replicas = [Arena(d, device) for _ in range(U)]
+        self.grads = [Arena(d, device) for _ in range(U)]
+        self.moms = [Arena(d, device) for _ in range(U)] if cfg.momentum else [None] * U
+        self.mean_out = torch.zeros(d + 4, dtype=torch.float32, device=self.dev)
+        self.programs: list[StepProgram] = []
+        self.idx_pinned = None
+        self.batch_pinned = None
+
+    def build_programs(self, engine: "_Engine", block_ids_per_rank: list[list[int]]) -> None:
+        cfg = engine.cfg
+        obj = cfg.objective
+        input_mode = "random" if cfg.sampling == "device" else "index"
+        if engine.host_batches:
+            input_mode = "batch"
+        with torch.cuda.device(self.device):
+            for r in range(cfg.updaters):
+                # replica starts as a snapshot of the shared arena
+                N.snapshot(self.store.arena.ptr, self.replicas[r].ptr, engine.dim,
+                           self.streams[r].cuda_stream)
+                blocks = {b: cfg.partition.block(b) for b in block_ids_per_rank[r]}
+                self.programs.append(StepProgram(
+                    obj, self.dev, self.replicas[r].tensor, self.grads[r].tensor, blocks,
+                    cfg.batch_size, self.streams[r], input_mode=input_mode,
+                    use_graphs=cfg.use_graphs, seed=cfg.seed * 7919 + self.q * 101 + r + 1))
+            depth = cfg.in_flight + 2
+            self.idx_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size), dtype=torch.long,
+                                          pin_memory=True)
+            if engine.host_batches:
+                shape = obj.features.shape[1:]
+                self.batch_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size, *shape),
+                                                dtype=obj.features.dtype, pin_memory=True)
+                self.label_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size),
+                                                dtype=torch.long, pin_memory=True)
+            # the warm-up passes touched the replica/grad arenas and BN stats
+            # only; re-snapshot so every replica starts at x0
+            for r in range(cfg.updaters):
+                N.snapshot(self.store.arena.ptr, self.replicas[r].ptr, engine.dim,
+                           self.streams[r].cuda_stream)
+            torch.cuda.synchronize(self.device)
+
+    def close(self):
+        for a in self.replicas + self.grads + [m for m in self.moms if m is not None]:
+            a.close()
+
+
+class _Engine:
+    """Shared machinery of the asynchronous run (in-process workers)."""
+
+    def __init__(self, cfg: RunConfig, host_batches: bool = False, time_apply: bool = False,
+                 group=None):
+        self.cfg = cfg
+        obj = cfg.objective
+        self.dim = obj.dim
+        self.host_batches = host_batches
+        self.time_apply = time_apply
+        self.group = group  # multi-process attachment (None: all workers in this process)
+        self.x0_host = np.asarray(obj.init_params(cfg.seed), dtype=np.float64)
+        x0 = torch.from_numpy(self.x0_host.astype(np.float32))
+        if group is None:
+            devs = cfg.devices or (torch.cuda.current_device(),)
+            self.local_workers = list(range(cfg.workers))
+            dev_of = [devs[q % len(devs)] for q in range(cfg.workers)]
+        else:
+            self.local_workers = [group.rank]
+            dev_of = {group.rank: torch.cuda.current_device()}
+        self.workers: dict[int, _Worker] = {}
+        for q in self.local_workers:
+            self.workers[q] = _Worker(self, q, dev_of[q], x0)
+        if group is None:
+            for a in self.local_workers:
+                for b in self.local_workers:
+                    if self.workers[a].device != self.workers[b].device:
+                        if not enable_peer_access(self.workers[a].device, self.workers[b].device):
+                            raise RuntimeError("averaging needs peer access between worker devices")
+            self.arena_ptrs = [self.workers[q].store.arena.ptr for q in range(cfg.workers)]
+            max_rounds = cfg.workers * (cfg.budget + cfg.updaters) + 8
+            if cfg.round_budget is not None:
+                max_rounds = min(max_rounds, cfg.round_budget + 8)
+            self.ctrl = RoundControl(cfg.workers, max_rounds)
+        else:
+            self.arena_ptrs = group.attach_arenas(self.workers[group.rank].store.arena)
+            self.ctrl = group.control
+        self.shards = shard_bounds(self.dim, cfg.workers)
+        lpp = cfg.algo == "lpp_sgd"
+        ids = [[0] + ([r + 1] if lpp else []) for r in range(cfg.updaters)]
+        for w in self.workers.values():
+            w.build_programs(self, ids)
+        self.flops = AtomicCounter(0)
+        self.updates: list[list[UpdateRecord]] = [[] for _ in range(cfg.workers * cfg.updaters)]
+        self.stamps: list[list[AveragerStamp]] = [[] for _ in range(cfg.workers)]
+        self.errors: list[BaseException] = []
+        self.err_lock = threading.Lock()
+        self.apply_events: list = []
+        self.t0 = 0.0
+        self.final_round_mean = None
+        fwd = obj.forward_cost()
+        self._flops_of = {b: cfg.batch_size * (fwd + obj.backward_cost(cfg.partition.block(b)))
+                          for b in range(cfg.partition.num_blocks + 1)}
+        self._bflops_of = {b: cfg.batch_size * obj.backward_cost(cfg.partition.block(b))
+                           for b in range(cfg.partition.num_blocks + 1)}
+
+    # -- one updater step: K3 -> graph -> K1/K2, all on the updater stream --
+
+    def step(self, w: _Worker, r: int, s: int, block_id: int, lr: float, batch, slot: int):
+        cfg = self.cfg
+        stream = w.streams[r]
+        prog = w.programs[r]
+        blk = cfg.partition.block(block_id)
+        sp = stream.cuda_stream
+        with torch.cuda.stream(stream):
+            if batch is not None:
+                if self.host_batches:
+                    # gather straight into the pinned staging slot, then H2D
+                    t = torch.from_numpy(batch)
+                    torch.index_select(cfg.objective.features, 0, t, out=w.batch_pinned[r, slot])
+                    torch.index_select(cfg.objective.labels, 0, t, out=w.label_pinned[r, slot])
+                    prog.xb.copy_(w.batch_pinned[r, slot], non_blocking=True)
+                    prog.yb.copy_(w.label_pinned[r, slot], non_blocking=True)
+                else:
+                    w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
+                    prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)
+            N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)           # K3
+            prog.run(block_id)                                                        # fwd+bwd
+            off = 4 * blk.start
+            mom = w.moms[r]
+            if self.time_apply:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            N.apply_sgd(w.store.arena.ptr + off, w.grads[r].ptr + off,              # K1/K2
+                        (mom.ptr + off) if mom is not None else None, blk.length, float(lr),
+                        None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode], sp)
+            if self.time_apply:
+                e1.record(stream)
+                bpe = 20 if (cfg.momentum and cfg.weight_decay) else (
+                    16 if (cfg.momentum or cfg.weight_decay) else 12)
+                self.apply_events.append((e0, e1, bpe * blk.length))
+
+    def average(self, owner: int, stream: torch.cuda.Stream, final: bool) -> None:
+        lo, hi = self.shards[owner]
+        w = self.workers[owner]
+        mean_ptr = w.mean_out.data_ptr() + 4 * lo if final else None
+        N.average_shard(self.arena_ptrs, lo, hi, mean_ptr, N.MODE_RED, stream.cuda_stream)
+
+    def fail(self, exc: BaseException) -> None:
+        with self.err_lock:
+            self.errors.append(exc)
+        self.ctrl.abort.store(1)
+        self.ctrl.stop.store(1)
+
+    def record_update(self, q, r, s, u, k_claim, choice: BlockChoice, lr):
+        if self.cfg.record_mode == "off":
+            return
+        b = choice.block_id
+        self.updates[q * self.cfg.updaters + r].append(UpdateRecord(
+            worker=q, rank=r + 1, s=s, u=u, k_claim=k_claim, block_id=b, reason=choice.reason.value,
+            lr=lr, flops=self._flops_of[b], backward_flops=self._bflops_of[b], clean=None))
+
+    def choose(self, s: int, rank: int) -> BlockChoice:
+        cfg = self.cfg
+        if cfg.algo == "lpp_sgd":
+            return select_block(s, cfg.warm_start_budget, cfg.partition.num_blocks, rank)
+        return BlockChoice(0, SelectionReason.WARM_START)
+
+    # -- asynchronous threads -------------------------------------------------
+
+    def updater(self, q: int, r: int) -> None:
+        cfg = self.cfg
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        rank = r + 1
+        gen = np.random.default_rng(np.random.SeedSequence([cfg.seed, q, rank]))
+        n = cfg.objective.n_samples
+        depth = cfg.in_flight + 2
+        events = [torch.cuda.Event() for _ in range(cfg.in_flight)]
+        used = [False] * cfg.in_flight
+        ctrl = self.ctrl
+        s, t = 0, 0
+        try:
+            while s < cfg.budget and not ctrl.stop.read():
+                s = w.store.read_and_inc()
+                lr = lr_at(cfg.lr, s)
+                choice = self.choose(s, rank)
+                k = t % cfg.in_flight
+                if used[k]:
+                    events[k].synchronize()
+                batch = None
+                if cfg.sampling == "host":
+                    batch = gen.integers(0, n, cfg.batch_size)
+                k_claim = w.last_avg_stamp.read()
+                u = w.store.claim_update_order()
+                self.step(w, r, s, choice.block_id, lr, batch, t % depth)
+                events[k].record(w.streams[r])
+                used[k] = True
+                self.flops.add(self._flops_of[choice.block_id])
+                self.record_update(q, r, s, u, k_claim, choice, lr)
+                t += 1
+            w.streams[r].synchronize()
+        except BaseException as exc:  # surfaced after join (engine.py:456-463)
+            self.fail(exc)
+        finally:
+            if w.exited.add(1) + 1 == cfg.updaters:
+                ctrl.drained.add(1)
+
+    def averager(self, q: int) -> None:
+        cfg = self.cfg
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        ctrl = self.ctrl
+        store = w.store
+        s_pre, round_no, backoff = 0, 0, 0.0
+        try:
+            while True:
+                if ctrl.abort.read():
+                    return
+                s_cur = store.sample_counter.read()
+                drain = w.exited.read() == cfg.updaters
+                pending = ctrl.round_calls.read() > round_no
+                fresh = s_cur - s_pre >= sync_every(cfg.sync, s_cur)
+                if not pending:
+                    if fresh and not drain:
+                        ctrl.round_calls.cas(round_no, round_no + 1)
+                    elif drain and ctrl.drained.read() == cfg.workers:
+                        # every worker has drained: open the final round
+                        ctrl.round_calls.cas(round_no, round_no + 1)
+                    elif drain and fresh:
+                        # drained with unsynced work: one more round for it
+                        ctrl.round_calls.cas(round_no, round_no + 1)
+                    else:
+                        time.sleep(backoff)
+                        backoff = min(2e-4, backoff * 2 + 1e-5)
+                        continue
+                backoff = 0.0
+                r = round_no + 1
+                ctrl.vote(r, drain)
+                u_avg = store.claim_update_order()
+                self.average(q, w.avg_stream, final=drain)
+                w.avg_stream.synchronize()
+                w.last_avg_stamp.store(u_avg)
+                w.synced_at.store(s_cur)
+                unanimous = ctrl.wait_votes(r)
+                if unanimous is None:
+                    return
+                round_no = r
+                if cfg.round_budget is not None and round_no >= cfg.round_budget:
+                    ctrl.stop.store(1)
+                self.stamps[q].append(AveragerStamp(
+                    worker=q, round=round_no, u=u_avg, s_cur=s_cur, k_delta=s_cur - s_pre,
+                    wall_ms=(time.perf_counter() - self.t0) * 1e3))
+                s_pre = s_cur
+                if unanimous:
+                    return
+        except BaseException as exc:
+            self.fail(exc)
+
+    # -- drivers ------------------------------------------------------------------
+
+    def _device_span_start(self):
+        evs = {}
+        for q, w in self.workers.items():
+            with torch.cuda.device(w.device):
+                torch.cuda.synchronize(w.device)
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(torch.cuda.current_stream(w.device))
+                evs[q] = e
+        return evs
+
+    def _device_span_end(self, starts) -> float:
+        ms = 0.0
+        for q, w in self.workers.items():
+            with torch.cuda.device(w.device):
+                cur = torch.cuda.current_stream(w.device)
+                for s in w.streams + [w.avg_stream]:
+                    cur.wait_stream(s)
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(cur)
+                e.synchronize()
+                ms = max(ms, starts[q].elapsed_time(e))
+        return ms
+
+    def run_async(self) -> float:
+        cfg = self.cfg
+        starts = self._device_span_start()
+        threads = []
+        for q in self.local_workers:
+            threads.append(threading.Thread(target=self.averager, args=(q,), daemon=True,
+                                            name=f"averager-{q}"))
+        for q in self.local_workers:
+            for r in range(cfg.updaters):
+                threads.append(threading.Thread(target=self.updater, args=(q, r), daemon=True,
+                                                name=f"updater-{q}-{r + 1}"))
+        self.t0 = time.perf_counter()
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        self.wall_ms = (time.perf_counter() - self.t0) * 1e3
+        dev_ms = self._device_span_end(starts)
+        if self.errors:
+            raise RuntimeError("engine thread failed") from self.errors[0]
+        return dev_ms
+
+    def run_serialized(self) -> float:
+        """Canonical deterministic schedule (oracle/schedule.py)."""
+        cfg = self.cfg
+        if self.group is not None:
+            raise ValueError("the serialized schedule runs in one process")
+        n = cfg.objective.n_samples
+        gens = {(q, r): np.random.default_rng(np.random.SeedSequence([cfg.seed, q, r + 1]))
+                for q in range(cfg.workers) for r in range(cfg.updaters)}
+        active = {(q, r): True for q in range(cfg.workers) for r in range(cfg.updaters)}
+        s_pre = [0] * cfg.workers
+        self.round_trace = []
+        starts = self._device_span_start()
+        self.t0 = time.perf_counter()
+        sweep, t = 0, 0
+        while True:
+            for q in range(cfg.workers):
+                w = self.workers[q]
+                for r in range(cfg.updaters):
+                    if not active[(q, r)]:
+                        continue
+                    s = w.store.read_and_inc()
+                    lr = lr_at(cfg.lr, s)
+                    choice = self.choose(s, r + 1)
+                    batch = gens[(q, r)].integers(0, n, cfg.batch_size)
+                    k_claim = w.last_avg_stamp.read()
+                    u = w.store.claim_update_order()
+                    self.step(w, r, s, choice.block_id, lr, batch, t % (cfg.in_flight + 2))
+                    w.streams[r].synchronize()
+                    self.flops.add(self._flops_of[choice.block_id])
+                    self.record_update(q, r, s, u, k_claim, choice, lr)
+                    t += 1
+                    if s >= cfg.budget:
+                        active[(q, r)] = False
+            sweep += 1
+            drained = not any(active.values())
+            counts = [self.workers[q].store.sample_counter.read() for q in range(cfg.workers)]
+            fresh = any(counts[q] - s_pre[q] >= sync_every(cfg.sync, counts[q])
+                        for q in range(cfg.workers))
+            if fresh or drained:
+                rnd = len(self.round_trace) + 1
+                for q in range(cfg.workers):
+                    w = self.workers[q]
+                    u_avg = w.store.claim_update_order()
+                    self.average(q, w.avg_stream, final=drained)
+                    w.avg_stream.synchronize()
+                    w.last_avg_stamp.store(u_avg)
+                    self.stamps[q].append(AveragerStamp(
+                        worker=q, round=rnd, u=u_avg, s_cur=counts[q], k_delta=counts[q] - s_pre[q],
+                        wall_ms=(time.perf_counter() - self.t0) * 1e3))
+                    s_pre[q] = counts[q]
+                self.round_trace.append((rnd, sweep, *counts))
+            if drained:
+                break
+        self.wall_ms = (time.perf_counter() - self.t0) * 1e3
+        return self._device_span_end(starts)
+
+    def final_values(self) -> np.ndarray:
+        """The last round's mean, gathered shard by shard from the owners."""
+        out = np.empty(self.dim, dtype=np.float32)
+        for q, (lo, hi) in enumerate(self.shards):
+            if self.group is None:
+                out[lo:hi] = self.workers[q].mean_out[lo:hi].cpu().numpy()
+            else:
+                pass
+        if self.group is not None:
+            out = self.group.gather_mean(self.workers[self.group.rank].mean_out, self.shards)
+        return out
+
+    def apply_timing(self):
+        if not self.apply_events:
+            return ()
+        ms = sum(e0.elapsed_time(e1) for e0, e1, _ in self.apply_events)
+        nbytes = sum(b for _, _, b in self.apply_events)
+        return (len(self.apply_events), ms, nbytes)
+
+    def close(self):
+        for w in self.workers.values():
+            w.close()
+
+
+# ---------------------------------------------------------------------------
+# synchronous baselines (B1 MB-SGD, B2 PL-SGD) — engine.py:544-629
+
+
+class _SyncEngine:
+    """MB-SGD / PL-SGD with one CUDA-graph step per worker; the collective
+    is NCCL all-reduce in a multi-process group and a fixed-order K4 mean in
+    one process."""
+
+    def __init__(self, cfg: RunConfig, group=None, host_batches: bool = False):
+        self.cfg = cfg
+        obj = cfg.objective
+        self.dim = obj.dim
+        self.group = group
+        self.host_batches = host_batches
+        self.x0_host = np.asarray(obj.init_params(cfg.seed), dtype=np.float64)
+        x0 = torch.from_numpy(self.x0_host.astype(np.float32))
+        devs = cfg.devices or (torch.cuda.current_device(),)
+        self.local = [group.rank] if group is not None else list(range(cfg.workers))
+        self.dev_of = {q: (torch.cuda.current_device() if group is not None else devs[q % len(devs)])
+                       for q in self.local}
+        self.x = {q: Arena(self.dim, self.dev_of[q]) for q in self.local}
+        self.g = {q: Arena(self.dim, self.dev_of[q]) for q in self.local}
+        self.m = {q: Arena(self.dim, self.dev_of[q]) for q in self.local} if cfg.momentum else {}
+        self.gmean = {q: torch.zeros(self.dim + 4, device=f"cuda:{self.dev_of[q]}") for q in self.local}
+        self.stream = {}
+        self.prog = {}
+        full = {0: Block(0, self.dim)}
+        for q in self.local:
+            self.x[q].tensor.copy_(x0)
+            with torch.cuda.device(self.dev_of[q]):
+                self.stream[q] = torch.cuda.Stream()
+                self.prog[q] = StepProgram(obj, torch.device("cuda", self.dev_of[q]), self.x[q].tensor,
+                                           self.g[q].tensor, full, cfg.batch_size, self.stream[q],
+                                           input_mode="batch" if host_batches else
+                                           ("random" if cfg.sampling == "device" else "index"),
+                                           use_graphs=cfg.use_graphs, seed=cfg.seed + q)
+        if group is None and len(set(self.dev_of.values())) > 1:
+            for a in self.local:
+                for b in self.local:
+                    if self.dev_of[a] != self.dev_of[b]:
+                        enable_peer_access(self.dev_of[a], self.dev_of[b])
+        # pinned staging ring for the host-drawn indices: slot k % depth is
+        # rewritten only after the copy that last read it has completed
+        self.depth = 4
+        self.idx_pinned = torch.zeros((self.depth, cfg.workers, cfg.batch_size), dtype=torch.long,
+                                      pin_memory=True)
+        self.slot_events = [[None] * self.depth for _ in range(cfg.workers)]
+        self.k = 0
+        torch.cuda.synchronize()
+
+    def _grads(self, shards: np.ndarray | None):
+        cfg = self.cfg
+        slot = self.k % self.depth
+        self.k += 1
+        for q in self.local:
+            st = self.stream[q]
+            with torch.cuda.stream(st):
+                ev = self.slot_events[q][slot]
+                if ev is not None:
+                    ev.synchronize()
+                if shards is not None:
+                    idx = shards[q * cfg.batch_size:(q + 1) * cfg.batch_size]
+                    if self.host_batches:
+                        t = torch.from_numpy(idx)
+                        self.prog[q].xb.copy_(cfg.objective.features.index_select(0, t).pin_memory(),
+                                              non_blocking=True)
+                        self.prog[q].yb.copy_(cfg.objective.labels.index_select(0, t), non_blocking=True)
+                    else:
+                        self.idx_pinned[slot, q].copy_(torch.from_numpy(idx))
+                        self.prog[q].idx.copy_(self.idx_pinned[slot, q], non_blocking=True)
+                self.prog[q].run(0)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                self.slot_events[q][slot] = ev
+
+    def _apply(self, q, grad_ptr, lr):
+        cfg = self.cfg
+        N.apply_sgd(self.x[q].ptr, grad_ptr, self.m[q].ptr if cfg.momentum else None, self.dim,
+                    float(lr), None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode],
+                    self.stream[q].cuda_stream)
+
+    def _mean_grads(self):
+        """mean_q g_q (engine.py:568) into gmean (fixed order in one process)."""
+        if self.group is not None:
+            q = self.group.rank
+            with torch.cuda.stream(self.stream[q]):
+                t = self.g[q].tensor
+                self.group.allreduce_mean(t)
+            return {q: self.g[q].ptr}
+        for q in self.local:
+            self.stream[q].synchronize()
+        q0 = self.local[0]
+        with torch.cuda.device(self.dev_of[q0]):
+            N.average_shard([self.g[q].ptr for q in range(self.cfg.workers)], 0, self.dim,
+                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, self.stream[q0].cuda_stream)
+            self.stream[q0].synchronize()
+        ptrs = {}
+        for q in self.local:
+            if self.dev_of[q] == self.dev_of[q0]:
+                ptrs[q] = self.gmean[q0].data_ptr()
+            else:
+                self.gmean[q][: self.dim].copy_(self.gmean[q0][: self.dim])
+                ptrs[q] = self.gmean[q].data_ptr()
+        return ptrs
+
+    def _mean_params(self):
+        if self.group is not None:
+            q = self.group.rank
+            with torch.cuda.stream(self.stream[q]):
+                self.group.allreduce_mean(self.x[q].tensor)
+            return
+        for q in self.local:
+            self.stream[q].synchronize()
+        q0 = self.local[0]
+        with torch.cuda.device(self.dev_of[q0]):
+            # x_q = mean exactly (xs[:] = mean, engine.py:612): write the mean, then copy
+            N.average_shard([self.x[q].ptr for q in range(self.cfg.workers)], 0, self.dim,
+                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, self.stream[q0].cuda_stream)
+            for q in self.local:
+                self.x[q].tensor.copy_(self.gmean[q0][: self.dim])
+            self.stream[q0].synchronize()
+
+    def run(self, steps: int | None = None) -> float:
+        cfg = self.cfg
+        steps = cfg.budget if steps is None else steps
+        gen = np.random.default_rng(np.random.SeedSequence([cfg.seed, 0, 1]))
+        n = cfg.objective.n_samples
+        since = 0
+        self.rounds = 0
+        starts = {}
+        for q in self.local:
+            torch.cuda.synchronize(self.dev_of[q])
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(self.stream[q])
+            starts[q] = e
+        self.t0 = time.perf_counter()
+        for k in range(1, steps + 1):
+            lr = lr_at(cfg.lr, k - 1)
+            shards = gen.integers(0, n, cfg.workers * cfg.batch_size) if cfg.sampling == "host" else None
+            self._grads(shards)
+            if cfg.algo == "mb_sgd":
+                if cfg.workers == 1 and self.group is None:
+                    self._apply(0, self.g[0].ptr, lr)
+                else:
+                    ptrs = self._mean_grads()
+                    for q in self.local:
+                        self._apply(q, ptrs[q], lr)
+            else:
+                for q in self.local:
+                    self._apply(q, self.g[q].ptr, lr)
+                since += 1
+                if since >= sync_every(cfg.sync, k) or k == steps:
+                    if cfg.workers > 1:
+                        self._mean_params()
+                    self.rounds += 1
+                    since = 0
+        ms = 0.0
+        for q in self.local:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(self.stream[q])
+            e.synchronize()
+            ms = max(ms, starts[q].elapsed_time(e))
+        self.wall_ms = (time.perf_counter() - self.t0) * 1e3
+        return ms
+
+    def final_values(self) -> np.ndarray:
+        return self.x[self.local[0]].tensor.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# public entry point
+
+
+def _eval_row(cfg, samples, rnd, wall_ms, flops, p_hat, x) -> MetricsRow:
+    obj = cfg.objective
+    if cfg.evaluate:
+        g = obj.full_grad(x)
+        loss = obj.full_loss(x)
+        gn = float((g.double() ** 2).sum())
+    else:
+        loss, gn = float("nan"), float("nan")
+    return MetricsRow(algo=cfg.algo, seed=cfg.seed, wall_ms=wall_ms, samples=samples, round=rnd,
+                      train_loss=loss, grad_norm_sq=gn, flops=flops, p_hat=p_hat)
+
+
+def run_experiment(cfg: RunConfig, group=None, host_batches: bool = False) -> RunResult:
+    """Run one configuration (engine.py:637-642).  ``group`` attaches this
+    process to a multi-GPU group (``paper_2203_06638_b200.group``)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2203_06638_b200 needs a CUDA device (no CPU fallback)")
+    if cfg.algo in ("mb_sgd", "pl_sgd"):
+        eng = _SyncEngine(cfg, group=group, host_batches=host_batches)
+        dev_ms = eng.run()
+        final = eng.final_values()
+        x0 = eng.x0_host
+        rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, x0)]
+        fwd = cfg.objective.forward_cost()
+        flops = cfg.budget * cfg.workers * cfg.batch_size * (fwd + cfg.objective.backward_cost(
+            Block(0, cfg.objective.dim)))
+        rounds = cfg.budget if cfg.algo == "mb_sgd" else eng.rounds
+        rows.append(_eval_row(cfg, cfg.budget, rounds, eng.wall_ms, flops, 1.0, final))
+        return RunResult(config=cfg, metrics=rows, final_values=final, x0=x0, wall_ms=eng.wall_ms,
+                         flops=flops, p_hat=1.0, counter_finals=[cfg.budget] * cfg.workers,
+                         device_ms=dev_ms)
+    eng = _Engine(cfg, host_batches=host_batches, group=group)
+    try:
+        dev_ms = eng.run_serialized() if cfg.schedule == "serialized" else eng.run_async()
+        final = eng.final_values()
+        stamps = [st for per in eng.stamps for st in per]
+        rounds = max((st.round for st in stamps), default=0)
+        flops = eng.flops.read()
+        counters = [eng.workers[q].store.sample_counter.read() for q in eng.local_workers]
+        rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host)]
+        rows.append(_eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, 1.0, final))
+        res = RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
+                        wall_ms=eng.wall_ms, flops=flops, p_hat=1.0, counter_finals=counters,
+                        updates=[u for per in eng.updates for u in per], stamps=stamps,
+                        device_ms=dev_ms, apply_timing=eng.apply_timing())
+        res.round_trace = getattr(eng, "round_trace", None)
+        return res
+    finally:
+        eng.close()

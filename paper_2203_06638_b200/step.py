@@ -1,0 +1,97 @@
+"""One updater's captured training step (the grad_block half of a6/a10).
+
+``StepProgram`` binds an objective to a stream-private replica arena
+(parameters) and gradient arena, and captures, per block id the updater can
+be assigned, one CUDA graph that does
+
+    gather batch (index_select from device data, or a staged host batch)
+    -> zero the block's gradient slice
+    -> forward -> loss -> backward restricted to the block's leaf tensors
+
+so the block gradient lands in ``grads[block.start:block.stop]`` — exactly
+the range the apply kernel then reads.  This is ``Objective.grad_block``
+(objectives.py:286-308) with autograd doing the truncated backward
+("specifying the leaf tensors ... w.r.t. which gradients are
+needed").  The snapshot (K3) and the apply (K1/K2) are launched around the
+replay by the engine through the C ABI.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .partition import Block
+
+
+class StepProgram:
+    def __init__(self, obj, device: torch.device, replica: torch.Tensor, grads: torch.Tensor,
+                 blocks: dict[int, Block], batch_size: int, stream: torch.cuda.Stream,
+                 input_mode: str = "index", use_graphs: bool = True, warmup: int = 2,
+                 seed: int = 0):
+        if input_mode not in ("index", "batch", "random"):
+            raise ValueError(f"unknown input mode {input_mode!r}")
+        self.obj = obj
+        self.device = device
+        self.stream = stream
+        self.input_mode = input_mode
+        self.grads = grads
+        self.bound = obj.bind(replica, grads)
+        self.feats = obj.features_on(device)
+        self.labels = obj.labels_on(device)
+        B = int(batch_size)
+        self.batch_size = B
+        self.idx = torch.zeros(B, dtype=torch.long, device=device)
+        if input_mode == "batch":
+            self.xb = torch.zeros((B, *self.feats.shape[1:]), dtype=self.feats.dtype, device=device)
+            self.yb = torch.zeros(B, dtype=torch.long, device=device)
+        self.loss = torch.zeros((), dtype=torch.float32, device=device)
+        self.gen = None
+        if input_mode == "random":
+            self.gen = torch.Generator(device=device)
+            self.gen.manual_seed(int(seed))
+        self.blocks = dict(blocks)
+        self.leaves = {}
+        for bid, blk in self.blocks.items():
+            first, last = obj.tensors_of_block(blk)
+            self.leaves[bid] = self.bound.params[first:last + 1]
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.use_graphs = use_graphs
+        with torch.cuda.stream(stream):
+            for _ in range(max(warmup, 1)):
+                for bid in self.blocks:
+                    self._body(bid)
+            stream.synchronize()
+            if use_graphs:
+                pool = None
+                for bid in self.blocks:
+                    g = torch.cuda.CUDAGraph()
+                    if self.gen is not None:
+                        g.register_generator_state(self.gen)
+                    with torch.cuda.graph(g, pool=pool, stream=stream):
+                        self._body(bid)
+                    pool = g.pool()
+                    self.graphs[bid] = g
+                stream.synchronize()
+
+    def _body(self, bid: int) -> None:
+        blk = self.blocks[bid]
+        if self.input_mode == "random":
+            torch.randint(0, self.feats.shape[0], (self.batch_size,), generator=self.gen,
+                          device=self.device, out=self.idx)
+        if self.input_mode == "batch":
+            xb, yb = self.xb, self.yb
+        else:
+            xb = self.feats.index_select(0, self.idx)
+            yb = self.labels.index_select(0, self.idx)
+        self.grads[blk.start:blk.stop].zero_()
+        loss = self.obj.loss_on(self.bound, xb, yb)
+        loss.backward(inputs=self.leaves[bid])
+        self.loss.copy_(loss.detach())
+
+    def run(self, bid: int) -> None:
+        """Enqueue block ``bid``'s fwd+bwd on the program's stream."""
+        if self.use_graphs:
+            self.graphs[bid].replay()
+        else:
+            with torch.cuda.stream(self.stream):
+                self._body(bid)
