@@ -1,0 +1,348 @@
+"""Benchmark: LPP-SGD training images/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): ResNet-20 on synthetic CIFAR-10-shaped
+data (N(0,1) images, 50,000 x 3x32x32 fp32 = 614 MB resident in HBM, larger
+than the 126 MB L2), LPP-SGD with U = 4 Hogwild CUDA streams per GPU,
+B = 128 per stream, 4-block PASSM+ partition (balanced_boundaries),
+momentum 0.9, wd 5e-4, cosine lr with warm-up, averaging every tick until
+T/2 then every 16 (SyncScheme defaults).  One *step* = one minibatch on
+every updater stream (U x B images per GPU); K steps are timed with CUDA
+events (max over ranks), after W untimed warm-up steps.
+
+Extra keys beyond the base contract:
+  roofline      the apply kernel (K1/K2), timed live with CUDA events around
+                every launch in the timed region, algorithmic bytes
+                (12 B/elem + 8 with momentum) vs MEASURED_PEAKS.json hbm_gbs
+  e2e           the same metric through Trainer(..., host_batches=True): each
+                step's batch gathered from pinned host memory and copied H2D
+                inside the step, each step's loss copied D2H
+  cpu_baseline  oracle/engine_port.py (threaded CPU LPP-SGD, the reference's
+                compiled _atomics) on this host, bounded sample, rank 0, N=1
+  baselines     the box's own synchronous MB-SGD (same per-GPU B, 1 stream)
+  kernel_sweep  K1/K3 alone at 16M/64M params (HBM roofline evidence)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+B = 128
+U = 4
+N_SAMPLES = 50_000
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+        else:
+            self.out = ""
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reference_arm(args) -> None:
+    """The reference's CPU implementation of the path (oracle port + the
+    reference's compiled _atomics), rank 0 only, same metric/config."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle.engine_port import run_lpp_cpu
+
+    cores = len(os.sched_getaffinity(0))
+    run_lpp_cpu(slots=max(args.warmup, 1) * U - U, updaters=U, batch_size=B)  # warm-up
+    r = run_lpp_cpu(slots=max(args.steps * U - U, 1), updaters=U, batch_size=B, threads=cores)
+    value = r["images"] / r["seconds"]
+    steps = r["minibatches"] / U
+    line = {
+        "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": "resnet20_cifar10_lpp_sgd_cpu", "global_batch": B * U,
+                   "updaters": U, "workers": 1, "batch_per_updater": B},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"],
+                         "kind": "reference" if r["atomics"] == "reference" else "port",
+                         "sample": f"{r['minibatches']} minibatches x {B} images (LPP-SGD, U={U}, "
+                                   f"torch-CPU ResNet-20 grads, store ops = reference _atomics "
+                                   f"({r['atomics']}))"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def build_cfg(obj, steps_slots: int, algo: str = "lpp_sgd", workers: int = 1, sampling: str = "device",
+              updaters: int = U):
+    from paper_2203_06638_b200.engine import RunConfig
+    from paper_2203_06638_b200.partition import balanced_boundaries, make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    total = max(steps_slots, 8)
+    nb = max(updaters, 1)
+    bounds = balanced_boundaries(obj.layer_param_counts, nb) if algo == "lpp_sgd" else (0, obj.dim)
+    return RunConfig(
+        algo=algo, objective=obj, partition=make_partition(obj.dim, bounds),
+        lr=LrSchedule(kind="cosine", alpha0=0.1, total=total, warmup=max(total // 10, 1),
+                      batch_local=B, workers=workers, batch_base=B, boost=(algo == "lpp_sgd")),
+        sync=SyncScheme(total=total, period=16), budget=total,
+        warm_start_budget=max(total // 10, 1), workers=workers,
+        updaters=updaters if algo in ("lap_sgd", "lpp_sgd") else 1, batch_size=B, seed=0,
+        momentum=0.9, weight_decay=5e-4, sampling=sampling, evaluate=False, record_mode="off")
+
+
+def ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    torch.backends.cudnn.benchmark = True
+    group = None
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2203_06638_b200.group import ProcessGroup
+
+        group = ProcessGroup(workers=ws, max_rounds=(args.steps + args.warmup + 4) * U * ws + 64)
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    peaks = _peaks()
+    K, W = args.steps, args.warmup
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if ws == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident throughput (value) ----------------
+    obj = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data="device")
+    cfg = build_cfg(obj, (K + W) * U, workers=ws)
+    tr = Trainer(cfg, group=group, time_apply=True)
+    tr.run(W * U, evaluate=False)
+    barrier()
+    with Clocks(local) as clk:
+        barrier()
+        res = tr.run(K * U, evaluate=False)
+        barrier()
+    dev_ms = max_over_ranks(res.device_ms)
+    slots = sum(res.counter_finals)  # claim-then-process: K*U + U minibatches
+    images = slots * B * ws
+    value = images / (dev_ms / 1e3)
+    n_app, app_ms, app_bytes = res.apply_timing
+    achieved = app_bytes / (app_ms / 1e3) / 1e9
+    rounds = max((st.round for st in res.stamps), default=0)
+    launches = 2 * slots + (rounds if ws > 1 else 0) + 1
+    tr.close()
+    del tr
+
+    line = {
+        "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": ws,
+        "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (N(0,1) CIFAR-10-shaped images, uniform labels; random init)",
+        "config": {"workload": "resnet20_cifar10_lpp_sgd", "model": "resnet20", "global_batch": B * U * ws,
+                   "batch_per_updater": B, "updaters_per_gpu": U, "workers": ws, "blocks": U,
+                   "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
+                   "conv_compute": "bf16 autocast (arena, grads, apply, averaging in fp32)",
+                   "l2": "inputs larger than L2 (614 MB dataset gathered per step)",
+                   "sampling": "in-graph device RNG", "momentum": 0.9, "weight_decay": 5e-4},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)",
+                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],
+                     "traffic": None, "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
+                     "bytes_per_launch": app_bytes / max(n_app, 1),
+                     "note": "d20 arena (1.09 MB) is L2-resident: latency-bound; see kernel_sweep"},
+    }
+
+    # ---------------- clocks ----------------
+    line["clocks"] = clk.summary()
+
+    # ---------------- end to end (host buffers) ----------------
+    if not args.no_e2e:
+        hobj = ResNetObjective("resnet20", n_samples=N_SAMPLES if ws == 1 else N_SAMPLES, seed=0, data="host")
+        hcfg = build_cfg(hobj, (K + W) * U, workers=ws, sampling="host")
+        htr = Trainer(hcfg, group=group, host_batches=True, read_loss=True)
+        htr.run(W * U, evaluate=False)
+        barrier()
+        hres = htr.run(K * U, evaluate=False)
+        barrier()
+        e_ms = max_over_ranks(hres.device_ms)
+        hslots = sum(hres.counter_finals)
+        e2e = hslots * B * ws / (e_ms / 1e3)
+        per_img = 3 * 32 * 32 * 4 + 8
+        line["e2e"] = {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": U * B * per_img,
+                       "d2h_bytes_per_step": U * 4, "api": "Trainer(cfg, host_batches=True, read_loss=True).run",
+                       "losses_read": len(hres.losses),
+                       "last_loss": hres.losses[-1] if hres.losses else None}
+        htr.close()
+        del htr
+
+    # ---------------- MB-SGD baseline on the same box ----------------
+    if not args.no_baselines and ws == 1:
+        mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)
+        mtr = Trainer(mcfg)
+        mtr.run(W * U, evaluate=False)
+        torch.cuda.synchronize()
+        mres = mtr.run(K * U, evaluate=False)
+        mb = K * U * B / (mres.device_ms / 1e3)
+        line["baselines"] = {"mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
+                                        "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
+                             "lpp_over_mb": value / mb}
+        del mtr
+
+    # ---------------- kernel sweep (HBM roofline evidence) ----------------
+    if not args.no_sweep and rank == 0:
+        from paper_2203_06638_b200.arena import Arena
+
+        st = torch.cuda.current_stream().cuda_stream
+        scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        sweep = []
+        for d in (16_000_000, 64_000_000):
+            x, g, m = Arena(d, local), Arena(d, local), Arena(d, local)
+            r_ = Arena(d, local)
+            for name, fn, bpe in (
+                ("apply_red", lambda: N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st), 12),
+                ("apply_red_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st), 20),
+                ("apply_bulk_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_BULK, st), 20),
+                ("snapshot", lambda: N.snapshot(x.ptr, r_.ptr, d, st), 8),
+            ):
+                for _ in range(5):
+                    fn()
+                ts = []
+                for _ in range(10):
+                    N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    fn()
+                    b.record()
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b))
+                t = sorted(ts)[len(ts) // 2] / 1e3
+                gbs = bpe * d / t / 1e9
+                sweep.append({"kernel": name, "params": d, "us": t * 1e6, "gbs": gbs,
+                              "frac": gbs / peaks["hbm_gbs"]})
+            for a_ in (x, g, m, r_):
+                a_.close()
+        line["kernel_sweep"] = sweep
+
+    # ---------------- CPU baseline (rank 0, N=1) ----------------
+    if not args.no_cpu and rank == 0 and ws == 1:
+        from oracle.engine_port import run_lpp_cpu
+
+        r = run_lpp_cpu(slots=4 * U, updaters=U, batch_size=B)
+        line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
+                                "cores": r["cores"], "kind": "port",
+                                "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U}, "
+                                          f"torch-CPU ResNet-20 grads, store ops via reference "
+                                          f"_atomics ({r['atomics']})"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.out:
+            Path(args.out).write_text(json.dumps(line, indent=1) + "\n")
+    if ws > 1:
+        group.close()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -303,6 +303,7 @@ class _Worker:
                     cfg.batch_size, self.streams[r], input_mode=input_mode,
                     use_graphs=cfg.use_graphs, seed=cfg.seed * 7919 + self.q * 101 + r + 1))
             depth = cfg.in_flight + 2
+            self.loss_pinned = torch.zeros((cfg.updaters, depth), dtype=torch.float32, pin_memory=True)
             self.idx_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size), dtype=torch.long,
                                           pin_memory=True)
             if engine.host_batches:
@@ -372,12 +373,38 @@ class _Engine:
         self.err_lock = threading.Lock()
         self.apply_events: list = []
         self.t0 = 0.0
-        self.final_round_mean = None
+        self.budget = cfg.budget
+        self.read_loss = False
+        self.loss_log: list = []
+        mu, wd = cfg.momentum, cfg.weight_decay
+        # algorithmic bytes per element of K1/K2: read g, read +
+        # write x (the weight-decay read of x is that same read), + read and
+        # write the per-stream momentum buffer
+        self.apply_bytes_per_elem = 12 + (8 if mu else 0)
         fwd = obj.forward_cost()
         self._flops_of = {b: cfg.batch_size * (fwd + obj.backward_cost(cfg.partition.block(b)))
                           for b in range(cfg.partition.num_blocks + 1)}
         self._bflops_of = {b: cfg.batch_size * obj.backward_cost(cfg.partition.block(b))
                            for b in range(cfg.partition.num_blocks + 1)}
+
+    def reset(self, budget: int) -> None:
+        """Start a new phase of ``budget`` slots per worker on the same
+        arenas and captured graphs (counters, control block and logs reset)."""
+        self.budget = int(budget)
+        for w in self.workers.values():
+            for c in (w.store.sample_counter, w.store.update_order_counter, w.exited,
+                      w.last_avg_stamp, w.synced_at):
+                c.store(0)
+        if self.group is None:
+            self.ctrl.buf[:] = 0
+        else:
+            self.group.reset_control()
+        self.flops.store(0)
+        self.updates = [[] for _ in range(self.cfg.workers * self.cfg.updaters)]
+        self.stamps = [[] for _ in range(self.cfg.workers)]
+        self.errors = []
+        self.apply_events = []
+        self.loss_log = []
 
     # -- one updater step: K3 -> graph -> K1/K2, all on the updater stream --
 
@@ -412,13 +439,20 @@ class _Engine:
                         None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode], sp)
             if self.time_apply:
                 e1.record(stream)
-                bpe = 20 if (cfg.momentum and cfg.weight_decay) else (
-                    16 if (cfg.momentum or cfg.weight_decay) else 12)
-                self.apply_events.append((e0, e1, bpe * blk.length))
+                self.apply_events.append((e0, e1, self.apply_bytes_per_elem * blk.length))
+            if self.read_loss:
+                # the step's result back to the host (end-to-end measurement)
+                w.loss_pinned[r, slot].copy_(prog.loss, non_blocking=True)
 
     def average(self, owner: int, stream: torch.cuda.Stream, final: bool) -> None:
         lo, hi = self.shards[owner]
         w = self.workers[owner]
+        if self.cfg.workers == 1:
+            # a single worker's mean is itself: the correction is exactly 0
+            # (test_engine.py:169-182), so only the final mean is copied out
+            if final:
+                N.snapshot(w.store.arena.ptr, w.mean_out.data_ptr(), self.dim, stream.cuda_stream)
+            return
         mean_ptr = w.mean_out.data_ptr() + 4 * lo if final else None
         N.average_shard(self.arena_ptrs, lo, hi, mean_ptr, N.MODE_RED, stream.cuda_stream)
 
@@ -457,13 +491,15 @@ class _Engine:
         ctrl = self.ctrl
         s, t = 0, 0
         try:
-            while s < cfg.budget and not ctrl.stop.read():
+            while s < self.budget and not ctrl.stop.read():
                 s = w.store.read_and_inc()
                 lr = lr_at(cfg.lr, s)
                 choice = self.choose(s, rank)
                 k = t % cfg.in_flight
                 if used[k]:
                     events[k].synchronize()
+                    if self.read_loss:
+                        self.loss_log.append(float(w.loss_pinned[r, (t - cfg.in_flight) % depth]))
                 batch = None
                 if cfg.sampling == "host":
                     batch = gen.integers(0, n, cfg.batch_size)
@@ -611,7 +647,7 @@ class _Engine:
                     self.flops.add(self._flops_of[choice.block_id])
                     self.record_update(q, r, s, u, k_claim, choice, lr)
                     t += 1
-                    if s >= cfg.budget:
+                    if s >= self.budget:
                         active[(q, r)] = False
             sweep += 1
             drained = not any(active.values())
@@ -846,40 +882,81 @@ def _eval_row(cfg, samples, rnd, wall_ms, flops, p_hat, x) -> MetricsRow:
                       train_loss=loss, grad_norm_sq=gn, flops=flops, p_hat=p_hat)
 
 
-def run_experiment(cfg: RunConfig, group=None, host_batches: bool = False) -> RunResult:
-    """Run one configuration (engine.py:637-642).  ``group`` attaches this
-    process to a multi-GPU group (``paper_2203_06638_b200.group``)."""
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2203_06638_b200 needs a CUDA device (no CPU fallback)")
-    if cfg.algo in ("mb_sgd", "pl_sgd"):
-        eng = _SyncEngine(cfg, group=group, host_batches=host_batches)
-        dev_ms = eng.run()
-        final = eng.final_values()
-        x0 = eng.x0_host
-        rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, x0)]
-        fwd = cfg.objective.forward_cost()
-        flops = cfg.budget * cfg.workers * cfg.batch_size * (fwd + cfg.objective.backward_cost(
-            Block(0, cfg.objective.dim)))
-        rounds = cfg.budget if cfg.algo == "mb_sgd" else eng.rounds
-        rows.append(_eval_row(cfg, cfg.budget, rounds, eng.wall_ms, flops, 1.0, final))
-        return RunResult(config=cfg, metrics=rows, final_values=final, x0=x0, wall_ms=eng.wall_ms,
-                         flops=flops, p_hat=1.0, counter_finals=[cfg.budget] * cfg.workers,
-                         device_ms=dev_ms)
-    eng = _Engine(cfg, host_batches=host_batches, group=group)
-    try:
+class Trainer:
+    """Public session API: build once (arenas, captured graphs), run phases.
+
+    ``Trainer(cfg).run()`` is ``run_experiment(cfg)``; ``run(budget)`` may be
+    called repeatedly (bench warm-up, then timed phase) on the same arenas.
+    ``host_batches`` feeds every step from host (pinned) memory with an H2D
+    copy inside the step; ``read_loss`` copies each step's loss back.
+    """
+
+    def __init__(self, cfg: RunConfig, group=None, host_batches: bool = False,
+                 time_apply: bool = False, read_loss: bool = False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2203_06638_b200 needs a CUDA device (no CPU fallback)")
+        self.cfg = cfg
+        self.sync = cfg.algo in ("mb_sgd", "pl_sgd")
+        if self.sync:
+            self.eng = _SyncEngine(cfg, group=group, host_batches=host_batches)
+        else:
+            self.eng = _Engine(cfg, host_batches=host_batches, time_apply=time_apply, group=group)
+            self.eng.read_loss = read_loss
+        self.phases = 0
+
+    def run(self, budget: int | None = None, evaluate: bool | None = None) -> RunResult:
+        cfg = self.cfg
+        budget = cfg.budget if budget is None else int(budget)
+        ev = cfg.evaluate if evaluate is None else evaluate
+        eng = self.eng
+        if self.sync:
+            dev_ms = eng.run(budget)
+            final = eng.final_values()
+            fwd = cfg.objective.forward_cost()
+            flops = budget * cfg.workers * cfg.batch_size * (
+                fwd + cfg.objective.backward_cost(Block(0, cfg.objective.dim)))
+            rounds = budget if cfg.algo == "mb_sgd" else eng.rounds
+            rows = []
+            if ev:
+                rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host),
+                        _eval_row(cfg, budget, rounds, eng.wall_ms, flops, 1.0, final)]
+            self.phases += 1
+            return RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
+                             wall_ms=eng.wall_ms, flops=flops, p_hat=1.0,
+                             counter_finals=[budget] * cfg.workers, device_ms=dev_ms)
+        if self.phases:
+            eng.reset(budget)
+        else:
+            eng.budget = budget
+        self.phases += 1
         dev_ms = eng.run_serialized() if cfg.schedule == "serialized" else eng.run_async()
         final = eng.final_values()
         stamps = [st for per in eng.stamps for st in per]
         rounds = max((st.round for st in stamps), default=0)
         flops = eng.flops.read()
         counters = [eng.workers[q].store.sample_counter.read() for q in eng.local_workers]
-        rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host)]
-        rows.append(_eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, 1.0, final))
+        rows = []
+        if ev:
+            rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host),
+                    _eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, 1.0, final)]
         res = RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
                         wall_ms=eng.wall_ms, flops=flops, p_hat=1.0, counter_finals=counters,
                         updates=[u for per in eng.updates for u in per], stamps=stamps,
                         device_ms=dev_ms, apply_timing=eng.apply_timing())
         res.round_trace = getattr(eng, "round_trace", None)
+        res.losses = list(eng.loss_log)
         return res
+
+    def close(self) -> None:
+        if not self.sync:
+            self.eng.close()
+
+
+def run_experiment(cfg: RunConfig, group=None, host_batches: bool = False) -> RunResult:
+    """Run one configuration (engine.py:637-642).  ``group`` attaches this
+    process to a multi-GPU group (``paper_2203_06638_b200.group``)."""
+    tr = Trainer(cfg, group=group, host_batches=host_batches)
+    try:
+        return tr.run()
     finally:
-        eng.close()
+        tr.close()
