@@ -49,6 +49,7 @@ from .objectives import ArenaObjective
 from .paramstore import AtomicCounter, ParamStore
 from .partition import Block, BlockChoice, BlockPartition, SelectionReason, select_block
 from .schedules import LrSchedule, SyncScheme, lr_at, sync_every
+from .rounds import RoundControl, averager_loop
 from .step import StepProgram
 
 ALGOS = ("mb_sgd", "pl_sgd", "lap_sgd", "lpp_sgd")
@@ -183,70 +184,6 @@ class RunResult:
 
 # ---------------------------------------------------------------------------
 # round control block (host int64 cells; shared memory for multi-process)
-
-
-class RoundControl:
-    """Cells shared by a group's averagers.
-
-    layout: [0] round_calls  [1] stop  [2] abort  [3] drained workers
-            [8 : 8+R]        per-round vote count
-            [8+R : 8+2R]     per-round final-vote count
-    """
-
-    HEADER = 8
-
-    def __init__(self, workers: int, max_rounds: int, buf: np.ndarray | None = None):
-        self.workers = workers
-        self.max_rounds = max_rounds
-        n = self.HEADER + 2 * (max_rounds + 2)
-        if buf is None:
-            buf = np.zeros(n, dtype=np.int64)
-        if buf.shape[0] < n:
-            raise ValueError("control buffer too small")
-        self.buf = buf
-        self.round_calls = _Cell(buf, 0)
-        self.stop = _Cell(buf, 1)
-        self.abort = _Cell(buf, 2)
-        self.drained = _Cell(buf, 3)
-
-    @staticmethod
-    def nbytes(max_rounds: int) -> int:
-        return 8 * (RoundControl.HEADER + 2 * (max_rounds + 2))
-
-    def vote(self, r: int, final: bool) -> None:
-        if r > self.max_rounds:
-            raise RuntimeError("averaging round budget of the control block exceeded")
-        if final:
-            N.atomic_fetch_add(self.buf, self.HEADER + self.max_rounds + 2 + r, 1)
-        N.atomic_fetch_add(self.buf, self.HEADER + r, 1)
-
-    def wait_votes(self, r: int) -> bool | None:
-        """Wait (GIL released) until all workers voted in round r; unanimous-final?"""
-        got = N.atomic_wait_ge(self.buf, self.HEADER + r, self.workers, self.buf, 2)
-        if got is None:
-            return None
-        return N.atomic_load(self.buf, self.HEADER + self.max_rounds + 2 + r) == self.workers
-
-
-class _Cell:
-    """An AtomicCounter-like view of one cell (no initial store)."""
-
-    __slots__ = ("_b", "_i")
-
-    def __init__(self, buf, i):
-        self._b, self._i = buf, i
-
-    def read(self):
-        return N.atomic_load(self._b, self._i)
-
-    def add(self, d):
-        return N.atomic_fetch_add(self._b, self._i, d)
-
-    def store(self, v):
-        N.atomic_store(self._b, self._i, v)
-
-    def cas(self, e, d):
-        return N.atomic_cas(self._b, self._i, e, d)
 
 
 def shard_bounds(dim: int, workers: int) -> list[tuple[int, int]]:
@@ -522,50 +459,27 @@ class _Engine:
         cfg = self.cfg
         w = self.workers[q]
         torch.cuda.set_device(w.device)
-        ctrl = self.ctrl
         store = w.store
-        s_pre, round_no, backoff = 0, 0, 0.0
+        u_of = {}
+
+        def do_round(r, final, s_cur):
+            u_of[r] = store.claim_update_order()
+            self.average(q, w.avg_stream, final=final)
+            w.avg_stream.synchronize()
+            w.last_avg_stamp.store(u_of[r])
+            w.synced_at.store(s_cur)
+
+        def on_round(r, s_cur, k_delta, unanimous):
+            self.stamps[q].append(AveragerStamp(
+                worker=q, round=r, u=u_of.pop(r), s_cur=s_cur, k_delta=k_delta,
+                wall_ms=(time.perf_counter() - self.t0) * 1e3))
+
         try:
-            while True:
-                if ctrl.abort.read():
-                    return
-                s_cur = store.sample_counter.read()
-                drain = w.exited.read() == cfg.updaters
-                pending = ctrl.round_calls.read() > round_no
-                fresh = s_cur - s_pre >= sync_every(cfg.sync, s_cur)
-                if not pending:
-                    if fresh and not drain:
-                        ctrl.round_calls.cas(round_no, round_no + 1)
-                    elif drain and ctrl.drained.read() == cfg.workers:
-                        # every worker has drained: open the final round
-                        ctrl.round_calls.cas(round_no, round_no + 1)
-                    elif drain and fresh:
-                        # drained with unsynced work: one more round for it
-                        ctrl.round_calls.cas(round_no, round_no + 1)
-                    else:
-                        time.sleep(backoff)
-                        backoff = min(2e-4, backoff * 2 + 1e-5)
-                        continue
-                backoff = 0.0
-                r = round_no + 1
-                ctrl.vote(r, drain)
-                u_avg = store.claim_update_order()
-                self.average(q, w.avg_stream, final=drain)
-                w.avg_stream.synchronize()
-                w.last_avg_stamp.store(u_avg)
-                w.synced_at.store(s_cur)
-                unanimous = ctrl.wait_votes(r)
-                if unanimous is None:
-                    return
-                round_no = r
-                if cfg.round_budget is not None and round_no >= cfg.round_budget:
-                    ctrl.stop.store(1)
-                self.stamps[q].append(AveragerStamp(
-                    worker=q, round=round_no, u=u_avg, s_cur=s_cur, k_delta=s_cur - s_pre,
-                    wall_ms=(time.perf_counter() - self.t0) * 1e3))
-                s_pre = s_cur
-                if unanimous:
-                    return
+            averager_loop(self.ctrl, workers=cfg.workers,
+                          read_counter=store.sample_counter.read,
+                          local_drained=lambda: w.exited.read() == cfg.updaters,
+                          sync_period=lambda s: sync_every(cfg.sync, s),
+                          do_round=do_round, on_round=on_round, stop_after=cfg.round_budget)
         except BaseException as exc:
             self.fail(exc)
 
@@ -605,6 +519,8 @@ class _Engine:
             for r in range(cfg.updaters):
                 threads.append(threading.Thread(target=self.updater, args=(q, r), daemon=True,
                                                 name=f"updater-{q}-{r + 1}"))
+        if self.group is not None:
+            self.group.barrier()
         self.t0 = time.perf_counter()
         for t in threads:
             t.start()
@@ -612,6 +528,9 @@ class _Engine:
             t.join()
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         dev_ms = self._device_span_end(starts)
+        if self.group is not None:
+            # peers may not release or reuse arenas until every owner is done
+            self.group.barrier()
         if self.errors:
             raise RuntimeError("engine thread failed") from self.errors[0]
         return dev_ms

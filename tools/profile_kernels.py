@@ -1,0 +1,34 @@
+"""Standalone launches of K1/K3/K4 for ncu (one stream, one thread):
+d20 = 272,474 (ResNet-20 arena) and 64M (sweep) for apply/snapshot, and
+K4 over Q=4 local arenas at 16M.  L2 flushed before every launch."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2203_06638_b200 import _native as N  # noqa: E402
+from paper_2203_06638_b200.arena import Arena  # noqa: E402
+
+st = torch.cuda.current_stream().cuda_stream
+scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush = lambda: N.l2_flush(scratch.data_ptr(), scratch.numel(), st)  # noqa: E731
+for d in (272_474, 64_000_000):
+    x, g, m, r = (Arena(d, 0) for _ in range(4))
+    x.tensor.normal_(), g.tensor.normal_()
+    for _ in range(2):
+        flush()
+        N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st)
+        flush()
+        N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st)
+        flush()
+        N.snapshot(x.ptr, r.ptr, d, st)
+    for a in (x, g, m, r):
+        a.close()
+d = 16_000_000
+ars = [Arena(d, 0) for _ in range(4)]
+for _ in range(2):
+    flush()
+    N.average_shard([a.ptr for a in ars], 0, d, None, N.MODE_RED, st)
+torch.cuda.synchronize()
+print("ok")
