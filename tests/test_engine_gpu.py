@@ -284,5 +284,9 @@ def test_resnet20_async_lpp_runs():
     res = run_experiment(cfg)
     assert res.counter_finals == [44]
     assert np.all(np.isfinite(res.final_values))
-    assert {u.block_id for u in res.updates if u.s > 4} == {0, 1, 2, 3, 4}
+    late = [u for u in res.updates if u.s > 4]
+    # which updater claims which slot is timing-dependent; the
+    # PASSM+ rule itself is not: partial steps train the updater's own block
+    assert all(u.block_id == (u.rank if (u.s - 4) % 2 == 0 else 0) for u in late)
+    assert {u.block_id for u in late} - {0}
     assert np.isfinite(res.metrics[-1].train_loss)
