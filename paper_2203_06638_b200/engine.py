@@ -197,6 +197,56 @@ def shard_bounds(dim: int, workers: int) -> list[tuple[int, int]]:
 
 
 # ---------------------------------------------------------------------------
+# quiescent mode (test-only, engine.py:153-196)
+
+
+class PauseGate:
+    """Lets an averager fence its worker's updaters between two steps.
+
+    Same contract as the reference's gate (engine.py:153-196): updaters
+    pass ``checkpoint`` before claiming a slot; ``pause`` returns once every
+    registered updater is parked there.  On the GPU the averager then also
+    drains the updater streams, so no device write overlaps the round."""
+
+    def __init__(self):
+        self._cv = threading.Condition()
+        self._active = 0
+        self._idle = 0
+        self._paused = False
+
+    def register(self) -> None:
+        with self._cv:
+            self._active += 1
+
+    def leave(self) -> None:
+        with self._cv:
+            self._active -= 1
+            self._cv.notify_all()
+
+    def checkpoint(self) -> None:
+        with self._cv:
+            if not self._paused:
+                return
+            self._idle += 1
+            self._cv.notify_all()
+            while self._paused:
+                self._cv.wait()
+            self._idle -= 1
+            self._cv.notify_all()
+
+    def pause(self) -> None:
+        with self._cv:
+            self._paused = True
+            while self._idle < self._active:
+                self._cv.wait()
+
+    def resume(self) -> None:
+        with self._cv:
+            self._paused = False
+            self._cv.notify_all()
+
+
+# ---------------------------------------------------------------------------
 # workers
 
 
@@ -210,6 +260,7 @@ class _Worker:
         self.exited = AtomicCounter(0)
         self.last_avg_stamp = AtomicCounter(0)
         self.synced_at = AtomicCounter(0)
+        self.gate = PauseGate() if cfg.quiescent else None
         d = engine.dim
         U = cfg.updaters
         with torch.cuda.device(device):
@@ -398,6 +449,9 @@ class _Engine:
             self.errors.append(exc)
         self.ctrl.abort.store(1)
         self.ctrl.stop.store(1)
+        for w in self.workers.values():
+            if w.gate is not None:
+                w.gate.resume()
 
     def record_update(self, q, r, s, u, k_claim, choice: BlockChoice, lr):
         if self.cfg.record_mode == "off":
@@ -427,8 +481,12 @@ class _Engine:
         used = [False] * cfg.in_flight
         ctrl = self.ctrl
         s, t = 0, 0
+        if w.gate is not None:
+            w.gate.register()
         try:
             while s < self.budget and not ctrl.stop.read():
+                if w.gate is not None:
+                    w.gate.checkpoint()
                 s = w.store.read_and_inc()
                 lr = lr_at(cfg.lr, s)
                 choice = self.choose(s, rank)
@@ -452,6 +510,8 @@ class _Engine:
         except BaseException as exc:  # surfaced after join (engine.py:456-463)
             self.fail(exc)
         finally:
+            if w.gate is not None:
+                w.gate.leave()
             if w.exited.add(1) + 1 == cfg.updaters:
                 ctrl.drained.add(1)
 
@@ -463,11 +523,27 @@ class _Engine:
         u_of = {}
 
         def do_round(r, final, s_cur):
-            u_of[r] = store.claim_update_order()
-            self.average(q, w.avg_stream, final=final)
-            w.avg_stream.synchronize()
-            w.last_avg_stamp.store(u_of[r])
-            w.synced_at.store(s_cur)
+            quiet = w.gate is not None
+            if quiet:
+                # fence: every worker's updaters parked and their streams
+                # drained before any owner touches the arenas
+                w.gate.pause()
+                for st in w.streams:
+                    st.synchronize()
+                if not self.ctrl.fence(0, r):
+                    w.gate.resume()
+                    return
+            try:
+                u_of[r] = store.claim_update_order()
+                self.average(q, w.avg_stream, final=final)
+                w.avg_stream.synchronize()
+                w.last_avg_stamp.store(u_of[r])
+                w.synced_at.store(s_cur)
+                if quiet:
+                    self.ctrl.fence(1, r)
+            finally:
+                if quiet:
+                    w.gate.resume()
 
         def on_round(r, s_cur, k_delta, unanimous):
             self.stamps[q].append(AveragerStamp(

@@ -57,8 +57,8 @@ class RoundControl:
     """Cells shared by a group's averagers.
 
     layout: [0] round_calls  [1] stop  [2] abort  [3] drained workers
-            [8 : 8+R+2]          per-round vote count
-            [8+R+2 : 8+2(R+2)]   per-round final-vote count
+            then four per-round arrays of R+2 cells: vote count, final-vote
+            count, and the two fences of quiescent mode (all paused / all done)
     """
 
     HEADER = 8
@@ -77,9 +77,11 @@ class RoundControl:
         self.abort = _Cell(buf, 2)
         self.drained = _Cell(buf, 3)
 
+    ARRAYS = 4
+
     @staticmethod
     def cells(max_rounds: int) -> int:
-        return RoundControl.HEADER + 2 * (int(max_rounds) + 2)
+        return RoundControl.HEADER + RoundControl.ARRAYS * (int(max_rounds) + 2)
 
     @staticmethod
     def nbytes(max_rounds: int) -> int:
@@ -87,6 +89,15 @@ class RoundControl:
 
     def _final_cell(self, r: int) -> int:
         return self.HEADER + self.max_rounds + 2 + r
+
+    def _fence_cell(self, which: int, r: int) -> int:
+        return self.HEADER + (2 + which) * (self.max_rounds + 2) + r
+
+    def fence(self, which: int, r: int) -> bool:
+        """Group-wide barrier number ``which`` (0/1) of round r; False on abort."""
+        c = self._fence_cell(which, r)
+        N.atomic_fetch_add(self.buf, c, 1)
+        return N.atomic_wait_ge(self.buf, c, self.workers, self.buf, 2) is not None
 
     def vote(self, r: int, final: bool) -> None:
         if r > self.max_rounds:

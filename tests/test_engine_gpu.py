@@ -290,3 +290,34 @@ def test_resnet20_async_lpp_runs():
     assert all(u.block_id == (u.rank if (u.s - 4) % 2 == 0 else 0) for u in late)
     assert {u.block_id for u in late} - {0}
     assert np.isfinite(res.metrics[-1].train_loss)
+
+
+def test_async_quiescent_single_updater_matches_reference_engine():
+    """test_engine.py:47-59: Q=U=1, quiescent — the async engine's run equals
+    the reference engine's own run (golden) within the fp32 contract."""
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import SyncScheme, constant_schedule
+
+    obj = _mlp("small")[0]
+    g = load_npz("engine_q1u1.npz")
+    cfg = RunConfig(algo="lap_sgd", objective=obj, partition=make_partition(obj.dim, (0, obj.dim)),
+                    lr=constant_schedule(0.05, 50), sync=SyncScheme(total=50, period=4, switch_point=0),
+                    budget=50, warm_start_budget=0, workers=1, updaters=1, batch_size=8, seed=1,
+                    record_mode="full", quiescent=True, evaluate=False)
+    res = run_experiment(cfg)
+    np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
+    assert res.counter_finals == list(g["counter_finals"])
+
+
+def test_async_quiescent_group_runs_fenced_rounds():
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    res = run_experiment(_tiny(obj, algo="lap_sgd", budget=120, workers=2, updaters=2, quiescent=True))
+    assert res.counter_finals == [122, 122]
+    rounds = {}
+    for st in res.stamps:
+        rounds.setdefault(st.round, set()).add(st.worker)
+    assert rounds and all(v == {0, 1} for v in rounds.values())
+    assert np.all(np.isfinite(res.final_values))
