@@ -139,6 +139,36 @@ int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t hi,
                       float* mean_out, int mode, void* stream);
 
 /* ------------------------------------------------------------------ */
+/* K5 write tags — replace the tagged _atomics ops (_atomics.c:217-310,  */
+/* 346-392).  Tags are int32 update-order stamps, one per element, in a  */
+/* buffer with the same alignment as the values.  Writers update the     */
+/* value first and the tag second; readers load the tag first and the    */
+/* value second, so a tag never claims a newer write than the value it   */
+/* is read with (paramstore.py:47-53).                                   */
+
+/* lpp_apply_sgd + tags[e] = stamp (mode BULK is served as RED) */
+int lpp_apply_sgd_tagged(float* x, const float* g, float* m, size_t n, float lr,
+                         const float* lr_dev, float mu, float wd, int mode,
+                         int32_t* tags, int32_t stamp, void* stream);
+/* accum_cas_tagged_f64(dst, tags, start, delta, scale, stamp) */
+int lpp_accum_tagged(float* dst, int32_t* tags, size_t dst_len, size_t start,
+                     const float* delta, size_t n, float scale, int32_t stamp,
+                     int mode, void* stream);
+/* snapshot_tagged_f64: out / out_tags may be NULL; if min_tag_out != NULL
+ * the minimum tag seen is atomicMin-ed into *min_tag_out (init INT32_MAX) */
+int lpp_snapshot_tagged(const float* src, const int32_t* tags, float* out,
+                        int32_t* out_tags, size_t n, int32_t* min_tag_out,
+                        void* stream);
+/* gather_i64(tags, idx, out): out[k] = tags[idx[k]] (device idx, caller
+ * guarantees 0 <= idx[k] < len(tags)) */
+int lpp_gather_tags(const int32_t* tags, const int64_t* idx, size_t k, int32_t* out,
+                    void* stream);
+/* K4 + tags_q[e] = stamps[q] after the correction (host arrays of Q) */
+int lpp_average_shard_tagged(float* const* arenas, int32_t* const* tags,
+                             const int32_t* stamps, int Q, size_t lo, size_t hi,
+                             float* mean_out, int mode, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* utilities */
 /* Write a buffer of n_bytes (>= L2 size to flush it) on the stream. */
 int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream);

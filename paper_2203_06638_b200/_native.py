@@ -76,6 +76,20 @@ _SIGS = {
         _c.c_int,
         [_c.POINTER(_vp), _c.c_int, _size, _size, _vp, _c.c_int, _vp],
     ),
+    "lpp_apply_sgd_tagged": (
+        _c.c_int,
+        [_vp, _vp, _vp, _size, _c.c_float, _vp, _c.c_float, _c.c_float, _c.c_int, _vp,
+         _c.c_int32, _vp],
+    ),
+    "lpp_accum_tagged": (
+        _c.c_int, [_vp, _vp, _size, _size, _vp, _size, _c.c_float, _c.c_int32, _c.c_int, _vp]),
+    "lpp_snapshot_tagged": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _vp, _vp]),
+    "lpp_gather_tags": (_c.c_int, [_vp, _vp, _size, _vp, _vp]),
+    "lpp_average_shard_tagged": (
+        _c.c_int,
+        [_c.POINTER(_vp), _c.POINTER(_vp), _c.POINTER(_c.c_int32), _c.c_int, _size, _size, _vp,
+         _c.c_int, _vp],
+    ),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
 }
@@ -174,6 +188,37 @@ def average_shard(arena_ptrs, lo: int, hi: int, mean_out_ptr: int | None, mode: 
     q = len(arena_ptrs)
     table = (_vp * max(q, 1))(*arena_ptrs)
     check(lib.lpp_average_shard(table, q, lo, hi, mean_out_ptr, mode, stream), "average_shard")
+
+
+def apply_sgd_tagged(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, tags_ptr, stamp,
+                     stream) -> None:
+    check(lib.lpp_apply_sgd_tagged(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, tags_ptr,
+                                   int(stamp), stream), "apply_sgd_tagged")
+
+
+def accum_tagged(dst_ptr, tags_ptr, dst_len, start, delta_ptr, n, scale, stamp, mode,
+                 stream) -> None:
+    check(lib.lpp_accum_tagged(dst_ptr, tags_ptr, dst_len, start, delta_ptr, n, scale,
+                               int(stamp), mode, stream), "accum_tagged")
+
+
+def snapshot_tagged(src_ptr, tags_ptr, out_ptr, out_tags_ptr, n, min_tag_ptr, stream) -> None:
+    check(lib.lpp_snapshot_tagged(src_ptr, tags_ptr, out_ptr, out_tags_ptr, n, min_tag_ptr,
+                                  stream), "snapshot_tagged")
+
+
+def gather_tags(tags_ptr, idx_ptr, k, out_ptr, stream) -> None:
+    check(lib.lpp_gather_tags(tags_ptr, idx_ptr, k, out_ptr, stream), "gather_tags")
+
+
+def average_shard_tagged(arena_ptrs, tag_ptrs, stamps, lo, hi, mean_out_ptr, mode,
+                         stream) -> None:
+    q = len(arena_ptrs)
+    a = (_vp * q)(*arena_ptrs)
+    t = (_vp * q)(*tag_ptrs)
+    st = (_c.c_int32 * q)(*[int(v) for v in stamps])
+    check(lib.lpp_average_shard_tagged(a, t, st, q, lo, hi, mean_out_ptr, mode, stream),
+          "average_shard_tagged")
 
 
 def l2_flush(ptr: int, nbytes: int, stream: int) -> None:

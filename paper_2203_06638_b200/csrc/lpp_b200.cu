@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <climits>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
@@ -151,6 +152,37 @@ __device__ __forceinline__ float4 ld_cg4(const float* p) {
 }
 __device__ __forceinline__ float ld_cg(const float* p) { return __ldcg(p); }
 
+// K5 write tags: value first, tag second (accum_cas_tagged_f64,
+// _atomics.c:346-392).  One gpu-scope fence per unrolled group orders the
+// preceding value reductions before the tag stores; a reader loads tags
+// first, fences, then values (snapshot_tagged_f64, _atomics.c:217-266), so a
+// tag can only under-report how fresh the value it describes is.
+__device__ __forceinline__ void st_tag4(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.v4.b32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_tag(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_tag4_sys(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.v4.b32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_tag_sys(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int4 ld_tag4(const int* p) {
+  int4 r;
+  asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ int ld_tag(const int* p) {
+  int r;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+
 // The per-element SGD arithmetic, written with explicit round-to-nearest
 // intrinsics so that ptxas cannot contract it into FMAs; oracle/apply_ref.c
 // restates exactly this sequence.
@@ -173,7 +205,8 @@ __device__ __forceinline__ float sgd_delta(float g, float x, float& m, float lr,
 template <int MODE, bool WD, bool MOM>
 __global__ void __launch_bounds__(kThreads)
     k_apply(float* x, const float* __restrict__ g, float* m, size_t n, size_t head,
-            size_t nvec, float lr, const float* __restrict__ lr_dev, float mu, float wd) {
+            size_t nvec, float lr, const float* __restrict__ lr_dev, float mu, float wd,
+            int* tags, int stamp) {
   if (lr_dev) lr = *lr_dev;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -214,6 +247,14 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
     }
+    if (tags) {
+      __threadfence();
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        size_t i = i0 + (size_t)u * stride;
+        if (i < nvec) st_tag4(tags + head + 4 * i, stamp);
+      }
+    }
   }
   // scalar head [0, head) and tail [head + 4*nvec, n): first block only
   if (blockIdx.x == 0) {
@@ -229,6 +270,10 @@ __global__ void __launch_bounds__(kThreads)
         __stcg(x + e, __fadd_rn(xv, d));
       else
         red_add_f32(x + e, d);
+      if (tags) {
+        __threadfence();
+        st_tag(tags + e, stamp);
+      }
     }
   }
 }
@@ -307,7 +352,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int MODE, bool WD, bool MOM>
 static void launch_apply_t(float* x, const float* g, float* m, size_t n, size_t head,
                            size_t nvec, float lr, const float* lr_dev, float mu, float wd,
-                           cudaStream_t st) {
+                           int* tags, int stamp, cudaStream_t st) {
   int sms = current_sms();
   if (MODE == LPP_MODE_BULK) {
     size_t ntiles = (nvec + kBulkTileV - 1) / kBulkTileV;
@@ -318,28 +363,48 @@ static void launch_apply_t(float* x, const float* g, float* m, size_t n, size_t 
                                                        mu, wd);
   } else {
     k_apply<MODE, WD, MOM><<<grid_for(nvec, sms), kThreads, 0, st>>>(x, g, m, n, head, nvec,
-                                                                    lr, lr_dev, mu, wd);
+                                                                    lr, lr_dev, mu, wd, tags,
+                                                                    stamp);
   }
 }
 
 template <int MODE>
 static void launch_apply_mode(float* x, const float* g, float* m, size_t n, size_t head,
                               size_t nvec, float lr, const float* lr_dev, float mu, float wd,
-                              cudaStream_t st) {
+                              int* tags, int stamp, cudaStream_t st) {
   bool WD = wd != 0.f, MOM = mu != 0.f;
   if (WD && MOM)
-    launch_apply_t<MODE, true, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+    launch_apply_t<MODE, true, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp, st);
   else if (WD)
-    launch_apply_t<MODE, true, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+    launch_apply_t<MODE, true, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp, st);
   else if (MOM)
-    launch_apply_t<MODE, false, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+    launch_apply_t<MODE, false, true>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp, st);
   else
-    launch_apply_t<MODE, false, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+    launch_apply_t<MODE, false, false>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp,
+                                       st);
 }
+
+static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, const float* lr_dev,
+                      float mu, float wd, int mode, int32_t* tags, int32_t stamp, void* stream);
 
 extern "C" int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float lr,
                              const float* lr_dev, float mu, float wd, int mode,
                              void* stream) {
+  return apply_impl(x, g, m, n, lr, lr_dev, mu, wd, mode, nullptr, 0, stream);
+}
+
+extern "C" int lpp_apply_sgd_tagged(float* x, const float* g, float* m, size_t n, float lr,
+                                    const float* lr_dev, float mu, float wd, int mode,
+                                    int32_t* tags, int32_t stamp, void* stream) {
+  if (!tags) return set_err(LPP_E_VALUE, "apply_sgd_tagged: null tags");
+  if (mode == LPP_MODE_BULK) mode = LPP_MODE_RED;  // tags need the value update done in-thread
+  if ((((uintptr_t)x) ^ ((uintptr_t)tags)) & 15u)
+    return set_err(LPP_E_VALUE, "apply_sgd_tagged: tags must share x's alignment modulo 16");
+  return apply_impl(x, g, m, n, lr, lr_dev, mu, wd, mode, tags, stamp, stream);
+}
+
+static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, const float* lr_dev,
+                      float mu, float wd, int mode, int32_t* tags, int32_t stamp, void* stream) {
   if (n == 0) return LPP_OK;
   if (!x || !g) return set_err(LPP_E_VALUE, "apply_sgd: null x or g");
   if (mu != 0.f && !m) return set_err(LPP_E_VALUE, "apply_sgd: momentum needs a buffer");
@@ -355,13 +420,16 @@ extern "C" int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float
   cudaStream_t st = (cudaStream_t)stream;
   switch (mode) {
     case LPP_MODE_PLAIN:
-      launch_apply_mode<LPP_MODE_PLAIN>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      launch_apply_mode<LPP_MODE_PLAIN>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp,
+                                        st);
       break;
     case LPP_MODE_RED:
-      launch_apply_mode<LPP_MODE_RED>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      launch_apply_mode<LPP_MODE_RED>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp,
+                                      st);
       break;
     default:
-      launch_apply_mode<LPP_MODE_BULK>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, st);
+      launch_apply_mode<LPP_MODE_BULK>(x, g, m, n, head, nvec, lr, lr_dev, mu, wd, tags, stamp,
+                                       st);
       break;
   }
   LAUNCH_CHECK("apply_sgd");
@@ -371,7 +439,7 @@ extern "C" int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float
 // reference-shaped accumulate: dst[start+e] += scale*delta[e]
 __global__ void __launch_bounds__(kThreads)
     k_accum(float* d, const float* __restrict__ s, size_t n, size_t head, size_t nvec,
-            float scale, int mode) {
+            float scale, int mode, int* tags, int stamp) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (size_t i = tid; i < nvec; i += stride) {
@@ -390,6 +458,10 @@ __global__ void __launch_bounds__(kThreads)
     } else {
       red_add_v4(d + head + 4 * i, v);
     }
+    if (tags) {
+      __threadfence();
+      st_tag4(tags + head + 4 * i, stamp);
+    }
   }
   if (blockIdx.x == 0) {
     size_t tail0 = head + 4 * nvec;
@@ -401,12 +473,35 @@ __global__ void __launch_bounds__(kThreads)
         __stcg(d + e, __fadd_rn(ld_cg(d + e), v));
       else
         red_add_f32(d + e, v);
+      if (tags) {
+        __threadfence();
+        st_tag(tags + e, stamp);
+      }
     }
   }
 }
 
+static int accum_impl(float* dst, int32_t* tags, size_t dst_len, size_t start,
+                      const float* delta, size_t n, float scale, int32_t stamp, int mode,
+                      void* stream);
+
 extern "C" int lpp_accum(float* dst, size_t dst_len, size_t start, const float* delta,
                          size_t n, float scale, int mode, void* stream) {
+  return accum_impl(dst, nullptr, dst_len, start, delta, n, scale, 0, mode, stream);
+}
+
+extern "C" int lpp_accum_tagged(float* dst, int32_t* tags, size_t dst_len, size_t start,
+                                const float* delta, size_t n, float scale, int32_t stamp,
+                                int mode, void* stream) {
+  if (!tags) return set_err(LPP_E_VALUE, "accum_tagged: null tags");
+  if ((((uintptr_t)dst) ^ ((uintptr_t)tags)) & 15u)
+    return set_err(LPP_E_VALUE, "accum_tagged: tags must share dst's alignment modulo 16");
+  return accum_impl(dst, tags, dst_len, start, delta, n, scale, stamp, mode, stream);
+}
+
+static int accum_impl(float* dst, int32_t* tags, size_t dst_len, size_t start,
+                      const float* delta, size_t n, float scale, int32_t stamp, int mode,
+                      void* stream) {
   if (start > dst_len || n > dst_len - start)
     return set_err(LPP_E_INDEX, "update range out of bounds");
   if (n == 0) return LPP_OK;
@@ -414,15 +509,16 @@ extern "C" int lpp_accum(float* dst, size_t dst_len, size_t start, const float* 
   if (mode != LPP_MODE_PLAIN && mode != LPP_MODE_RED)
     return set_err(LPP_E_VALUE, "accum: mode must be PLAIN or RED");
   float* d = dst + start;
+  int* t = tags ? tags + start : nullptr;
   if (((uintptr_t)d ^ (uintptr_t)delta) & 15u) {
     // mismatched alignment: scalar path (treat everything as head)
     k_accum<<<grid_for((n + 3) / 4, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
-        d, delta, n, n, 0, scale, mode);
+        d, delta, n, n, 0, scale, mode, t, stamp);
   } else {
     size_t head = head_elems(d, n);
     size_t nvec = (n - head) / 4;
     k_accum<<<grid_for(nvec, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
-        d, delta, n, head, nvec, scale, mode);
+        d, delta, n, head, nvec, scale, mode, t, stamp);
   }
   LAUNCH_CHECK("accum");
   return LPP_OK;
@@ -477,11 +573,101 @@ extern "C" int lpp_snapshot(const float* src, float* out, size_t n, void* stream
   return LPP_OK;
 }
 
+// K5: tagged snapshot (tags first, fence, then values) + optional min tag,
+// and the sampled-tag gather (snapshot_tagged_f64 / gather_i64).
+
+__global__ void __launch_bounds__(kThreads)
+    k_snapshot_tagged(const float* src, const int* tags, float* __restrict__ out,
+                      int* __restrict__ out_tags, size_t n, size_t head, size_t nvec,
+                      int* min_tag) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int local_min = INT_MAX;
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * kUnroll) {
+    int4 t[kUnroll];
+    float4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) t[u] = ld_tag4(tags + head + 4 * i);
+    }
+    __threadfence();
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) r[u] = ld_cg4(src + head + 4 * i);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+        if (out) reinterpret_cast<float4*>(out + head)[i] = r[u];
+        if (out_tags) reinterpret_cast<int4*>(out_tags + head)[i] = t[u];
+        local_min = min(local_min, min(min(t[u].x, t[u].y), min(t[u].z, t[u].w)));
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      int tv = ld_tag(tags + e);
+      __threadfence();
+      float v = ld_cg(src + e);
+      if (out) out[e] = v;
+      if (out_tags) out_tags[e] = tv;
+      local_min = min(local_min, tv);
+    }
+  }
+  if (min_tag) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local_min = min(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
+    if ((threadIdx.x & 31) == 0 && local_min != INT_MAX) atomicMin(min_tag, local_min);
+  }
+}
+
+extern "C" int lpp_snapshot_tagged(const float* src, const int32_t* tags, float* out,
+                                   int32_t* out_tags, size_t n, int32_t* min_tag_out,
+                                   void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!src || !tags) return set_err(LPP_E_VALUE, "snapshot_tagged: null src or tags");
+  uintptr_t a = (uintptr_t)src;
+  bool aligned = !(((a ^ (uintptr_t)tags) & 15u) || (out && ((a ^ (uintptr_t)out) & 15u)) ||
+                   (out_tags && ((a ^ (uintptr_t)out_tags) & 15u)));
+  size_t head = aligned ? head_elems(src, n) : n;
+  size_t nvec = aligned ? (n - head) / 4 : 0;
+  k_snapshot_tagged<<<grid_for(nvec ? nvec : 1, current_sms()), kThreads, 0,
+                      (cudaStream_t)stream>>>(src, tags, out, out_tags, n, head, nvec,
+                                              min_tag_out);
+  LAUNCH_CHECK("snapshot_tagged");
+  return LPP_OK;
+}
+
+__global__ void k_gather_tags(const int* tags, const int64_t* __restrict__ idx, size_t k,
+                              int* __restrict__ out) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = ld_tag(tags + idx[i]);
+}
+
+extern "C" int lpp_gather_tags(const int32_t* tags, const int64_t* idx, size_t k, int32_t* out,
+                               void* stream) {
+  if (k == 0) return LPP_OK;
+  if (!tags || !idx || !out) return set_err(LPP_E_VALUE, "gather_tags: null buffer");
+  unsigned grid = (unsigned)((k + kThreads - 1) / kThreads);
+  k_gather_tags<<<grid, kThreads, 0, (cudaStream_t)stream>>>(tags, idx, k, out);
+  LAUNCH_CHECK("gather_tags");
+  return LPP_OK;
+}
+
 // ---------------------------------------------------------------------------
 // K4: owner-computes averaging over a shard of Q arenas
 
 struct ArenaTable {
   float* p[LPP_MAX_WORKERS];
+  int* tag[LPP_MAX_WORKERS];   // K5: per-worker write tags (all null: untagged)
+  int stamp[LPP_MAX_WORKERS];  // each worker's update-order stamp for this round
+  int tagged;
 };
 
 template <int MODE>
@@ -546,6 +732,18 @@ __global__ void __launch_bounds__(kThreads)
         if (mean_out) reinterpret_cast<float4*>(mean_out + head)[i] = mean;
       }
     }
+    if (t.tagged) {
+      __threadfence_system();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        size_t i = i0 + (size_t)u * stride;
+        if (i < nvec) {
+#pragma unroll
+          for (int q = 0; q < LPP_MAX_WORKERS; ++q)
+            if (q < Q) st_tag4_sys(t.tag[q] + lo + head + 4 * i, t.stamp[q]);
+        }
+      }
+    }
   }
   if (blockIdx.x == 0) {
     size_t tail0 = head + 4 * nvec;
@@ -572,12 +770,33 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
       if (mean_out) mean_out[e] = mean;
+      if (t.tagged) {
+        __threadfence_system();
+#pragma unroll
+        for (int q = 0; q < LPP_MAX_WORKERS; ++q)
+          if (q < Q) st_tag_sys(t.tag[q] + lo + e, t.stamp[q]);
+      }
     }
   }
 }
 
+static int average_impl(float* const* arenas, int32_t* const* tags, const int32_t* stamps, int Q,
+                        size_t lo, size_t hi, float* mean_out, int mode, void* stream);
+
 extern "C" int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t hi,
                                  float* mean_out, int mode, void* stream) {
+  return average_impl(arenas, nullptr, nullptr, Q, lo, hi, mean_out, mode, stream);
+}
+
+extern "C" int lpp_average_shard_tagged(float* const* arenas, int32_t* const* tags,
+                                        const int32_t* stamps, int Q, size_t lo, size_t hi,
+                                        float* mean_out, int mode, void* stream) {
+  if (!tags || !stamps) return set_err(LPP_E_VALUE, "average_shard_tagged: null tags/stamps");
+  return average_impl(arenas, tags, stamps, Q, lo, hi, mean_out, mode, stream);
+}
+
+static int average_impl(float* const* arenas, int32_t* const* tags, const int32_t* stamps, int Q,
+                        size_t lo, size_t hi, float* mean_out, int mode, void* stream) {
   if (Q < 1 || Q > LPP_MAX_WORKERS)
     return set_err(LPP_E_VALUE, "average_shard: Q=%d outside [1, %d]", Q, LPP_MAX_WORKERS);
   if (hi < lo) return set_err(LPP_E_INDEX, "average_shard: hi < lo");
@@ -593,7 +812,15 @@ extern "C" int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t 
     if (((uintptr_t)arenas[q] ^ (uintptr_t)arenas[0]) & 15u)
       return set_err(LPP_E_VALUE, "average_shard: arenas must share 16-byte alignment");
     t.p[q] = arenas[q];
+    if (tags) {
+      if (!tags[q]) return set_err(LPP_E_VALUE, "average_shard_tagged: null tags %d", q);
+      if (((uintptr_t)tags[q] ^ (uintptr_t)arenas[0]) & 15u)
+        return set_err(LPP_E_VALUE, "average_shard_tagged: tags must share the arenas' alignment");
+      t.tag[q] = tags[q];
+      t.stamp[q] = stamps[q];
+    }
   }
+  t.tagged = tags ? 1 : 0;
   if (mean_out && ((((uintptr_t)mean_out) ^ (uintptr_t)(arenas[0] + lo)) & 15u))
     return set_err(LPP_E_VALUE, "average_shard: mean_out alignment must match the shard");
   size_t head = head_elems(arenas[0] + lo, n);

@@ -84,6 +84,14 @@ class RunConfig:
     use_graphs: bool = True
     in_flight: int = 2
     evaluate: bool = True            # compute the initial/final MetricsRow losses
+    track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
+    record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
+
+    @property
+    def tracks(self) -> bool:
+        if self.track_writes is not None:
+            return bool(self.track_writes)
+        return self.algo in ("lap_sgd", "lpp_sgd")
 
     def __post_init__(self):
         if self.algo not in ALGOS:
@@ -270,6 +278,20 @@ class _Worker:
         self.grads = [Arena(d, device) for _ in range(U)]
         self.moms = [Arena(d, device) for _ in range(U)] if cfg.momentum else [None] * U
         self.mean_out = torch.zeros(d + 4, dtype=torch.float32, device=self.dev)
+        # K5 write tags (int32 stamps, an arena reinterpreted) + per-updater
+        # staging for the sampled-tag gather and the full-snapshot min tag
+        self.tag_arena = Arena(d, device) if cfg.tracks else None
+        self.tags = self.tag_arena.tensor.view(torch.int32) if cfg.tracks else None
+        depth = cfg.in_flight + 2
+        self.tag_pick = min(cfg.tag_sample, d)
+        if cfg.tracks:
+            k = max(self.tag_pick, 1)
+            self.tag_idx_dev = torch.zeros((U, k), dtype=torch.long, device=self.dev)
+            self.tag_idx_pinned = torch.zeros((U, depth, k), dtype=torch.long, pin_memory=True)
+            self.tag_out_dev = torch.zeros((U, depth, k), dtype=torch.int32, device=self.dev)
+            self.tag_pinned = torch.zeros((U, depth, k), dtype=torch.int32, pin_memory=True)
+            self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
+            self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
         self.programs: list[StepProgram] = []
         self.idx_pinned = None
         self.batch_pinned = None
@@ -308,7 +330,8 @@ class _Worker:
             torch.cuda.synchronize(self.device)
 
     def close(self):
-        for a in self.replicas + self.grads + [m for m in self.moms if m is not None]:
+        extra = [self.tag_arena] if self.tag_arena is not None else []
+        for a in self.replicas + self.grads + [m for m in self.moms if m is not None] + extra:
             a.close()
 
 
@@ -342,12 +365,17 @@ class _Engine:
                         if not enable_peer_access(self.workers[a].device, self.workers[b].device):
                             raise RuntimeError("averaging needs peer access between worker devices")
             self.arena_ptrs = [self.workers[q].store.arena.ptr for q in range(cfg.workers)]
+            self.tag_ptrs = ([self.workers[q].tag_arena.ptr for q in range(cfg.workers)]
+                             if cfg.tracks else None)
             max_rounds = cfg.workers * (cfg.budget + cfg.updaters) + 8
             if cfg.round_budget is not None:
                 max_rounds = min(max_rounds, cfg.round_budget + 8)
             self.ctrl = RoundControl(cfg.workers, max_rounds)
         else:
+            group.reset_control()
             self.arena_ptrs = group.attach_arenas(self.workers[group.rank].store.arena)
+            self.tag_ptrs = (group.attach_arenas(self.workers[group.rank].tag_arena)
+                             if cfg.tracks else None)
             self.ctrl = group.control
         self.shards = shard_bounds(self.dim, cfg.workers)
         lpp = cfg.algo == "lpp_sgd"
@@ -355,6 +383,8 @@ class _Engine:
         for w in self.workers.values():
             w.build_programs(self, ids)
         self.flops = AtomicCounter(0)
+        self.clean_count = AtomicCounter(0)
+        self.classified_count = AtomicCounter(0)
         self.updates: list[list[UpdateRecord]] = [[] for _ in range(cfg.workers * cfg.updaters)]
         self.stamps: list[list[AveragerStamp]] = [[] for _ in range(cfg.workers)]
         self.errors: list[BaseException] = []
@@ -367,8 +397,8 @@ class _Engine:
         mu, wd = cfg.momentum, cfg.weight_decay
         # algorithmic bytes per element of K1/K2: read g, read +
         # write x (the weight-decay read of x is that same read), + read and
-        # write the per-stream momentum buffer
-        self.apply_bytes_per_elem = 12 + (8 if mu else 0)
+        # write the per-stream momentum buffer, + the int32 write tag (K5)
+        self.apply_bytes_per_elem = 12 + (8 if mu else 0) + (4 if cfg.tracks else 0)
         fwd = obj.forward_cost()
         self._flops_of = {b: cfg.batch_size * (fwd + obj.backward_cost(cfg.partition.block(b)))
                           for b in range(cfg.partition.num_blocks + 1)}
@@ -388,6 +418,12 @@ class _Engine:
         else:
             self.group.reset_control()
         self.flops.store(0)
+        self.clean_count.store(0)
+        self.classified_count.store(0)
+        for w in self.workers.values():
+            if w.tags is not None:
+                w.tags.zero_()
+        torch.cuda.synchronize()
         self.updates = [[] for _ in range(self.cfg.workers * self.cfg.updaters)]
         self.stamps = [[] for _ in range(self.cfg.workers)]
         self.errors = []
@@ -396,12 +432,14 @@ class _Engine:
 
     # -- one updater step: K3 -> graph -> K1/K2, all on the updater stream --
 
-    def step(self, w: _Worker, r: int, s: int, block_id: int, lr: float, batch, slot: int):
+    def step(self, w: _Worker, r: int, s: int, block_id: int, lr: float, batch, slot: int,
+             u: int = 0, tag_idx=None, rec=None):
         cfg = self.cfg
         stream = w.streams[r]
         prog = w.programs[r]
         blk = cfg.partition.block(block_id)
         sp = stream.cuda_stream
+        tracks = w.tags is not None
         with torch.cuda.stream(stream):
             if batch is not None:
                 if self.host_batches:
@@ -414,17 +452,42 @@ class _Engine:
                 else:
                     w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
                     prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)
-            N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)           # K3
+            if not tracks:
+                N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)       # K3
+            elif cfg.record_mode == "full":
+                # K5: full tagged snapshot; the min tag decides "clean"
+                w.min_dev[r, slot].fill_(2**31 - 1)
+                N.snapshot_tagged(w.store.arena.ptr, w.tag_arena.ptr, w.replicas[r].ptr, None,
+                                  self.dim, w.min_dev[r, slot].data_ptr(), sp)
+                w.min_pinned[r, slot].copy_(w.min_dev[r, slot], non_blocking=True)
+            else:
+                # K5: sampled tags are gathered BEFORE the value copy (paramstore.py:108-112)
+                k = w.tag_pick
+                w.tag_idx_pinned[r, slot, :k].copy_(torch.from_numpy(tag_idx))
+                w.tag_idx_dev[r, :k].copy_(w.tag_idx_pinned[r, slot, :k], non_blocking=True)
+                N.gather_tags(w.tag_arena.ptr, w.tag_idx_dev[r].data_ptr(), k,
+                              w.tag_out_dev[r, slot].data_ptr(), sp)
+                w.tag_pinned[r, slot].copy_(w.tag_out_dev[r, slot], non_blocking=True)
+                N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)       # K3
             prog.run(block_id)                                                        # fwd+bwd
+            if rec is not None and cfg.record_mode == "full" and cfg.record_tensors:
+                rec.grad = w.grads[r].tensor[blk.start:blk.stop].clone()
+                rec.snapshot = w.replicas[r].tensor.clone()
             off = 4 * blk.start
             mom = w.moms[r]
             if self.time_apply:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            N.apply_sgd(w.store.arena.ptr + off, w.grads[r].ptr + off,              # K1/K2
-                        (mom.ptr + off) if mom is not None else None, blk.length, float(lr),
-                        None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode], sp)
+            if tracks:                                                                # K1/K2 + K5
+                N.apply_sgd_tagged(w.store.arena.ptr + off, w.grads[r].ptr + off,
+                                   (mom.ptr + off) if mom is not None else None, blk.length,
+                                   float(lr), None, cfg.momentum, cfg.weight_decay,
+                                   N.MODES[cfg.apply_mode], w.tag_arena.ptr + off, u, sp)
+            else:
+                N.apply_sgd(w.store.arena.ptr + off, w.grads[r].ptr + off,          # K1/K2
+                            (mom.ptr + off) if mom is not None else None, blk.length, float(lr),
+                            None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode], sp)
             if self.time_apply:
                 e1.record(stream)
                 self.apply_events.append((e0, e1, self.apply_bytes_per_elem * blk.length))
@@ -432,17 +495,25 @@ class _Engine:
                 # the step's result back to the host (end-to-end measurement)
                 w.loss_pinned[r, slot].copy_(prog.loss, non_blocking=True)
 
-    def average(self, owner: int, stream: torch.cuda.Stream, final: bool) -> None:
+    def average(self, owner: int, stream: torch.cuda.Stream, final: bool, stamps=None) -> None:
         lo, hi = self.shards[owner]
         w = self.workers[owner]
         if self.cfg.workers == 1:
             # a single worker's mean is itself: the correction is exactly 0
             # (test_engine.py:169-182), so only the final mean is copied out
+            # (and the round's stamp written into the tags, add_assign's tagging)
             if final:
                 N.snapshot(w.store.arena.ptr, w.mean_out.data_ptr(), self.dim, stream.cuda_stream)
+            if w.tags is not None:
+                with torch.cuda.stream(stream):
+                    w.tags.fill_(int(stamps[0]))
             return
         mean_ptr = w.mean_out.data_ptr() + 4 * lo if final else None
-        N.average_shard(self.arena_ptrs, lo, hi, mean_ptr, N.MODE_RED, stream.cuda_stream)
+        if self.tag_ptrs is not None:
+            N.average_shard_tagged(self.arena_ptrs, self.tag_ptrs, stamps, lo, hi, mean_ptr,
+                                   N.MODE_RED, stream.cuda_stream)
+        else:
+            N.average_shard(self.arena_ptrs, lo, hi, mean_ptr, N.MODE_RED, stream.cuda_stream)
 
     def fail(self, exc: BaseException) -> None:
         with self.err_lock:
@@ -453,13 +524,36 @@ class _Engine:
             if w.gate is not None:
                 w.gate.resume()
 
-    def record_update(self, q, r, s, u, k_claim, choice: BlockChoice, lr):
-        if self.cfg.record_mode == "off":
-            return
+    def record_update(self, q, r, s, u, k_claim, choice: BlockChoice, lr, tag_idx=None):
         b = choice.block_id
-        self.updates[q * self.cfg.updaters + r].append(UpdateRecord(
+        rec = UpdateRecord(
             worker=q, rank=r + 1, s=s, u=u, k_claim=k_claim, block_id=b, reason=choice.reason.value,
-            lr=lr, flops=self._flops_of[b], backward_flops=self._bflops_of[b], clean=None))
+            lr=lr, flops=self._flops_of[b], backward_flops=self._bflops_of[b], clean=None,
+            tag_indices=tag_idx)
+        if self.cfg.record_mode != "off":
+            self.updates[q * self.cfg.updaters + r].append(rec)
+        return rec
+
+    def classify(self, w: _Worker, r: int, slot: int, rec: UpdateRecord) -> None:
+        """Clean iff every sampled (or every, in full mode) tag is at or after
+        the last averaging stamp seen at claim time (engine.py:357-362);
+        called once the step's D2H of its tags has completed."""
+        if w.tags is None:
+            return
+        if self.cfg.record_mode == "full":
+            clean = int(w.min_pinned[r, slot]) >= rec.k_claim
+        else:
+            tg = w.tag_pinned[r, slot, :w.tag_pick].numpy().astype(np.int64)
+            rec.tags = tg
+            clean = bool((tg >= rec.k_claim).all())
+        rec.clean = clean
+        self.classified_count.add(1)
+        if clean:
+            self.clean_count.add(1)
+
+    def p_hat(self) -> float:
+        total = self.classified_count.read()
+        return self.clean_count.read() / total if total else 1.0
 
     def choose(self, s: int, rank: int) -> BlockChoice:
         cfg = self.cfg
@@ -479,7 +573,9 @@ class _Engine:
         depth = cfg.in_flight + 2
         events = [torch.cuda.Event() for _ in range(cfg.in_flight)]
         used = [False] * cfg.in_flight
+        pending = [None] * cfg.in_flight
         ctrl = self.ctrl
+        sampled_tags = w.tags is not None and cfg.record_mode != "full"
         s, t = 0, 0
         if w.gate is not None:
             w.gate.register()
@@ -493,20 +589,34 @@ class _Engine:
                 k = t % cfg.in_flight
                 if used[k]:
                     events[k].synchronize()
+                    old_slot = (t - cfg.in_flight) % depth
                     if self.read_loss:
-                        self.loss_log.append(float(w.loss_pinned[r, (t - cfg.in_flight) % depth]))
+                        self.loss_log.append(float(w.loss_pinned[r, old_slot]))
+                    self.classify(w, r, old_slot, pending[k])
+                # reference rng order: sampled tag indices first, then the batch
+                # (engine.py:343-351)
+                tag_idx = (np.sort(gen.choice(self.dim, size=w.tag_pick, replace=False))
+                           if sampled_tags else None)
                 batch = None
                 if cfg.sampling == "host":
                     batch = gen.integers(0, n, cfg.batch_size)
                 k_claim = w.last_avg_stamp.read()
                 u = w.store.claim_update_order()
-                self.step(w, r, s, choice.block_id, lr, batch, t % depth)
+                rec = self.record_update(q, r, s, u, k_claim, choice, lr, tag_idx)
+                self.step(w, r, s, choice.block_id, lr, batch, t % depth, u=u, tag_idx=tag_idx,
+                          rec=rec)
                 events[k].record(w.streams[r])
                 used[k] = True
+                pending[k] = rec
                 self.flops.add(self._flops_of[choice.block_id])
-                self.record_update(q, r, s, u, k_claim, choice, lr)
                 t += 1
             w.streams[r].synchronize()
+            for j in range(1, cfg.in_flight + 1):
+                tt = t - j
+                if tt >= 0 and used[tt % cfg.in_flight]:
+                    if self.read_loss:
+                        self.loss_log.append(float(w.loss_pinned[r, tt % depth]))
+                    self.classify(w, r, tt % depth, pending[tt % cfg.in_flight])
         except BaseException as exc:  # surfaced after join (engine.py:456-463)
             self.fail(exc)
         finally:
@@ -524,23 +634,30 @@ class _Engine:
 
         def do_round(r, final, s_cur):
             quiet = w.gate is not None
+            fenced = quiet or w.tags is not None
             if quiet:
-                # fence: every worker's updaters parked and their streams
+                # quiescent: every worker's updaters parked and their streams
                 # drained before any owner touches the arenas
                 w.gate.pause()
                 for st in w.streams:
                     st.synchronize()
-                if not self.ctrl.fence(0, r):
-                    w.gate.resume()
-                    return
             try:
                 u_of[r] = store.claim_update_order()
-                self.average(q, w.avg_stream, final=final)
+                stamps = None
+                if fenced:
+                    # every worker's round stamp is published before the owners
+                    # write them into the tags (K5); the round counts as applied
+                    # to this worker's arena only when every owner is done
+                    self.ctrl.publish_stamp(q, u_of[r])
+                    if not self.ctrl.fence(0, r):
+                        return
+                    stamps = self.ctrl.stamps()
+                self.average(q, w.avg_stream, final=final, stamps=stamps)
                 w.avg_stream.synchronize()
+                if fenced and not self.ctrl.fence(1, r):
+                    return
                 w.last_avg_stamp.store(u_of[r])
                 w.synced_at.store(s_cur)
-                if quiet:
-                    self.ctrl.fence(1, r)
             finally:
                 if quiet:
                     w.gate.resume()
@@ -634,13 +751,20 @@ class _Engine:
                     s = w.store.read_and_inc()
                     lr = lr_at(cfg.lr, s)
                     choice = self.choose(s, r + 1)
+                    tag_idx = None
+                    if w.tags is not None and cfg.record_mode != "full":
+                        tag_idx = np.sort(gens[(q, r)].choice(self.dim, size=w.tag_pick,
+                                                              replace=False))
                     batch = gens[(q, r)].integers(0, n, cfg.batch_size)
                     k_claim = w.last_avg_stamp.read()
                     u = w.store.claim_update_order()
-                    self.step(w, r, s, choice.block_id, lr, batch, t % (cfg.in_flight + 2))
+                    slot = t % (cfg.in_flight + 2)
+                    rec = self.record_update(q, r, s, u, k_claim, choice, lr, tag_idx)
+                    self.step(w, r, s, choice.block_id, lr, batch, slot, u=u, tag_idx=tag_idx,
+                              rec=rec)
                     w.streams[r].synchronize()
+                    self.classify(w, r, slot, rec)
                     self.flops.add(self._flops_of[choice.block_id])
-                    self.record_update(q, r, s, u, k_claim, choice, lr)
                     t += 1
                     if s >= self.budget:
                         active[(q, r)] = False
@@ -651,11 +775,14 @@ class _Engine:
                         for q in range(cfg.workers))
             if fresh or drained:
                 rnd = len(self.round_trace) + 1
+                u_avgs = [self.workers[q].store.claim_update_order() for q in range(cfg.workers)]
                 for q in range(cfg.workers):
                     w = self.workers[q]
-                    u_avg = w.store.claim_update_order()
-                    self.average(q, w.avg_stream, final=drained)
+                    self.average(q, w.avg_stream, final=drained, stamps=u_avgs)
                     w.avg_stream.synchronize()
+                for q in range(cfg.workers):
+                    w = self.workers[q]
+                    u_avg = u_avgs[q]
                     w.last_avg_stamp.store(u_avg)
                     self.stamps[q].append(AveragerStamp(
                         worker=q, round=rnd, u=u_avg, s_cur=counts[q], k_delta=counts[q] - s_pre[q],
@@ -933,9 +1060,9 @@ class Trainer:
         rows = []
         if ev:
             rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host),
-                    _eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, 1.0, final)]
+                    _eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, eng.p_hat(), final)]
         res = RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
-                        wall_ms=eng.wall_ms, flops=flops, p_hat=1.0, counter_finals=counters,
+                        wall_ms=eng.wall_ms, flops=flops, p_hat=eng.p_hat(), counter_finals=counters,
                         updates=[u for per in eng.updates for u in per], stamps=stamps,
                         device_ms=dev_ms, apply_timing=eng.apply_timing())
         res.round_trace = getattr(eng, "round_trace", None)

@@ -13,7 +13,11 @@ Drop-in for ``asyncsgd.paramstore`` (``/root/reference/pkg/src/asyncsgd/paramsto
   lost (``_atomics.c:58-74``).  Device ops are asynchronous on the current
   torch stream (or the ``stream=`` given); ``read``/``write`` synchronise.
 
-Not yet implemented: write tags (``track_writes=True``, K5 in SURVEY §2).
+``track_writes=True`` keeps int32 write tags (K5): ``sub_assign`` /
+``add_assign`` stamp every written element after its value
+(``accum_cas_tagged_f64``), and ``snapshot`` returns tags read before the
+values — sampled at ``tag_indices`` or for the whole vector
+(``paramstore.py:97-117``).  Tags are device tensors.
 """
 
 from __future__ import annotations
@@ -88,8 +92,6 @@ class ParamStore:
         arr = torch.as_tensor(np.asarray(initial) if not torch.is_tensor(initial) else initial)
         if arr.dim() != 1:
             raise ValueError("parameter vector must be one-dimensional")
-        if track_writes:
-            raise NotImplementedError("write tags (K5) are not implemented on the GPU path yet")
         if device is None:
             device = torch.cuda.current_device()
         self.device = int(device)
@@ -100,7 +102,8 @@ class ParamStore:
         self.mode = N.MODES[mode]
         self.sample_counter = AtomicCounter(0)
         self.update_order_counter = AtomicCounter(0)
-        self.tags = None
+        self.tag_arena = Arena(self.dim, self.device) if track_writes else None
+        self.tags = self.tag_arena.tensor.view(torch.int32) if track_writes else None
 
     @property
     def values(self) -> torch.Tensor:
@@ -136,28 +139,53 @@ class ParamStore:
             out = torch.empty(self.dim, dtype=torch.float32, device=f"cuda:{self.device}")
         elif out.numel() != self.dim or out.dtype != torch.float32 or not out.is_contiguous():
             raise ValueError("snapshot out must be a contiguous fp32 vector of the store's length")
+        sp = stream_ptr(stream)
+        if self.tags is None:
+            if self.dim:
+                N.snapshot(self.arena.ptr, out.data_ptr(), self.dim, sp)
+            return Snapshot(out, order)
+        dev = f"cuda:{self.device}"
+        if tag_indices is not None:
+            idx_np = np.asarray(tag_indices, dtype=np.int64)
+            if idx_np.size and (idx_np.min() < 0 or idx_np.max() >= self.dim):
+                raise IndexError("tag index out of range")
+            idx = torch.as_tensor(idx_np, device=dev)
+            out_tags = torch.empty(idx.numel(), dtype=torch.int32, device=dev)
+            # tags gathered before the value copy (paramstore.py:108-112)
+            N.gather_tags(self.tag_arena.ptr, idx.data_ptr(), idx.numel(), out_tags.data_ptr(), sp)
+            if self.dim:
+                N.snapshot(self.arena.ptr, out.data_ptr(), self.dim, sp)
+            if stream is not None:
+                idx.record_stream(stream)
+            return Snapshot(out, order, out_tags, idx_np)
+        out_tags = torch.empty(self.dim, dtype=torch.int32, device=dev)
         if self.dim:
-            N.snapshot(self.arena.ptr, out.data_ptr(), self.dim, stream_ptr(stream))
-        return Snapshot(out, order)
+            N.snapshot_tagged(self.arena.ptr, self.tag_arena.ptr, out.data_ptr(), out_tags.data_ptr(),
+                              self.dim, None, sp)
+        return Snapshot(out, order, out_tags)
 
     # -- range updates (K1) -------------------------------------------------
 
     def sub_assign(self, start: int, delta, stamp: int = 0,
                    stream: torch.cuda.Stream | None = None) -> None:
-        self._accum(start, delta, -1.0, stream)
+        self._accum(start, delta, -1.0, stamp, stream)
 
     def add_assign(self, start: int, delta, stamp: int = 0,
                    stream: torch.cuda.Stream | None = None) -> None:
-        self._accum(start, delta, 1.0, stream)
+        self._accum(start, delta, 1.0, stamp, stream)
 
-    def _accum(self, start: int, delta, scale: float, stream) -> None:
+    def _accum(self, start: int, delta, scale: float, stamp: int, stream) -> None:
         d = _as_device_f32(delta, self.device)
         n = d.numel()
         if start < 0 or start + n > self.dim:
             raise IndexError("update range out of bounds")
         mode = self.mode if self.mode != N.MODE_BULK else N.MODE_RED
-        N.accum(self.arena.ptr, self.dim, int(start), d.data_ptr(), n, scale, mode,
-                stream_ptr(stream))
+        if self.tags is None:
+            N.accum(self.arena.ptr, self.dim, int(start), d.data_ptr(), n, scale, mode,
+                    stream_ptr(stream))
+        else:
+            N.accum_tagged(self.arena.ptr, self.tag_arena.ptr, self.dim, int(start), d.data_ptr(),
+                           n, scale, int(stamp), mode, stream_ptr(stream))
         if stream is not None:
             # `d` may be a temporary of the current stream: keep its block
             # reserved until the kernel on `stream` has consumed it

@@ -57,11 +57,14 @@ class RoundControl:
     """Cells shared by a group's averagers.
 
     layout: [0] round_calls  [1] stop  [2] abort  [3] drained workers
+            [8 : 16]  each worker's update-order stamp for the current round
+                      (the owners write it into every arena's tags, K5)
             then four per-round arrays of R+2 cells: vote count, final-vote
-            count, and the two fences of quiescent mode (all paused / all done)
+            count, and the two fences (all published/paused; all shards done)
     """
 
-    HEADER = 8
+    HEADER = 16
+    STAMPS = 8
 
     def __init__(self, workers: int, max_rounds: int, buf: np.ndarray | None = None):
         self.workers = int(workers)
@@ -86,6 +89,12 @@ class RoundControl:
     @staticmethod
     def nbytes(max_rounds: int) -> int:
         return 8 * RoundControl.cells(max_rounds)
+
+    def publish_stamp(self, q: int, u: int) -> None:
+        N.atomic_store(self.buf, self.STAMPS + q, u)
+
+    def stamps(self) -> list[int]:
+        return [N.atomic_load(self.buf, self.STAMPS + q) for q in range(self.workers)]
 
     def _final_cell(self, r: int) -> int:
         return self.HEADER + self.max_rounds + 2 + r

@@ -63,7 +63,7 @@ def _cfg_from_golden(name, obj, **over):
     kw = dict(algo=c["algo"], objective=obj, partition=make_partition(obj.dim, tuple(c["bounds"])),
               lr=lr, sync=sync, budget=c["budget"], warm_start_budget=c["t_st"], workers=c["Q"],
               updaters=c["U"], batch_size=c["B"], seed=c["seed"], schedule="serialized",
-              record_mode="light", evaluate=False)
+              record_mode="full", record_tensors=False, evaluate=False)
     kw.update(over)
     return g, RunConfig(**kw)
 
@@ -126,7 +126,7 @@ def test_serialized_q1u1_matches_reference_engine_run():
     cfg = RunConfig(algo="lap_sgd", objective=obj, partition=make_partition(obj.dim, (0, obj.dim)),
                     lr=constant_schedule(0.05, 50), sync=SyncScheme(total=50, period=4, switch_point=0),
                     budget=50, warm_start_budget=0, workers=1, updaters=1, batch_size=8, seed=1,
-                    schedule="serialized", evaluate=False)
+                    schedule="serialized", record_mode="full", evaluate=False)
     res = run_experiment(cfg)
     np.testing.assert_allclose(res.x0, g["x0"])
     np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
@@ -311,13 +311,36 @@ def test_async_quiescent_single_updater_matches_reference_engine():
 
 
 def test_async_quiescent_group_runs_fenced_rounds():
+    """Quiescent rounds: every update is clean, p_hat == 1 (test_engine.py:62-74)."""
     from paper_2203_06638_b200.engine import run_experiment
 
     obj = _mlp("deep")[0]
-    res = run_experiment(_tiny(obj, algo="lap_sgd", budget=120, workers=2, updaters=2, quiescent=True))
+    res = run_experiment(_tiny(obj, algo="lap_sgd", budget=120, workers=2, updaters=2, quiescent=True,
+                               record_mode="full"))
+    assert res.p_hat == 1.0 and all(u.clean is True for u in res.updates)
     assert res.counter_finals == [122, 122]
     rounds = {}
     for st in res.stamps:
         rounds.setdefault(st.round, set()).add(st.worker)
     assert rounds and all(v == {0, 1} for v in rounds.values())
     assert np.all(np.isfinite(res.final_values))
+
+
+def test_async_tags_classify_updates_and_p_hat():
+    """Sampled write tags (light mode) classify every update; p_hat in (0, 1]."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("c0")[0]
+    res = run_experiment(_tiny(obj, algo="lpp_sgd", budget=300, workers=2, updaters=2,
+                               partition=__import__("paper_2203_06638_b200.partition", fromlist=["x"])
+                               .make_partition(obj.dim, (0, obj.edges[1], obj.dim)),
+                               warm_start_budget=30))
+    assert all(u.clean is not None for u in res.updates)
+    assert all(u.tags is not None and len(u.tags) == 16 for u in res.updates)
+    assert all((np.diff(u.tag_indices) > 0).all() for u in res.updates)
+    assert 0.0 < res.p_hat <= 1.0
+    # every tag is a stamp that exists: at most the worker's last write stamp
+    for q in range(2):
+        top = max([u.u for u in res.updates if u.worker == q] +
+                  [st.u for st in res.stamps if st.worker == q])
+        assert all(int(t) <= top for u in res.updates if u.worker == q for t in u.tags)

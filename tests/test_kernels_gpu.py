@@ -247,3 +247,113 @@ def test_snapshot_elements_are_written_values(N):
     torch.cuda.synchronize()
     for o in outs:
         assert bool((o == o.round()).all()) and float(o.min()) >= 0 and float(o.max()) <= rounds
+
+
+# ---------------------------------------------------------------------------
+# K5 write tags (_atomics.c:217-310, 346-392)
+
+
+def test_store_tags_worked_examples(golden_scalars):
+    """test_paramstore.py:368-388."""
+    from paper_2203_06638_b200.paramstore import ParamStore
+
+    st = ParamStore(np.zeros(4), track_writes=True)
+    st.sub_assign(1, np.array([1.0, 1.0]), stamp=7)
+    snap = st.snapshot()
+    assert snap.tags.tolist() == golden_scalars["paramstore"]["tags"] == [0, 7, 7, 0]
+    st2 = ParamStore(np.zeros(6), track_writes=True)
+    st2.add_assign(2, np.array([1.0, 1.0, 1.0]), stamp=3)
+    sn = st2.snapshot(tag_indices=np.array([0, 2, 5], dtype=np.int64))
+    assert sn.tag_indices.tolist() == [0, 2, 5] and sn.tags.tolist() == [0, 3, 0]
+    assert len(sn.values) == 6
+    plain = ParamStore(np.zeros(3))
+    s3 = plain.snapshot(tag_indices=np.array([1], dtype=np.int64))
+    assert s3.tags is None and s3.tag_indices is None
+    with pytest.raises(IndexError):
+        st2.snapshot(tag_indices=np.array([6], dtype=np.int64))
+
+
+@pytest.mark.parametrize("n,off", [(1, 0), (7, 1), (4099, 3), (100_003, 2)])
+def test_apply_tagged_values_match_untagged_and_stamp_the_range(N, orc, n, off):
+    from paper_2203_06638_b200.arena import Arena
+
+    gen = np.random.default_rng(n)
+    total = n + off + 9
+    x = gen.normal(size=total).astype(np.float32)
+    g = gen.normal(size=total).astype(np.float32)
+    ax, ag, at = Arena(total, 0), Arena(total, 0), Arena(total, 0)
+    ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g))
+    tags = at.tensor.view(torch.int32)
+    tags.fill_(5)
+    N.apply_sgd_tagged(ax.ptr + 4 * off, ag.ptr + 4 * off, None, n, 0.25, None, 0.0, 0.0,
+                       N.MODE_RED, at.ptr + 4 * off, 42, 0)
+    torch.cuda.synchronize()
+    xv = x[off:off + n].copy()
+    orc.apply_sgd(xv, g[off:off + n].copy(), None, 0.25)
+    want = x.copy()
+    want[off:off + n] = xv
+    assert np.array_equal(ax.tensor.cpu().numpy(), want)
+    t = tags.cpu().numpy()
+    assert (t[off:off + n] == 42).all() and (t[:off] == 5).all() and (t[off + n:] == 5).all()
+
+
+def test_snapshot_tagged_gather_and_min(N):
+    from paper_2203_06638_b200.arena import Arena
+
+    n = 70_001
+    src, tg = Arena(n, 0), Arena(n, 0)
+    src.tensor.copy_(torch.randn(n, device="cuda"))
+    tags = tg.tensor.view(torch.int32)
+    tags.copy_(torch.randint(3, 1000, (n,), device="cuda", dtype=torch.int32))
+    out = torch.empty(n, device="cuda")
+    out_tags = torch.empty(n, dtype=torch.int32, device="cuda")
+    mn = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+    N.snapshot_tagged(src.ptr, tg.ptr, out.data_ptr(), out_tags.data_ptr(), n, mn.data_ptr(), 0)
+    idx = torch.tensor([0, 5, 777, n - 1], device="cuda")
+    got = torch.empty(4, dtype=torch.int32, device="cuda")
+    N.gather_tags(tg.ptr, idx.data_ptr(), 4, got.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, src.tensor) and torch.equal(out_tags, tags)
+    assert int(mn) == int(tags.min())
+    assert got.tolist() == tags[idx].tolist()
+
+
+def test_average_tagged_stamps_every_arena(N, orc):
+    from paper_2203_06638_b200.arena import Arena
+
+    Q, n = 3, 10_003
+    xs = [np.random.default_rng(q).normal(size=n).astype(np.float32) for q in range(Q)]
+    ars = [Arena(n, 0) for _ in range(Q)]
+    tgs = [Arena(n, 0) for _ in range(Q)]
+    for a, x in zip(ars, xs):
+        a.tensor.copy_(_cuda(x))
+    N.average_shard_tagged([a.ptr for a in ars], [t.ptr for t in tgs], [11, 22, 33], 1, n - 1,
+                           None, N.MODE_RED, 0)
+    torch.cuda.synchronize()
+    orc.average(xs, 1, n - 1)
+    for q in range(Q):
+        assert np.array_equal(ars[q].tensor.cpu().numpy(), xs[q])
+        t = tgs[q].tensor.view(torch.int32).cpu().numpy()
+        assert (t[1:n - 1] == 11 * (q + 1)).all() and t[0] == 0 and t[n - 1] == 0
+
+
+def test_tags_never_newer_than_values_under_concurrency(N):
+    """A reader that sees tag u must see a value that includes write u:
+    writers add 1 per stamp; reader checks value >= tag (value first, tag second)."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, rounds = 1 << 15, 30
+    x, tg = Arena(n, 0), Arena(n, 0)
+    g = torch.full((n,), -1.0, device="cuda")
+    ws, rs = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [(torch.empty(n, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda"))
+            for _ in range(rounds)]
+    torch.cuda.synchronize()
+    for r in range(rounds):
+        N.apply_sgd_tagged(x.ptr, g.data_ptr(), None, n, 1.0, None, 0.0, 0.0, N.MODE_RED, tg.ptr,
+                           r + 1, ws.cuda_stream)
+        N.snapshot_tagged(x.ptr, tg.ptr, outs[r][0].data_ptr(), outs[r][1].data_ptr(), n, None,
+                          rs.cuda_stream)
+    torch.cuda.synchronize()
+    for v, t in outs:
+        assert bool((v >= t.float()).all())
