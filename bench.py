@@ -21,6 +21,9 @@ Extra keys beyond the base contract:
   cpu_baseline  oracle/engine_port.py (threaded CPU LPP-SGD, the reference's
                 compiled _atomics) on this host, bounded sample, rank 0, N=1
   baselines     the box's own synchronous MB-SGD (same per-GPU B, 1 stream)
+                and LAP-SGD (same engine, no partial backprop)
+  resnet50      config C3 (ImageNet-shaped, d = 25.6M, B = 32 per stream):
+                images/s and the apply kernel's in-situ HBM roofline
   kernel_sweep  K1/K3 alone at 16M/64M params (HBM roofline evidence)
 """
 
@@ -66,7 +69,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
@@ -224,7 +227,8 @@ def ours(args) -> None:
                    "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
                    "conv_compute": "bf16 autocast (arena, grads, apply, averaging in fp32)",
                    "l2": "inputs larger than L2 (614 MB dataset gathered per step)",
-                   "sampling": "in-graph device RNG", "momentum": 0.9, "weight_decay": 5e-4},
+                   "sampling": "in-graph device RNG", "momentum": 0.9, "weight_decay": 5e-4,
+                   "write_tags": cfg.tracks},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -257,7 +261,7 @@ def ours(args) -> None:
         htr.close()
         del htr
 
-    # ---------------- MB-SGD baseline on the same box ----------------
+    # ---------------- baselines on the same box: MB-SGD and LAP-SGD ----------------
     if not args.no_baselines and ws == 1:
         mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)
         mtr = Trainer(mcfg)
@@ -265,10 +269,42 @@ def ours(args) -> None:
         torch.cuda.synchronize()
         mres = mtr.run(K * U, evaluate=False)
         mb = K * U * B / (mres.device_ms / 1e3)
-        line["baselines"] = {"mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
-                                        "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
-                             "lpp_over_mb": value / mb}
         del mtr
+        lcfg = build_cfg(obj, (K + W) * U, algo="lap_sgd", workers=1)
+        ltr = Trainer(lcfg)
+        ltr.run(W * U, evaluate=False)
+        torch.cuda.synchronize()
+        lres = ltr.run(K * U, evaluate=False)
+        lap = sum(lres.counter_finals) * B / (lres.device_ms / 1e3)
+        ltr.close()
+        del ltr
+        line["baselines"] = {
+            "mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
+                       "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
+            "lap_sgd": {"value": lap, "unit": "images/s", "streams": U,
+                        "note": "same engine, full backprop every step (no PASSM+ blocks)"},
+            "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
+
+    # ---------------- ResNet-50 / ImageNet shape (config C3): in-situ HBM apply ----------------
+    if not args.no_rn50 and ws == 1:
+        obj50 = ResNetObjective("resnet50", n_samples=2048, seed=0, data="device")
+        c50 = build_cfg(obj50, 64, workers=1)
+        c50 = __import__("dataclasses").replace(c50, batch_size=32)
+        t50 = Trainer(c50, time_apply=True)
+        t50.run(3 * U, evaluate=False)
+        torch.cuda.synchronize()
+        r50 = t50.run(args.rn50_steps * U, evaluate=False)
+        n50, ms50, by50 = r50.apply_timing
+        a50 = by50 / (ms50 / 1e3) / 1e9
+        line["resnet50"] = {
+            "workload": "resnet50_imagenet224_lpp_sgd_u4_b32", "params": obj50.dim,
+            "value": sum(r50.counter_finals) * 32 / (r50.device_ms / 1e3), "unit": "images/s",
+            "apply_roofline": {"achieved": a50, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": a50 / peaks["hbm_gbs"], "launches": n50,
+                               "avg_us": 1e3 * ms50 / max(n50, 1),
+                               "bytes_per_launch": by50 / max(n50, 1)}}
+        t50.close()
+        del t50
 
     # ---------------- kernel sweep (HBM roofline evidence) ----------------
     if not args.no_sweep and rank == 0:
@@ -334,6 +370,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-rn50", action="store_true")
+    ap.add_argument("--rn50-steps", type=int, default=10)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     if args.warmup < 3:
