@@ -169,11 +169,18 @@ def ours(args) -> None:
     import torch.distributed as dist
 
     ws, rank, local = _dist()
-    torch.cuda.set_device(local)
+    # one process per GPU; LPP_DIST_BACKEND=gloo + fewer GPUs than ranks is the
+    # single-GPU validation mode of the N>1 path (no kernel waits on a peer)
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     torch.backends.cudnn.benchmark = True
     group = None
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LPP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
         from paper_2203_06638_b200.group import ProcessGroup
 
         group = ProcessGroup(workers=ws, max_rounds=(args.steps + args.warmup + 4) * U * ws + 64)
@@ -202,7 +209,7 @@ def ours(args) -> None:
     tr = Trainer(cfg, group=group, time_apply=True)
     tr.run(W * U, evaluate=False)
     barrier()
-    with Clocks(local) as clk:
+    with Clocks(dev) as clk:
         barrier()
         res = tr.run(K * U, evaluate=False)
         barrier()
@@ -314,8 +321,8 @@ def ours(args) -> None:
         scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         sweep = []
         for d in (16_000_000, 64_000_000):
-            x, g, m = Arena(d, local), Arena(d, local), Arena(d, local)
-            r_ = Arena(d, local)
+            x, g, m = Arena(d, dev), Arena(d, dev), Arena(d, dev)
+            r_ = Arena(d, dev)
             for name, fn, bpe in (
                 ("apply_red", lambda: N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st), 12),
                 ("apply_red_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st), 20),

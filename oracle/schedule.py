@@ -87,9 +87,33 @@ class SerializedTrace:
     counter_finals: list = field(default_factory=list)
 
 
+class EpochSampler:
+    """objectives.py:77-104: per-epoch reshuffled walk over an index shard."""
+
+    def __init__(self, indices, seed):
+        self.ix, self.seed, self.epoch, self.pos = np.asarray(indices), seed, -1, 0
+        self.perm = self.ix[:0]
+
+    def next_batch(self, b):
+        out = np.empty(b, dtype=np.int64)
+        f = 0
+        while f < b:
+            if self.pos >= len(self.perm):
+                self.epoch += 1
+                g = np.random.default_rng(np.random.SeedSequence([self.seed, self.epoch]))
+                self.perm = self.ix[g.permutation(len(self.ix))]
+                self.pos = 0
+            k = min(b - f, len(self.perm) - self.pos)
+            out[f:f + k] = self.perm[self.pos:self.pos + k]
+            self.pos += k
+            f += k
+        return out
+
+
 def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: tuple,
                    lr: Lr, switch_point: int, period: int, budget: int, warm_start: int,
-                   batch_size: int, seed: int, dtype=np.float64) -> SerializedTrace:
+                   batch_size: int, seed: int, dtype=np.float64,
+                   epoch_partition: bool = False) -> SerializedTrace:
     """Run the canonical schedule; ``obj`` has init_params/grad_block(x, lo, hi, batch)."""
     if algo not in ("lap_sgd", "lpp_sgd"):
         raise ValueError("serialized schedule covers the asynchronous algorithms")
@@ -102,6 +126,9 @@ def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: t
     gens = [[np.random.default_rng(np.random.SeedSequence([seed, q, r]))
              for r in range(1, updaters + 1)] for q in range(workers)]
     active = [[True] * updaters for _ in range(workers)]
+    # engine.py:294-296: shard arange(n)[q::Q], seed seed*1000 + q*10 + rank
+    samplers = [[EpochSampler(np.arange(obj.n_samples)[q::workers], seed * 1000 + q * 10 + r)
+                 for r in range(1, updaters + 1)] for q in range(workers)] if epoch_partition else None
     trace = SerializedTrace(final_values=x0.copy(), xs=xs)
     sweep = 0
     mean = x0.copy()
@@ -116,7 +143,10 @@ def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: t
                 step_lr = lr.at(s)
                 b = select_block(s, warm_start, nblocks, rank) if algo == "lpp_sgd" else 0
                 lo, hi = (0, dim) if b == 0 else (boundaries[b - 1], boundaries[b])
-                batch = gens[q][ri].integers(0, obj.n_samples, batch_size)
+                if samplers is not None:
+                    batch = samplers[q][ri].next_batch(batch_size)
+                else:
+                    batch = gens[q][ri].integers(0, obj.n_samples, batch_size)
                 g = obj.grad_block(xs[q], lo, hi, batch)
                 if dtype == np.float32:
                     delta = np.float32(step_lr) * g.astype(np.float32)

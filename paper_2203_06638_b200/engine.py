@@ -48,6 +48,7 @@ from .arena import Arena, enable_peer_access
 from .objectives import ArenaObjective
 from .paramstore import AtomicCounter, ParamStore
 from .partition import Block, BlockChoice, BlockPartition, SelectionReason, select_block
+from .sampling import worker_sampler
 from .schedules import LrSchedule, SyncScheme, lr_at, sync_every
 from .rounds import RoundControl, averager_loop
 from .step import StepProgram
@@ -117,8 +118,8 @@ class RunConfig:
             raise ValueError(f"unknown apply mode {self.apply_mode!r}")
         if self.sampling not in ("host", "device"):
             raise ValueError(f"unknown sampling {self.sampling!r}")
-        if self.epoch_partition:
-            raise ValueError("epoch_partition sampling is not implemented on the GPU path yet")
+        if self.epoch_partition and self.sampling != "host":
+            raise ValueError("epoch_partition draws indices on the host: use sampling='host'")
         if self.workers > N.MAX_WORKERS:
             raise ValueError(f"at most {N.MAX_WORKERS} workers per averaging group")
 
@@ -570,6 +571,7 @@ class _Engine:
         rank = r + 1
         gen = np.random.default_rng(np.random.SeedSequence([cfg.seed, q, rank]))
         n = cfg.objective.n_samples
+        sampler = worker_sampler(n, cfg.workers, q, rank, cfg.seed) if cfg.epoch_partition else None
         depth = cfg.in_flight + 2
         events = [torch.cuda.Event() for _ in range(cfg.in_flight)]
         used = [False] * cfg.in_flight
@@ -598,7 +600,9 @@ class _Engine:
                 tag_idx = (np.sort(gen.choice(self.dim, size=w.tag_pick, replace=False))
                            if sampled_tags else None)
                 batch = None
-                if cfg.sampling == "host":
+                if sampler is not None:
+                    batch = sampler.next_batch(cfg.batch_size)
+                elif cfg.sampling == "host":
                     batch = gen.integers(0, n, cfg.batch_size)
                 k_claim = w.last_avg_stamp.read()
                 u = w.store.claim_update_order()
@@ -736,6 +740,9 @@ class _Engine:
         n = cfg.objective.n_samples
         gens = {(q, r): np.random.default_rng(np.random.SeedSequence([cfg.seed, q, r + 1]))
                 for q in range(cfg.workers) for r in range(cfg.updaters)}
+        samplers = ({(q, r): worker_sampler(n, cfg.workers, q, r + 1, cfg.seed)
+                     for q in range(cfg.workers) for r in range(cfg.updaters)}
+                    if cfg.epoch_partition else None)
         active = {(q, r): True for q in range(cfg.workers) for r in range(cfg.updaters)}
         s_pre = [0] * cfg.workers
         self.round_trace = []
@@ -755,7 +762,10 @@ class _Engine:
                     if w.tags is not None and cfg.record_mode != "full":
                         tag_idx = np.sort(gens[(q, r)].choice(self.dim, size=w.tag_pick,
                                                               replace=False))
-                    batch = gens[(q, r)].integers(0, n, cfg.batch_size)
+                    if samplers is not None:
+                        batch = samplers[(q, r)].next_batch(cfg.batch_size)
+                    else:
+                        batch = gens[(q, r)].integers(0, n, cfg.batch_size)
                     k_claim = w.last_avg_stamp.read()
                     u = w.store.claim_update_order()
                     slot = t % (cfg.in_flight + 2)

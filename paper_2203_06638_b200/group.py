@@ -44,6 +44,14 @@ class ProcessGroup:
         dist.broadcast_object_list(name, src=0)
         if self.rank != 0:
             self._shm = shared_memory.SharedMemory(name=name[0])
+            # only the creator (rank 0) owns the segment's lifetime; attached
+            # ranks must not let their resource tracker unlink it at exit
+            try:
+                from multiprocessing import resource_tracker
+
+                resource_tracker.unregister(self._shm._name, "shared_memory")
+            except Exception:
+                pass
         self._buf = np.ndarray((RoundControl.cells(self.max_rounds),), dtype=np.int64,
                                buffer=self._shm.buf)
         if self.rank == 0:

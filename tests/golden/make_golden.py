@@ -126,6 +126,14 @@ def main() -> None:
     ex3 = st3.snapshot().tags.tolist()
     out["paramstore"] = {"sub_assign": ex1, "add_assign": ex2, "tags": ex3}
 
+    # ---------------- EpochSampler (objectives.py:77-104) ----------------
+    epochs = []
+    for n, Q, q, rank, seed, bs in [(37, 2, 0, 1, 1, 5), (37, 2, 1, 2, 1, 7), (48, 3, 2, 1, 9, 16),
+                                    (10, 1, 0, 1, 3, 4)]:
+        smp = robj.EpochSampler(np.arange(n)[q::Q], seed=seed * 1000 + q * 10 + rank)
+        epochs.append([n, Q, q, rank, seed, bs, [smp.next_batch(bs).tolist() for _ in range(9)]])
+    out["epoch_sampler"] = epochs
+
     (HERE / "scalars.json").write_text(json.dumps(out, indent=None, separators=(",", ":")))
 
     # ---------------- datasets (data.py:34-52) ----------------
@@ -175,13 +183,16 @@ def main() -> None:
     np.savez_compressed(HERE / "mlp.npz", **mlp)
 
     # ---------------- canonical serialized schedule from reference primitives ----------------
-    def serialized(obj, *, algo, Q, U, bounds, sched, sync, budget, t_st, B, seed):
+    def serialized(obj, *, algo, Q, U, bounds, sched, sync, budget, t_st, B, seed,
+                   epoch_partition=False):
         part = rpart.make_partition(obj.dim, bounds)
         x0 = obj.init_params(seed)
         stores = [ParamStore(x0) for _ in range(Q)]
         rngs = [[np.random.default_rng(np.random.SeedSequence([seed, q, r])) for r in range(1, U + 1)]
                 for q in range(Q)]
         active = [[True] * U for _ in range(Q)]
+        samplers = ([[robj.EpochSampler(np.arange(obj.n_samples)[q::Q], seed=seed * 1000 + q * 10 + r)
+                      for r in range(1, U + 1)] for q in range(Q)] if epoch_partition else None)
         s_pre = [0] * Q
         block_trace, lr_trace, round_trace = [], [], []
         sweep = 0
@@ -200,7 +211,10 @@ def main() -> None:
                         bid = 0
                     blk = part.block(bid)
                     snap = stores[q].snapshot()
-                    batch = robj.sample_batch(rngs[q][ri], obj.n_samples, B)
+                    if samplers is not None:
+                        batch = samplers[q][ri].next_batch(B)
+                    else:
+                        batch = robj.sample_batch(rngs[q][ri], obj.n_samples, B)
                     g = obj.grad_block(snap.values, blk, batch)
                     stores[q].sub_assign(blk.start, lr * g.values)
                     block_trace.append((q, rank, s, bid))
@@ -256,6 +270,12 @@ def main() -> None:
         "small_lap", small, True, algo="lap_sgd", Q=3, U=2, bounds=(0, small.dim),
         sched=rsched.constant_schedule(0.05, 40), sync=rsched.SyncScheme(total=40, period=3, switch_point=10),
         budget=40, t_st=0, B=8, seed=2)
+    save_serialized(
+        "deep_lpp_epoch", deep, True, algo="lpp_sgd", Q=2, U=2, bounds=(0, int(e[2]), deep.dim),
+        sched=rsched.LrSchedule(kind="cosine", alpha0=0.05, total=60, warmup=6, batch_local=8,
+                                workers=2, batch_base=8, boost=True),
+        sync=rsched.SyncScheme(total=60, period=4), budget=60, t_st=6, B=8, seed=1,
+        epoch_partition=True)
     c0_bounds = rpart.balanced_boundaries(c0.layer_param_counts, 2)
     save_serialized(
         "c0_lpp", c0, False, algo="lpp_sgd", Q=2, U=2, bounds=c0_bounds,

@@ -63,7 +63,8 @@ def _cfg_from_golden(name, obj, **over):
     kw = dict(algo=c["algo"], objective=obj, partition=make_partition(obj.dim, tuple(c["bounds"])),
               lr=lr, sync=sync, budget=c["budget"], warm_start_budget=c["t_st"], workers=c["Q"],
               updaters=c["U"], batch_size=c["B"], seed=c["seed"], schedule="serialized",
-              record_mode="full", record_tensors=False, evaluate=False)
+              record_mode="full", record_tensors=False, evaluate=False,
+              epoch_partition=c.get("epoch_partition", False))
     kw.update(over)
     return g, RunConfig(**kw)
 
@@ -86,10 +87,12 @@ def _oracle_run(g, X, y, hidden, k):
         lr=osched.Lr(kind=s["kind"], alpha0=s["alpha0"], total=s["total"], warmup=s["warmup"],
                      peak=s["peak"], milestones=tuple(s["milestones"]), gamma=s["gamma"]),
         switch_point=c["sync"]["switch_point"], period=c["sync"]["period"], budget=c["budget"],
-        warm_start=c["t_st"], batch_size=c["B"], seed=c["seed"])
+        warm_start=c["t_st"], batch_size=c["B"], seed=c["seed"],
+        epoch_partition=c.get("epoch_partition", False))
 
 
-@pytest.mark.parametrize("name,kind", [("deep_lpp", "deep"), ("small_lap", "small"), ("c0_lpp", "c0")])
+@pytest.mark.parametrize("name,kind", [("deep_lpp", "deep"), ("small_lap", "small"), ("c0_lpp", "c0"),
+                                       ("deep_lpp_epoch", "deep")])
 @pytest.mark.parametrize("mode", ["red", "bulk"])
 def test_serialized_engine_matches_oracle(name, kind, mode):
     from paper_2203_06638_b200.engine import run_experiment

@@ -135,3 +135,18 @@ def test_schedule_validation():
         SyncScheme(total=10, period=0)
     with pytest.raises(ValueError):
         lr_at(constant_schedule(0.1, 10), -1)
+
+
+def test_product_epoch_sampler_matches_reference(golden_scalars):
+    """objectives.py:77-104 / engine.py:294-296 (the product's host sampler)."""
+    from paper_2203_06638_b200.sampling import EpochSampler, sample_batch, worker_sampler
+
+    for n, Q, q, rank, seed, bs, batches in golden_scalars["epoch_sampler"]:
+        smp = worker_sampler(n, Q, q, rank, seed)
+        assert [smp.next_batch(bs).tolist() for _ in batches] == batches
+    with pytest.raises(ValueError):
+        EpochSampler([], 0)
+    import numpy as np
+
+    with pytest.raises(ValueError):
+        sample_batch(np.random.default_rng(0), 0, 4)
