@@ -293,6 +293,12 @@ class _Worker:
             self.tag_pinned = torch.zeros((U, depth, k), dtype=torch.int32, pin_memory=True)
             self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
             self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
+        # full record mode keeps every update's whole tag snapshot (reference
+        # full mode, engine.py:343-344); one buffer per in-flight slot
+        self.snap_tags = None
+        if cfg.tracks and cfg.record_mode == "full" and cfg.record_tensors:
+            self.snap_tags = [[torch.zeros(d, dtype=torch.int32, device=self.dev)
+                               for _ in range(depth)] for _ in range(U)]
         self.programs: list[StepProgram] = []
         self.idx_pinned = None
         self.batch_pinned = None
@@ -458,7 +464,10 @@ class _Engine:
             elif cfg.record_mode == "full":
                 # K5: full tagged snapshot; the min tag decides "clean"
                 w.min_dev[r, slot].fill_(2**31 - 1)
-                N.snapshot_tagged(w.store.arena.ptr, w.tag_arena.ptr, w.replicas[r].ptr, None,
+                out_tags = None
+                if w.snap_tags is not None and rec is not None:
+                    out_tags = w.snap_tags[r][slot].data_ptr()
+                N.snapshot_tagged(w.store.arena.ptr, w.tag_arena.ptr, w.replicas[r].ptr, out_tags,
                                   self.dim, w.min_dev[r, slot].data_ptr(), sp)
                 w.min_pinned[r, slot].copy_(w.min_dev[r, slot], non_blocking=True)
             else:
@@ -543,6 +552,8 @@ class _Engine:
             return
         if self.cfg.record_mode == "full":
             clean = int(w.min_pinned[r, slot]) >= rec.k_claim
+            if self.cfg.record_tensors and rec.snapshot is not None and rec.tags is None:
+                rec.tags = w.snap_tags[r][slot].cpu().numpy().astype(np.int64)
         else:
             tg = w.tag_pinned[r, slot, :w.tag_pick].numpy().astype(np.int64)
             rec.tags = tg
@@ -647,6 +658,9 @@ class _Engine:
                     st.synchronize()
             try:
                 u_of[r] = store.claim_update_order()
+                full = cfg.record_mode == "full" and cfg.record_tensors
+                # the worker's own view before any owner corrects it (quiescent: exact)
+                snap = w.store.arena.tensor.clone() if full else None
                 stamps = None
                 if fenced:
                     # every worker's round stamp is published before the owners
@@ -656,20 +670,28 @@ class _Engine:
                     if not self.ctrl.fence(0, r):
                         return
                     stamps = self.ctrl.stamps()
-                self.average(q, w.avg_stream, final=final, stamps=stamps)
+                self.average(q, w.avg_stream, final=final or full, stamps=stamps)
                 w.avg_stream.synchronize()
                 if fenced and not self.ctrl.fence(1, r):
                     return
+                if full:
+                    # the round mean, assembled from every owner's shard
+                    # (engine.py:441 keeps it for worker 0 only)
+                    mean = self.gather_round_mean() if q == 0 else None
+                    snaps[r] = (snap, mean)
                 w.last_avg_stamp.store(u_of[r])
                 w.synced_at.store(s_cur)
             finally:
                 if quiet:
                     w.gate.resume()
 
+        snaps = {}
+
         def on_round(r, s_cur, k_delta, unanimous):
+            snap, mean = snaps.pop(r, (None, None))
             self.stamps[q].append(AveragerStamp(
                 worker=q, round=r, u=u_of.pop(r), s_cur=s_cur, k_delta=k_delta,
-                wall_ms=(time.perf_counter() - self.t0) * 1e3))
+                wall_ms=(time.perf_counter() - self.t0) * 1e3, snapshot=snap, mean=mean))
 
         try:
             averager_loop(self.ctrl, workers=cfg.workers,
@@ -786,23 +808,35 @@ class _Engine:
             if fresh or drained:
                 rnd = len(self.round_trace) + 1
                 u_avgs = [self.workers[q].store.claim_update_order() for q in range(cfg.workers)]
+                full = cfg.record_mode == "full" and cfg.record_tensors
+                snaps = [self.workers[q].store.arena.tensor.clone() if full else None
+                         for q in range(cfg.workers)]
                 for q in range(cfg.workers):
                     w = self.workers[q]
-                    self.average(q, w.avg_stream, final=drained, stamps=u_avgs)
+                    self.average(q, w.avg_stream, final=drained or full, stamps=u_avgs)
                     w.avg_stream.synchronize()
+                mean = self.gather_round_mean() if full else None
                 for q in range(cfg.workers):
                     w = self.workers[q]
                     u_avg = u_avgs[q]
                     w.last_avg_stamp.store(u_avg)
                     self.stamps[q].append(AveragerStamp(
                         worker=q, round=rnd, u=u_avg, s_cur=counts[q], k_delta=counts[q] - s_pre[q],
-                        wall_ms=(time.perf_counter() - self.t0) * 1e3))
+                        wall_ms=(time.perf_counter() - self.t0) * 1e3, snapshot=snaps[q],
+                        mean=mean if q == 0 else None))
                     s_pre[q] = counts[q]
                 self.round_trace.append((rnd, sweep, *counts))
             if drained:
                 break
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         return self._device_span_end(starts)
+
+    def gather_round_mean(self):
+        """The current round's mean from the owners' mean_out shards (one process)."""
+        if self.group is not None:
+            return None
+        parts = [self.workers[q].mean_out[lo:hi] for q, (lo, hi) in enumerate(self.shards)]
+        return torch.cat(parts).clone()
 
     def final_values(self) -> np.ndarray:
         """The last round's mean, gathered shard by shard from the owners."""
@@ -993,6 +1027,13 @@ class _SyncEngine:
             ms = max(ms, starts[q].elapsed_time(e))
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         return ms
+
+    def gather_round_mean(self):
+        """The current round's mean from the owners' mean_out shards (one process)."""
+        if self.group is not None:
+            return None
+        parts = [self.workers[q].mean_out[lo:hi] for q, (lo, hi) in enumerate(self.shards)]
+        return torch.cat(parts).clone()
 
     def final_values(self) -> np.ndarray:
         return self.x[self.local[0]].tensor.cpu().numpy()

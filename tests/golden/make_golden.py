@@ -293,6 +293,26 @@ def main() -> None:
     res = rengine.run_experiment(cfg)
     np.savez_compressed(HERE / "engine_q1u1.npz", final=res.final_values, x0=res.x0,
                         counter_finals=np.array(res.counter_finals))
+    # ---------------- event log + replay (instrumentation.py:166-219, 371-463) ----------------
+    from asyncsgd import instrumentation as rinst
+
+    cfg = rengine.RunConfig(
+        algo="lpp_sgd", objective=deep, partition=rpart.make_partition(deep.dim, (0, int(e[2]), deep.dim)),
+        lr=rsched.constant_schedule(0.05, 40), sync=rsched.SyncScheme(total=40, period=4, switch_point=8),
+        budget=40, warm_start_budget=6, workers=2, updaters=2, batch_size=8, seed=3,
+        record_mode="full", quiescent=True)
+    res = rengine.run_experiment(cfg)
+    import gzip
+
+    tmp = Path("/tmp/eventlog_ref.ndjson")
+    rinst.save_event_log(tmp, res)
+    with open(tmp, "rb") as src, gzip.GzipFile(HERE / "eventlog_ref.ndjson.gz", "wb", mtime=0) as dst:
+        dst.write(src.read())
+    rep = rinst.replay_rounds(res)
+    measured = [st.mean for st in sorted(res.stamps, key=lambda st: st.round) if st.worker == 0]
+    np.savez_compressed(HERE / "eventlog_ref_replay.npz", round_means=np.stack(rep.round_means),
+                        measured=np.stack(measured), x0=res.x0, distances=rep.distances,
+                        clean=rep.clean, k_bar=np.array([rep.k_bar]))
     print("golden vectors written to", HERE)
 
 

@@ -347,3 +347,31 @@ def test_async_tags_classify_updates_and_p_hat():
         top = max([u.u for u in res.updates if u.worker == q] +
                   [st.u for st in res.stamps if st.worker == q])
         assert all(int(t) <= top for u in res.updates if u.worker == q for t in u.tags)
+
+
+@pytest.mark.parametrize("schedule", ["serialized", "async"])
+def test_event_log_replays_gpu_run(tmp_path, schedule):
+    """a GPU run's NDJSON event log (reference schema)
+    replays on the CPU oracle to the round means the GPU measured (quiescent
+    async run, or the serialized schedule), within the fp32 contract."""
+    from oracle import replay
+    from paper_2203_06638_b200.engine import run_experiment
+    from paper_2203_06638_b200.eventlog import save_event_log
+    from paper_2203_06638_b200.partition import make_partition
+
+    obj = _mlp("deep")[0]
+    bounds = (0, obj.edges[2], obj.dim)
+    cfg = _tiny(obj, algo="lpp_sgd", budget=40, workers=2, updaters=2, record_mode="full",
+                partition=make_partition(obj.dim, bounds), warm_start_budget=6,
+                quiescent=(schedule == "async"), schedule=schedule)
+    res = run_experiment(cfg)
+    path = tmp_path / "run.ndjson"
+    save_event_log(path, res)
+    ups, sts = replay.load_event_log(path)
+    assert len(ups) == len(res.updates) == sum(res.counter_finals)
+    rep = replay.replay_rounds(ups, sts, res.x0, bounds)
+    measured = [st.mean for st in sorted(sts, key=lambda s: s.round) if st.worker == 0]
+    assert len(measured) == len(rep["round_means"]) - 1
+    np.testing.assert_allclose(np.stack(rep["round_means"][1:]), np.stack(measured), atol=ATOL, rtol=RTOL)
+    np.testing.assert_allclose(measured[-1], res.final_values, atol=1e-6)
+    assert all(c is True for c in rep["clean"])     # quiescent / serialized: every update clean
