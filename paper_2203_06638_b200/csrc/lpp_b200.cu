@@ -121,7 +121,7 @@ static int current_sms() {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;       // independent 16-byte loads in flight per thread
-constexpr int kBlocksPerSM = 8;  // 8 x 256 threads = 2048 = full SM occupancy
+constexpr int kBlocksPerSM = 16;  // 2 waves of 8 x 256 threads: better tail than 1 wave
 
 static unsigned grid_for(size_t nvec, int sms) {
   size_t want = (nvec + kThreads - 1) / kThreads;
