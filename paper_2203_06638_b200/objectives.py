@@ -234,6 +234,16 @@ class MlpObjective(ArenaObjective):
         return sum(2 * self.widths[l] * self.widths[l + 1] for l in range(first, self.n_layers))
 
 
+def flops_savings_ratio(obj: ArenaObjective, partition) -> float:
+    """Backward work saved by cycling partial blocks instead of full passes:
+    ``1 - sum_i cost(block_i) / (U * cost(full))`` (objectives.py:326-337)."""
+    if obj.layer_param_counts is None:
+        raise ValueError("truncated-backprop savings need a layered objective")
+    full = obj.backward_cost(Block(0, obj.dim))
+    blocks = partition.blocks()
+    return 1.0 - sum(obj.backward_cost(b) for b in blocks) / (len(blocks) * full)
+
+
 # ---------------------------------------------------------------------------
 # ResNets (CIFAR ResNet-20 / ResNet-18, ImageNet ResNet-50)
 

@@ -375,3 +375,53 @@ def test_event_log_replays_gpu_run(tmp_path, schedule):
     np.testing.assert_allclose(np.stack(rep["round_means"][1:]), np.stack(measured), atol=ATOL, rtol=RTOL)
     np.testing.assert_allclose(measured[-1], res.final_values, atol=1e-6)
     assert all(c is True for c in rep["clean"])     # quiescent / serialized: every update clean
+
+
+def test_block_gradients_are_slices_of_full_mlp():
+    """test_objectives.py:211-221 on the GPU objective (fp32)."""
+    from paper_2203_06638_b200.partition import Block, balanced_boundaries, make_partition
+
+    obj = _mlp("deep")[0]
+    x = obj.init_params(5)
+    batch = np.random.default_rng(5).integers(0, obj.n_samples, 8)
+    full = obj.grad_block(x, Block(0, obj.dim), batch).values
+    part = make_partition(obj.dim, balanced_boundaries(obj.layer_param_counts, 4))
+    for blk in part.blocks():
+        got = obj.grad_block(x, blk, batch).values
+        assert torch.equal(got, full[blk.start:blk.stop])
+
+
+def test_captured_partial_backprop_matches_full_slices_resnet20():
+    """The engine's captured per-block graphs (StepProgram) on ResNet-20:
+    every block's gradient equals the full gradient's slice (fp32, TF32 off,
+    deterministic cuDNN)."""
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.partition import balanced_boundaries, make_partition
+    from paper_2203_06638_b200.step import StepProgram
+
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    try:
+        obj = ResNetObjective("resnet20", n_samples=256, seed=0, autocast=None)
+        part = make_partition(obj.dim, balanced_boundaries(obj.layer_param_counts, 4))
+        dev = torch.device("cuda", 0)
+        x = torch.from_numpy(obj.init_params(0).astype(np.float32)).to(dev)
+        replica, grads = x.clone(), torch.zeros_like(x)
+        st = torch.cuda.Stream()
+        blocks = {b: part.block(b) for b in range(5)}
+        prog = StepProgram(obj, dev, replica, grads, blocks, 32, st, input_mode="index")
+        prog.idx.copy_(torch.arange(32, device=dev) * 3)
+        outs = {}
+        for b in range(5):
+            replica.copy_(x)          # BN running stats change; params identical
+            with torch.cuda.stream(st):
+                prog.run(b)
+            st.synchronize()
+            outs[b] = grads.clone()
+        full = outs[0]
+        for b in range(1, 5):
+            blk = blocks[b]
+            np.testing.assert_allclose(outs[b][blk.start:blk.stop].cpu().numpy(),
+                                       full[blk.start:blk.stop].cpu().numpy(), rtol=1e-5, atol=1e-6)
+    finally:
+        torch.backends.cudnn.deterministic = False
