@@ -169,6 +169,42 @@ int lpp_average_shard_tagged(float* const* arenas, int32_t* const* tags,
                              float* mean_out, int mode, void* stream);
 
 /* ------------------------------------------------------------------ */
+/* NVLS averaging: VMM buffers bound to a multicast  */
+/* object; the owner reduces its shard IN the NVSwitch and broadcasts    */
+/* the mean (multimem.ld_reduce / multimem.st), each worker then adds    */
+/* (mean - snapshot) locally — the reference round snapshot -> mean      */
+/* all-reduce -> add_assign(mean - snap) (engine.py:418-421).            */
+typedef struct lpp_vmm* lpp_vmm_t;
+typedef struct lpp_mc* lpp_mc_t;
+int lpp_mc_supported(int device, int* out);
+/* allocation granularity for a multicast object over num_devices */
+int lpp_mc_granularity(int device, int num_devices, size_t* out);
+/* device memory from cuMemCreate (size rounded up to the granularity),
+ * mapped read/write on `device`, zero-filled */
+int lpp_vmm_create(int device, size_t bytes, lpp_vmm_t* out);
+float* lpp_vmm_ptr(lpp_vmm_t v);
+size_t lpp_vmm_size(lpp_vmm_t v);
+int lpp_vmm_destroy(lpp_vmm_t v);
+/* multicast object lifecycle: create (one process) -> export/import the
+ * POSIX fd (others) -> every process adds its device -> (group barrier) ->
+ * every process binds its VMM buffer -> map the multicast VA */
+int lpp_mc_create(int num_devices, size_t bytes, lpp_mc_t* out);
+int lpp_mc_export_fd(lpp_mc_t mc, int* fd_out);
+int lpp_mc_import_fd(int fd, size_t bytes, lpp_mc_t* out);
+int lpp_mc_add_device(lpp_mc_t mc, int device);
+int lpp_mc_bind(lpp_mc_t mc, lpp_vmm_t mem, size_t mc_offset);
+int lpp_mc_map(lpp_mc_t mc, int device, float** mc_ptr_out);
+int lpp_mc_destroy(lpp_mc_t mc);
+/* owner: mc_mean[e] = (sum over workers of mc_stage[e]) / Q for e in
+ * [lo, hi) (lo a multiple of 4); both pointers are multicast addresses */
+int lpp_nvls_mean_shard(const float* mc_stage, float* mc_mean, size_t lo, size_t hi,
+                        int Q, void* stream);
+/* local: x[e] += mean[e] - stage[e] atomically, tags[e] = stamp (tags may
+ * be NULL); 16-byte aligned buffers */
+int lpp_nvls_apply(float* x, const float* stage, const float* mean, size_t n,
+                   int32_t* tags, int32_t stamp, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* utilities */
 /* Write a buffer of n_bytes (>= L2 size to flush it) on the stream. */
 int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream);

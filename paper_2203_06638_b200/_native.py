@@ -90,6 +90,21 @@ _SIGS = {
         [_c.POINTER(_vp), _c.POINTER(_vp), _c.POINTER(_c.c_int32), _c.c_int, _size, _size, _vp,
          _c.c_int, _vp],
     ),
+    "lpp_mc_supported": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
+    "lpp_mc_granularity": (_c.c_int, [_c.c_int, _c.c_int, _c.POINTER(_size)]),
+    "lpp_vmm_create": (_c.c_int, [_c.c_int, _size, _c.POINTER(_vp)]),
+    "lpp_vmm_ptr": (_vp, [_vp]),
+    "lpp_vmm_size": (_size, [_vp]),
+    "lpp_vmm_destroy": (_c.c_int, [_vp]),
+    "lpp_mc_create": (_c.c_int, [_c.c_int, _size, _c.POINTER(_vp)]),
+    "lpp_mc_export_fd": (_c.c_int, [_vp, _c.POINTER(_c.c_int)]),
+    "lpp_mc_import_fd": (_c.c_int, [_c.c_int, _size, _c.POINTER(_vp)]),
+    "lpp_mc_add_device": (_c.c_int, [_vp, _c.c_int]),
+    "lpp_mc_bind": (_c.c_int, [_vp, _vp, _size]),
+    "lpp_mc_map": (_c.c_int, [_vp, _c.c_int, _c.POINTER(_vp)]),
+    "lpp_mc_destroy": (_c.c_int, [_vp]),
+    "lpp_nvls_mean_shard": (_c.c_int, [_vp, _vp, _size, _size, _c.c_int, _vp]),
+    "lpp_nvls_apply": (_c.c_int, [_vp, _vp, _vp, _size, _vp, _c.c_int32, _vp]),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
 }

@@ -951,3 +951,414 @@ extern "C" int lpp_sm_count(int device, int* out) {
   CUDA_TRY(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device));
   return LPP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// NVLS (NVLink SHARP) averaging: SURVEY §8f rank 1.
+//
+// The reference round is snapshot -> mean all-reduce -> add_assign(mean -
+// snapshot) (engine.py:418-421).  On NVSwitch the all-reduce runs IN the
+// switch: every worker stages its snapshot in a VMM buffer bound to one
+// multicast object; the owner of shard o issues multimem.ld_reduce (SASS
+// LDGMC) on the multicast address — the switch reads shard o from all Q
+// GPUs and returns the sum — and multimem.st broadcasts the mean into every
+// worker's mean buffer; each worker then adds (mean - snapshot) into its own
+// arena locally.  Per GPU and direction the NVLink bytes are ~4d(1 + 1/Q)
+// instead of the 2·4d(Q-1)/Q of the P2P owner-computes round.
+
+#include <cuda.h>
+
+// The driver API is resolved at run time through the runtime's entry-point
+// query, so the library needs no link-time libcuda (it loads on CPU-only
+// build hosts; every device entry point then reports the missing driver).
+namespace drv {
+#define LPP_DRV_FN(name, ret, args) \
+  typedef ret(*name##_t) args;      \
+  static name##_t name = nullptr;
+LPP_DRV_FN(cuGetErrorString, CUresult, (CUresult, const char**))
+LPP_DRV_FN(cuDeviceGet, CUresult, (CUdevice*, int))
+LPP_DRV_FN(cuDeviceGetAttribute, CUresult, (int*, CUdevice_attribute, CUdevice))
+LPP_DRV_FN(cuMulticastGetGranularity, CUresult,
+           (size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags))
+LPP_DRV_FN(cuMemGetAllocationGranularity, CUresult,
+           (size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags))
+LPP_DRV_FN(cuMemCreate, CUresult,
+           (CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long))
+LPP_DRV_FN(cuMemAddressReserve, CUresult,
+           (CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long))
+LPP_DRV_FN(cuMemAddressFree, CUresult, (CUdeviceptr, size_t))
+LPP_DRV_FN(cuMemMap, CUresult,
+           (CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long))
+LPP_DRV_FN(cuMemUnmap, CUresult, (CUdeviceptr, size_t))
+LPP_DRV_FN(cuMemSetAccess, CUresult, (CUdeviceptr, size_t, const CUmemAccessDesc*, size_t))
+LPP_DRV_FN(cuMemsetD8, CUresult, (CUdeviceptr, unsigned char, size_t))
+LPP_DRV_FN(cuMemRelease, CUresult, (CUmemGenericAllocationHandle))
+LPP_DRV_FN(cuMulticastCreate, CUresult, (CUmemGenericAllocationHandle*, const CUmulticastObjectProp*))
+LPP_DRV_FN(cuMulticastAddDevice, CUresult, (CUmemGenericAllocationHandle, CUdevice))
+LPP_DRV_FN(cuMulticastBindMem, CUresult,
+           (CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+            unsigned long long))
+LPP_DRV_FN(cuMulticastUnbind, CUresult, (CUmemGenericAllocationHandle, CUdevice, size_t, size_t))
+LPP_DRV_FN(cuMemExportToShareableHandle, CUresult,
+           (void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long))
+LPP_DRV_FN(cuMemImportFromShareableHandle, CUresult,
+           (CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType))
+#undef LPP_DRV_FN
+
+template <typename T>
+static bool load(T& fn, const char* name) {
+  if (fn) return true;
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    return false;
+  fn = reinterpret_cast<T>(p);
+  return true;
+}
+
+static int init() {
+  static std::atomic<int> state{0};  // 0 unknown, 1 ok, -1 failed
+  int st = state.load();
+  if (st) return st > 0 ? LPP_OK : set_err(LPP_E_CUDA, "CUDA driver entry points unavailable");
+  bool ok = load(cuGetErrorString, "cuGetErrorString") && load(cuDeviceGet, "cuDeviceGet") &&
+            load(cuDeviceGetAttribute, "cuDeviceGetAttribute") &&
+            load(cuMulticastGetGranularity, "cuMulticastGetGranularity") &&
+            load(cuMemGetAllocationGranularity, "cuMemGetAllocationGranularity") &&
+            load(cuMemCreate, "cuMemCreate") && load(cuMemAddressReserve, "cuMemAddressReserve") &&
+            load(cuMemAddressFree, "cuMemAddressFree") && load(cuMemMap, "cuMemMap") &&
+            load(cuMemUnmap, "cuMemUnmap") && load(cuMemSetAccess, "cuMemSetAccess") &&
+            load(cuMemsetD8, "cuMemsetD8") && load(cuMemRelease, "cuMemRelease") &&
+            load(cuMulticastCreate, "cuMulticastCreate") &&
+            load(cuMulticastAddDevice, "cuMulticastAddDevice") &&
+            load(cuMulticastBindMem, "cuMulticastBindMem") &&
+            load(cuMulticastUnbind, "cuMulticastUnbind") &&
+            load(cuMemExportToShareableHandle, "cuMemExportToShareableHandle") &&
+            load(cuMemImportFromShareableHandle, "cuMemImportFromShareableHandle");
+  state.store(ok ? 1 : -1);
+  return ok ? LPP_OK : set_err(LPP_E_CUDA, "CUDA driver entry points unavailable");
+}
+}  // namespace drv
+
+#define CU_TRY(expr)                                                        \
+  do {                                                                      \
+    CUresult r_ = (drv::expr);                                              \
+    if (r_ != CUDA_SUCCESS) {                                               \
+      const char* s_ = nullptr;                                             \
+      drv::cuGetErrorString(r_, &s_);                                       \
+      return set_err(LPP_E_CUDA, "%s failed: %s", #expr, s_ ? s_ : "?");    \
+    }                                                                       \
+  } while (0)
+#define DRV_INIT()                   \
+  do {                               \
+    int rc_ = drv::init();           \
+    if (rc_) return rc_;             \
+  } while (0)
+
+struct lpp_vmm {
+  CUmemGenericAllocationHandle h;
+  CUdeviceptr ptr;
+  size_t size;
+  int device;
+};
+
+struct lpp_mc {
+  CUmemGenericAllocationHandle h;
+  size_t size;
+  CUdeviceptr ptr;  // mapped multicast VA (0 until lpp_mc_map)
+  int mapped_device;
+  int bound_device;
+  size_t bound_offset, bound_size;
+};
+
+static CUmemAllocationProp vmm_prop(int device) {
+  CUmemAllocationProp p;
+  memset(&p, 0, sizeof(p));
+  p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  p.location.id = device;
+  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return p;
+}
+
+static int ensure_ctx(int device) {
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaFree(0));  // make the primary context current for the driver API
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_supported(int device, int* out) {
+  if (!out) return set_err(LPP_E_VALUE, "mc_supported: null out");
+  DRV_INIT();
+  CUDA_TRY(cudaFree(0));
+  CUdevice dev;
+  CU_TRY(cuDeviceGet(&dev, device));
+  CU_TRY(cuDeviceGetAttribute(out, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_granularity(int device, int num_devices, size_t* out) {
+  if (!out) return set_err(LPP_E_VALUE, "mc_granularity: null out");
+  DRV_INIT();
+  CUDA_TRY(cudaFree(0));
+  CUmulticastObjectProp mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.numDevices = (unsigned)num_devices;
+  mp.size = 1;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g1 = 0, g2 = 0;
+  CU_TRY(cuMulticastGetGranularity(&g1, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap = vmm_prop(device);
+  CU_TRY(cuMemGetAllocationGranularity(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  *out = g1 > g2 ? g1 : g2;
+  return LPP_OK;
+}
+
+extern "C" int lpp_vmm_create(int device, size_t bytes, lpp_vmm_t* out) {
+  if (!out) return set_err(LPP_E_VALUE, "vmm_create: null out");
+  *out = nullptr;
+  DeviceGuard guard(device);
+  int rc = ensure_ctx(device);
+  if (rc) return rc;
+  size_t gran = 0;
+  rc = lpp_mc_granularity(device, 1, &gran);
+  if (rc) return rc;
+  size_t size = ((bytes ? bytes : 1) + gran - 1) / gran * gran;
+  CUmemAllocationProp prop = vmm_prop(device);
+  lpp_vmm* v = new lpp_vmm{0, 0, size, device};
+  CUresult r = drv::cuMemCreate(&v->h, size, &prop, 0);
+  if (r != CUDA_SUCCESS) {
+    delete v;
+    return set_err(LPP_E_NOMEM, "vmm_create: cuMemCreate(%zu) failed (%d)", size, (int)r);
+  }
+  CU_TRY(cuMemAddressReserve(&v->ptr, size, gran, 0, 0));
+  CU_TRY(cuMemMap(v->ptr, size, 0, v->h, 0));
+  CUmemAccessDesc ad;
+  memset(&ad, 0, sizeof(ad));
+  ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ad.location.id = device;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CU_TRY(cuMemSetAccess(v->ptr, size, &ad, 1));
+  CU_TRY(cuMemsetD8(v->ptr, 0, size));
+  *out = v;
+  return LPP_OK;
+}
+
+extern "C" float* lpp_vmm_ptr(lpp_vmm_t v) { return v ? (float*)v->ptr : nullptr; }
+extern "C" size_t lpp_vmm_size(lpp_vmm_t v) { return v ? v->size : 0; }
+
+extern "C" int lpp_vmm_destroy(lpp_vmm_t v) {
+  if (!v) return LPP_OK;
+  DeviceGuard guard(v->device);
+  CU_TRY(cuMemUnmap(v->ptr, v->size));
+  CU_TRY(cuMemAddressFree(v->ptr, v->size));
+  CU_TRY(cuMemRelease(v->h));
+  delete v;
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_create(int num_devices, size_t bytes, lpp_mc_t* out) {
+  if (!out || num_devices < 1) return set_err(LPP_E_VALUE, "mc_create: bad arguments");
+  DRV_INIT();
+  CUDA_TRY(cudaFree(0));
+  CUmulticastObjectProp mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.numDevices = (unsigned)num_devices;
+  mp.size = bytes;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  lpp_mc* m = new lpp_mc{0, bytes, 0, -1, -1, 0, 0};
+  CUresult r = drv::cuMulticastCreate(&m->h, &mp);
+  if (r != CUDA_SUCCESS) {
+    delete m;
+    const char* s = nullptr;
+    drv::cuGetErrorString(r, &s);
+    return set_err(LPP_E_CUDA, "cuMulticastCreate(%d devices, %zu B) failed: %s", num_devices,
+                   bytes, s ? s : "?");
+  }
+  *out = m;
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_export_fd(lpp_mc_t m, int* fd_out) {
+  if (!m || !fd_out) return set_err(LPP_E_VALUE, "mc_export_fd: null argument");
+  CU_TRY(cuMemExportToShareableHandle(fd_out, m->h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_import_fd(int fd, size_t bytes, lpp_mc_t* out) {
+  if (!out) return set_err(LPP_E_VALUE, "mc_import_fd: null out");
+  DRV_INIT();
+  CUDA_TRY(cudaFree(0));
+  lpp_mc* m = new lpp_mc{0, bytes, 0, -1, -1, 0, 0};
+  CUresult r = drv::cuMemImportFromShareableHandle(&m->h, (void*)(uintptr_t)fd,
+                                              CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  if (r != CUDA_SUCCESS) {
+    delete m;
+    return set_err(LPP_E_CUDA, "mc_import_fd failed (%d)", (int)r);
+  }
+  *out = m;
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_add_device(lpp_mc_t m, int device) {
+  if (!m) return set_err(LPP_E_VALUE, "mc_add_device: null mc");
+  int rc = ensure_ctx(device);
+  if (rc) return rc;
+  CUdevice dev;
+  CU_TRY(cuDeviceGet(&dev, device));
+  CU_TRY(cuMulticastAddDevice(m->h, dev));
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_bind(lpp_mc_t m, lpp_vmm_t mem, size_t mc_offset) {
+  if (!m || !mem) return set_err(LPP_E_VALUE, "mc_bind: null argument");
+  if (mc_offset + mem->size > m->size) return set_err(LPP_E_INDEX, "mc_bind: range outside object");
+  DeviceGuard guard(mem->device);
+  CU_TRY(cuMulticastBindMem(m->h, mc_offset, mem->h, 0, mem->size, 0));
+  m->bound_device = mem->device;
+  m->bound_offset = mc_offset;
+  m->bound_size = mem->size;
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_map(lpp_mc_t m, int device, float** ptr_out) {
+  if (!m || !ptr_out) return set_err(LPP_E_VALUE, "mc_map: null argument");
+  DeviceGuard guard(device);
+  size_t gran = 0;
+  int rc = lpp_mc_granularity(device, 1, &gran);
+  if (rc) return rc;
+  CU_TRY(cuMemAddressReserve(&m->ptr, m->size, gran, 0, 0));
+  CU_TRY(cuMemMap(m->ptr, m->size, 0, m->h, 0));
+  CUmemAccessDesc ad;
+  memset(&ad, 0, sizeof(ad));
+  ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ad.location.id = device;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CU_TRY(cuMemSetAccess(m->ptr, m->size, &ad, 1));
+  m->mapped_device = device;
+  *ptr_out = (float*)m->ptr;
+  return LPP_OK;
+}
+
+extern "C" int lpp_mc_destroy(lpp_mc_t m) {
+  if (!m) return LPP_OK;
+  if (m->ptr) {
+    DeviceGuard guard(m->mapped_device);
+    CU_TRY(cuMemUnmap(m->ptr, m->size));
+    CU_TRY(cuMemAddressFree(m->ptr, m->size));
+  }
+  if (m->bound_device >= 0) {
+    CUdevice dev;
+    CU_TRY(cuDeviceGet(&dev, m->bound_device));
+    CU_TRY(cuMulticastUnbind(m->h, dev, m->bound_offset, m->bound_size));
+  }
+  CU_TRY(cuMemRelease(m->h));
+  delete m;
+  return LPP_OK;
+}
+
+// owner: mean of shard [lo, hi) reduced in the switch, broadcast to all
+__global__ void __launch_bounds__(kThreads)
+    k_nvls_mean(const float* mc_stage, float* mc_mean, size_t lo, size_t n, size_t nvec, int Q) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float fq = (float)Q;
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * kUnroll) {
+    float4 s[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(s[u].x), "=f"(s[u].y), "=f"(s[u].z), "=f"(s[u].w)
+                     : "l"(mc_stage + lo + 4 * i)
+                     : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (i < nvec) {
+        float4 m;
+        m.x = __fdiv_rn(s[u].x, fq);
+        m.y = __fdiv_rn(s[u].y, fq);
+        m.z = __fdiv_rn(s[u].z, fq);
+        m.w = __fdiv_rn(s[u].w, fq);
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(
+                         mc_mean + lo + 4 * i),
+                     "f"(m.x), "f"(m.y), "f"(m.z), "f"(m.w)
+                     : "memory");
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x) {
+      float sum;
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];"
+                   : "=f"(sum)
+                   : "l"(mc_stage + lo + e)
+                   : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc_mean + lo + e),
+                   "f"(__fdiv_rn(sum, fq))
+                   : "memory");
+    }
+  }
+}
+
+extern "C" int lpp_nvls_mean_shard(const float* mc_stage, float* mc_mean, size_t lo, size_t hi,
+                                   int Q, void* stream) {
+  if (!mc_stage || !mc_mean) return set_err(LPP_E_VALUE, "nvls_mean_shard: null pointer");
+  if (hi < lo) return set_err(LPP_E_INDEX, "nvls_mean_shard: hi < lo");
+  if (lo & 3u) return set_err(LPP_E_VALUE, "nvls_mean_shard: shard start must be a multiple of 4");
+  if (Q < 1) return set_err(LPP_E_VALUE, "nvls_mean_shard: Q < 1");
+  size_t n = hi - lo;
+  if (n == 0) return LPP_OK;
+  size_t nvec = n / 4;
+  k_nvls_mean<<<grid_for(nvec ? nvec : 1, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
+      mc_stage, mc_mean, lo, n, nvec, Q);
+  LAUNCH_CHECK("nvls_mean_shard");
+  return LPP_OK;
+}
+
+// local: x[e] += mean[e] - stage[e] (element-atomic), then the round's tag
+__global__ void __launch_bounds__(kThreads)
+    k_nvls_apply(float* x, const float* __restrict__ stage, const float* __restrict__ mean,
+                 size_t n, size_t nvec, int* tags, int stamp) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (size_t i = tid; i < nvec; i += stride) {
+    float4 s = __ldcg(reinterpret_cast<const float4*>(stage) + i);
+    float4 m = __ldcg(reinterpret_cast<const float4*>(mean) + i);
+    float4 c;
+    c.x = __fsub_rn(m.x, s.x);
+    c.y = __fsub_rn(m.y, s.y);
+    c.z = __fsub_rn(m.z, s.z);
+    c.w = __fsub_rn(m.w, s.w);
+    red_add_v4(x + 4 * i, c);
+    if (tags) {
+      __threadfence();
+      st_tag4(tags + 4 * i, stamp);
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x) {
+      red_add_f32(x + e, __fsub_rn(ld_cg(mean + e), ld_cg(stage + e)));
+      if (tags) {
+        __threadfence();
+        st_tag(tags + e, stamp);
+      }
+    }
+  }
+}
+
+extern "C" int lpp_nvls_apply(float* x, const float* stage, const float* mean, size_t n,
+                              int32_t* tags, int32_t stamp, void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!x || !stage || !mean) return set_err(LPP_E_VALUE, "nvls_apply: null pointer");
+  if ((((uintptr_t)x) | ((uintptr_t)stage) | ((uintptr_t)mean) | (tags ? (uintptr_t)tags : 0)) &
+      15u)
+    return set_err(LPP_E_VALUE, "nvls_apply: buffers must be 16-byte aligned");
+  size_t nvec = n / 4;
+  k_nvls_apply<<<grid_for(nvec ? nvec : 1, current_sms()), kThreads, 0, (cudaStream_t)stream>>>(
+      x, stage, mean, n, nvec, tags, stamp);
+  LAUNCH_CHECK("nvls_apply");
+  return LPP_OK;
+}

@@ -85,6 +85,7 @@ class RunConfig:
     use_graphs: bool = True
     in_flight: int = 2
     evaluate: bool = True            # compute the initial/final MetricsRow losses
+    averaging: str = "p2p"           # "p2p": owner-computes over peer arenas; "nvls": in-switch
     track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
     record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
 
@@ -120,6 +121,8 @@ class RunConfig:
             raise ValueError(f"unknown sampling {self.sampling!r}")
         if self.epoch_partition and self.sampling != "host":
             raise ValueError("epoch_partition draws indices on the host: use sampling='host'")
+        if self.averaging not in ("p2p", "nvls"):
+            raise ValueError(f"unknown averaging {self.averaging!r}")
         if self.workers > N.MAX_WORKERS:
             raise ValueError(f"at most {N.MAX_WORKERS} workers per averaging group")
 
@@ -385,6 +388,12 @@ class _Engine:
                              if cfg.tracks else None)
             self.ctrl = group.control
         self.shards = shard_bounds(self.dim, cfg.workers)
+        self.nvls = {}
+        if cfg.averaging == "nvls" and cfg.algo in ("lap_sgd", "lpp_sgd"):
+            from .nvls import NvlsGroup
+
+            for q in self.local_workers:
+                self.nvls[q] = NvlsGroup(self.dim, cfg.workers, self.workers[q].device, group=group)
         lpp = cfg.algo == "lpp_sgd"
         ids = [[0] + ([r + 1] if lpp else []) for r in range(cfg.updaters)]
         for w in self.workers.values():
@@ -525,6 +534,29 @@ class _Engine:
         else:
             N.average_shard(self.arena_ptrs, lo, hi, mean_ptr, N.MODE_RED, stream.cuda_stream)
 
+    def nvls_round(self, q: int, u: int, final: bool, fence=None) -> None:
+        """One NVLS round for worker q: stage -> (all staged) -> in-switch
+        mean of the owned shard -> (all broadcast) -> local add of
+        (mean - stage).  ``fence(i)`` is the group barrier between phases."""
+        w = self.workers[q]
+        nv = self.nvls[q]
+        st = w.avg_stream
+        sp = st.cuda_stream
+        nv.stage_copy(w.store.arena.ptr, sp)
+        st.synchronize()
+        if fence is not None and not fence(0):
+            return
+        lo, hi = self.shards[q]
+        nv.reduce_mean(lo, hi, sp)
+        st.synchronize()
+        if fence is not None and not fence(1):
+            return
+        nv.apply(w.store.arena.ptr, w.tag_arena.ptr if w.tags is not None else None, u, sp)
+        if final:
+            with torch.cuda.stream(st):
+                w.mean_out[: self.dim].copy_(nv.mean_tensor)
+        st.synchronize()
+
     def fail(self, exc: BaseException) -> None:
         with self.err_lock:
             self.errors.append(exc)
@@ -661,6 +693,13 @@ class _Engine:
                 full = cfg.record_mode == "full" and cfg.record_tensors
                 # the worker's own view before any owner corrects it (quiescent: exact)
                 snap = w.store.arena.tensor.clone() if full else None
+                if self.nvls:
+                    self.nvls_round(q, u_of[r], final or full, fence=lambda i: self.ctrl.fence(i, r))
+                    w.last_avg_stamp.store(u_of[r])
+                    w.synced_at.store(s_cur)
+                    if full:
+                        snaps[r] = (snap, self.nvls[q].mean_tensor.clone() if q == 0 else None)
+                    return
                 stamps = None
                 if fenced:
                     # every worker's round stamp is published before the owners
@@ -813,9 +852,13 @@ class _Engine:
                          for q in range(cfg.workers)]
                 for q in range(cfg.workers):
                     w = self.workers[q]
-                    self.average(q, w.avg_stream, final=drained or full, stamps=u_avgs)
+                    if self.nvls:
+                        self.nvls_round(q, u_avgs[q], drained or full)
+                    else:
+                        self.average(q, w.avg_stream, final=drained or full, stamps=u_avgs)
                     w.avg_stream.synchronize()
-                mean = self.gather_round_mean() if full else None
+                mean = (self.gather_round_mean() if not self.nvls else
+                        self.nvls[0].mean_tensor.clone()) if full else None
                 for q in range(cfg.workers):
                     w = self.workers[q]
                     u_avg = u_avgs[q]
@@ -840,14 +883,15 @@ class _Engine:
 
     def final_values(self) -> np.ndarray:
         """The last round's mean, gathered shard by shard from the owners."""
+        if self.nvls:
+            # every worker holds the whole broadcast mean
+            q = self.local_workers[0]
+            return self.workers[q].mean_out[: self.dim].cpu().numpy()
+        if self.group is not None:
+            return self.group.gather_mean(self.workers[self.group.rank].mean_out, self.shards)
         out = np.empty(self.dim, dtype=np.float32)
         for q, (lo, hi) in enumerate(self.shards):
-            if self.group is None:
-                out[lo:hi] = self.workers[q].mean_out[lo:hi].cpu().numpy()
-            else:
-                pass
-        if self.group is not None:
-            out = self.group.gather_mean(self.workers[self.group.rank].mean_out, self.shards)
+            out[lo:hi] = self.workers[q].mean_out[lo:hi].cpu().numpy()
         return out
 
     def apply_timing(self):
@@ -858,6 +902,8 @@ class _Engine:
         return (len(self.apply_events), ms, nbytes)
 
     def close(self):
+        for nv in self.nvls.values():
+            nv.close()
         for w in self.workers.values():
             w.close()
 
