@@ -86,6 +86,7 @@ class RunConfig:
     in_flight: int = 2
     evaluate: bool = True            # compute the initial/final MetricsRow losses
     averaging: str = "p2p"           # "p2p": owner-computes over peer arenas; "nvls": in-switch
+    apply_priority: bool = False     # run K1/K2 on a high-priority stream per updater
     track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
     record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
 
@@ -278,6 +279,13 @@ class _Worker:
         with torch.cuda.device(device):
             self.streams = [torch.cuda.Stream(device=device) for _ in range(U)]
             self.avg_stream = torch.cuda.Stream(device=device, priority=-1)
+            # optional: the apply of every updater on its own high-priority
+            # stream, so parameter updates are not queued behind other
+            # streams' convolutions (less staleness); ordered by events
+            self.apply_streams = ([torch.cuda.Stream(device=device, priority=-1) for _ in range(U)]
+                                  if cfg.apply_priority else None)
+            self.graph_done = [torch.cuda.Event() for _ in range(U)]
+            self.apply_done = [torch.cuda.Event() for _ in range(U)]
         self.replicas = [Arena(d, device) for _ in range(U)]
         self.grads = [Arena(d, device) for _ in range(U)]
         self.moms = [Arena(d, device) for _ in range(U)] if cfg.momentum else [None] * U
@@ -494,10 +502,16 @@ class _Engine:
                 rec.snapshot = w.replicas[r].tensor.clone()
             off = 4 * blk.start
             mom = w.moms[r]
+            astream = stream
+            if w.apply_streams is not None:
+                astream = w.apply_streams[r]
+                w.graph_done[r].record(stream)
+                astream.wait_event(w.graph_done[r])
+                sp = astream.cuda_stream
             if self.time_apply:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+                e0.record(astream)
             if tracks:                                                                # K1/K2 + K5
                 N.apply_sgd_tagged(w.store.arena.ptr + off, w.grads[r].ptr + off,
                                    (mom.ptr + off) if mom is not None else None, blk.length,
@@ -508,8 +522,11 @@ class _Engine:
                             (mom.ptr + off) if mom is not None else None, blk.length, float(lr),
                             None, cfg.momentum, cfg.weight_decay, N.MODES[cfg.apply_mode], sp)
             if self.time_apply:
-                e1.record(stream)
+                e1.record(astream)
                 self.apply_events.append((e0, e1, self.apply_bytes_per_elem * blk.length))
+            if astream is not stream:
+                w.apply_done[r].record(astream)
+                stream.wait_event(w.apply_done[r])
             if self.read_loss:
                 # the step's result back to the host (end-to-end measurement)
                 w.loss_pinned[r, slot].copy_(prog.loss, non_blocking=True)
