@@ -340,6 +340,15 @@ class _Worker:
                                                 dtype=obj.features.dtype, pin_memory=True)
                 self.label_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size),
                                                 dtype=torch.long, pin_memory=True)
+                # H2D prefetch: a copy stream per updater fills a device ring,
+                # overlapping the previous step's compute; the step then does
+                # a D2D into the captured graph's static input
+                self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in range(cfg.updaters)]
+                self.batch_dev = torch.zeros((cfg.updaters, depth, cfg.batch_size, *shape),
+                                             dtype=obj.features.dtype, device=self.dev)
+                self.label_dev = torch.zeros((cfg.updaters, depth, cfg.batch_size),
+                                             dtype=torch.long, device=self.dev)
+                self.copied = [[torch.cuda.Event() for _ in range(depth)] for _ in range(cfg.updaters)]
             # the warm-up passes touched the replica/grad arenas and BN stats
             # only; re-snapshot so every replica starts at x0
             for r in range(cfg.updaters):
@@ -467,12 +476,20 @@ class _Engine:
         with torch.cuda.stream(stream):
             if batch is not None:
                 if self.host_batches:
-                    # gather straight into the pinned staging slot, then H2D
+                    # gather straight into the pinned staging slot, H2D on the
+                    # updater's copy stream (overlaps the previous step), then
+                    # a D2D into the graph input on the compute stream
                     t = torch.from_numpy(batch)
                     torch.index_select(cfg.objective.features, 0, t, out=w.batch_pinned[r, slot])
                     torch.index_select(cfg.objective.labels, 0, t, out=w.label_pinned[r, slot])
-                    prog.xb.copy_(w.batch_pinned[r, slot], non_blocking=True)
-                    prog.yb.copy_(w.label_pinned[r, slot], non_blocking=True)
+                    cs = w.copy_streams[r]
+                    with torch.cuda.stream(cs):
+                        w.batch_dev[r, slot].copy_(w.batch_pinned[r, slot], non_blocking=True)
+                        w.label_dev[r, slot].copy_(w.label_pinned[r, slot], non_blocking=True)
+                        w.copied[r][slot].record(cs)
+                    stream.wait_event(w.copied[r][slot])
+                    prog.xb.copy_(w.batch_dev[r, slot])
+                    prog.yb.copy_(w.label_dev[r, slot])
                 else:
                     w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
                     prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)

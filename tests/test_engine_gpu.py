@@ -425,3 +425,15 @@ def test_captured_partial_backprop_matches_full_slices_resnet20():
                                        full[blk.start:blk.stop].cpu().numpy(), rtol=1e-5, atol=1e-6)
     finally:
         torch.backends.cudnn.deterministic = False
+
+
+def test_host_batches_path_matches_oracle():
+    """The end-to-end input path (host gather -> pinned -> H2D on a copy stream
+    -> D2D into the graph input) feeds exactly the reference's batches."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj, X, y, hidden, k = _mlp("deep")
+    g, cfg = _cfg_from_golden("deep_lpp", obj)
+    res = run_experiment(cfg, host_batches=True)
+    tr = _oracle_run(g, X, y, hidden, k)
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=ATOL, rtol=RTOL)
