@@ -22,6 +22,8 @@ Extra keys beyond the base contract:
                 compiled _atomics) on this host, bounded sample, rank 0, N=1
   baselines     the box's own synchronous MB-SGD (same per-GPU B, 1 stream)
                 and LAP-SGD (same engine, no partial backprop)
+  resnet18      config C2 (CIFAR-100-shaped, d = 11.2M): LPP vs MB-SGD images/s
+                and the apply kernel's in-situ HBM roofline
   resnet50      config C3 (ImageNet-shaped, d = 25.6M, B = 32 per stream):
                 images/s and the apply kernel's in-situ HBM roofline
   kernel_sweep  K1/K3 alone at 16M/64M params (HBM roofline evidence)
@@ -134,10 +136,10 @@ def reference_arm(args) -> None:
         "data": "synthetic", "impl": "reference",
         "config": {"workload": "resnet20_cifar10_lpp_sgd_cpu", "global_batch": B * U,
                    "updaters": U, "workers": 1, "batch_per_updater": B},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"],
-                         "kind": "reference" if r["atomics"] == "reference" else "port",
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"], "kind": "port",
                          "sample": f"{r['minibatches']} minibatches x {B} images (LPP-SGD, U={U}, "
-                                   f"torch-CPU ResNet-20 grads, store ops = reference _atomics "
+                                   f"threaded port of engine.py:315-383, torch-CPU ResNet-20 grads, "
+                                   f"store ops = the reference's own compiled _atomics "
                                    f"({r['atomics']}))"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -209,10 +211,13 @@ def ours(args) -> None:
     tr = Trainer(cfg, group=group, time_apply=True)
     tr.run(W * U, evaluate=False)
     barrier()
+    if os.environ.get("LPP_NVTX"):
+        tr.eng.nvtx = "lpp_timed"   # ncu --nvtx --nvtx-include lpp_timed/ profiles this phase only
     with Clocks(dev) as clk:
         barrier()
         res = tr.run(K * U, evaluate=False)
         barrier()
+    tr.eng.nvtx = None
     dev_ms = max_over_ranks(res.device_ms)
     slots = sum(res.counter_finals)  # claim-then-process: K*U + U minibatches
     images = slots * B * ws
@@ -291,6 +296,30 @@ def ours(args) -> None:
             "lap_sgd": {"value": lap, "unit": "images/s", "streams": U,
                         "note": "same engine, full backprop every step (no PASSM+ blocks)"},
             "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
+
+    # ---------------- ResNet-18 / CIFAR-100 shape (config C2) ----------------
+    if not args.no_rn18 and ws == 1:
+        obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
+        out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s"}
+        for algo in ("lpp_sgd", "mb_sgd"):
+            c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=1)
+            t18 = Trainer(c18, time_apply=(algo == "lpp_sgd"))
+            t18.run(3 * U, evaluate=False)
+            torch.cuda.synchronize()
+            r18 = t18.run(args.rn18_steps * U, evaluate=False)
+            n18 = sum(r18.counter_finals) if algo == "lpp_sgd" else args.rn18_steps * U
+            out18[algo] = n18 * B / (r18.device_ms / 1e3)
+            if algo == "lpp_sgd":
+                na, msa, bya = r18.apply_timing
+                a18 = bya / (msa / 1e3) / 1e9
+                out18["apply_roofline"] = {"achieved": a18, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                           "frac": a18 / peaks["hbm_gbs"], "launches": na,
+                                           "avg_us": 1e3 * msa / max(na, 1),
+                                           "bytes_per_launch": bya / max(na, 1)}
+                t18.close()
+            del t18
+        out18["lpp_over_mb"] = out18["lpp_sgd"] / out18["mb_sgd"]
+        line["resnet18"] = out18
 
     # ---------------- ResNet-50 / ImageNet shape (config C3): in-situ HBM apply ----------------
     if not args.no_rn50 and ws == 1:
@@ -378,6 +407,8 @@ def main() -> None:
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-rn50", action="store_true")
+    ap.add_argument("--no-rn18", action="store_true")
+    ap.add_argument("--rn18-steps", type=int, default=15)
     ap.add_argument("--rn50-steps", type=int, default=10)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()

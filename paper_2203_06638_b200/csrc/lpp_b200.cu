@@ -670,23 +670,26 @@ struct ArenaTable {
   int tagged;
 };
 
-template <int MODE>
+// Q and TAGGED are compile-time so each instantiation keeps exactly the
+// 2*Q float4 registers it needs (a runtime Q sized for LPP_MAX_WORKERS spilled
+// occupancy to 1 CTA/SM).
+template <int MODE, int Q, bool TAGGED>
 __global__ void __launch_bounds__(kThreads)
-    k_average(ArenaTable t, int Q, size_t lo, size_t n, size_t head, size_t nvec,
+    k_average(ArenaTable t, size_t lo, size_t n, size_t head, size_t nvec,
               float* __restrict__ mean_out) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const float fq = (float)Q;
   constexpr int U = 2;  // 2 x Q independent 16-byte loads in flight
   for (size_t i0 = tid; i0 < nvec; i0 += stride * U) {
-    float4 v[U][LPP_MAX_WORKERS];
+    float4 v[U][Q];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       size_t i = i0 + (size_t)u * stride;
       if (i < nvec) {
 #pragma unroll
-        for (int q = 0; q < LPP_MAX_WORKERS; ++q)
-          if (q < Q) v[u][q] = ld_cg4(t.p[q] + lo + head + 4 * i);
+        for (int q = 0; q < Q; ++q)
+          v[u][q] = ld_cg4(t.p[q] + lo + head + 4 * i);
       }
     }
 #pragma unroll
@@ -732,7 +735,7 @@ __global__ void __launch_bounds__(kThreads)
         if (mean_out) reinterpret_cast<float4*>(mean_out + head)[i] = mean;
       }
     }
-    if (t.tagged) {
+    if (TAGGED) {
       __threadfence_system();
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(kThreads)
     size_t nscalar = head + (n - tail0);
     for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
       size_t e = k < head ? k : tail0 + (k - head);
-      float vv[LPP_MAX_WORKERS];
+      float vv[Q];
 #pragma unroll
       for (int q = 0; q < LPP_MAX_WORKERS; ++q)
         if (q < Q) vv[q] = ld_cg(t.p[q] + lo + e);
@@ -770,7 +773,7 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
       if (mean_out) mean_out[e] = mean;
-      if (t.tagged) {
+      if (TAGGED) {
         __threadfence_system();
 #pragma unroll
         for (int q = 0; q < LPP_MAX_WORKERS; ++q)
@@ -778,6 +781,40 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
+}
+
+template <int MODE, int Q>
+static void launch_average_q(bool tagged, unsigned grid, cudaStream_t st, const ArenaTable& t,
+                             size_t lo, size_t n, size_t head, size_t nvec, float* mean_out) {
+  if (tagged)
+    k_average<MODE, Q, true><<<grid, kThreads, 0, st>>>(t, lo, n, head, nvec, mean_out);
+  else
+    k_average<MODE, Q, false><<<grid, kThreads, 0, st>>>(t, lo, n, head, nvec, mean_out);
+}
+
+template <int MODE>
+static void launch_average_m(int Q, bool tagged, unsigned grid, cudaStream_t st,
+                             const ArenaTable& t, size_t lo, size_t n, size_t head, size_t nvec,
+                             float* mean_out) {
+  switch (Q) {
+    case 1: launch_average_q<MODE, 1>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 2: launch_average_q<MODE, 2>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 3: launch_average_q<MODE, 3>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 4: launch_average_q<MODE, 4>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 5: launch_average_q<MODE, 5>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 6: launch_average_q<MODE, 6>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    case 7: launch_average_q<MODE, 7>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+    default: launch_average_q<MODE, 8>(tagged, grid, st, t, lo, n, head, nvec, mean_out); break;
+  }
+}
+
+static void launch_average(int mode, int Q, bool tagged, unsigned grid, cudaStream_t st,
+                           const ArenaTable& t, size_t lo, size_t n, size_t head, size_t nvec,
+                           float* mean_out) {
+  if (mode == LPP_MODE_PLAIN)
+    launch_average_m<LPP_MODE_PLAIN>(Q, tagged, grid, st, t, lo, n, head, nvec, mean_out);
+  else
+    launch_average_m<LPP_MODE_RED>(Q, tagged, grid, st, t, lo, n, head, nvec, mean_out);
 }
 
 static int average_impl(float* const* arenas, int32_t* const* tags, const int32_t* stamps, int Q,
@@ -826,12 +863,8 @@ static int average_impl(float* const* arenas, int32_t* const* tags, const int32_
   size_t head = head_elems(arenas[0] + lo, n);
   size_t nvec = (n - head) / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
-  if (mode == LPP_MODE_PLAIN)
-    k_average<LPP_MODE_PLAIN><<<grid, kThreads, 0, (cudaStream_t)stream>>>(t, Q, lo, n, head,
-                                                                          nvec, mean_out);
-  else
-    k_average<LPP_MODE_RED><<<grid, kThreads, 0, (cudaStream_t)stream>>>(t, Q, lo, n, head,
-                                                                        nvec, mean_out);
+  launch_average(mode, Q, t.tagged != 0, grid, (cudaStream_t)stream, t, lo, n, head, nvec,
+                 mean_out);
   LAUNCH_CHECK("average_shard");
   return LPP_OK;
 }

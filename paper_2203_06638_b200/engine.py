@@ -427,6 +427,7 @@ class _Engine:
         self.budget = cfg.budget
         self.read_loss = False
         self.loss_log: list = []
+        self.nvtx: str | None = None   # per-thread NVTX range name for profiling a phase
         mu, wd = cfg.momentum, cfg.weight_decay
         # algorithmic bytes per element of K1/K2: read g, read +
         # write x (the weight-decay read of x is that same read), + read and
@@ -658,6 +659,8 @@ class _Engine:
         s, t = 0, 0
         if w.gate is not None:
             w.gate.register()
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
         try:
             while s < self.budget and not ctrl.stop.read():
                 if w.gate is not None:
@@ -701,6 +704,8 @@ class _Engine:
         except BaseException as exc:  # surfaced after join (engine.py:456-463)
             self.fail(exc)
         finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
             if w.gate is not None:
                 w.gate.leave()
             if w.exited.add(1) + 1 == cfg.updaters:
@@ -766,6 +771,8 @@ class _Engine:
                 worker=q, round=r, u=u_of.pop(r), s_cur=s_cur, k_delta=k_delta,
                 wall_ms=(time.perf_counter() - self.t0) * 1e3, snapshot=snap, mean=mean))
 
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
         try:
             averager_loop(self.ctrl, workers=cfg.workers,
                           read_counter=store.sample_counter.read,
@@ -774,6 +781,9 @@ class _Engine:
                           do_round=do_round, on_round=on_round, stop_after=cfg.round_budget)
         except BaseException as exc:
             self.fail(exc)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
 
     # -- drivers ------------------------------------------------------------------
 

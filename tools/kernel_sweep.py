@@ -59,8 +59,11 @@ def main():
                 continue
             ars = [x, r] + [Arena(d, 0) for _ in range(Q - 2)]
             t = timed(lambda: N.average_shard([a.ptr for a in ars], 0, d, None, N.MODE_RED, st), flush)
-            # single-GPU emulation: all Q arenas local -> HBM bytes = Q reads + Q RMW reds
-            hbm = 3 * 4 * d * Q
+            # single-GPU emulation: all Q arenas in one HBM.  DRAM bytes = one
+            # read + one write-back per arena element (the red.add hits the L2
+            # line its own load just brought in); the NVLink-facing number of a
+            # real Q-GPU group is 2(Q-1)/Q x 4d per GPU and direction.
+            hbm = 2 * 4 * d * Q
             rows.append(dict(kernel=f"average_Q{Q}_local", d=d, us=t * 1e6, gbs=hbm / t / 1e9,
                              frac=hbm / t / 1e9 / peak))
             for a in ars[2:]:

@@ -25,6 +25,15 @@ for d in (272_474, 64_000_000):
         N.snapshot(x.ptr, r.ptr, d, st)
     for a in (x, g, m, r):
         a.close()
+# K1/K2 + K5 (the engine's default for lap/lpp) at the ResNet-18 / ResNet-50 arena sizes
+for d in (11_220_132, 25_557_032):
+    x, g, m, tg = (Arena(d, 0) for _ in range(4))
+    x.tensor.normal_(), g.tensor.normal_()
+    for _ in range(2):
+        flush()
+        N.apply_sgd_tagged(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, tg.ptr, 7, st)
+    for a in (x, g, m, tg):
+        a.close()
 d = 16_000_000
 ars = [Arena(d, 0) for _ in range(4)]
 for _ in range(2):
