@@ -437,3 +437,38 @@ def test_host_batches_path_matches_oracle():
     res = run_experiment(cfg, host_batches=True)
     tr = _oracle_run(g, X, y, hidden, k)
     np.testing.assert_allclose(res.final_values, tr.final_values, atol=ATOL, rtol=RTOL)
+
+
+@pytest.mark.parametrize("kind,workers,updaters,bounds", [("small", 3, 2, (0, 25, 43)),
+                                                       ("deep", 2, 3, (0, 42, 84, 168))])
+def test_serialized_misaligned_blocks_match_oracle(kind, workers, updaters, bounds):
+    """Layer boundaries at elements 25 / 42 / 84 (not 16-byte aligned) exercise
+    the scalar head/tail paths of K1/K3/K4/K5 inside the engine; odd Q
+    exercises uneven owner shards."""
+    from oracle import schedule as osched
+    from oracle.mlp import MlpOracle
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    obj, X, y, hidden, k = _mlp(kind)
+    sched = LrSchedule(kind="cosine", alpha0=0.05, total=60, warmup=6, batch_local=8, workers=workers,
+                       batch_base=8)
+    cfg = RunConfig(algo="lpp_sgd", objective=obj, partition=make_partition(obj.dim, bounds),
+                    lr=sched, sync=SyncScheme(total=60, period=3), budget=60, warm_start_budget=6,
+                    workers=workers, updaters=updaters, batch_size=8, seed=4, schedule="serialized",
+                    record_mode="full", record_tensors=False, evaluate=False)
+    o = MlpOracle(X, y, hidden, k)
+
+    class A:
+        dim, n_samples = o.dim, o.n_samples
+        init_params = staticmethod(o.init_params)
+        grad_block = staticmethod(o.grad_block)
+
+    res = run_experiment(cfg)
+    tr = osched.run_serialized(A, algo="lpp_sgd", workers=workers, updaters=updaters, boundaries=bounds,
+                               lr=osched.Lr(kind="cosine", alpha0=0.05, total=60, warmup=6,
+                                            peak=sched.peak),
+                               switch_point=30, period=3, budget=60, warm_start=6, batch_size=8, seed=4)
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=ATOL, rtol=RTOL)
+    assert [tuple(r) for r in res.round_trace] == [(a, b, *c) for a, b, c in tr.rounds]
