@@ -106,6 +106,16 @@ int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float lr,
                   const float* lr_dev, float mu, float wd, int mode,
                   void* stream);
 
+/* K1+K3 fused: apply the block [lo, hi) of this step (as lpp_apply_sgd on
+ * x + lo, g + lo, m + lo, with tags[e] = stamp when tags != NULL) and write
+ * replica[e] for every e in [0, n): old + delta inside the block (returning
+ * element atomic: a value the arena really held), an untorn copy of x
+ * outside it.  x, g, m, replica, tags are arena BASES (16-byte aligned). */
+int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
+                       int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
+                       const float* lr_dev, float mu, float wd, int32_t stamp,
+                       void* stream);
+
 /* Reference-shaped accumulate: dst[start + e] += scale * delta[e],
  * e in [0, n), with dst of length dst_len (range-checked like
  * _atomics.c:328-333).  fp32 mirror of accum_cas_f64. */

@@ -71,6 +71,11 @@ _SIGS = {
         [_vp, _vp, _vp, _size, _c.c_float, _vp, _c.c_float, _c.c_float, _c.c_int, _vp],
     ),
     "lpp_accum": (_c.c_int, [_vp, _size, _size, _vp, _size, _c.c_float, _c.c_int, _vp]),
+    "lpp_apply_snapshot": (
+        _c.c_int,
+        [_vp, _vp, _vp, _vp, _vp, _size, _size, _size, _c.c_float, _vp, _c.c_float, _c.c_float,
+         _c.c_int32, _vp],
+    ),
     "lpp_snapshot": (_c.c_int, [_vp, _vp, _size, _vp]),
     "lpp_average_shard": (
         _c.c_int,
@@ -198,6 +203,13 @@ def apply_sgd(x_ptr: int, g_ptr: int, m_ptr: int | None, n: int, lr: float,
         lib.lpp_apply_sgd(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, stream),
         "apply_sgd",
     )
+
+
+def apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr, lr_dev_ptr, mu, wd,
+                   stamp, stream) -> None:
+    _count()
+    check(lib.lpp_apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr,
+                                 lr_dev_ptr, mu, wd, int(stamp), stream), "apply_snapshot")
 
 
 def accum(dst_ptr: int, dst_len: int, start: int, delta_ptr: int, n: int, scale: float,

@@ -436,6 +436,130 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
   return LPP_OK;
 }
 
+// ---------------------------------------------------------------------------
+// K1+K3 fused: apply this step's block gradient AND refresh the stream's
+// replica for its next step in one pass over the arena.  Inside [lo, hi)
+// the element update is a returning vector atomic (atom.add.v4.f32, SASS
+// ATOMG.E.ADD.F32x4): the replica receives old + delta — the value the
+// element held right after this update, i.e. a value that was really in the
+// arena; outside the block the replica is a plain untorn copy.  It replaces
+// the next step's K3 launch (the step's snapshot is taken when the previous
+// step's apply lands, which on the updater's stream is when K3 would have
+// run anyway) and saves 4 B/elem of block traffic.
+
+__device__ __forceinline__ float4 atom_add_v4(float* p, float4 v) {
+  float4 r;
+  asm volatile("atom.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4], {%5,%6,%7,%8};"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float atom_add_f32(float* p, float v) {
+  float r;
+  asm volatile("atom.relaxed.sys.global.add.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "f"(v) : "memory");
+  return r;
+}
+
+template <bool WD, bool MOM>
+__device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, float* rep, int* tags,
+                                           size_t e, size_t lo, size_t hi, float lr, float mu,
+                                           float wd, int stamp) {
+  if (e >= lo && e < hi) {
+    float xv = WD ? ld_cg(x + e) : 0.f;
+    float mv = MOM ? m[e] : 0.f;
+    float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
+    if (MOM) m[e] = mv;
+    float old = atom_add_f32(x + e, d);
+    rep[e] = __fadd_rn(old, d);
+    if (tags) {
+      __threadfence();
+      st_tag(tags + e, stamp);
+    }
+  } else {
+    rep[e] = ld_cg(x + e);
+  }
+}
+
+template <bool WD, bool MOM>
+__global__ void __launch_bounds__(kThreads)
+    k_apply_snapshot(float* x, const float* __restrict__ g, float* m, float* __restrict__ rep,
+                     int* tags, size_t n, size_t lo, size_t hi, float lr,
+                     const float* __restrict__ lr_dev, float mu, float wd, int stamp) {
+  if (lr_dev) lr = *lr_dev;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nvec = n / 4;
+  // vectors fully inside [lo, hi): the apply path; fully outside: the copy
+  // path; straddling (layer-aligned blocks start anywhere): per element
+  for (size_t i = tid; i < nvec; i += stride) {
+    size_t e0 = 4 * i;
+    if (e0 >= lo && e0 + 4 <= hi) {
+      float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+      float4 xv = make_float4(0.f, 0.f, 0.f, 0.f), mv = xv;
+      if (WD) xv = ld_cg4(x + e0);
+      if (MOM) mv = reinterpret_cast<const float4*>(m)[i];
+      float4 d;
+      d.x = sgd_delta<WD, MOM>(gv.x, xv.x, mv.x, lr, mu, wd);
+      d.y = sgd_delta<WD, MOM>(gv.y, xv.y, mv.y, lr, mu, wd);
+      d.z = sgd_delta<WD, MOM>(gv.z, xv.z, mv.z, lr, mu, wd);
+      d.w = sgd_delta<WD, MOM>(gv.w, xv.w, mv.w, lr, mu, wd);
+      if (MOM) reinterpret_cast<float4*>(m)[i] = mv;
+      float4 old = atom_add_v4(x + e0, d);
+      float4 nv;
+      nv.x = __fadd_rn(old.x, d.x);
+      nv.y = __fadd_rn(old.y, d.y);
+      nv.z = __fadd_rn(old.z, d.z);
+      nv.w = __fadd_rn(old.w, d.w);
+      reinterpret_cast<float4*>(rep)[i] = nv;
+      if (tags) {
+        __threadfence();
+        st_tag4(tags + e0, stamp);
+      }
+    } else if (e0 + 4 <= lo || e0 >= hi) {
+      reinterpret_cast<float4*>(rep)[i] = ld_cg4(x + e0);
+    } else {
+      for (size_t e = e0; e < e0 + 4; ++e)
+        fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x)
+      fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
+}
+
+extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
+                                  int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
+                                  const float* lr_dev, float mu, float wd, int32_t stamp,
+                                  void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!x || !g || !replica) return set_err(LPP_E_VALUE, "apply_snapshot: null buffer");
+  if (lo > hi || hi > n) return set_err(LPP_E_INDEX, "apply_snapshot: block outside [0, n)");
+  if (mu != 0.f && !m) return set_err(LPP_E_VALUE, "apply_snapshot: momentum needs a buffer");
+  uintptr_t a = (uintptr_t)x | (uintptr_t)g | (uintptr_t)replica | (m ? (uintptr_t)m : 0) |
+                (tags ? (uintptr_t)tags : 0);
+  if (a & 15u)
+    return set_err(LPP_E_VALUE, "apply_snapshot: arena bases must be 16-byte aligned");
+  size_t nvec = n / 4;
+  unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
+  cudaStream_t st = (cudaStream_t)stream;
+  bool WD = wd != 0.f, MOM = mu != 0.f;
+  if (WD && MOM)
+    k_apply_snapshot<true, true><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
+                                                           lr_dev, mu, wd, stamp);
+  else if (WD)
+    k_apply_snapshot<true, false><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
+                                                            lr_dev, mu, wd, stamp);
+  else if (MOM)
+    k_apply_snapshot<false, true><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
+                                                            lr_dev, mu, wd, stamp);
+  else
+    k_apply_snapshot<false, false><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi,
+                                                             lr, lr_dev, mu, wd, stamp);
+  LAUNCH_CHECK("apply_snapshot");
+  return LPP_OK;
+}
+
 // reference-shaped accumulate: dst[start+e] += scale*delta[e]
 __global__ void __launch_bounds__(kThreads)
     k_accum(float* d, const float* __restrict__ s, size_t n, size_t head, size_t nvec,

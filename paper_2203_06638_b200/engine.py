@@ -87,6 +87,7 @@ class RunConfig:
     evaluate: bool = True            # compute the initial/final MetricsRow losses
     averaging: str = "p2p"           # "p2p": owner-computes over peer arenas; "nvls": in-switch
     apply_priority: bool = False     # run K1/K2 on a high-priority stream per updater
+    fuse_snapshot: bool = True       # async: fuse each apply with the next step's snapshot
     track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
     record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
 
@@ -549,6 +550,76 @@ class _Engine:
                 # the step's result back to the host (end-to-end measurement)
                 w.loss_pinned[r, slot].copy_(prog.loss, non_blocking=True)
 
+    def fused(self) -> bool:
+        """Whether async steps use the fused apply+next-snapshot kernel."""
+        cfg = self.cfg
+        return (cfg.fuse_snapshot and cfg.schedule == "async" and not cfg.quiescent
+                and cfg.record_mode != "full" and cfg.apply_mode != "plain"
+                and not cfg.apply_priority)
+
+    def gather_tags(self, w: _Worker, r: int, slot: int, tag_idx) -> None:
+        """K5: sampled tags of the NEXT snapshot into slot, then D2H (on the
+        updater stream; must precede the values it describes)."""
+        k = w.tag_pick
+        w.tag_idx_pinned[r, slot, :k].copy_(torch.from_numpy(tag_idx))
+        w.tag_idx_dev[r, :k].copy_(w.tag_idx_pinned[r, slot, :k], non_blocking=True)
+        N.gather_tags(w.tag_arena.ptr, w.tag_idx_dev[r].data_ptr(), k,
+                      w.tag_out_dev[r, slot].data_ptr(), w.streams[r].cuda_stream)
+        w.tag_pinned[r, slot].copy_(w.tag_out_dev[r, slot], non_blocking=True)
+
+    def step_fused(self, w: _Worker, r: int, block_id: int, lr: float, batch, slot: int,
+                   next_slot: int, u: int, first: bool, tag_idx, next_tag_idx) -> None:
+        """One async step with K1+K3 fused: [first: gather + K3] -> graph ->
+        gather(next) -> apply(this) fused with snapshot(next)."""
+        cfg = self.cfg
+        stream = w.streams[r]
+        prog = w.programs[r]
+        blk = cfg.partition.block(block_id)
+        sp = stream.cuda_stream
+        tracks = w.tags is not None
+        with torch.cuda.stream(stream):
+            if batch is not None:
+                if self.host_batches:
+                    t = torch.from_numpy(batch)
+                    torch.index_select(cfg.objective.features, 0, t, out=w.batch_pinned[r, slot])
+                    torch.index_select(cfg.objective.labels, 0, t, out=w.label_pinned[r, slot])
+                    cs = w.copy_streams[r]
+                    with torch.cuda.stream(cs):
+                        w.batch_dev[r, slot].copy_(w.batch_pinned[r, slot], non_blocking=True)
+                        w.label_dev[r, slot].copy_(w.label_pinned[r, slot], non_blocking=True)
+                        w.copied[r][slot].record(cs)
+                    stream.wait_event(w.copied[r][slot])
+                    prog.xb.copy_(w.batch_dev[r, slot])
+                    prog.yb.copy_(w.label_dev[r, slot])
+                else:
+                    w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
+                    prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)
+            if first:
+                if tracks:
+                    self.gather_tags(w, r, slot, tag_idx)
+                N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)          # K3
+            prog.run(block_id)                                                           # fwd+bwd
+            if tracks:
+                self.gather_tags(w, r, next_slot, next_tag_idx)                          # K5 (next)
+            mom = w.moms[r]
+            if self.time_apply:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            N.apply_snapshot(w.store.arena.ptr, w.grads[r].ptr,                           # K1+K3
+                             mom.ptr if mom is not None else None, w.replicas[r].ptr,
+                             w.tag_arena.ptr if tracks else None, self.dim, blk.start, blk.stop,
+                             float(lr), None, cfg.momentum, cfg.weight_decay, u, sp)
+            if self.time_apply:
+                e1.record(stream)
+                # block: read g, RMW x, (+m), (+tag); whole arena: read x outside
+                # the block, write the replica
+                nbytes = self.apply_bytes_per_elem * blk.length + 4 * (self.dim - blk.length) \
+                    + 4 * self.dim
+                self.apply_events.append((e0, e1, nbytes))
+            if self.read_loss:
+                w.loss_pinned[r, slot].copy_(prog.loss, non_blocking=True)
+
     def average(self, owner: int, stream: torch.cuda.Stream, final: bool, stamps=None) -> None:
         lo, hi = self.shards[owner]
         w = self.workers[owner]
@@ -656,6 +727,14 @@ class _Engine:
         pending = [None] * cfg.in_flight
         ctrl = self.ctrl
         sampled_tags = w.tags is not None and cfg.record_mode != "full"
+        fused = self.fused()
+        next_tag_idx = None
+
+        def draw_tags():
+            if not sampled_tags:
+                return None
+            return np.sort(gen.choice(self.dim, size=w.tag_pick, replace=False))
+
         s, t = 0, 0
         if w.gate is not None:
             w.gate.register()
@@ -676,9 +755,12 @@ class _Engine:
                         self.loss_log.append(float(w.loss_pinned[r, old_slot]))
                     self.classify(w, r, old_slot, pending[k])
                 # reference rng order: sampled tag indices first, then the batch
-                # (engine.py:343-351)
-                tag_idx = (np.sort(gen.choice(self.dim, size=w.tag_pick, replace=False))
-                           if sampled_tags else None)
+                # (engine.py:343-351); the fused path draws the NEXT step's tag
+                # indices right after this batch, which keeps that order
+                if fused:
+                    tag_idx = next_tag_idx if t else draw_tags()
+                else:
+                    tag_idx = draw_tags()
                 batch = None
                 if sampler is not None:
                     batch = sampler.next_batch(cfg.batch_size)
@@ -687,8 +769,13 @@ class _Engine:
                 k_claim = w.last_avg_stamp.read()
                 u = w.store.claim_update_order()
                 rec = self.record_update(q, r, s, u, k_claim, choice, lr, tag_idx)
-                self.step(w, r, s, choice.block_id, lr, batch, t % depth, u=u, tag_idx=tag_idx,
-                          rec=rec)
+                if fused:
+                    next_tag_idx = draw_tags()
+                    self.step_fused(w, r, choice.block_id, lr, batch, t % depth, (t + 1) % depth,
+                                    u, t == 0, tag_idx, next_tag_idx)
+                else:
+                    self.step(w, r, s, choice.block_id, lr, batch, t % depth, u=u, tag_idx=tag_idx,
+                              rec=rec)
                 events[k].record(w.streams[r])
                 used[k] = True
                 pending[k] = rec

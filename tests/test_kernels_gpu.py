@@ -357,3 +357,61 @@ def test_tags_never_newer_than_values_under_concurrency(N):
     torch.cuda.synchronize()
     for v, t in outs:
         assert bool((v >= t.float()).all())
+
+
+@pytest.mark.parametrize("mu,wd", [(0.0, 0.0), (0.9, 5e-4)])
+@pytest.mark.parametrize("n,lo,hi", [(1, 0, 1), (7, 2, 5), (4099, 0, 4099), (4099, 13, 2050),
+                                     (100_003, 4, 99_999), (100_003, 1, 3)])
+def test_apply_snapshot_fused_bitexact(N, orc, mu, wd, n, lo, hi):
+    """K1+K3 fused: the arena update equals the oracle apply on [lo, hi); the
+    replica equals the updated arena everywhere (single writer); tags stamped
+    on the block only."""
+    from paper_2203_06638_b200.arena import Arena
+
+    gen = np.random.default_rng(n + lo)
+    x = gen.normal(size=n).astype(np.float32)
+    g = (1e-2 * gen.normal(size=n)).astype(np.float32)
+    m = gen.normal(size=n).astype(np.float32)
+    ax, ag, am, ar, at = (Arena(n, 0) for _ in range(5))
+    ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g)), am.tensor.copy_(_cuda(m))
+    ar.tensor.fill_(-5.0)
+    N.apply_snapshot(ax.ptr, ag.ptr, am.ptr if mu else None, ar.ptr, at.ptr, n, lo, hi, 0.05, None,
+                     mu, wd, 9, 0)
+    torch.cuda.synchronize()
+    xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
+    orc.apply_sgd(xv, g[lo:hi].copy(), mv if mu else None, 0.05, mu, wd)
+    want = x.copy()
+    want[lo:hi] = xv
+    got = ax.tensor.cpu().numpy()
+    assert np.array_equal(got, want)
+    assert np.array_equal(ar.tensor.cpu().numpy(), want)
+    if mu:
+        wm = m.copy()
+        wm[lo:hi] = mv
+        assert np.array_equal(am.tensor.cpu().numpy(), wm)
+    t = at.tensor.view(torch.int32).cpu().numpy()
+    assert (t[lo:hi] == 9).all() and (t[:lo] == 0).all() and (t[hi:] == 0).all()
+
+
+def test_apply_snapshot_no_lost_updates_and_member_values(N):
+    """Concurrent fused steps on 4 streams: every +1 lands (no lost update) and
+    every replica element is an integer the arena actually held."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, K, ops = 8192 + 5, 4, 40
+    x = Arena(n, 0)
+    g = torch.full((n,), -1.0, device="cuda")
+    reps = [Arena(n, 0) for _ in range(K)]
+    streams = [torch.cuda.Stream() for _ in range(K)]
+    torch.cuda.synchronize()
+    for _ in range(ops):
+        for k, s in enumerate(streams):
+            N.apply_snapshot(x.ptr, g.data_ptr(), None, reps[k].ptr, None, n, 3, n - 2, 1.0, None,
+                             0.0, 0.0, 0, s.cuda_stream)
+    torch.cuda.synchronize()
+    inner = x.tensor[3:n - 2]
+    assert bool((inner == float(K * ops)).all())
+    assert bool((x.tensor[:3] == 0).all()) and bool((x.tensor[n - 2:] == 0).all())
+    for r in reps:
+        v = r.tensor[3:n - 2]
+        assert bool((v == v.round()).all()) and float(v.min()) >= 1 and float(v.max()) <= K * ops
