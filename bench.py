@@ -209,6 +209,7 @@ def ours(args) -> None:
     obj = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data="device")
     cfg = build_cfg(obj, (K + W) * U, workers=ws)
     tr = Trainer(cfg, group=group, time_apply=True)
+    fused = tr.eng.fused()
     tr.run(W * U, evaluate=False)
     barrier()
     if os.environ.get("LPP_NVTX"):
@@ -245,7 +246,9 @@ def ours(args) -> None:
         "gpu_launches": launches,
         "gpu_launches_note": "lpp_b200 kernels launched in the timed region on this rank "
                              "(K3 snapshot + K5 tag gather + K1/K2 apply per minibatch, + K4 per round)",
-        "roofline": {"bound": "hbm", "kernel": "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("lpp_apply_snapshot (K1+K3 fused, atom.add.v4.f32)" if fused else
+                                "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)"),
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],
                      "traffic": None, "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
