@@ -166,7 +166,6 @@ def build_cfg(obj, steps_slots: int, algo: str = "lpp_sgd", workers: int = 1, sa
 
 
 def ours(args) -> None:
-    import numpy as np
     import torch
     import torch.distributed as dist
 

@@ -35,7 +35,6 @@ parity tests) or spread over the visible devices.
 
 from __future__ import annotations
 
-import math
 import threading
 import time
 from dataclasses import dataclass, field

@@ -22,7 +22,6 @@ into the gradient arena, so one apply launch covers any block range.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import numpy as np

@@ -16,8 +16,6 @@ import socket
 import threading
 import time
 
-import numpy as np
-import pytest
 import torch.multiprocessing as mp
 
 
