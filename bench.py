@@ -138,9 +138,9 @@ def reference_arm(args) -> None:
                    "updaters": U, "workers": 1, "batch_per_updater": B},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"], "kind": "port",
                          "sample": f"{r['minibatches']} minibatches x {B} images (LPP-SGD, U={U}, "
-                                   f"threaded port of engine.py:315-383, torch-CPU ResNet-20 grads, "
-                                   f"store ops = the reference's own compiled _atomics "
-                                   f"({r['atomics']}))"},
+                                   f"threaded port of engine.py:289-523 incl. the averager and "
+                                   f"write tags, torch-CPU ResNet-20 grads, store ops = the "
+                                   f"reference's own compiled _atomics ({r['atomics']}))"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -407,9 +407,10 @@ def ours(args) -> None:
         r = run_lpp_cpu(slots=4 * U, updaters=U, batch_size=B)
         line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
                                 "cores": r["cores"], "kind": "port",
-                                "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U}, "
-                                          f"torch-CPU ResNet-20 grads, store ops via reference "
-                                          f"_atomics ({r['atomics']})"}
+                                "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
+                                          f"(port of engine.py:289-523 incl. averager + tags), "
+                                          f"torch-CPU ResNet-20 grads, store ops via the "
+                                          f"reference's compiled _atomics ({r['atomics']})"}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.out:
