@@ -27,7 +27,7 @@ class StepProgram:
     def __init__(self, obj, device: torch.device, replica: torch.Tensor, grads: torch.Tensor,
                  blocks: dict[int, Block], batch_size: int, stream: torch.cuda.Stream,
                  input_mode: str = "index", use_graphs: bool = True, warmup: int = 2,
-                 seed: int = 0):
+                 seed: int = 0, nbuf: int = 1):
         if input_mode not in ("index", "batch", "random"):
             raise ValueError(f"unknown input mode {input_mode!r}")
         self.obj = obj
@@ -41,10 +41,19 @@ class StepProgram:
         B = int(batch_size)
         self.batch_size = B
         self.idx = torch.zeros(B, dtype=torch.long, device=device)
+        # "batch" mode: nbuf static input buffers, one captured graph variant per
+        # buffer, so the next step's H2D can land in the buffer the running
+        # step is not reading (no device-side staging copy)
+        self.nbuf = nbuf if input_mode == "batch" else 1
         if input_mode == "batch":
-            self.xb = torch.zeros((B, *self.feats.shape[1:]), dtype=self.feats.dtype, device=device)
-            self.yb = torch.zeros(B, dtype=torch.long, device=device)
-        self.loss = torch.zeros((), dtype=torch.float32, device=device)
+            self.xbs = [torch.zeros((B, *self.feats.shape[1:]), dtype=self.feats.dtype, device=device)
+                        for _ in range(self.nbuf)]
+            self.ybs = [torch.zeros(B, dtype=torch.long, device=device) for _ in range(self.nbuf)]
+            self.xb, self.yb = self.xbs[0], self.ybs[0]
+        # the step's loss, one slot per input buffer so a D2H of step t's loss
+        # can overlap step t+1 (which writes the other slot)
+        self.losses = [torch.zeros((), dtype=torch.float32, device=device) for _ in range(self.nbuf)]
+        self.loss = self.losses[0]
         self.gen = None
         if input_mode == "random":
             self.gen = torch.Generator(device=device)
@@ -64,34 +73,39 @@ class StepProgram:
             if use_graphs:
                 pool = None
                 for bid in self.blocks:
-                    g = torch.cuda.CUDAGraph()
-                    if self.gen is not None:
-                        g.register_generator_state(self.gen)
-                    with torch.cuda.graph(g, pool=pool, stream=stream):
-                        self._body(bid)
-                    pool = g.pool()
-                    self.graphs[bid] = g
+                    for buf in range(self.nbuf):
+                        g = torch.cuda.CUDAGraph()
+                        if self.gen is not None:
+                            g.register_generator_state(self.gen)
+                        with torch.cuda.graph(g, pool=pool, stream=stream):
+                            self._body(bid, buf)
+                        pool = g.pool()
+                        self.graphs[(bid, buf)] = g
                 stream.synchronize()
 
-    def _body(self, bid: int) -> None:
+    def _body(self, bid: int, buf: int = 0) -> None:
         blk = self.blocks[bid]
         if self.input_mode == "random":
             torch.randint(0, self.feats.shape[0], (self.batch_size,), generator=self.gen,
                           device=self.device, out=self.idx)
         if self.input_mode == "batch":
-            xb, yb = self.xb, self.yb
+            xb, yb = self.xbs[buf], self.ybs[buf]
         else:
             xb = self.feats.index_select(0, self.idx)
             yb = self.labels.index_select(0, self.idx)
         self.grads[blk.start:blk.stop].zero_()
         loss = self.obj.loss_on(self.bound, xb, yb)
         loss.backward(inputs=self.leaves[bid])
-        self.loss.copy_(loss.detach())
+        self.losses[buf].copy_(loss.detach())
 
-    def run(self, bid: int) -> None:
-        """Enqueue block ``bid``'s fwd+bwd on the program's stream."""
+    def loss_of(self, buf: int) -> torch.Tensor:
+        return self.losses[buf % self.nbuf]
+
+    def run(self, bid: int, buf: int = 0) -> None:
+        """Enqueue block ``bid``'s fwd+bwd (reading input buffer ``buf``)."""
+        buf %= self.nbuf
         if self.use_graphs:
-            self.graphs[bid].replay()
+            self.graphs[(bid, buf)].replay()
         else:
             with torch.cuda.stream(self.stream):
-                self._body(bid)
+                self._body(bid, buf)
