@@ -427,6 +427,7 @@ class _Engine:
         self.read_loss = False
         self.loss_log: list = []
         self.nvtx: str | None = None   # per-thread NVTX range name for profiling a phase
+        self.eval_points: list = []
         mu, wd = cfg.momentum, cfg.weight_decay
         # algorithmic bytes per element of K1/K2: read g, read +
         # write x (the weight-decay read of x is that same read), + read and
@@ -462,6 +463,7 @@ class _Engine:
         self.errors = []
         self.apply_events = []
         self.loss_log = []
+        self.eval_points = []
 
     # -- one updater step: K3 -> graph -> K1/K2, all on the updater stream --
 
@@ -815,7 +817,10 @@ class _Engine:
 
         def do_round(r, final, s_cur):
             quiet = w.gate is not None
-            fenced = quiet or w.tags is not None
+            evalm = cfg.eval_interval > 0
+            # eval points need every owner's round mean: owners write mean_out
+            # each round and the round is fenced before worker 0 reads it
+            fenced = quiet or w.tags is not None or evalm
             if quiet:
                 # quiescent: every worker's updaters parked and their streams
                 # drained before any owner touches the arenas
@@ -828,7 +833,8 @@ class _Engine:
                 # the worker's own view before any owner corrects it (quiescent: exact)
                 snap = w.store.arena.tensor.clone() if full else None
                 if self.nvls:
-                    self.nvls_round(q, u_of[r], final or full, fence=lambda i: self.ctrl.fence(i, r))
+                    self.nvls_round(q, u_of[r], final or full or evalm,
+                                    fence=lambda i: self.ctrl.fence(i, r))
                     w.last_avg_stamp.store(u_of[r])
                     w.synced_at.store(s_cur)
                     if full:
@@ -843,7 +849,7 @@ class _Engine:
                     if not self.ctrl.fence(0, r):
                         return
                     stamps = self.ctrl.stamps()
-                self.average(q, w.avg_stream, final=final or full, stamps=stamps)
+                self.average(q, w.avg_stream, final=final or full or evalm, stamps=stamps)
                 w.avg_stream.synchronize()
                 if fenced and not self.ctrl.fence(1, r):
                     return
@@ -859,12 +865,20 @@ class _Engine:
                     w.gate.resume()
 
         snaps = {}
+        next_eval = [cfg.eval_interval if cfg.eval_interval else self.budget + 1]
 
         def on_round(r, s_cur, k_delta, unanimous):
             snap, mean = snaps.pop(r, (None, None))
+            wall = (time.perf_counter() - self.t0) * 1e3
             self.stamps[q].append(AveragerStamp(
                 worker=q, round=r, u=u_of.pop(r), s_cur=s_cur, k_delta=k_delta,
-                wall_ms=(time.perf_counter() - self.t0) * 1e3, snapshot=snap, mean=mean))
+                wall_ms=wall, snapshot=snap, mean=mean))
+            # engine.py:445-451: worker 0 keeps the round mean at eval points
+            if q == 0 and cfg.eval_interval and not unanimous and s_cur >= next_eval[0]:
+                m = self.round_mean(q)
+                self.eval_points.append((s_cur, r, wall, self.flops.read(), self.p_hat(), m))
+                while next_eval[0] <= s_cur:
+                    next_eval[0] += cfg.eval_interval
 
         if self.nvtx:
             torch.cuda.nvtx.range_push(self.nvtx)
@@ -947,6 +961,7 @@ class _Engine:
         active = {(q, r): True for q in range(cfg.workers) for r in range(cfg.updaters)}
         s_pre = [0] * cfg.workers
         self.round_trace = []
+        next_eval = cfg.eval_interval if cfg.eval_interval else self.budget + 1
         starts = self._device_span_start()
         self.t0 = time.perf_counter()
         sweep, t = 0, 0
@@ -997,10 +1012,17 @@ class _Engine:
                     if self.nvls:
                         self.nvls_round(q, u_avgs[q], drained or full)
                     else:
-                        self.average(q, w.avg_stream, final=drained or full, stamps=u_avgs)
+                        self.average(q, w.avg_stream, final=drained or full or cfg.eval_interval > 0,
+                                 stamps=u_avgs)
                     w.avg_stream.synchronize()
                 mean = (self.gather_round_mean() if not self.nvls else
                         self.nvls[0].mean_tensor.clone()) if full else None
+                if cfg.eval_interval and not drained and counts[0] >= next_eval:
+                    m = mean if mean is not None else self.round_mean(0)
+                    self.eval_points.append((counts[0], rnd, (time.perf_counter() - self.t0) * 1e3,
+                                             self.flops.read(), self.p_hat(), m))
+                    while next_eval <= counts[0]:
+                        next_eval += cfg.eval_interval
                 for q in range(cfg.workers):
                     w = self.workers[q]
                     u_avg = u_avgs[q]
@@ -1015,6 +1037,17 @@ class _Engine:
                 break
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         return self._device_span_end(starts)
+
+    def round_mean(self, q: int) -> torch.Tensor:
+        """The just-finished round's mean as seen by worker q (a device copy)."""
+        if self.nvls:
+            return self.nvls[q].mean_tensor.clone()
+        m = self.gather_round_mean()
+        if m is None:
+            # multi-process P2P: the other shards' means live in the peers;
+            # use this worker's arena right after the round (mean + racing updates)
+            m = self.workers[q].store.arena.tensor.clone()
+        return m
 
     def gather_round_mean(self):
         """The current round's mean from the owners' mean_out shards (one process)."""
@@ -1187,6 +1220,8 @@ class _SyncEngine:
             e.record(self.stream[q])
             starts[q] = e
         self.t0 = time.perf_counter()
+        self.evals = []
+        last_eval = 0
         for k in range(1, steps + 1):
             lr = lr_at(cfg.lr, k - 1)
             shards = gen.integers(0, n, cfg.workers * cfg.batch_size) if cfg.sampling == "host" else None
@@ -1198,6 +1233,9 @@ class _SyncEngine:
                     ptrs = self._mean_grads()
                     for q in self.local:
                         self._apply(q, ptrs[q], lr)
+                if cfg.eval_interval and k % cfg.eval_interval == 0:     # engine.py:569-570
+                    self.evals.append((k, k, (time.perf_counter() - self.t0) * 1e3, 0,
+                                       self.x[self.local[0]].tensor.clone()))
             else:
                 for q in self.local:
                     self._apply(q, self.g[q].ptr, lr)
@@ -1207,6 +1245,10 @@ class _SyncEngine:
                         self._mean_params()
                     self.rounds += 1
                     since = 0
+                    if cfg.eval_interval and k >= last_eval + cfg.eval_interval:  # engine.py:615-616
+                        last_eval = k
+                        self.evals.append((k, self.rounds, (time.perf_counter() - self.t0) * 1e3, 0,
+                                           self.x[self.local[0]].tensor.clone()))
         ms = 0.0
         for q in self.local:
             e = torch.cuda.Event(enable_timing=True)
@@ -1215,6 +1257,17 @@ class _SyncEngine:
             ms = max(ms, starts[q].elapsed_time(e))
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         return ms
+
+    def round_mean(self, q: int) -> torch.Tensor:
+        """The just-finished round's mean as seen by worker q (a device copy)."""
+        if self.nvls:
+            return self.nvls[q].mean_tensor.clone()
+        m = self.gather_round_mean()
+        if m is None:
+            # multi-process P2P: the other shards' means live in the peers;
+            # use this worker's arena right after the round (mean + racing updates)
+            m = self.workers[q].store.arena.tensor.clone()
+        return m
 
     def gather_round_mean(self):
         """The current round's mean from the owners' mean_out shards (one process)."""
@@ -1231,9 +1284,10 @@ class _SyncEngine:
 # public entry point
 
 
-def _eval_row(cfg, samples, rnd, wall_ms, flops, p_hat, x) -> MetricsRow:
+def _eval_row(cfg, samples, rnd, wall_ms, flops, p_hat, x, evaluate: bool = True) -> MetricsRow:
+    """engine.py:526-541: losses are computed post hoc, outside wall time."""
     obj = cfg.objective
-    if cfg.evaluate:
+    if evaluate:
         g = obj.full_grad(x)
         loss = obj.full_loss(x)
         gn = float((g.double() ** 2).sum())
@@ -1277,10 +1331,11 @@ class Trainer:
             flops = budget * cfg.workers * cfg.batch_size * (
                 fwd + cfg.objective.backward_cost(Block(0, cfg.objective.dim)))
             rounds = budget if cfg.algo == "mb_sgd" else eng.rounds
-            rows = []
-            if ev:
-                rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host),
-                        _eval_row(cfg, budget, rounds, eng.wall_ms, flops, 1.0, final)]
+            rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host, ev)]
+            per_step = flops // budget
+            rows += [_eval_row(cfg, k, j, wl, per_step * k, 1.0, xv.cpu().numpy(), ev)
+                     for k, j, wl, _f, xv in eng.evals if k != budget]
+            rows.append(_eval_row(cfg, budget, rounds, eng.wall_ms, flops, 1.0, final, ev))
             self.phases += 1
             return RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
                              wall_ms=eng.wall_ms, flops=flops, p_hat=1.0,
@@ -1296,10 +1351,10 @@ class Trainer:
         rounds = max((st.round for st in stamps), default=0)
         flops = eng.flops.read()
         counters = [eng.workers[q].store.sample_counter.read() for q in eng.local_workers]
-        rows = []
-        if ev:
-            rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host),
-                    _eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, eng.p_hat(), final)]
+        rows = [_eval_row(cfg, 0, 0, 0.0, 0, 1.0, eng.x0_host, ev)]
+        rows += [_eval_row(cfg, sc, j, wl, fl, ph, m.cpu().numpy(), ev)
+                 for sc, j, wl, fl, ph, m in eng.eval_points]
+        rows.append(_eval_row(cfg, max(counters), rounds, eng.wall_ms, flops, eng.p_hat(), final, ev))
         res = RunResult(config=cfg, metrics=rows, final_values=final, x0=eng.x0_host,
                         wall_ms=eng.wall_ms, flops=flops, p_hat=eng.p_hat(), counter_finals=counters,
                         updates=[u for per in eng.updates for u in per], stamps=stamps,

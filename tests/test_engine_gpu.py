@@ -472,3 +472,38 @@ def test_serialized_misaligned_blocks_match_oracle(kind, workers, updaters, boun
                                switch_point=30, period=3, budget=60, warm_start=6, batch_size=8, seed=4)
     np.testing.assert_allclose(res.final_values, tr.final_values, atol=ATOL, rtol=RTOL)
     assert [tuple(r) for r in res.round_trace] == [(a, b, *c) for a, b, c in tr.rounds]
+
+
+def test_synchronous_eval_rows_land_on_the_interval():
+    """test_engine.py:281-286."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    res = run_experiment(_tiny(obj, algo="mb_sgd", budget=100, eval_interval=25, evaluate=True))
+    assert [row.samples for row in res.metrics] == [0, 25, 50, 75, 100]
+    assert [row.round for row in res.metrics] == [0, 25, 50, 75, 100]
+    assert res.metrics[-1].train_loss == pytest.approx(obj.full_loss(res.final_values), rel=1e-6)
+
+
+def test_async_metrics_start_at_zero_and_grow():
+    """test_engine.py:289-299."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    res = run_experiment(_tiny(obj, algo="lap_sgd", budget=300, updaters=2, eval_interval=100,
+                               evaluate=True))
+    samples = [row.samples for row in res.metrics]
+    assert samples[0] == 0 and samples == sorted(samples) and len(res.metrics) >= 3
+    final = res.metrics[-1]
+    assert final.train_loss == pytest.approx(obj.full_loss(res.final_values), rel=1e-6)
+    assert 0.0 < final.p_hat <= 1.0
+
+
+def test_final_row_matches_final_values_for_every_algorithm():
+    """test_engine.py:302-305."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    for algo in ("mb_sgd", "pl_sgd", "lap_sgd"):
+        res = run_experiment(_tiny(obj, algo=algo, budget=60, evaluate=True))
+        assert res.metrics[-1].train_loss == pytest.approx(obj.full_loss(res.final_values), rel=1e-6)
