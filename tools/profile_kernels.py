@@ -34,6 +34,18 @@ for d in (11_220_132, 25_557_032):
         N.apply_sgd_tagged(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, tg.ptr, 7, st)
     for a in (x, g, m, tg):
         a.close()
+# K1+K3 fused (the async default) at d20 and d50 with a partial block, + the K5 gather
+for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000)):
+    x, g, m, rep, tg = (Arena(d, 0) for _ in range(5))
+    x.tensor.normal_(), g.tensor.normal_()
+    idx = torch.randint(0, d, (16,), device="cuda")
+    out = torch.empty(16, dtype=torch.int32, device="cuda")
+    for _ in range(2):
+        flush()
+        N.gather_tags(tg.ptr, idx.data_ptr(), 16, out.data_ptr(), st)
+        N.apply_snapshot(x.ptr, g.ptr, m.ptr, rep.ptr, tg.ptr, d, lo, hi, 1e-3, None, 0.9, 5e-4, 3, st)
+    for a in (x, g, m, rep, tg):
+        a.close()
 d = 16_000_000
 ars = [Arena(d, 0) for _ in range(4)]
 for _ in range(2):
