@@ -110,6 +110,7 @@ _SIGS = {
     "lpp_mc_destroy": (_c.c_int, [_vp]),
     "lpp_nvls_mean_shard": (_c.c_int, [_vp, _vp, _size, _size, _c.c_int, _vp]),
     "lpp_nvls_apply": (_c.c_int, [_vp, _vp, _vp, _size, _vp, _c.c_int32, _vp]),
+    "lpp_copy_async": (_c.c_int, [_vp, _vp, _size, _vp]),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
 }
@@ -160,6 +161,11 @@ def _cell_ptr(buf: np.ndarray, i: int) -> int:
     if not 0 <= i < buf.shape[0]:
         raise IndexError(f"index {i} out of range [0, {buf.shape[0]})")
     return buf.ctypes.data + 8 * i
+
+
+def cell_address(buf: np.ndarray, i: int) -> int:
+    """Address of int64 cell i (validated); the caller keeps ``buf`` alive."""
+    return _cell_ptr(buf, i)
 
 
 def atomic_load(buf: np.ndarray, i: int = 0) -> int:
@@ -265,6 +271,12 @@ def average_shard_tagged(arena_ptrs, tag_ptrs, stamps, lo, hi, mean_out_ptr, mod
     _count()
     check(lib.lpp_average_shard_tagged(a, t, st, q, lo, hi, mean_out_ptr, mode, stream),
           "average_shard_tagged")
+
+
+def copy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream: int) -> None:
+    rc = lib.lpp_copy_async(dst_ptr, src_ptr, nbytes, stream)
+    if rc:
+        check(rc, "copy_async")
 
 
 def l2_flush(ptr: int, nbytes: int, stream: int) -> None:

@@ -1098,6 +1098,13 @@ extern "C" int lpp_enable_peer_access(int device, int peer) {
 // ---------------------------------------------------------------------------
 // utilities
 
+extern "C" int lpp_copy_async(void* dst, const void* src, size_t n_bytes, void* stream) {
+  if (n_bytes == 0) return LPP_OK;
+  if (!dst || !src) return set_err(LPP_E_VALUE, "copy_async: null pointer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, n_bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return LPP_OK;
+}
+
 extern "C" int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream) {
   if (!scratch) return set_err(LPP_E_VALUE, "l2_flush: null scratch");
   CUDA_TRY(cudaMemsetAsync(scratch, 0x5a, n_bytes, (cudaStream_t)stream));

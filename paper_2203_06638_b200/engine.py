@@ -348,6 +348,13 @@ class _Worker:
                 self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in range(U_)]
                 self.copied = [[torch.cuda.Event() for _ in range(depth)] for _ in range(U_)]
                 self.buf_free = [[torch.cuda.Event() for _ in range(2)] for _ in range(U_)]
+            # numpy views of the pinned staging rings: the per-step host
+            # writes/reads skip the framework's dispatch
+            self.idx_np = self.idx_pinned.numpy()
+            if cfg.tracks:
+                self.tag_idx_np = self.tag_idx_pinned.numpy()
+                self.tag_np = self.tag_pinned.numpy()
+                self.min_np = self.min_pinned.numpy()
             # the warm-up passes touched the replica/grad arenas and BN stats
             # only; re-snapshot so every replica starts at x0
             for r in range(cfg.updaters):
@@ -480,8 +487,9 @@ class _Engine:
                 if self.host_batches:
                     self.stage_host_batch(w, r, batch, slot, buf)
                 else:
-                    w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
-                    prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)
+                    w.idx_np[r, slot] = batch
+                    N.copy_async(prog.idx.data_ptr(), w.idx_pinned[r, slot].data_ptr(),
+                                 8 * cfg.batch_size, sp)
             if not tracks:
                 N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)       # K3
             elif cfg.record_mode == "full":
@@ -495,12 +503,7 @@ class _Engine:
                 w.min_pinned[r, slot].copy_(w.min_dev[r, slot], non_blocking=True)
             else:
                 # K5: sampled tags are gathered BEFORE the value copy (paramstore.py:108-112)
-                k = w.tag_pick
-                w.tag_idx_pinned[r, slot, :k].copy_(torch.from_numpy(tag_idx))
-                w.tag_idx_dev[r, :k].copy_(w.tag_idx_pinned[r, slot, :k], non_blocking=True)
-                N.gather_tags(w.tag_arena.ptr, w.tag_idx_dev[r].data_ptr(), k,
-                              w.tag_out_dev[r, slot].data_ptr(), sp)
-                w.tag_pinned[r, slot].copy_(w.tag_out_dev[r, slot], non_blocking=True)
+                self.gather_tags(w, r, slot, tag_idx)
                 N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)       # K3
             prog.run(block_id, buf)                                                   # fwd+bwd
             if self.host_batches:
@@ -578,11 +581,12 @@ class _Engine:
         """K5: sampled tags of the NEXT snapshot into slot, then D2H (on the
         updater stream; must precede the values it describes)."""
         k = w.tag_pick
-        w.tag_idx_pinned[r, slot, :k].copy_(torch.from_numpy(tag_idx))
-        w.tag_idx_dev[r, :k].copy_(w.tag_idx_pinned[r, slot, :k], non_blocking=True)
+        sp = w.streams[r].cuda_stream
+        w.tag_idx_np[r, slot, :k] = tag_idx
+        N.copy_async(w.tag_idx_dev[r].data_ptr(), w.tag_idx_pinned[r, slot].data_ptr(), 8 * k, sp)
         N.gather_tags(w.tag_arena.ptr, w.tag_idx_dev[r].data_ptr(), k,
-                      w.tag_out_dev[r, slot].data_ptr(), w.streams[r].cuda_stream)
-        w.tag_pinned[r, slot].copy_(w.tag_out_dev[r, slot], non_blocking=True)
+                      w.tag_out_dev[r, slot].data_ptr(), sp)
+        N.copy_async(w.tag_pinned[r, slot].data_ptr(), w.tag_out_dev[r, slot].data_ptr(), 4 * k, sp)
 
     def step_fused(self, w: _Worker, r: int, block_id: int, lr: float, batch, slot: int,
                    next_slot: int, u: int, first: bool, tag_idx, next_tag_idx,
@@ -600,8 +604,9 @@ class _Engine:
                 if self.host_batches:
                     self.stage_host_batch(w, r, batch, slot, buf)
                 else:
-                    w.idx_pinned[r, slot].copy_(torch.from_numpy(batch))
-                    prog.idx.copy_(w.idx_pinned[r, slot], non_blocking=True)
+                    w.idx_np[r, slot] = batch
+                    N.copy_async(prog.idx.data_ptr(), w.idx_pinned[r, slot].data_ptr(),
+                                 8 * cfg.batch_size, sp)
             if first:
                 if tracks:
                     self.gather_tags(w, r, slot, tag_idx)
@@ -699,11 +704,11 @@ class _Engine:
         if w.tags is None:
             return
         if self.cfg.record_mode == "full":
-            clean = int(w.min_pinned[r, slot]) >= rec.k_claim
+            clean = int(w.min_np[r, slot]) >= rec.k_claim
             if self.cfg.record_tensors and rec.snapshot is not None and rec.tags is None:
                 rec.tags = w.snap_tags[r][slot].cpu().numpy().astype(np.int64)
         else:
-            tg = w.tag_pinned[r, slot, :w.tag_pick].numpy().astype(np.int64)
+            tg = w.tag_np[r, slot, :w.tag_pick].astype(np.int64)
             rec.tags = tg
             clean = bool((tg >= rec.k_claim).all())
         rec.clean = clean

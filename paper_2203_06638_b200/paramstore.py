@@ -34,7 +34,7 @@ from .arena import Arena, stream_ptr
 class AtomicCounter:
     """A shared int64 with atomic fetch-and-add (``paramstore.py:19-39``)."""
 
-    __slots__ = ("_cell", "_i")
+    __slots__ = ("_cell", "_i", "_a")
 
     def __init__(self, initial: int = 0, cell: np.ndarray | None = None, index: int = 0):
         if cell is None:
@@ -42,23 +42,24 @@ class AtomicCounter:
             index = 0
         else:
             N.atomic_store(cell, index, initial)
-        self._cell = cell
+        self._cell = cell                  # keeps the cell's buffer alive
         self._i = index
+        self._a = N.cell_address(cell, index)
 
     def read_and_inc(self) -> int:
-        return N.atomic_fetch_add(self._cell, self._i, 1)
+        return N.lib.lpp_atomic_fetch_add_i64(self._a, 1)
 
     def read(self) -> int:
-        return N.atomic_load(self._cell, self._i)
+        return N.lib.lpp_atomic_load_i64(self._a)
 
     def add(self, delta: int) -> int:
-        return N.atomic_fetch_add(self._cell, self._i, delta)
+        return N.lib.lpp_atomic_fetch_add_i64(self._a, delta)
 
     def store(self, value: int) -> None:
-        N.atomic_store(self._cell, self._i, value)
+        N.lib.lpp_atomic_store_i64(self._a, value)
 
     def cas(self, expected: int, desired: int) -> bool:
-        return N.atomic_cas(self._cell, self._i, expected, desired)
+        return bool(N.lib.lpp_atomic_cas_i64(self._a, expected, desired))
 
     def wait_ge(self, target: int, abort: "AtomicCounter | None" = None) -> int | None:
         """Block without the GIL until the value is >= target (None: aborted)."""

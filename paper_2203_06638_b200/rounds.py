@@ -33,24 +33,25 @@ from . import _native as N
 
 
 class _Cell:
-    """One int64 cell of the control block."""
+    """One int64 cell of the control block (address resolved once)."""
 
-    __slots__ = ("_b", "_i")
+    __slots__ = ("_b", "_a")
 
     def __init__(self, buf, i):
-        self._b, self._i = buf, i
+        self._b = buf                      # keeps the buffer alive
+        self._a = N.cell_address(buf, i)
 
     def read(self) -> int:
-        return N.atomic_load(self._b, self._i)
+        return N.lib.lpp_atomic_load_i64(self._a)
 
     def add(self, d: int) -> int:
-        return N.atomic_fetch_add(self._b, self._i, d)
+        return N.lib.lpp_atomic_fetch_add_i64(self._a, d)
 
     def store(self, v: int) -> None:
-        N.atomic_store(self._b, self._i, v)
+        N.lib.lpp_atomic_store_i64(self._a, v)
 
     def cas(self, expected: int, desired: int) -> bool:
-        return N.atomic_cas(self._b, self._i, expected, desired)
+        return bool(N.lib.lpp_atomic_cas_i64(self._a, expected, desired))
 
 
 class RoundControl:
