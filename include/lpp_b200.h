@@ -220,6 +220,9 @@ int lpp_nvls_apply(float* x, const float* stage, const float* mean, size_t n,
  * (cudaMemcpyAsync, kind inferred): the per-step index / tag H2D and D2H
  * without a framework dispatch. */
 int lpp_copy_async(void* dst, const void* src, size_t n_bytes, void* stream);
+/* Launch an instantiated CUDA graph (cudaGraphExec_t) on a stream: the
+ * captured fwd/bwd step replayed without a framework wrapper. */
+int lpp_graph_launch(void* graph_exec, void* stream);
 /* Write a buffer of n_bytes (>= L2 size to flush it) on the stream. */
 int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream);
 /* number of SMs of `device` */

@@ -111,6 +111,7 @@ _SIGS = {
     "lpp_nvls_mean_shard": (_c.c_int, [_vp, _vp, _size, _size, _c.c_int, _vp]),
     "lpp_nvls_apply": (_c.c_int, [_vp, _vp, _vp, _size, _vp, _c.c_int32, _vp]),
     "lpp_copy_async": (_c.c_int, [_vp, _vp, _size, _vp]),
+    "lpp_graph_launch": (_c.c_int, [_vp, _vp]),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
 }
@@ -271,6 +272,12 @@ def average_shard_tagged(arena_ptrs, tag_ptrs, stamps, lo, hi, mean_out_ptr, mod
     _count()
     check(lib.lpp_average_shard_tagged(a, t, st, q, lo, hi, mean_out_ptr, mode, stream),
           "average_shard_tagged")
+
+
+def graph_launch(exec_ptr: int, stream: int) -> None:
+    rc = lib.lpp_graph_launch(exec_ptr, stream)
+    if rc:
+        check(rc, "graph_launch")
 
 
 def copy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream: int) -> None:

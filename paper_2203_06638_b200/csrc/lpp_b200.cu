@@ -1098,6 +1098,12 @@ extern "C" int lpp_enable_peer_access(int device, int peer) {
 // ---------------------------------------------------------------------------
 // utilities
 
+extern "C" int lpp_graph_launch(void* graph_exec, void* stream) {
+  if (!graph_exec) return set_err(LPP_E_VALUE, "graph_launch: null graph");
+  CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));
+  return LPP_OK;
+}
+
 extern "C" int lpp_copy_async(void* dst, const void* src, size_t n_bytes, void* stream) {
   if (n_bytes == 0) return LPP_OK;
   if (!dst || !src) return set_err(LPP_E_VALUE, "copy_async: null pointer");

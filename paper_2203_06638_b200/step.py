@@ -82,6 +82,16 @@ class StepProgram:
                         pool = g.pool()
                         self.graphs[(bid, buf)] = g
                 stream.synchronize()
+        # raw cudaGraphExec_t handles: graphs without a registered generator
+        # are launched straight through the C ABI (torch's replay() also
+        # advances generator offsets, which the "random" input mode needs)
+        self.execs = {}
+        if use_graphs and self.gen is None:
+            from . import _native
+
+            self._native = _native
+            for key, g in self.graphs.items():
+                self.execs[key] = int(g.raw_cuda_graph_exec())
 
     def _body(self, bid: int, buf: int = 0) -> None:
         blk = self.blocks[bid]
@@ -104,7 +114,9 @@ class StepProgram:
     def run(self, bid: int, buf: int = 0) -> None:
         """Enqueue block ``bid``'s fwd+bwd (reading input buffer ``buf``)."""
         buf %= self.nbuf
-        if self.use_graphs:
+        if self.execs:
+            self._native.graph_launch(self.execs[(bid, buf)], self.stream.cuda_stream)
+        elif self.use_graphs:
             self.graphs[(bid, buf)].replay()
         else:
             with torch.cuda.stream(self.stream):
