@@ -230,6 +230,15 @@ def ours(args) -> None:
     tr.close()
     del tr
 
+    # traffic: DRAM bytes per launch of the same kernel at the ResNet-20 arena
+    # size from the committed ncu --set full capture (profiles/)
+    traffic = None
+    tp = ROOT / "profiles" / "r1_kernel_traffic.json"
+    if tp.exists():
+        name = "void k_apply_snapshot<1, 1>" if fused else "void k_apply<1, 1, 1>"
+        cands = [e["dram_bytes"] for e in json.loads(tp.read_text())["launches"]
+                 if e["kernel"] == name and e["grid"] == 267]
+        traffic = sum(cands) / len(cands) if cands else None
     line = {
         "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": ws,
         "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
@@ -250,7 +259,9 @@ def ours(args) -> None:
                                 "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)"),
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],
-                     "traffic": None, "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
+                     "traffic": traffic,
+                     "traffic_src": "profiles/r1_kernel_traffic.json (ncu --set full, d20, cold L2)",
+                     "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
                      "bytes_per_launch": app_bytes / max(n_app, 1),
                      "note": "d20 arena (1.09 MB) is L2-resident: latency-bound; see kernel_sweep"},
     }
