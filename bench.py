@@ -313,6 +313,19 @@ def ours(args) -> None:
                         "note": "same engine, full backprop every step (no PASSM+ blocks)"},
             "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
 
+    # ---------------- the paper's U = 6 variant ----------------
+    if not args.no_baselines and ws == 1:
+        c6 = build_cfg(obj, (K + W) * 6, workers=1, updaters=6)
+        t6 = Trainer(c6)
+        t6.run(W * 6, evaluate=False)
+        torch.cuda.synchronize()
+        r6 = t6.run(K * 6, evaluate=False)
+        line["baselines"]["lpp_sgd_u6"] = {
+            "value": sum(r6.counter_finals) * B / (r6.device_ms / 1e3), "unit": "images/s",
+            "streams": 6, "note": "same workload with 6 updater streams (the paper's best LPP row)"}
+        t6.close()
+        del t6
+
     # ---------------- ResNet-18 / CIFAR-100 shape (config C2) ----------------
     if not args.no_rn18 and ws == 1:
         obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
@@ -357,6 +370,15 @@ def ours(args) -> None:
                                "bytes_per_launch": by50 / max(n50, 1)}}
         t50.close()
         del t50
+        m50 = build_cfg(obj50, 64, algo="mb_sgd", workers=1)
+        m50 = __import__("dataclasses").replace(m50, batch_size=32)
+        tm50 = Trainer(m50)
+        tm50.run(3 * U, evaluate=False)
+        torch.cuda.synchronize()
+        rm50 = tm50.run(args.rn50_steps * U, evaluate=False)
+        line["resnet50"]["mb_sgd"] = args.rn50_steps * U * 32 / (rm50.device_ms / 1e3)
+        line["resnet50"]["lpp_over_mb"] = line["resnet50"]["value"] / line["resnet50"]["mb_sgd"]
+        del tm50
 
     # ---------------- kernel sweep (HBM roofline evidence) ----------------
     if not args.no_sweep and rank == 0:
