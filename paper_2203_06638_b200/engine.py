@@ -1263,24 +1263,6 @@ class _SyncEngine:
         self.wall_ms = (time.perf_counter() - self.t0) * 1e3
         return ms
 
-    def round_mean(self, q: int) -> torch.Tensor:
-        """The just-finished round's mean as seen by worker q (a device copy)."""
-        if self.nvls:
-            return self.nvls[q].mean_tensor.clone()
-        m = self.gather_round_mean()
-        if m is None:
-            # multi-process P2P: the other shards' means live in the peers;
-            # use this worker's arena right after the round (mean + racing updates)
-            m = self.workers[q].store.arena.tensor.clone()
-        return m
-
-    def gather_round_mean(self):
-        """The current round's mean from the owners' mean_out shards (one process)."""
-        if self.group is not None:
-            return None
-        parts = [self.workers[q].mean_out[lo:hi] for q, (lo, hi) in enumerate(self.shards)]
-        return torch.cat(parts).clone()
-
     def final_values(self) -> np.ndarray:
         return self.x[self.local[0]].tensor.cpu().numpy()
 
