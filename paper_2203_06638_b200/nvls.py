@@ -90,6 +90,40 @@ class _Mc:
             self.h = None
 
 
+def share_fds(group, fds: list[int] | None, count: int | None = None) -> list[int]:
+    """Hand rank 0's file descriptors to every other rank of the group.
+
+    Rank 0 passes ``fds`` (it keeps its own copies and gets them back); the
+    others pass None and ``count``, and receive duplicates of the same open
+    files over an abstract-namespace Unix socket (SCM_RIGHTS) whose name
+    travels over ``torch.distributed``.  Used for the multicast-object
+    handles, which are POSIX file descriptors."""
+    import torch.distributed as dist
+
+    name = [None]
+    srv = None
+    if group.rank == 0:
+        name[0] = f"lpp-fds-{uuid.uuid4().hex}"
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind("\0" + name[0])
+        srv.listen(max(group.world - 1, 1))
+    dist.broadcast_object_list(name, src=0)
+    if group.rank == 0:
+        for _ in range(group.world - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"fds"], fds)
+            conn.close()
+        srv.close()
+        return list(fds)
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect("\0" + name[0])
+    _, got, _, _ = socket.recv_fds(cli, 16, count)
+    cli.close()
+    if len(got) != count:
+        raise RuntimeError(f"expected {count} file descriptors, received {len(got)}")
+    return list(got)
+
+
 def supported(device: int, workers: int = 1) -> bool:
     """Multicast attribute AND a multicast object can actually be created
     (containers that expose one GPU without fabric-manager access report the
@@ -147,35 +181,16 @@ class NvlsGroup:
         self.mean_tensor = _view(self.mean.ptr, self.dim, self.device)
 
     def _exchange(self, group) -> None:
-        import torch.distributed as dist
-
-        name = [None]
         if group.rank == 0:
             self.mc_stage = _Mc.create(self.workers, self.nbytes)
             self.mc_mean = _Mc.create(self.workers, self.nbytes)
-            fds = [self.mc_stage.export_fd(), self.mc_mean.export_fd()]
-            name[0] = f"lpp-nvls-{uuid.uuid4().hex}"
-            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            srv.bind("\0" + name[0])
-            srv.listen(self.workers)
-        dist.broadcast_object_list(name, src=0)
-        if group.rank == 0:
-            for _ in range(self.workers - 1):
-                conn, _ = srv.accept()
-                socket.send_fds(conn, [b"fds"], fds)
-                conn.close()
-            srv.close()
-            for fd in fds:
-                os.close(fd)
+            fds = share_fds(group, [self.mc_stage.export_fd(), self.mc_mean.export_fd()])
         else:
-            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            cli.connect("\0" + name[0])
-            _, fds, _, _ = socket.recv_fds(cli, 16, 2)
-            cli.close()
+            fds = share_fds(group, None, count=2)
             self.mc_stage = _Mc.import_fd(fds[0], self.nbytes)
             self.mc_mean = _Mc.import_fd(fds[1], self.nbytes)
-            for fd in fds:
-                os.close(fd)
+        for fd in fds:
+            os.close(fd)
         for mc in (self.mc_stage, self.mc_mean):
             mc.add_device(self.device)
         group.barrier()   # every device added before anyone binds

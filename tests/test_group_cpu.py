@@ -115,3 +115,51 @@ def test_group_round_budget_stops_updaters():
     assert n0 == n1 and n0 >= 5
     assert l0[-1][3] and l1[-1][3]
     assert c0 < 10**6 and c1 < 10**6
+
+
+def _fd_worker(rank, world, port, out_q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_06638_b200.group import ProcessGroup
+    from paper_2203_06638_b200.nvls import share_fds
+
+    g = ProcessGroup(workers=world, max_rounds=8)
+    if rank == 0:
+        r1, w1 = os.pipe()
+        r2, w2 = os.pipe()
+        got = share_fds(g, [r1, r2])
+        g.barrier()
+        os.write(w1, b"stage")
+        os.write(w2, b"mean")
+        g.barrier()
+        out_q.put((rank, "sent"))
+    else:
+        got = share_fds(g, None, count=2)
+        g.barrier()
+        g.barrier()
+        out_q.put((rank, os.read(got[0], 16).decode() + "/" + os.read(got[1], 16).decode()))
+    g.close()
+    dist.destroy_process_group()
+
+
+def test_nvls_fd_exchange_between_ranks():
+    """The multicast-handle exchange of NVLS averaging (SCM_RIGHTS over a
+    Unix socket, name over torch.distributed), exercised with pipe fds: the
+    ranks read what rank 0 wrote into its own descriptors."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fd_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(30)
+        assert p.exitcode == 0
+    assert res == [(0, "sent"), (1, "stage/mean")]
