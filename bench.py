@@ -215,9 +215,9 @@ def ours(args) -> None:
         tr.eng.nvtx = "lpp_timed"   # ncu --nvtx --nvtx-include lpp_timed/ profiles this phase only
     with Clocks(dev) as clk:
         barrier()
-        l0 = N.launches
+        l0 = N.launch_count()
         res = tr.run(K * U, evaluate=False)
-        launches = N.launches - l0
+        launches = N.launch_count() - l0
         barrier()
     tr.eng.nvtx = None
     dev_ms = max_over_ranks(res.device_ms)

@@ -47,6 +47,8 @@ extern "C" {
 
 int lpp_abi_version(void);
 const char* lpp_last_error(void);
+/* number of kernels this library has launched so far (process-wide) */
+unsigned long long lpp_launch_count(void);
 
 /* ------------------------------------------------------------------ */
 /* host atomics (K6) — replace _atomics.{load,store,fetch_add}_i64     */

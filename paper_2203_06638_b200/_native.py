@@ -51,6 +51,7 @@ _i64p = _c.POINTER(_c.c_int64)
 _SIGS = {
     "lpp_abi_version": (_c.c_int, []),
     "lpp_last_error": (_c.c_char_p, []),
+    "lpp_launch_count": (_c.c_ulonglong, []),
     "lpp_atomic_load_i64": (_c.c_int64, [_vp]),
     "lpp_atomic_store_i64": (None, [_vp, _c.c_int64]),
     "lpp_atomic_fetch_add_i64": (_c.c_int64, [_vp, _c.c_int64]),
@@ -124,14 +125,10 @@ for _name, (_res, _args) in _SIGS.items():
     _fn.argtypes = _args
 
 
-# number of device launches issued through this binding (every wrapper below
-# that enqueues a kernel bumps it; bench.py reports the timed-region delta)
-launches = 0
-
-
-def _count(n: int = 1) -> None:
-    global launches
-    launches += n
+def launch_count() -> int:
+    """Kernels launched by the library so far (an atomic counter in C; the
+    bench reports its delta over the timed region)."""
+    return int(lib.lpp_launch_count())
 
 
 def last_error() -> str:
@@ -205,7 +202,6 @@ def sm_count(device: int) -> int:
 
 def apply_sgd(x_ptr: int, g_ptr: int, m_ptr: int | None, n: int, lr: float,
               lr_dev_ptr: int | None, mu: float, wd: float, mode: int, stream: int) -> None:
-    _count()
     check(
         lib.lpp_apply_sgd(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, stream),
         "apply_sgd",
@@ -214,19 +210,16 @@ def apply_sgd(x_ptr: int, g_ptr: int, m_ptr: int | None, n: int, lr: float,
 
 def apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr, lr_dev_ptr, mu, wd,
                    stamp, stream) -> None:
-    _count()
     check(lib.lpp_apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr,
                                  lr_dev_ptr, mu, wd, int(stamp), stream), "apply_snapshot")
 
 
 def accum(dst_ptr: int, dst_len: int, start: int, delta_ptr: int, n: int, scale: float,
           mode: int, stream: int) -> None:
-    _count()
     check(lib.lpp_accum(dst_ptr, dst_len, start, delta_ptr, n, scale, mode, stream), "accum")
 
 
 def snapshot(src_ptr: int, out_ptr: int, n: int, stream: int) -> None:
-    _count()
     check(lib.lpp_snapshot(src_ptr, out_ptr, n, stream), "snapshot")
 
 
@@ -234,32 +227,27 @@ def average_shard(arena_ptrs, lo: int, hi: int, mean_out_ptr: int | None, mode: 
                   stream: int) -> None:
     q = len(arena_ptrs)
     table = (_vp * max(q, 1))(*arena_ptrs)
-    _count()
     check(lib.lpp_average_shard(table, q, lo, hi, mean_out_ptr, mode, stream), "average_shard")
 
 
 def apply_sgd_tagged(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, tags_ptr, stamp,
                      stream) -> None:
-    _count()
     check(lib.lpp_apply_sgd_tagged(x_ptr, g_ptr, m_ptr, n, lr, lr_dev_ptr, mu, wd, mode, tags_ptr,
                                    int(stamp), stream), "apply_sgd_tagged")
 
 
 def accum_tagged(dst_ptr, tags_ptr, dst_len, start, delta_ptr, n, scale, stamp, mode,
                  stream) -> None:
-    _count()
     check(lib.lpp_accum_tagged(dst_ptr, tags_ptr, dst_len, start, delta_ptr, n, scale,
                                int(stamp), mode, stream), "accum_tagged")
 
 
 def snapshot_tagged(src_ptr, tags_ptr, out_ptr, out_tags_ptr, n, min_tag_ptr, stream) -> None:
-    _count()
     check(lib.lpp_snapshot_tagged(src_ptr, tags_ptr, out_ptr, out_tags_ptr, n, min_tag_ptr,
                                   stream), "snapshot_tagged")
 
 
 def gather_tags(tags_ptr, idx_ptr, k, out_ptr, stream) -> None:
-    _count()
     check(lib.lpp_gather_tags(tags_ptr, idx_ptr, k, out_ptr, stream), "gather_tags")
 
 
@@ -269,7 +257,6 @@ def average_shard_tagged(arena_ptrs, tag_ptrs, stamps, lo, hi, mean_out_ptr, mod
     a = (_vp * q)(*arena_ptrs)
     t = (_vp * q)(*tag_ptrs)
     st = (_c.c_int32 * q)(*[int(v) for v in stamps])
-    _count()
     check(lib.lpp_average_shard_tagged(a, t, st, q, lo, hi, mean_out_ptr, mode, stream),
           "average_shard_tagged")
 

@@ -53,15 +53,21 @@ static int set_err(int code, const char* fmt, ...) {
                      cudaGetErrorString(e_));                               \
   } while (0)
 
+// every successful kernel launch of this library is counted (the bench's
+// gpu_launches is the delta of this counter over the timed region)
+static std::atomic<unsigned long long> g_launches{0};
+
 #define LAUNCH_CHECK(name)                                                  \
   do {                                                                      \
     cudaError_t e_ = cudaGetLastError();                                    \
     if (e_ != cudaSuccess)                                                  \
       return set_err(LPP_E_CUDA, "%s launch failed: %s", name,              \
                      cudaGetErrorString(e_));                               \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                     \
   } while (0)
 
 extern "C" int lpp_abi_version(void) { return LPP_ABI_VERSION; }
+extern "C" unsigned long long lpp_launch_count(void) { return g_launches.load(); }
 extern "C" const char* lpp_last_error(void) { return g_err; }
 
 // ---------------------------------------------------------------------------

@@ -201,12 +201,10 @@ class NvlsGroup:
         N.snapshot(arena_ptr, self.stage.ptr, self.dim, stream)
 
     def reduce_mean(self, lo: int, hi: int, stream: int) -> None:
-        N._count()
         _ck(N.lib.lpp_nvls_mean_shard(self.mc_stage.ptr, self.mc_mean.ptr, lo, hi, self.workers,
                                       stream), "nvls_mean_shard")
 
     def apply(self, arena_ptr: int, tags_ptr: int | None, stamp: int, stream: int) -> None:
-        N._count()
         _ck(N.lib.lpp_nvls_apply(arena_ptr, self.stage.ptr, self.mean.ptr, self.dim, tags_ptr,
                                  int(stamp), stream), "nvls_apply")
 
