@@ -400,7 +400,8 @@ class ResNetObjective(ArenaObjective):
 
     def __init__(self, arch: str = "resnet20", n_samples: int = 8192, seed: int = 0,
                  channels_last: bool = True, autocast: str | None = "bf16",
-                 data: str = "device", n_classes: int | None = None):
+                 data: str = "device", n_classes: int | None = None,
+                 pattern_scale: float = 0.0):
         if arch not in _ARCHS:
             raise ValueError(f"unknown arch {arch!r}")
         cls, shape, k = _ARCHS[arch]
@@ -412,6 +413,10 @@ class ResNetObjective(ArenaObjective):
         self.channels_last = channels_last
         self.autocast_dtype = {"bf16": torch.bfloat16, "fp16": torch.float16, None: None}[autocast]
         self.data_mode = data
+        # 0: N(0,1) images, uniform labels; > 0: a fixed
+        # random pattern per class times pattern_scale plus N(0,1) noise —
+        # make_blobs (data.py:34-52) in image space, a learnable task
+        self.pattern_scale = float(pattern_scale)
         self._feat_cache, self._lab_cache = {}, {}
         self._template = cls(self.n_classes)
         self.param_names = [n for n, _ in self._template.named_parameters()]
@@ -429,6 +434,10 @@ class ResNetObjective(ArenaObjective):
         self._features = None
 
     # synthetic dataset: N(0,1) images, uniform labels
+    def _patterns(self) -> torch.Tensor:
+        g = torch.Generator().manual_seed(self.seed + 7919)
+        return torch.randn(self.n_classes, *self.image_shape, generator=g) * self.pattern_scale
+
     @property
     def features(self) -> torch.Tensor:
         if self._features is None:
@@ -436,6 +445,8 @@ class ResNetObjective(ArenaObjective):
             self._labels = torch.randint(0, self.n_classes, (self.n_samples,), generator=g)
             if self.data_mode == "host":
                 f = torch.randn(self.n_samples, *self.image_shape, generator=g)
+                if self.pattern_scale:
+                    f += self._patterns()[self._labels]
                 self._features = f.pin_memory() if torch.cuda.is_available() else f
             else:
                 self._features = "device"
@@ -454,8 +465,10 @@ class ResNetObjective(ArenaObjective):
                 self._feat_cache[key] = self._features.to(device)
             else:
                 g = torch.Generator(device=device).manual_seed(self.seed)
-                self._feat_cache[key] = torch.randn(self.n_samples, *self.image_shape, generator=g,
-                                                    device=device)
+                f = torch.randn(self.n_samples, *self.image_shape, generator=g, device=device)
+                if self.pattern_scale:
+                    f += self._patterns().to(device)[self._labels.to(device)]
+                self._feat_cache[key] = f
             self._lab_cache[key] = self._labels.to(device)
         return self._feat_cache[key]
 
