@@ -539,3 +539,35 @@ def test_cnn_async_lpp_loss_band_vs_synchronous():
     print(f"\nCNN band: initial {l0:.3f}  LPP async {la:.3f}  MB-SGD {lm:.3f}")
     assert la < 0.5 * l0 and lm < 0.5 * l0, (l0, la, lm)
     assert abs(la - lm) <= 0.35 * l0, (l0, la, lm)
+
+
+@pytest.mark.parametrize("quiescent", [False, True])
+def test_updater_failure_aborts_the_run(quiescent):
+    """engine.py:456-463, 504-505: a failing updater stops every thread
+    (averagers blocked on votes / fences / gates included) and the run raises."""
+    import time as _t
+
+    from paper_2203_06638_b200 import async_engine
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    cfg = _tiny(obj, algo="lap_sgd", budget=10_000, workers=2, updaters=2, quiescent=quiescent)
+    orig = async_engine._Engine.step_fused if not quiescent else async_engine._Engine.step
+    calls = {"n": 0}
+
+    def boom(self, *a, **k):
+        calls["n"] += 1
+        if calls["n"] == 25:
+            raise ValueError("injected updater failure")
+        return orig(self, *a, **k)
+
+    name = "step" if quiescent else "step_fused"
+    setattr(async_engine._Engine, name, boom)
+    try:
+        t0 = _t.perf_counter()
+        with pytest.raises(RuntimeError, match="engine thread failed") as ei:
+            run_experiment(cfg)
+        assert isinstance(ei.value.__cause__, ValueError)
+        assert _t.perf_counter() - t0 < 60
+    finally:
+        setattr(async_engine._Engine, name, orig)
