@@ -289,6 +289,46 @@ def ours(args) -> None:
         htr.close()
         del htr
 
+    # ---------------- averaging bandwidth across the group (N > 1) ----------------
+    # BASELINE.json's second metric: K4 over the P2P/NVLink-mapped arenas of
+    # all ranks, each rank averaging its owned shard of a d-element group;
+    # busbw = 2(Q-1)/Q x 4d bytes per GPU and direction / max-over-ranks time
+    if ws > 1 and not args.no_sweep:
+        from paper_2203_06638_b200.arena import Arena
+        from paper_2203_06638_b200.engine import shard_bounds
+
+        avg = {}
+        for d in (16_000_000, 64_000_000):
+            ar = Arena(d, dev)
+            ar.tensor.normal_()
+            ptrs = group.attach_arenas(ar)
+            lo, hi = shard_bounds(d, ws)[rank]
+            st = torch.cuda.current_stream().cuda_stream
+            for _ in range(3):
+                N.average_shard(ptrs, lo, hi, None, N.MODE_RED, st)
+            ts = []
+            for _ in range(10):
+                barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                N.average_shard(ptrs, lo, hi, None, N.MODE_RED, st)
+                b.record()
+                b.synchronize()
+                ts.append(max_over_ranks(a.elapsed_time(b)))
+            t = sorted(ts)[len(ts) // 2] / 1e3
+            busbw = 2 * (ws - 1) / ws * 4 * d / t / 1e9
+            avg[str(d)] = {"us": t * 1e6, "busbw_gbs": busbw, "frac_of_770": busbw / 770.0,
+                           "frac_of_900": busbw / 900.0}
+            barrier()
+            for pm in group.peers[-(ws - 1):]:
+                pm.close()
+            del group.peers[-(ws - 1):]
+            ar.close()
+        line["averaging"] = {"kernel": "lpp_average_shard (K4, owner-computes over peer arenas)",
+                             "unit": "GB/s", "sizes": avg,
+                             "note": "busbw = 2(Q-1)/Q x 4d per GPU per direction (nccl-tests convention); "
+                                     "770 GB/s = measured peer copy, 900 = NVLink 5 nominal"}
+
     # ---------------- baselines on the same box: MB-SGD and LAP-SGD ----------------
     if not args.no_baselines and ws == 1:
         mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)

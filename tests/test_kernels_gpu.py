@@ -415,3 +415,31 @@ def test_apply_snapshot_no_lost_updates_and_member_values(N):
     for r in reps:
         v = r.tensor[3:n - 2]
         assert bool((v == v.round()).all()) and float(v.min()) >= 1 and float(v.max()) <= K * ops
+
+
+@pytest.mark.parametrize("Q", [2, 4])
+def test_average_in_place_preserves_concurrent_updates(N, Q):
+    """K4 runs while another stream keeps adding +1 to every arena element.
+    The averaging corrections sum to exactly 0 over the workers (integer
+    values, Q a power of two: the mean and the corrections are exact), so
+    the sum over arenas must equal the initial sum plus every add — no
+    update that raced with the round is lost or double-counted."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, rounds, adds = 1 << 18, 20, 40
+    ars = [Arena(n, 0) for _ in range(Q)]
+    for q, a in enumerate(ars):
+        a.tensor.copy_(torch.randint(-1000, 1000, (n,), device="cuda").float())
+    before = sum(a.tensor.double().sum() for a in ars)
+    g = torch.full((n,), -1.0, device="cuda")
+    ws, avs = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for k in range(max(rounds, adds)):
+        if k < adds:
+            N.apply_sgd(ars[k % Q].ptr, g.data_ptr(), None, n, 1.0, None, 0.0, 0.0, N.MODE_RED,
+                        ws.cuda_stream)
+        if k < rounds:
+            N.average_shard([a.ptr for a in ars], 0, n, None, N.MODE_RED, avs.cuda_stream)
+    torch.cuda.synchronize()
+    after = sum(a.tensor.double().sum() for a in ars)
+    assert float(after - before) == float(adds * n)
