@@ -244,6 +244,78 @@ def flops_savings_ratio(obj: ArenaObjective, partition) -> float:
 
 
 # ---------------------------------------------------------------------------
+# desk-scale objectives of the reference (objectives.py:111-193): one flat
+# parameter tensor, blocks may split it anywhere (layer_param_counts = None)
+
+
+class _FlatObjective(ArenaObjective):
+    layer_param_counts = None
+
+    def _flat_init(self, features, labels):
+        self.features = torch.as_tensor(np.asarray(features), dtype=torch.float32)
+        self.labels = torch.as_tensor(np.asarray(labels))
+        self._feat_cache, self._lab_cache = {}, {}
+        self.n_samples = int(self.features.shape[0])
+        self.edges = (0, self.dim)
+
+    def tensors_of_block(self, block: Block) -> tuple[int, int]:
+        self.check_block(block)
+        return 0, 0          # the block is a range inside the single tensor
+
+    def init_params(self, seed: int) -> np.ndarray:
+        return np.zeros(self.dim)
+
+    def bind(self, arena: torch.Tensor, grad_arena: torch.Tensor | None) -> Bound:
+        w = arena.detach().requires_grad_(grad_arena is not None)
+        if grad_arena is not None:
+            w.grad = grad_arena
+        return Bound([w], lambda xb: xb)
+
+    def forward_cost(self) -> int:
+        return self.dim
+
+    def backward_cost(self, block: Block) -> int:
+        return self.dim
+
+
+class QuadraticObjective(_FlatObjective):
+    """f(x) = mean_n 0.5 ||x - t_n||^2 (objectives.py:111-145)."""
+
+    def __init__(self, targets):
+        t = np.asarray(targets, dtype=np.float64)
+        if t.ndim != 2 or t.shape[0] == 0:
+            raise ValueError("targets must be a non-empty (n, d) array")
+        self.dim = int(t.shape[1])
+        self.n_classes = 0
+        self._flat_init(t, np.zeros(t.shape[0], dtype=np.int64))
+        self.minimizer = t.mean(axis=0)
+
+    def loss_on(self, bound: Bound, xb: torch.Tensor, yb: torch.Tensor) -> torch.Tensor:
+        diff = bound.params[0].unsqueeze(0) - xb
+        return 0.5 * (diff * diff).sum(dim=1).mean()
+
+
+class LogisticObjective(_FlatObjective):
+    """Binary logistic loss over +-1 labels (objectives.py:152-193)."""
+
+    def __init__(self, features, labels):
+        f = np.asarray(features, dtype=np.float64)
+        lab = np.asarray(labels)
+        if f.ndim != 2 or f.shape[0] == 0:
+            raise ValueError("features must be a non-empty (n, f) array")
+        if set(np.unique(lab)) - {-1, 1}:
+            raise ValueError("labels must be +-1")
+        self.dim = int(f.shape[1])
+        self.n_classes = 2
+        self._flat_init(f, lab.astype(np.float64))
+        self.labels = self.labels.to(torch.float32)
+
+    def loss_on(self, bound: Bound, xb: torch.Tensor, yb: torch.Tensor) -> torch.Tensor:
+        margin = yb * (xb @ bound.params[0])
+        return F.softplus(-margin).mean()           # log(1 + exp(-margin))
+
+
+# ---------------------------------------------------------------------------
 # ResNets (CIFAR ResNet-20 / ResNet-18, ImageNet ResNet-50)
 
 

@@ -276,6 +276,16 @@ def main() -> None:
                                 workers=2, batch_base=8, boost=True),
         sync=rsched.SyncScheme(total=60, period=4), budget=60, t_st=6, B=8, seed=1,
         epoch_partition=True)
+    quad8 = robj.QuadraticObjective.from_dataset(rdata.make_linear_targets(32, 8, 1.0, 0.5, 3))
+    save_serialized(
+        "quad8_lpp", quad8, True, algo="lpp_sgd", Q=2, U=2, bounds=(0, 2, 4, 6, 8),
+        sched=rsched.constant_schedule(0.05, 50), sync=rsched.SyncScheme(total=50, period=4),
+        budget=50, t_st=8, B=8, seed=1)
+    logreg8 = robj.LogisticObjective.from_dataset(rdata.make_blobs(64, 8, 2, 3.0, 0.5, 5))
+    save_serialized(
+        "logreg8_lap", logreg8, True, algo="lap_sgd", Q=2, U=2, bounds=(0, 8),
+        sched=rsched.LrSchedule(kind="cosine", alpha0=0.1, total=60, warmup=6),
+        sync=rsched.SyncScheme(total=60, period=4), budget=60, t_st=0, B=8, seed=2)
     c0_bounds = rpart.balanced_boundaries(c0.layer_param_counts, 2)
     save_serialized(
         "c0_lpp", c0, False, algo="lpp_sgd", Q=2, U=2, bounds=c0_bounds,

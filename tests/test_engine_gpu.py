@@ -571,3 +571,27 @@ def test_updater_failure_aborts_the_run(quiescent):
         assert _t.perf_counter() - t0 < 60
     finally:
         setattr(async_engine._Engine, name, orig)
+
+
+@pytest.mark.parametrize("name", ["quad8_lpp", "logreg8_lap"])
+def test_serialized_flat_objectives_match_oracle(name):
+    """The reference's desk-scale objectives on the GPU engine; quad8 uses the
+    unlayered partition (0, 2, 4, 6, 8): partial updates that cut inside one
+    parameter tensor."""
+    from oracle import data as odata
+    from oracle import flat
+    from paper_2203_06638_b200.engine import run_experiment
+    from paper_2203_06638_b200.objectives import LogisticObjective, QuadraticObjective
+
+    if name == "quad8_lpp":
+        t = flat.make_linear_targets(32, 8, 1.0, 0.5, 3)
+        obj, orc_obj = QuadraticObjective(t), flat.QuadOracle(t)
+    else:
+        X, y = odata.make_blobs(64, 8, 2, 3.0, 0.5, 5)
+        obj, orc_obj = LogisticObjective(X, np.where(y == 1, 1, -1)), flat.LogisticOracle(X, y)
+    g, cfg = _cfg_from_golden(name, obj)
+    res = run_experiment(cfg)
+    got_blocks = sorted((u.worker, u.rank, u.s, u.block_id) for u in res.updates)
+    assert got_blocks == sorted(tuple(int(v) for v in row) for row in g["block_trace"])
+    assert np.array_equal(np.array(res.round_trace, dtype=np.int64), g["round_trace"])
+    np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
