@@ -154,6 +154,12 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 // L2-coherent loads for data other agents may be writing concurrently
+// release/acquire fences for the value -> tag message passing (K5).  The
+// pattern only needs acq_rel (MEMBAR.ALL), not sequential consistency
+// (MEMBAR.SC + L1 invalidate, which __threadfence() emits).
+__device__ __forceinline__ void fence_ar_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_ar_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ __forceinline__ float4 ld_cg4(const float* p) {
   return __ldcg(reinterpret_cast<const float4*>(p));
 }
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
     if (tags) {
-      __threadfence();
+      fence_ar_gpu();
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         size_t i = i0 + (size_t)u * stride;
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kThreads)
       else
         red_add_f32(x + e, d);
       if (tags) {
-        __threadfence();
+        fence_ar_gpu();
         st_tag(tags + e, stamp);
       }
     }
@@ -476,13 +482,11 @@ __device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, f
     float xv = WD ? ld_cg(x + e) : 0.f;
     float mv = MOM ? m[e] : 0.f;
     float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
-    if (MOM) m[e] = mv;
     float old = atom_add_f32(x + e, d);
+    if (tags) fence_ar_gpu();
+    if (MOM) m[e] = mv;
     rep[e] = __fadd_rn(old, d);
-    if (tags) {
-      __threadfence();
-      st_tag(tags + e, stamp);
-    }
+    if (tags) st_tag(tags + e, stamp);
   } else {
     rep[e] = ld_cg(x + e);
   }
@@ -511,18 +515,18 @@ __global__ void __launch_bounds__(kThreads)
       d.y = sgd_delta<WD, MOM>(gv.y, xv.y, mv.y, lr, mu, wd);
       d.z = sgd_delta<WD, MOM>(gv.z, xv.z, mv.z, lr, mu, wd);
       d.w = sgd_delta<WD, MOM>(gv.w, xv.w, mv.w, lr, mu, wd);
-      if (MOM) reinterpret_cast<float4*>(m)[i] = mv;
       float4 old = atom_add_v4(x + e0, d);
+      // the fence sits between the (returning) value atomic and every later
+      // store, so it only waits for the atomic the replica needs anyway
+      if (tags) fence_ar_gpu();
+      if (MOM) reinterpret_cast<float4*>(m)[i] = mv;
       float4 nv;
       nv.x = __fadd_rn(old.x, d.x);
       nv.y = __fadd_rn(old.y, d.y);
       nv.z = __fadd_rn(old.z, d.z);
       nv.w = __fadd_rn(old.w, d.w);
       reinterpret_cast<float4*>(rep)[i] = nv;
-      if (tags) {
-        __threadfence();
-        st_tag4(tags + e0, stamp);
-      }
+      if (tags) st_tag4(tags + e0, stamp);
     } else if (e0 + 4 <= lo || e0 >= hi) {
       reinterpret_cast<float4*>(rep)[i] = ld_cg4(x + e0);
     } else {
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(kThreads)
       red_add_v4(d + head + 4 * i, v);
     }
     if (tags) {
-      __threadfence();
+      fence_ar_gpu();
       st_tag4(tags + head + 4 * i, stamp);
     }
   }
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(kThreads)
       else
         red_add_f32(d + e, v);
       if (tags) {
-        __threadfence();
+        fence_ar_gpu();
         st_tag(tags + e, stamp);
       }
     }
@@ -722,7 +726,7 @@ __global__ void __launch_bounds__(kThreads)
       size_t i = i0 + (size_t)u * stride;
       if (i < nvec) t[u] = ld_tag4(tags + head + 4 * i);
     }
-    __threadfence();
+    fence_ar_gpu();
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       size_t i = i0 + (size_t)u * stride;
@@ -744,7 +748,7 @@ __global__ void __launch_bounds__(kThreads)
     for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
       size_t e = k < head ? k : tail0 + (k - head);
       int tv = ld_tag(tags + e);
-      __threadfence();
+      fence_ar_gpu();
       float v = ld_cg(src + e);
       if (out) out[e] = v;
       if (out_tags) out_tags[e] = tv;
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
     if (TAGGED) {
-      __threadfence_system();
+      fence_ar_sys();
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         size_t i = i0 + (size_t)u * stride;
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(kThreads)
       }
       if (mean_out) mean_out[e] = mean;
       if (TAGGED) {
-        __threadfence_system();
+        fence_ar_sys();
 #pragma unroll
         for (int q = 0; q < LPP_MAX_WORKERS; ++q)
           if (q < Q) st_tag_sys(t.tag[q] + lo + e, t.stamp[q]);
@@ -1511,7 +1515,7 @@ __global__ void __launch_bounds__(kThreads)
     c.w = __fsub_rn(m.w, s.w);
     red_add_v4(x + 4 * i, c);
     if (tags) {
-      __threadfence();
+      fence_ar_gpu();
       st_tag4(tags + 4 * i, stamp);
     }
   }
@@ -1519,7 +1523,7 @@ __global__ void __launch_bounds__(kThreads)
     for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x) {
       red_add_f32(x + e, __fsub_rn(ld_cg(mean + e), ld_cg(stage + e)));
       if (tags) {
-        __threadfence();
+        fence_ar_gpu();
         st_tag(tags + e, stamp);
       }
     }
