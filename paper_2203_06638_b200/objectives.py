@@ -10,7 +10,8 @@ the engine's captured CUDA-graph steps run (``bind`` / ``loss_on``).
 * ``MlpObjective`` — the reference MLP (``objectives.py:200-319``) with the
   reference flat layout ``[W1, b1, ...]``, ``W_l`` of shape (in, out),
   ``z = a @ W + b``; used for the deterministic parity gate.
-* ``ResNetObjective`` — CIFAR ResNet-20 (d=272,474, 65 tensors), CIFAR
+* ``ResNetObjective`` — the small CNN of BASELINE config 0 (``smallcnn``),
+  CIFAR ResNet-20 (d=272,474, 65 tensors), CIFAR
   ResNet-18 (d=11,220,132, 62 tensors), ImageNet ResNet-50 (d=25,557,032,
   161 tensors) on synthetic data.  The CNN
   forward/backward stays in PyTorch, as in the paper; partial
@@ -433,7 +434,26 @@ class ResNet50(nn.Module):
         return self.fc(out)
 
 
+class SmallCnn(nn.Module):
+    """The "small CNN" of BASELINE config 0 (the reference's CPU-runnable
+    case): conv 3->16 s2 -> tanh -> conv 16->32 s2 -> tanh -> 2x2 average
+    pool -> linear 512->10; 6 tensors, 10,218 parameters.  Smooth (tanh,
+    average pooling) so fp32-vs-fp64 parity has no kink flips."""
+
+    def __init__(self, num_classes=10):
+        super().__init__()
+        self.conv1 = nn.Conv2d(3, 16, 3, stride=2, padding=1)
+        self.conv2 = nn.Conv2d(16, 32, 3, stride=2, padding=1)
+        self.fc = nn.Linear(32 * 4 * 4, num_classes)
+
+    def forward(self, x):
+        x = torch.tanh(self.conv1(x))
+        x = torch.tanh(self.conv2(x))
+        return self.fc(F.avg_pool2d(x, 2).flatten(1))
+
+
 _ARCHS = {
+    "smallcnn": (SmallCnn, (3, 32, 32), 10),
     "resnet20": (CifarResNet20, (3, 32, 32), 10),
     "resnet18": (CifarResNet18, (3, 32, 32), 100),
     "resnet50": (ResNet50, (3, 224, 224), 1000),

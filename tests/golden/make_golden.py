@@ -293,6 +293,46 @@ def main() -> None:
                                 workers=2, batch_base=32),
         sync=rsched.SyncScheme(total=200, period=16), budget=200, t_st=20, B=32, seed=1)
 
+    # ---------------- BASELINE config 0: a small CNN in the reference's Objective protocol ----------------
+    sys.path.insert(0, str(HERE.parents[1]))
+    from oracle.cnn import SmallCnnOracle, make_images
+
+    class RefCnn(robj.Objective):
+        """The small CNN (oracle/cnn.py network math) plugged into the
+        reference's Objective ABC, so the reference's own schedule primitives
+        and engine drive it."""
+
+        def __init__(self, o):
+            self.o, self.dim, self.n_samples = o, o.dim, o.n_samples
+            self.layer_param_counts = o.layer_param_counts
+
+        def loss(self, x, batch):
+            return self.o.loss(x, batch)
+
+        def init_params(self, seed):
+            return self.o.init_params(seed)
+
+        def grad_block(self, x, block, batch):
+            self.check_block(block)
+            v = self.o.grad_block(x, block.start, block.stop, batch)
+            return robj.GradResult(v, 0, 0, len(batch))
+
+    cnn = RefCnn(SmallCnnOracle(*make_images(256, 3)))
+    save_serialized(
+        "cnn_lpp", cnn, True, algo="lpp_sgd", Q=2, U=2,
+        bounds=rpart.balanced_boundaries(cnn.layer_param_counts, 2),
+        sched=rsched.LrSchedule(kind="cosine", alpha0=0.05, total=40, warmup=4, batch_local=16,
+                                workers=2, batch_base=16),
+        sync=rsched.SyncScheme(total=40, period=4), budget=40, t_st=4, B=16, seed=1)
+    cfg = rengine.RunConfig(
+        algo="lap_sgd", objective=cnn, partition=rpart.make_partition(cnn.dim, (0, cnn.dim)),
+        lr=rsched.constant_schedule(0.05, 30), sync=rsched.SyncScheme(total=30, period=4, switch_point=0),
+        budget=30, warm_start_budget=0, workers=1, updaters=1, batch_size=16, seed=2,
+        record_mode="full", quiescent=True)
+    res = rengine.run_experiment(cfg)
+    np.savez_compressed(HERE / "engine_cnn_q1u1.npz", final=res.final_values, x0=res.x0,
+                        counter_finals=np.array(res.counter_finals))
+
     # ---------------- the reference engine itself: Q=1, U=1, quiescent, full ----------------
     sched = rsched.constant_schedule(0.05, 50)
     cfg = rengine.RunConfig(

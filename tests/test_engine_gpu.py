@@ -595,3 +595,41 @@ def test_serialized_flat_objectives_match_oracle(name):
     assert got_blocks == sorted(tuple(int(v) for v in row) for row in g["block_trace"])
     assert np.array_equal(np.array(res.round_trace, dtype=np.int64), g["round_trace"])
     np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
+
+
+def _smallcnn():
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    return ResNetObjective("smallcnn", n_samples=256, seed=3, channels_last=False, autocast=None,
+                           data="host")
+
+
+def test_serialized_small_cnn_matches_oracle():
+    """BASELINE config 0 on the GPU engine: small CNN, Q=2 x U=2, 2-block
+    partial backprop, fp32 cuDNN (TF32 off) vs the fp64 reference-driven run."""
+    from paper_2203_06638_b200.engine import run_experiment
+
+    g, cfg = _cfg_from_golden("cnn_lpp", _smallcnn())
+    res = run_experiment(cfg)
+    got_blocks = sorted((u.worker, u.rank, u.s, u.block_id) for u in res.updates)
+    assert got_blocks == sorted(tuple(int(v) for v in row) for row in g["block_trace"])
+    assert np.array_equal(np.array(res.round_trace, dtype=np.int64), g["round_trace"])
+    np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
+
+
+def test_small_cnn_q1u1_matches_reference_engine_run():
+    """The reference's own engine driving the small CNN (engine_cnn_q1u1.npz)."""
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import SyncScheme, constant_schedule
+
+    obj = _smallcnn()
+    g = load_npz("engine_cnn_q1u1.npz")
+    cfg = RunConfig(algo="lap_sgd", objective=obj, partition=make_partition(obj.dim, (0, obj.dim)),
+                    lr=constant_schedule(0.05, 30), sync=SyncScheme(total=30, period=4, switch_point=0),
+                    budget=30, warm_start_budget=0, workers=1, updaters=1, batch_size=16, seed=2,
+                    schedule="serialized", record_mode="full", evaluate=False)
+    res = run_experiment(cfg)
+    np.testing.assert_allclose(res.x0, g["x0"])
+    np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
+    assert res.counter_finals == list(g["counter_finals"])

@@ -60,3 +60,18 @@ def test_resnet_arena_sizes(arch, dim, tensors):
     part = make_partition(obj.dim, balanced_boundaries(obj.layer_param_counts, 4))
     r = flops_savings_ratio(obj, part)
     assert 0.0 < r < 0.75          # at most (U-1)/U
+
+
+def test_smallcnn_objective_matches_oracle_layout_data_and_init():
+    """The product's config-0 CNN shares the oracle's flat layout, synthetic
+    data stream and init (so GPU parity compares like with like)."""
+    from oracle.cnn import LAYER_COUNTS, SmallCnnOracle, make_images
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("smallcnn", n_samples=64, seed=3, channels_last=False, autocast=None,
+                          data="host")
+    X, y = make_images(64, 3)
+    assert obj.layer_param_counts == LAYER_COUNTS and obj.dim == 10218
+    assert np.array_equal(obj.features.double().numpy(), X)
+    assert np.array_equal(obj.labels.numpy(), y)
+    assert np.array_equal(obj.init_params(5), SmallCnnOracle(X, y).init_params(5))
