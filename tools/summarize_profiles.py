@@ -50,9 +50,33 @@ def kernel_table(rep):
     return "\n".join(out)
 
 
+def traffic_json(rep):
+    """Per-launch duration and DRAM bytes (read + write) -> the JSON bench.py
+    reads for roofline.traffic."""
+    import json
+
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    col = {w: hdr.index(w) for w in ("Kernel Name", "launch__grid_size", "gpu__time_duration.sum",
+                                      "dram__bytes_read.sum", "dram__bytes_write.sum")}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
+    out = []
+    for r in rows[2:]:
+        by = sum(float(r[col[k]]) * scale[units[col[k]]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        us = float(r[col["gpu__time_duration.sum"]]) * tscale[units[col["gpu__time_duration.sum"]]]
+        out.append({"kernel": r[col["Kernel Name"]].split("(")[0], "grid": int(r[col["launch__grid_size"]]),
+                    "us": us, "dram_bytes": by})
+    return json.dumps({"source": "ncu --set full, tools/profile_kernels.py (L2 flushed before each launch)",
+                       "launches": out}, indent=1)
+
+
 if __name__ == "__main__":
     kind, src = sys.argv[1], sys.argv[2]
     if kind == "launches":
         print(launch_share(src, last=int(sys.argv[3]) if len(sys.argv) > 3 else None))
+    elif kind == "traffic":
+        print(traffic_json(src))
     else:
         print(kernel_table(src))
