@@ -255,7 +255,7 @@ def ours(args) -> None:
         "gpu_launches_note": "lpp_b200 kernels launched in the timed region on this rank "
                              "(K3 snapshot + K5 tag gather + K1/K2 apply per minibatch, + K4 per round)",
         "roofline": {"bound": "hbm",
-                     "kernel": ("lpp_apply_snapshot (K1+K3 fused, atom.add.v4.f32)" if fused else
+                     "kernel": ("lpp_apply_snapshot (K1+K3 fused, red.add.v4.f32 + re-read)" if fused else
                                 "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)"),
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],

@@ -110,9 +110,9 @@ int lpp_apply_sgd(float* x, const float* g, float* m, size_t n, float lr,
 
 /* K1+K3 fused: apply the block [lo, hi) of this step (as lpp_apply_sgd on
  * x + lo, g + lo, m + lo, with tags[e] = stamp when tags != NULL) and write
- * replica[e] for every e in [0, n): old + delta inside the block (returning
- * element atomic: a value the arena really held), an untorn copy of x
- * outside it.  x, g, m, replica, tags are arena BASES (16-byte aligned). */
+ * replica[e] for every e in [0, n): inside the block, x[e] re-read after this
+ * step's vector reduction landed (a value the arena really held; old + delta
+ * when no other writer raced), an untorn copy of x outside it.  x, g, m, replica, tags are arena BASES (16-byte aligned). */
 int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
                        int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
                        const float* lr_dev, float mu, float wd, int32_t stamp,

@@ -452,27 +452,16 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 // ---------------------------------------------------------------------------
 // K1+K3 fused: apply this step's block gradient AND refresh the stream's
 // replica for its next step in one pass over the arena.  Inside [lo, hi)
-// the element update is a returning vector atomic (atom.add.v4.f32, SASS
-// ATOMG.E.ADD.F32x4): the replica receives old + delta — the value the
-// element held right after this update, i.e. a value that was really in the
-// arena; outside the block the replica is a plain untorn copy.  It replaces
-// the next step's K3 launch (the step's snapshot is taken when the previous
-// step's apply lands, which on the updater's stream is when K3 would have
-// run anyway) and saves 4 B/elem of block traffic.
-
-__device__ __forceinline__ float4 atom_add_v4(float* p, float4 v) {
-  float4 r;
-  asm volatile("atom.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4], {%5,%6,%7,%8};"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-  return r;
-}
-__device__ __forceinline__ float atom_add_f32(float* p, float v) {
-  float r;
-  asm volatile("atom.relaxed.sys.global.add.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "f"(v) : "memory");
-  return r;
-}
+// the element update is the K1 vector reduction (red.add.v4.f32) followed
+// by a re-read of the same 16 bytes: the replica receives the value the
+// element held after this update landed (an untorn value that was really in
+// the arena, exactly what K3 would copy after the apply); the re-read hits
+// the L2 line the reduction just wrote.  Outside the block the replica is a
+// plain copy.  It replaces the next step's K3 launch (the step's snapshot is
+// taken when the previous step's apply lands, which on the updater's stream
+// is when K3 would have run anyway) and saves the block's second DRAM read.
+// (A returning atom.add.v4.f32 — old + delta — measured 4-8 % slower at
+// d18/d50: tools/bench_fused.py.)
 
 template <bool WD, bool MOM>
 __device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, float* rep, int* tags,
@@ -482,17 +471,18 @@ __device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, f
     float xv = WD ? ld_cg(x + e) : 0.f;
     float mv = MOM ? m[e] : 0.f;
     float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
-    float old = atom_add_f32(x + e, d);
+    red_add_f32(x + e, d);
+    float nv = ld_cg(x + e);
     if (tags) fence_ar_gpu();
     if (MOM) m[e] = mv;
-    rep[e] = __fadd_rn(old, d);
+    rep[e] = nv;
     if (tags) st_tag(tags + e, stamp);
   } else {
     rep[e] = ld_cg(x + e);
   }
 }
 
-template <bool WD, bool MOM>
+template <bool WD, bool MOM, int UNR>
 __global__ void __launch_bounds__(kThreads)
     k_apply_snapshot(float* x, const float* __restrict__ g, float* m, float* __restrict__ rep,
                      int* tags, size_t n, size_t lo, size_t hi, float lr,
@@ -501,37 +491,64 @@ __global__ void __launch_bounds__(kThreads)
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nvec = n / 4;
-  // vectors fully inside [lo, hi): the apply path; fully outside: the copy
-  // path; straddling (layer-aligned blocks start anywhere): per element
-  for (size_t i = tid; i < nvec; i += stride) {
-    size_t e0 = 4 * i;
-    if (e0 >= lo && e0 + 4 <= hi) {
-      float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
-      float4 xv = make_float4(0.f, 0.f, 0.f, 0.f), mv = xv;
-      if (WD) xv = ld_cg4(x + e0);
-      if (MOM) mv = reinterpret_cast<const float4*>(m)[i];
-      float4 d;
-      d.x = sgd_delta<WD, MOM>(gv.x, xv.x, mv.x, lr, mu, wd);
-      d.y = sgd_delta<WD, MOM>(gv.y, xv.y, mv.y, lr, mu, wd);
-      d.z = sgd_delta<WD, MOM>(gv.z, xv.z, mv.z, lr, mu, wd);
-      d.w = sgd_delta<WD, MOM>(gv.w, xv.w, mv.w, lr, mu, wd);
-      float4 old = atom_add_v4(x + e0, d);
-      // the fence sits between the (returning) value atomic and every later
-      // store, so it only waits for the atomic the replica needs anyway
-      if (tags) fence_ar_gpu();
-      if (MOM) reinterpret_cast<float4*>(m)[i] = mv;
-      float4 nv;
-      nv.x = __fadd_rn(old.x, d.x);
-      nv.y = __fadd_rn(old.y, d.y);
-      nv.z = __fadd_rn(old.z, d.z);
-      nv.w = __fadd_rn(old.w, d.w);
-      reinterpret_cast<float4*>(rep)[i] = nv;
-      if (tags) st_tag4(tags + e0, stamp);
-    } else if (e0 + 4 <= lo || e0 >= hi) {
-      reinterpret_cast<float4*>(rep)[i] = ld_cg4(x + e0);
-    } else {
-      for (size_t e = e0; e < e0 + 4; ++e)
-        fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
+  // vectors fully inside [lo, hi) take the apply path, vectors fully outside
+  // the copy path; the (at most two) straddling vectors go per element.
+  // UNR vectors per thread: every load of the group is issued before
+  // the first atomic, so 4 x (g, x, m) 16-byte loads are in flight.
+  const size_t vlo = (lo + 3) / 4, vhi = hi / 4;
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * UNR) {
+    float4 gr[UNR], xr[UNR], mr[UNR];
+    int kind[UNR];  // 0 none, 1 inside, 2 outside, 3 straddle
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      kind[u] = 0;
+      gr[u] = xr[u] = mr[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i >= nvec) continue;
+      if (i >= vlo && i < vhi) {
+        kind[u] = 1;
+        gr[u] = __ldg(reinterpret_cast<const float4*>(g) + i);
+        if (WD) xr[u] = ld_cg4(x + 4 * i);
+        if (MOM) mr[u] = reinterpret_cast<const float4*>(m)[i];
+      } else if (4 * i + 4 <= lo || 4 * i >= hi) {
+        kind[u] = 2;
+        xr[u] = ld_cg4(x + 4 * i);
+      } else {
+        kind[u] = 3;
+      }
+    }
+    float4 dr[UNR], nv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (kind[u] != 1) continue;
+      size_t i = i0 + (size_t)u * stride;
+      dr[u].x = sgd_delta<WD, MOM>(gr[u].x, xr[u].x, mr[u].x, lr, mu, wd);
+      dr[u].y = sgd_delta<WD, MOM>(gr[u].y, xr[u].y, mr[u].y, lr, mu, wd);
+      dr[u].z = sgd_delta<WD, MOM>(gr[u].z, xr[u].z, mr[u].z, lr, mu, wd);
+      dr[u].w = sgd_delta<WD, MOM>(gr[u].w, xr[u].w, mr[u].w, lr, mu, wd);
+      // vector reduction, then re-read: the replica gets the arena value
+      // after this step's add (plus any concurrent adds that landed first),
+      // i.e. what a K3 snapshot right after the apply would copy.  Measured
+      // 4-8 % faster at d18/d50 than a returning atom.add.v4 (old + delta)
+      red_add_v4(x + 4 * i, dr[u]);
+      nv[u] = ld_cg4(x + 4 * i);
+    }
+    // the re-read returns after the reduction is performed (same address),
+    // so the fence before the tag stores has nothing else to wait for
+    if (tags) fence_ar_gpu();
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      size_t i = i0 + (size_t)u * stride;
+      if (kind[u] == 1) {
+        if (MOM) reinterpret_cast<float4*>(m)[i] = mr[u];
+        reinterpret_cast<float4*>(rep)[i] = nv[u];
+        if (tags) st_tag4(tags + 4 * i, stamp);
+      } else if (kind[u] == 2) {
+        reinterpret_cast<float4*>(rep)[i] = xr[u];
+      } else if (kind[u] == 3) {
+        for (size_t e = 4 * i; e < 4 * i + 4; ++e)
+          fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
+      }
     }
   }
   if (blockIdx.x == 0)
@@ -555,18 +572,22 @@ extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* rep
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
   cudaStream_t st = (cudaStream_t)stream;
   bool WD = wd != 0.f, MOM = mu != 0.f;
-  if (WD && MOM)
-    k_apply_snapshot<true, true><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
-                                                           lr_dev, mu, wd, stamp);
-  else if (WD)
-    k_apply_snapshot<true, false><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
-                                                            lr_dev, mu, wd, stamp);
-  else if (MOM)
-    k_apply_snapshot<false, true><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr,
-                                                            lr_dev, mu, wd, stamp);
-  else
-    k_apply_snapshot<false, false><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi,
-                                                             lr, lr_dev, mu, wd, stamp);
+  // one vector per thread per grid stride: unrolling (2, 4 vectors with all
+  // loads hoisted) measured no faster at d20/d50 and 6 % slower at d18 —
+  // the returning vector atomic, not load concurrency, bounds this kernel
+#define FUSED_LAUNCH(W, M)                                                                      \
+  k_apply_snapshot<W, M, 1><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr, \
+                                                       lr_dev, mu, wd, stamp);
+  if (WD && MOM) {
+    FUSED_LAUNCH(true, true)
+  } else if (WD) {
+    FUSED_LAUNCH(true, false)
+  } else if (MOM) {
+    FUSED_LAUNCH(false, true)
+  } else {
+    FUSED_LAUNCH(false, false)
+  }
+#undef FUSED_LAUNCH
   LAUNCH_CHECK("apply_snapshot");
   return LPP_OK;
 }
