@@ -209,6 +209,7 @@ def ours(args) -> None:
     cfg = build_cfg(obj, (K + W) * U, workers=ws)
     tr = Trainer(cfg, group=group, time_apply=True)
     fused = tr.eng.fused()
+    tr_native = tr.eng.native_loop()
     tr.run(W * U, evaluate=False)
     barrier()
     if os.environ.get("LPP_NVTX"):
@@ -249,7 +250,8 @@ def ours(args) -> None:
                    "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
                    "conv_compute": "bf16 autocast (arena, grads, apply, averaging in fp32)",
                    "l2": "inputs larger than L2 (614 MB dataset gathered per step)",
-                   "sampling": "in-graph device RNG", "momentum": 0.9, "weight_decay": 5e-4,
+                   "sampling": "in-graph device RNG", "host_loop": "native" if tr_native else "python",
+                   "momentum": 0.9, "weight_decay": 5e-4,
                    "write_tags": cfg.tracks},
         "gpu_launches": launches,
         "gpu_launches_note": "lpp_b200 kernels launched in the timed region on this rank "

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define LPP_ABI_VERSION 1
+#define LPP_ABI_VERSION 2
 
 /* error codes */
 #define LPP_OK 0
@@ -229,6 +229,97 @@ int lpp_graph_launch(void* graph_exec, void* stream);
 int lpp_l2_flush(void* scratch, size_t n_bytes, void* stream);
 /* number of SMs of `device` */
 int lpp_sm_count(int device, int* out);
+
+/* ------------------------------------------------------------------ */
+/* Native updater loop (a10: _updater_loop / _updater_body,
+ * engine.py:289-383) and its pure helpers.
+ *
+ * lpp_lr_at: lr_at (schedules.py:56-68), bit-identical to the Python
+ * restatement (same IEEE operation order, libm cos/pow): kind 0 = cosine,
+ * 1 = multistep.  lpp_select_block: select_block (partition.py:132-145),
+ * returns the block id, or LPP_E_VALUE for a rank outside [1, num_blocks]. */
+double lpp_lr_at(int kind, double alpha0, double peak, int64_t warmup, int64_t total,
+                 const int64_t* milestones, int n_milestones, double gamma, int64_t s);
+int lpp_select_block(int64_t s, int64_t warm_start, int num_blocks, int rank);
+
+/* Device-side uniform batch sampling for captured steps: idx[i] =
+ * floor(h(key, step, i) * n / 2^64) for i in [0, batch), h a splitmix64
+ * chain, step read from the device counter *step which the kernel then
+ * increments — so a CUDA graph that captured this launch draws a fresh
+ * batch on every replay with no host involvement.  The host twin computes
+ * the same indices for a given step (tests). */
+int lpp_sample_indices(int64_t* idx, int64_t* step, int32_t batch, int64_t n, uint64_t key,
+                       void* stream);
+int lpp_sample_indices_host(int64_t* out, int32_t batch, int64_t n, uint64_t key, int64_t step);
+
+/* One updater's whole asynchronous loop in native code (GIL-free): claim
+ * s = C^q++ (host cell), lr = lr_at(s), b = select_block(s, ...), u = the
+ * write stamp, then on the updater's stream
+ *   [sampled tags: H2D of k sorted distinct indices, K5 gather, D2H]
+ *   K3 snapshot (or, fused, only before the first step)
+ *   cudaGraphLaunch(graph_exec[b])          -- the captured fwd/bwd
+ *   K1/K2 apply (+K5 tags) or the fused K1+K3 apply_snapshot
+ * with in_flight steps outstanding (an event per slot); a step's sampled
+ * tags are classified clean iff all >= the averaging stamp read at claim
+ * time (engine.py:357-362) once its event completed.  Stops at the claim
+ * rule of engine.py:336 (each updater processes exactly one slot >= budget)
+ * or when *stop becomes non-zero.  Pointers to host int64 cells are shared
+ * with the averager thread (host atomics K6). */
+typedef struct {
+  int64_t* sample_counter;        /* C^q (read_and_inc) */
+  int64_t* update_order;          /* write stamps: u = fetch_add + 1 */
+  const int64_t* stop;            /* non-zero: stop claiming */
+  const int64_t* last_avg_stamp;  /* k_claim */
+  int64_t budget;
+  /* lr_at */
+  int32_t lr_kind;
+  int32_t n_milestones;
+  double alpha0, peak, gamma;
+  int64_t warmup, total;
+  const int64_t* milestones;
+  /* select_block */
+  int32_t lpp;                    /* 1: lpp_sgd block rule, 0: always block 0 */
+  int32_t num_blocks;
+  int32_t rank;                   /* 1-based */
+  int32_t fused;                  /* 1: K1+K3 fused apply_snapshot */
+  int64_t warm_start;
+  const int64_t* block_lo;        /* [num_blocks + 1] element ranges per block id */
+  const int64_t* block_hi;
+  void* const* graph_exec;        /* cudaGraphExec_t per block id */
+  const int64_t* flops_of;        /* per block id */
+  /* arenas (bases) */
+  float* x;
+  float* g;
+  float* m;                       /* NULL without momentum */
+  float* replica;
+  int32_t* tags;                  /* NULL: no write tags */
+  size_t n;
+  float mu, wd;
+  int32_t apply_mode;
+  int32_t in_flight;
+  /* sampled tags (K5); ignored when tags == NULL or tag_pick == 0 */
+  int32_t tag_pick;
+  int32_t time_apply;             /* 1: CUDA events around every apply */
+  uint64_t tag_seed;
+  int64_t* tag_idx_pinned;        /* [in_flight + 2][tag_pick] */
+  int64_t* tag_idx_dev;           /* [tag_pick] */
+  int32_t* tag_out_dev;           /* [in_flight + 2][tag_pick] */
+  int32_t* tag_out_pinned;        /* [in_flight + 2][tag_pick] */
+  int64_t* classified;            /* host counters (+= per classified step) */
+  int64_t* clean;
+  double apply_bytes_per_elem;    /* algorithmic bytes per block element */
+  void* stream;
+} lpp_updater_cfg;
+
+typedef struct {
+  int64_t steps;                  /* minibatches processed */
+  int64_t flops;                  /* sum of flops_of over the steps */
+  int64_t apply_launches;         /* timed applies (time_apply) */
+  double apply_ms;                /* summed CUDA-event time of the applies */
+  double apply_bytes;             /* summed algorithmic bytes of the applies */
+} lpp_updater_stats;
+
+int lpp_updater_run(const lpp_updater_cfg* cfg, lpp_updater_stats* stats);
 
 #ifdef __cplusplus
 }

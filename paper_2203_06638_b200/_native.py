@@ -48,6 +48,35 @@ _size = _c.c_size_t
 _vp = _c.c_void_p
 _i64p = _c.POINTER(_c.c_int64)
 
+class UpdaterCfg(ctypes.Structure):
+    """``lpp_updater_cfg`` (include/lpp_b200.h), field for field."""
+
+    _fields_ = [
+        ("sample_counter", _vp), ("update_order", _vp), ("stop", _vp), ("last_avg_stamp", _vp),
+        ("budget", _c.c_int64),
+        ("lr_kind", _c.c_int32), ("n_milestones", _c.c_int32),
+        ("alpha0", _c.c_double), ("peak", _c.c_double), ("gamma", _c.c_double),
+        ("warmup", _c.c_int64), ("total", _c.c_int64), ("milestones", _vp),
+        ("lpp", _c.c_int32), ("num_blocks", _c.c_int32), ("rank", _c.c_int32),
+        ("fused", _c.c_int32), ("warm_start", _c.c_int64),
+        ("block_lo", _vp), ("block_hi", _vp), ("graph_exec", _vp), ("flops_of", _vp),
+        ("x", _vp), ("g", _vp), ("m", _vp), ("replica", _vp), ("tags", _vp), ("n", _size),
+        ("mu", _c.c_float), ("wd", _c.c_float), ("apply_mode", _c.c_int32),
+        ("in_flight", _c.c_int32),
+        ("tag_pick", _c.c_int32), ("time_apply", _c.c_int32), ("tag_seed", _c.c_uint64),
+        ("tag_idx_pinned", _vp), ("tag_idx_dev", _vp), ("tag_out_dev", _vp),
+        ("tag_out_pinned", _vp), ("classified", _vp), ("clean", _vp),
+        ("apply_bytes_per_elem", _c.c_double), ("stream", _vp),
+    ]
+
+
+class UpdaterStats(ctypes.Structure):
+    """``lpp_updater_stats``."""
+
+    _fields_ = [("steps", _c.c_int64), ("flops", _c.c_int64), ("apply_launches", _c.c_int64),
+                ("apply_ms", _c.c_double), ("apply_bytes", _c.c_double)]
+
+
 _SIGS = {
     "lpp_abi_version": (_c.c_int, []),
     "lpp_last_error": (_c.c_char_p, []),
@@ -115,6 +144,12 @@ _SIGS = {
     "lpp_graph_launch": (_c.c_int, [_vp, _vp]),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
+    "lpp_lr_at": (_c.c_double, [_c.c_int, _c.c_double, _c.c_double, _c.c_int64, _c.c_int64, _vp,
+                                _c.c_int, _c.c_double, _c.c_int64]),
+    "lpp_select_block": (_c.c_int, [_c.c_int64, _c.c_int64, _c.c_int, _c.c_int]),
+    "lpp_sample_indices": (_c.c_int, [_vp, _vp, _c.c_int32, _c.c_int64, _c.c_uint64, _vp]),
+    "lpp_sample_indices_host": (_c.c_int, [_vp, _c.c_int32, _c.c_int64, _c.c_uint64, _c.c_int64]),
+    "lpp_updater_run": (_c.c_int, [_c.POINTER(UpdaterCfg), _c.POINTER(UpdaterStats)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -275,3 +310,40 @@ def copy_async(dst_ptr: int, src_ptr: int, nbytes: int, stream: int) -> None:
 
 def l2_flush(ptr: int, nbytes: int, stream: int) -> None:
     check(lib.lpp_l2_flush(ptr, nbytes, stream), "l2_flush")
+
+
+# -- native updater loop helpers ---------------------------------------------
+
+
+def lr_at_native(sched, s: int) -> float:
+    """``lpp_lr_at`` for an ``LrSchedule`` (the native loop's lr)."""
+    ms = np.ascontiguousarray(sched.milestones, dtype=np.int64)
+    return float(lib.lpp_lr_at(0 if sched.kind == "cosine" else 1, sched.alpha0, sched.peak,
+                               sched.warmup, sched.total, ms.ctypes.data if len(ms) else None,
+                               len(ms), sched.gamma, int(s)))
+
+
+def select_block_native(s: int, warm_start: int, num_blocks: int, rank: int) -> int:
+    b = int(lib.lpp_select_block(int(s), int(warm_start), int(num_blocks), int(rank)))
+    if b < 0:
+        raise ValueError(last_error())
+    return b
+
+
+def sample_indices(idx_ptr: int, step_ptr: int, batch: int, n: int, key: int, stream: int) -> None:
+    check(lib.lpp_sample_indices(idx_ptr, step_ptr, batch, n, key & (2**64 - 1), stream),
+          "sample_indices")
+
+
+def sample_indices_host(batch: int, n: int, key: int, step: int) -> np.ndarray:
+    out = np.zeros(batch, dtype=np.int64)
+    check(lib.lpp_sample_indices_host(out.ctypes.data, batch, n, key & (2**64 - 1), step),
+          "sample_indices_host")
+    return out
+
+
+def updater_run(cfg: UpdaterCfg) -> UpdaterStats:
+    """Run one updater's loop natively (ctypes drops the GIL for the call)."""
+    st = UpdaterStats()
+    check(lib.lpp_updater_run(ctypes.byref(cfg), ctypes.byref(st)), "updater_run")
+    return st

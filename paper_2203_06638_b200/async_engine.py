@@ -10,6 +10,7 @@ deterministic interleaving used as the parity mode.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 import time
 
@@ -257,6 +258,8 @@ class _Engine:
         self.errors: list[BaseException] = []
         self.err_lock = threading.Lock()
         self.apply_events: list = []
+        self.native_apply = [0, 0.0, 0.0]   # launches, ms, bytes (native loop, time_apply)
+        self.native_lock = threading.Lock()
         self.t0 = 0.0
         self.budget = cfg.budget
         self.read_loss = False
@@ -297,6 +300,7 @@ class _Engine:
         self.stamps = [[] for _ in range(self.cfg.workers)]
         self.errors = []
         self.apply_events = []
+        self.native_apply = [0, 0.0, 0.0]
         self.loss_log = []
         self.eval_points = []
 
@@ -556,6 +560,104 @@ class _Engine:
 
     # -- asynchronous threads -------------------------------------------------
 
+    def native_loop(self) -> bool:
+        """Whether updaters run the C++ loop (lpp_updater_run): the
+        throughput configuration — async, device sampling, no per-update
+        records, no host batches / loss read-back / quiescent pauses."""
+        cfg = self.cfg
+        ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
+              and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs
+              and not self.host_batches and not self.read_loss and not cfg.apply_priority)
+        if cfg.host_loop == "native" and not ok:
+            raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
+                             "sampling='device', CUDA graphs, no host batches / loss read-back / "
+                             "quiescent / apply_priority")
+        return ok and cfg.host_loop != "python"
+
+    def updater_cfg(self, w: _Worker, r: int) -> tuple:
+        """The ``lpp_updater_cfg`` of updater r of worker w (+ the arrays it
+        points into, which the caller keeps alive for the run)."""
+        cfg = self.cfg
+        sched = cfg.lr
+        nb = cfg.partition.num_blocks
+        prog = w.programs[r]
+        lo = np.zeros(nb + 1, dtype=np.int64)
+        hi = np.zeros(nb + 1, dtype=np.int64)
+        execs = (ctypes.c_void_p * (nb + 1))()
+        flops = np.zeros(nb + 1, dtype=np.int64)
+        for b in range(nb + 1):
+            blk = cfg.partition.block(b)
+            lo[b], hi[b] = blk.start, blk.stop
+            flops[b] = self._flops_of[b]
+            if (b, 0) in prog.execs:
+                execs[b] = prog.execs[(b, 0)]
+        ms = np.ascontiguousarray(sched.milestones, dtype=np.int64)
+        tracks = w.tags is not None
+        k = w.tag_pick if tracks else 0
+        c = N.UpdaterCfg()
+        c.sample_counter = w.store.sample_counter._a
+        c.update_order = w.store.update_order_counter._a
+        c.stop = self.ctrl.stop._a
+        c.last_avg_stamp = w.last_avg_stamp._a
+        c.budget = self.budget
+        c.lr_kind = 0 if sched.kind == "cosine" else 1
+        c.n_milestones = len(ms)
+        c.alpha0, c.peak, c.gamma = sched.alpha0, sched.peak, sched.gamma
+        c.warmup, c.total = sched.warmup, sched.total
+        c.milestones = ms.ctypes.data if len(ms) else None
+        c.lpp = int(cfg.algo == "lpp_sgd")
+        c.num_blocks, c.rank = nb, r + 1
+        c.fused = int(self.fused())
+        c.warm_start = cfg.warm_start_budget
+        c.block_lo, c.block_hi = lo.ctypes.data, hi.ctypes.data
+        c.graph_exec = ctypes.addressof(execs)
+        c.flops_of = flops.ctypes.data
+        c.x, c.g = w.store.arena.ptr, w.grads[r].ptr
+        c.m = w.moms[r].ptr if w.moms[r] is not None else None
+        c.replica = w.replicas[r].ptr
+        c.tags = w.tag_arena.ptr if tracks else None
+        c.n = self.dim
+        c.mu, c.wd = cfg.momentum, cfg.weight_decay
+        c.apply_mode = N.MODES[cfg.apply_mode]
+        c.in_flight = cfg.in_flight
+        c.tag_pick = k
+        c.time_apply = int(self.time_apply)
+        c.tag_seed = (cfg.seed * 1_000_003 + w.q * 1009 + r + 1) & (2**64 - 1)
+        if tracks:
+            c.tag_idx_pinned = w.tag_idx_pinned[r].data_ptr()
+            c.tag_idx_dev = w.tag_idx_dev[r].data_ptr()
+            c.tag_out_dev = w.tag_out_dev[r].data_ptr()
+            c.tag_out_pinned = w.tag_pinned[r].data_ptr()
+        c.classified = self.classified_count._a
+        c.clean = self.clean_count._a
+        c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
+        c.stream = w.streams[r].cuda_stream
+        return c, (lo, hi, execs, flops, ms)
+
+    def updater_native(self, q: int, r: int) -> None:
+        """a10 in native code: the whole loop is one GIL-free C call."""
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
+        try:
+            c, keep = self.updater_cfg(w, r)
+            st = N.updater_run(c)
+            del keep
+            self.flops.add(int(st.flops))
+            if self.time_apply:
+                with self.native_lock:
+                    self.native_apply[0] += int(st.apply_launches)
+                    self.native_apply[1] += float(st.apply_ms)
+                    self.native_apply[2] += float(st.apply_bytes)
+        except BaseException as exc:  # surfaced after join (engine.py:456-463)
+            self.fail(exc)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
+            if w.exited.add(1) + 1 == self.cfg.updaters:
+                self.ctrl.drained.add(1)
+
     def updater(self, q: int, r: int) -> None:
         cfg = self.cfg
         w = self.workers[q]
@@ -762,7 +864,8 @@ class _Engine:
                                             name=f"averager-{q}"))
         for q in self.local_workers:
             for r in range(cfg.updaters):
-                threads.append(threading.Thread(target=self.updater, args=(q, r), daemon=True,
+                target = self.updater_native if self.native_loop() else self.updater
+                threads.append(threading.Thread(target=target, args=(q, r), daemon=True,
                                                 name=f"updater-{q}-{r + 1}"))
         if self.group is not None:
             self.group.barrier()
@@ -903,11 +1006,12 @@ class _Engine:
         return out
 
     def apply_timing(self):
-        if not self.apply_events:
+        n, ms, nbytes = self.native_apply
+        if not self.apply_events and not n:
             return ()
-        ms = sum(e0.elapsed_time(e1) for e0, e1, _ in self.apply_events)
-        nbytes = sum(b for _, _, b in self.apply_events)
-        return (len(self.apply_events), ms, nbytes)
+        ms += sum(e0.elapsed_time(e1) for e0, e1, _ in self.apply_events)
+        nbytes += sum(b for _, _, b in self.apply_events)
+        return (n + len(self.apply_events), ms, nbytes)
 
     def close(self):
         for nv in self.nvls.values():

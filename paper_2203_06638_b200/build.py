@@ -15,7 +15,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = PKG / "csrc" / "lpp_b200.cu"
+SRCS = [PKG / "csrc" / "lpp_b200.cu", PKG / "csrc" / "updater.cu"]
 OUT = PKG / "lib" / "liblpp_b200.so"
 
 NVCC_FLAGS = [
@@ -36,7 +36,7 @@ def needs_build() -> bool:
     if not OUT.exists():
         return True
     mtime = OUT.stat().st_mtime
-    deps = [SRC, ROOT / "include" / "lpp_b200.h"]
+    deps = [*SRCS, PKG / "csrc" / "common.cuh", ROOT / "include" / "lpp_b200.h"]
     return any(p.stat().st_mtime > mtime for p in deps)
 
 
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, str(SRC), "-o", str(tmp)]
+    cmd = [nvcc(), *NVCC_FLAGS, *map(str, SRCS), "-o", str(tmp)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -19,25 +19,21 @@
 // REDG.E.ADD.F32x4) or the bulk-async reduction cp.reduce.async.bulk
 // .add.f32 (SASS UBLKRED) issued from shared memory.
 
-#include "../../include/lpp_b200.h"
-
-#include <cuda_runtime.h>
+#include "common.cuh"
 
 #include <atomic>
 #include <climits>
 #include <chrono>
-#include <cstdarg>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <thread>
 
 // ---------------------------------------------------------------------------
-// errors
+// errors and the launch counter (shared with updater.cu through common.cuh)
 
 static thread_local char g_err[512] = "";
 
-static int set_err(int code, const char* fmt, ...) {
+int lpp_set_err(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
@@ -45,26 +41,11 @@ static int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
-#define CUDA_TRY(expr)                                                      \
-  do {                                                                      \
-    cudaError_t e_ = (expr);                                                \
-    if (e_ != cudaSuccess)                                                  \
-      return set_err(LPP_E_CUDA, "%s failed: %s", #expr,                    \
-                     cudaGetErrorString(e_));                               \
-  } while (0)
-
 // every successful kernel launch of this library is counted (the bench's
 // gpu_launches is the delta of this counter over the timed region)
 static std::atomic<unsigned long long> g_launches{0};
 
-#define LAUNCH_CHECK(name)                                                  \
-  do {                                                                      \
-    cudaError_t e_ = cudaGetLastError();                                    \
-    if (e_ != cudaSuccess)                                                  \
-      return set_err(LPP_E_CUDA, "%s launch failed: %s", name,              \
-                     cudaGetErrorString(e_));                               \
-    g_launches.fetch_add(1, std::memory_order_relaxed);                     \
-  } while (0)
+void lpp_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 extern "C" int lpp_abi_version(void) { return LPP_ABI_VERSION; }
 extern "C" unsigned long long lpp_launch_count(void) { return g_launches.load(); }

@@ -55,6 +55,7 @@ class RunConfig:
     fuse_snapshot: bool = True       # async: fuse each apply with the next step's snapshot
     track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
     record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
+    host_loop: str = "auto"          # updater loop: "native" (C++, GIL-free), "python", "auto"
 
     @property
     def tracks(self) -> bool:
@@ -90,6 +91,8 @@ class RunConfig:
             raise ValueError("epoch_partition draws indices on the host: use sampling='host'")
         if self.averaging not in ("p2p", "nvls"):
             raise ValueError(f"unknown averaging {self.averaging!r}")
+        if self.host_loop not in ("auto", "native", "python"):
+            raise ValueError(f"unknown host loop {self.host_loop!r}")
         if self.workers > N.MAX_WORKERS:
             raise ValueError(f"at most {N.MAX_WORKERS} workers per averaging group")
 

@@ -54,10 +54,14 @@ class StepProgram:
         # can overlap step t+1 (which writes the other slot)
         self.losses = [torch.zeros((), dtype=torch.float32, device=device) for _ in range(self.nbuf)]
         self.loss = self.losses[0]
-        self.gen = None
+        # "random": the batch indices are drawn on the device inside the
+        # captured graph (lpp_sample_indices: a splitmix64 stream keyed by
+        # seed, advanced by a device-side step counter on every replay)
+        self.sample_key = int(seed)
+        self.sample_step = torch.zeros(1, dtype=torch.long, device=device)
         if input_mode == "random":
-            self.gen = torch.Generator(device=device)
-            self.gen.manual_seed(int(seed))
+            from . import _native
+            self._sampler = _native.sample_indices
         self.blocks = dict(blocks)
         self.leaves = {}
         for bid, blk in self.blocks.items():
@@ -75,18 +79,15 @@ class StepProgram:
                 for bid in self.blocks:
                     for buf in range(self.nbuf):
                         g = torch.cuda.CUDAGraph()
-                        if self.gen is not None:
-                            g.register_generator_state(self.gen)
                         with torch.cuda.graph(g, pool=pool, stream=stream):
                             self._body(bid, buf)
                         pool = g.pool()
                         self.graphs[(bid, buf)] = g
                 stream.synchronize()
-        # raw cudaGraphExec_t handles: graphs without a registered generator
-        # are launched straight through the C ABI (torch's replay() also
-        # advances generator offsets, which the "random" input mode needs)
+        # raw cudaGraphExec_t handles, launched straight through the C ABI
+        # (no framework generator state to advance: sampling is our kernel)
         self.execs = {}
-        if use_graphs and self.gen is None:
+        if use_graphs:
             from . import _native
 
             self._native = _native
@@ -96,8 +97,8 @@ class StepProgram:
     def _body(self, bid: int, buf: int = 0) -> None:
         blk = self.blocks[bid]
         if self.input_mode == "random":
-            torch.randint(0, self.feats.shape[0], (self.batch_size,), generator=self.gen,
-                          device=self.device, out=self.idx)
+            self._sampler(self.idx.data_ptr(), self.sample_step.data_ptr(), self.batch_size,
+                          self.feats.shape[0], self.sample_key, torch.cuda.current_stream().cuda_stream)
         if self.input_mode == "batch":
             xb, yb = self.xbs[buf], self.ybs[buf]
         else:

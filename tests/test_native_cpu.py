@@ -42,7 +42,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_error_channel():
-    assert N.lib.lpp_abi_version() == 1
+    assert N.lib.lpp_abi_version() == 2
     with pytest.raises(IndexError):
         # range check happens before any device work
         N.accum(0, 4, 3, 0, 2, 1.0, N.MODE_RED, 0)
@@ -133,3 +133,67 @@ def test_counter_checks_buffer_type_and_range():
         N.atomic_load(np.zeros(1, dtype=np.float64), 0)
     with pytest.raises(IndexError):
         N.atomic_load(np.zeros(1, dtype=np.int64), 1)
+
+
+def test_updater_cfg_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of lpp_updater_cfg / lpp_updater_stats has the C
+    layout (offsets and sizes from the header, compiled with gcc)."""
+    import ctypes
+
+    fields = [f for f, _ in N.UpdaterCfg._fields_]
+    sfields = [f for f, _ in N.UpdaterStats._fields_]
+    src = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT / "include" / "lpp_b200.h"}"',
+           'int main(void) {', 'printf("%zu %zu", sizeof(lpp_updater_cfg), sizeof(lpp_updater_stats));']
+    src += [f'printf(" %zu", offsetof(lpp_updater_cfg, {f}));' for f in fields]
+    src += [f'printf(" %zu", offsetof(lpp_updater_stats, {f}));' for f in sfields]
+    src += ['return 0; }']
+    (tmp_path / "off.c").write_text("\n".join(src))
+    subprocess.run(["gcc", "-I/usr/local/cuda/include", str(tmp_path / "off.c"), "-o",
+                    str(tmp_path / "off")], check=True)
+    got = [int(v) for v in subprocess.run([str(tmp_path / "off")], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [ctypes.sizeof(N.UpdaterCfg), ctypes.sizeof(N.UpdaterStats)]
+    want += [getattr(N.UpdaterCfg, f).offset for f in fields]
+    want += [getattr(N.UpdaterStats, f).offset for f in sfields]
+    assert got == want
+
+
+def test_native_lr_at_is_bit_identical_to_python():
+    """lpp_lr_at (the native loop's lr) == schedules.lr_at bit for bit."""
+    from paper_2203_06638_b200.schedules import LrSchedule, constant_schedule, lr_at
+
+    scheds = [LrSchedule(kind="cosine", alpha0=0.1, total=997, warmup=97, batch_local=128,
+                         workers=8, batch_base=128, boost=True),
+              LrSchedule(kind="cosine", alpha0=0.05, total=60, warmup=0),
+              LrSchedule(kind="multistep", alpha0=0.1, total=500, warmup=13, milestones=(100, 250, 400),
+                         gamma=0.1, batch_local=32, workers=2, batch_base=32),
+              constant_schedule(0.05, 50)]
+    for sc in scheds:
+        for s in list(range(0, sc.total + 5)) + [10**6]:
+            assert N.lr_at_native(sc, s) == lr_at(sc, s), (sc, s)
+
+
+def test_native_select_block_matches_python():
+    from paper_2203_06638_b200.partition import select_block
+
+    for t_st in (0, 1, 5, 100):
+        for nb in (1, 2, 4):
+            for rank in range(1, nb + 1):
+                for s in range(0, 240):
+                    assert N.select_block_native(s, t_st, nb, rank) == select_block(s, t_st, nb, rank).block_id
+    with pytest.raises(ValueError):
+        N.select_block_native(3, 0, 4, 5)
+    with pytest.raises(ValueError):
+        N.select_block_native(3, 0, 4, 0)
+
+
+def test_device_sampler_host_twin():
+    """The in-graph sampler's host twin: indices in [0, n), a deterministic
+    function of (key, step), different per step and per key, ~uniform."""
+    a = N.sample_indices_host(4096, 1000, 7, 0)
+    assert a.min() >= 0 and a.max() < 1000
+    assert np.array_equal(a, N.sample_indices_host(4096, 1000, 7, 0))
+    assert not np.array_equal(a, N.sample_indices_host(4096, 1000, 7, 1))
+    assert not np.array_equal(a, N.sample_indices_host(4096, 1000, 8, 0))
+    counts = np.bincount(N.sample_indices_host(100_000, 10, 3, 5), minlength=10)
+    assert counts.min() > 9_500 and counts.max() < 10_500

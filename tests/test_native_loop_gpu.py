@@ -1,0 +1,153 @@
+"""The native updater loop (lpp_updater_run, a10 in C++) and the in-graph
+device sampler, on the GPU.
+
+The loop must keep the reference engine's updater contract
+(test_engine.py:203-235): claim-then-process (each updater processes
+exactly one slot >= budget, so counter_final = budget + U), every step's
+flops accounted, sampled write tags classified once per step; and it must
+train like the Python loop it replaces (same kernels, same sampler).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _resnet_cfg(obj, budget=40, workers=1, updaters=4, **kw):
+    from paper_2203_06638_b200.engine import RunConfig
+    from paper_2203_06638_b200.partition import balanced_boundaries, make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    d = dict(algo="lpp_sgd", objective=obj,
+             partition=make_partition(obj.dim, balanced_boundaries(obj.layer_param_counts, updaters)),
+             lr=LrSchedule(kind="cosine", alpha0=0.05, total=budget + 4, warmup=4),
+             sync=SyncScheme(total=budget, period=8), budget=budget, warm_start_budget=4,
+             workers=workers, updaters=updaters, batch_size=64, seed=1, momentum=0.9,
+             weight_decay=5e-4, sampling="device", record_mode="off", evaluate=False,
+             host_loop="native")
+    d.update(kw)
+    return RunConfig(**d)
+
+
+def test_device_sampler_matches_host_twin_and_advances_in_graph():
+    from paper_2203_06638_b200 import _native as N
+
+    idx = torch.zeros(100, dtype=torch.long, device="cuda")
+    step = torch.zeros(1, dtype=torch.long, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for t in range(3):
+        N.sample_indices(idx.data_ptr(), step.data_ptr(), 100, 5000, 42, st)
+        torch.cuda.synchronize()
+        assert np.array_equal(idx.cpu().numpy(), N.sample_indices_host(100, 5000, 42, t))
+    assert int(step) == 3
+    # captured once, every replay draws the next step's batch
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        N.sample_indices(idx.data_ptr(), step.data_ptr(), 100, 5000, 42, s.cuda_stream)
+    torch.cuda.synchronize()
+    start = int(step)
+    for t in range(start, start + 3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(idx.cpu().numpy(), N.sample_indices_host(100, 5000, 42, t))
+
+
+@pytest.mark.parametrize("fuse,tags", [(True, True), (False, True), (True, False), (False, False)])
+def test_native_loop_accounting(fuse, tags):
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    cfg = _resnet_cfg(obj, budget=40, workers=2, updaters=4, fuse_snapshot=fuse, track_writes=tags)
+    tr = Trainer(cfg, time_apply=True)
+    try:
+        assert tr.eng.native_loop()
+        res = tr.run()
+        assert res.counter_finals == [44, 44]          # budget + U per worker
+        assert np.all(np.isfinite(res.final_values))
+        steps = sum(res.counter_finals)
+        n, ms, nbytes = res.apply_timing
+        assert n == steps and ms > 0 and nbytes > 0
+        if tags:
+            assert tr.eng.classified_count.read() == steps
+            assert 0.0 <= res.p_hat <= 1.0
+        else:
+            assert tr.eng.classified_count.read() == 0
+        # flops: warm-up slots run block 0 (full); afterwards half the slots
+        # are partial blocks, so the total sits strictly between the bounds
+        full = tr.eng._flops_of[0]
+        assert min(tr.eng._flops_of.values()) * steps <= res.flops <= full * steps
+        assert res.flops < full * steps
+        rounds = {}
+        for st in res.stamps:
+            rounds.setdefault(st.round, set()).add(st.worker)
+        assert rounds and all(v == {0, 1} for v in rounds.values())
+    finally:
+        tr.close()
+
+
+def test_native_loop_repeated_phases_and_ineligible_configs():
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    tr = Trainer(_resnet_cfg(obj, budget=400))
+    try:
+        for budget in (12, 20):
+            res = tr.run(budget, evaluate=False)
+            assert res.counter_finals == [budget + 4]
+    finally:
+        tr.close()
+    with pytest.raises(ValueError, match="host_loop='native'"):
+        Trainer(_resnet_cfg(obj, record_mode="light")).run()
+
+
+def test_native_loop_trains_like_the_python_loop():
+    """Async band: the native and Python updater loops (same kernels, same
+    device sampler) both learn a learnable synthetic task and land within a
+    band of each other."""
+    from paper_2203_06638_b200.engine import run_experiment
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.schedules import LrSchedule
+
+    obj = ResNetObjective("resnet20", n_samples=2048, seed=0, pattern_scale=0.5)
+    base = _resnet_cfg(obj, budget=160, momentum=0.0, evaluate=True, warm_start_budget=16,
+                       lr=LrSchedule(kind="cosine", alpha0=0.05, total=164, warmup=16))
+    nat = run_experiment(base)
+    py = run_experiment(dataclasses.replace(base, host_loop="python"))
+    l0 = nat.metrics[0].train_loss
+    ln, lp = nat.metrics[-1].train_loss, py.metrics[-1].train_loss
+    print(f"\nnative {ln:.3f}  python {lp:.3f}  initial {l0:.3f}")
+    assert ln < 0.5 * l0 and lp < 0.5 * l0
+    assert abs(ln - lp) <= 0.25 * l0
+
+
+def test_native_loop_mlp_and_lap():
+    """The loop on the reference MLP objective, lap_sgd (always block 0)."""
+    from paper_2203_06638_b200.engine import RunConfig, Trainer
+    from paper_2203_06638_b200.objectives import MlpObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import SyncScheme, constant_schedule
+
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(512, 32))
+    y = rng.integers(0, 4, 512)
+    obj = MlpObjective(X, y, (16,), 4)
+    cfg = RunConfig(algo="lap_sgd", objective=obj, partition=make_partition(obj.dim, (0, obj.dim)),
+                    lr=constant_schedule(0.05, 300), sync=SyncScheme(total=300, period=4),
+                    budget=300, warm_start_budget=0, workers=2, updaters=3, batch_size=16, seed=3,
+                    sampling="device", record_mode="off", evaluate=True, host_loop="native")
+    tr = Trainer(cfg)
+    try:
+        res = tr.run()
+        assert res.counter_finals == [303, 303]
+        assert res.metrics[-1].train_loss < res.metrics[0].train_loss
+    finally:
+        tr.close()
