@@ -142,6 +142,7 @@ _SIGS = {
     "lpp_nvls_apply": (_c.c_int, [_vp, _vp, _vp, _size, _vp, _c.c_int32, _vp]),
     "lpp_copy_async": (_c.c_int, [_vp, _vp, _size, _vp]),
     "lpp_graph_launch": (_c.c_int, [_vp, _vp]),
+    "lpp_host_gather_rows": (_c.c_int, [_vp, _vp, _size, _size, _vp, _size]),
     "lpp_l2_flush": (_c.c_int, [_vp, _size, _vp]),
     "lpp_sm_count": (_c.c_int, [_c.c_int, _c.POINTER(_c.c_int)]),
     "lpp_lr_at": (_c.c_double, [_c.c_int, _c.c_double, _c.c_double, _c.c_int64, _c.c_int64, _vp,
@@ -347,3 +348,10 @@ def updater_run(cfg: UpdaterCfg) -> UpdaterStats:
     st = UpdaterStats()
     check(lib.lpp_updater_run(ctypes.byref(cfg), ctypes.byref(st)), "updater_run")
     return st
+
+
+def host_gather_rows(dst_ptr: int, src_ptr: int, n_rows: int, row_bytes: int, idx: np.ndarray) -> None:
+    """dst row i = src row idx[i] (host memory, GIL released)."""
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    check(lib.lpp_host_gather_rows(dst_ptr, src_ptr, n_rows, row_bytes, idx.ctypes.data, len(idx)),
+          "host_gather_rows")

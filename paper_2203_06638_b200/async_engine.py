@@ -169,7 +169,7 @@ class _Worker:
                 self.batch_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size, *shape),
                                                 dtype=obj.features.dtype, pin_memory=True)
                 self.label_pinned = torch.zeros((cfg.updaters, depth, cfg.batch_size),
-                                                dtype=torch.long, pin_memory=True)
+                                                dtype=obj.labels.dtype, pin_memory=True)
                 # H2D prefetch: a copy stream per updater fills a device ring,
                 # overlapping the previous step's compute; the step then does
                 # a D2D into the captured graph's static input
@@ -381,9 +381,11 @@ class _Engine:
         cfg = self.cfg
         stream = w.streams[r]
         prog = w.programs[r]
-        t = torch.from_numpy(batch)
-        torch.index_select(cfg.objective.features, 0, t, out=w.batch_pinned[r, slot])
-        torch.index_select(cfg.objective.labels, 0, t, out=w.label_pinned[r, slot])
+        feats, labs = cfg.objective.features, cfg.objective.labels
+        xs, ls = w.batch_pinned[r, slot], w.label_pinned[r, slot]
+        n = feats.shape[0]
+        N.host_gather_rows(xs.data_ptr(), feats.data_ptr(), n, xs[0].numel() * xs.element_size(), batch)
+        N.host_gather_rows(ls.data_ptr(), labs.data_ptr(), n, ls.element_size(), batch)
         cs = w.copy_streams[r]
         cs.wait_event(w.buf_free[r][buf])
         with torch.cuda.stream(cs):

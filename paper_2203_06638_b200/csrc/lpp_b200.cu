@@ -1110,6 +1110,20 @@ extern "C" int lpp_enable_peer_access(int device, int peer) {
 // ---------------------------------------------------------------------------
 // utilities
 
+extern "C" int lpp_host_gather_rows(void* dst, const void* src, size_t n_rows, size_t row_bytes,
+                                    const int64_t* idx, size_t n_idx) {
+  if (n_idx == 0 || row_bytes == 0) return LPP_OK;
+  if (!dst || !src || !idx) return set_err(LPP_E_VALUE, "host_gather_rows: null pointer");
+  for (size_t i = 0; i < n_idx; ++i)
+    if (idx[i] < 0 || (size_t)idx[i] >= n_rows)
+      return set_err(LPP_E_INDEX, "host_gather_rows: index %lld outside [0, %zu)",
+                     (long long)idx[i], n_rows);
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  for (size_t i = 0; i < n_idx; ++i) memcpy(d + i * row_bytes, s + (size_t)idx[i] * row_bytes, row_bytes);
+  return LPP_OK;
+}
+
 extern "C" int lpp_graph_launch(void* graph_exec, void* stream) {
   if (!graph_exec) return set_err(LPP_E_VALUE, "graph_launch: null graph");
   CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));

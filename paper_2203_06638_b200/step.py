@@ -48,7 +48,7 @@ class StepProgram:
         if input_mode == "batch":
             self.xbs = [torch.zeros((B, *self.feats.shape[1:]), dtype=self.feats.dtype, device=device)
                         for _ in range(self.nbuf)]
-            self.ybs = [torch.zeros(B, dtype=torch.long, device=device) for _ in range(self.nbuf)]
+            self.ybs = [torch.zeros(B, dtype=self.labels.dtype, device=device) for _ in range(self.nbuf)]
             self.xb, self.yb = self.xbs[0], self.ybs[0]
         # the step's loss, one slot per input buffer so a D2H of step t's loss
         # can overlap step t+1 (which writes the other slot)

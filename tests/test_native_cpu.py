@@ -197,3 +197,14 @@ def test_device_sampler_host_twin():
     assert not np.array_equal(a, N.sample_indices_host(4096, 1000, 8, 0))
     counts = np.bincount(N.sample_indices_host(100_000, 10, 3, 5), minlength=10)
     assert counts.min() > 9_500 and counts.max() < 10_500
+
+
+def test_host_gather_rows_and_range_check():
+    src = np.arange(40, dtype=np.float32).reshape(10, 4)
+    dst = np.zeros((3, 4), dtype=np.float32)
+    N.host_gather_rows(dst.ctypes.data, src.ctypes.data, 10, 16, np.array([7, 0, 7]))
+    assert np.array_equal(dst, src[[7, 0, 7]])
+    with pytest.raises(IndexError):
+        N.host_gather_rows(dst.ctypes.data, src.ctypes.data, 10, 16, np.array([1, 10, 2]))
+    with pytest.raises(IndexError):
+        N.host_gather_rows(dst.ctypes.data, src.ctypes.data, 10, 16, np.array([-1]))
