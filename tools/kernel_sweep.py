@@ -66,6 +66,35 @@ def main():
             hbm = 2 * 4 * d * Q
             rows.append(dict(kernel=f"average_Q{Q}_local", d=d, us=t * 1e6, gbs=hbm / t / 1e9,
                              frac=hbm / t / 1e9 / peak))
+            if Q == 4:
+                # the same round while 3 updater streams keep applying K1
+                # (momentum + wd) into the averaged arena
+                side = [torch.cuda.Stream() for _ in range(3)]
+                gs = [Arena(d, 0) for _ in range(3)]
+                for ga in gs:
+                    ga.tensor.normal_().mul_(1e-3)
+                ts = []
+                for _ in range(5):
+                    flush()
+                    torch.cuda.synchronize()
+                    for sd, ga in zip(side, gs):
+                        for _ in range(3):
+                            N.apply_sgd(ars[0].ptr, ga.ptr, None, d, 1e-3, None, 0.0, 5e-4,
+                                        N.MODE_RED, sd.cuda_stream)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
+                    b.record()
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b) * 1e-3)
+                    torch.cuda.synchronize()
+                tc = sorted(ts)[len(ts) // 2]
+                rows.append(dict(kernel="average_Q4_local_under_K1", d=d, us=tc * 1e6,
+                                 gbs=hbm / tc / 1e9, frac=hbm / tc / 1e9 / peak,
+                                 slowdown=tc / t, note="3 streams of K1 (red, wd) into arena 0 "
+                                                       "concurrently; frac counts K4's bytes only"))
+                for ga in gs:
+                    ga.close()
             for a in ars[2:]:
                 a.close()
         for a in (x, g, m, r):
