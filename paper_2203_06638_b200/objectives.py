@@ -571,6 +571,12 @@ class ResNetObjective(ArenaObjective):
 
     def make_module(self, device) -> nn.Module:
         m = type(self._template)(self.n_classes).to(device)
+        # BatchNorm's num_batches_tracked counter only matters for
+        # momentum=None (cumulative averaging); with the fixed momentum used
+        # here it is an extra int64 add kernel per BN layer per step
+        for mod in m.modules():
+            if isinstance(mod, nn.modules.batchnorm._BatchNorm) and mod.momentum is not None:
+                mod.num_batches_tracked = None
         if self.channels_last:
             m = m.to(memory_format=torch.channels_last)
         return m

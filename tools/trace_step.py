@@ -1,0 +1,57 @@
+"""Complete kernel launch list of the bench's timed region (ResNet-20
+LPP-SGD, U=4, native loop) from a CUPTI activity trace (torch.profiler):
+every kernel of K steps, concurrent (not serialised like ncu), with its
+duration — the full-coverage complement of the ncu launch list, which
+cannot finish the whole bench under replay in reasonable time."""
+import collections, csv, json, sys
+from pathlib import Path
+import torch
+from torch.profiler import ProfilerActivity, profile
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import bench
+from paper_2203_06638_b200.engine import Trainer
+from paper_2203_06638_b200.objectives import ResNetObjective
+
+torch.backends.cudnn.benchmark = True
+K, W, U = 20, 5, 4
+out_dir = Path(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out")
+obj = ResNetObjective("resnet20", n_samples=50_000, seed=0, data="device")
+cfg = bench.build_cfg(obj, (K + W) * U)
+tr = Trainer(cfg)
+tr.run(W * U, evaluate=False)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    res = tr.run(K * U, evaluate=False)
+    torch.cuda.synchronize()
+rows = []
+for ev in prof.events():
+    if ev.device_type == torch.autograd.DeviceType.CUDA and ev.name and not ev.name.startswith("Memcpy") \
+            and not ev.name.startswith("Memset"):
+        rows.append((ev.name, ev.time_range.start, ev.time_range.end - ev.time_range.start))
+rows.sort(key=lambda r: r[1])
+with open(out_dir / "trace_launches.csv", "w", newline="") as f:
+    w = csv.writer(f)
+    w.writerow(["kernel", "start_us", "dur_us"])
+    t0 = rows[0][1] if rows else 0
+    for n, s, d in rows:
+        w.writerow([n, s - t0, d])
+tot, cnt = collections.Counter(), collections.Counter()
+for n, _, d in rows:
+    k = n.split("(")[0][:110]
+    tot[k] += d
+    cnt[k] += 1
+T = sum(tot.values())
+ours = ("k_apply", "void k_apply", "k_snapshot", "void k_average", "k_accum", "k_gather", "(anonymous namespace)::k_sample")
+mine = sum(v for k, v in tot.items() if k.startswith(ours))
+span = (rows[-1][1] + rows[-1][2] - rows[0][1]) if rows else 0
+lines = [f"# {len(rows)} kernels in the timed region of {K * U + U} minibatches "
+         f"(ResNet-20 LPP-SGD U=4 B=128, native loop); summed kernel time {T / 1e3:.1f} ms "
+         f"over a {span / 1e3:.1f} ms span (4 streams overlap)",
+         f"# our kernels (K1-K5 + in-graph sampler): {100 * mine / T:.2f}% of summed kernel time",
+         "share%   total_us   n   kernel"]
+for k, v in tot.most_common():
+    tag = "[ours] " if k.startswith(ours) else ""
+    lines.append(f"{100 * v / T:6.2f} {v:10.1f} {cnt[k]:5d}  {tag}{k}")
+(out_dir / "trace_share.txt").write_text("\n".join(lines) + "\n")
+print("\n".join(lines[:30]))
+tr.close()
