@@ -333,6 +333,23 @@ def main() -> None:
     np.savez_compressed(HERE / "engine_cnn_q1u1.npz", final=res.final_values, x0=res.x0,
                         counter_finals=np.array(res.counter_finals))
 
+    # ---------------- async band: the reference's own async runs of config C0 ----------------
+    # (live threads: not deterministic, so the fixture is a band over seeds)
+    band = {"config": "C0 MLP 3072-64-10, lpp_sgd Q=2 U=2 B=32 T=200, cosine 0.05 warmup 20, "
+                      "T_st 20, period 16 after T/2, record light", "seeds": [], "initial": [], "final": []}
+    for seed in (1, 2, 3, 4, 5):
+        cfg = rengine.RunConfig(
+            algo="lpp_sgd", objective=c0, partition=rpart.make_partition(c0.dim, c0_bounds),
+            lr=rsched.LrSchedule(kind="cosine", alpha0=0.05, total=200, warmup=20, batch_local=32,
+                                 workers=2, batch_base=32),
+            sync=rsched.SyncScheme(total=200, period=16), budget=200, warm_start_budget=20,
+            workers=2, updaters=2, batch_size=32, seed=seed, record_mode="light")
+        res = rengine.run_experiment(cfg)
+        band["seeds"].append(seed)
+        band["initial"].append(res.metrics[0].train_loss)
+        band["final"].append(res.metrics[-1].train_loss)
+    (HERE / "async_band_c0.json").write_text(json.dumps(band, indent=1))
+
     # ---------------- the reference engine itself: Q=1, U=1, quiescent, full ----------------
     sched = rsched.constant_schedule(0.05, 50)
     cfg = rengine.RunConfig(

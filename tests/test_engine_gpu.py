@@ -14,6 +14,7 @@
 from __future__ import annotations
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -633,3 +634,32 @@ def test_small_cnn_q1u1_matches_reference_engine_run():
     np.testing.assert_allclose(res.x0, g["x0"])
     np.testing.assert_allclose(res.final_values, g["final"], atol=ATOL, rtol=RTOL)
     assert res.counter_finals == list(g["counter_finals"])
+
+
+def test_async_loss_band_vs_reference_async_runs():
+    """North star: in async mode the loss trajectory stays within a stated
+    band of the REFERENCE's.  The reference's own async engine (live threads,
+    tests/golden/async_band_c0.json, 5 seeds) on config C0; the GPU engine on
+    the same config and seeds.  Band: every GPU final loss inside the
+    reference's [min, max] widened by 0.05 (absolute; ~2 % of the initial
+    loss), the initial loss (same x0, same data) equal to 1e-4."""
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.partition import balanced_boundaries, make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    ref = json.loads((Path(__file__).parent / "golden" / "async_band_c0.json").read_text())
+    obj = _mlp("c0")[0]
+    bounds = balanced_boundaries(obj.layer_param_counts, 2)
+    finals = []
+    for seed, ref_init in zip(ref["seeds"], ref["initial"]):
+        cfg = RunConfig(algo="lpp_sgd", objective=obj, partition=make_partition(obj.dim, bounds),
+                        lr=LrSchedule(kind="cosine", alpha0=0.05, total=200, warmup=20, batch_local=32,
+                                      workers=2, batch_base=32),
+                        sync=SyncScheme(total=200, period=16), budget=200, warm_start_budget=20,
+                        workers=2, updaters=2, batch_size=32, seed=seed, record_mode="light")
+        res = run_experiment(cfg)
+        assert abs(res.metrics[0].train_loss - ref_init) <= 1e-4
+        finals.append(res.metrics[-1].train_loss)
+    lo, hi = min(ref["final"]) - 0.05, max(ref["final"]) + 0.05
+    print(f"\nasync band: GPU finals {np.round(finals, 4)}  reference {np.round(ref['final'], 4)}")
+    assert all(lo <= f <= hi for f in finals), (finals, ref["final"])
