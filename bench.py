@@ -134,8 +134,9 @@ def reference_arm(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": "resnet20_cifar10_lpp_sgd_cpu", "global_batch": B * U,
-                   "updaters": U, "workers": 1, "batch_per_updater": B},
+        "config": {"workload": "resnet20_cifar10_lpp_sgd", "model": "resnet20", "global_batch": B * U,
+                   "batch_per_updater": B, "updaters_per_gpu": U, "workers": 1, "blocks": U,
+                   "parallelism": f"lpp_sgd_q1_u{U}", "device": "host CPU (reference arm)"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"], "kind": "port",
                          "sample": f"{r['minibatches']} minibatches x {B} images (LPP-SGD, U={U}, "
                                    f"threaded port of engine.py:289-523 incl. the averager and "
