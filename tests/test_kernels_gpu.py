@@ -443,3 +443,58 @@ def test_average_in_place_preserves_concurrent_updates(N, Q):
     torch.cuda.synchronize()
     after = sum(a.tensor.double().sum() for a in ars)
     assert float(after - before) == float(adds * n)
+
+
+GUARD = 68  # sentinel elements on both sides (272 B: interior bases stay 16-byte aligned)
+
+
+def _guarded(n, fill, dtype=torch.float32):
+    """A device buffer [guard | n | guard] with the guards set to a bit
+    pattern no kernel produces; returns (buffer, interior pointer)."""
+    buf = torch.full((n + 2 * GUARD,), fill, dtype=dtype, device="cuda")
+    return buf, buf.data_ptr() + GUARD * buf.element_size()
+
+
+def _guards_intact(buf, fill):
+    g = buf.cpu()
+    return bool((g[:GUARD] == fill).all() and (g[-GUARD:] == fill).all())
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 131, 4099, 100_003])
+def test_no_kernel_writes_outside_its_range(N, n):
+    """The bounds discipline compute-sanitizer would check (closed on this
+    pool): every kernel, at odd sizes and every 4-byte misalignment inside
+    guarded buffers, leaves the guard elements bit-identical."""
+    S = -12345.5
+    T = -777
+    st = 0
+    for off in (0, 1, 2, 3):
+        x, xp = _guarded(n + off, S)
+        g, gp = _guarded(n + off, S)
+        m, mp = _guarded(n + off, S)
+        r, rp = _guarded(n + off, S)
+        t, tp = _guarded(n + off, T, torch.int32)
+        o = 4 * off
+        x[GUARD:-GUARD] = 1.0
+        g[GUARD:-GUARD] = 0.5
+        m[GUARD:-GUARD] = 0.25
+        for mode in (N.MODE_PLAIN, N.MODE_RED, N.MODE_BULK):
+            N.apply_sgd(xp + o, gp + o, mp + o, n, 0.1, None, 0.9, 5e-4, mode, st)
+        N.apply_sgd_tagged(xp + o, gp + o, mp + o, n, 0.1, None, 0.9, 5e-4, N.MODE_RED, tp + o, 3, st)
+        N.accum(xp + o, n, 0, gp + o, n, -1.0, N.MODE_RED, st)
+        N.accum_tagged(xp + o, tp + o, n, 0, gp + o, n, -1.0, 4, N.MODE_RED, st)
+        N.snapshot(xp + o, rp + o, n, st)
+        mn = torch.full((1,), 2**31 - 1, dtype=torch.int32, device="cuda")
+        N.snapshot_tagged(xp + o, tp + o, rp + o, tp + o, n, mn.data_ptr(), st)
+        N.average_shard([xp + o, rp + o], 0, n, None, N.MODE_RED, st)
+        N.average_shard_tagged([xp + o, rp + o], [tp + o, tp + o], [5, 5], 0, n, None, N.MODE_RED, st)
+        torch.cuda.synchronize()
+        for b, f in ((x, S), (g, S), (m, S), (r, S), (t, T)):
+            assert _guards_intact(b, f), (n, off)
+        # the fused kernel takes arena bases (16-byte aligned): guard the end
+        if off == 0:
+            lo, hi = n // 3, n - n // 4
+            N.apply_snapshot(xp, gp, mp, rp, tp, n, lo, hi, 0.1, None, 0.9, 5e-4, 6, st)
+            torch.cuda.synchronize()
+            for b, f in ((x, S), (g, S), (m, S), (r, S), (t, T)):
+                assert _guards_intact(b, f), (n, "fused")
