@@ -329,6 +329,51 @@ typedef struct {
 
 int lpp_updater_run(const lpp_updater_cfg* cfg, lpp_updater_stats* stats);
 
+/* One worker's averager (a11: _averager_body, engine.py:385-453) in native
+ * code: the round protocol of paper_2203_06638_b200/rounds.py over the
+ * shared int64 control block (RoundControl layout: [0] round_calls, [1]
+ * stop, [2] abort, [3] drained workers, [8, 8+Q) round stamps, then the
+ * per-round vote / final-vote / fence0 / fence1 arrays of max_rounds + 2
+ * cells) and the owner-computes K4 round on its own stream:
+ *   open (CAS on round_calls when this worker's sync_every period is due,
+ *   or every worker drained) -> vote -> u = stamp; [tags: publish u,
+ *   fence 0] -> K4 over the owned shard (+ the mean on the final round)
+ *   -> stream sync -> [fence 1] -> last_avg_stamp = u -> wait for all Q
+ *   votes -> stop after the unanimous final round.
+ * One record per joined round (round, u, s_cur, k_delta, unanimous,
+ * wall ms since t0) for RunResult.stamps. */
+typedef struct {
+  int64_t* ctrl;                  /* RoundControl buffer */
+  int64_t max_rounds;
+  int32_t workers;                /* Q */
+  int32_t q;                      /* this worker */
+  int32_t updaters;               /* U: this worker drained when *exited == U */
+  int32_t tagged;                 /* stamp the tags (K5) with the round's stamps */
+  const int64_t* sample_counter;  /* C^q */
+  int64_t* update_order;          /* u = fetch_add + 1 */
+  const int64_t* exited;
+  int64_t* last_avg_stamp;
+  int64_t* synced_at;
+  int64_t switch_point;           /* sync_every: 1 before, period after */
+  int64_t period;
+  int64_t stop_after;             /* round budget (0: none) */
+  float* const* arenas;           /* [Q] local or peer-mapped arena bases */
+  int32_t* const* tags;           /* [Q] or NULL */
+  size_t lo, hi;                  /* owned shard */
+  size_t n;                       /* arena length */
+  float* mean_out;                /* final round: the mean (shard [lo, hi); all of it at Q = 1) */
+  void* stream;
+  double t0;                      /* CLOCK_MONOTONIC seconds at the run start */
+  int64_t* rec;                   /* [max_records][5] round, u, s_cur, k_delta, unanimous */
+  double* rec_wall_ms;            /* [max_records] */
+  int64_t max_records;
+} lpp_averager_cfg;
+
+int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);
+
+/* p[i] = v for i in [0, n) (int32, stream-ordered) */
+int lpp_fill_i32(int32_t* p, size_t n, int32_t v, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

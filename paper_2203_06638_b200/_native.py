@@ -70,6 +70,20 @@ class UpdaterCfg(ctypes.Structure):
     ]
 
 
+class AveragerCfg(ctypes.Structure):
+    """``lpp_averager_cfg`` (include/lpp_b200.h), field for field."""
+
+    _fields_ = [
+        ("ctrl", _vp), ("max_rounds", _c.c_int64),
+        ("workers", _c.c_int32), ("q", _c.c_int32), ("updaters", _c.c_int32), ("tagged", _c.c_int32),
+        ("sample_counter", _vp), ("update_order", _vp), ("exited", _vp), ("last_avg_stamp", _vp),
+        ("synced_at", _vp), ("switch_point", _c.c_int64), ("period", _c.c_int64),
+        ("stop_after", _c.c_int64), ("arenas", _vp), ("tags", _vp), ("lo", _size), ("hi", _size),
+        ("n", _size), ("mean_out", _vp), ("stream", _vp), ("t0", _c.c_double), ("rec", _vp),
+        ("rec_wall_ms", _vp), ("max_records", _c.c_int64),
+    ]
+
+
 class UpdaterStats(ctypes.Structure):
     """``lpp_updater_stats``."""
 
@@ -151,6 +165,8 @@ _SIGS = {
     "lpp_sample_indices": (_c.c_int, [_vp, _vp, _c.c_int32, _c.c_int64, _c.c_uint64, _vp]),
     "lpp_sample_indices_host": (_c.c_int, [_vp, _c.c_int32, _c.c_int64, _c.c_uint64, _c.c_int64]),
     "lpp_updater_run": (_c.c_int, [_c.POINTER(UpdaterCfg), _c.POINTER(UpdaterStats)]),
+    "lpp_averager_run": (_c.c_int, [_c.POINTER(AveragerCfg), _c.POINTER(_c.c_int64)]),
+    "lpp_fill_i32": (_c.c_int, [_vp, _size, _c.c_int32, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -355,3 +371,14 @@ def host_gather_rows(dst_ptr: int, src_ptr: int, n_rows: int, row_bytes: int, id
     idx = np.ascontiguousarray(idx, dtype=np.int64)
     check(lib.lpp_host_gather_rows(dst_ptr, src_ptr, n_rows, row_bytes, idx.ctypes.data, len(idx)),
           "host_gather_rows")
+
+
+def averager_run(cfg: AveragerCfg) -> int:
+    """Run one worker's averager natively (GIL released); returns rounds."""
+    n = ctypes.c_int64(0)
+    check(lib.lpp_averager_run(ctypes.byref(cfg), ctypes.byref(n)), "averager_run")
+    return int(n.value)
+
+
+def fill_i32(ptr: int, n: int, value: int, stream: int) -> None:
+    check(lib.lpp_fill_i32(ptr, n, int(value), stream), "fill_i32")

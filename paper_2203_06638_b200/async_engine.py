@@ -745,6 +745,59 @@ class _Engine:
             if w.exited.add(1) + 1 == cfg.updaters:
                 ctrl.drained.add(1)
 
+    def native_averager(self) -> bool:
+        """Whether averagers run the C++ round loop (lpp_averager_run): p2p
+        averaging without quiescent pauses, eval points or full records."""
+        cfg = self.cfg
+        return (cfg.host_loop != "python" and cfg.schedule == "async" and not cfg.quiescent
+                and not self.nvls and cfg.eval_interval == 0 and cfg.record_mode != "full")
+
+    def averager_native(self, q: int) -> None:
+        """a11 in native code: the round protocol + K4 in one GIL-free call."""
+        cfg = self.cfg
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        ctrl = self.ctrl
+        Q = cfg.workers
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
+        try:
+            arenas = (ctypes.c_void_p * Q)(*self.arena_ptrs)
+            tags = (ctypes.c_void_p * Q)(*self.tag_ptrs) if self.tag_ptrs is not None else None
+            cap = min(ctrl.max_rounds, 1 << 20)
+            rec = np.zeros((cap, 5), dtype=np.int64)
+            wall = np.zeros(cap, dtype=np.float64)
+            lo, hi = self.shards[q]
+            c = N.AveragerCfg()
+            c.ctrl = ctrl.buf.ctypes.data
+            c.max_rounds = ctrl.max_rounds
+            c.workers, c.q, c.updaters = Q, q, cfg.updaters
+            c.tagged = int(self.tag_ptrs is not None)
+            c.sample_counter = w.store.sample_counter._a
+            c.update_order = w.store.update_order_counter._a
+            c.exited = w.exited._a
+            c.last_avg_stamp = w.last_avg_stamp._a
+            c.synced_at = w.synced_at._a
+            c.switch_point, c.period = cfg.sync.switch_point, cfg.sync.period
+            c.stop_after = cfg.round_budget or 0
+            c.arenas = ctypes.addressof(arenas)
+            c.tags = ctypes.addressof(tags) if tags is not None else None
+            c.lo, c.hi, c.n = lo, hi, self.dim
+            c.mean_out = w.mean_out.data_ptr()
+            c.stream = w.avg_stream.cuda_stream
+            c.t0 = self.t0
+            c.rec, c.rec_wall_ms, c.max_records = rec.ctypes.data, wall.ctypes.data, cap
+            n = N.averager_run(c)
+            for i in range(min(n, cap)):
+                r, u, s_cur, k_delta, _ = (int(v) for v in rec[i])
+                self.stamps[q].append(AveragerStamp(worker=q, round=r, u=u, s_cur=s_cur,
+                                                    k_delta=k_delta, wall_ms=float(wall[i])))
+        except BaseException as exc:  # surfaced after join (engine.py:456-463)
+            self.fail(exc)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
+
     def averager(self, q: int) -> None:
         cfg = self.cfg
         w = self.workers[q]
@@ -862,7 +915,8 @@ class _Engine:
         starts = self._device_span_start()
         threads = []
         for q in self.local_workers:
-            threads.append(threading.Thread(target=self.averager, args=(q,), daemon=True,
+            target = self.averager_native if self.native_averager() else self.averager
+            threads.append(threading.Thread(target=target, args=(q,), daemon=True,
                                             name=f"averager-{q}"))
         for q in self.local_workers:
             for r in range(cfg.updaters):

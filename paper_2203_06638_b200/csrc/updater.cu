@@ -1,5 +1,5 @@
-// updater.cu — the native updater loop and device-side
-// batch sampling for captured steps.
+// updater.cu — the native updater loop, the native
+// averager (a11) and device-side batch sampling for captured steps.
 //
 // lpp_updater_run is the reference's _updater_loop / _updater_body
 // (engine.py:289-383) for one updater stream, with the per-step host work
@@ -11,11 +11,19 @@
 // enqueues per step is exactly the Python loop's: the K5 gather, K3 (or
 // nothing, fused), the captured fwd/bwd graph of the step's block, and the
 // K1/K2 (or fused K1+K3) apply — through the same C-ABI entry points.
+//
+// lpp_averager_run is _averager_body (engine.py:385-453) restated over the
+// round-control block of rounds.py: the same open / vote / fence / stamp
+// protocol, so native and Python averagers interoperate across processes.
 
 #include "common.cuh"
 
 #include <algorithm>
+#include <chrono>
+#include <climits>
 #include <cmath>
+#include <ctime>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -248,5 +256,153 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if ((rc = retire((int)(tt % F))) != LPP_OK) return rc;
   }
   st->steps = t;
+  return LPP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// native averager (a11)
+
+namespace {
+
+__global__ void k_fill_i32(int32_t* p, size_t n, int32_t v) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = v;
+}
+
+inline double now_s() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+// RoundControl layout (rounds.py)
+constexpr int64_t kHeader = 16, kStamps = 8;
+inline int64_t* cell(const lpp_averager_cfg* c, int64_t i) { return c->ctrl + i; }
+inline int64_t* vote_cell(const lpp_averager_cfg* c, int64_t r) { return cell(c, kHeader + r); }
+inline int64_t* final_cell(const lpp_averager_cfg* c, int64_t r) {
+  return cell(c, kHeader + c->max_rounds + 2 + r);
+}
+inline int64_t* fence_cell(const lpp_averager_cfg* c, int which, int64_t r) {
+  return cell(c, kHeader + (2 + which) * (c->max_rounds + 2) + r);
+}
+inline int64_t ld(const int64_t* p) { return __atomic_load_n(p, __ATOMIC_ACQUIRE); }
+inline void st(int64_t* p, int64_t v) { __atomic_store_n(p, v, __ATOMIC_RELEASE); }
+inline int64_t add(int64_t* p, int64_t d) { return __atomic_fetch_add(p, d, __ATOMIC_ACQ_REL); }
+
+}  // namespace
+
+extern "C" int lpp_fill_i32(int32_t* p, size_t n, int32_t v, void* stream) {
+  if (n == 0) return LPP_OK;
+  if (!p) return set_err(LPP_E_VALUE, "fill_i32: null buffer");
+  size_t want = (n + 255) / 256;
+  unsigned grid = (unsigned)(want < 2368 ? want : 2368);
+  k_fill_i32<<<grid, 256, 0, (cudaStream_t)stream>>>(p, n, v);
+  LAUNCH_CHECK("fill_i32");
+  return LPP_OK;
+}
+
+extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) {
+  if (!c || !rounds_out) return set_err(LPP_E_VALUE, "averager_run: null cfg");
+  if (!c->ctrl || !c->sample_counter || !c->update_order || !c->exited || !c->last_avg_stamp ||
+      !c->synced_at || !c->arenas || !c->mean_out)
+    return set_err(LPP_E_VALUE, "averager_run: null pointer");
+  if (c->workers < 1 || c->workers > LPP_MAX_WORKERS || c->q < 0 || c->q >= c->workers)
+    return set_err(LPP_E_VALUE, "averager_run: worker %d of %d", c->q, c->workers);
+  if (c->tagged && !c->tags) return set_err(LPP_E_VALUE, "averager_run: tagged without tags");
+  const int Q = c->workers;
+  int64_t* round_calls = cell(c, 0);
+  int64_t* stop = cell(c, 1);
+  int64_t* abort_ = cell(c, 2);
+  int64_t* drained = cell(c, 3);
+  cudaStream_t stream = (cudaStream_t)c->stream;
+  int64_t s_pre = 0, round_no = 0;
+  double backoff = 0.0;
+  *rounds_out = 0;
+  auto wait_ge = [&](const int64_t* p, int64_t target) -> bool {
+    return lpp_atomic_wait_ge_i64(p, target, abort_, 200) != INT64_MIN;
+  };
+  auto fail = [&](int code) {
+    st(abort_, 1);
+    st(stop, 1);
+    return code;
+  };
+  for (;;) {
+    if (ld(abort_)) break;
+    const int64_t s_cur = ld(c->sample_counter);
+    const bool drain = ld(c->exited) == c->updaters;
+    const bool pending = ld(round_calls) > round_no;
+    const int64_t period = s_cur < c->switch_point ? 1 : c->period;      // sync_every
+    const bool fresh = s_cur - s_pre >= period;
+    if (!pending) {
+      if (fresh || (drain && ld(drained) == Q)) {
+        int64_t expected = round_no;
+        __atomic_compare_exchange_n(round_calls, &expected, round_no + 1, false, __ATOMIC_ACQ_REL,
+                                    __ATOMIC_ACQUIRE);
+      } else {
+        std::this_thread::sleep_for(std::chrono::duration<double>(backoff));
+        backoff = std::min(2e-4, backoff * 2 + 1e-5);
+        continue;
+      }
+    }
+    backoff = 0.0;
+    const int64_t r = round_no + 1;
+    // vote (rounds.RoundControl.vote)
+    if (r > c->max_rounds) {
+      fail(LPP_E_INDEX);
+      return set_err(LPP_E_INDEX, "averaging round budget of the control block exceeded");
+    }
+    if (drain) add(final_cell(c, r), 1);
+    add(vote_cell(c, r), 1);
+    // do_round: this worker's share of round r
+    const int64_t u = add(c->update_order, 1) + 1;
+    bool ok = true;
+    int32_t stamps[LPP_MAX_WORKERS] = {0};
+    if (c->tagged) {
+      st(cell(c, kStamps + c->q), u);
+      add(fence_cell(c, 0, r), 1);
+      ok = wait_ge(fence_cell(c, 0, r), Q);
+      for (int i = 0; ok && i < Q; ++i) stamps[i] = (int32_t)ld(cell(c, kStamps + i));
+    }
+    if (ok) {
+      int rc = LPP_OK;
+      if (Q == 1) {
+        // a single worker's mean is itself (test_engine.py:169-182)
+        if (drain) rc = lpp_snapshot(c->arenas[0], c->mean_out, c->n, stream);
+        if (rc == LPP_OK && c->tagged) rc = lpp_fill_i32(c->tags[0], c->n, stamps[0], stream);
+      } else {
+        float* mean = drain ? c->mean_out + c->lo : nullptr;
+        rc = c->tagged ? lpp_average_shard_tagged(c->arenas, c->tags, stamps, Q, c->lo, c->hi, mean,
+                                                  LPP_MODE_RED, stream)
+                       : lpp_average_shard(c->arenas, Q, c->lo, c->hi, mean, LPP_MODE_RED, stream);
+      }
+      if (rc != LPP_OK) return fail(rc);
+      cudaError_t e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) {
+        fail(LPP_E_CUDA);
+        return set_err(LPP_E_CUDA, "averager: stream sync failed: %s", cudaGetErrorString(e));
+      }
+      if (c->tagged) {
+        add(fence_cell(c, 1, r), 1);
+        ok = wait_ge(fence_cell(c, 1, r), Q);
+      }
+      if (ok) {
+        st(c->last_avg_stamp, u);
+        st(c->synced_at, s_cur);
+      }
+    }
+    // wait for every worker's vote (rounds.RoundControl.wait_votes)
+    if (!wait_ge(vote_cell(c, r), Q)) break;
+    const bool unanimous = ld(final_cell(c, r)) == Q;
+    round_no = r;
+    if (c->stop_after > 0 && round_no >= c->stop_after) st(stop, 1);
+    if (c->rec && round_no <= c->max_records) {
+      int64_t* row = c->rec + 5 * (round_no - 1);
+      row[0] = r, row[1] = u, row[2] = s_cur, row[3] = s_cur - s_pre, row[4] = unanimous;
+      if (c->rec_wall_ms) c->rec_wall_ms[round_no - 1] = 1e3 * (now_s() - c->t0);
+    }
+    *rounds_out = round_no;
+    s_pre = s_cur;
+    if (unanimous) break;
+  }
   return LPP_OK;
 }

@@ -136,25 +136,28 @@ def test_counter_checks_buffer_type_and_range():
 
 
 def test_updater_cfg_struct_layout_matches_header(tmp_path):
-    """The ctypes mirror of lpp_updater_cfg / lpp_updater_stats has the C
-    layout (offsets and sizes from the header, compiled with gcc)."""
+    """The ctypes mirrors of lpp_updater_cfg / lpp_updater_stats /
+    lpp_averager_cfg have the C layout (offsets and sizes from the header,
+    compiled with gcc)."""
     import ctypes
 
-    fields = [f for f, _ in N.UpdaterCfg._fields_]
-    sfields = [f for f, _ in N.UpdaterStats._fields_]
+    structs = (("lpp_updater_cfg", N.UpdaterCfg), ("lpp_updater_stats", N.UpdaterStats),
+               ("lpp_averager_cfg", N.AveragerCfg))
     src = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{ROOT / "include" / "lpp_b200.h"}"',
-           'int main(void) {', 'printf("%zu %zu", sizeof(lpp_updater_cfg), sizeof(lpp_updater_stats));']
-    src += [f'printf(" %zu", offsetof(lpp_updater_cfg, {f}));' for f in fields]
-    src += [f'printf(" %zu", offsetof(lpp_updater_stats, {f}));' for f in sfields]
+           'int main(void) {']
+    want = []
+    for cname, py in structs:
+        src.append(f'printf(" %zu", sizeof({cname}));')
+        want.append(ctypes.sizeof(py))
+        for f, _ in py._fields_:
+            src.append(f'printf(" %zu", offsetof({cname}, {f}));')
+            want.append(getattr(py, f).offset)
     src += ['return 0; }']
     (tmp_path / "off.c").write_text("\n".join(src))
     subprocess.run(["gcc", "-I/usr/local/cuda/include", str(tmp_path / "off.c"), "-o",
                     str(tmp_path / "off")], check=True)
     got = [int(v) for v in subprocess.run([str(tmp_path / "off")], capture_output=True, text=True,
                                           check=True).stdout.split()]
-    want = [ctypes.sizeof(N.UpdaterCfg), ctypes.sizeof(N.UpdaterStats)]
-    want += [getattr(N.UpdaterCfg, f).offset for f in fields]
-    want += [getattr(N.UpdaterStats, f).offset for f in sfields]
     assert got == want
 
 

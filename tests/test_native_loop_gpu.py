@@ -151,3 +151,55 @@ def test_native_loop_mlp_and_lap():
         assert res.metrics[-1].train_loss < res.metrics[0].train_loss
     finally:
         tr.close()
+
+
+@pytest.mark.parametrize("tags", [True, False])
+def test_native_averager_round_protocol(tags):
+    """lpp_averager_run keeps the reference's averager contract
+    (test_engine.py:152-235): every round is joined by every worker, rounds
+    are numbered 1..n on both, the run ends on the drain round, the final
+    values are the last round's mean — which every arena holds once all
+    updaters have exited — and round stamps interleave with update stamps
+    as one permutation per worker."""
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.schedules import SyncScheme
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    cfg = _resnet_cfg(obj, budget=60, workers=2, updaters=3, track_writes=tags,
+                      sync=SyncScheme(total=60, period=4, switch_point=10))
+    tr = Trainer(cfg)
+    try:
+        assert tr.eng.native_averager() and tr.eng.native_loop()
+        res = tr.run()
+        per = {q: sorted(st.round for st in res.stamps if st.worker == q) for q in (0, 1)}
+        assert per[0] == per[1] == list(range(1, len(per[0]) + 1)) and len(per[0]) >= 3
+        for q in (0, 1):
+            arena = tr.eng.workers[q].store.arena.tensor.cpu().numpy()
+            np.testing.assert_allclose(arena, res.final_values, rtol=1e-6, atol=1e-6)
+            # stamps: rounds and updates draw from the same update-order counter
+            n_updates = res.counter_finals[q]
+            rounds_u = sorted(st.u for st in res.stamps if st.worker == q)
+            assert len(set(rounds_u)) == len(rounds_u)
+            assert max(rounds_u) <= n_updates + len(rounds_u)
+        if tags:
+            # the drain round stamped every element of worker 0's arena with
+            # the round stamps published by the owners (K5, add_assign)
+            t = tr.eng.workers[0].tags.cpu().numpy()
+            assert (t > 0).all()
+    finally:
+        tr.close()
+
+
+def test_native_averager_round_budget():
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    tr = Trainer(_resnet_cfg(obj, budget=10_000, workers=2, updaters=2, round_budget=5))
+    try:
+        res = tr.run()
+        assert max(st.round for st in res.stamps) >= 5      # + the drain round (engine.py:429)
+        assert max(res.counter_finals) < 10_000
+    finally:
+        tr.close()

@@ -1,6 +1,7 @@
-"""Native (C++) vs Python updater loop: minibatches/s and images/s on a
-host-bound tiny MLP, the config-0 small CNN and ResNet-20 (U=4, device
-sampling, record_mode off; CUDA-event device time)."""
+"""Native (C++) vs Python updater + averager loops: minibatches/s,
+images/s and averaging rounds/s on a host-bound tiny MLP, the config-0
+small CNN and ResNet-20 (U=4, device sampling, record_mode off; CUDA-event
+device time; sync period 1 for the first half, 16 after)."""
 import dataclasses, json, sys
 from pathlib import Path
 import numpy as np
@@ -23,7 +24,10 @@ for name, obj, B, K in cases:
         torch.cuda.synchronize()
         r = tr.run(K * 4, evaluate=False)
         steps = sum(r.counter_finals)
-        print(json.dumps({"model": name, "loop": loop, "native": tr.eng.native_loop(), "B": B,
+        rounds = max((st.round for st in r.stamps), default=0)
+        print(json.dumps({"model": name, "loop": loop, "native": tr.eng.native_loop(),
+                          "native_averager": tr.eng.native_averager(), "B": B,
+                          "rounds": rounds, "rounds_per_s": round(rounds / (r.device_ms / 1e3)),
                           "minibatches_per_s": round(steps / (r.device_ms / 1e3)),
                           "images_per_s": round(steps * B / (r.device_ms / 1e3))}), flush=True)
         tr.close()
