@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, algo, out_q):
+def _rank_main(rank, world, port, algo, out_q, loops=("auto", "auto")):
     import sys
     from pathlib import Path
 
@@ -52,7 +52,8 @@ def _rank_main(rank, world, port, algo, out_q):
                     partition=make_partition(obj.dim, (0, e[2], obj.dim) if algo == "lpp_sgd" else (0, obj.dim)),
                     lr=constant_schedule(0.05, budget), sync=SyncScheme(total=budget, period=4),
                     budget=budget, warm_start_budget=20, workers=world,
-                    updaters=2 if algo == "lpp_sgd" else 1, batch_size=8, seed=1, evaluate=False)
+                    updaters=2 if algo == "lpp_sgd" else 1, batch_size=8, seed=1, evaluate=False,
+                    host_loop=loops[rank])
     g = ProcessGroup(workers=world, max_rounds=4096)
     res = run_experiment(cfg, group=g)
     rounds = [st.round for st in res.stamps]
@@ -61,14 +62,18 @@ def _rank_main(rank, world, port, algo, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo", ["lpp_sgd", "mb_sgd", "pl_sgd"])
-def test_two_process_group_on_one_gpu(algo):
+@pytest.mark.parametrize("algo,loops", [("lpp_sgd", ("auto", "auto")), ("lpp_sgd", ("python", "auto")),
+                                        ("mb_sgd", ("auto", "auto")), ("pl_sgd", ("auto", "auto"))])
+def test_two_process_group_on_one_gpu(algo, loops):
+    """("python", "auto"): rank 0 runs the Python averager, rank 1 the native
+    one (lpp_averager_run) — the two implement the same protocol over the
+    shared control block."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, algo, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, algo, q, loops)) for r in range(2)]
     for p in ps:
         p.start()
     res = sorted(q.get(timeout=300) for _ in ps)
