@@ -1,0 +1,177 @@
+"""Native (C++) updater and averager loops of the asynchronous engine.
+
+``lpp_updater_run`` / ``lpp_averager_run`` (``csrc/updater.cu``) run one
+updater's step loop (a10, engine.py:289-383) and one worker's averager
+(a11, engine.py:385-453) GIL-free; this mixin decides when they apply
+(the throughput configuration: no per-update records, device sampling,
+p2p averaging without eval points / quiescent pauses) and builds their
+C configuration structs from the engine's arenas, streams, captured graphs
+and host counters.  The Python loops in ``async_engine`` remain the
+record / parity / host-batch paths; both drive the same kernels through the
+same C ABI, and the two averagers share one round protocol.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .records import AveragerStamp
+
+
+class NativeLoops:
+    """Mixin of ``async_engine._Engine``."""
+
+    def native_loop(self) -> bool:
+        """Whether updaters run the C++ loop (lpp_updater_run): the
+        throughput configuration — async, device sampling, no per-update
+        records, no host batches / loss read-back / quiescent pauses."""
+        cfg = self.cfg
+        ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
+              and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs
+              and not self.host_batches and not self.read_loss and not cfg.apply_priority)
+        if cfg.host_loop == "native" and not ok:
+            raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
+                             "sampling='device', CUDA graphs, no host batches / loss read-back / "
+                             "quiescent / apply_priority")
+        return ok and cfg.host_loop != "python"
+
+    def updater_cfg(self, w: _Worker, r: int) -> tuple:
+        """The ``lpp_updater_cfg`` of updater r of worker w (+ the arrays it
+        points into, which the caller keeps alive for the run)."""
+        cfg = self.cfg
+        sched = cfg.lr
+        nb = cfg.partition.num_blocks
+        prog = w.programs[r]
+        lo = np.zeros(nb + 1, dtype=np.int64)
+        hi = np.zeros(nb + 1, dtype=np.int64)
+        execs = (ctypes.c_void_p * (nb + 1))()
+        flops = np.zeros(nb + 1, dtype=np.int64)
+        for b in range(nb + 1):
+            blk = cfg.partition.block(b)
+            lo[b], hi[b] = blk.start, blk.stop
+            flops[b] = self._flops_of[b]
+            if (b, 0) in prog.execs:
+                execs[b] = prog.execs[(b, 0)]
+        ms = np.ascontiguousarray(sched.milestones, dtype=np.int64)
+        tracks = w.tags is not None
+        k = w.tag_pick if tracks else 0
+        c = N.UpdaterCfg()
+        c.sample_counter = w.store.sample_counter._a
+        c.update_order = w.store.update_order_counter._a
+        c.stop = self.ctrl.stop._a
+        c.last_avg_stamp = w.last_avg_stamp._a
+        c.budget = self.budget
+        c.lr_kind = 0 if sched.kind == "cosine" else 1
+        c.n_milestones = len(ms)
+        c.alpha0, c.peak, c.gamma = sched.alpha0, sched.peak, sched.gamma
+        c.warmup, c.total = sched.warmup, sched.total
+        c.milestones = ms.ctypes.data if len(ms) else None
+        c.lpp = int(cfg.algo == "lpp_sgd")
+        c.num_blocks, c.rank = nb, r + 1
+        c.fused = int(self.fused())
+        c.warm_start = cfg.warm_start_budget
+        c.block_lo, c.block_hi = lo.ctypes.data, hi.ctypes.data
+        c.graph_exec = ctypes.addressof(execs)
+        c.flops_of = flops.ctypes.data
+        c.x, c.g = w.store.arena.ptr, w.grads[r].ptr
+        c.m = w.moms[r].ptr if w.moms[r] is not None else None
+        c.replica = w.replicas[r].ptr
+        c.tags = w.tag_arena.ptr if tracks else None
+        c.n = self.dim
+        c.mu, c.wd = cfg.momentum, cfg.weight_decay
+        c.apply_mode = N.MODES[cfg.apply_mode]
+        c.in_flight = cfg.in_flight
+        c.tag_pick = k
+        c.time_apply = int(self.time_apply)
+        c.tag_seed = (cfg.seed * 1_000_003 + w.q * 1009 + r + 1) & (2**64 - 1)
+        if tracks:
+            c.tag_idx_pinned = w.tag_idx_pinned[r].data_ptr()
+            c.tag_idx_dev = w.tag_idx_dev[r].data_ptr()
+            c.tag_out_dev = w.tag_out_dev[r].data_ptr()
+            c.tag_out_pinned = w.tag_pinned[r].data_ptr()
+        c.classified = self.classified_count._a
+        c.clean = self.clean_count._a
+        c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
+        c.stream = w.streams[r].cuda_stream
+        return c, (lo, hi, execs, flops, ms)
+
+    def updater_native(self, q: int, r: int) -> None:
+        """a10 in native code: the whole loop is one GIL-free C call."""
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
+        try:
+            c, keep = self.updater_cfg(w, r)
+            st = N.updater_run(c)
+            del keep
+            self.flops.add(int(st.flops))
+            if self.time_apply:
+                with self.native_lock:
+                    self.native_apply[0] += int(st.apply_launches)
+                    self.native_apply[1] += float(st.apply_ms)
+                    self.native_apply[2] += float(st.apply_bytes)
+        except BaseException as exc:  # surfaced after join (engine.py:456-463)
+            self.fail(exc)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
+            if w.exited.add(1) + 1 == self.cfg.updaters:
+                self.ctrl.drained.add(1)
+
+    def native_averager(self) -> bool:
+        """Whether averagers run the C++ round loop (lpp_averager_run): p2p
+        averaging without quiescent pauses, eval points or full records."""
+        cfg = self.cfg
+        return (cfg.host_loop != "python" and cfg.schedule == "async" and not cfg.quiescent
+                and not self.nvls and cfg.eval_interval == 0 and cfg.record_mode != "full")
+
+    def averager_native(self, q: int) -> None:
+        """a11 in native code: the round protocol + K4 in one GIL-free call."""
+        cfg = self.cfg
+        w = self.workers[q]
+        torch.cuda.set_device(w.device)
+        ctrl = self.ctrl
+        Q = cfg.workers
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(self.nvtx)
+        try:
+            arenas = (ctypes.c_void_p * Q)(*self.arena_ptrs)
+            tags = (ctypes.c_void_p * Q)(*self.tag_ptrs) if self.tag_ptrs is not None else None
+            cap = min(ctrl.max_rounds, 1 << 20)
+            rec = np.zeros((cap, 5), dtype=np.int64)
+            wall = np.zeros(cap, dtype=np.float64)
+            lo, hi = self.shards[q]
+            c = N.AveragerCfg()
+            c.ctrl = ctrl.buf.ctypes.data
+            c.max_rounds = ctrl.max_rounds
+            c.workers, c.q, c.updaters = Q, q, cfg.updaters
+            c.tagged = int(self.tag_ptrs is not None)
+            c.sample_counter = w.store.sample_counter._a
+            c.update_order = w.store.update_order_counter._a
+            c.exited = w.exited._a
+            c.last_avg_stamp = w.last_avg_stamp._a
+            c.synced_at = w.synced_at._a
+            c.switch_point, c.period = cfg.sync.switch_point, cfg.sync.period
+            c.stop_after = cfg.round_budget or 0
+            c.arenas = ctypes.addressof(arenas)
+            c.tags = ctypes.addressof(tags) if tags is not None else None
+            c.lo, c.hi, c.n = lo, hi, self.dim
+            c.mean_out = w.mean_out.data_ptr()
+            c.stream = w.avg_stream.cuda_stream
+            c.t0 = self.t0
+            c.rec, c.rec_wall_ms, c.max_records = rec.ctypes.data, wall.ctypes.data, cap
+            n = N.averager_run(c)
+            for i in range(min(n, cap)):
+                r, u, s_cur, k_delta, _ = (int(v) for v in rec[i])
+                self.stamps[q].append(AveragerStamp(worker=q, round=r, u=u, s_cur=s_cur,
+                                                    k_delta=k_delta, wall_ms=float(wall[i])))
+        except BaseException as exc:  # surfaced after join (engine.py:456-463)
+            self.fail(exc)
+        finally:
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
