@@ -63,29 +63,36 @@ def _rank_main(rank, world, port, algo, out_q, loops=("auto", "auto")):
 
 
 @pytest.mark.parametrize("algo,loops", [("lpp_sgd", ("auto", "auto")), ("lpp_sgd", ("python", "auto")),
+                                        ("lpp_sgd", ("auto", "python", "auto", "auto")),
                                         ("mb_sgd", ("auto", "auto")), ("pl_sgd", ("auto", "auto"))])
-def test_two_process_group_on_one_gpu(algo, loops):
-    """("python", "auto"): rank 0 runs the Python averager, rank 1 the native
-    one (lpp_averager_run) — the two implement the same protocol over the
-    shared control block."""
+def test_process_group_on_one_gpu(algo, loops):
+    """One process per worker (2 or 4 ranks on one GPU).  A "python" entry
+    runs that rank's Python averager / updater loops, "auto" the native ones
+    (lpp_averager_run) — both implement the same protocol over the shared
+    control block, so mixed groups must agree."""
     import torch.multiprocessing as mp
 
+    world = len(loops)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, algo, q, loops)) for r in range(2)]
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, algo, q, loops)) for r in range(world)]
     for p in ps:
         p.start()
     res = sorted(q.get(timeout=300) for _ in ps)
     for p in ps:
         p.join(60)
         assert p.exitcode == 0
-    (_, c0, r0, f0), (_, c1, r1, f1) = res
-    f0, f1 = np.array(f0), np.array(f1)
-    assert np.all(np.isfinite(f0))
+    counters = [c for _, c, _, _ in res]
+    rounds = [r for _, _, r, _ in res]
+    finals = [np.array(f) for _, _, _, f in res]
+    assert np.all(np.isfinite(finals[0]))
     if algo == "lpp_sgd":
-        assert c0 == [202] and c1 == [202]
-        assert r0 == r1 == list(range(1, len(r0) + 1)) and len(r0) >= 2
-        assert np.array_equal(f0, f1)     # both ranks gather the same final mean
+        assert all(c == [202] for c in counters)
+        assert all(r == rounds[0] for r in rounds)
+        assert rounds[0] == list(range(1, len(rounds[0]) + 1)) and len(rounds[0]) >= 2
+        for f in finals[1:]:
+            assert np.array_equal(f, finals[0])     # every rank gathers the same final mean
     else:
-        np.testing.assert_allclose(f0, f1, atol=1e-6)
+        for f in finals[1:]:
+            np.testing.assert_allclose(f, finals[0], atol=1e-6)
