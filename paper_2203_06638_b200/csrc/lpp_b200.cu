@@ -554,7 +554,8 @@ extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* rep
   cudaStream_t st = (cudaStream_t)stream;
   bool WD = wd != 0.f, MOM = mu != 0.f;
   // one vector per thread per grid stride: unrolling (2, 4 vectors with all
-  // loads hoisted) measured no faster at d20/d50 and 6 % slower at d18; 64-
+  // loads hoisted) measured no faster at d20/d50 and 4-10 % slower at d18
+  // (with both the returning-atomic and the reduction + re-read bodies); 64-
   // or 128-thread CTAs (easier to fit between other streams' CTAs) changed
   // neither the in-situ d20 time nor images/s
 #define FUSED_LAUNCH(W, M)                                                                      \
