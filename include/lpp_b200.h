@@ -317,6 +317,8 @@ typedef struct {
   int64_t* clean;
   double apply_bytes_per_elem;    /* algorithmic bytes per block element */
   void* stream;
+  void* apply_stream;             /* NULL: apply on `stream`; else a (high-priority) stream
+                                     ordered after the step's graph by events */
 } lpp_updater_cfg;
 
 typedef struct {

@@ -66,7 +66,7 @@ class UpdaterCfg(ctypes.Structure):
         ("tag_pick", _c.c_int32), ("time_apply", _c.c_int32), ("tag_seed", _c.c_uint64),
         ("tag_idx_pinned", _vp), ("tag_idx_dev", _vp), ("tag_out_dev", _vp),
         ("tag_out_pinned", _vp), ("classified", _vp), ("clean", _vp),
-        ("apply_bytes_per_elem", _c.c_double), ("stream", _vp),
+        ("apply_bytes_per_elem", _c.c_double), ("stream", _vp), ("apply_stream", _vp),
     ]
 
 

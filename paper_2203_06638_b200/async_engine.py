@@ -411,8 +411,7 @@ class _Engine(NativeLoops):
         """Whether async steps use the fused apply+next-snapshot kernel."""
         cfg = self.cfg
         return (cfg.fuse_snapshot and cfg.schedule == "async" and not cfg.quiescent
-                and cfg.record_mode != "full" and cfg.apply_mode != "plain"
-                and not cfg.apply_priority)
+                and cfg.record_mode != "full" and cfg.apply_mode != "plain")
 
     def gather_tags(self, w: _Worker, r: int, slot: int, tag_idx) -> None:
         """K5: sampled tags of the NEXT snapshot into slot, then D2H (on the
@@ -454,21 +453,30 @@ class _Engine(NativeLoops):
             if tracks:
                 self.gather_tags(w, r, next_slot, next_tag_idx)                          # K5 (next)
             mom = w.moms[r]
+            astream = stream
+            if w.apply_streams is not None:
+                astream = w.apply_streams[r]
+                w.graph_done[r].record(stream)
+                astream.wait_event(w.graph_done[r])
+                sp = astream.cuda_stream
             if self.time_apply:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+                e0.record(astream)
             N.apply_snapshot(w.store.arena.ptr, w.grads[r].ptr,                           # K1+K3
                              mom.ptr if mom is not None else None, w.replicas[r].ptr,
                              w.tag_arena.ptr if tracks else None, self.dim, blk.start, blk.stop,
                              float(lr), None, cfg.momentum, cfg.weight_decay, u, sp)
             if self.time_apply:
-                e1.record(stream)
+                e1.record(astream)
                 # block: read g, RMW x, (+m), (+tag); whole arena: read x outside
                 # the block, write the replica
                 nbytes = self.apply_bytes_per_elem * blk.length + 4 * (self.dim - blk.length) \
                     + 4 * self.dim
                 self.apply_events.append((e0, e1, nbytes))
+            if astream is not stream:
+                w.apply_done[r].record(astream)
+                stream.wait_event(w.apply_done[r])
             if self.read_loss:
                 self.read_back_loss(w, r, slot, buf)
 

@@ -155,9 +155,12 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   const int depth = F + 2;
   cudaStream_t stream = (cudaStream_t)c->stream;
 
-  Events done, t0, t1;
+  cudaStream_t astream = c->apply_stream ? (cudaStream_t)c->apply_stream : stream;
+  const bool side = astream != stream;
+  Events done, t0, t1, order;
   int rc;
   if ((rc = done.make(F, cudaEventDisableTiming)) != LPP_OK) return rc;
+  if (side && (rc = order.make(2, cudaEventDisableTiming)) != LPP_OK) return rc;
   if (c->time_apply) {
     if ((rc = t0.make(F, cudaEventDefault)) != LPP_OK) return rc;
     if ((rc = t1.make(F, cudaEventDefault)) != LPP_OK) return rc;
@@ -223,25 +226,33 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if ((rc = lpp_graph_launch(c->graph_exec[b], stream)) != LPP_OK) return rc;       // fwd+bwd
     if (c->fused && K > 0 && (rc = gather(next_slot)) != LPP_OK) return rc;          // K5 (next)
-    if (c->time_apply) CUDA_TRY(cudaEventRecord(t0.ev[k], stream));
+    if (side) {  // the apply on its own (high-priority) stream, after the graph
+      CUDA_TRY(cudaEventRecord(order.ev[0], stream));
+      CUDA_TRY(cudaStreamWaitEvent(astream, order.ev[0], 0));
+    }
+    if (c->time_apply) CUDA_TRY(cudaEventRecord(t0.ev[k], astream));
     if (c->fused) {
       rc = lpp_apply_snapshot(c->x, c->g, c->m, c->replica, tagged ? c->tags : nullptr, c->n,
                               (size_t)lo, (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u,
-                              stream);                                                // K1+K3
+                              astream);                                               // K1+K3
       bytes_of[k] = c->apply_bytes_per_elem * (double)len + 4.0 * (double)(c->n - len) +
                     4.0 * (double)c->n;
     } else if (tagged) {
       rc = lpp_apply_sgd_tagged(c->x + lo, c->g + lo, c->m ? c->m + lo : nullptr, (size_t)len,
                                 lr32, nullptr, c->mu, c->wd, c->apply_mode, c->tags + lo,
-                                (int32_t)u, stream);                                  // K1/K2+K5
+                                (int32_t)u, astream);                                 // K1/K2+K5
       bytes_of[k] = c->apply_bytes_per_elem * (double)len;
     } else {
       rc = lpp_apply_sgd(c->x + lo, c->g + lo, c->m ? c->m + lo : nullptr, (size_t)len, lr32,
-                         nullptr, c->mu, c->wd, c->apply_mode, stream);               // K1/K2
+                         nullptr, c->mu, c->wd, c->apply_mode, astream);              // K1/K2
       bytes_of[k] = c->apply_bytes_per_elem * (double)len;
     }
     if (rc != LPP_OK) return rc;
-    if (c->time_apply) CUDA_TRY(cudaEventRecord(t1.ev[k], stream));
+    if (c->time_apply) CUDA_TRY(cudaEventRecord(t1.ev[k], astream));
+    if (side) {
+      CUDA_TRY(cudaEventRecord(order.ev[1], astream));
+      CUDA_TRY(cudaStreamWaitEvent(stream, order.ev[1], 0));
+    }
     CUDA_TRY(cudaEventRecord(done.ev[k], stream));
     used[k] = 1;
     claim_of[k] = k_claim;

@@ -32,11 +32,11 @@ class NativeLoops:
         cfg = self.cfg
         ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
               and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs
-              and not self.host_batches and not self.read_loss and not cfg.apply_priority)
+              and not self.host_batches and not self.read_loss)
         if cfg.host_loop == "native" and not ok:
             raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
                              "sampling='device', CUDA graphs, no host batches / loss read-back / "
-                             "quiescent / apply_priority")
+                             "quiescent")
         return ok and cfg.host_loop != "python"
 
     def updater_cfg(self, w: _Worker, r: int) -> tuple:
@@ -97,6 +97,7 @@ class NativeLoops:
         c.clean = self.clean_count._a
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
         c.stream = w.streams[r].cuda_stream
+        c.apply_stream = w.apply_streams[r].cuda_stream if w.apply_streams is not None else None
         return c, (lo, hi, execs, flops, ms)
 
     def updater_native(self, q: int, r: int) -> None:
