@@ -114,8 +114,7 @@ class _Worker:
             # optional: the apply of every updater on its own high-priority
             # stream, so parameter updates are not queued behind other
             # streams' convolutions (less staleness); ordered by events
-            self.apply_streams = ([torch.cuda.Stream(device=device, priority=-1) for _ in range(U)]
-                                  if cfg.apply_priority else None)
+            self.apply_streams = [torch.cuda.Stream(device=device, priority=-1) for _ in range(U)]
             self.graph_done = [torch.cuda.Event() for _ in range(U)]
             self.apply_done = [torch.cuda.Event() for _ in range(U)]
         self.replicas = [Arena(d, device) for _ in range(U)]
@@ -262,6 +261,7 @@ class _Engine(NativeLoops):
         self.err_lock = threading.Lock()
         self.apply_events: list = []
         self.native_apply = [0, 0.0, 0.0]   # launches, ms, bytes (native loop, time_apply)
+        self.side_apply = False             # applies on the high-priority stream (set per run)
         self.native_lock = threading.Lock()
         self.t0 = 0.0
         self.budget = cfg.budget
@@ -349,7 +349,7 @@ class _Engine(NativeLoops):
             off = 4 * blk.start
             mom = w.moms[r]
             astream = stream
-            if w.apply_streams is not None:
+            if self.side_apply:
                 astream = w.apply_streams[r]
                 w.graph_done[r].record(stream)
                 astream.wait_event(w.graph_done[r])
@@ -454,7 +454,7 @@ class _Engine(NativeLoops):
                 self.gather_tags(w, r, next_slot, next_tag_idx)                          # K5 (next)
             mom = w.moms[r]
             astream = stream
-            if w.apply_streams is not None:
+            if self.side_apply:
                 astream = w.apply_streams[r]
                 w.graph_done[r].record(stream)
                 astream.wait_event(w.graph_done[r])
@@ -772,6 +772,7 @@ class _Engine(NativeLoops):
 
     def run_async(self) -> float:
         cfg = self.cfg
+        self.side_apply = self.apply_on_side()
         starts = self._device_span_start()
         threads = []
         for q in self.local_workers:
@@ -802,6 +803,7 @@ class _Engine(NativeLoops):
     def run_serialized(self) -> float:
         """Canonical deterministic schedule (oracle/schedule.py)."""
         cfg = self.cfg
+        self.side_apply = bool(cfg.apply_priority)
         if self.group is not None:
             raise ValueError("the serialized schedule runs in one process")
         n = cfg.objective.n_samples

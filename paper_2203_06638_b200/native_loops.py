@@ -39,6 +39,11 @@ class NativeLoops:
                              "quiescent")
         return ok and cfg.host_loop != "python"
 
+    def apply_on_side(self) -> bool:
+        """Whether applies run on the per-updater high-priority stream."""
+        p = self.cfg.apply_priority
+        return self.native_loop() if p is None else bool(p)
+
     def updater_cfg(self, w: _Worker, r: int) -> tuple:
         """The ``lpp_updater_cfg`` of updater r of worker w (+ the arrays it
         points into, which the caller keeps alive for the run)."""
@@ -97,7 +102,7 @@ class NativeLoops:
         c.clean = self.clean_count._a
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
         c.stream = w.streams[r].cuda_stream
-        c.apply_stream = w.apply_streams[r].cuda_stream if w.apply_streams is not None else None
+        c.apply_stream = w.apply_streams[r].cuda_stream if self.side_apply else None
         return c, (lo, hi, execs, flops, ms)
 
     def updater_native(self, q: int, r: int) -> None:
