@@ -40,9 +40,18 @@ class NativeLoops:
         return ok and cfg.host_loop != "python"
 
     def apply_on_side(self) -> bool:
-        """Whether applies run on the per-updater high-priority stream."""
+        """Whether applies run on the per-updater high-priority stream.
+
+        Auto (``apply_priority=None``): native loop and U <= 4.  The side
+        stream doubles a worker's streams; past the device's 8 hardware work
+        queues (CUDA_DEVICE_MAX_CONNECTIONS) streams share queues and
+        serialise — measured -12 % images/s at U = 6 (neutral at U = 4, and
+        raising the queue count to 32 costs 2-3 % everywhere;
+        tools/ab_priority_streams.py)."""
         p = self.cfg.apply_priority
-        return self.native_loop() if p is None else bool(p)
+        if p is None:
+            return self.native_loop() and self.cfg.updaters <= 4
+        return bool(p)
 
     def updater_cfg(self, w: _Worker, r: int) -> tuple:
         """The ``lpp_updater_cfg`` of updater r of worker w (+ the arrays it

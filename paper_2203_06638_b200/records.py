@@ -53,9 +53,10 @@ class RunConfig:
     averaging: str = "p2p"           # "p2p": owner-computes over peer arenas; "nvls": in-switch
     apply_priority: bool | None = None  # K1/K2 (or fused K1+K3) on a high-priority stream per
                                      # updater, ordered by events, so the apply is not queued behind
-                                     # other streams' kernels; None = on for the native loop
-                                     # (in-situ apply -33 %, images/s neutral), off for the Python
-                                     # loop (its 4 extra calls per step cost host time)
+                                     # other streams' kernels; None = on for the native loop with
+                                     # U <= 4 (in-situ apply -33 %, images/s neutral), off for the
+                                     # Python loop (4 extra calls per step cost host time) and for
+                                     # U > 4 (2U streams exceed the 8 hardware queues)
     fuse_snapshot: bool = True       # async: fuse each apply with the next step's snapshot
     track_writes: bool | None = None  # K5 write tags; None = reference default (lap/lpp)
     record_tensors: bool = True      # record_mode="full": keep per-update grad/snapshot copies
