@@ -203,3 +203,32 @@ def test_native_averager_round_budget():
         assert max(res.counter_finals) < 10_000
     finally:
         tr.close()
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_native_loop_is_bitwise_the_python_loop_without_concurrency(fuse):
+    """Q = U = 1 takes the concurrency out: both loops then claim the same
+    slots, draw the same in-graph batches (same sampler key and device step
+    counter), compute the same lr / block and launch the same kernels — so
+    the native loop's final model must equal the Python loop's bit for bit."""
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.objectives import MlpObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    rng = np.random.default_rng(4)
+    X = rng.normal(size=(256, 24))
+    y = rng.integers(0, 5, 256)
+    obj = MlpObjective(X, y, (12, 12), 5)
+    cfg = RunConfig(algo="lpp_sgd", objective=obj,
+                    partition=make_partition(obj.dim, (0, obj.edges[2], obj.dim)),
+                    lr=LrSchedule(kind="cosine", alpha0=0.05, total=120, warmup=10),
+                    sync=SyncScheme(total=120, period=4), budget=120, warm_start_budget=10,
+                    workers=1, updaters=1, batch_size=16, seed=7, momentum=0.9, weight_decay=5e-4,
+                    sampling="device", record_mode="off", evaluate=False, fuse_snapshot=fuse)
+    nat = run_experiment(dataclasses.replace(cfg, host_loop="native"))
+    py = run_experiment(dataclasses.replace(cfg, host_loop="python"))
+    assert nat.counter_finals == py.counter_finals == [121]
+    assert nat.flops == py.flops
+    assert np.array_equal(nat.final_values, py.final_values)
+    assert not np.array_equal(nat.final_values, nat.x0.astype(np.float32))
