@@ -5,8 +5,8 @@
 be assigned, one CUDA graph that does
 
     gather batch (index_select from device data, or a staged host batch)
-    -> zero the block's gradient slice
-    -> forward -> loss -> backward restricted to the block's leaf tensors
+    -> forward -> loss -> autograd.grad over the block's leaf tensors
+    -> one multi-tensor copy of those gradients into the gradient arena
 
 so the block gradient lands in ``grads[block.start:block.stop]`` — exactly
 the range the apply kernel then reads.  This is ``Objective.grad_block``
@@ -27,7 +27,7 @@ class StepProgram:
     def __init__(self, obj, device: torch.device, replica: torch.Tensor, grads: torch.Tensor,
                  blocks: dict[int, Block], batch_size: int, stream: torch.cuda.Stream,
                  input_mode: str = "index", use_graphs: bool = True, warmup: int = 2,
-                 seed: int = 0, nbuf: int = 1):
+                 seed: int = 0, nbuf: int = 1, grad_mode: str = "copy"):
         if input_mode not in ("index", "batch", "random"):
             raise ValueError(f"unknown input mode {input_mode!r}")
         self.obj = obj
@@ -64,9 +64,16 @@ class StepProgram:
             self._sampler = _native.sample_indices
         self.blocks = dict(blocks)
         self.leaves = {}
+        self.grad_views = {}
         for bid, blk in self.blocks.items():
             first, last = obj.tensors_of_block(blk)
             self.leaves[bid] = self.bound.params[first:last + 1]
+            self.grad_views[bid] = [p.grad for p in self.leaves[bid]]
+        # "copy": autograd.grad over the block's leaves, then one multi-tensor
+        # copy into the gradient arena's views; "accumulate": zero the block's
+        # slice and let backward() accumulate into the views (one add kernel
+        # per tensor) — same values, ~45 fewer launches per step for "copy"
+        self.grad_mode = grad_mode
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.use_graphs = use_graphs
         with torch.cuda.stream(stream):
@@ -104,9 +111,13 @@ class StepProgram:
         else:
             xb = self.feats.index_select(0, self.idx)
             yb = self.labels.index_select(0, self.idx)
-        self.grads[blk.start:blk.stop].zero_()
         loss = self.obj.loss_on(self.bound, xb, yb)
-        loss.backward(inputs=self.leaves[bid])
+        if self.grad_mode == "copy":
+            grads = torch.autograd.grad(loss, self.leaves[bid])
+            torch._foreach_copy_(self.grad_views[bid], list(grads))
+        else:
+            self.grads[blk.start:blk.stop].zero_()
+            loss.backward(inputs=self.leaves[bid])
         self.losses[buf].copy_(loss.detach())
 
     def loss_of(self, buf: int) -> torch.Tensor:
