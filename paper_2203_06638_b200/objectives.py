@@ -44,11 +44,18 @@ class GradResult:
 
 
 class Bound:
-    """A model whose parameters / grads are views into two arenas."""
+    """A model whose parameters / grads are views into two arenas.
 
-    def __init__(self, params: list[torch.Tensor], forward):
+    ``grad_views[i]`` is where the gradient of ``params[i]`` belongs in the
+    fp32 gradient arena (by default ``params[i].grad``; a bf16 shadow weight
+    has an fp32 view here instead).  ``mixed`` is False when the bound model
+    already computes in its compute dtype (no autocast needed)."""
+
+    def __init__(self, params: list[torch.Tensor], forward, grad_views=None, mixed: bool = True):
         self.params = params
         self.forward = forward  # forward(xb) -> logits
+        self.grad_views = grad_views if grad_views is not None else [p.grad for p in params]
+        self.mixed = mixed
 
 
 class ArenaObjective:
@@ -104,11 +111,11 @@ class ArenaObjective:
         return t.to(device=device, dtype=torch.float32).contiguous()
 
     def loss_on(self, bound: Bound, xb: torch.Tensor, yb: torch.Tensor) -> torch.Tensor:
-        if self.autocast_dtype is not None:
+        if self.autocast_dtype is not None and bound.mixed:
             with torch.autocast("cuda", dtype=self.autocast_dtype):
                 logits = bound.forward(xb)
             return F.cross_entropy(logits.float(), yb)
-        return F.cross_entropy(bound.forward(xb), yb)
+        return F.cross_entropy(bound.forward(xb).float(), yb)
 
     def loss(self, x, batch) -> float:
         device = torch.device("cuda", torch.cuda.current_device())
@@ -127,7 +134,8 @@ class ArenaObjective:
         bound = self.bind(xp, g)
         idx = torch.as_tensor(np.asarray(batch), device=device, dtype=torch.long)
         loss = self.loss_on(bound, self.features_on(device)[idx], self.labels_on(device)[idx])
-        loss.backward(inputs=bound.params[first:last + 1])
+        grads = torch.autograd.grad(loss, bound.params[first:last + 1])
+        torch._foreach_copy_(bound.grad_views[first:last + 1], list(grads))
         n = len(idx)
         back = n * self.backward_cost(block)
         return GradResult(g[block.start:block.stop], n * self.forward_cost() + back, back, n)
@@ -493,7 +501,7 @@ class ResNetObjective(ArenaObjective):
     def __init__(self, arch: str = "resnet20", n_samples: int = 8192, seed: int = 0,
                  channels_last: bool = True, autocast: str | None = "bf16",
                  data: str = "device", n_classes: int | None = None,
-                 pattern_scale: float = 0.0):
+                 pattern_scale: float = 0.0, shadow_weights: bool = True):
         if arch not in _ARCHS:
             raise ValueError(f"unknown arch {arch!r}")
         cls, shape, k = _ARCHS[arch]
@@ -512,6 +520,12 @@ class ResNetObjective(ArenaObjective):
         self._feat_cache, self._lab_cache = {}, {}
         self._template = cls(self.n_classes)
         self.param_names = [n for n, _ in self._template.named_parameters()]
+        # bf16 compute: conv / linear parameters live in a bf16 shadow (the
+        # tensors autocast would cast); BatchNorm parameters stay fp32
+        self.shadow_weights = shadow_weights and self.autocast_dtype is not None
+        self._compute_in_shadow = [
+            isinstance(self._template.get_submodule(n.rsplit(".", 1)[0]), (nn.Conv2d, nn.Linear))
+            for n in self.param_names]
         self.param_shapes = [tuple(p.shape) for p in self._template.parameters()]
         self.layer_param_counts = tuple(int(p.numel()) for p in self._template.parameters())
         self._finish_layout()
@@ -582,26 +596,45 @@ class ResNetObjective(ArenaObjective):
         return m
 
     def bind(self, arena: torch.Tensor, grad_arena: torch.Tensor | None, module: nn.Module | None = None) -> Bound:
+        """Parameters become views into ``arena`` (fp32).  With bf16 compute
+        (``autocast="bf16"``) the conv / linear weights are instead views
+        into a bf16 shadow of the arena that the forward refreshes with ONE
+        cast kernel, and the model runs natively in bf16: the same values
+        autocast produces (round-to-nearest casts of the same fp32 weights,
+        bf16 grads widened exactly into the fp32 gradient arena) without its
+        per-tensor cast kernels in forward and backward (44 -> 1 per step)."""
         device = arena.device
         if module is None:
             module = self.make_module(device)
         params = list(module.parameters())
+        shadow_dtype = self.autocast_dtype if self.shadow_weights else None
+        shadow = (torch.empty(arena.shape[0], dtype=shadow_dtype, device=device)
+                  if shadow_dtype is not None else None)
+        grad_views = []
         for i, p in enumerate(params):
             lo, hi = self.edges[i], self.edges[i + 1]
             shape = self.param_shapes[i]
-            view = self._view(arena[lo:hi], shape)
-            p.data = view
-            if grad_arena is not None:
-                p.grad = self._view(grad_arena[lo:hi], shape)
+            gview = self._view(grad_arena[lo:hi], shape) if grad_arena is not None else None
+            if shadow is not None and self._compute_in_shadow[i]:
+                p.data = self._view(shadow[lo:hi], shape)
+                p.grad = None
+            else:
+                p.data = self._view(arena[lo:hi], shape)
+                if gview is not None:
+                    p.grad = gview
+            grad_views.append(gview)
             p.requires_grad_(grad_arena is not None)
         cl = self.channels_last
 
         def forward(xb):
+            if shadow is not None:
+                shadow.copy_(arena)                 # fp32 arena -> bf16 weights, one kernel
+                xb = xb.to(shadow_dtype)
             if cl:
                 xb = xb.contiguous(memory_format=torch.channels_last)
             return module(xb)
 
-        b = Bound(params, forward)
+        b = Bound(params, forward, grad_views=grad_views, mixed=shadow is None)
         b.module = module
         return b
 

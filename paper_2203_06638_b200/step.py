@@ -68,12 +68,15 @@ class StepProgram:
         for bid, blk in self.blocks.items():
             first, last = obj.tensors_of_block(blk)
             self.leaves[bid] = self.bound.params[first:last + 1]
-            self.grad_views[bid] = [p.grad for p in self.leaves[bid]]
+            self.grad_views[bid] = self.bound.grad_views[first:last + 1]
         # "copy": autograd.grad over the block's leaves, then one multi-tensor
         # copy into the gradient arena's views; "accumulate": zero the block's
         # slice and let backward() accumulate into the views (one add kernel
         # per tensor) — same values, ~45 fewer launches per step for "copy"
         self.grad_mode = grad_mode
+        if grad_mode == "accumulate" and not self.bound.mixed:
+            raise ValueError("grad_mode='accumulate' needs fp32 parameters (bf16 shadow weights "
+                             "have no arena .grad views)")
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.use_graphs = use_graphs
         with torch.cuda.stream(stream):
