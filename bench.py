@@ -3,7 +3,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (BASELINE.json configs[1]): ResNet-20 on synthetic CIFAR-10-shaped
-data (N(0,1) images, 50,000 x 3x32x32 fp32 = 614 MB resident in HBM, larger
+data (N(0,1) images, 50,000 x 32x32x3 stored in the bf16 compute dtype = 307 MB resident in HBM, larger
 than the 126 MB L2), LPP-SGD with U = 4 Hogwild CUDA streams per GPU,
 B = 128 per stream, 4-block PASSM+ partition (balanced_boundaries),
 momentum 0.9, wd 5e-4, cosine lr with warm-up, averaging every tick until
@@ -260,7 +260,7 @@ def ours(args) -> None:
                    "batch_per_updater": B, "updaters_per_gpu": U, "workers": ws, "blocks": U,
                    "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
                    "conv_compute": "bf16 autocast (arena, grads, apply, averaging in fp32)",
-                   "l2": "inputs larger than L2 (614 MB dataset gathered per step)",
+                   "l2": "inputs larger than L2 (50,000-image dataset, 307 MB as NHWC bf16, gathered per step)",
                    "sampling": "in-graph device RNG", "host_loop": "native" if tr_native else "python",
                    "momentum": 0.9, "weight_decay": 5e-4,
                    "write_tags": cfg.tracks},

@@ -574,6 +574,11 @@ class ResNetObjective(ArenaObjective):
                 f = torch.randn(self.n_samples, *self.image_shape, generator=g, device=device)
                 if self.pattern_scale:
                     f += self._patterns().to(device)[self._labels.to(device)]
+                if self.shadow_weights and self.channels_last:
+                    # stored as the first conv consumes it: NHWC in the compute
+                    # dtype (the values the per-step cast + layout change would
+                    # produce), so a step gathers 2 B/value and runs no cast
+                    f = f.permute(0, 2, 3, 1).to(self.autocast_dtype).contiguous()
                 self._feat_cache[key] = f
             self._lab_cache[key] = self._labels.to(device)
         return self._feat_cache[key]
@@ -626,9 +631,14 @@ class ResNetObjective(ArenaObjective):
             p.requires_grad_(grad_arena is not None)
         cl = self.channels_last
 
+        image_shape = tuple(self.image_shape)
+
         def forward(xb):
             if shadow is not None:
                 shadow.copy_(arena)                 # fp32 arena -> bf16 weights, one kernel
+            if tuple(xb.shape[1:]) != image_shape:  # NHWC device dataset: a free view
+                xb = xb.permute(0, 3, 1, 2)
+            if shadow is not None:
                 xb = xb.to(shadow_dtype)
             if cl:
                 xb = xb.contiguous(memory_format=torch.channels_last)
