@@ -259,7 +259,7 @@ def ours(args) -> None:
         "config": {"workload": "resnet20_cifar10_lpp_sgd", "model": "resnet20", "global_batch": B * U * ws,
                    "batch_per_updater": B, "updaters_per_gpu": U, "workers": ws, "blocks": U,
                    "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
-                   "conv_compute": "bf16 autocast (arena, grads, apply, averaging in fp32)",
+                   "conv_compute": "bf16 (weights cast once per step from the fp32 replica; arena, grads, apply, averaging in fp32)",
                    "l2": "inputs larger than L2 (50,000-image dataset, 307 MB as NHWC bf16, gathered per step)",
                    "sampling": "in-graph device RNG", "host_loop": "native" if tr_native else "python",
                    "momentum": 0.9, "weight_decay": 5e-4,
