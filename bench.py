@@ -494,7 +494,10 @@ def ours(args) -> None:
     if not args.no_cpu and rank == 0 and ws == 1:
         from oracle.engine_port import run_lpp_cpu
 
-        r = run_lpp_cpu(slots=4 * U, updaters=U, batch_size=B)
+        # bounded sample of the same workload: ~100 minibatches, 10-15 s of
+        # CPU work on the box's host cores (after a short warm-up)
+        run_lpp_cpu(slots=U, updaters=U, batch_size=B)
+        r = run_lpp_cpu(slots=24 * U, updaters=U, batch_size=B)
         line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
                                 "cores": r["cores"], "kind": "port",
                                 "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
