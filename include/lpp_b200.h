@@ -144,7 +144,11 @@ int lpp_snapshot(const float* src, float* out, size_t n, void* stream);
  *   mean_out[e - lo] = mean                    (mean_out may be NULL)
  * Updaters may keep writing the arenas concurrently: their updates are
  * preserved (the correction is added, not stored).  Q <= LPP_MAX_WORKERS.
- * `arenas` is a HOST array of Q device pointers.
+ * `arenas` is a HOST array of Q device pointers.  Mode BULK stages the
+ * round through shared memory with the bulk-copy (TMA) engine: bulk loads
+ * of the Q shard tiles on an mbarrier, the correction written in place,
+ * cp.reduce.async.bulk .add.f32 back into every arena (same values as RED;
+ * the tagged variant serves BULK as RED).
  */
 #define LPP_MAX_WORKERS 8
 int lpp_average_shard(float* const* arenas, int Q, size_t lo, size_t hi,

@@ -922,6 +922,189 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// K4 mode BULK (untagged): the round staged through shared memory by the
+// bulk-copy (TMA) engine.  Per tile one thread issues Q bulk loads (one per
+// arena — peer arenas are read over NVLink by the copy engine, not by LSU
+// loads) completing on an mbarrier; the CTA forms the fixed-order mean and
+// overwrites each staged tile with its correction mean - v_q in place; one
+// thread then hands the Q tiles to cp.reduce.async.bulk .add.f32 (the
+// correction lands as element-wise atomic adds, exactly like K4's red.add).
+// kAvgStages - 1 tiles' loads are in flight while a tile is reduced.
+constexpr int kAvgTileV = 256;   // float4 per arena per tile (4 KB)
+constexpr int kAvgStages = 3;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes,
+                                          uint64_t* bar) {
+  uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          d),
+      "l"(gmem), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+template <int Q>
+__global__ void __launch_bounds__(kThreads)
+    k_average_bulk(ArenaTable t, size_t lo, size_t n, size_t head, size_t nvec,
+                   float* __restrict__ mean_out) {
+  extern __shared__ __align__(128) float4 s_avg[];   // [kAvgStages][Q][kAvgTileV]
+  __shared__ __align__(8) uint64_t bars[kAvgStages];
+  const float fq = (float)Q;
+  const size_t ntiles = (nvec + kAvgTileV - 1) / kAvgTileV;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kAvgStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](size_t tile, int stage) {
+    const size_t base = tile * kAvgTileV;
+    const int cnt = (int)((nvec - base) < (size_t)kAvgTileV ? (nvec - base) : kAvgTileV);
+    mbar_expect_tx(&bars[stage], (uint32_t)(Q * cnt * 16));
+    for (int q = 0; q < Q; ++q)
+      bulk_load(s_avg + ((size_t)stage * Q + q) * kAvgTileV, t.p[q] + lo + head + 4 * base,
+                (uint32_t)(cnt * 16), &bars[stage]);
+  };
+  uint32_t phase[kAvgStages] = {};
+  size_t tile = blockIdx.x;
+  // prologue: the first kAvgStages - 1 tiles' loads in flight
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kAvgStages - 1; ++k) {
+      size_t tk = tile + (size_t)k * gridDim.x;
+      if (tk < ntiles) issue(tk, k);
+    }
+  int stage = 0;
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const size_t ahead = tile + (size_t)(kAvgStages - 1) * gridDim.x;
+    const int astage = (stage + kAvgStages - 1) % kAvgStages;
+    if (threadIdx.x == 0 && ahead < ntiles) {
+      // astage is the stage the previous iteration just handed to the bulk
+      // reductions (the most recent group): they must have read it first
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue(ahead, astage);
+    }
+    mbar_wait(&bars[stage], phase[stage]);
+    phase[stage] ^= 1;
+    const size_t base = tile * kAvgTileV;
+    const int cnt = (int)((nvec - base) < (size_t)kAvgTileV ? (nvec - base) : kAvgTileV);
+    float4* buf = s_avg + (size_t)stage * Q * kAvgTileV;
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      float4 v[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) v[q] = buf[q * kAvgTileV + j];
+      float4 sum = v[0];
+#pragma unroll
+      for (int q = 1; q < Q; ++q) {
+        sum.x = __fadd_rn(sum.x, v[q].x);
+        sum.y = __fadd_rn(sum.y, v[q].y);
+        sum.z = __fadd_rn(sum.z, v[q].z);
+        sum.w = __fadd_rn(sum.w, v[q].w);
+      }
+      float4 mean;
+      mean.x = __fdiv_rn(sum.x, fq);
+      mean.y = __fdiv_rn(sum.y, fq);
+      mean.z = __fdiv_rn(sum.z, fq);
+      mean.w = __fdiv_rn(sum.w, fq);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        float4 c;
+        c.x = __fsub_rn(mean.x, v[q].x);
+        c.y = __fsub_rn(mean.y, v[q].y);
+        c.z = __fsub_rn(mean.z, v[q].z);
+        c.w = __fsub_rn(mean.w, v[q].w);
+        buf[q * kAvgTileV + j] = c;
+      }
+      if (mean_out) reinterpret_cast<float4*>(mean_out + head)[base + j] = mean;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < Q; ++q) {
+        uint32_t saddr = (uint32_t)__cvta_generic_to_shared(buf + q * kAvgTileV);
+        asm volatile(
+            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                t.p[q] + lo + head + 4 * base),
+            "r"(saddr), "r"(cnt * 16)
+            : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    stage = (stage + 1) % kAvgStages;
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // scalar head / tail (first block), as the LSU variant
+  if (blockIdx.x == 0) {
+    size_t tail0 = head + 4 * nvec;
+    size_t nscalar = head + (n - tail0);
+    for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
+      size_t e = k < head ? k : tail0 + (k - head);
+      float vv[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) vv[q] = ld_cg(t.p[q] + lo + e);
+      float sm = vv[0];
+#pragma unroll
+      for (int q = 1; q < Q; ++q) sm = __fadd_rn(sm, vv[q]);
+      float mean = __fdiv_rn(sm, fq);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) red_add_f32(t.p[q] + lo + e, __fsub_rn(mean, vv[q]));
+      if (mean_out) mean_out[e] = mean;
+    }
+  }
+}
+
+template <int Q>
+static void launch_average_bulk_q(cudaStream_t st, const ArenaTable& t, size_t lo, size_t n,
+                                  size_t head, size_t nvec, float* mean_out) {
+  size_t smem = (size_t)kAvgStages * Q * kAvgTileV * sizeof(float4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_average_bulk<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  size_t ntiles = (nvec + kAvgTileV - 1) / kAvgTileV;
+  int per_sm = (int)((200 * 1024) / (smem + 64));
+  if (per_sm < 1) per_sm = 1;
+  size_t cap = (size_t)current_sms() * (size_t)per_sm;
+  unsigned grid = (unsigned)(ntiles < cap ? (ntiles ? ntiles : 1) : cap);
+  k_average_bulk<Q><<<grid, kThreads, smem, st>>>(t, lo, n, head, nvec, mean_out);
+}
+
+static void launch_average_bulk(int Q, cudaStream_t st, const ArenaTable& t, size_t lo, size_t n,
+                                size_t head, size_t nvec, float* mean_out) {
+  switch (Q) {
+    case 1: launch_average_bulk_q<1>(st, t, lo, n, head, nvec, mean_out); break;
+    case 2: launch_average_bulk_q<2>(st, t, lo, n, head, nvec, mean_out); break;
+    case 3: launch_average_bulk_q<3>(st, t, lo, n, head, nvec, mean_out); break;
+    case 4: launch_average_bulk_q<4>(st, t, lo, n, head, nvec, mean_out); break;
+    case 5: launch_average_bulk_q<5>(st, t, lo, n, head, nvec, mean_out); break;
+    case 6: launch_average_bulk_q<6>(st, t, lo, n, head, nvec, mean_out); break;
+    case 7: launch_average_bulk_q<7>(st, t, lo, n, head, nvec, mean_out); break;
+    default: launch_average_bulk_q<8>(st, t, lo, n, head, nvec, mean_out); break;
+  }
+}
+
 template <int MODE, int Q>
 static void launch_average_q(bool tagged, unsigned grid, cudaStream_t st, const ArenaTable& t,
                              size_t lo, size_t n, size_t head, size_t nvec, float* mean_out) {
@@ -950,7 +1133,9 @@ static void launch_average_m(int Q, bool tagged, unsigned grid, cudaStream_t st,
 static void launch_average(int mode, int Q, bool tagged, unsigned grid, cudaStream_t st,
                            const ArenaTable& t, size_t lo, size_t n, size_t head, size_t nvec,
                            float* mean_out) {
-  if (mode == LPP_MODE_PLAIN)
+  if (mode == LPP_MODE_BULK && !tagged)
+    launch_average_bulk(Q, st, t, lo, n, head, nvec, mean_out);
+  else if (mode == LPP_MODE_PLAIN)
     launch_average_m<LPP_MODE_PLAIN>(Q, tagged, grid, st, t, lo, n, head, nvec, mean_out);
   else
     launch_average_m<LPP_MODE_RED>(Q, tagged, grid, st, t, lo, n, head, nvec, mean_out);
@@ -977,8 +1162,8 @@ static int average_impl(float* const* arenas, int32_t* const* tags, const int32_
     return set_err(LPP_E_VALUE, "average_shard: Q=%d outside [1, %d]", Q, LPP_MAX_WORKERS);
   if (hi < lo) return set_err(LPP_E_INDEX, "average_shard: hi < lo");
   if (!arenas) return set_err(LPP_E_VALUE, "average_shard: null arena table");
-  if (mode != LPP_MODE_PLAIN && mode != LPP_MODE_RED)
-    return set_err(LPP_E_VALUE, "average_shard: mode must be PLAIN or RED");
+  if (mode != LPP_MODE_PLAIN && mode != LPP_MODE_RED && mode != LPP_MODE_BULK)
+    return set_err(LPP_E_VALUE, "average_shard: mode must be PLAIN, RED or BULK");
   size_t n = hi - lo;
   if (n == 0) return LPP_OK;
   ArenaTable t;

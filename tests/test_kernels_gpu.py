@@ -143,7 +143,7 @@ def test_snapshot_exact_and_misaligned(N, n):
 
 
 @pytest.mark.parametrize("Q", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("mode", ["plain", "red"])
+@pytest.mark.parametrize("mode", ["plain", "red", "bulk"])
 def test_average_shard_bitexact_vs_oracle(N, orc, Q, mode):
     from paper_2203_06638_b200.arena import Arena
 

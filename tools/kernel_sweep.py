@@ -66,6 +66,9 @@ def main():
             hbm = 2 * 4 * d * Q
             rows.append(dict(kernel=f"average_Q{Q}_local", d=d, us=t * 1e6, gbs=hbm / t / 1e9,
                              frac=hbm / t / 1e9 / peak))
+            tb = timed(lambda: N.average_shard([a.ptr for a in ars], 0, d, None, N.MODE_BULK, st), flush)
+            rows.append(dict(kernel=f"average_Q{Q}_local_bulk", d=d, us=tb * 1e6, gbs=hbm / tb / 1e9,
+                             frac=hbm / tb / 1e9 / peak))
             if Q == 4:
                 # the same round while 3 updater streams keep applying K1
                 # (momentum + wd) into the averaged arena
