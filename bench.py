@@ -286,7 +286,9 @@ def ours(args) -> None:
     # ---------------- end to end (host buffers) ----------------
     if not args.no_e2e:
         hobj = ResNetObjective("resnet20", n_samples=N_SAMPLES if ws == 1 else N_SAMPLES, seed=0, data="host")
-        hcfg = build_cfg(hobj, (K + W) * U, workers=ws, sampling="host")
+        # host-drawn batches (the device sampler's stream), pinned row gather, H2D
+        # every step, loss D2H every step — inside the native updater loop
+        hcfg = build_cfg(hobj, (K + W) * U, workers=ws, sampling="device")
         htr = Trainer(hcfg, group=group, host_batches=True, read_loss=True)
         htr.run(W * U, evaluate=False)
         barrier()
@@ -298,6 +300,7 @@ def ours(args) -> None:
         per_img = 3 * 32 * 32 * 4 + 8
         line["e2e"] = {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": U * B * per_img,
                        "d2h_bytes_per_step": U * 4, "api": "Trainer(cfg, host_batches=True, read_loss=True).run",
+                       "host_loop": "native" if htr.eng.native_loop() else "python",
                        "losses_read": len(hres.losses),
                        "last_loss": hres.losses[-1] if hres.losses else None}
         htr.close()

@@ -297,7 +297,7 @@ typedef struct {
   int64_t warm_start;
   const int64_t* block_lo;        /* [num_blocks + 1] element ranges per block id */
   const int64_t* block_hi;
-  void* const* graph_exec;        /* cudaGraphExec_t per block id */
+  void* const* graph_exec;        /* cudaGraphExec_t [block id][input buffer 0/1] */
   const int64_t* flops_of;        /* per block id */
   /* arenas (bases) */
   float* x;
@@ -323,6 +323,31 @@ typedef struct {
   void* stream;
   void* apply_stream;             /* NULL: apply on `stream`; else a (high-priority) stream
                                      ordered after the step's graph by events */
+  /* end-to-end input: when host_feats != NULL every step draws its batch
+   * indices on the host (the device sampler's stream, lpp_sample_indices_host
+   * keyed by sample_key), gathers the rows from pinned host memory into a
+   * pinned staging slot and copies them on copy_stream into the graph's
+   * input buffer t % 2 (double-buffered: the copy for step t+1 overlaps
+   * step t, ordered by events) */
+  const void* host_feats;         /* pinned [n_rows][row_bytes] */
+  const void* host_labels;        /* pinned [n_rows][label_bytes] */
+  int64_t n_rows;
+  int64_t row_bytes;
+  int64_t label_bytes;
+  int32_t batch;
+  int32_t read_loss;              /* 1: D2H of each step's loss, logged in loss_log */
+  uint64_t sample_key;
+  void* feat_pinned;              /* [in_flight + 2][batch * row_bytes] */
+  void* label_pinned;             /* [in_flight + 2][batch * label_bytes] */
+  void* xbuf[2];                  /* the captured graphs' input buffers */
+  void* ybuf[2];
+  void* copy_stream;
+  const float* loss_dev[2];       /* the graphs' loss scalars (per input buffer) */
+  float* loss_pinned;             /* [in_flight + 2] */
+  float* loss_log;                /* [loss_cap] losses in step order */
+  int64_t loss_cap;
+  int64_t* loss_count;
+  int64_t sample_step0;           /* host draws use steps sample_step0, sample_step0 + 1, ... */
 } lpp_updater_cfg;
 
 typedef struct {

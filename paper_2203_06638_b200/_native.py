@@ -67,6 +67,12 @@ class UpdaterCfg(ctypes.Structure):
         ("tag_idx_pinned", _vp), ("tag_idx_dev", _vp), ("tag_out_dev", _vp),
         ("tag_out_pinned", _vp), ("classified", _vp), ("clean", _vp),
         ("apply_bytes_per_elem", _c.c_double), ("stream", _vp), ("apply_stream", _vp),
+        ("host_feats", _vp), ("host_labels", _vp), ("n_rows", _c.c_int64), ("row_bytes", _c.c_int64),
+        ("label_bytes", _c.c_int64), ("batch", _c.c_int32), ("read_loss", _c.c_int32),
+        ("sample_key", _c.c_uint64), ("feat_pinned", _vp), ("label_pinned", _vp),
+        ("xbuf", _vp * 2), ("ybuf", _vp * 2), ("copy_stream", _vp), ("loss_dev", _vp * 2),
+        ("loss_pinned", _vp), ("loss_log", _vp), ("loss_cap", _c.c_int64), ("loss_count", _vp),
+        ("sample_step0", _c.c_int64),
     ]
 
 

@@ -772,6 +772,10 @@ class _Engine(NativeLoops):
 
     def run_async(self) -> float:
         cfg = self.cfg
+        if self.host_batches and cfg.sampling == "device" and not self.native_loop():
+            raise ValueError("host batches drawn from the device sampler's stream need the native "
+                             "loop (record_mode='off', host_loop != 'python'); the Python loop "
+                             "samples host batches with sampling='host'")
         self.side_apply = self.apply_on_side()
         starts = self._device_span_start()
         threads = []

@@ -154,13 +154,25 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   const int F = c->in_flight < 1 ? 1 : c->in_flight;
   const int depth = F + 2;
   cudaStream_t stream = (cudaStream_t)c->stream;
+  const bool host = c->host_feats != nullptr;
+  if (host && (!c->host_labels || !c->feat_pinned || !c->label_pinned || !c->xbuf[0] ||
+               !c->xbuf[1] || !c->ybuf[0] || !c->ybuf[1] || !c->copy_stream || c->batch <= 0 ||
+               c->n_rows <= 0 || c->row_bytes <= 0 || c->label_bytes <= 0))
+    return set_err(LPP_E_VALUE, "updater_run: host-batch buffers missing");
+  if (c->read_loss && (!c->loss_dev[0] || !c->loss_dev[1] || !c->loss_pinned || !c->loss_log ||
+                       !c->loss_count))
+    return set_err(LPP_E_VALUE, "updater_run: loss read-back buffers missing");
 
   cudaStream_t astream = c->apply_stream ? (cudaStream_t)c->apply_stream : stream;
   const bool side = astream != stream;
-  Events done, t0, t1, order;
+  cudaStream_t cstream = host ? (cudaStream_t)c->copy_stream : stream;
+  Events done, t0, t1, order, copied, buf_free;
   int rc;
   if ((rc = done.make(F, cudaEventDisableTiming)) != LPP_OK) return rc;
   if (side && (rc = order.make(2, cudaEventDisableTiming)) != LPP_OK) return rc;
+  if (host && (rc = copied.make(depth, cudaEventDisableTiming)) != LPP_OK) return rc;
+  if (host && (rc = buf_free.make(2, cudaEventDisableTiming)) != LPP_OK) return rc;
+  std::vector<int64_t> idx(host ? c->batch : 0);
   if (c->time_apply) {
     if ((rc = t0.make(F, cudaEventDefault)) != LPP_OK) return rc;
     if ((rc = t1.make(F, cudaEventDefault)) != LPP_OK) return rc;
@@ -187,6 +199,11 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   };
   // once a step's event completed: classify its tags, collect its apply time
   auto retire = [&](int k) -> int {
+    if (c->read_loss) {
+      int64_t i = *c->loss_count;
+      if (i < c->loss_cap) c->loss_log[i] = c->loss_pinned[slot_of[k]];
+      *c->loss_count = i + 1;
+    }
     if (K > 0) {
       const int32_t* tg = c->tag_out_pinned + (size_t)slot_of[k] * K;
       bool clean = true;
@@ -220,11 +237,37 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     const int64_t u = __atomic_fetch_add(c->update_order, 1, __ATOMIC_ACQ_REL) + 1;
     const int64_t lo = c->block_lo[b], hi = c->block_hi[b], len = hi - lo;
     const float lr32 = (float)lr;
+    const int buf = host ? (int)(t & 1) : 0;
+    if (host) {
+      // end-to-end input: host draw + pinned row gather + H2D on the copy
+      // stream into input buffer `buf` once the step that last read it is done
+      for (int i = 0; i < c->batch; ++i)
+        idx[i] = sample_one(c->sample_key, c->sample_step0 + t, i, (uint64_t)c->n_rows);
+      char* fdst = static_cast<char*>(c->feat_pinned) + (size_t)slot * c->batch * c->row_bytes;
+      char* ldst = static_cast<char*>(c->label_pinned) + (size_t)slot * c->batch * c->label_bytes;
+      if ((rc = lpp_host_gather_rows(fdst, c->host_feats, (size_t)c->n_rows, (size_t)c->row_bytes,
+                                     idx.data(), (size_t)c->batch)) != LPP_OK)
+        return rc;
+      if ((rc = lpp_host_gather_rows(ldst, c->host_labels, (size_t)c->n_rows,
+                                     (size_t)c->label_bytes, idx.data(), (size_t)c->batch)) != LPP_OK)
+        return rc;
+      CUDA_TRY(cudaStreamWaitEvent(cstream, buf_free.ev[buf], 0));
+      CUDA_TRY(cudaMemcpyAsync(c->xbuf[buf], fdst, (size_t)c->batch * c->row_bytes,
+                               cudaMemcpyHostToDevice, cstream));
+      CUDA_TRY(cudaMemcpyAsync(c->ybuf[buf], ldst, (size_t)c->batch * c->label_bytes,
+                               cudaMemcpyHostToDevice, cstream));
+      CUDA_TRY(cudaEventRecord(copied.ev[slot], cstream));
+      CUDA_TRY(cudaStreamWaitEvent(stream, copied.ev[slot], 0));
+    }
     if (!c->fused || t == 0) {
       if (K > 0 && (rc = gather(slot)) != LPP_OK) return rc;
       if ((rc = lpp_snapshot(c->x, c->replica, c->n, stream)) != LPP_OK) return rc;   // K3
     }
-    if ((rc = lpp_graph_launch(c->graph_exec[b], stream)) != LPP_OK) return rc;       // fwd+bwd
+    if ((rc = lpp_graph_launch(c->graph_exec[2 * b + buf], stream)) != LPP_OK) return rc;  // fwd+bwd
+    if (host) CUDA_TRY(cudaEventRecord(buf_free.ev[buf], stream));
+    if (c->read_loss)
+      CUDA_TRY(cudaMemcpyAsync(c->loss_pinned + slot, c->loss_dev[buf], sizeof(float),
+                               cudaMemcpyDeviceToHost, stream));
     if (c->fused && K > 0 && (rc = gather(next_slot)) != LPP_OK) return rc;          // K5 (next)
     if (side) {  // the apply on its own (high-priority) stream, after the graph
       CUDA_TRY(cudaEventRecord(order.ev[0], stream));

@@ -27,30 +27,32 @@ class NativeLoops:
 
     def native_loop(self) -> bool:
         """Whether updaters run the C++ loop (lpp_updater_run): the
-        throughput configuration — async, device sampling, no per-update
-        records, no host batches / loss read-back / quiescent pauses."""
+        throughput configuration — async, device-stream sampling (drawn in
+        the captured graph, or on the host for end-to-end host batches), no
+        per-update records, no quiescent pauses."""
         cfg = self.cfg
         ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
-              and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs
-              and not self.host_batches and not self.read_loss)
+              and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs)
         if cfg.host_loop == "native" and not ok:
             raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
-                             "sampling='device', CUDA graphs, no host batches / loss read-back / "
-                             "quiescent")
+                             "sampling='device', CUDA graphs, no quiescent pauses")
         return ok and cfg.host_loop != "python"
 
     def apply_on_side(self) -> bool:
         """Whether applies run on the per-updater high-priority stream.
 
-        Auto (``apply_priority=None``): native loop and U <= 4.  The side
-        stream doubles a worker's streams; past the device's 8 hardware work
-        queues (CUDA_DEVICE_MAX_CONNECTIONS) streams share queues and
-        serialise — measured -12 % images/s at U = 6 (neutral at U = 4, and
-        raising the queue count to 32 costs 2-3 % everywhere;
-        tools/ab_priority_streams.py)."""
+        Auto (``apply_priority=None``): native loop and at most ~8 streams
+        per worker.  The side stream doubles a worker's streams; past the
+        device's 8 hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS) streams
+        share queues and serialise — measured -12 % images/s at U = 6 and
+        -13 % end to end at U = 4 (3 streams per updater with the copy
+        stream), neutral at U = 4 device-resident; raising the queue count
+        to 32 costs 2-3 % everywhere (tools/ab_priority_streams.py)."""
         p = self.cfg.apply_priority
         if p is None:
-            return self.native_loop() and self.cfg.updaters <= 4
+            # updater + apply (+ copy, end to end) streams per updater, + the averager's
+            streams = self.cfg.updaters * (3 if self.host_batches else 2) + 1
+            return self.native_loop() and streams <= 9
         return bool(p)
 
     def updater_cfg(self, w: _Worker, r: int) -> tuple:
@@ -62,14 +64,16 @@ class NativeLoops:
         prog = w.programs[r]
         lo = np.zeros(nb + 1, dtype=np.int64)
         hi = np.zeros(nb + 1, dtype=np.int64)
-        execs = (ctypes.c_void_p * (nb + 1))()
+        execs = (ctypes.c_void_p * (2 * (nb + 1)))()       # [block][input buffer]
         flops = np.zeros(nb + 1, dtype=np.int64)
         for b in range(nb + 1):
             blk = cfg.partition.block(b)
             lo[b], hi[b] = blk.start, blk.stop
             flops[b] = self._flops_of[b]
-            if (b, 0) in prog.execs:
-                execs[b] = prog.execs[(b, 0)]
+            for buf in (0, 1):
+                key = (b, buf % prog.nbuf)
+                if key in prog.execs:
+                    execs[2 * b + buf] = prog.execs[key]
         ms = np.ascontiguousarray(sched.milestones, dtype=np.int64)
         tracks = w.tags is not None
         k = w.tag_pick if tracks else 0
@@ -112,7 +116,33 @@ class NativeLoops:
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
         c.stream = w.streams[r].cuda_stream
         c.apply_stream = w.apply_streams[r].cuda_stream if self.side_apply else None
-        return c, (lo, hi, execs, flops, ms)
+        keep = [lo, hi, execs, flops, ms]
+        if self.host_batches:
+            obj = cfg.objective
+            feats, labs = obj.features, obj.labels
+            c.host_feats, c.host_labels = feats.data_ptr(), labs.data_ptr()
+            c.n_rows = feats.shape[0]
+            c.row_bytes = feats[0].numel() * feats.element_size()
+            c.label_bytes = labs.element_size()
+            c.batch = cfg.batch_size
+            c.sample_key = prog.sample_key & (2**64 - 1)
+            c.sample_step0 = prog.host_step
+            c.feat_pinned = w.batch_pinned[r].data_ptr()
+            c.label_pinned = w.label_pinned[r].data_ptr()
+            c.xbuf[0], c.xbuf[1] = prog.xbs[0].data_ptr(), prog.xbs[1 % prog.nbuf].data_ptr()
+            c.ybuf[0], c.ybuf[1] = prog.ybs[0].data_ptr(), prog.ybs[1 % prog.nbuf].data_ptr()
+            c.copy_stream = w.copy_streams[r].cuda_stream
+        if self.read_loss:
+            cap = self.budget + cfg.updaters + 8
+            log = np.zeros(cap, dtype=np.float32)
+            count = np.zeros(1, dtype=np.int64)
+            c.read_loss = 1
+            c.loss_dev[0] = prog.loss_of(0).data_ptr()
+            c.loss_dev[1] = prog.loss_of(1).data_ptr()
+            c.loss_pinned = w.loss_pinned[r].data_ptr()
+            c.loss_log, c.loss_cap, c.loss_count = log.ctypes.data, cap, count.ctypes.data
+            keep += [log, count]
+        return c, keep
 
     def updater_native(self, q: int, r: int) -> None:
         """a10 in native code: the whole loop is one GIL-free C call."""
@@ -123,6 +153,11 @@ class NativeLoops:
         try:
             c, keep = self.updater_cfg(w, r)
             st = N.updater_run(c)
+            w.programs[r].host_step += int(st.steps)
+            if self.read_loss:
+                log, count = keep[-2], int(keep[-1][0])
+                with self.native_lock:
+                    self.loss_log.extend(float(v) for v in log[:min(count, len(log))])
             del keep
             self.flops.add(int(st.flops))
             if self.time_apply:

@@ -94,6 +94,11 @@ class StepProgram:
                         pool = g.pool()
                         self.graphs[(bid, buf)] = g
                 stream.synchronize()
+        # the batch stream starts at step 0 on the first replay (warm-up
+        # draws do not count), and the native loop's host-drawn batches
+        # (end-to-end input) continue the same stream from host_step
+        self.sample_step.zero_()
+        self.host_step = 0
         # raw cudaGraphExec_t handles, launched straight through the C ABI
         # (no framework generator state to advance: sampling is our kernel)
         self.execs = {}

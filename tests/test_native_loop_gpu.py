@@ -232,3 +232,53 @@ def test_native_loop_is_bitwise_the_python_loop_without_concurrency(fuse):
     assert nat.flops == py.flops
     assert np.array_equal(nat.final_values, py.final_values)
     assert not np.array_equal(nat.final_values, nat.x0.astype(np.float32))
+
+
+def test_native_loop_end_to_end_host_batches_and_loss_readback():
+    """The end-to-end input path inside the native loop: host-drawn indices
+    (the device sampler's stream), pinned row gather, H2D into the graphs'
+    double-buffered inputs, one loss D2H per step — with the same batches
+    the in-graph sampler draws, so at Q = U = 1 it trains bit for bit like
+    the device-data run."""
+    from paper_2203_06638_b200.engine import RunConfig, Trainer, run_experiment
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    def cfg_for(obj, **kw):
+        d = dict(algo="lpp_sgd", objective=obj,
+                 partition=make_partition(obj.dim, (0, obj.edges[2], obj.dim)),
+                 lr=LrSchedule(kind="cosine", alpha0=0.05, total=60, warmup=6),
+                 sync=SyncScheme(total=60, period=4), budget=60, warm_start_budget=6, workers=1,
+                 updaters=1, batch_size=32, seed=3, momentum=0.9, sampling="device",
+                 record_mode="off", evaluate=False, host_loop="native")
+        d.update(kw)
+        return RunConfig(**d)
+
+    host = ResNetObjective("smallcnn", n_samples=512, seed=0, data="host", channels_last=False,
+                           autocast=None)
+    # deterministic cuDNN algorithms so both runs do the same arithmetic
+    det, bench_ = torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
+    tr = Trainer(cfg_for(host), host_batches=True, read_loss=True)
+    try:
+        assert tr.eng.native_loop()
+        res = tr.run()
+        assert res.counter_finals == [61]
+        assert len(res.losses) == 61 and np.all(np.isfinite(res.losses))
+    finally:
+        tr.close()
+    # the same data resident on the device, batches drawn inside the graph
+    try:
+        ref = run_experiment(cfg_for(host))
+    finally:
+        torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = det, bench_
+    np.testing.assert_array_equal(res.final_values, ref.final_values)
+    # and the multi-updater e2e run keeps the counter contract
+    tr = Trainer(cfg_for(host, updaters=2, partition=make_partition(host.dim, (0, host.edges[2], host.edges[4], host.dim)),
+                         workers=2), host_batches=True, read_loss=True)
+    try:
+        res = tr.run()
+        assert res.counter_finals == [62, 62] and len(res.losses) == 124
+    finally:
+        tr.close()
