@@ -12,12 +12,15 @@ every updater stream (U x B images per GPU); K steps are timed with CUDA
 events (max over ranks), after W untimed warm-up steps.
 
 Extra keys beyond the base contract:
-  roofline      the apply kernel (K1/K2), timed live with CUDA events around
-                every launch in the timed region, algorithmic bytes
-                (12 B/elem + 8 with momentum) vs MEASURED_PEAKS.json hbm_gbs
-  e2e           the same metric through Trainer(..., host_batches=True): each
-                step's batch gathered from pinned host memory and copied H2D
-                inside the step, each step's loss copied D2H
+  roofline      the fused apply kernel (K1+K3), timed live with CUDA events
+                around every launch in the timed region, algorithmic bytes
+                (block 12 B/elem + 8 momentum + 4 tag, replica refresh 4-8)
+                vs MEASURED_PEAKS.json hbm_gbs; + the ncu standalone time and
+                DRAM traffic of the same kernel (profiles/)
+  e2e           the same metric through Trainer(..., host_batches=True,
+                read_loss=True): each step's batch gathered from pinned host
+                memory and copied H2D inside the step (native updater loop,
+                copy stream), each step's loss copied D2H
   cpu_baseline  oracle/engine_port.py (threaded CPU LPP-SGD, the reference's
                 compiled _atomics) on this host, bounded sample, rank 0, N=1
   baselines     the box's own synchronous MB-SGD (same per-GPU B, 1 stream)
