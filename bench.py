@@ -324,28 +324,32 @@ def ours(args) -> None:
             ptrs = group.attach_arenas(ar)
             lo, hi = shard_bounds(d, ws)[rank]
             st = torch.cuda.current_stream().cuda_stream
-            for _ in range(3):
-                N.average_shard(ptrs, lo, hi, None, N.MODE_RED, st)
-            ts = []
-            for _ in range(10):
-                barrier()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                N.average_shard(ptrs, lo, hi, None, N.MODE_RED, st)
-                b.record()
-                b.synchronize()
-                ts.append(max_over_ranks(a.elapsed_time(b)))
-            t = sorted(ts)[len(ts) // 2] / 1e3
-            busbw = 2 * (ws - 1) / ws * 4 * d / t / 1e9
-            avg[str(d)] = {"us": t * 1e6, "busbw_gbs": busbw, "frac_of_770": busbw / 770.0,
-                           "frac_of_900": busbw / 900.0}
+            for mode_name, mode in (("red", N.MODE_RED), ("bulk", N.MODE_BULK)):
+                for _ in range(3):
+                    N.average_shard(ptrs, lo, hi, None, mode, st)
+                ts = []
+                for _ in range(10):
+                    barrier()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    N.average_shard(ptrs, lo, hi, None, mode, st)
+                    b.record()
+                    b.synchronize()
+                    ts.append(max_over_ranks(a.elapsed_time(b)))
+                t = sorted(ts)[len(ts) // 2] / 1e3
+                busbw = 2 * (ws - 1) / ws * 4 * d / t / 1e9
+                avg.setdefault(str(d), {})[mode_name] = {
+                    "us": t * 1e6, "busbw_gbs": busbw, "frac_of_770": busbw / 770.0,
+                    "frac_of_900": busbw / 900.0}
             barrier()
             for pm in group.peers[-(ws - 1):]:
                 pm.close()
             del group.peers[-(ws - 1):]
             ar.close()
-        line["averaging"] = {"kernel": "lpp_average_shard (K4, owner-computes over peer arenas)",
+        line["averaging"] = {"kernel": "lpp_average_shard (K4, owner-computes over peer arenas; "
+                                       "red = LSU loads + red.add, bulk = TMA-staged)",
                              "unit": "GB/s", "sizes": avg,
+                             "ranks_share_device": torch.cuda.device_count() < ws,
                              "note": "busbw = 2(Q-1)/Q x 4d per GPU per direction (nccl-tests convention); "
                                      "770 GB/s = measured peer copy, 900 = NVLink 5 nominal"}
 
