@@ -1077,11 +1077,16 @@ template <int Q>
 static void launch_average_bulk_q(cudaStream_t st, const ArenaTable& t, size_t lo, size_t n,
                                   size_t head, size_t nvec, float* mean_out) {
   size_t smem = (size_t)kAvgStages * Q * kAvgTileV * sizeof(float4);
-  static bool attr = false;
-  if (!attr) {
+  // the dynamic shared-memory opt-in is per device (workers of one process
+  // may sit on several GPUs)
+  static std::atomic<unsigned long long> done_mask{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  unsigned long long bit = 1ull << (dev & 63);
+  if (!(done_mask.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(k_average_bulk<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attr = true;
+    done_mask.fetch_or(bit, std::memory_order_acq_rel);
   }
   size_t ntiles = (nvec + kAvgTileV - 1) / kAvgTileV;
   int per_sm = (int)((200 * 1024) / (smem + 64));
