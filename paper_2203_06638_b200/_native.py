@@ -197,7 +197,9 @@ def last_error() -> str:
 def check(status: int, what: str) -> None:
     if status == 0:
         return
-    msg = f"{what}: {last_error()}"
+    err = last_error()
+    # the C side names the entry point already; do not repeat it
+    msg = err if err.startswith(what.split("(")[0] + ":") else f"{what}: {err}"
     if status == E_VALUE:
         raise ValueError(msg)
     if status == E_INDEX:
