@@ -264,6 +264,18 @@ int lpp_sample_indices(int64_t* idx, int64_t* step, int32_t batch, int64_t n, ui
                        void* stream);
 int lpp_sample_indices_host(int64_t* out, int32_t batch, int64_t n, uint64_t key, int64_t step);
 
+/* Device-side epoch-partition sampling (f4; EpochSampler, objectives.py:
+ * 77-104): position step * batch + i of the stream is element
+ * perm_e(pos mod shard_len) of the shard {shard_base + p * shard_stride},
+ * epoch e = pos / shard_len, perm_e a keyed Feistel bijection — each
+ * epoch visits every shard element exactly once in a fresh order.  Same
+ * device step counter protocol as lpp_sample_indices; host twin for tests
+ * and for the native loop's end-to-end input. */
+int lpp_sample_epoch(int64_t* idx, int64_t* step, int32_t batch, int64_t shard_base,
+                     int64_t shard_stride, int64_t shard_len, uint64_t key, void* stream);
+int lpp_sample_epoch_host(int64_t* out, int32_t batch, int64_t shard_base, int64_t shard_stride,
+                          int64_t shard_len, uint64_t key, int64_t step);
+
 /* One updater's whole asynchronous loop in native code (GIL-free): claim
  * s = C^q++ (host cell), lr = lr_at(s), b = select_block(s, ...), u = the
  * write stamp, then on the updater's stream
@@ -348,6 +360,9 @@ typedef struct {
   int64_t loss_cap;
   int64_t* loss_count;
   int64_t sample_step0;           /* host draws use steps sample_step0, sample_step0 + 1, ... */
+  int64_t epoch_base;             /* epoch_len > 0: host draws follow lpp_sample_epoch_host */
+  int64_t epoch_stride;
+  int64_t epoch_len;
 } lpp_updater_cfg;
 
 typedef struct {

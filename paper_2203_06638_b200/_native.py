@@ -72,7 +72,8 @@ class UpdaterCfg(ctypes.Structure):
         ("sample_key", _c.c_uint64), ("feat_pinned", _vp), ("label_pinned", _vp),
         ("xbuf", _vp * 2), ("ybuf", _vp * 2), ("copy_stream", _vp), ("loss_dev", _vp * 2),
         ("loss_pinned", _vp), ("loss_log", _vp), ("loss_cap", _c.c_int64), ("loss_count", _vp),
-        ("sample_step0", _c.c_int64),
+        ("sample_step0", _c.c_int64), ("epoch_base", _c.c_int64), ("epoch_stride", _c.c_int64),
+        ("epoch_len", _c.c_int64),
     ]
 
 
@@ -170,6 +171,10 @@ _SIGS = {
     "lpp_select_block": (_c.c_int, [_c.c_int64, _c.c_int64, _c.c_int, _c.c_int]),
     "lpp_sample_indices": (_c.c_int, [_vp, _vp, _c.c_int32, _c.c_int64, _c.c_uint64, _vp]),
     "lpp_sample_indices_host": (_c.c_int, [_vp, _c.c_int32, _c.c_int64, _c.c_uint64, _c.c_int64]),
+    "lpp_sample_epoch": (_c.c_int, [_vp, _vp, _c.c_int32, _c.c_int64, _c.c_int64, _c.c_int64,
+                                    _c.c_uint64, _vp]),
+    "lpp_sample_epoch_host": (_c.c_int, [_vp, _c.c_int32, _c.c_int64, _c.c_int64, _c.c_int64,
+                                         _c.c_uint64, _c.c_int64]),
     "lpp_updater_run": (_c.c_int, [_c.POINTER(UpdaterCfg), _c.POINTER(UpdaterStats)]),
     "lpp_averager_run": (_c.c_int, [_c.POINTER(AveragerCfg), _c.POINTER(_c.c_int64)]),
     "lpp_fill_i32": (_c.c_int, [_vp, _size, _c.c_int32, _vp]),
@@ -390,3 +395,16 @@ def averager_run(cfg: AveragerCfg) -> int:
 
 def fill_i32(ptr: int, n: int, value: int, stream: int) -> None:
     check(lib.lpp_fill_i32(ptr, n, int(value), stream), "fill_i32")
+
+
+def sample_epoch(idx_ptr: int, step_ptr: int, batch: int, base: int, stride: int, length: int,
+                 key: int, stream: int) -> None:
+    check(lib.lpp_sample_epoch(idx_ptr, step_ptr, batch, base, stride, length, key & (2**64 - 1),
+                               stream), "sample_epoch")
+
+
+def sample_epoch_host(batch: int, base: int, stride: int, length: int, key: int, step: int) -> np.ndarray:
+    out = np.zeros(batch, dtype=np.int64)
+    check(lib.lpp_sample_epoch_host(out.ctypes.data, batch, base, stride, length, key & (2**64 - 1),
+                                    step), "sample_epoch_host")
+    return out

@@ -161,6 +161,7 @@ class _Worker:
                     obj, self.dev, self.replicas[r].tensor, self.grads[r].tensor, blocks,
                     cfg.batch_size, self.streams[r], input_mode=input_mode,
                     use_graphs=cfg.use_graphs, seed=cfg.seed * 7919 + self.q * 101 + r + 1,
+                    epoch=self.epoch_shard(engine) if cfg.epoch_partition else None,
                     nbuf=2))
             depth = cfg.in_flight + 2
             self.loss_pinned = torch.zeros((cfg.updaters, depth), dtype=torch.float32, pin_memory=True)
@@ -192,6 +193,12 @@ class _Worker:
                 N.snapshot(self.store.arena.ptr, self.replicas[r].ptr, engine.dim,
                            self.streams[r].cuda_stream)
             torch.cuda.synchronize(self.device)
+
+    def epoch_shard(self, engine: "_Engine") -> tuple[int, int, int]:
+        """This worker's index shard arange(n)[q::Q] as (base, stride, length)
+        (engine.py:294-296)."""
+        n, Q = engine.cfg.objective.n_samples, engine.cfg.workers
+        return self.q, Q, (n - self.q + Q - 1) // Q
 
     def close(self):
         extra = [self.tag_arena] if self.tag_arena is not None else []
@@ -580,7 +587,8 @@ class _Engine(NativeLoops):
         rank = r + 1
         gen = np.random.default_rng(np.random.SeedSequence([cfg.seed, q, rank]))
         n = cfg.objective.n_samples
-        sampler = worker_sampler(n, cfg.workers, q, rank, cfg.seed) if cfg.epoch_partition else None
+        sampler = (worker_sampler(n, cfg.workers, q, rank, cfg.seed)
+                   if cfg.epoch_partition and cfg.sampling == "host" else None)
         depth = cfg.in_flight + 2
         events = [torch.cuda.Event() for _ in range(cfg.in_flight)]
         used = [False] * cfg.in_flight

@@ -46,6 +46,50 @@ __host__ __device__ __forceinline__ int64_t sample_one(uint64_t key, int64_t ste
 #endif
 }
 
+// epoch-partition sampling (f4: EpochSampler, objectives.py:77-104, on the
+// device): position pos = step * B + i of an updater's stream is element
+// perm_e(pos mod m) of its worker's shard (base + p * stride, the
+// reference's arange(n)[q::Q]), epoch e = pos / m, perm_e a keyed bijection
+// of [0, m): a 4-round balanced Feistel network on the next even power of two,
+// cycle-walked back into [0, m).  Every epoch visits each shard element
+// exactly once, in a fresh order, with no stored permutation.
+__host__ __device__ __forceinline__ uint64_t feistel_perm(uint64_t j, uint64_t m, uint64_t key) {
+  int bits = 2;
+  while ((1ull << bits) < m) ++bits;
+  if (bits & 1) ++bits;
+  const int half = bits / 2;
+  const uint64_t mask = (1ull << half) - 1;
+  uint64_t x = j;
+  do {
+    uint64_t l = x >> half, r = x & mask;
+#pragma unroll
+    for (int round = 0; round < 4; ++round) {
+      uint64_t f = mix64(key ^ (0x9E3779B97F4A7C15ull * (uint64_t)(round + 1)) ^ r) & mask;
+      uint64_t nl = r;
+      r = l ^ f;
+      l = nl;
+    }
+    x = (l << half) | r;
+  } while (x >= m);
+  return x;
+}
+
+__host__ __device__ __forceinline__ int64_t epoch_one(uint64_t key, int64_t step, int i, int batch,
+                                                      int64_t base, int64_t stride, uint64_t m) {
+  uint64_t pos = (uint64_t)step * (uint64_t)batch + (uint64_t)i;
+  uint64_t e = pos / m, j = pos % m;
+  uint64_t p = feistel_perm(j, m, mix64(key ^ mix64(e + 0x632BE59BD9B4E019ull)));
+  return base + (int64_t)p * stride;
+}
+
+__global__ void k_sample_epoch(int64_t* idx, int64_t* step, int b, int64_t base, int64_t stride,
+                               uint64_t m, uint64_t key) {
+  const int64_t t = *step;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) idx[i] = epoch_one(key, t, i, b, base, stride, m);
+  __syncthreads();
+  if (threadIdx.x == 0) *step = t + 1;
+}
+
 __global__ void k_sample_indices(int64_t* idx, int64_t* step, int b, uint64_t n, uint64_t key) {
   const int64_t t = *step;
   for (int i = threadIdx.x; i < b; i += blockDim.x) idx[i] = sample_one(key, t, i, n);
@@ -72,6 +116,32 @@ extern "C" int lpp_sample_indices_host(int64_t* out, int32_t batch, int64_t n, u
   if (!out) return set_err(LPP_E_VALUE, "sample_indices_host: null buffer");
   if (n <= 0) return set_err(LPP_E_VALUE, "sample_indices_host: empty population");
   for (int i = 0; i < batch; ++i) out[i] = sample_one(key, step, i, (uint64_t)n);
+  return LPP_OK;
+}
+
+extern "C" int lpp_sample_epoch(int64_t* idx, int64_t* step, int32_t batch, int64_t shard_base,
+                                int64_t shard_stride, int64_t shard_len, uint64_t key,
+                                void* stream) {
+  if (batch <= 0) return LPP_OK;
+  if (!idx || !step) return set_err(LPP_E_VALUE, "sample_epoch: null buffer");
+  if (shard_len <= 0 || shard_stride <= 0 || shard_base < 0)
+    return set_err(LPP_E_VALUE, "sample_epoch: empty or invalid shard");
+  int threads = std::min(1024, ((batch + 31) / 32) * 32);
+  k_sample_epoch<<<1, threads, 0, (cudaStream_t)stream>>>(idx, step, batch, shard_base, shard_stride,
+                                                          (uint64_t)shard_len, key);
+  LAUNCH_CHECK("sample_epoch");
+  return LPP_OK;
+}
+
+extern "C" int lpp_sample_epoch_host(int64_t* out, int32_t batch, int64_t shard_base,
+                                     int64_t shard_stride, int64_t shard_len, uint64_t key,
+                                     int64_t step) {
+  if (batch <= 0) return LPP_OK;
+  if (!out) return set_err(LPP_E_VALUE, "sample_epoch_host: null buffer");
+  if (shard_len <= 0 || shard_stride <= 0 || shard_base < 0)
+    return set_err(LPP_E_VALUE, "sample_epoch_host: empty or invalid shard");
+  for (int i = 0; i < batch; ++i)
+    out[i] = epoch_one(key, step, i, batch, shard_base, shard_stride, (uint64_t)shard_len);
   return LPP_OK;
 }
 
@@ -242,7 +312,10 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       // end-to-end input: host draw + pinned row gather + H2D on the copy
       // stream into input buffer `buf` once the step that last read it is done
       for (int i = 0; i < c->batch; ++i)
-        idx[i] = sample_one(c->sample_key, c->sample_step0 + t, i, (uint64_t)c->n_rows);
+        idx[i] = c->epoch_len > 0
+                     ? epoch_one(c->sample_key, c->sample_step0 + t, i, c->batch, c->epoch_base,
+                                 c->epoch_stride, (uint64_t)c->epoch_len)
+                     : sample_one(c->sample_key, c->sample_step0 + t, i, (uint64_t)c->n_rows);
       char* fdst = static_cast<char*>(c->feat_pinned) + (size_t)slot * c->batch * c->row_bytes;
       char* ldst = static_cast<char*>(c->label_pinned) + (size_t)slot * c->batch * c->label_bytes;
       if ((rc = lpp_host_gather_rows(fdst, c->host_feats, (size_t)c->n_rows, (size_t)c->row_bytes,

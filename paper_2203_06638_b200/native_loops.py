@@ -32,7 +32,7 @@ class NativeLoops:
         per-update records, no quiescent pauses."""
         cfg = self.cfg
         ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
-              and cfg.sampling == "device" and not cfg.epoch_partition and cfg.use_graphs)
+              and cfg.sampling == "device" and cfg.use_graphs)
         if cfg.host_loop == "native" and not ok:
             raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
                              "sampling='device', CUDA graphs, no quiescent pauses")
@@ -127,6 +127,8 @@ class NativeLoops:
             c.batch = cfg.batch_size
             c.sample_key = prog.sample_key & (2**64 - 1)
             c.sample_step0 = prog.host_step
+            if prog.epoch is not None:
+                c.epoch_base, c.epoch_stride, c.epoch_len = prog.epoch
             c.feat_pinned = w.batch_pinned[r].data_ptr()
             c.label_pinned = w.label_pinned[r].data_ptr()
             c.xbuf[0], c.xbuf[1] = prog.xbs[0].data_ptr(), prog.xbs[1 % prog.nbuf].data_ptr()

@@ -92,8 +92,6 @@ class RunConfig:
             raise ValueError(f"unknown apply mode {self.apply_mode!r}")
         if self.sampling not in ("host", "device"):
             raise ValueError(f"unknown sampling {self.sampling!r}")
-        if self.epoch_partition and self.sampling != "host":
-            raise ValueError("epoch_partition draws indices on the host: use sampling='host'")
         if self.averaging not in ("p2p", "nvls"):
             raise ValueError(f"unknown averaging {self.averaging!r}")
         if self.host_loop not in ("auto", "native", "python"):

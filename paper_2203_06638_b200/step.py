@@ -27,7 +27,8 @@ class StepProgram:
     def __init__(self, obj, device: torch.device, replica: torch.Tensor, grads: torch.Tensor,
                  blocks: dict[int, Block], batch_size: int, stream: torch.cuda.Stream,
                  input_mode: str = "index", use_graphs: bool = True, warmup: int = 2,
-                 seed: int = 0, nbuf: int = 1, grad_mode: str = "copy"):
+                 seed: int = 0, nbuf: int = 1, grad_mode: str = "copy",
+                 epoch: tuple[int, int, int] | None = None):
         if input_mode not in ("index", "batch", "random"):
             raise ValueError(f"unknown input mode {input_mode!r}")
         self.obj = obj
@@ -59,9 +60,12 @@ class StepProgram:
         # seed, advanced by a device-side step counter on every replay)
         self.sample_key = int(seed)
         self.sample_step = torch.zeros(1, dtype=torch.long, device=device)
+        # epoch = (shard base, stride, length): the epoch-partition walk over
+        # the worker's shard (lpp_sample_epoch) instead of i.i.d. draws
+        self.epoch = epoch
         if input_mode == "random":
             from . import _native
-            self._sampler = _native.sample_indices
+            self._native_mod = _native
         self.blocks = dict(blocks)
         self.leaves = {}
         self.grad_views = {}
@@ -112,8 +116,14 @@ class StepProgram:
     def _body(self, bid: int, buf: int = 0) -> None:
         blk = self.blocks[bid]
         if self.input_mode == "random":
-            self._sampler(self.idx.data_ptr(), self.sample_step.data_ptr(), self.batch_size,
-                          self.feats.shape[0], self.sample_key, torch.cuda.current_stream().cuda_stream)
+            sp = torch.cuda.current_stream().cuda_stream
+            if self.epoch is not None:
+                self._native_mod.sample_epoch(self.idx.data_ptr(), self.sample_step.data_ptr(),
+                                              self.batch_size, *self.epoch, self.sample_key, sp)
+            else:
+                self._native_mod.sample_indices(self.idx.data_ptr(), self.sample_step.data_ptr(),
+                                                self.batch_size, self.feats.shape[0],
+                                                self.sample_key, sp)
         if self.input_mode == "batch":
             xb, yb = self.xbs[buf], self.ybs[buf]
         else:

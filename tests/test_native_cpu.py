@@ -211,3 +211,23 @@ def test_host_gather_rows_and_range_check():
         N.host_gather_rows(dst.ctypes.data, src.ctypes.data, 10, 16, np.array([1, 10, 2]))
     with pytest.raises(IndexError):
         N.host_gather_rows(dst.ctypes.data, src.ctypes.data, 10, 16, np.array([-1]))
+
+
+def test_device_epoch_sampler_host_twin_covers_each_epoch():
+    """f4 on the device: every epoch of an updater's stream visits each
+    element of its worker's shard arange(n)[q::Q] exactly once, epochs are
+    reshuffled, batch boundaries may cut an epoch anywhere, and the stream
+    is a function of (key, step) only."""
+    for m, B, base, stride in ((1000, 64, 3, 8), (37, 5, 0, 1), (2, 3, 1, 2), (50_000, 128, 0, 1)):
+        steps = (3 * m + B - 1) // B + 1
+        a = np.concatenate([N.sample_epoch_host(B, base, stride, m, 77, t) for t in range(steps)])
+        shard = list(range(base, base + stride * m, stride))
+        orders = []
+        for e in range(3):
+            ep = a[e * m:(e + 1) * m]
+            assert sorted(ep.tolist()) == shard, (m, e)
+            orders.append(ep.tolist())
+        if m > 2:
+            assert orders[0] != orders[1] != orders[2]
+    assert np.array_equal(N.sample_epoch_host(16, 0, 1, 100, 5, 9), N.sample_epoch_host(16, 0, 1, 100, 5, 9))
+    assert not np.array_equal(N.sample_epoch_host(16, 0, 1, 100, 5, 9), N.sample_epoch_host(16, 0, 1, 100, 6, 9))

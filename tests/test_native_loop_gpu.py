@@ -282,3 +282,31 @@ def test_native_loop_end_to_end_host_batches_and_loss_readback():
         assert res.counter_finals == [62, 62] and len(res.losses) == 124
     finally:
         tr.close()
+
+
+def test_device_epoch_sampler_and_engine_run():
+    """The epoch-partition walk on the device equals its host twin (and
+    advances per replay); an async run with epoch_partition on device
+    sampling keeps the counter contract through the native loop, device-
+    resident and end to end."""
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    idx = torch.zeros(128, dtype=torch.long, device="cuda")
+    step = torch.zeros(1, dtype=torch.long, device="cuda")
+    for t in range(5):
+        N.sample_epoch(idx.data_ptr(), step.data_ptr(), 128, 1, 2, 25_000, 11, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(idx.cpu().numpy(), N.sample_epoch_host(128, 1, 2, 25_000, 11, t))
+    for data, hb in (("device", False), ("host", True)):
+        obj = ResNetObjective("resnet20", n_samples=1000, seed=0, data=data)
+        tr = Trainer(_resnet_cfg(obj, budget=40, workers=2, updaters=2, epoch_partition=True),
+                     host_batches=hb, read_loss=hb)
+        try:
+            assert tr.eng.native_loop()
+            assert tr.eng.workers[1].programs[0].epoch == (1, 2, 500)
+            res = tr.run()
+            assert res.counter_finals == [42, 42] and np.all(np.isfinite(res.final_values))
+        finally:
+            tr.close()
