@@ -11,7 +11,8 @@ from paper_2203_06638_b200.engine import Trainer
 from paper_2203_06638_b200.objectives import ResNetObjective
 
 torch.backends.cudnn.benchmark = True
-obj = ResNetObjective("resnet20", n_samples=50_000, seed=0)
+# fp32 parameters under autocast (the accumulate mode needs arena .grad views)
+obj = ResNetObjective("resnet20", n_samples=50_000, seed=0, shadow_weights=False)
 orig = step_mod.StepProgram.__init__
 res = {"copy": [], "accumulate": []}
 for rep in range(3):
