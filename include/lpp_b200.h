@@ -363,6 +363,16 @@ typedef struct {
   int64_t epoch_base;             /* epoch_len > 0: host draws follow lpp_sample_epoch_host */
   int64_t epoch_stride;
   int64_t epoch_len;
+  /* per-update records (record_mode "light", UpdateRecord, engine.py:74-92):
+   * row t = (s, u, k_claim, block_id, reason 0 warm_start / 1 alternate_full
+   * / 2 alternate_partial, clean -1 unknown / 0 / 1), its lr, and its
+   * sampled tag indices and tag values; NULL rec_i64 = no records */
+  int64_t* rec_i64;               /* [rec_cap][6] */
+  double* rec_lr;                 /* [rec_cap] */
+  int64_t* rec_tag_idx;           /* [rec_cap][tag_pick] or NULL */
+  int32_t* rec_tags;              /* [rec_cap][tag_pick] or NULL */
+  int64_t rec_cap;
+  int64_t* rec_count;
 } lpp_updater_cfg;
 
 typedef struct {

@@ -73,7 +73,8 @@ class UpdaterCfg(ctypes.Structure):
         ("xbuf", _vp * 2), ("ybuf", _vp * 2), ("copy_stream", _vp), ("loss_dev", _vp * 2),
         ("loss_pinned", _vp), ("loss_log", _vp), ("loss_cap", _c.c_int64), ("loss_count", _vp),
         ("sample_step0", _c.c_int64), ("epoch_base", _c.c_int64), ("epoch_stride", _c.c_int64),
-        ("epoch_len", _c.c_int64),
+        ("epoch_len", _c.c_int64), ("rec_i64", _vp), ("rec_lr", _vp), ("rec_tag_idx", _vp),
+        ("rec_tags", _vp), ("rec_cap", _c.c_int64), ("rec_count", _vp),
     ]
 
 

@@ -268,6 +268,7 @@ class _Engine(NativeLoops):
         self.err_lock = threading.Lock()
         self.apply_events: list = []
         self.native_apply = [0, 0.0, 0.0]   # launches, ms, bytes (native loop, time_apply)
+        self._records: dict = {}             # native loop record buffers per (worker, updater)
         self.side_apply = False             # applies on the high-priority stream (set per run)
         self.native_lock = threading.Lock()
         self.t0 = 0.0

@@ -251,6 +251,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   std::vector<int64_t> claim_of(F, 0);
   std::vector<int> slot_of(F, 0);
   std::vector<double> bytes_of(F, 0.0);
+  std::vector<int64_t> step_of(F, 0);
   uint64_t tag_state = c->tag_seed;
   *st = lpp_updater_stats{};
 
@@ -280,6 +281,16 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       for (int j = 0; j < K; ++j) clean &= ((int64_t)tg[j] >= claim_of[k]);
       __atomic_fetch_add(c->classified, 1, __ATOMIC_ACQ_REL);
       if (clean) __atomic_fetch_add(c->clean, 1, __ATOMIC_ACQ_REL);
+      const int64_t ts = step_of[k];
+      if (c->rec_i64 && ts < c->rec_cap) {
+        c->rec_i64[6 * ts + 5] = clean ? 1 : 0;
+        if (c->rec_tags)
+          for (int j = 0; j < K; ++j) c->rec_tags[(size_t)ts * K + j] = tg[j];
+        if (c->rec_tag_idx) {
+          const int64_t* ti = c->tag_idx_pinned + (size_t)slot_of[k] * K;
+          for (int j = 0; j < K; ++j) c->rec_tag_idx[(size_t)ts * K + j] = ti[j];
+        }
+      }
     }
     if (c->time_apply) {
       float ms = 0.f;
@@ -305,6 +316,13 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     const int slot = (int)(t % depth), next_slot = (int)((t + 1) % depth);
     const int64_t k_claim = __atomic_load_n(c->last_avg_stamp, __ATOMIC_ACQUIRE);
     const int64_t u = __atomic_fetch_add(c->update_order, 1, __ATOMIC_ACQ_REL) + 1;
+    if (c->rec_i64 && t < c->rec_cap) {
+      int64_t* row = c->rec_i64 + 6 * t;
+      int reason = 0;  // select_block's reason (partition.py:132-145)
+      if (c->lpp && s > c->warm_start) reason = ((s - c->warm_start) & 1) ? 1 : 2;
+      row[0] = s, row[1] = u, row[2] = k_claim, row[3] = b, row[4] = reason, row[5] = -1;
+      c->rec_lr[t] = lr;
+    }
     const int64_t lo = c->block_lo[b], hi = c->block_hi[b], len = hi - lo;
     const float lr32 = (float)lr;
     const int buf = host ? (int)(t & 1) : 0;
@@ -373,6 +391,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     used[k] = 1;
     claim_of[k] = k_claim;
     slot_of[k] = slot;
+    step_of[k] = t;
     st->flops += c->flops_of[b];
     ++t;
   }
@@ -383,6 +402,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if ((rc = retire((int)(tt % F))) != LPP_OK) return rc;
   }
   st->steps = t;
+  if (c->rec_count) *c->rec_count = t < c->rec_cap ? t : c->rec_cap;
   return LPP_OK;
 }
 

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .records import AveragerStamp
+from .records import AveragerStamp, UpdateRecord
 
 
 class NativeLoops:
@@ -31,11 +31,11 @@ class NativeLoops:
         the captured graph, or on the host for end-to-end host batches), no
         per-update records, no quiescent pauses."""
         cfg = self.cfg
-        ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode == "off"
+        ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode in ("off", "light")
               and cfg.sampling == "device" and cfg.use_graphs)
         if cfg.host_loop == "native" and not ok:
-            raise ValueError("host_loop='native' needs schedule='async', record_mode='off', "
-                             "sampling='device', CUDA graphs, no quiescent pauses")
+            raise ValueError("host_loop='native' needs schedule='async', record_mode 'off' or "
+                             "'light', sampling='device', CUDA graphs, no quiescent pauses")
         return ok and cfg.host_loop != "python"
 
     def apply_on_side(self) -> bool:
@@ -134,6 +134,19 @@ class NativeLoops:
             c.xbuf[0], c.xbuf[1] = prog.xbs[0].data_ptr(), prog.xbs[1 % prog.nbuf].data_ptr()
             c.ybuf[0], c.ybuf[1] = prog.ybs[0].data_ptr(), prog.ybs[1 % prog.nbuf].data_ptr()
             c.copy_stream = w.copy_streams[r].cuda_stream
+        if cfg.record_mode == "light":
+            rcap = self.budget + 2           # an updater processes at most budget + 1 slots
+            rec = np.zeros((rcap, 6), dtype=np.int64)
+            rlr = np.zeros(rcap, dtype=np.float64)
+            kk = max(k, 1)
+            rti = np.zeros((rcap, kk), dtype=np.int64)
+            rtg = np.zeros((rcap, kk), dtype=np.int32)
+            rcount = np.zeros(1, dtype=np.int64)
+            c.rec_i64, c.rec_lr = rec.ctypes.data, rlr.ctypes.data
+            c.rec_tag_idx = rti.ctypes.data if k else None
+            c.rec_tags = rtg.ctypes.data if k else None
+            c.rec_cap, c.rec_count = rcap, rcount.ctypes.data
+            self._records[(w.q, r)] = (rec, rlr, rti, rtg, rcount, k)
         if self.read_loss:
             cap = self.budget + cfg.updaters + 8
             log = np.zeros(cap, dtype=np.float32)
@@ -156,6 +169,8 @@ class NativeLoops:
             c, keep = self.updater_cfg(w, r)
             st = N.updater_run(c)
             w.programs[r].host_step += int(st.steps)
+            if (q, r) in self._records:
+                self._collect_records(q, r)
             if self.read_loss:
                 log, count = keep[-2], int(keep[-1][0])
                 with self.native_lock:
@@ -227,3 +242,18 @@ class NativeLoops:
         finally:
             if self.nvtx:
                 torch.cuda.nvtx.range_pop()
+
+    _REASONS = ("warm_start", "alternate_full", "alternate_partial")
+
+    def _collect_records(self, q: int, r: int) -> None:
+        """UpdateRecords of one native updater run (record_mode "light")."""
+        rec, rlr, rti, rtg, rcount, k = self._records.pop((q, r))
+        out = self.updates[q * self.cfg.updaters + r]
+        for i in range(int(rcount[0])):
+            s_, u, k_claim, b, reason, clean = (int(v) for v in rec[i])
+            out.append(UpdateRecord(
+                worker=q, rank=r + 1, s=s_, u=u, k_claim=k_claim, block_id=b,
+                reason=self._REASONS[reason], lr=float(rlr[i]), flops=self._flops_of[b],
+                backward_flops=self._bflops_of[b], clean=None if clean < 0 else bool(clean),
+                tag_indices=rti[i, :k].copy() if k else None,
+                tags=rtg[i, :k].astype(np.int64) if k else None))

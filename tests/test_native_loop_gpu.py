@@ -106,7 +106,7 @@ def test_native_loop_repeated_phases_and_ineligible_configs():
     finally:
         tr.close()
     with pytest.raises(ValueError, match="host_loop='native'"):
-        Trainer(_resnet_cfg(obj, record_mode="light")).run()
+        Trainer(_resnet_cfg(obj, record_mode="full")).run()
 
 
 def test_native_loop_trains_like_the_python_loop():
@@ -310,3 +310,40 @@ def test_device_epoch_sampler_and_engine_run():
             assert res.counter_finals == [42, 42] and np.all(np.isfinite(res.final_values))
         finally:
             tr.close()
+
+
+def test_native_loop_light_records_keep_the_reference_invariants():
+    """record_mode="light" through the native loop: one UpdateRecord per
+    processed slot with the reference's invariants (test_engine.py:203-235,
+    308-333) — slots 0..budget+U-1 per worker, update stamps and round
+    stamps one permutation, PASSM+ block rule and reason, lr = lr_at(s),
+    clean flags consistent with p_hat and with the recorded tags."""
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.schedules import lr_at
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    cfg = _resnet_cfg(obj, budget=60, workers=2, updaters=3, record_mode="light")
+    tr = Trainer(cfg)
+    try:
+        assert tr.eng.native_loop()
+        res = tr.run()
+    finally:
+        tr.close()
+    assert res.counter_finals == [63, 63]
+    for q in range(2):
+        recs = [u for u in res.updates if u.worker == q]
+        assert sorted(u.s for u in recs) == list(range(63))
+        orders = [u.u for u in recs] + [st.u for st in res.stamps if st.worker == q]
+        assert sorted(orders) == list(range(1, len(orders) + 1))
+        for u in recs:
+            want = 0 if u.s <= 4 or (u.s - 4) % 2 else u.rank
+            assert u.block_id == want
+            assert u.reason == ("warm_start" if u.s <= 4 else
+                                "alternate_full" if (u.s - 4) % 2 else "alternate_partial")
+            assert u.lr == lr_at(cfg.lr, u.s)
+            assert u.clean is not None and len(u.tags) == 16
+            assert u.clean == bool((u.tags >= u.k_claim).all())
+            assert np.all(np.diff(u.tag_indices) > 0)
+    cleans = [u.clean for u in res.updates]
+    assert abs(res.p_hat - sum(cleans) / len(cleans)) < 1e-12
