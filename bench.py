@@ -114,6 +114,31 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class _Optional:
+    """An optional section of the bench line: a failure there (e.g. an
+    out-of-memory on a smaller box) is recorded in the line instead of
+    losing the headline measurement."""
+
+    def __init__(self, line: dict, key: str):
+        self.line, self.key = line, key
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, et, ev, tb):
+        if et is None or not issubclass(et, Exception):
+            return False
+        self.line.setdefault("optional_errors", {})[self.key] = f"{et.__name__}: {ev}"[:300]
+        try:
+            import torch
+
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+        except Exception:
+            pass
+        return True
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -355,165 +380,171 @@ def ours(args) -> None:
 
     # ---------------- baselines on the same box: MB-SGD and LAP-SGD ----------------
     if not args.no_baselines and ws == 1:
-        mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)
-        mtr = Trainer(mcfg)
-        mtr.run(W * U, evaluate=False)
-        torch.cuda.synchronize()
-        mres = mtr.run(K * U, evaluate=False)
-        mb = K * U * B / (mres.device_ms / 1e3)
-        del mtr
-        lcfg = build_cfg(obj, (K + W) * U, algo="lap_sgd", workers=1)
-        ltr = Trainer(lcfg)
-        ltr.run(W * U, evaluate=False)
-        torch.cuda.synchronize()
-        lres = ltr.run(K * U, evaluate=False)
-        lap = sum(lres.counter_finals) * B / (lres.device_ms / 1e3)
-        ltr.close()
-        del ltr
-        line["baselines"] = {
-            "mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
-                       "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
-            "lap_sgd": {"value": lap, "unit": "images/s", "streams": U,
-                        "note": "same engine, full backprop every step (no PASSM+ blocks)"},
-            "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
+        with _Optional(line, "baselines"):
+            mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)
+            mtr = Trainer(mcfg)
+            mtr.run(W * U, evaluate=False)
+            torch.cuda.synchronize()
+            mres = mtr.run(K * U, evaluate=False)
+            mb = K * U * B / (mres.device_ms / 1e3)
+            del mtr
+            lcfg = build_cfg(obj, (K + W) * U, algo="lap_sgd", workers=1)
+            ltr = Trainer(lcfg)
+            ltr.run(W * U, evaluate=False)
+            torch.cuda.synchronize()
+            lres = ltr.run(K * U, evaluate=False)
+            lap = sum(lres.counter_finals) * B / (lres.device_ms / 1e3)
+            ltr.close()
+            del ltr
+            line["baselines"] = {
+                "mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
+                           "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
+                "lap_sgd": {"value": lap, "unit": "images/s", "streams": U,
+                            "note": "same engine, full backprop every step (no PASSM+ blocks)"},
+                "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
 
     # ---------------- the paper's U = 6 variant ----------------
     if not args.no_baselines and ws == 1:
-        c6 = build_cfg(obj, (K + W) * 6, workers=1, updaters=6)
-        t6 = Trainer(c6)
-        t6.run(W * 6, evaluate=False)
-        torch.cuda.synchronize()
-        r6 = t6.run(K * 6, evaluate=False)
-        line["baselines"]["lpp_sgd_u6"] = {
-            "value": sum(r6.counter_finals) * B / (r6.device_ms / 1e3), "unit": "images/s",
-            "streams": 6, "note": "same workload with 6 updater streams (the paper's best LPP row)"}
-        t6.close()
-        del t6
+        with _Optional(line, "lpp_sgd_u6"):
+            c6 = build_cfg(obj, (K + W) * 6, workers=1, updaters=6)
+            t6 = Trainer(c6)
+            t6.run(W * 6, evaluate=False)
+            torch.cuda.synchronize()
+            r6 = t6.run(K * 6, evaluate=False)
+            line["baselines"]["lpp_sgd_u6"] = {
+                "value": sum(r6.counter_finals) * B / (r6.device_ms / 1e3), "unit": "images/s",
+                "streams": 6, "note": "same workload with 6 updater streams (the paper's best LPP row)"}
+            t6.close()
+            del t6
 
     # ---------------- ResNet-18 / CIFAR-100 shape (config C2) ----------------
     if not args.no_rn18 and ws == 1:
-        obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
-        out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s"}
-        for algo in ("lpp_sgd", "mb_sgd"):
-            c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=1)
-            t18 = Trainer(c18, time_apply=(algo == "lpp_sgd"))
-            t18.run(3 * U, evaluate=False)
-            torch.cuda.synchronize()
-            r18 = t18.run(args.rn18_steps * U, evaluate=False)
-            n18 = sum(r18.counter_finals) if algo == "lpp_sgd" else args.rn18_steps * U
-            out18[algo] = n18 * B / (r18.device_ms / 1e3)
-            if algo == "lpp_sgd":
-                na, msa, bya = r18.apply_timing
-                a18 = bya / (msa / 1e3) / 1e9
-                out18["apply_roofline"] = {"achieved": a18, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                           "frac": a18 / peaks["hbm_gbs"], "launches": na,
-                                           "avg_us": 1e3 * msa / max(na, 1),
-                                           "bytes_per_launch": bya / max(na, 1)}
-                t18.close()
-            del t18
-        out18["lpp_over_mb"] = out18["lpp_sgd"] / out18["mb_sgd"]
-        line["resnet18"] = out18
+        with _Optional(line, "resnet18"):
+            obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
+            out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s"}
+            for algo in ("lpp_sgd", "mb_sgd"):
+                c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=1)
+                t18 = Trainer(c18, time_apply=(algo == "lpp_sgd"))
+                t18.run(3 * U, evaluate=False)
+                torch.cuda.synchronize()
+                r18 = t18.run(args.rn18_steps * U, evaluate=False)
+                n18 = sum(r18.counter_finals) if algo == "lpp_sgd" else args.rn18_steps * U
+                out18[algo] = n18 * B / (r18.device_ms / 1e3)
+                if algo == "lpp_sgd":
+                    na, msa, bya = r18.apply_timing
+                    a18 = bya / (msa / 1e3) / 1e9
+                    out18["apply_roofline"] = {"achieved": a18, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                               "frac": a18 / peaks["hbm_gbs"], "launches": na,
+                                               "avg_us": 1e3 * msa / max(na, 1),
+                                               "bytes_per_launch": bya / max(na, 1)}
+                    t18.close()
+                del t18
+            out18["lpp_over_mb"] = out18["lpp_sgd"] / out18["mb_sgd"]
+            line["resnet18"] = out18
 
     # ---------------- ResNet-50 / ImageNet shape (config C3): in-situ HBM apply ----------------
     if not args.no_rn50 and ws == 1:
-        obj50 = ResNetObjective("resnet50", n_samples=2048, seed=0, data="device")
-        c50 = build_cfg(obj50, 64, workers=1)
-        # C3: B = 32 per stream, non-blocking averaging every H = 16 local
-        # steps from the start (switch_point 0)
-        c50 = dataclasses.replace(c50, batch_size=32,
-                                  sync=SyncScheme(total=c50.sync.total, period=16, switch_point=0))
-        t50 = Trainer(c50, time_apply=True)
-        t50.run(3 * U, evaluate=False)
-        torch.cuda.synchronize()
-        r50 = t50.run(args.rn50_steps * U, evaluate=False)
-        n50, ms50, by50 = r50.apply_timing
-        a50 = by50 / (ms50 / 1e3) / 1e9
-        line["resnet50"] = {
-            "workload": "resnet50_imagenet224_lpp_sgd_u4_b32_h16", "params": obj50.dim,
-            "value": sum(r50.counter_finals) * 32 / (r50.device_ms / 1e3), "unit": "images/s",
-            "apply_roofline": {"achieved": a50, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                               "frac": a50 / peaks["hbm_gbs"], "launches": n50,
-                               "avg_us": 1e3 * ms50 / max(n50, 1),
-                               "bytes_per_launch": by50 / max(n50, 1)}}
-        t50.close()
-        del t50
-        m50 = build_cfg(obj50, 64, algo="mb_sgd", workers=1)
-        m50 = dataclasses.replace(m50, batch_size=32)
-        tm50 = Trainer(m50)
-        tm50.run(3 * U, evaluate=False)
-        torch.cuda.synchronize()
-        rm50 = tm50.run(args.rn50_steps * U, evaluate=False)
-        line["resnet50"]["mb_sgd"] = args.rn50_steps * U * 32 / (rm50.device_ms / 1e3)
-        line["resnet50"]["lpp_over_mb"] = line["resnet50"]["value"] / line["resnet50"]["mb_sgd"]
-        del tm50
+        with _Optional(line, "resnet50"):
+            obj50 = ResNetObjective("resnet50", n_samples=2048, seed=0, data="device")
+            c50 = build_cfg(obj50, 64, workers=1)
+            # C3: B = 32 per stream, non-blocking averaging every H = 16 local
+            # steps from the start (switch_point 0)
+            c50 = dataclasses.replace(c50, batch_size=32,
+                                      sync=SyncScheme(total=c50.sync.total, period=16, switch_point=0))
+            t50 = Trainer(c50, time_apply=True)
+            t50.run(3 * U, evaluate=False)
+            torch.cuda.synchronize()
+            r50 = t50.run(args.rn50_steps * U, evaluate=False)
+            n50, ms50, by50 = r50.apply_timing
+            a50 = by50 / (ms50 / 1e3) / 1e9
+            line["resnet50"] = {
+                "workload": "resnet50_imagenet224_lpp_sgd_u4_b32_h16", "params": obj50.dim,
+                "value": sum(r50.counter_finals) * 32 / (r50.device_ms / 1e3), "unit": "images/s",
+                "apply_roofline": {"achieved": a50, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                   "frac": a50 / peaks["hbm_gbs"], "launches": n50,
+                                   "avg_us": 1e3 * ms50 / max(n50, 1),
+                                   "bytes_per_launch": by50 / max(n50, 1)}}
+            t50.close()
+            del t50
+            m50 = build_cfg(obj50, 64, algo="mb_sgd", workers=1)
+            m50 = dataclasses.replace(m50, batch_size=32)
+            tm50 = Trainer(m50)
+            tm50.run(3 * U, evaluate=False)
+            torch.cuda.synchronize()
+            rm50 = tm50.run(args.rn50_steps * U, evaluate=False)
+            line["resnet50"]["mb_sgd"] = args.rn50_steps * U * 32 / (rm50.device_ms / 1e3)
+            line["resnet50"]["lpp_over_mb"] = line["resnet50"]["value"] / line["resnet50"]["mb_sgd"]
+            del tm50
 
     # ---------------- kernel sweep (HBM roofline evidence) ----------------
     if not args.no_sweep and rank == 0:
-        from paper_2203_06638_b200.arena import Arena
+        with _Optional(line, "kernel_sweep"):
+            from paper_2203_06638_b200.arena import Arena
 
-        st = torch.cuda.current_stream().cuda_stream
-        scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-        sweep = []
-        for d in (16_000_000, 64_000_000):
-            x, g, m = Arena(d, dev), Arena(d, dev), Arena(d, dev)
-            r_ = Arena(d, dev)
-            for name, fn, bpe in (
-                ("apply_red", lambda: N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st), 12),
-                ("apply_red_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st), 20),
-                ("apply_bulk_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_BULK, st), 20),
-                ("snapshot", lambda: N.snapshot(x.ptr, r_.ptr, d, st), 8),
-            ):
-                for _ in range(5):
-                    fn()
+            st = torch.cuda.current_stream().cuda_stream
+            scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+            sweep = []
+            for d in (16_000_000, 64_000_000):
+                x, g, m = Arena(d, dev), Arena(d, dev), Arena(d, dev)
+                r_ = Arena(d, dev)
+                for name, fn, bpe in (
+                    ("apply_red", lambda: N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st), 12),
+                    ("apply_red_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st), 20),
+                    ("apply_bulk_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_BULK, st), 20),
+                    ("snapshot", lambda: N.snapshot(x.ptr, r_.ptr, d, st), 8),
+                ):
+                    for _ in range(5):
+                        fn()
+                    ts = []
+                    for _ in range(10):
+                        N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record()
+                        fn()
+                        b.record()
+                        b.synchronize()
+                        ts.append(a.elapsed_time(b))
+                    t = sorted(ts)[len(ts) // 2] / 1e3
+                    gbs = bpe * d / t / 1e9
+                    sweep.append({"kernel": name, "params": d, "us": t * 1e6, "gbs": gbs,
+                                  "frac": gbs / peaks["hbm_gbs"]})
+                # K4 over Q=4 arenas in this one HBM (the NVLink path needs >1 GPU):
+                # DRAM bytes = read + write-back of every arena element
+                ars = [x, r_, Arena(d, dev), Arena(d, dev)]
+                for _ in range(3):
+                    N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
                 ts = []
                 for _ in range(10):
                     N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record()
-                    fn()
+                    N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
                     b.record()
                     b.synchronize()
                     ts.append(a.elapsed_time(b))
                 t = sorted(ts)[len(ts) // 2] / 1e3
-                gbs = bpe * d / t / 1e9
-                sweep.append({"kernel": name, "params": d, "us": t * 1e6, "gbs": gbs,
+                gbs = 8 * 4 * d / t / 1e9
+                sweep.append({"kernel": "average_q4_local_hbm", "params": d, "us": t * 1e6, "gbs": gbs,
                               "frac": gbs / peaks["hbm_gbs"]})
-            # K4 over Q=4 arenas in this one HBM (the NVLink path needs >1 GPU):
-            # DRAM bytes = read + write-back of every arena element
-            ars = [x, r_, Arena(d, dev), Arena(d, dev)]
-            for _ in range(3):
-                N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
-            ts = []
-            for _ in range(10):
-                N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
-                b.record()
-                b.synchronize()
-                ts.append(a.elapsed_time(b))
-            t = sorted(ts)[len(ts) // 2] / 1e3
-            gbs = 8 * 4 * d / t / 1e9
-            sweep.append({"kernel": "average_q4_local_hbm", "params": d, "us": t * 1e6, "gbs": gbs,
-                          "frac": gbs / peaks["hbm_gbs"]})
-            for a_ in (x, g, m, r_) + tuple(ars[2:]):
-                a_.close()
-        line["kernel_sweep"] = sweep
+                for a_ in (x, g, m, r_) + tuple(ars[2:]):
+                    a_.close()
+            line["kernel_sweep"] = sweep
 
     # ---------------- CPU baseline (rank 0, N=1) ----------------
     if not args.no_cpu and rank == 0 and ws == 1:
-        from oracle.engine_port import run_lpp_cpu
+        with _Optional(line, "cpu_baseline"):
+            from oracle.engine_port import run_lpp_cpu
 
-        # bounded sample of the same workload: ~100 minibatches, 10-15 s of
-        # CPU work on the box's host cores (after a short warm-up)
-        run_lpp_cpu(slots=U, updaters=U, batch_size=B)
-        r = run_lpp_cpu(slots=24 * U, updaters=U, batch_size=B)
-        line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
-                                "cores": r["cores"], "kind": "port",
-                                "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
-                                          f"(port of engine.py:289-523 incl. averager + tags), "
-                                          f"torch-CPU ResNet-20 grads, store ops via the "
-                                          f"reference's compiled _atomics ({r['atomics']})"}
+            # bounded sample of the same workload: ~100 minibatches, 10-15 s of
+            # CPU work on the box's host cores (after a short warm-up)
+            run_lpp_cpu(slots=U, updaters=U, batch_size=B)
+            r = run_lpp_cpu(slots=24 * U, updaters=U, batch_size=B)
+            line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
+                                    "cores": r["cores"], "kind": "port",
+                                    "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
+                                              f"(port of engine.py:289-523 incl. averager + tags), "
+                                              f"torch-CPU ResNet-20 grads, store ops via the "
+                                              f"reference's compiled _atomics ({r['atomics']})"}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.out:
