@@ -155,10 +155,12 @@ def reference_arm(args) -> None:
     from oracle.engine_port import run_lpp_cpu
 
     cores = len(os.sched_getaffinity(0))
-    run_lpp_cpu(slots=max(args.warmup, 1) * U - U, updaters=U, batch_size=B)  # warm-up
-    r = run_lpp_cpu(slots=max(args.steps * U - U, 1), updaters=U, batch_size=B, threads=cores)
+    # a reference-arm step is ONE minibatch of B images (a bounded sample of
+    # the workload: K = 200 steps is ~25 s of CPU work); images/s is the metric
+    run_lpp_cpu(slots=max(args.warmup - U, 1), updaters=U, batch_size=B)  # warm-up
+    r = run_lpp_cpu(slots=max(args.steps - U, 1), updaters=U, batch_size=B, threads=cores)
     value = r["images"] / r["seconds"]
-    steps = r["minibatches"] / U
+    steps = r["minibatches"]
     line = {
         "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / steps,
@@ -168,7 +170,8 @@ def reference_arm(args) -> None:
                    "batch_per_updater": B, "updaters_per_gpu": U, "workers": 1, "blocks": U,
                    "parallelism": f"lpp_sgd_q1_u{U}", "device": "host CPU (reference arm)"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"], "kind": "port",
-                         "sample": f"{r['minibatches']} minibatches x {B} images (LPP-SGD, U={U}, "
+                         "sample": f"{r['minibatches']} minibatches x {B} images, one minibatch per "
+                                   f"reference-arm step (LPP-SGD, U={U}, "
                                    f"threaded port of engine.py:289-523 incl. the averager and "
                                    f"write tags, torch-CPU ResNet-20 grads, store ops = the "
                                    f"reference's own compiled _atomics ({r['atomics']}))"},
@@ -557,8 +560,8 @@ def ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)   # timed minibatches = steps x U; ramp-up and drain are <2 % at 200
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
