@@ -51,5 +51,8 @@ ars = [Arena(d, 0) for _ in range(4)]
 for _ in range(2):
     flush()
     N.average_shard([a.ptr for a in ars], 0, d, None, N.MODE_RED, st)
+for _ in range(2):
+    flush()
+    N.average_shard([a.ptr for a in ars], 0, d, None, N.MODE_BULK, st)   # TMA-staged K4
 torch.cuda.synchronize()
 print("ok")
