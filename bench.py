@@ -533,6 +533,36 @@ def ours(args) -> None:
                     a_.close()
             line["kernel_sweep"] = sweep
 
+    # ---------------- the reference's own store primitives on this host ----------------
+    # accum_cas_f64 (the apply) and snapshot_f64 (K3) of the
+    # reference's compiled _atomics, 1 thread, at 1M / 4M elements (fp64)
+    if not args.no_cpu and rank == 0 and ws == 1:
+        with _Optional(line, "cpu_reference_primitives"):
+            import numpy as np
+
+            from oracle.native import reference_atomics
+
+            at = reference_atomics()
+            if at is not None:
+                prims = []
+                for d in (1_000_000, 4_000_000):
+                    x = np.random.default_rng(0).normal(size=d)
+                    g = 1e-3 * np.random.default_rng(1).normal(size=d)
+                    out = np.empty(d)
+                    for name, fn, nbytes in (("accum_cas_f64", lambda: at.accum_cas_f64(x, 0, g, -1.0), 24 * d),
+                                             ("snapshot_f64", lambda: at.snapshot_f64(x, out), 16 * d)):
+                        fn()
+                        t0 = time.perf_counter()
+                        reps = 3
+                        for _ in range(reps):
+                            fn()
+                        sec = (time.perf_counter() - t0) / reps
+                        prims.append({"primitive": name, "elements": d, "ms": 1e3 * sec,
+                                      "gbs": nbytes / sec / 1e9})
+                line["cpu_reference_primitives"] = {
+                    "threads": 1, "source": "oracle/_ref (the reference's _atomics.c, compiled from "
+                                            "its own source)", "rows": prims}
+
     # ---------------- CPU baseline (rank 0, N=1) ----------------
     if not args.no_cpu and rank == 0 and ws == 1:
         with _Optional(line, "cpu_baseline"):
