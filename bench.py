@@ -559,6 +559,22 @@ def ours(args) -> None:
                         sec = (time.perf_counter() - t0) / reps
                         prims.append({"primitive": name, "elements": d, "ms": 1e3 * sec,
                                       "gbs": nbytes / sec / 1e9})
+                # one averaging round of the reference at Q = 2 (engine.py:418-421,
+                # 199-229): snapshot both stores, fixed-order mean, add_assign
+                # (mean - snap) through the reference's CAS accumulate
+                d = 1_000_000
+                xs = [np.random.default_rng(q).normal(size=d) for q in range(2)]
+                snaps = [np.empty(d) for _ in range(2)]
+                t0 = time.perf_counter()
+                for q in range(2):
+                    at.snapshot_f64(xs[q], snaps[q])
+                mean = np.mean(np.stack(snaps), axis=0)
+                for q in range(2):
+                    at.accum_cas_f64(xs[q], 0, mean - snaps[q], 1.0)
+                sec = time.perf_counter() - t0
+                prims.append({"primitive": "averaging_round_Q2 (snapshot + mean + add_assign)",
+                              "elements": d, "ms": 1e3 * sec,
+                              "gbs_busbw_convention": 2 * (2 - 1) / 2 * 8 * d / sec / 1e9})
                 line["cpu_reference_primitives"] = {
                     "threads": 1, "source": "oracle/_ref (the reference's _atomics.c, compiled from "
                                             "its own source)", "rows": prims}
