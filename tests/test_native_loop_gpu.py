@@ -347,3 +347,23 @@ def test_native_loop_light_records_keep_the_reference_invariants():
             assert np.all(np.diff(u.tag_indices) > 0)
     cleans = [u.clean for u in res.updates]
     assert abs(res.p_hat - sum(cleans) / len(cleans)) < 1e-12
+
+
+@pytest.mark.parametrize("in_flight", [1, 4])
+def test_native_loop_in_flight_depths(in_flight):
+    """The in-flight window (events per slot, staging rings of depth
+    in_flight + 2) at other depths: counters, records and losses stay whole."""
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0, data="host")
+    tr = Trainer(_resnet_cfg(obj, budget=30, workers=1, updaters=4, in_flight=in_flight,
+                             record_mode="light"), host_batches=True, read_loss=True)
+    try:
+        res = tr.run()
+        assert res.counter_finals == [34]
+        assert len(res.updates) == 34 and len(res.losses) == 34
+        assert all(u.clean is not None for u in res.updates)
+        assert np.all(np.isfinite(res.losses))
+    finally:
+        tr.close()
