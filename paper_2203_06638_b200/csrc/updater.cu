@@ -396,11 +396,8 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     ++t;
   }
   CUDA_TRY(cudaStreamSynchronize(stream));
-  for (int64_t j = 1; j <= F; ++j) {
-    int64_t tt = t - j;
-    if (tt < 0) break;
+  for (int64_t tt = t - F < 0 ? 0 : t - F; tt < t; ++tt)   // the last steps, in step order
     if ((rc = retire((int)(tt % F))) != LPP_OK) return rc;
-  }
   st->steps = t;
   if (c->rec_count) *c->rec_count = t < c->rec_cap ? t : c->rec_cap;
   return LPP_OK;
