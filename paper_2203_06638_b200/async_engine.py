@@ -651,9 +651,8 @@ class _Engine(NativeLoops):
                 self.flops.add(self._flops_of[choice.block_id])
                 t += 1
             w.streams[r].synchronize()
-            for j in range(1, cfg.in_flight + 1):
-                tt = t - j
-                if tt >= 0 and used[tt % cfg.in_flight]:
+            for tt in range(max(t - cfg.in_flight, 0), t):     # the last steps, in step order
+                if used[tt % cfg.in_flight]:
                     if self.read_loss:
                         self.loss_log.append(self.loss_value(w, r, tt % depth, tt % 2))
                     self.classify(w, r, tt % depth, pending[tt % cfg.in_flight])
