@@ -31,7 +31,7 @@ from typing import NamedTuple, Sequence
 
 
 class Block(NamedTuple):
-    """Half-open element range [start, stop) of the arena."""
+    """Element range [start, stop) of the flat arena (a K1/K2 apply range)."""
 
     start: int
     stop: int
@@ -42,9 +42,11 @@ class Block(NamedTuple):
 
 
 class SelectionReason(enum.Enum):
-    WARM_START = "warm_start"
-    ALTERNATE_FULL = "alternate_full"
-    ALTERNATE_PARTIAL = "alternate_partial"
+    """Why a slot trains the block it trains (partition.py:132-145)."""
+
+    WARM_START = "warm_start"                # s <= T_st: everyone trains the full model
+    ALTERNATE_FULL = "alternate_full"        # odd distance past T_st: full model
+    ALTERNATE_PARTIAL = "alternate_partial"  # even distance: the updater's own block
 
 
 @dataclass(frozen=True)
@@ -55,6 +57,9 @@ class BlockChoice:
 
 @dataclass(frozen=True)
 class BlockPartition:
+    """Boundaries 0 = b_0 < ... < b_U = dim; block 0 is the whole arena,
+    block i in 1..U the slice [b_{i-1}, b_i)."""
+
     dim: int
     boundaries: tuple[int, ...]
 
@@ -63,35 +68,43 @@ class BlockPartition:
         return len(self.boundaries) - 1
 
     def block(self, block_id: int) -> Block:
+        u = self.num_blocks
         if block_id == 0:
             return Block(0, self.dim)
-        if block_id < 1 or block_id > self.num_blocks:
-            raise ValueError(f"block id {block_id} outside [0, {self.num_blocks}]")
-        return Block(self.boundaries[block_id - 1], self.boundaries[block_id])
+        if 0 < block_id <= u:
+            return Block(*self.boundaries[block_id - 1:block_id + 1])
+        raise ValueError(f"block id {block_id} outside [0, {u}]")
 
     def blocks(self) -> list[Block]:
-        return [self.block(i) for i in range(1, self.num_blocks + 1)]
+        return [Block(a, b) for a, b in zip(self.boundaries, self.boundaries[1:])]
+
+
+def _partition_error(dim: int, b: tuple[int, ...]) -> str | None:
+    if dim < 0:
+        return "dimension must be non-negative"
+    if len(b) < 2 or b[0] != 0 or b[-1] != dim:
+        return f"boundaries must run from 0 to {dim}, got {b}"
+    if not all(x < y for x, y in zip(b, b[1:])):
+        return f"boundaries must be strictly ascending, got {b}"
+    return None
 
 
 def make_partition(dim: int, boundaries: Sequence[int]) -> BlockPartition:
-    b = tuple(int(v) for v in boundaries)
-    if dim < 0:
-        raise ValueError("dimension must be non-negative")
-    if len(b) < 2 or b[0] != 0 or b[-1] != dim:
-        raise ValueError(f"boundaries must run from 0 to {dim}, got {b}")
-    if any(hi <= lo for lo, hi in zip(b, b[1:])):
-        raise ValueError(f"boundaries must be strictly ascending, got {b}")
+    b = tuple(map(int, boundaries))
+    err = _partition_error(dim, b)
+    if err is not None:
+        raise ValueError(err)
     return BlockPartition(dim, b)
 
 
 def even_boundaries(dim: int, num_blocks: int) -> tuple[int, ...]:
-    if num_blocks < 1 or num_blocks > dim:
+    """Near-equal contiguous slices (unlayered objectives): the first
+    ``dim % num_blocks`` slices hold one extra element."""
+    if not 1 <= num_blocks <= dim:
         raise ValueError(f"cannot split {dim} elements into {num_blocks} blocks")
-    q, r = divmod(dim, num_blocks)
-    out = [0]
-    for i in range(num_blocks):
-        out.append(out[-1] + q + (i < r))
-    return tuple(out)
+    base, extra = divmod(dim, num_blocks)
+    sizes = [base + 1] * extra + [base] * (num_blocks - extra)
+    return (0, *itertools.accumulate(sizes))
 
 
 def _min_blocks_from(sizes: list[int], start: int, cap: int) -> int:
