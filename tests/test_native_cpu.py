@@ -231,3 +231,24 @@ def test_device_epoch_sampler_host_twin_covers_each_epoch():
             assert orders[0] != orders[1] != orders[2]
     assert np.array_equal(N.sample_epoch_host(16, 0, 1, 100, 5, 9), N.sample_epoch_host(16, 0, 1, 100, 5, 9))
     assert not np.array_equal(N.sample_epoch_host(16, 0, 1, 100, 5, 9), N.sample_epoch_host(16, 0, 1, 100, 6, 9))
+
+
+def test_native_loops_validate_before_touching_the_device():
+    """The C++ loops reject incomplete configurations with status codes (no
+    device work, no crash) — the error channel the engine turns into a
+    failed run."""
+    with pytest.raises(ValueError, match="null"):
+        N.updater_run(N.UpdaterCfg())
+    cells = np.zeros(4, dtype=np.int64)
+    c = N.UpdaterCfg()
+    c.sample_counter = c.update_order = c.stop = c.last_avg_stamp = cells.ctypes.data
+    with pytest.raises(ValueError, match="block tables"):
+        N.updater_run(c)
+    with pytest.raises(ValueError, match="null"):
+        N.averager_run(N.AveragerCfg())
+    a = N.AveragerCfg()
+    a.ctrl = a.sample_counter = a.update_order = a.exited = a.last_avg_stamp = a.synced_at = cells.ctypes.data
+    a.arenas = a.mean_out = cells.ctypes.data
+    a.workers, a.q = 9, 0
+    with pytest.raises(ValueError, match="worker"):
+        N.averager_run(a)
