@@ -514,21 +514,23 @@ def ours(args) -> None:
                 # K4 over Q=4 arenas in this one HBM (the NVLink path needs >1 GPU):
                 # DRAM bytes = read + write-back of every arena element
                 ars = [x, r_, Arena(d, dev), Arena(d, dev)]
-                for _ in range(3):
-                    N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
-                ts = []
-                for _ in range(10):
-                    N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record()
-                    N.average_shard([a_.ptr for a_ in ars], 0, d, None, N.MODE_RED, st)
-                    b.record()
-                    b.synchronize()
-                    ts.append(a.elapsed_time(b))
-                t = sorted(ts)[len(ts) // 2] / 1e3
-                gbs = 8 * 4 * d / t / 1e9
-                sweep.append({"kernel": "average_q4_local_hbm", "params": d, "us": t * 1e6, "gbs": gbs,
-                              "frac": gbs / peaks["hbm_gbs"]})
+                for kname, kmode in (("average_q4_local_hbm", N.MODE_RED),
+                                     ("average_q4_local_hbm_tma", N.MODE_BULK)):
+                    for _ in range(3):
+                        N.average_shard([a_.ptr for a_ in ars], 0, d, None, kmode, st)
+                    ts = []
+                    for _ in range(10):
+                        N.l2_flush(scratch.data_ptr(), scratch.numel(), st)
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record()
+                        N.average_shard([a_.ptr for a_ in ars], 0, d, None, kmode, st)
+                        b.record()
+                        b.synchronize()
+                        ts.append(a.elapsed_time(b))
+                    t = sorted(ts)[len(ts) // 2] / 1e3
+                    gbs = 8 * 4 * d / t / 1e9
+                    sweep.append({"kernel": kname, "params": d, "us": t * 1e6, "gbs": gbs,
+                                  "frac": gbs / peaks["hbm_gbs"]})
                 for a_ in (x, g, m, r_) + tuple(ars[2:]):
                     a_.close()
             line["kernel_sweep"] = sweep
