@@ -406,6 +406,23 @@ def ours(args) -> None:
                             "note": "same engine, full backprop every step (no PASSM+ blocks)"},
                 "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
 
+    # ---------------- MB-SGD at the same images per step as LPP (B = U x 128) ----------------
+    # the paper's "MB-SGD B=1024" rows: one big synchronous batch per step
+    # (bigger kernels, fewer updates); reported beside, not the headline ratio
+    if not args.no_baselines and ws == 1:
+        with _Optional(line, "mb_sgd_large_batch"):
+            bl = B * U
+            mcfg = dataclasses.replace(build_cfg(obj, (K + W), algo="mb_sgd", workers=1), batch_size=bl)
+            mtr = Trainer(mcfg)
+            mtr.run(W, evaluate=False)
+            torch.cuda.synchronize()
+            mres = mtr.run(K, evaluate=False)
+            line["baselines"]["mb_sgd_b%d" % bl] = {
+                "value": K * bl / (mres.device_ms / 1e3), "unit": "images/s", "batch": bl, "streams": 1,
+                "note": "synchronous SGD, one batch of U x 128 per step (as many images per step as "
+                        "the U LPP updaters together, U x fewer model updates)"}
+            del mtr
+
     # ---------------- the paper's U = 6 variant ----------------
     if not args.no_baselines and ws == 1:
         with _Optional(line, "lpp_sgd_u6"):
