@@ -423,6 +423,22 @@ typedef struct {
   int64_t* rec;                   /* [max_records][5] round, u, s_cur, k_delta, unanimous */
   double* rec_wall_ms;            /* [max_records] */
   int64_t max_records;
+  /* eval points (engine.py:445-451, worker 0): with eval_interval > 0 every
+   * round writes its mean and is fenced; at the first non-final round with
+   * s_cur past the next multiple of eval_interval worker 0 copies the round
+   * mean (the owners' mean_out shards, or — mean_parts == NULL, one process
+   * per GPU — its own arena) into eval_buf and records the point */
+  int64_t eval_interval;
+  float* const* mean_parts;       /* [Q] every owner's mean_out base, or NULL */
+  const int64_t* shard_bounds;    /* [Q + 1] owner shard boundaries */
+  float* eval_buf;                /* [eval_cap][n] */
+  int64_t eval_cap;
+  int64_t* eval_rec;              /* [eval_cap][5] s_cur, round, flops, classified, clean */
+  double* eval_wall_ms;           /* [eval_cap] */
+  int64_t* eval_count;
+  const int64_t* flops_cell;
+  const int64_t* classified_cell;
+  const int64_t* clean_cell;
 } lpp_averager_cfg;
 
 int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);

@@ -89,6 +89,9 @@ class AveragerCfg(ctypes.Structure):
         ("stop_after", _c.c_int64), ("arenas", _vp), ("tags", _vp), ("lo", _size), ("hi", _size),
         ("n", _size), ("mean_out", _vp), ("stream", _vp), ("t0", _c.c_double), ("rec", _vp),
         ("rec_wall_ms", _vp), ("max_records", _c.c_int64),
+        ("eval_interval", _c.c_int64), ("mean_parts", _vp), ("shard_bounds", _vp), ("eval_buf", _vp),
+        ("eval_cap", _c.c_int64), ("eval_rec", _vp), ("eval_wall_ms", _vp), ("eval_count", _vp),
+        ("flops_cell", _vp), ("classified_cell", _vp), ("clean_cell", _vp),
     ]
 
 

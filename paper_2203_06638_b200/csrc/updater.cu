@@ -462,6 +462,13 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
   int64_t s_pre = 0, round_no = 0;
   double backoff = 0.0;
   *rounds_out = 0;
+  const bool evalm = c->eval_interval > 0;
+  if (evalm && (!c->eval_buf || !c->eval_rec || !c->eval_wall_ms || !c->eval_count ||
+                !c->shard_bounds || !c->flops_cell || !c->classified_cell || !c->clean_cell))
+    return set_err(LPP_E_VALUE, "averager_run: eval buffers missing");
+  int64_t next_eval = c->eval_interval;
+  if (evalm) *c->eval_count = 0;
+  const bool fenced = c->tagged || evalm;
   auto wait_ge = [&](const int64_t* p, int64_t target) -> bool {
     return lpp_atomic_wait_ge_i64(p, target, abort_, 200) != INT64_MIN;
   };
@@ -501,20 +508,21 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
     const int64_t u = add(c->update_order, 1) + 1;
     bool ok = true;
     int32_t stamps[LPP_MAX_WORKERS] = {0};
-    if (c->tagged) {
+    if (fenced) {
       st(cell(c, kStamps + c->q), u);
       add(fence_cell(c, 0, r), 1);
       ok = wait_ge(fence_cell(c, 0, r), Q);
       for (int i = 0; ok && i < Q; ++i) stamps[i] = (int32_t)ld(cell(c, kStamps + i));
     }
+    const bool with_mean = drain || evalm;   // eval points need every round's mean
     if (ok) {
       int rc = LPP_OK;
       if (Q == 1) {
         // a single worker's mean is itself (test_engine.py:169-182)
-        if (drain) rc = lpp_snapshot(c->arenas[0], c->mean_out, c->n, stream);
+        if (with_mean) rc = lpp_snapshot(c->arenas[0], c->mean_out, c->n, stream);
         if (rc == LPP_OK && c->tagged) rc = lpp_fill_i32(c->tags[0], c->n, stamps[0], stream);
       } else {
-        float* mean = drain ? c->mean_out + c->lo : nullptr;
+        float* mean = with_mean ? c->mean_out + c->lo : nullptr;
         rc = c->tagged ? lpp_average_shard_tagged(c->arenas, c->tags, stamps, Q, c->lo, c->hi, mean,
                                                   LPP_MODE_RED, stream)
                        : lpp_average_shard(c->arenas, Q, c->lo, c->hi, mean, LPP_MODE_RED, stream);
@@ -525,7 +533,7 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
         fail(LPP_E_CUDA);
         return set_err(LPP_E_CUDA, "averager: stream sync failed: %s", cudaGetErrorString(e));
       }
-      if (c->tagged) {
+      if (fenced) {
         add(fence_cell(c, 1, r), 1);
         ok = wait_ge(fence_cell(c, 1, r), Q);
       }
@@ -545,6 +553,29 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
       if (c->rec_wall_ms) c->rec_wall_ms[round_no - 1] = 1e3 * (now_s() - c->t0);
     }
     *rounds_out = round_no;
+    // eval point (worker 0): this round's mean, assembled from the owners
+    if (evalm && ok && c->q == 0 && !unanimous && s_cur >= next_eval &&
+        *c->eval_count < c->eval_cap) {
+      const int64_t i = *c->eval_count;
+      float* dst = c->eval_buf + (size_t)i * c->n;
+      if (c->mean_parts) {
+        for (int o = 0; o < Q; ++o) {
+          const int64_t a = c->shard_bounds[o], b = c->shard_bounds[o + 1];
+          if (b > a)
+            CUDA_TRY(cudaMemcpyAsync(dst + a, c->mean_parts[o] + a, 4 * (size_t)(b - a),
+                                     cudaMemcpyDeviceToDevice, stream));
+        }
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(dst, c->arenas[c->q], 4 * c->n, cudaMemcpyDeviceToDevice, stream));
+      }
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      int64_t* row = c->eval_rec + 5 * i;
+      row[0] = s_cur, row[1] = r, row[2] = ld(c->flops_cell);
+      row[3] = ld(c->classified_cell), row[4] = ld(c->clean_cell);
+      c->eval_wall_ms[i] = 1e3 * (now_s() - c->t0);
+      *c->eval_count = i + 1;
+      while (next_eval <= s_cur) next_eval += c->eval_interval;
+    }
     s_pre = s_cur;
     if (unanimous) break;
   }

@@ -195,7 +195,7 @@ class NativeLoops:
         averaging without quiescent pauses, eval points or full records."""
         cfg = self.cfg
         return (cfg.host_loop != "python" and cfg.schedule == "async" and not cfg.quiescent
-                and not self.nvls and cfg.eval_interval == 0 and cfg.record_mode != "full")
+                and not self.nvls and cfg.record_mode != "full")
 
     def averager_native(self, q: int) -> None:
         """a11 in native code: the round protocol + K4 in one GIL-free call."""
@@ -232,7 +232,33 @@ class NativeLoops:
             c.stream = w.avg_stream.cuda_stream
             c.t0 = self.t0
             c.rec, c.rec_wall_ms, c.max_records = rec.ctypes.data, wall.ctypes.data, cap
+            keep = []
+            if cfg.eval_interval > 0:
+                # eval points (engine.py:445-451): worker 0 keeps round means
+                ecap = (self.budget // cfg.eval_interval + 2) if q == 0 else 0
+                ebuf = torch.empty((max(ecap, 1), self.dim), dtype=torch.float32, device=w.dev)
+                erec = np.zeros((max(ecap, 1), 5), dtype=np.int64)
+                ewall = np.zeros(max(ecap, 1), dtype=np.float64)
+                ecount = np.zeros(1, dtype=np.int64)
+                bounds = np.array([lo_ for lo_, _ in self.shards] + [self.shards[-1][1]], dtype=np.int64)
+                parts = None
+                if self.group is None:
+                    parts = (ctypes.c_void_p * Q)(*[self.workers[o].mean_out.data_ptr() for o in range(Q)])
+                c.eval_interval = cfg.eval_interval
+                c.mean_parts = ctypes.addressof(parts) if parts is not None else None
+                c.shard_bounds = bounds.ctypes.data
+                c.eval_buf, c.eval_cap = ebuf.data_ptr(), ecap
+                c.eval_rec, c.eval_wall_ms, c.eval_count = erec.ctypes.data, ewall.ctypes.data, ecount.ctypes.data
+                c.flops_cell = self.flops._a
+                c.classified_cell, c.clean_cell = self.classified_count._a, self.clean_count._a
+                keep = [ebuf, erec, ewall, ecount, bounds, parts]
             n = N.averager_run(c)
+            if keep:
+                ebuf, erec, ewall, ecount = keep[:4]
+                for i in range(int(ecount[0])):
+                    s_cur, r_, fl, classified, clean = (int(v) for v in erec[i])
+                    ph = clean / classified if classified else 1.0
+                    self.eval_points.append((s_cur, r_, float(ewall[i]), fl, ph, ebuf[i].clone()))
             for i in range(min(n, cap)):
                 r, u, s_cur, k_delta, _ = (int(v) for v in rec[i])
                 self.stamps[q].append(AveragerStamp(worker=q, round=r, u=u, s_cur=s_cur,

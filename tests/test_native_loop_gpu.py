@@ -367,3 +367,25 @@ def test_native_loop_in_flight_depths(in_flight):
         assert np.all(np.isfinite(res.losses))
     finally:
         tr.close()
+
+
+def test_native_averager_eval_points():
+    """Eval points through lpp_averager_run (engine.py:445-451): worker 0
+    keeps the round mean at every eval interval; the rows land in order,
+    past each interval, with finite losses and p_hat in [0, 1]."""
+    from paper_2203_06638_b200.engine import Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
+    tr = Trainer(_resnet_cfg(obj, budget=120, workers=2, updaters=2, eval_interval=30,
+                             evaluate=True))
+    try:
+        assert tr.eng.native_averager() and tr.eng.native_loop()
+        res = tr.run()
+    finally:
+        tr.close()
+    samples = [row.samples for row in res.metrics]
+    assert samples[0] == 0 and samples == sorted(samples) and len(res.metrics) >= 4
+    mids = res.metrics[1:-1]
+    assert all(30 * (i + 1) <= row.samples for i, row in enumerate(mids))
+    assert all(np.isfinite(row.train_loss) and 0.0 <= row.p_hat <= 1.0 for row in res.metrics)
