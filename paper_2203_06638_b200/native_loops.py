@@ -3,12 +3,14 @@
 ``lpp_updater_run`` / ``lpp_averager_run`` (``csrc/updater.cu``) run one
 updater's step loop (a10, engine.py:289-383) and one worker's averager
 (a11, engine.py:385-453) GIL-free; this mixin decides when they apply
-(the throughput configuration: no per-update records, device sampling,
-p2p averaging without eval points / quiescent pauses) and builds their
+(updaters: async, device-stream sampling, record mode off / light, with
+or without end-to-end host batches; averagers: p2p averaging without
+quiescent pauses or full records, eval points included) and builds their
 C configuration structs from the engine's arenas, streams, captured graphs
 and host counters.  The Python loops in ``async_engine`` remain the
-record / parity / host-batch paths; both drive the same kernels through the
-same C ABI, and the two averagers share one round protocol.
+reference-rng / full-record / quiescent / parity paths; both drive the
+same kernels through the same C ABI, and the two averagers share one
+round protocol.
 """
 
 from __future__ import annotations
@@ -192,7 +194,7 @@ class NativeLoops:
 
     def native_averager(self) -> bool:
         """Whether averagers run the C++ round loop (lpp_averager_run): p2p
-        averaging without quiescent pauses, eval points or full records."""
+        averaging without quiescent pauses or full records."""
         cfg = self.cfg
         return (cfg.host_loop != "python" and cfg.schedule == "async" and not cfg.quiescent
                 and not self.nvls and cfg.record_mode != "full")
