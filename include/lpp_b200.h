@@ -264,6 +264,17 @@ int lpp_sample_indices(int64_t* idx, int64_t* step, int32_t batch, int64_t n, ui
                        void* stream);
 int lpp_sample_indices_host(int64_t* out, int32_t batch, int64_t n, uint64_t key, int64_t step);
 
+/* The reference's host sampling stream in native code (csrc/nprng.cu):
+ * numpy.random.default_rng(SeedSequence(entropy)) restated bit for bit —
+ * integers(0, n, b), choice(pop, k, replace=False), permutation(m) — so the
+ * native updater loop draws exactly the reference's batches and sampled tag
+ * indices (engine.py:293, 343-351).  A handle is one generator's state. */
+int lpp_nprng_create(const uint64_t* entropy, int n, void** out);
+int lpp_nprng_destroy(void* h);
+int lpp_nprng_integers(void* h, int64_t n, int32_t b, int64_t* out);
+int lpp_nprng_choice(void* h, int64_t pop, int32_t k, int64_t* out);
+int lpp_nprng_permutation(void* h, int64_t m, int64_t* out);
+
 /* Device-side epoch-partition sampling (f4; EpochSampler, objectives.py:
  * 77-104): position step * batch + i of the stream is element
  * perm_e(pos mod shard_len) of the shard {shard_base + p * shard_stride},

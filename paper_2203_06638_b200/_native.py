@@ -180,6 +180,11 @@ _SIGS = {
     "lpp_sample_epoch_host": (_c.c_int, [_vp, _c.c_int32, _c.c_int64, _c.c_int64, _c.c_int64,
                                          _c.c_uint64, _c.c_int64]),
     "lpp_updater_run": (_c.c_int, [_c.POINTER(UpdaterCfg), _c.POINTER(UpdaterStats)]),
+    "lpp_nprng_create": (_c.c_int, [_vp, _c.c_int, _c.POINTER(_vp)]),
+    "lpp_nprng_destroy": (_c.c_int, [_vp]),
+    "lpp_nprng_integers": (_c.c_int, [_vp, _c.c_int64, _c.c_int32, _vp]),
+    "lpp_nprng_choice": (_c.c_int, [_vp, _c.c_int64, _c.c_int32, _vp]),
+    "lpp_nprng_permutation": (_c.c_int, [_vp, _c.c_int64, _vp]),
     "lpp_averager_run": (_c.c_int, [_c.POINTER(AveragerCfg), _c.POINTER(_c.c_int64)]),
     "lpp_fill_i32": (_c.c_int, [_vp, _size, _c.c_int32, _vp]),
 }
@@ -412,3 +417,33 @@ def sample_epoch_host(batch: int, base: int, stride: int, length: int, key: int,
     check(lib.lpp_sample_epoch_host(out.ctypes.data, batch, base, stride, length, key & (2**64 - 1),
                                     step), "sample_epoch_host")
     return out
+
+
+class NpRng:
+    """The reference's numpy sampling stream, restated natively (tests)."""
+
+    def __init__(self, *entropy: int):
+        ent = np.array(entropy, dtype=np.uint64)
+        h = ctypes.c_void_p()
+        check(lib.lpp_nprng_create(ent.ctypes.data, len(ent), ctypes.byref(h)), "nprng_create")
+        self._h = h
+
+    def integers(self, n: int, b: int) -> np.ndarray:
+        out = np.zeros(b, dtype=np.int64)
+        check(lib.lpp_nprng_integers(self._h, n, b, out.ctypes.data), "nprng_integers")
+        return out
+
+    def choice(self, pop: int, k: int) -> np.ndarray:
+        out = np.zeros(k, dtype=np.int64)
+        check(lib.lpp_nprng_choice(self._h, pop, k, out.ctypes.data), "nprng_choice")
+        return out
+
+    def permutation(self, m: int) -> np.ndarray:
+        out = np.zeros(m, dtype=np.int64)
+        check(lib.lpp_nprng_permutation(self._h, m, out.ctypes.data), "nprng_permutation")
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.lpp_nprng_destroy(self._h)
+            self._h = None

@@ -252,3 +252,19 @@ def test_native_loops_validate_before_touching_the_device():
     a.workers, a.q = 9, 0
     with pytest.raises(ValueError, match="worker"):
         N.averager_run(a)
+
+
+def test_native_numpy_stream_is_bit_identical_to_numpy():
+    """csrc/nprng.cu restates numpy's default_rng(SeedSequence(entropy)):
+    interleaved integers / choice(replace=False) / permutation calls give
+    numpy's exact values (the reference's batches, sampled tag indices and
+    epoch permutations, engine.py:293, 343-351, objectives.py:70-104)."""
+    for ent in ([1, 0, 1], [0, 0, 0], [12345, 3, 2], [2**40 + 7, 1, 4], [7], [99, 1007]):
+        g = np.random.default_rng(np.random.SeedSequence(ent))
+        h = N.NpRng(*ent)
+        for _ in range(3):
+            for pop, k in ((272474, 16), (11220132, 16), (5000, 16), (30, 16), (20000, 500), (10001, 300)):
+                assert np.array_equal(g.choice(pop, k, replace=False), h.choice(pop, k)), (ent, pop, k)
+            for n in (50_000, 2048, 2**40, 2**32, 1):
+                assert np.array_equal(g.integers(0, n, 64), h.integers(n, 64)), (ent, n)
+            assert np.array_equal(g.permutation(1000), h.permutation(1000))
