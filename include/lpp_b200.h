@@ -384,6 +384,21 @@ typedef struct {
   int32_t* rec_tags;              /* [rec_cap][tag_pick] or NULL */
   int64_t rec_cap;
   int64_t* rec_count;
+  /* the reference's host sampling stream (sampling="host"): every step
+   * draws, from numpy's default_rng(SeedSequence(rng_entropy)) restated in
+   * csrc/nprng.cu, first the sampled tag indices (sorted choice(n, tag_pick),
+   * when tags are sampled) and then the batch — integers(0, n_rows, batch),
+   * or with epoch_seed >= 0 the EpochSampler walk over the shard (epoch e
+   * permuted by default_rng(SeedSequence([epoch_seed, e]))) — exactly the
+   * reference updater's draws (engine.py:293-296, 343-351).  Without host
+   * batches the indices are copied into idx_dev (the captured graph gathers
+   * from the device dataset) through the pinned ring idx_pinned. */
+  int32_t host_rng;
+  int32_t n_entropy;
+  uint64_t rng_entropy[4];
+  int64_t epoch_seed;             /* < 0: i.i.d. draws */
+  int64_t* idx_pinned;            /* [in_flight + 2][batch] */
+  int64_t* idx_dev;               /* [batch] */
 } lpp_updater_cfg;
 
 typedef struct {

@@ -75,6 +75,8 @@ class UpdaterCfg(ctypes.Structure):
         ("sample_step0", _c.c_int64), ("epoch_base", _c.c_int64), ("epoch_stride", _c.c_int64),
         ("epoch_len", _c.c_int64), ("rec_i64", _vp), ("rec_lr", _vp), ("rec_tag_idx", _vp),
         ("rec_tags", _vp), ("rec_cap", _c.c_int64), ("rec_count", _vp),
+        ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
+        ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
     ]
 
 

@@ -249,6 +249,8 @@ void lpp_nprng_permutation_impl(Pcg64* g, int64_t m, int64_t* out) {
   nprng::shuffle_int(g, m, 1, out, false);
 }
 
+void lpp_nprng_free_impl(Pcg64* g) { delete g; }
+
 Pcg64* lpp_nprng_new_impl(const uint64_t* ints, int n) {
   Pcg64* g = new Pcg64();
   nprng::pcg64_seed(g, ints, n);

@@ -22,6 +22,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstring>
 #include <ctime>
 #include <thread>
 #include <vector>
@@ -171,7 +172,24 @@ extern "C" int lpp_select_block(int64_t s, int64_t warm_start, int num_blocks, i
   return rank;
 }
 
+// the reference's numpy sampling stream (csrc/nprng.cu)
+namespace nprng {
+struct Pcg64;
+}
+nprng::Pcg64* lpp_nprng_new_impl(const uint64_t* ints, int n);
+void lpp_nprng_free_impl(nprng::Pcg64* g);
+void lpp_nprng_integers_impl(nprng::Pcg64* g, int64_t n, int32_t b, int64_t* out);
+void lpp_nprng_choice_impl(nprng::Pcg64* g, int64_t pop, int32_t k, int64_t* out);
+void lpp_nprng_permutation_impl(nprng::Pcg64* g, int64_t m, int64_t* out);
+
 namespace {
+
+struct NpRngOwner {
+  nprng::Pcg64* g = nullptr;
+  ~NpRngOwner() {
+    if (g) lpp_nprng_free_impl(g);
+  }
+};
 
 struct Events {
   std::vector<cudaEvent_t> ev;
@@ -242,7 +260,45 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   if (side && (rc = order.make(2, cudaEventDisableTiming)) != LPP_OK) return rc;
   if (host && (rc = copied.make(depth, cudaEventDisableTiming)) != LPP_OK) return rc;
   if (host && (rc = buf_free.make(2, cudaEventDisableTiming)) != LPP_OK) return rc;
-  std::vector<int64_t> idx(host ? c->batch : 0);
+  std::vector<int64_t> idx((host || c->host_rng) ? c->batch : 0);
+  // the reference's host stream: one generator per updater, plus the
+  // EpochSampler's per-epoch generators (objectives.py:77-104)
+  NpRngOwner rng;
+  if (c->host_rng) {
+    if (c->n_entropy < 1 || c->n_entropy > 4 || c->batch <= 0 || c->n_rows <= 0)
+      return set_err(LPP_E_VALUE, "updater_run: host_rng needs entropy, batch and n_rows");
+    if (!host && (!c->idx_pinned || !c->idx_dev))
+      return set_err(LPP_E_VALUE, "updater_run: host_rng index ring missing");
+    rng.g = lpp_nprng_new_impl(c->rng_entropy, c->n_entropy);
+  }
+  std::vector<int64_t> ep_order, ep_perm;
+  int64_t ep_pos = 0, ep_epoch = -1;
+  auto epoch_batch = [&](int64_t* out) {
+    int got = 0;
+    while (got < c->batch) {
+      if (ep_pos >= (int64_t)ep_order.size()) {
+        ++ep_epoch;
+        const uint64_t ent[2] = {(uint64_t)c->epoch_seed, (uint64_t)ep_epoch};
+        NpRngOwner eg;
+        eg.g = lpp_nprng_new_impl(ent, 2);
+        ep_perm.resize(c->epoch_len);
+        lpp_nprng_permutation_impl(eg.g, c->epoch_len, ep_perm.data());
+        ep_order.resize(c->epoch_len);
+        for (int64_t i = 0; i < c->epoch_len; ++i)
+          ep_order[i] = c->epoch_base + ep_perm[i] * c->epoch_stride;
+        ep_pos = 0;
+      }
+      int64_t take = std::min<int64_t>(c->batch - got, (int64_t)ep_order.size() - ep_pos);
+      for (int64_t i = 0; i < take; ++i) out[got + i] = ep_order[ep_pos + i];
+      ep_pos += take;
+      got += (int)take;
+    }
+  };
+  auto draw_ref_tags = [&](int slot) {
+    int64_t* h = c->tag_idx_pinned + (size_t)slot * K;
+    lpp_nprng_choice_impl(rng.g, (int64_t)c->n, K, h);
+    std::sort(h, h + K);
+  };
   if (c->time_apply) {
     if ((rc = t0.make(F, cudaEventDefault)) != LPP_OK) return rc;
     if ((rc = t1.make(F, cudaEventDefault)) != LPP_OK) return rc;
@@ -259,7 +315,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   // before its snapshot values are read (paramstore.py:108-112)
   auto gather = [&](int slot) -> int {
     int64_t* hidx = c->tag_idx_pinned + (size_t)slot * K;
-    draw_tags(&tag_state, (int64_t)c->n, K, hidx);
+    if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, hidx);  // else drawn in step order
     int r;
     if ((r = lpp_copy_async(c->tag_idx_dev, hidx, 8 * (size_t)K, stream)) != LPP_OK) return r;
     if ((r = lpp_gather_tags(c->tags, c->tag_idx_dev, (size_t)K, c->tag_out_dev + (size_t)slot * K,
@@ -326,14 +382,31 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     const int64_t lo = c->block_lo[b], hi = c->block_hi[b], len = hi - lo;
     const float lr32 = (float)lr;
     const int buf = host ? (int)(t & 1) : 0;
+    if (c->host_rng) {
+      // the reference updater's draw order: sampled tag indices, then the
+      // batch (engine.py:343-351); fused, the next step's tag indices follow
+      if (K > 0 && (!c->fused || t == 0)) draw_ref_tags(slot);
+      if (c->epoch_seed >= 0)
+        epoch_batch(idx.data());
+      else
+        lpp_nprng_integers_impl(rng.g, c->n_rows, c->batch, idx.data());
+      if (K > 0 && c->fused) draw_ref_tags(next_slot);
+      if (!host) {
+        int64_t* hp = c->idx_pinned + (size_t)slot * c->batch;
+        std::memcpy(hp, idx.data(), sizeof(int64_t) * (size_t)c->batch);
+        if ((rc = lpp_copy_async(c->idx_dev, hp, sizeof(int64_t) * (size_t)c->batch, stream)) != LPP_OK)
+          return rc;
+      }
+    }
     if (host) {
       // end-to-end input: host draw + pinned row gather + H2D on the copy
       // stream into input buffer `buf` once the step that last read it is done
-      for (int i = 0; i < c->batch; ++i)
-        idx[i] = c->epoch_len > 0
-                     ? epoch_one(c->sample_key, c->sample_step0 + t, i, c->batch, c->epoch_base,
-                                 c->epoch_stride, (uint64_t)c->epoch_len)
-                     : sample_one(c->sample_key, c->sample_step0 + t, i, (uint64_t)c->n_rows);
+      if (!c->host_rng)
+        for (int i = 0; i < c->batch; ++i)
+          idx[i] = c->epoch_len > 0
+                       ? epoch_one(c->sample_key, c->sample_step0 + t, i, c->batch, c->epoch_base,
+                                   c->epoch_stride, (uint64_t)c->epoch_len)
+                       : sample_one(c->sample_key, c->sample_step0 + t, i, (uint64_t)c->n_rows);
       char* fdst = static_cast<char*>(c->feat_pinned) + (size_t)slot * c->batch * c->row_bytes;
       char* ldst = static_cast<char*>(c->label_pinned) + (size_t)slot * c->batch * c->label_bytes;
       if ((rc = lpp_host_gather_rows(fdst, c->host_feats, (size_t)c->n_rows, (size_t)c->row_bytes,

@@ -3,14 +3,14 @@
 ``lpp_updater_run`` / ``lpp_averager_run`` (``csrc/updater.cu``) run one
 updater's step loop (a10, engine.py:289-383) and one worker's averager
 (a11, engine.py:385-453) GIL-free; this mixin decides when they apply
-(updaters: async, device-stream sampling, record mode off / light, with
-or without end-to-end host batches; averagers: p2p averaging without
-quiescent pauses or full records, eval points included) and builds their
-C configuration structs from the engine's arenas, streams, captured graphs
-and host counters.  The Python loops in ``async_engine`` remain the
-reference-rng / full-record / quiescent / parity paths; both drive the
-same kernels through the same C ABI, and the two averagers share one
-round protocol.
+(updaters: async, record mode off / light, the in-graph device sampler
+or the reference's numpy stream restated in csrc/nprng.cu, with or without
+end-to-end host batches; averagers: p2p averaging without quiescent pauses
+or full records, eval points included) and builds their C configuration
+structs from the engine's arenas, streams, captured graphs and host
+counters.  The Python loops in ``async_engine`` remain the full-record /
+quiescent / parity paths; both drive the same kernels through the same C
+ABI, and the two averagers share one round protocol.
 """
 
 from __future__ import annotations
@@ -34,10 +34,10 @@ class NativeLoops:
         per-update records, no quiescent pauses."""
         cfg = self.cfg
         ok = (cfg.schedule == "async" and not cfg.quiescent and cfg.record_mode in ("off", "light")
-              and cfg.sampling == "device" and cfg.use_graphs)
+              and cfg.use_graphs)
         if cfg.host_loop == "native" and not ok:
             raise ValueError("host_loop='native' needs schedule='async', record_mode 'off' or "
-                             "'light', sampling='device', CUDA graphs, no quiescent pauses")
+                             "'light', CUDA graphs, no quiescent pauses")
         return ok and cfg.host_loop != "python"
 
     def apply_on_side(self) -> bool:
@@ -119,6 +119,21 @@ class NativeLoops:
         c.stream = w.streams[r].cuda_stream
         c.apply_stream = w.apply_streams[r].cuda_stream if self.side_apply else None
         keep = [lo, hi, execs, flops, ms]
+        if cfg.sampling == "host":
+            # the reference's numpy stream (engine.py:293-296), restated natively
+            c.host_rng = 1
+            c.n_entropy = 3
+            c.rng_entropy[0], c.rng_entropy[1], c.rng_entropy[2] = cfg.seed, w.q, r + 1
+            c.batch = cfg.batch_size
+            c.n_rows = cfg.objective.n_samples
+            c.epoch_seed = (cfg.seed * 1000 + w.q * 10 + r + 1) if cfg.epoch_partition else -1
+            if cfg.epoch_partition:
+                c.epoch_base, c.epoch_stride, c.epoch_len = w.epoch_shard(self)
+            if not self.host_batches:
+                c.idx_pinned = w.idx_pinned[r].data_ptr()
+                c.idx_dev = prog.idx.data_ptr()
+        else:
+            c.epoch_seed = -1
         if self.host_batches:
             obj = cfg.objective
             feats, labs = obj.features, obj.labels

@@ -552,7 +552,10 @@ def test_updater_failure_aborts_the_run(quiescent):
     from paper_2203_06638_b200.engine import run_experiment
 
     obj = _mlp("deep")[0]
-    cfg = _tiny(obj, algo="lap_sgd", budget=10_000, workers=2, updaters=2, quiescent=quiescent)
+    # the Python updater loop (the native loop's failure path is
+    # test_native_updater_failure_aborts_the_run)
+    cfg = _tiny(obj, algo="lap_sgd", budget=10_000, workers=2, updaters=2, quiescent=quiescent,
+                host_loop="python")
     orig = async_engine._Engine.step_fused if not quiescent else async_engine._Engine.step
     calls = {"n": 0}
 
@@ -663,3 +666,35 @@ def test_async_loss_band_vs_reference_async_runs():
     lo, hi = min(ref["final"]) - 0.05, max(ref["final"]) + 0.05
     print(f"\nasync band: GPU finals {np.round(finals, 4)}  reference {np.round(ref['final'], 4)}")
     assert all(lo <= f <= hi for f in finals), (finals, ref["final"])
+
+
+def test_native_updater_failure_aborts_the_run():
+    """The same contract with the native loops: one updater's failed
+    lpp_updater_run sets abort / stop, the other native updaters and the
+    native averagers (waiting on votes or fences) return, the run raises."""
+    import time as _t
+
+    from paper_2203_06638_b200 import _native, native_loops
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    cfg = _tiny(obj, algo="lap_sgd", budget=200_000, workers=2, updaters=2)
+    orig = _native.updater_run
+    calls = {"n": 0}
+
+    def boom(c):
+        calls["n"] += 1
+        if calls["n"] == 3:
+            _t.sleep(0.2)          # let the other loops get going first
+            raise ValueError("injected native updater failure")
+        return orig(c)
+
+    native_loops.N.updater_run = boom
+    try:
+        t0 = _t.perf_counter()
+        with pytest.raises(RuntimeError, match="engine thread failed") as ei:
+            run_experiment(cfg)
+        assert isinstance(ei.value.__cause__, ValueError)
+        assert _t.perf_counter() - t0 < 60
+    finally:
+        native_loops.N.updater_run = orig
