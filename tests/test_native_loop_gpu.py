@@ -427,3 +427,37 @@ def test_native_loop_reproduces_the_reference_rng_stream(fuse, epoch):
     assert [(u.s, u.block_id, u.reason, u.lr) for u in a] == [(u.s, u.block_id, u.reason, u.lr) for u in b]
     for u, v in zip(a, b):
         assert np.array_equal(u.tag_indices, v.tag_indices)
+
+
+def test_native_end_to_end_with_the_reference_stream_matches_python():
+    """End-to-end host batches drawn from the reference's numpy stream:
+    native loop (pinned gather + copy-stream H2D) and Python loop train the
+    small CNN bit for bit alike at Q = U = 1 (deterministic cuDNN)."""
+    from paper_2203_06638_b200.engine import RunConfig, Trainer
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    obj = ResNetObjective("smallcnn", n_samples=400, seed=1, data="host", channels_last=False,
+                          autocast=None)
+    cfg = RunConfig(algo="lpp_sgd", objective=obj,
+                    partition=make_partition(obj.dim, (0, obj.edges[2], obj.dim)),
+                    lr=LrSchedule(kind="cosine", alpha0=0.05, total=40, warmup=4),
+                    sync=SyncScheme(total=40, period=4), budget=40, warm_start_budget=4, workers=1,
+                    updaters=1, batch_size=24, seed=2, sampling="host", record_mode="light",
+                    evaluate=False)
+    det, bench_ = torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
+    out = {}
+    try:
+        for loop in ("native", "python"):
+            tr = Trainer(dataclasses.replace(cfg, host_loop=loop), host_batches=True, read_loss=True)
+            try:
+                assert tr.eng.native_loop() == (loop == "native")
+                out[loop] = tr.run()
+            finally:
+                tr.close()
+    finally:
+        torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = det, bench_
+    assert np.array_equal(out["native"].final_values, out["python"].final_values)
+    assert out["native"].losses == out["python"].losses
