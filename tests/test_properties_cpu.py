@@ -88,3 +88,36 @@ def test_owner_shards_cover_the_arena(dim, q):
         assert b == c and a <= b
     for lo, hi in sh[:-1]:
         assert lo % 4 == 0 and hi % 4 == 0          # 16-byte aligned shard starts
+
+
+@settings(max_examples=150, deadline=None)
+@given(st.lists(st.integers(0, 2**40), min_size=1, max_size=4), st.integers(1, 3_000_000),
+       st.integers(1, 64), st.integers(1, 40))
+def test_native_numpy_stream_random_cases(entropy, n, b, k):
+    """csrc/nprng.cu == numpy for random entropy, population and sizes
+    (the draw sequence of a reference updater: choice, then integers)."""
+    import numpy as np
+
+    from paper_2203_06638_b200 import _native as N
+
+    g = np.random.default_rng(np.random.SeedSequence(entropy))
+    h = N.NpRng(*entropy)
+    k = min(k, n)
+    assert np.array_equal(g.choice(n, k, replace=False), h.choice(n, k))
+    assert np.array_equal(g.integers(0, n, b), h.integers(n, b))
+    assert np.array_equal(g.choice(n, k, replace=False), h.choice(n, k))
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.sampled_from(["cosine", "multistep"]), st.floats(1e-4, 1.0), st.integers(1, 5000),
+       st.data())
+def test_native_lr_at_random_schedules(kind, alpha0, total, data):
+    from paper_2203_06638_b200 import _native as N
+
+    warmup = data.draw(st.integers(0, total))
+    ms = tuple(sorted(data.draw(st.lists(st.integers(0, total), max_size=4))))
+    sched = LrSchedule(kind=kind, alpha0=alpha0, total=total, warmup=warmup, milestones=ms,
+                       batch_local=data.draw(st.integers(1, 256)), workers=data.draw(st.integers(1, 8)),
+                       batch_base=data.draw(st.integers(1, 256)), boost=data.draw(st.booleans()))
+    for s in data.draw(st.lists(st.integers(0, total + 10), min_size=1, max_size=20)):
+        assert N.lr_at_native(sched, s) == lr_at(sched, s)
