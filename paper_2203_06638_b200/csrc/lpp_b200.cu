@@ -6,11 +6,20 @@
 //          (paramstore.py:121-136, _atomics.c:312-344, call site engine.py:355)
 //   K3     k_snapshot             : replica refresh,
 //          replaces ParamStore.snapshot -> snapshot_f64 (_atomics.c:186-215)
+//   K1+K3  k_apply_snapshot       : the async default — one step's apply
+//          fused with the next step's replica refresh (engine.py:343-355)
 //   K4     k_average              : owner-computes in-place model averaging,
 //          replaces _averager_body + _MeanAllReduce + add_assign(mean - snap)
-//          (engine.py:199-229, 418-421)
+//          (engine.py:199-229, 418-421); k_average_bulk: the TMA-staged
+//          variant (bulk loads on an mbarrier, bulk reductions)
+//   K5     tagged variants / k_gather_tags : write stamps and the sampled
+//          tag gather (_atomics.c:217-310, 346-392)
 //   K6     host atomics           : _atomics.{load,store,fetch_add}_i64
 //          (_atomics.c:125-183)
+//   NVLS   k_nvls_mean / k_nvls_apply : the averaging round in the switch
+//          (multimem.ld_reduce / multimem.st)
+// The native updater / averager loops and the device samplers live in
+// updater.cu, the reference's numpy sampling stream in nprng.cu.
 //
 // All of them are HBM- (or NVLink-) bound streaming kernels: 128-bit
 // vectorised, grid-stride with several independent 16-byte loads in flight
