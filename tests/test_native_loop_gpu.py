@@ -153,8 +153,8 @@ def test_native_loop_mlp_and_lap():
         tr.close()
 
 
-@pytest.mark.parametrize("tags", [True, False])
-def test_native_averager_round_protocol(tags):
+@pytest.mark.parametrize("tags,workers", [(True, 2), (False, 2), (True, 3)])
+def test_native_averager_round_protocol(tags, workers):
     """lpp_averager_run keeps the reference's averager contract
     (test_engine.py:152-235): every round is joined by every worker, rounds
     are numbered 1..n on both, the run ends on the drain round, the final
@@ -166,15 +166,16 @@ def test_native_averager_round_protocol(tags):
     from paper_2203_06638_b200.schedules import SyncScheme
 
     obj = ResNetObjective("resnet20", n_samples=1024, seed=0)
-    cfg = _resnet_cfg(obj, budget=60, workers=2, updaters=3, track_writes=tags,
+    cfg = _resnet_cfg(obj, budget=60, workers=workers, updaters=3, track_writes=tags,
                       sync=SyncScheme(total=60, period=4, switch_point=10))
     tr = Trainer(cfg)
     try:
         assert tr.eng.native_averager() and tr.eng.native_loop()
         res = tr.run()
-        per = {q: sorted(st.round for st in res.stamps if st.worker == q) for q in (0, 1)}
-        assert per[0] == per[1] == list(range(1, len(per[0]) + 1)) and len(per[0]) >= 3
-        for q in (0, 1):
+        per = {q: sorted(st.round for st in res.stamps if st.worker == q) for q in range(workers)}
+        assert all(per[q] == per[0] for q in per) and per[0] == list(range(1, len(per[0]) + 1))
+        assert len(per[0]) >= 3
+        for q in range(workers):
             arena = tr.eng.workers[q].store.arena.tensor.cpu().numpy()
             np.testing.assert_allclose(arena, res.final_values, rtol=1e-6, atol=1e-6)
             # stamps: rounds and updates draw from the same update-order counter
