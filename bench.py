@@ -261,6 +261,7 @@ def ours(args) -> None:
     images = slots * B * ws
     value = images / (dev_ms / 1e3)
     n_app, app_ms, app_bytes = res.apply_timing
+    k4_rounds, k4_ms = getattr(res, "k4_timing", (0, 0.0))
     achieved = app_bytes / (app_ms / 1e3) / 1e9
     rounds = max((st.round for st in res.stamps), default=0)
     tr.close()
@@ -374,6 +375,13 @@ def ours(args) -> None:
                 pm.close()
             del group.peers[-(ws - 1):]
             ar.close()
+        # the training run's own rounds (native averager, CUDA events around
+        # every K4 launch): ResNet-20's 1.09 MB arena, latency-bound
+        avg_us = 1e3 * k4_ms / k4_rounds if k4_rounds else 0.0
+        avg_us = max_over_ranks(avg_us)
+        avg["in_situ_resnet20"] = {
+            "rounds": k4_rounds, "avg_us": avg_us,
+            "busbw_gbs": (2 * (ws - 1) / ws * 4 * obj.dim / (avg_us * 1e-6) / 1e9) if avg_us else None}
         line["averaging"] = {"kernel": "lpp_average_shard (K4, owner-computes over peer arenas; "
                                        "red = LSU loads + red.add, bulk = TMA-staged)",
                              "unit": "GB/s", "sizes": avg,

@@ -465,6 +465,10 @@ typedef struct {
   const int64_t* flops_cell;
   const int64_t* classified_cell;
   const int64_t* clean_cell;
+  /* in-situ K4 timing (CUDA events around every round's launch) */
+  int32_t time_rounds;
+  double* k4_ms;                  /* summed */
+  int64_t* k4_rounds;             /* timed rounds */
 } lpp_averager_cfg;
 
 int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);

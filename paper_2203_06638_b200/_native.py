@@ -94,6 +94,7 @@ class AveragerCfg(ctypes.Structure):
         ("eval_interval", _c.c_int64), ("mean_parts", _vp), ("shard_bounds", _vp), ("eval_buf", _vp),
         ("eval_cap", _c.c_int64), ("eval_rec", _vp), ("eval_wall_ms", _vp), ("eval_count", _vp),
         ("flops_cell", _vp), ("classified_cell", _vp), ("clean_cell", _vp),
+        ("time_rounds", _c.c_int32), ("k4_ms", _vp), ("k4_rounds", _vp),
     ]
 
 

@@ -270,6 +270,7 @@ class _Engine(NativeLoops):
         self.native_apply = [0, 0.0, 0.0]   # launches, ms, bytes (native loop, time_apply)
         self._records: dict = {}             # native loop record buffers per (worker, updater)
         self.side_apply = False             # applies on the high-priority stream (set per run)
+        self.k4_timing = [0, 0.0]           # in-situ K4 rounds, summed ms (native averager, time_apply)
         self.native_lock = threading.Lock()
         self.t0 = 0.0
         self.budget = cfg.budget
@@ -312,6 +313,7 @@ class _Engine(NativeLoops):
         self.errors = []
         self.apply_events = []
         self.native_apply = [0, 0.0, 0.0]
+        self.k4_timing = [0, 0.0]
         self.loss_log = []
         self.eval_points = []
 

@@ -542,6 +542,22 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
   int64_t next_eval = c->eval_interval;
   if (evalm) *c->eval_count = 0;
   const bool fenced = c->tagged || evalm;
+  const bool timed = c->time_rounds && c->k4_ms && c->k4_rounds && Q > 1;
+  cudaEvent_t k4a = nullptr, k4b = nullptr;
+  struct EvPair {
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~EvPair() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } k4ev{&k4a, &k4b};
+  if (timed) {
+    CUDA_TRY(cudaEventCreate(&k4a));
+    CUDA_TRY(cudaEventCreate(&k4b));
+    *c->k4_ms = 0.0;
+    *c->k4_rounds = 0;
+  }
   auto wait_ge = [&](const int64_t* p, int64_t target) -> bool {
     return lpp_atomic_wait_ge_i64(p, target, abort_, 200) != INT64_MIN;
   };
@@ -596,15 +612,24 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
         if (rc == LPP_OK && c->tagged) rc = lpp_fill_i32(c->tags[0], c->n, stamps[0], stream);
       } else {
         float* mean = with_mean ? c->mean_out + c->lo : nullptr;
+        if (timed) cudaEventRecord(k4a, stream);
         rc = c->tagged ? lpp_average_shard_tagged(c->arenas, c->tags, stamps, Q, c->lo, c->hi, mean,
                                                   LPP_MODE_RED, stream)
                        : lpp_average_shard(c->arenas, Q, c->lo, c->hi, mean, LPP_MODE_RED, stream);
+        if (timed) cudaEventRecord(k4b, stream);
       }
       if (rc != LPP_OK) return fail(rc);
       cudaError_t e = cudaStreamSynchronize(stream);
       if (e != cudaSuccess) {
         fail(LPP_E_CUDA);
         return set_err(LPP_E_CUDA, "averager: stream sync failed: %s", cudaGetErrorString(e));
+      }
+      if (timed) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, k4a, k4b) == cudaSuccess) {
+          *c->k4_ms += ms;
+          *c->k4_rounds += 1;
+        }
       }
       if (fenced) {
         add(fence_cell(c, 1, r), 1);

@@ -133,6 +133,7 @@ class Trainer:
                         device_ms=dev_ms, apply_timing=eng.apply_timing())
         res.round_trace = getattr(eng, "round_trace", None)
         res.losses = list(eng.loss_log)
+        res.k4_timing = tuple(getattr(eng, "k4_timing", (0, 0.0)))   # (rounds, summed ms), in situ
         return res
 
     def close(self) -> None:

@@ -269,7 +269,15 @@ class NativeLoops:
                 c.flops_cell = self.flops._a
                 c.classified_cell, c.clean_cell = self.classified_count._a, self.clean_count._a
                 keep = [ebuf, erec, ewall, ecount, bounds, parts]
+            k4_ms = np.zeros(1, dtype=np.float64)
+            k4_n = np.zeros(1, dtype=np.int64)
+            if self.time_apply:
+                c.time_rounds, c.k4_ms, c.k4_rounds = 1, k4_ms.ctypes.data, k4_n.ctypes.data
             n = N.averager_run(c)
+            if self.time_apply:
+                with self.native_lock:
+                    self.k4_timing[0] += int(k4_n[0])
+                    self.k4_timing[1] += float(k4_ms[0])
             if keep:
                 ebuf, erec, ewall, ecount = keep[:4]
                 for i in range(int(ecount[0])):
