@@ -23,6 +23,17 @@ with the thread interleaving fixed:
         stop after the round in which every updater is inactive   engine.py:452-453
     final_values = m of the last round                          engine.py:507
 
+Extensions for the configuration bench.py times (B200 side):
+``mu``/``wd`` give every updater its own momentum buffer m[q][r] over the
+whole arena and apply, per element of the block, in the kernels' operation
+order (oracle/apply_ref.c ``sgd_delta``; the momentum / weight-decay
+extension point SPEC.md:382,385):  g' = g + wd*x;  m = mu*m + g';
+x += -(lr*m).  ``tag_draw=k`` reproduces record modes other than "full":
+the updater's rng first draws ``rng.choice(d, k, replace=False)`` tag
+indices, then the batch (engine.py:343-351).  ``batch_fn(q, r, t)`` replaces
+the numpy batch stream with another index stream (e.g. the device sampler
+restated in oracle/devsample.py), t = the updater's local step count.
+
 The scalar schedule helpers are restated here (not imported from the
 product package) so the checker is independent of the checked code:
 select_block (partition.py:132-145), lr_at (schedules.py:56-68),
@@ -85,6 +96,7 @@ class SerializedTrace:
     lrs: list = field(default_factory=list)         # (q, rank, s, lr)
     rounds: list = field(default_factory=list)      # (round, sweep, (C_q...))
     counter_finals: list = field(default_factory=list)
+    losses: list = field(default_factory=list)      # (q, rank, s, loss at the step's snapshot)
 
 
 class EpochSampler:
@@ -113,7 +125,8 @@ class EpochSampler:
 def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: tuple,
                    lr: Lr, switch_point: int, period: int, budget: int, warm_start: int,
                    batch_size: int, seed: int, dtype=np.float64,
-                   epoch_partition: bool = False) -> SerializedTrace:
+                   epoch_partition: bool = False, mu: float = 0.0, wd: float = 0.0,
+                   tag_draw: int = 0, batch_fn=None, record_loss: bool = False) -> SerializedTrace:
     """Run the canonical schedule; ``obj`` has init_params/grad_block(x, lo, hi, batch)."""
     if algo not in ("lap_sgd", "lpp_sgd"):
         raise ValueError("serialized schedule covers the asynchronous algorithms")
@@ -129,6 +142,8 @@ def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: t
     # engine.py:294-296: shard arange(n)[q::Q], seed seed*1000 + q*10 + rank
     samplers = [[EpochSampler(np.arange(obj.n_samples)[q::workers], seed * 1000 + q * 10 + r)
                  for r in range(1, updaters + 1)] for q in range(workers)] if epoch_partition else None
+    moms = [[np.zeros(dim, dtype=dtype) for _ in range(updaters)] for _ in range(workers)] if mu else None
+    local_t = [[0] * updaters for _ in range(workers)]
     trace = SerializedTrace(final_values=x0.copy(), xs=xs)
     sweep = 0
     mean = x0.copy()
@@ -143,11 +158,26 @@ def run_serialized(obj, *, algo: str, workers: int, updaters: int, boundaries: t
                 step_lr = lr.at(s)
                 b = select_block(s, warm_start, nblocks, rank) if algo == "lpp_sgd" else 0
                 lo, hi = (0, dim) if b == 0 else (boundaries[b - 1], boundaries[b])
-                if samplers is not None:
+                if tag_draw:
+                    gens[q][ri].choice(dim, size=min(tag_draw, dim), replace=False)
+                if batch_fn is not None:
+                    batch = batch_fn(q, ri, local_t[q][ri])
+                elif samplers is not None:
                     batch = samplers[q][ri].next_batch(batch_size)
                 else:
                     batch = gens[q][ri].integers(0, obj.n_samples, batch_size)
+                local_t[q][ri] += 1
+                if record_loss:
+                    trace.losses.append((q, rank, s, obj.loss(xs[q], batch)))
                 g = obj.grad_block(xs[q], lo, hi, batch)
+                if mu or wd:
+                    g = np.asarray(g, dtype=dtype)
+                    if wd:
+                        g = g + dtype(wd) * xs[q][lo:hi]
+                    if mu:
+                        m = moms[q][ri]
+                        m[lo:hi] = dtype(mu) * m[lo:hi] + g
+                        g = m[lo:hi]
                 if dtype == np.float32:
                     delta = np.float32(step_lr) * g.astype(np.float32)
                 else:

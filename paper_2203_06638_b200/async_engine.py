@@ -201,9 +201,20 @@ class _Worker:
         return self.q, Q, (n - self.q + Q - 1) // Q
 
     def close(self):
+        """Free every device resource now: captured graphs first, then the
+        arenas (a failed run may leave this worker in a reference cycle, and
+        a later collector pass must not free device memory mid-capture)."""
+        torch.cuda.synchronize(self.device)
+        for p in self.programs:
+            p.close()
+        self.programs = []
         extra = [self.tag_arena] if self.tag_arena is not None else []
-        for a in self.replicas + self.grads + [m for m in self.moms if m is not None] + extra:
+        for a in (self.replicas + self.grads + [m for m in self.moms if m is not None] + extra
+                  + [self.store.arena]):
             a.close()
+        if self.store.tag_arena is not None:
+            self.store.tag_arena.close()
+        self.tags = None
 
 
 class _Engine(NativeLoops):
@@ -811,7 +822,10 @@ class _Engine(NativeLoops):
             # peers may not release or reuse arenas until every owner is done
             self.group.barrier()
         if self.errors:
-            raise RuntimeError("engine thread failed") from self.errors[0]
+            # drop the engine's references to the failures before raising, so
+            # engine -> errors -> traceback -> thread frame -> engine is no cycle
+            first, self.errors = self.errors[0], []
+            raise RuntimeError("engine thread failed") from first
         return dev_ms
 
     def run_serialized(self) -> float:
@@ -948,5 +962,8 @@ class _Engine(NativeLoops):
     def close(self):
         for nv in self.nvls.values():
             nv.close()
+        self.nvls = {}
         for w in self.workers.values():
             w.close()
+        self.errors = []
+        self.apply_events = []

@@ -137,8 +137,7 @@ class Trainer:
         return res
 
     def close(self) -> None:
-        if not self.sync:
-            self.eng.close()
+        self.eng.close()
 
 
 def run_experiment(cfg: RunConfig, group=None, host_batches: bool = False) -> RunResult:

@@ -18,6 +18,8 @@ replay by the engine through the C ABI.
 
 from __future__ import annotations
 
+import gc
+
 import torch
 
 from .partition import Block
@@ -89,14 +91,25 @@ class StepProgram:
                     self._body(bid)
             stream.synchronize()
             if use_graphs:
-                pool = None
-                for bid in self.blocks:
-                    for buf in range(self.nbuf):
-                        g = torch.cuda.CUDAGraph()
-                        with torch.cuda.graph(g, pool=pool, stream=stream):
-                            self._body(bid, buf)
-                        pool = g.pool()
-                        self.graphs[(bid, buf)] = g
+                # a cyclic-GC pass during capture may finalise an earlier run's
+                # arenas or graphs (cudaFree / cudaGraphExecDestroy), which
+                # invalidates the capture; torch 2.11 no longer collects before
+                # capturing, so collect now and keep the collector off until done
+                gc.collect()
+                was_enabled = gc.isenabled()
+                gc.disable()
+                try:
+                    pool = None
+                    for bid in self.blocks:
+                        for buf in range(self.nbuf):
+                            g = torch.cuda.CUDAGraph()
+                            with torch.cuda.graph(g, pool=pool, stream=stream):
+                                self._body(bid, buf)
+                            pool = g.pool()
+                            self.graphs[(bid, buf)] = g
+                finally:
+                    if was_enabled:
+                        gc.enable()
                 stream.synchronize()
         # the batch stream starts at step 0 on the first replay (warm-up
         # draws do not count), and the native loop's host-drawn batches
@@ -151,3 +164,11 @@ class StepProgram:
         else:
             with torch.cuda.stream(self.stream):
                 self._body(bid, buf)
+
+    def close(self) -> None:
+        """Release the captured graphs now (not whenever the collector
+        reaches this object, which may be inside another capture)."""
+        self.execs = {}
+        for g in self.graphs.values():
+            g.reset()
+        self.graphs = {}

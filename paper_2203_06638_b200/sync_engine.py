@@ -110,17 +110,20 @@ class _SyncEngine:
         for q in self.local:
             self.stream[q].synchronize()
         q0 = self.local[0]
-        with torch.cuda.device(self.dev_of[q0]):
+        s0 = self.stream[q0]
+        with torch.cuda.device(self.dev_of[q0]), torch.cuda.stream(s0):
             N.average_shard([self.g[q].ptr for q in range(self.cfg.workers)], 0, self.dim,
-                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, self.stream[q0].cuda_stream)
-            self.stream[q0].synchronize()
-        ptrs = {}
-        for q in self.local:
-            if self.dev_of[q] == self.dev_of[q0]:
-                ptrs[q] = self.gmean[q0].data_ptr()
-            else:
-                self.gmean[q][: self.dim].copy_(self.gmean[q0][: self.dim])
-                ptrs[q] = self.gmean[q].data_ptr()
+                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, s0.cuda_stream)
+            ptrs = {}
+            for q in self.local:
+                if self.dev_of[q] == self.dev_of[q0]:
+                    ptrs[q] = self.gmean[q0].data_ptr()
+                else:
+                    # cross-device copy ordered after the mean on s0
+                    self.gmean[q][: self.dim].copy_(self.gmean[q0][: self.dim])
+                    ptrs[q] = self.gmean[q].data_ptr()
+        # every worker's apply (on its own stream) after the mean and the copies
+        s0.synchronize()
         return ptrs
 
     def _mean_params(self):
@@ -132,13 +135,16 @@ class _SyncEngine:
         for q in self.local:
             self.stream[q].synchronize()
         q0 = self.local[0]
-        with torch.cuda.device(self.dev_of[q0]):
-            # x_q = mean exactly (xs[:] = mean, engine.py:612): write the mean, then copy
+        s0 = self.stream[q0]
+        with torch.cuda.device(self.dev_of[q0]), torch.cuda.stream(s0):
+            # x_q = mean exactly (xs[:] = mean, engine.py:612): write the mean,
+            # then copy it into every arena, all on s0 (ordered after the mean)
             N.average_shard([self.x[q].ptr for q in range(self.cfg.workers)], 0, self.dim,
-                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, self.stream[q0].cuda_stream)
+                            self.gmean[q0].data_ptr(), N.MODE_PLAIN, s0.cuda_stream)
             for q in self.local:
                 self.x[q].tensor.copy_(self.gmean[q0][: self.dim])
-            self.stream[q0].synchronize()
+        # the next _grads on every stream[q] reads x[q]: finish the copies first
+        s0.synchronize()
 
     def run(self, steps: int | None = None) -> float:
         cfg = self.cfg
@@ -194,3 +200,12 @@ class _SyncEngine:
 
     def final_values(self) -> np.ndarray:
         return self.x[self.local[0]].tensor.cpu().numpy()
+
+    def close(self) -> None:
+        """Free graphs and arenas now (see ``_Worker.close``)."""
+        torch.cuda.synchronize()
+        for p in self.prog.values():
+            p.close()
+        self.prog = {}
+        for a in [*self.x.values(), *self.g.values(), *self.m.values()]:
+            a.close()

@@ -1,0 +1,180 @@
+"""Parity of the exact configuration bench.py times, against the oracle.
+
+bench.py's headline run is: LPP-SGD, the native C++ updater loop
+(``lpp_updater_run``), the fused K1+K3 apply-and-snapshot kernel on the
+high-priority apply stream, momentum 0.9 / weight decay 5e-4, K5 write tags,
+the in-graph device sampler, and (for ``e2e``) host batches with an H2D copy
+and a loss read-back every step.  At Q = U = 1 that pipeline is
+deterministic (one stream; the next step's snapshot is taken when this
+step's apply lands — engine.py:336-362 in order; averaging a single worker
+is the identity, test_engine.py:169-182), so its parameters must follow the
+serialized oracle (oracle/schedule.py with per-updater momentum in the
+kernels' operation order, oracle/apply_ref.c ``sgd_delta``) driven by the
+device sampler's batch stream restated in oracle/devsample.py.
+
+Tolerance (fp32 engine vs fp64 oracle, TF32 off): the SURVEY §8c contract
+``atol 1e-5, rtol 1e-4`` for the reference MLP (C0) and the small CNN;
+ResNet-20 (BatchNorm, ReLU kinks, 272k parameters) ``atol 1e-4, rtol 1e-3``
+over 25 steps.  Block ids and learning rates are exact.
+
+The file name sorts before test_engine_gpu.py so a later failure cannot
+hide it under ``pytest -x``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+MU, WD = 0.9, 5e-4
+
+
+@pytest.fixture(autouse=True)
+def _no_tf32():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+
+
+def _cfg(obj, bounds, budget, B, record_mode="off", alpha0=0.1, **over):
+    """bench.build_cfg at Q = U = 1 (same schedule shapes, smaller budget)."""
+    from paper_2203_06638_b200.engine import RunConfig
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    kw = dict(algo="lpp_sgd", objective=obj, partition=make_partition(obj.dim, bounds),
+              lr=LrSchedule(kind="cosine", alpha0=alpha0, total=budget, warmup=max(budget // 10, 1),
+                            batch_local=B, workers=1, batch_base=B, boost=True),
+              sync=SyncScheme(total=budget, period=16), budget=budget,
+              warm_start_budget=max(budget // 10, 1), workers=1, updaters=1, batch_size=B, seed=0,
+              momentum=MU, weight_decay=WD, sampling="device", evaluate=False,
+              record_mode=record_mode, host_loop="native")
+    kw.update(over)
+    return RunConfig(**kw)
+
+
+def _oracle(orc, cfg, bounds, record_loss=False):
+    from oracle import devsample
+    from oracle import schedule as osched
+
+    n, B, seed = orc.n_samples, cfg.batch_size, cfg.seed
+    s = cfg.lr
+    return osched.run_serialized(
+        orc, algo="lpp_sgd", workers=1, updaters=1, boundaries=tuple(bounds),
+        lr=osched.Lr(kind="cosine", alpha0=s.alpha0, total=s.total, warmup=s.warmup, peak=s.peak),
+        switch_point=cfg.sync.switch_point, period=cfg.sync.period, budget=cfg.budget,
+        warm_start=cfg.warm_start_budget, batch_size=B, seed=seed, mu=MU, wd=WD,
+        batch_fn=lambda q, r, t: devsample.iid_batch(devsample.engine_key(seed, q, r), t, B, n),
+        record_loss=record_loss)
+
+
+def _check_trainer_flags(tr):
+    eng = tr.eng
+    assert eng.native_loop(), "bench config must run the native updater loop"
+    assert eng.fused(), "bench config must run the fused K1+K3 kernel"
+    assert eng.apply_on_side(), "bench config applies on the high-priority stream"
+    assert eng.cfg.tracks, "bench config keeps K5 write tags"
+
+
+def _run(cfg, host_batches=False, read_loss=False):
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200.engine import Trainer
+
+    tr = Trainer(cfg, host_batches=host_batches, read_loss=read_loss)
+    try:
+        _check_trainer_flags(tr)
+        l0 = N.launch_count()
+        res = tr.run()
+        assert N.launch_count() - l0 >= cfg.budget   # our kernels ran: >= one apply per step
+        return res
+    finally:
+        tr.close()
+
+
+def _c0():
+    from oracle import data as odata
+    from oracle.mlp import MlpOracle
+    from paper_2203_06638_b200.objectives import MlpObjective
+
+    X, y = odata.cifar_blobs()
+    obj = MlpObjective(X, y, (64,), 10)
+    orc = MlpOracle(X, y, (64,), 10)
+    bounds = (0, obj.edges[2], obj.dim)        # balanced_boundaries of C0: (0, 196672, 197322)
+    return obj, orc, bounds
+
+
+@pytest.mark.parametrize("record_mode", ["off", "light"])
+def test_bench_pipeline_matches_oracle_c0_mlp(record_mode):
+    obj, orc, bounds = _c0()
+    cfg = _cfg(obj, bounds, budget=160, B=32, record_mode=record_mode, alpha0=0.05)
+    res = _run(cfg)
+    tr = _oracle(orc, cfg, bounds)
+    assert res.counter_finals == tr.counter_finals == [161]
+    err = float(np.max(np.abs(res.final_values - tr.final_values)))
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-5, rtol=1e-4,
+                               err_msg=f"max |dx| = {err:.3e}")
+    # the run actually moved the model (momentum + wd + partial blocks)
+    assert np.max(np.abs(tr.final_values - res.x0)) > 1e-2
+    if record_mode == "light":
+        got = sorted((u.worker, u.rank, u.s, u.block_id) for u in res.updates)
+        assert got == sorted(tr.block_ids)
+        lrs = {(u.worker, u.rank, u.s): u.lr for u in res.updates}
+        assert all(lrs[(q, r, s)] == lr for q, r, s, lr in tr.lrs)
+        # Q = 1: every update is clean (no other worker's round can land)
+        assert res.p_hat == 1.0
+        assert all(u.clean for u in res.updates)
+
+
+def test_bench_e2e_pipeline_matches_oracle_c0_mlp():
+    """The e2e leg: host batches (the device sampler's stream drawn on the
+    host, pinned gather, H2D per step) and the loss read back per step."""
+    obj, orc, bounds = _c0()
+    cfg = _cfg(obj, bounds, budget=120, B=32, alpha0=0.05)
+    res = _run(cfg, host_batches=True, read_loss=True)
+    tr = _oracle(orc, cfg, bounds, record_loss=True)
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-5, rtol=1e-4)
+    want = [l for *_, l in sorted(tr.losses)]
+    assert len(res.losses) == len(want)
+    np.testing.assert_allclose(res.losses, want, atol=1e-5, rtol=1e-4)
+
+
+def test_bench_pipeline_matches_oracle_small_cnn():
+    from oracle.cnn import SmallCnnOracle
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("smallcnn", n_samples=512, seed=3, channels_last=False, autocast=None,
+                          data="host")
+    orc = SmallCnnOracle(obj.features.double().numpy(), obj.labels.numpy())
+    e = orc.edges
+    bounds = (0, e[2], e[6])                   # 2 blocks: conv1 | conv2 + fc
+    cfg = _cfg(obj, bounds, budget=100, B=32, alpha0=0.05)
+    res = _run(cfg)
+    tr = _oracle(orc, cfg, bounds)
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-5, rtol=1e-4)
+
+
+def test_bench_pipeline_matches_oracle_resnet20_fp32():
+    """The bench's own network (ResNet-20, channels-last arena layout, fp32
+    compute — the headline precision) through the bench pipeline, 4 blocks
+    from balanced_boundaries as in bench.py, vs the fp64 functional oracle."""
+    from oracle.resnet import ResNet20Oracle
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.partition import balanced_boundaries
+
+    obj = ResNetObjective("resnet20", n_samples=1024, seed=0, autocast=None, channels_last=True,
+                          data="device")
+    bounds = balanced_boundaries(obj.layer_param_counts, 4)
+    cfg = _cfg(obj, bounds, budget=24, B=32, alpha0=0.05)
+    res = _run(cfg)
+    feats = obj.features_on(torch.device("cuda", 0)).double().cpu().numpy()
+    orc = ResNet20Oracle(feats, obj.labels.numpy(), res.x0, channels_last=True)
+    assert orc.dim == obj.dim
+    tr = _oracle(orc, cfg, bounds)
+    err = float(np.max(np.abs(res.final_values - tr.final_values)))
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-4, rtol=1e-3,
+                               err_msg=f"max |dx| = {err:.3e}")
+    assert np.max(np.abs(tr.final_values - res.x0)) > 1e-3

@@ -577,6 +577,43 @@ def test_updater_failure_aborts_the_run(quiescent):
         setattr(async_engine._Engine, name, orig)
 
 
+def test_failed_run_then_capture_with_aggressive_gc():
+    """Regression (round-1 driver failure): a failed async run leaves its
+    engine as cyclic garbage; a collector pass during the next run's graph
+    capture must not free device memory or graphs mid-capture.  GC is forced
+    to run as often as possible while the second engine captures."""
+    import gc
+
+    from paper_2203_06638_b200 import async_engine
+    from paper_2203_06638_b200.engine import run_experiment
+
+    obj = _mlp("deep")[0]
+    orig = async_engine._Engine.step_fused
+    calls = {"n": 0}
+
+    def boom(self, *a, **k):
+        calls["n"] += 1
+        if calls["n"] == 5:
+            raise ValueError("injected updater failure")
+        return orig(self, *a, **k)
+
+    old = gc.get_threshold()
+    async_engine._Engine.step_fused = boom
+    try:
+        for _ in range(3):
+            calls["n"] = 0
+            with pytest.raises(RuntimeError, match="engine thread failed"):
+                run_experiment(_tiny(obj, algo="lap_sgd", budget=200, workers=2, updaters=2,
+                                     host_loop="python"))
+        async_engine._Engine.step_fused = orig
+        gc.set_threshold(1, 1, 1)
+        res = run_experiment(_tiny(obj, algo="lap_sgd", budget=40, workers=2, updaters=2))
+        assert np.all(np.isfinite(res.final_values))
+    finally:
+        async_engine._Engine.step_fused = orig
+        gc.set_threshold(*old)
+
+
 @pytest.mark.parametrize("name", ["quad8_lpp", "logreg8_lap"])
 def test_serialized_flat_objectives_match_oracle(name):
     """The reference's desk-scale objectives on the GPU engine; quad8 uses the

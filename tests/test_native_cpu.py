@@ -202,6 +202,17 @@ def test_device_sampler_host_twin():
     assert counts.min() > 9_500 and counts.max() < 10_500
 
 
+def test_device_sampler_matches_oracle_restatement():
+    """oracle/devsample.py (the checker's independent restatement of the
+    device sampler) equals the C ABI's host twin bit for bit."""
+    from oracle import devsample
+
+    for key, step, b, n in [(42, 0, 100, 5000), (7, 123, 64, 50_000), (2**63 + 5, 9, 33, 10),
+                            (devsample.engine_key(0, 0, 0), 0, 128, 50_000),
+                            (devsample.engine_key(3, 1, 2), 77, 32, 2048)]:
+        assert np.array_equal(devsample.iid_batch(key, step, b, n), N.sample_indices_host(b, n, key, step))
+
+
 def test_host_gather_rows_and_range_check():
     src = np.arange(40, dtype=np.float32).reshape(10, 4)
     dst = np.zeros((3, 4), dtype=np.float32)
