@@ -239,50 +239,65 @@ def ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- device-resident throughput (value) ----------------
-    obj = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data="device")
-    cfg = build_cfg(obj, (K + W) * U, workers=ws)
-    tr = Trainer(cfg, group=group, time_apply=True)
-    fused = tr.eng.fused()
-    tr_native = tr.eng.native_loop()
-    tr.run(W * U, evaluate=False)
-    barrier()
-    if os.environ.get("LPP_NVTX"):
-        tr.eng.nvtx = "lpp_timed"   # ncu --nvtx --nvtx-include lpp_timed/ profiles this phase only
-    with Clocks(dev) as clk:
+    # the headline runs at the reference arm's precision: fp32 convolutions
+    # with TF32 off; the bf16 variant is reported beside it
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def lpp_phase(autocast, data="device", host_batches=False, time_apply=False):
+        """W warm-up then K timed steps of LPP-SGD ResNet-20 through Trainer;
+        returns (images/s, result, trainer facts, launches in the timed phase)."""
+        o = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data=data, autocast=autocast)
+        c = build_cfg(o, (K + W) * U, workers=ws)
+        t = Trainer(c, group=group, host_batches=host_batches, read_loss=host_batches,
+                    time_apply=time_apply)
+        facts = {"fused": t.eng.fused(), "native": t.eng.native_loop(), "tracks": c.tracks,
+                 "dim": o.dim}
+        t.run(W * U, evaluate=False)
         barrier()
-        l0 = N.launch_count()
-        res = tr.run(K * U, evaluate=False)
-        launches = N.launch_count() - l0
-        barrier()
-    tr.eng.nvtx = None
-    dev_ms = max_over_ranks(res.device_ms)
-    slots = sum(res.counter_finals)  # claim-then-process: K*U + U minibatches
-    images = slots * B * ws
-    value = images / (dev_ms / 1e3)
+        if os.environ.get("LPP_NVTX") and not host_batches and autocast is None:
+            t.eng.nvtx = "lpp_timed"   # ncu --nvtx --nvtx-include lpp_timed/ profiles this phase only
+        with Clocks(dev) as clk:
+            barrier()
+            l0 = N.launch_count()
+            r = t.run(K * U, evaluate=False)
+            n_l = N.launch_count() - l0
+            barrier()
+        t.eng.nvtx = None
+        ms = max_over_ranks(r.device_ms)
+        v = sum(r.counter_finals) * B * ws / (ms / 1e3)   # claim-then-process: K*U + U per rank
+        facts["clocks"] = clk.summary()
+        t.close()
+        del t
+        return v, r, facts, n_l, ms
+
+    # ---------------- device-resident throughput (value), fp32 ----------------
+    value, res, facts, launches, dev_ms = lpp_phase(None, time_apply=True)
+    fused, tr_native, dim20 = facts["fused"], facts["native"], facts["dim"]
     n_app, app_ms, app_bytes = res.apply_timing
     k4_rounds, k4_ms = getattr(res, "k4_timing", (0, 0.0))
     achieved = app_bytes / (app_ms / 1e3) / 1e9
     rounds = max((st.round for st in res.stamps), default=0)
-    tr.close()
-    del tr
 
     # traffic: DRAM bytes per launch of the same kernel at the ResNet-20 arena
     # size from the committed ncu --set full capture (profiles/)
     traffic = None
     standalone = None
-    tp = ROOT / "profiles" / "r1_kernel_traffic.json"
+    tp = ROOT / "profiles" / "r2_kernel_traffic.json"
+    if not tp.exists():
+        tp = ROOT / "profiles" / "r1_kernel_traffic.json"
     if tp.exists():
         launches_ = json.loads(tp.read_text())["launches"]
-        name = "void k_apply_snapshot<1, 1" if fused else "void k_apply<1, 1, 1>"
-        cands = [e for e in launches_ if e["kernel"].startswith(name) and e["grid"] == 267]
+        name = "void k_apply_snapshot<" if fused else "void k_apply<1, 1, 1>"
+        cands = [e for e in launches_ if e["kernel"].startswith(name) and e.get("params", dim20) == dim20]
         traffic = sum(e["dram_bytes"] for e in cands) / len(cands) if cands else None
         floor = [e["us"] for e in launches_ if e["kernel"] == "k_gather_tags"]
         if cands:
             us = sum(e["us"] for e in cands) / len(cands)
             standalone = {"us": us, "latency_floor_us": min(floor) if floor else None,
-                          "src": "ncu gpu__time_duration of the same kernel at d20 launched alone "
-                                 "(cold L2); latency_floor_us = a 16-element gather kernel"}
+                          "src": f"{tp.relative_to(ROOT)}: ncu gpu__time_duration of the same kernel "
+                                 "at d20 launched alone (cold L2); latency_floor_us = a 16-element "
+                                 "gather kernel"}
     line = {
         "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": ws,
         "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,
@@ -290,151 +305,191 @@ def ours(args) -> None:
         "data": "synthetic (N(0,1) CIFAR-10-shaped images, uniform labels; random init)",
         "config": {"workload": "resnet20_cifar10_lpp_sgd", "model": "resnet20", "global_batch": B * U * ws,
                    "batch_per_updater": B, "updaters_per_gpu": U, "workers": ws, "blocks": U,
-                   "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": obj.dim,
-                   "conv_compute": "bf16 (weights cast once per step from the fp32 replica; arena, grads, apply, averaging in fp32)",
-                   "l2": "inputs larger than L2 (50,000-image dataset, 307 MB as NHWC bf16, gathered per step)",
+                   "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": dim20,
+                   "conv_compute": "fp32 (TF32 off), the reference arm's precision; arena, grads, "
+                                   "apply and averaging fp32",
+                   "l2": "inputs larger than L2 (50,000-image dataset, 614 MB fp32, gathered per step)",
                    "sampling": "in-graph device RNG", "host_loop": "native" if tr_native else "python",
                    "momentum": 0.9, "weight_decay": 5e-4,
-                   "write_tags": cfg.tracks},
+                   "write_tags": facts["tracks"], "averaging_rounds": rounds},
         "gpu_launches": launches,
         "gpu_launches_note": "lpp_b200 kernels launched in the timed region on this rank "
-                             "(K3 snapshot + K5 tag gather + K1/K2 apply per minibatch, + K4 per round)",
+                             "(fused K1+K3 apply + K5 tag gather + in-graph sampler per minibatch, "
+                             "+ K4 per round)",
         "roofline": {"bound": "hbm",
                      "kernel": ("lpp_apply_snapshot (K1+K3 fused, red.add.v4.f32 + re-read)" if fused else
                                 "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)"),
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],
                      "traffic": traffic,
-                     "traffic_src": "profiles/r1_kernel_traffic.json (ncu --set full, d20, cold L2)",
+                     "traffic_src": "ncu --set full, d20, cold L2 (profiles/)",
                      "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
                      "bytes_per_launch": app_bytes / max(n_app, 1),
                      "standalone": standalone,
-                     "note": "d20 arena (1.09 MB) is L2-resident: latency-bound; see kernel_sweep"},
+                     "note": "d20 arena (1.09 MB) is L2-resident: latency-bound; see kernel_sweep, "
+                             "resnet18 / resnet50 apply_roofline for the HBM-sized arenas"},
     }
+    line["clocks"] = facts["clocks"]
 
-    # ---------------- clocks ----------------
-    line["clocks"] = clk.summary()
-
-    # ---------------- end to end (host buffers) ----------------
+    # ---------------- end to end (host buffers), fp32 ----------------
     if not args.no_e2e:
-        hobj = ResNetObjective("resnet20", n_samples=N_SAMPLES if ws == 1 else N_SAMPLES, seed=0, data="host")
-        # host-drawn batches (the device sampler's stream), pinned row gather, H2D
-        # every step, loss D2H every step — inside the native updater loop
-        hcfg = build_cfg(hobj, (K + W) * U, workers=ws, sampling="device")
-        htr = Trainer(hcfg, group=group, host_batches=True, read_loss=True)
-        htr.run(W * U, evaluate=False)
-        barrier()
-        hres = htr.run(K * U, evaluate=False)
-        barrier()
-        e_ms = max_over_ranks(hres.device_ms)
-        hslots = sum(hres.counter_finals)
-        e2e = hslots * B * ws / (e_ms / 1e3)
+        # host-drawn batches (the device sampler's stream), pinned row gather,
+        # H2D every step, loss D2H every step — inside the native updater loop
+        e2e, hres, hfacts, _, _ = lpp_phase(None, data="host", host_batches=True)
         per_img = 3 * 32 * 32 * 4 + 8
         line["e2e"] = {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": U * B * per_img,
                        "d2h_bytes_per_step": U * 4, "api": "Trainer(cfg, host_batches=True, read_loss=True).run",
-                       "host_loop": "native" if htr.eng.native_loop() else "python",
+                       "host_loop": "native" if hfacts["native"] else "python",
                        "losses_read": len(hres.losses),
                        "last_loss": hres.losses[-1] if hres.losses else None}
-        htr.close()
-        del htr
+
+    # ---------------- the same two measurements with bf16 convolutions ----------------
+    if not args.no_bf16:
+        with _Optional(line, "bf16"):
+            vb, _, fb, _, _ = lpp_phase("bf16")
+            line["value_bf16"] = vb
+            line["bf16"] = {"conv_compute": "bf16 shadow weights (one cast per step from the fp32 "
+                                            "replica), dataset stored NHWC bf16; arena, grads, apply, "
+                                            "averaging fp32", "clocks": fb["clocks"]}
+            if not args.no_e2e:
+                eb, _, _, _, _ = lpp_phase("bf16", data="host", host_batches=True)
+                line["e2e_bf16"] = {"value": eb, "unit": "images/s",
+                                    "h2d_bytes_per_step": U * B * (3 * 32 * 32 * 4 + 8),
+                                    "d2h_bytes_per_step": U * 4}
 
     # ---------------- averaging bandwidth across the group (N > 1) ----------------
     # BASELINE.json's second metric: K4 over the P2P/NVLink-mapped arenas of
     # all ranks, each rank averaging its owned shard of a d-element group;
-    # busbw = 2(Q-1)/Q x 4d bytes per GPU and direction / max-over-ranks time
+    # busbw = 2(Q-1)/Q x 4d bytes per GPU and direction / max-over-ranks time.
+    # The denominators: NVLink 5's 900 GB/s per direction (nominal) and a peer
+    # copy measured here in the same run (cudaMemcpyPeer-class read of the
+    # next rank's arena into local HBM, 256 MB)
     if ws > 1 and not args.no_sweep:
         from paper_2203_06638_b200.arena import Arena
         from paper_2203_06638_b200.engine import shard_bounds
 
         avg = {}
+        peer_gbs = None
         for d in (16_000_000, 64_000_000):
             ar = Arena(d, dev)
             ar.tensor.normal_()
             ptrs = group.attach_arenas(ar)
             lo, hi = shard_bounds(d, ws)[rank]
             st = torch.cuda.current_stream().cuda_stream
+            if d == 64_000_000:
+                # peer copy: this rank pulls its right neighbour's whole arena
+                dst = torch.empty(d, dtype=torch.float32, device="cuda")
+                src = ptrs[(rank + 1) % ws]
+                for _ in range(3):
+                    N.copy_async(dst.data_ptr(), src, 4 * d, st)
+                ts = []
+                for _ in range(5):
+                    barrier()
+                    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a_.record()
+                    N.copy_async(dst.data_ptr(), src, 4 * d, st)
+                    b_.record()
+                    b_.synchronize()
+                    ts.append(max_over_ranks(a_.elapsed_time(b_)))
+                peer_gbs = 4 * d / (sorted(ts)[len(ts) // 2] / 1e3) / 1e9
+                del dst
             for mode_name, mode in (("red", N.MODE_RED), ("bulk", N.MODE_BULK)):
                 for _ in range(3):
                     N.average_shard(ptrs, lo, hi, None, mode, st)
                 ts = []
                 for _ in range(10):
                     barrier()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record()
+                    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a_.record()
                     N.average_shard(ptrs, lo, hi, None, mode, st)
-                    b.record()
-                    b.synchronize()
-                    ts.append(max_over_ranks(a.elapsed_time(b)))
+                    b_.record()
+                    b_.synchronize()
+                    ts.append(max_over_ranks(a_.elapsed_time(b_)))
                 t = sorted(ts)[len(ts) // 2] / 1e3
                 busbw = 2 * (ws - 1) / ws * 4 * d / t / 1e9
-                avg.setdefault(str(d), {})[mode_name] = {
-                    "us": t * 1e6, "busbw_gbs": busbw, "frac_of_770": busbw / 770.0,
-                    "frac_of_900": busbw / 900.0}
+                avg.setdefault(str(d), {})[mode_name] = {"us": t * 1e6, "busbw_gbs": busbw,
+                                                         "frac_of_900": busbw / 900.0}
             barrier()
             for pm in group.peers[-(ws - 1):]:
                 pm.close()
             del group.peers[-(ws - 1):]
             ar.close()
+        if peer_gbs:
+            for per in avg.values():
+                for v in per.values():
+                    v["frac_of_peer_copy"] = v["busbw_gbs"] / peer_gbs
         # the training run's own rounds (native averager, CUDA events around
         # every K4 launch): ResNet-20's 1.09 MB arena, latency-bound
         avg_us = 1e3 * k4_ms / k4_rounds if k4_rounds else 0.0
         avg_us = max_over_ranks(avg_us)
         avg["in_situ_resnet20"] = {
             "rounds": k4_rounds, "avg_us": avg_us,
-            "busbw_gbs": (2 * (ws - 1) / ws * 4 * obj.dim / (avg_us * 1e-6) / 1e9) if avg_us else None}
+            "busbw_gbs": (2 * (ws - 1) / ws * 4 * dim20 / (avg_us * 1e-6) / 1e9) if avg_us else None}
         line["averaging"] = {"kernel": "lpp_average_shard (K4, owner-computes over peer arenas; "
                                        "red = LSU loads + red.add, bulk = TMA-staged)",
-                             "unit": "GB/s", "sizes": avg,
+                             "unit": "GB/s", "sizes": avg, "peer_copy_gbs": peer_gbs,
                              "ranks_share_device": torch.cuda.device_count() < ws,
                              "note": "busbw = 2(Q-1)/Q x 4d per GPU per direction (nccl-tests convention); "
-                                     "770 GB/s = measured peer copy, 900 = NVLink 5 nominal"}
+                                     "900 = NVLink 5 nominal per direction; peer_copy_gbs = a 256 MB "
+                                     "read of the next rank's arena measured in this run"}
 
-    # ---------------- baselines on the same box: MB-SGD and LAP-SGD ----------------
-    if not args.no_baselines and ws == 1:
+    # ---------------- synchronous baselines on the same box, at the same N ----------------
+    # B1 NCCL MB-SGD (engine.py:544-583) and B2 NCCL L-SGD / PL-SGD (period 16
+    # after T/2, engine.py:586-629), same fp32 ResNet-20, same per-GPU batch;
+    # MB-SGD also at B = U x 128 per GPU (as many images per step as the U
+    # LPP updaters); LAP-SGD = the async engine without partial backprop
+    if not args.no_baselines:
         with _Optional(line, "baselines"):
-            mcfg = build_cfg(obj, (K + W) * U, algo="mb_sgd", workers=1)
-            mtr = Trainer(mcfg)
-            mtr.run(W * U, evaluate=False)
-            torch.cuda.synchronize()
-            mres = mtr.run(K * U, evaluate=False)
-            mb = K * U * B / (mres.device_ms / 1e3)
-            del mtr
-            lcfg = build_cfg(obj, (K + W) * U, algo="lap_sgd", workers=1)
-            ltr = Trainer(lcfg)
-            ltr.run(W * U, evaluate=False)
-            torch.cuda.synchronize()
-            lres = ltr.run(K * U, evaluate=False)
-            lap = sum(lres.counter_finals) * B / (lres.device_ms / 1e3)
-            ltr.close()
-            del ltr
-            line["baselines"] = {
-                "mb_sgd": {"value": mb, "unit": "images/s", "batch": B, "streams": 1,
-                           "note": "synchronous SGD, same per-GPU batch, CUDA graphs"},
-                "lap_sgd": {"value": lap, "unit": "images/s", "streams": U,
-                            "note": "same engine, full backprop every step (no PASSM+ blocks)"},
-                "lpp_over_mb": value / mb, "lpp_over_lap": value / lap}
+            bobj = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data="device", autocast=None)
 
-    # ---------------- MB-SGD at the same images per step as LPP (B = U x 128) ----------------
-    # the paper's "MB-SGD B=1024" rows: one big synchronous batch per step
-    # (bigger kernels, fewer updates); reported beside, not the headline ratio
-    if not args.no_baselines and ws == 1:
-        with _Optional(line, "mb_sgd_large_batch"):
-            bl = B * U
-            mcfg = dataclasses.replace(build_cfg(obj, (K + W), algo="mb_sgd", workers=1), batch_size=bl)
-            mtr = Trainer(mcfg)
-            mtr.run(W, evaluate=False)
-            torch.cuda.synchronize()
-            mres = mtr.run(K, evaluate=False)
-            line["baselines"]["mb_sgd_b%d" % bl] = {
-                "value": K * bl / (mres.device_ms / 1e3), "unit": "images/s", "batch": bl, "streams": 1,
-                "note": "synchronous SGD, one batch of U x 128 per step (as many images per step as "
-                        "the U LPP updaters together, U x fewer model updates)"}
-            del mtr
+            def sync_rate(algo, batch, steps, warm):
+                c = dataclasses.replace(build_cfg(bobj, steps + warm, algo=algo, workers=ws),
+                                        batch_size=batch)
+                t = Trainer(c, group=group)
+                t.run(warm, evaluate=False)
+                barrier()
+                r = t.run(steps, evaluate=False)
+                ms = max_over_ranks(r.device_ms)
+                t.close()
+                return steps * batch * ws / (ms / 1e3)
+
+            base = {}
+            coll = "NCCL all-reduce" if ws > 1 else "none (one worker)"
+            mb = sync_rate("mb_sgd", B, K * U, W * U)
+            base["mb_sgd"] = {"value": mb, "unit": "images/s", "batch_per_gpu": B, "streams": 1,
+                              "collective": coll, "note": "B1: synchronous SGD, same per-GPU batch"}
+            mbl = sync_rate("mb_sgd", B * U, K, W)
+            base[f"mb_sgd_b{B * U}"] = {"value": mbl, "unit": "images/s", "batch_per_gpu": B * U,
+                                        "streams": 1, "collective": coll,
+                                        "note": "B1 at U x 128 per GPU: the images per step of the U "
+                                                "LPP updaters together, U x fewer model updates"}
+            pl = sync_rate("pl_sgd", B, K * U, W * U)
+            base["pl_sgd"] = {"value": pl, "unit": "images/s", "batch_per_gpu": B, "streams": 1,
+                              "collective": coll,
+                              "note": "B2: local SGD, parameter average every step until T/2, then "
+                                      "every 16 steps"}
+            if ws == 1:
+                lcfg = build_cfg(bobj, (K + W) * U, algo="lap_sgd", workers=1)
+                ltr = Trainer(lcfg)
+                ltr.run(W * U, evaluate=False)
+                torch.cuda.synchronize()
+                lres = ltr.run(K * U, evaluate=False)
+                base["lap_sgd"] = {"value": sum(lres.counter_finals) * B / (lres.device_ms / 1e3),
+                                   "unit": "images/s", "streams": U,
+                                   "note": "same engine, full backprop every step (no PASSM+ blocks)"}
+                ltr.close()
+                del ltr
+            base["lpp_over_mb"] = value / mb
+            base[f"lpp_over_mb_b{B * U}"] = value / mbl
+            base["lpp_over_pl"] = value / pl
+            base["dtype"] = "f32"
+            line["baselines"] = base
 
     # ---------------- the paper's U = 6 variant ----------------
     if not args.no_baselines and ws == 1:
         with _Optional(line, "lpp_sgd_u6"):
-            c6 = build_cfg(obj, (K + W) * 6, workers=1, updaters=6)
+            o6 = ResNetObjective("resnet20", n_samples=N_SAMPLES, seed=0, data="device", autocast=None)
+            c6 = build_cfg(o6, (K + W) * 6, workers=1, updaters=6)
             t6 = Trainer(c6)
             t6.run(W * 6, evaluate=False)
             torch.cuda.synchronize()
@@ -449,14 +504,17 @@ def ours(args) -> None:
     if not args.no_rn18 and ws == 1:
         with _Optional(line, "resnet18"):
             obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
-            out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s"}
-            for algo in ("lpp_sgd", "mb_sgd"):
+            out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s",
+                     "conv_compute": "bf16 shadow weights (all three rows)"}
+            for algo in ("lpp_sgd", "mb_sgd", "pl_sgd"):
                 c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=1)
                 t18 = Trainer(c18, time_apply=(algo == "lpp_sgd"))
                 t18.run(3 * U, evaluate=False)
                 torch.cuda.synchronize()
                 r18 = t18.run(args.rn18_steps * U, evaluate=False)
                 n18 = sum(r18.counter_finals) if algo == "lpp_sgd" else args.rn18_steps * U
+                if algo != "lpp_sgd":
+                    t18.close()
                 out18[algo] = n18 * B / (r18.device_ms / 1e3)
                 if algo == "lpp_sgd":
                     na, msa, bya = r18.apply_timing
@@ -468,6 +526,7 @@ def ours(args) -> None:
                     t18.close()
                 del t18
             out18["lpp_over_mb"] = out18["lpp_sgd"] / out18["mb_sgd"]
+            out18["lpp_over_pl"] = out18["lpp_sgd"] / out18["pl_sgd"]
             line["resnet18"] = out18
 
     # ---------------- ResNet-50 / ImageNet shape (config C3): in-situ HBM apply ----------------
@@ -487,6 +546,7 @@ def ours(args) -> None:
             a50 = by50 / (ms50 / 1e3) / 1e9
             line["resnet50"] = {
                 "workload": "resnet50_imagenet224_lpp_sgd_u4_b32_h16", "params": obj50.dim,
+                "conv_compute": "bf16 shadow weights (both rows)",
                 "value": sum(r50.counter_finals) * 32 / (r50.device_ms / 1e3), "unit": "images/s",
                 "apply_roofline": {"achieved": a50, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                    "frac": a50 / peaks["hbm_gbs"], "launches": n50,
@@ -614,7 +674,7 @@ def ours(args) -> None:
             # bounded sample of the same workload: ~100 minibatches, 10-15 s of
             # CPU work on the box's host cores (after a short warm-up)
             run_lpp_cpu(slots=U, updaters=U, batch_size=B)
-            r = run_lpp_cpu(slots=24 * U, updaters=U, batch_size=B)
+            r = run_lpp_cpu(slots=25 * U, updaters=U, batch_size=B)
             line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
                                     "cores": r["cores"], "kind": "port",
                                     "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
@@ -637,6 +697,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bf16", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

@@ -222,10 +222,17 @@ def run_lpp_cpu(slots: int, updaters: int = 4, batch_size: int = 128, n_samples:
     def sync_every(s):
         return 1 if s < switch else period
 
+    # every updater's model is built before the clock starts; each updater
+    # thread runs its intra-op work on its share of the cores (OpenMP's
+    # thread count is per calling thread: without this, U threads x all cores)
+    models = {(q, r): Net() for q in range(workers) for r in range(1, updaters + 1)}
+    per_thread = max(1, cores // (updaters * workers))
+
     def updater(q: int, rank: int):
         w = ws[q]
         try:
-            model = Net()
+            torch.set_num_threads(per_thread)
+            model = models[(q, rank)]
             params = list(model.parameters())
             snap = np.empty(dim)
             mom = np.zeros(dim) if momentum else None
