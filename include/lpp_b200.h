@@ -67,6 +67,12 @@ int lpp_atomic_cas_i64(int64_t* p, int64_t expected, int64_t desired);
 int64_t lpp_atomic_wait_ge_i64(const int64_t* p, int64_t target,
                                const int64_t* abort_flag, int max_sleep_us);
 
+/* Host memory the kernels read and write directly (cudaHostAlloc mapped +
+ * portable, zero-filled): round-stamp cells, sampled-tag index rings and
+ * classification records.  *dev is the device view (== *host under UVA). */
+int lpp_host_alloc(size_t bytes, void** host, void** dev);
+int lpp_host_free(void* host);
+
 /* ------------------------------------------------------------------ */
 /* arenas: flat fp32 parameter vectors in device memory (a1)           */
 /* replace ParamStore.values (paramstore.py:59-77)                     */
@@ -78,6 +84,14 @@ int lpp_arena_destroy(lpp_arena_t arena);
 float* lpp_arena_data(lpp_arena_t arena);
 size_t lpp_arena_size(lpp_arena_t arena);
 int lpp_arena_device(lpp_arena_t arena);
+
+/* Element access — replaces _atomics.load_f64 / store_f64 (_atomics.c:41-56,
+ * method table :395-396; ParamStore.read / write, paramstore.py:79-86): one
+ * untorn element of a device arena of `len` elements, acquire load / release
+ * store at system scope, ordered on `stream` and synchronous (returns after
+ * the element was read / written).  i >= len -> LPP_E_INDEX (ref IndexError). */
+int lpp_load_f32(const float* arena, size_t len, size_t i, float* out, void* stream);
+int lpp_store_f32(float* arena, size_t len, size_t i, float v, void* stream);
 
 /* Multi-process peer mapping (one process per GPU, NVLink P2P).
  * export writes LPP_IPC_HANDLE_BYTES bytes to handle_out. */
@@ -117,6 +131,37 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
                        int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
                        const float* lr_dev, float mu, float wd, int32_t stamp,
                        void* stream);
+
+/* K5 inside the fused launch, in the reference updater's order
+ * (engine.py:343-362: sampled tags at the snapshot, k_claim after the
+ * gradient, then the apply):
+ *   cur_claim[0..1] = (k_claim, clean): k_claim = *avg_cell read when the
+ *       kernel starts (after this step's gradient), clean = all of this
+ *       step's k tags cur_dev[j] >= k_claim              (cur_claim may be NULL)
+ *   next_dev[j] (and next_host[j]) = max(tags[next_idx[j]], *avg_cell) for
+ *       j < k, read by the last CTA after every CTA's updates and tag
+ *       stores, i.e. at the next step's snapshot; the floor *avg_cell is
+ *       the worker's last completed round stamp, which a round writes
+ *       into every element (engine.py:421)        (next_idx may be NULL)
+ * avg_cell, next_idx, next_host, cur_claim may point into host memory from
+ * lpp_host_alloc (the kernel reads / writes it directly).  done: a 4-byte
+ * device counter, zero before the first launch, private to the stream (the
+ * last CTA resets it).  Write tags: every thread issues all of its
+ * reductions, one fence.acq_rel.gpu, then the tags of the same elements. */
+typedef struct lpp_tag_plan {
+  const int64_t* next_idx;
+  int32_t* next_dev;
+  int32_t* next_host;
+  const int32_t* cur_dev;
+  int64_t* cur_claim;
+  const int64_t* avg_cell;
+  uint32_t* done;
+  int32_t k;
+} lpp_tag_plan;
+int lpp_apply_snapshot_plan(float* x, const float* g, float* m, float* replica,
+                            int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
+                            const float* lr_dev, float mu, float wd, int32_t stamp,
+                            const lpp_tag_plan* plan, void* stream);
 
 /* Reference-shaped accumulate: dst[start + e] += scale * delta[e],
  * e in [0, n), with dst of length dst_len (range-checked like
@@ -179,6 +224,16 @@ int lpp_snapshot_tagged(const float* src, const int32_t* tags, float* out,
  * guarantees 0 <= idx[k] < len(tags)) */
 int lpp_gather_tags(const int32_t* tags, const int64_t* idx, size_t k, int32_t* out,
                     void* stream);
+/* the sampled-tag gather of an unfused snapshot with the round floor:
+ * out[j] = max(tags[idx[j]], *floor_cell) (floor_cell may be NULL = 0);
+ * idx / floor_cell / out_host may be lpp_host_alloc memory */
+int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
+                          const int64_t* floor_cell, int32_t* out_dev, int32_t* out_host,
+                          void* stream);
+/* classification at apply time (engine.py:353-362) for the unfused paths:
+ * out[0] = *claim_cell read when the kernel runs, out[1] = all k tags >= it */
+int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_cell, int64_t* out,
+                 void* stream);
 /* K4 + tags_q[e] = stamps[q] after the correction (host arrays of Q) */
 int lpp_average_shard_tagged(float* const* arenas, int32_t* const* tags,
                              const int32_t* stamps, int Q, size_t lo, size_t hi,
@@ -399,6 +454,20 @@ typedef struct {
   int64_t epoch_seed;             /* < 0: i.i.d. draws */
   int64_t* idx_pinned;            /* [in_flight + 2][batch] */
   int64_t* idx_dev;               /* [batch] */
+  /* K5 in the reference's order (lpp_tag_plan): with claim_ring != NULL the
+   * sampled-tag indices live in host-mapped memory (tag_idx_pinned, device
+   * view tag_idx_dev, [in_flight + 2][tag_pick]) and the kernels read them
+   * there; the effective tags go to tag_out_dev and the host-mapped
+   * tag_out_pinned (device view tag_out_host_dev); each step's (k_claim,
+   * clean) is written by its apply kernel into claim_ring[slot] (device
+   * view claim_ring_dev), k_claim read from avg_cell_dev (the device view
+   * of last_avg_stamp, which then must be host-mapped); done_ctr: a 4-byte
+   * zeroed device counter private to this updater */
+  int64_t* claim_ring;            /* [in_flight + 2][2] host view */
+  int64_t* claim_ring_dev;
+  int32_t* tag_out_host_dev;
+  const int64_t* avg_cell_dev;
+  uint32_t* done_ctr;
 } lpp_updater_cfg;
 
 typedef struct {
@@ -415,18 +484,21 @@ int lpp_updater_run(const lpp_updater_cfg* cfg, lpp_updater_stats* stats);
  * code: the round protocol of paper_2203_06638_b200/rounds.py over the
  * shared int64 control block (RoundControl layout: [0] round_calls, [1]
  * stop, [2] abort, [3] drained workers, [8, 8+Q) round stamps, then the
- * per-round vote / final-vote / fence0 / fence1 arrays of max_rounds + 2
- * cells) and the owner-computes K4 round on its own stream:
+ * vote / final-vote / fence0 / fence1 arrays of RING = 8 cells indexed by
+ * round mod 8, each round's cells zeroed once all votes of the next round
+ * are in — no limit on the number of rounds) and the owner-computes K4
+ * round on its own stream:
  *   open (CAS on round_calls when this worker's sync_every period is due,
  *   or every worker drained) -> vote -> u = stamp; [tags: publish u,
  *   fence 0] -> K4 over the owned shard (+ the mean on the final round)
- *   -> stream sync -> [fence 1] -> last_avg_stamp = u -> wait for all Q
- *   votes -> stop after the unanimous final round.
+ *   -> stream sync -> [tags / floor / eval: fence 1] -> last_avg_stamp = u
+ *   -> wait for all Q votes -> release the previous round's cells -> stop
+ *   after the unanimous final round.
  * One record per joined round (round, u, s_cur, k_delta, unanimous,
  * wall ms since t0) for RunResult.stamps. */
 typedef struct {
   int64_t* ctrl;                  /* RoundControl buffer */
-  int64_t max_rounds;
+  int64_t max_rounds;             /* unused (the control block is a ring); kept for layout */
   int32_t workers;                /* Q */
   int32_t q;                      /* this worker */
   int32_t updaters;               /* U: this worker drained when *exited == U */
@@ -469,6 +541,10 @@ typedef struct {
   int32_t time_rounds;
   double* k4_ms;                  /* summed */
   int64_t* k4_rounds;             /* timed rounds */
+  /* the updaters classify with the round floor (lpp_tag_plan): the round
+   * counts as applied (last_avg_stamp) only after every owner is done with
+   * this worker's arena (fence 1), with no per-element tag writes */
+  int32_t stamp_floor;
 } lpp_averager_cfg;
 
 int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);

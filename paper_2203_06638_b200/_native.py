@@ -77,7 +77,16 @@ class UpdaterCfg(ctypes.Structure):
         ("rec_tags", _vp), ("rec_cap", _c.c_int64), ("rec_count", _vp),
         ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
+        ("claim_ring", _vp), ("claim_ring_dev", _vp), ("tag_out_host_dev", _vp),
+        ("avg_cell_dev", _vp), ("done_ctr", _vp),
     ]
+
+
+class TagPlan(ctypes.Structure):
+    """``lpp_tag_plan`` (include/lpp_b200.h)."""
+
+    _fields_ = [("next_idx", _vp), ("next_dev", _vp), ("next_host", _vp), ("cur_dev", _vp),
+                ("cur_claim", _vp), ("avg_cell", _vp), ("done", _vp), ("k", _c.c_int32)]
 
 
 class AveragerCfg(ctypes.Structure):
@@ -95,6 +104,7 @@ class AveragerCfg(ctypes.Structure):
         ("eval_cap", _c.c_int64), ("eval_rec", _vp), ("eval_wall_ms", _vp), ("eval_count", _vp),
         ("flops_cell", _vp), ("classified_cell", _vp), ("clean_cell", _vp),
         ("time_rounds", _c.c_int32), ("k4_ms", _vp), ("k4_rounds", _vp),
+        ("stamp_floor", _c.c_int32),
     ]
 
 
@@ -134,6 +144,17 @@ _SIGS = {
         [_vp, _vp, _vp, _vp, _vp, _size, _size, _size, _c.c_float, _vp, _c.c_float, _c.c_float,
          _c.c_int32, _vp],
     ),
+    "lpp_apply_snapshot_plan": (
+        _c.c_int,
+        [_vp, _vp, _vp, _vp, _vp, _size, _size, _size, _c.c_float, _vp, _c.c_float, _c.c_float,
+         _c.c_int32, _c.POINTER(TagPlan), _vp],
+    ),
+    "lpp_gather_tags_floor": (_c.c_int, [_vp, _vp, _size, _vp, _vp, _vp, _vp]),
+    "lpp_classify": (_c.c_int, [_vp, _size, _vp, _vp, _vp]),
+    "lpp_host_alloc": (_c.c_int, [_size, _c.POINTER(_vp), _c.POINTER(_vp)]),
+    "lpp_host_free": (_c.c_int, [_vp]),
+    "lpp_load_f32": (_c.c_int, [_vp, _size, _size, _c.POINTER(_c.c_float), _vp]),
+    "lpp_store_f32": (_c.c_int, [_vp, _size, _size, _c.c_float, _vp]),
     "lpp_snapshot": (_c.c_int, [_vp, _vp, _size, _vp]),
     "lpp_average_shard": (
         _c.c_int,
@@ -289,6 +310,63 @@ def apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr, lr
                    stamp, stream) -> None:
     check(lib.lpp_apply_snapshot(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr,
                                  lr_dev_ptr, mu, wd, int(stamp), stream), "apply_snapshot")
+
+
+def apply_snapshot_plan(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr, lr_dev_ptr, mu,
+                        wd, stamp, plan: TagPlan, stream) -> None:
+    check(lib.lpp_apply_snapshot_plan(x_ptr, g_ptr, m_ptr, replica_ptr, tags_ptr, n, lo, hi, lr,
+                                      lr_dev_ptr, mu, wd, stamp, ctypes.byref(plan), stream),
+          "apply_snapshot_plan")
+
+
+def gather_tags_floor(tags_ptr, idx_ptr, k, floor_ptr, out_dev_ptr, out_host_ptr, stream) -> None:
+    check(lib.lpp_gather_tags_floor(tags_ptr, idx_ptr, k, floor_ptr, out_dev_ptr, out_host_ptr, stream),
+          "gather_tags_floor")
+
+
+def classify(tags_ptr, k, claim_ptr, out_ptr, stream) -> None:
+    check(lib.lpp_classify(tags_ptr, k, claim_ptr, out_ptr, stream), "classify")
+
+
+def load_f32(arena_ptr: int, length: int, i: int, stream: int = 0) -> float:
+    out = ctypes.c_float()
+    check(lib.lpp_load_f32(arena_ptr, length, i, ctypes.byref(out), stream), "load_f32")
+    return float(out.value)
+
+
+def store_f32(arena_ptr: int, length: int, i: int, v: float, stream: int = 0) -> None:
+    check(lib.lpp_store_f32(arena_ptr, length, i, float(v), stream), "store_f32")
+
+
+class HostBuffer:
+    """Mapped, portable host memory (``lpp_host_alloc``) that kernels read
+    and write directly; ``view(dtype, shape)`` gives numpy views, ``dev`` the
+    device address of the first byte."""
+
+    def __init__(self, nbytes: int):
+        h, d = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib.lpp_host_alloc(int(nbytes), ctypes.byref(h), ctypes.byref(d)), "host_alloc")
+        self.ptr, self.dev, self.nbytes = int(h.value), int(d.value), int(nbytes)
+        self._raw = (ctypes.c_char * self.nbytes).from_address(self.ptr)
+
+    def view(self, dtype, shape, offset: int = 0) -> np.ndarray:
+        dt = np.dtype(dtype)
+        count = int(np.prod(shape))
+        if offset + count * dt.itemsize > self.nbytes:
+            raise ValueError("view exceeds the host buffer")
+        return np.frombuffer(self._raw, dtype=dt, count=count, offset=offset).reshape(shape)
+
+    def close(self) -> None:
+        if self.ptr:
+            self._raw = None
+            check(lib.lpp_host_free(self.ptr), "host_free")
+            self.ptr = self.dev = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def accum(dst_ptr: int, dst_len: int, start: int, delta_ptr: int, n: int, scale: float,

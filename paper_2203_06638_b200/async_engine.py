@@ -103,7 +103,6 @@ class _Worker:
         self.dev = torch.device("cuda", device)
         self.store = ParamStore(x0, device=device, mode=cfg.apply_mode)
         self.exited = AtomicCounter(0)
-        self.last_avg_stamp = AtomicCounter(0)
         self.synced_at = AtomicCounter(0)
         self.gate = PauseGate() if cfg.quiescent else None
         d = engine.dim
@@ -121,18 +120,30 @@ class _Worker:
         self.grads = [Arena(d, device) for _ in range(U)]
         self.moms = [Arena(d, device) for _ in range(U)] if cfg.momentum else [None] * U
         self.mean_out = torch.zeros(d + 4, dtype=torch.float32, device=self.dev)
-        # K5 write tags (int32 stamps, an arena reinterpreted) + per-updater
-        # staging for the sampled-tag gather and the full-snapshot min tag
+        # K5 write tags (int32 stamps, an arena reinterpreted)
         self.tag_arena = Arena(d, device) if cfg.tracks else None
         self.tags = self.tag_arena.tensor.view(torch.int32) if cfg.tracks else None
         depth = cfg.in_flight + 2
         self.tag_pick = min(cfg.tag_sample, d)
+        k = max(self.tag_pick, 1)
+        self.kk = k
+        # host-mapped memory the kernels read / write directly (lpp_host_alloc):
+        # [0] last_avg_stamp — the worker's last completed round stamp, read by
+        # the apply kernels as k_claim and as the tag floor — then, per updater
+        # and in-flight slot, the sampled-tag indices (int64), the gathered
+        # effective tags (int32) and the apply's (k_claim, clean) record
+        self._o_idx = 64
+        self._o_tag = self._o_idx + 8 * U * depth * k
+        self._o_claim = self._o_tag + 4 * U * depth * k
+        self.hostmem = N.HostBuffer(self._o_claim + 16 * U * depth)
+        self.last_avg_stamp = AtomicCounter(0, cell=self.hostmem.view(np.int64, (1,)), index=0)
+        self.avg_dev = self.hostmem.dev
         if cfg.tracks:
-            k = max(self.tag_pick, 1)
-            self.tag_idx_dev = torch.zeros((U, k), dtype=torch.long, device=self.dev)
-            self.tag_idx_pinned = torch.zeros((U, depth, k), dtype=torch.long, pin_memory=True)
+            self.tag_idx_np = self.hostmem.view(np.int64, (U, depth, k), self._o_idx)
+            self.tag_np = self.hostmem.view(np.int32, (U, depth, k), self._o_tag)
+            self.claim_np = self.hostmem.view(np.int64, (U, depth, 2), self._o_claim)
             self.tag_out_dev = torch.zeros((U, depth, k), dtype=torch.int32, device=self.dev)
-            self.tag_pinned = torch.zeros((U, depth, k), dtype=torch.int32, pin_memory=True)
+            self.done_ctr = torch.zeros(U, dtype=torch.int32, device=self.dev)
             self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
             self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
         # full record mode keeps every update's whole tag snapshot (reference
@@ -144,6 +155,21 @@ class _Worker:
         self.programs: list[StepProgram] = []
         self.idx_pinned = None
         self.batch_pinned = None
+
+    def idx_dev(self, r: int, slot: int) -> int:
+        depth = self.tag_idx_np.shape[1]
+        return self.avg_dev + self._o_idx + 8 * self.kk * (r * depth + slot)
+
+    def tag_host_dev(self, r: int, slot: int) -> int:
+        depth = self.tag_idx_np.shape[1]
+        return self.avg_dev + self._o_tag + 4 * self.kk * (r * depth + slot)
+
+    def claim_dev(self, r: int, slot: int) -> int:
+        depth = self.tag_idx_np.shape[1]
+        return self.avg_dev + self._o_claim + 16 * (r * depth + slot)
+
+    def host_addr(self, dev_addr: int) -> int:
+        return self.hostmem.ptr + (dev_addr - self.avg_dev)
 
     def build_programs(self, engine: "_Engine", block_ids_per_rank: list[list[int]]) -> None:
         cfg = engine.cfg
@@ -184,8 +210,6 @@ class _Worker:
             # writes/reads skip the framework's dispatch
             self.idx_np = self.idx_pinned.numpy()
             if cfg.tracks:
-                self.tag_idx_np = self.tag_idx_pinned.numpy()
-                self.tag_np = self.tag_pinned.numpy()
                 self.min_np = self.min_pinned.numpy()
             # the warm-up passes touched the replica/grad arenas and BN stats
             # only; re-snapshot so every replica starts at x0
@@ -215,6 +239,7 @@ class _Worker:
         if self.store.tag_arena is not None:
             self.store.tag_arena.close()
         self.tags = None
+        self.hostmem.close()
 
 
 class _Engine(NativeLoops):
@@ -228,6 +253,11 @@ class _Engine(NativeLoops):
         self.host_batches = host_batches
         self.time_apply = time_apply
         self.group = group  # multi-process attachment (None: all workers in this process)
+        # K5: rounds write their stamp into every element's tag only in full
+        # record mode (whole-vector tag snapshots); otherwise the round floor
+        # stands for it — the updaters' tag gathers read max(tag, last round
+        # stamp), so averaging writes no tags and takes no stamp fence
+        self.round_tags = cfg.tracks and cfg.record_mode == "full"
         self.x0_host = np.asarray(obj.init_params(cfg.seed), dtype=np.float64)
         x0 = torch.from_numpy(self.x0_host.astype(np.float32))
         if group is None:
@@ -248,16 +278,13 @@ class _Engine(NativeLoops):
                             raise RuntimeError("averaging needs peer access between worker devices")
             self.arena_ptrs = [self.workers[q].store.arena.ptr for q in range(cfg.workers)]
             self.tag_ptrs = ([self.workers[q].tag_arena.ptr for q in range(cfg.workers)]
-                             if cfg.tracks else None)
-            max_rounds = cfg.workers * (cfg.budget + cfg.updaters) + 8
-            if cfg.round_budget is not None:
-                max_rounds = min(max_rounds, cfg.round_budget + 8)
-            self.ctrl = RoundControl(cfg.workers, max_rounds)
+                             if self.round_tags else None)
+            self.ctrl = RoundControl(cfg.workers)
         else:
             group.reset_control()
             self.arena_ptrs = group.attach_arenas(self.workers[group.rank].store.arena)
             self.tag_ptrs = (group.attach_arenas(self.workers[group.rank].tag_arena)
-                             if cfg.tracks else None)
+                             if self.round_tags else None)
             self.ctrl = group.control
         self.shards = shard_bounds(self.dim, cfg.workers)
         self.nvls = {}
@@ -380,6 +407,7 @@ class _Engine(NativeLoops):
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(astream)
             if tracks:                                                                # K1/K2 + K5
+                self.classify_on_device(w, r, slot, sp)
                 N.apply_sgd_tagged(w.store.arena.ptr + off, w.grads[r].ptr + off,
                                    (mom.ptr + off) if mom is not None else None, blk.length,
                                    float(lr), None, cfg.momentum, cfg.weight_decay,
@@ -435,15 +463,24 @@ class _Engine(NativeLoops):
                 and cfg.record_mode != "full" and cfg.apply_mode != "plain")
 
     def gather_tags(self, w: _Worker, r: int, slot: int, tag_idx) -> None:
-        """K5: sampled tags of the NEXT snapshot into slot, then D2H (on the
-        updater stream; must precede the values it describes)."""
+        """K5: the step's sampled tags, raised to the round floor, into slot
+        (device ring + host-mapped copy); on the updater stream before the
+        snapshot values it describes (paramstore.py:108-112).  The indices are
+        written into host-mapped memory and read there by the kernel."""
         k = w.tag_pick
-        sp = w.streams[r].cuda_stream
         w.tag_idx_np[r, slot, :k] = tag_idx
-        N.copy_async(w.tag_idx_dev[r].data_ptr(), w.tag_idx_pinned[r, slot].data_ptr(), 8 * k, sp)
-        N.gather_tags(w.tag_arena.ptr, w.tag_idx_dev[r].data_ptr(), k,
-                      w.tag_out_dev[r, slot].data_ptr(), sp)
-        N.copy_async(w.tag_pinned[r, slot].data_ptr(), w.tag_out_dev[r, slot].data_ptr(), 4 * k, sp)
+        N.gather_tags_floor(w.tag_arena.ptr, w.idx_dev(r, slot), k, w.avg_dev,
+                            w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot),
+                            w.streams[r].cuda_stream)
+
+    def classify_on_device(self, w: _Worker, r: int, slot: int, stream_ptr: int) -> None:
+        """K5 classification at apply time (engine.py:353-362): k_claim is
+        read by the kernel when it runs, i.e. after the step's gradient."""
+        if self.cfg.record_mode == "full":
+            N.classify(w.min_dev[r, slot].data_ptr(), 1, w.avg_dev, w.claim_dev(r, slot), stream_ptr)
+        else:
+            N.classify(w.tag_out_dev[r, slot].data_ptr(), w.tag_pick, w.avg_dev,
+                       w.claim_dev(r, slot), stream_ptr)
 
     def step_fused(self, w: _Worker, r: int, block_id: int, lr: float, batch, slot: int,
                    next_slot: int, u: int, first: bool, tag_idx, next_tag_idx,
@@ -471,8 +508,16 @@ class _Engine(NativeLoops):
             prog.run(block_id, buf)                                                      # fwd+bwd
             if self.host_batches:
                 w.buf_free[r][buf].record(stream)
+            plan = None
             if tracks:
-                self.gather_tags(w, r, next_slot, next_tag_idx)                          # K5 (next)
+                # K5 inside the apply: classify this step (k_claim read after
+                # its gradient), stamp, and gather the next step's tags after
+                # this apply landed (engine.py:343-362 order)
+                k = w.tag_pick
+                w.tag_idx_np[r, next_slot, :k] = next_tag_idx
+                plan = N.TagPlan(w.idx_dev(r, next_slot), w.tag_out_dev[r, next_slot].data_ptr(),
+                                 w.tag_host_dev(r, next_slot), w.tag_out_dev[r, slot].data_ptr(),
+                                 w.claim_dev(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(), k)
             mom = w.moms[r]
             astream = stream
             if self.side_apply:
@@ -484,10 +529,16 @@ class _Engine(NativeLoops):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(astream)
-            N.apply_snapshot(w.store.arena.ptr, w.grads[r].ptr,                           # K1+K3
-                             mom.ptr if mom is not None else None, w.replicas[r].ptr,
-                             w.tag_arena.ptr if tracks else None, self.dim, blk.start, blk.stop,
-                             float(lr), None, cfg.momentum, cfg.weight_decay, u, sp)
+            if plan is not None:                                                         # K1+K3+K5
+                N.apply_snapshot_plan(w.store.arena.ptr, w.grads[r].ptr,
+                                      mom.ptr if mom is not None else None, w.replicas[r].ptr,
+                                      w.tag_arena.ptr, self.dim, blk.start, blk.stop, float(lr), None,
+                                      cfg.momentum, cfg.weight_decay, u, plan, sp)
+            else:                                                                         # K1+K3
+                N.apply_snapshot(w.store.arena.ptr, w.grads[r].ptr,
+                                 mom.ptr if mom is not None else None, w.replicas[r].ptr,
+                                 None, self.dim, blk.start, blk.stop,
+                                 float(lr), None, cfg.momentum, cfg.weight_decay, u, sp)
             if self.time_apply:
                 e1.record(astream)
                 # block: read g, RMW x, (+m), (+tag); whole arena: read x outside
@@ -510,7 +561,7 @@ class _Engine(NativeLoops):
             # (and the round's stamp written into the tags, add_assign's tagging)
             if final:
                 N.snapshot(w.store.arena.ptr, w.mean_out.data_ptr(), self.dim, stream.cuda_stream)
-            if w.tags is not None:
+            if self.round_tags:
                 with torch.cuda.stream(stream):
                     w.tags.fill_(int(stamps[0]))
             return
@@ -538,7 +589,7 @@ class _Engine(NativeLoops):
         st.synchronize()
         if fence is not None and not fence(1):
             return
-        nv.apply(w.store.arena.ptr, w.tag_arena.ptr if w.tags is not None else None, u, sp)
+        nv.apply(w.store.arena.ptr, w.tag_arena.ptr if self.round_tags else None, u, sp)
         if final:
             with torch.cuda.stream(st):
                 w.mean_out[: self.dim].copy_(nv.mean_tensor)
@@ -565,18 +616,19 @@ class _Engine(NativeLoops):
 
     def classify(self, w: _Worker, r: int, slot: int, rec: UpdateRecord) -> None:
         """Clean iff every sampled (or every, in full mode) tag is at or after
-        the last averaging stamp seen at claim time (engine.py:357-362);
-        called once the step's D2H of its tags has completed."""
+        the last averaging stamp at apply time (engine.py:357-362).  The
+        apply-side kernel already compared them; called once the step's
+        event completed, this reads its (k_claim, clean) record."""
         if w.tags is None:
             return
+        kc, cl = (int(v) for v in w.claim_np[r, slot])
+        rec.k_claim = kc
+        clean = bool(cl)
         if self.cfg.record_mode == "full":
-            clean = int(w.min_np[r, slot]) >= rec.k_claim
             if self.cfg.record_tensors and rec.snapshot is not None and rec.tags is None:
                 rec.tags = w.snap_tags[r][slot].cpu().numpy().astype(np.int64)
         else:
-            tg = w.tag_np[r, slot, :w.tag_pick].astype(np.int64)
-            rec.tags = tg
-            clean = bool((tg >= rec.k_claim).all())
+            rec.tags = w.tag_np[r, slot, :w.tag_pick].astype(np.int64)
         rec.clean = clean
         self.classified_count.add(1)
         if clean:
@@ -689,9 +741,13 @@ class _Engine(NativeLoops):
         def do_round(r, final, s_cur):
             quiet = w.gate is not None
             evalm = cfg.eval_interval > 0
-            # eval points need every owner's round mean: owners write mean_out
-            # each round and the round is fenced before worker 0 reads it
-            fenced = quiet or w.tags is not None or evalm
+            # fence 0: every worker's stamp is published before owners write it
+            # into the tags (full records) / every updater parked (quiescent);
+            # fence 1: every owner is done with this worker's arena before the
+            # round counts as applied (the updaters' k_claim and tag floor) and
+            # before worker 0 reads the owners' round means (eval points)
+            fenced0 = quiet or self.round_tags
+            fenced1 = quiet or w.tags is not None or evalm
             if quiet:
                 # quiescent: every worker's updaters parked and their streams
                 # drained before any owner touches the arenas
@@ -712,7 +768,7 @@ class _Engine(NativeLoops):
                         snaps[r] = (snap, self.nvls[q].mean_tensor.clone() if q == 0 else None)
                     return
                 stamps = None
-                if fenced:
+                if fenced0:
                     # every worker's round stamp is published before the owners
                     # write them into the tags (K5); the round counts as applied
                     # to this worker's arena only when every owner is done
@@ -722,7 +778,7 @@ class _Engine(NativeLoops):
                     stamps = self.ctrl.stamps()
                 self.average(q, w.avg_stream, final=final or full or evalm, stamps=stamps)
                 w.avg_stream.synchronize()
-                if fenced and not self.ctrl.fence(1, r):
+                if fenced1 and not self.ctrl.fence(1, r):
                     return
                 if full:
                     # the round mean, assembled from every owner's shard

@@ -174,7 +174,7 @@ __device__ __forceinline__ void st_tag_sys(int* p, int v) {
 }
 __device__ __forceinline__ int4 ld_tag4(const int* p) {
   int4 r;
-  asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.relaxed.sys.global.v4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p)
                : "memory");
@@ -182,7 +182,7 @@ __device__ __forceinline__ int4 ld_tag4(const int* p) {
 }
 __device__ __forceinline__ int ld_tag(const int* p) {
   int r;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.sys.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
   return r;
 }
 
@@ -452,104 +452,153 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 // is when K3 would have run anyway) and saves the block's second DRAM read.
 // (A returning atom.add.v4.f32 — old + delta — measured 4-8 % slower at
 // d18/d50: tools/bench_fused.py.)
+//
+// K5 inside the same launch (``lpp_tag_plan``), in the reference's order
+// (engine.py:343-362: snapshot tags -> gradient -> k_claim -> apply):
+//   * write tags: every thread issues ALL its reductions first, then one
+//     fence.acq_rel.gpu, then the tag stores of the same vectors (value
+//     before tag, _atomics.c:346-392) — one fence per thread instead of one
+//     per vector;
+//   * classification of THIS step: block 0 reads k_claim from the worker's
+//     round-stamp cell (host-mapped) when the kernel starts, i.e. after the
+//     step's gradient, and compares the step's sampled tags with it;
+//   * the NEXT step's sampled tags: gathered by the last CTA to finish,
+//     after every CTA's reductions and tag stores (a completion counter),
+//     i.e. at the next snapshot's point in time; each tag is raised to the
+//     worker's last completed round stamp (rounds stamp every element,
+//     engine.py:421 add_assign(..., stamp=u_avg): the floor stands for it).
+
+struct TagPlanDev {
+  const int64_t* next_idx;  // k sampled indices of the next step (host-mapped)
+  int* next_dev;            // -> the next step's effective tags (device ring slot)
+  int* next_host;           // -> and a host-mapped copy for the records (may be null)
+  const int* cur_dev;       // this step's effective tags (gathered at its snapshot)
+  int64_t* cur_claim;       // -> this step's (k_claim, clean) (host-mapped; may be null)
+  const int64_t* avg_cell;  // the worker's last completed round stamp (host-mapped)
+  unsigned* done;           // CTA completion counter (device, 0 between launches)
+  int k;
+};
+
+__device__ __forceinline__ int64_t ld_sys_i64(const int64_t* p) {
+  int64_t r;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(r) : "l"(p));
+  return r;
+}
+
+// gather the k sampled tags of the next snapshot (last CTA), tag >= floor
+__device__ __forceinline__ void plan_gather(const TagPlanDev& plan, const int* tags) {
+  __shared__ int is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_ar_gpu();  // this CTA's reductions and tag stores before the count
+    unsigned old = atomicAdd(plan.done, 1u);
+    is_last = (old == gridDim.x - 1);
+    if (is_last) fence_ar_gpu();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  const int floor_ = plan.avg_cell ? (int)ld_sys_i64(plan.avg_cell) : 0;
+  for (int j = threadIdx.x; j < plan.k; j += blockDim.x) {
+    int t = ld_tag(tags + ld_sys_i64(plan.next_idx + j));
+    t = t > floor_ ? t : floor_;
+    plan.next_dev[j] = t;
+    if (plan.next_host) plan.next_host[j] = t;
+  }
+  if (threadIdx.x == 0) *plan.done = 0u;
+}
 
 template <bool WD, bool MOM>
-__device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, float* rep, int* tags,
-                                           size_t e, size_t lo, size_t hi, float lr, float mu,
-                                           float wd, int stamp) {
+__device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, float* rep, size_t e,
+                                           size_t lo, size_t hi, float lr, float mu, float wd) {
   if (e >= lo && e < hi) {
     float xv = WD ? ld_cg(x + e) : 0.f;
     float mv = MOM ? m[e] : 0.f;
     float d = sgd_delta<WD, MOM>(g[e], xv, mv, lr, mu, wd);
     red_add_f32(x + e, d);
     float nv = ld_cg(x + e);
-    if (tags) fence_ar_gpu();
     if (MOM) m[e] = mv;
     rep[e] = nv;
-    if (tags) st_tag(tags + e, stamp);
   } else {
     rep[e] = ld_cg(x + e);
   }
 }
 
-template <bool WD, bool MOM, int UNR>
+template <bool WD, bool MOM, bool TAGS, bool PLAN>
 __global__ void __launch_bounds__(kThreads)
     k_apply_snapshot(float* x, const float* __restrict__ g, float* m, float* __restrict__ rep,
                      int* tags, size_t n, size_t lo, size_t hi, float lr,
-                     const float* __restrict__ lr_dev, float mu, float wd, int stamp) {
+                     const float* __restrict__ lr_dev, float mu, float wd, int stamp,
+                     TagPlanDev plan) {
+  // k_claim of this step (engine.py:353: read after the gradient), issued
+  // first and consumed at the end so its host round trip overlaps the work
+  const bool classifier = PLAN && blockIdx.x == 0 && threadIdx.x == 0 && plan.cur_claim != nullptr;
+  int64_t k_claim = 0;
+  if (classifier) k_claim = plan.avg_cell ? ld_sys_i64(plan.avg_cell) : 0;
   if (lr_dev) lr = *lr_dev;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nvec = n / 4;
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
-  // the copy path; the (at most two) straddling vectors go per element.
-  // UNR vectors per thread: every load of the group is issued before
-  // the first atomic, so 4 x (g, x, m) 16-byte loads are in flight.
+  // the copy path; the (at most two) straddling vectors go per element
   const size_t vlo = (lo + 3) / 4, vhi = hi / 4;
-  for (size_t i0 = tid; i0 < nvec; i0 += stride * UNR) {
-    float4 gr[UNR], xr[UNR], mr[UNR];
-    int kind[UNR];  // 0 none, 1 inside, 2 outside, 3 straddle
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      size_t i = i0 + (size_t)u * stride;
-      kind[u] = 0;
-      gr[u] = xr[u] = mr[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i >= nvec) continue;
-      if (i >= vlo && i < vhi) {
-        kind[u] = 1;
-        gr[u] = __ldg(reinterpret_cast<const float4*>(g) + i);
-        if (WD) xr[u] = ld_cg4(x + 4 * i);
-        if (MOM) mr[u] = reinterpret_cast<const float4*>(m)[i];
-      } else if (4 * i + 4 <= lo || 4 * i >= hi) {
-        kind[u] = 2;
-        xr[u] = ld_cg4(x + 4 * i);
-      } else {
-        kind[u] = 3;
-      }
-    }
-    float4 dr[UNR], nv[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (kind[u] != 1) continue;
-      size_t i = i0 + (size_t)u * stride;
-      dr[u].x = sgd_delta<WD, MOM>(gr[u].x, xr[u].x, mr[u].x, lr, mu, wd);
-      dr[u].y = sgd_delta<WD, MOM>(gr[u].y, xr[u].y, mr[u].y, lr, mu, wd);
-      dr[u].z = sgd_delta<WD, MOM>(gr[u].z, xr[u].z, mr[u].z, lr, mu, wd);
-      dr[u].w = sgd_delta<WD, MOM>(gr[u].w, xr[u].w, mr[u].w, lr, mu, wd);
+  for (size_t i = tid; i < nvec; i += stride) {
+    if (i >= vlo && i < vhi) {
+      float4 gr = __ldg(reinterpret_cast<const float4*>(g) + i);
+      float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), mr = xr;
+      if (WD) xr = ld_cg4(x + 4 * i);
+      if (MOM) mr = reinterpret_cast<const float4*>(m)[i];
+      float4 dr;
+      dr.x = sgd_delta<WD, MOM>(gr.x, xr.x, mr.x, lr, mu, wd);
+      dr.y = sgd_delta<WD, MOM>(gr.y, xr.y, mr.y, lr, mu, wd);
+      dr.z = sgd_delta<WD, MOM>(gr.z, xr.z, mr.z, lr, mu, wd);
+      dr.w = sgd_delta<WD, MOM>(gr.w, xr.w, mr.w, lr, mu, wd);
       // vector reduction, then re-read: the replica gets the arena value
       // after this step's add (plus any concurrent adds that landed first),
-      // i.e. what a K3 snapshot right after the apply would copy.  Measured
-      // 4-8 % faster at d18/d50 than a returning atom.add.v4 (old + delta)
-      red_add_v4(x + 4 * i, dr[u]);
-      nv[u] = ld_cg4(x + 4 * i);
-    }
-    // the re-read returns after the reduction is performed (same address),
-    // so the fence before the tag stores has nothing else to wait for
-    if (tags) fence_ar_gpu();
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      size_t i = i0 + (size_t)u * stride;
-      if (kind[u] == 1) {
-        if (MOM) reinterpret_cast<float4*>(m)[i] = mr[u];
-        reinterpret_cast<float4*>(rep)[i] = nv[u];
-        if (tags) st_tag4(tags + 4 * i, stamp);
-      } else if (kind[u] == 2) {
-        reinterpret_cast<float4*>(rep)[i] = xr[u];
-      } else if (kind[u] == 3) {
-        for (size_t e = 4 * i; e < 4 * i + 4; ++e)
-          fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
-      }
+      // i.e. what a K3 snapshot right after the apply would copy
+      red_add_v4(x + 4 * i, dr);
+      float4 nv = ld_cg4(x + 4 * i);
+      if (MOM) reinterpret_cast<float4*>(m)[i] = mr;
+      reinterpret_cast<float4*>(rep)[i] = nv;
+    } else if (4 * i + 4 <= lo || 4 * i >= hi) {
+      reinterpret_cast<float4*>(rep)[i] = ld_cg4(x + 4 * i);
+    } else {
+      for (size_t e = 4 * i; e < 4 * i + 4; ++e) fused_elem<WD, MOM>(x, g, m, rep, e, lo, hi, lr, mu, wd);
     }
   }
   if (blockIdx.x == 0)
     for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x)
-      fused_elem<WD, MOM>(x, g, m, rep, tags, e, lo, hi, lr, mu, wd, stamp);
+      fused_elem<WD, MOM>(x, g, m, rep, e, lo, hi, lr, mu, wd);
+  if (TAGS) {
+    // one fence: all of this thread's reductions are performed before any of
+    // its tag stores; then the tags of exactly the elements it updated
+    fence_ar_gpu();
+    for (size_t i = tid; i < nvec; i += stride) {
+      if (i >= vlo && i < vhi) {
+        st_tag4(tags + 4 * i, stamp);
+      } else if (!(4 * i + 4 <= lo || 4 * i >= hi)) {
+        for (size_t e = 4 * i; e < 4 * i + 4; ++e)
+          if (e >= lo && e < hi) st_tag(tags + e, stamp);
+      }
+    }
+    if (blockIdx.x == 0)
+      for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x)
+        if (e >= lo && e < hi) st_tag(tags + e, stamp);
+  }
+  if (PLAN) {
+    if (classifier) {
+      int clean = 1;
+      for (int j = 0; j < plan.k; ++j) clean &= ((int64_t)plan.cur_dev[j] >= k_claim);
+      plan.cur_claim[0] = k_claim;
+      plan.cur_claim[1] = clean;
+    }
+    if (plan.k > 0 && plan.next_idx) plan_gather(plan, tags);
+  }
 }
 
-extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
-                                  int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
-                                  const float* lr_dev, float mu, float wd, int32_t stamp,
-                                  void* stream) {
+static int apply_snapshot_launch(float* x, const float* g, float* m, float* replica, int32_t* tags,
+                                 size_t n, size_t lo, size_t hi, float lr, const float* lr_dev,
+                                 float mu, float wd, int32_t stamp, const lpp_tag_plan* plan,
+                                 void* stream) {
   if (n == 0) return LPP_OK;
   if (!x || !g || !replica) return set_err(LPP_E_VALUE, "apply_snapshot: null buffer");
   if (lo > hi || hi > n) return set_err(LPP_E_INDEX, "apply_snapshot: block outside [0, n)");
@@ -558,6 +607,17 @@ extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* rep
                 (tags ? (uintptr_t)tags : 0);
   if (a & 15u)
     return set_err(LPP_E_VALUE, "apply_snapshot: arena bases must be 16-byte aligned");
+  TagPlanDev pd{};
+  if (plan) {
+    if (!tags) return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs the tag arena");
+    if (plan->k < 0) return set_err(LPP_E_VALUE, "apply_snapshot: negative tag count");
+    if (plan->k > 0 && plan->next_idx && (!plan->next_dev || !plan->done))
+      return set_err(LPP_E_VALUE, "apply_snapshot: next-step gather needs out and counter");
+    if (plan->cur_claim && plan->k > 0 && !plan->cur_dev)
+      return set_err(LPP_E_VALUE, "apply_snapshot: classification needs this step's tags");
+    pd = TagPlanDev{plan->next_idx, plan->next_dev, plan->next_host, plan->cur_dev,
+                    plan->cur_claim, plan->avg_cell, plan->done, plan->k};
+  }
   size_t nvec = n / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
   cudaStream_t st = (cudaStream_t)stream;
@@ -567,11 +627,16 @@ extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* rep
   // (with both the returning-atomic and the reduction + re-read bodies); 64-
   // or 128-thread CTAs (easier to fit between other streams' CTAs) changed
   // neither the in-situ d20 time nor images/s
-  // (a split layout — block vectors, then the outside vectors as a 4-way
-  // unrolled copy — measured 4-5 % slower for full blocks and at d20)
 #define FUSED_LAUNCH(W, M)                                                                      \
-  k_apply_snapshot<W, M, 1><<<grid, kThreads, 0, st>>>(x, g, m, replica, tags, n, lo, hi, lr, \
-                                                       lr_dev, mu, wd, stamp);
+  if (plan)                                                                                     \
+    k_apply_snapshot<W, M, true, true><<<grid, kThreads, 0, st>>>(                             \
+        x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
+  else if (tags)                                                                                \
+    k_apply_snapshot<W, M, true, false><<<grid, kThreads, 0, st>>>(                            \
+        x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
+  else                                                                                          \
+    k_apply_snapshot<W, M, false, false><<<grid, kThreads, 0, st>>>(                           \
+        x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);
   if (WD && MOM) {
     FUSED_LAUNCH(true, true)
   } else if (WD) {
@@ -583,6 +648,134 @@ extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* rep
   }
 #undef FUSED_LAUNCH
   LAUNCH_CHECK("apply_snapshot");
+  return LPP_OK;
+}
+
+extern "C" int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
+                                  int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
+                                  const float* lr_dev, float mu, float wd, int32_t stamp,
+                                  void* stream) {
+  return apply_snapshot_launch(x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp,
+                               nullptr, stream);
+}
+
+extern "C" int lpp_apply_snapshot_plan(float* x, const float* g, float* m, float* replica,
+                                       int32_t* tags, size_t n, size_t lo, size_t hi, float lr,
+                                       const float* lr_dev, float mu, float wd, int32_t stamp,
+                                       const lpp_tag_plan* plan, void* stream) {
+  if (!plan) return set_err(LPP_E_VALUE, "apply_snapshot_plan: null plan");
+  return apply_snapshot_launch(x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, plan,
+                               stream);
+}
+
+// K5 gather with the round floor, for a step whose snapshot is a separate
+// K3 (the first step of a fused run, the unfused paths): out = max(tag, floor)
+__global__ void k_gather_tags_floor(const int* tags, const int64_t* idx, int k,
+                                    const int64_t* floor_cell, int* out_dev, int* out_host) {
+  const int floor_ = floor_cell ? (int)ld_sys_i64(floor_cell) : 0;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    int t = ld_tag(tags + ld_sys_i64(idx + j));
+    t = t > floor_ ? t : floor_;
+    if (out_dev) out_dev[j] = t;
+    if (out_host) out_host[j] = t;
+  }
+}
+
+extern "C" int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
+                                     const int64_t* floor_cell, int32_t* out_dev,
+                                     int32_t* out_host, void* stream) {
+  if (k == 0) return LPP_OK;
+  if (!tags || !idx || (!out_dev && !out_host))
+    return set_err(LPP_E_VALUE, "gather_tags_floor: null buffer");
+  if (k > (1u << 20)) return set_err(LPP_E_VALUE, "gather_tags_floor: k too large");
+  k_gather_tags_floor<<<1, kThreads, 0, (cudaStream_t)stream>>>(tags, idx, (int)k, floor_cell,
+                                                                 out_dev, out_host);
+  LAUNCH_CHECK("gather_tags_floor");
+  return LPP_OK;
+}
+
+// K5 classification at apply time for the unfused paths (engine.py:353-362):
+// out[0] = k_claim read now from the round-stamp cell, out[1] = all tags >= it
+__global__ void k_classify(const int* tags, int k, const int64_t* claim_cell, int64_t* out) {
+  if (threadIdx.x != 0) return;
+  const int64_t kc = claim_cell ? ld_sys_i64(claim_cell) : 0;
+  int clean = 1;
+  for (int j = 0; j < k; ++j) clean &= ((int64_t)tags[j] >= kc);
+  out[0] = kc;
+  out[1] = clean;
+}
+
+extern "C" int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_cell,
+                            int64_t* out, void* stream) {
+  if (!out || (k > 0 && !tags)) return set_err(LPP_E_VALUE, "classify: null buffer");
+  if (k > (1u << 20)) return set_err(LPP_E_VALUE, "classify: k too large");
+  k_classify<<<1, 32, 0, (cudaStream_t)stream>>>(tags, (int)k, claim_cell, out);
+  LAUNCH_CHECK("classify");
+  return LPP_OK;
+}
+
+// element access (_atomics.load_f64 / store_f64, _atomics.c:41-56)
+__global__ void k_load_f32(const float* p, float* out) {
+  float v;
+  asm volatile("ld.acquire.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  *out = v;
+}
+__global__ void k_store_f32(float* p, float v) {
+  asm volatile("st.release.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+namespace {
+struct HostScratch {  // per host thread: 16 bytes of mapped host memory
+  void* h = nullptr;
+  void* d = nullptr;
+  ~HostScratch() {
+    if (h) cudaFreeHost(h);
+  }
+};
+thread_local HostScratch g_scratch;
+}  // namespace
+
+extern "C" int lpp_load_f32(const float* arena, size_t len, size_t i, float* out, void* stream) {
+  if (!arena || !out) return set_err(LPP_E_VALUE, "load_f32: null buffer");
+  if (i >= len) return set_err(LPP_E_INDEX, "index %zu out of range [0, %zu)", i, len);
+  if (!g_scratch.h) {
+    CUDA_TRY(cudaHostAlloc(&g_scratch.h, 16, cudaHostAllocMapped | cudaHostAllocPortable));
+    CUDA_TRY(cudaHostGetDevicePointer(&g_scratch.d, g_scratch.h, 0));
+  }
+  k_load_f32<<<1, 1, 0, (cudaStream_t)stream>>>(arena + i, static_cast<float*>(g_scratch.d));
+  LAUNCH_CHECK("load_f32");
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  *out = *static_cast<volatile float*>(g_scratch.h);
+  return LPP_OK;
+}
+
+extern "C" int lpp_store_f32(float* arena, size_t len, size_t i, float v, void* stream) {
+  if (!arena) return set_err(LPP_E_VALUE, "store_f32: null buffer");
+  if (i >= len) return set_err(LPP_E_INDEX, "index %zu out of range [0, %zu)", i, len);
+  k_store_f32<<<1, 1, 0, (cudaStream_t)stream>>>(arena + i, v);
+  LAUNCH_CHECK("store_f32");
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return LPP_OK;
+}
+
+// host memory the kernels read and write directly (mapped, portable)
+extern "C" int lpp_host_alloc(size_t bytes, void** host, void** dev) {
+  if (!host || !dev) return set_err(LPP_E_VALUE, "host_alloc: null out");
+  *host = *dev = nullptr;
+  if (bytes == 0) bytes = 16;
+  CUDA_TRY(cudaHostAlloc(host, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(*host, 0, bytes);
+  cudaError_t e = cudaHostGetDevicePointer(dev, *host, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(*host);
+    *host = nullptr;
+    return set_err(LPP_E_CUDA, "cudaHostGetDevicePointer failed: %s", cudaGetErrorString(e));
+  }
+  return LPP_OK;
+}
+
+extern "C" int lpp_host_free(void* host) {
+  if (host) CUDA_TRY(cudaFreeHost(host));
   return LPP_OK;
 }
 
@@ -741,7 +934,7 @@ __global__ void __launch_bounds__(kThreads)
       size_t i = i0 + (size_t)u * stride;
       if (i < nvec) t[u] = ld_tag4(tags + head + 4 * i);
     }
-    fence_ar_gpu();
+    fence_ar_sys();  // tags may come from peer GPUs' owners (.sys stores)
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       size_t i = i0 + (size_t)u * stride;
@@ -763,7 +956,7 @@ __global__ void __launch_bounds__(kThreads)
     for (size_t k = threadIdx.x; k < nscalar; k += blockDim.x) {
       size_t e = k < head ? k : tail0 + (k - head);
       int tv = ld_tag(tags + e);
-      fence_ar_gpu();
+      fence_ar_sys();  // tags may come from peer GPUs' owners (.sys stores)
       float v = ld_cg(src + e);
       if (out) out[e] = v;
       if (out_tags) out_tags[e] = tv;

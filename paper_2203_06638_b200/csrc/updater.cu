@@ -237,7 +237,8 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   const bool tagged = c->tags != nullptr;
   const int K = tagged ? c->tag_pick : 0;
   if (K > 0 && (!c->tag_idx_pinned || !c->tag_idx_dev || !c->tag_out_dev || !c->tag_out_pinned ||
-                !c->classified || !c->clean))
+                !c->tag_out_host_dev || !c->claim_ring || !c->claim_ring_dev ||
+                !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean))
     return set_err(LPP_E_VALUE, "updater_run: tag sampling buffers missing");
   const int F = c->in_flight < 1 ? 1 : c->in_flight;
   const int depth = F + 2;
@@ -311,18 +312,18 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   uint64_t tag_state = c->tag_seed;
   *st = lpp_updater_stats{};
 
-  // a step's sampled tags live in slot t % depth; the gather for step t runs
-  // before its snapshot values are read (paramstore.py:108-112)
+  // a step's sampled tags live in slot t % depth (indices in host-mapped
+  // memory, read there by the kernels).  Unfused steps (and the first fused
+  // one) gather them before their snapshot values are read
+  // (paramstore.py:108-112); fused steps get them from the previous step's
+  // apply kernel, after that apply landed (engine.py:343-362 order)
+  auto draw_idx = [&](int slot) {
+    if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, c->tag_idx_pinned + (size_t)slot * K);
+  };
   auto gather = [&](int slot) -> int {
-    int64_t* hidx = c->tag_idx_pinned + (size_t)slot * K;
-    if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, hidx);  // else drawn in step order
-    int r;
-    if ((r = lpp_copy_async(c->tag_idx_dev, hidx, 8 * (size_t)K, stream)) != LPP_OK) return r;
-    if ((r = lpp_gather_tags(c->tags, c->tag_idx_dev, (size_t)K, c->tag_out_dev + (size_t)slot * K,
-                             stream)) != LPP_OK)
-      return r;
-    return lpp_copy_async(c->tag_out_pinned + (size_t)slot * K, c->tag_out_dev + (size_t)slot * K,
-                          4 * (size_t)K, stream);
+    const size_t o = (size_t)slot * K;
+    return lpp_gather_tags_floor(c->tags, c->tag_idx_dev + o, (size_t)K, c->avg_cell_dev,
+                                 c->tag_out_dev + o, c->tag_out_host_dev + o, stream);
   };
   // once a step's event completed: classify its tags, collect its apply time
   auto retire = [&](int k) -> int {
@@ -332,13 +333,16 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       *c->loss_count = i + 1;
     }
     if (K > 0) {
+      // (k_claim, clean) as the step's apply kernel saw them
       const int32_t* tg = c->tag_out_pinned + (size_t)slot_of[k] * K;
-      bool clean = true;
-      for (int j = 0; j < K; ++j) clean &= ((int64_t)tg[j] >= claim_of[k]);
+      const volatile int64_t* cr = c->claim_ring + 2 * (size_t)slot_of[k];
+      const int64_t kc = cr[0];
+      const bool clean = cr[1] != 0;
       __atomic_fetch_add(c->classified, 1, __ATOMIC_ACQ_REL);
       if (clean) __atomic_fetch_add(c->clean, 1, __ATOMIC_ACQ_REL);
       const int64_t ts = step_of[k];
       if (c->rec_i64 && ts < c->rec_cap) {
+        c->rec_i64[6 * ts + 2] = kc;
         c->rec_i64[6 * ts + 5] = clean ? 1 : 0;
         if (c->rec_tags)
           for (int j = 0; j < K; ++j) c->rec_tags[(size_t)ts * K + j] = tg[j];
@@ -370,7 +374,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       if ((rc = retire(k)) != LPP_OK) return rc;
     }
     const int slot = (int)(t % depth), next_slot = (int)((t + 1) % depth);
-    const int64_t k_claim = __atomic_load_n(c->last_avg_stamp, __ATOMIC_ACQUIRE);
+    // untagged runs record k_claim at enqueue; tagged ones take it from
+    // the apply kernel, which reads it after the gradient (engine.py:353)
+    const int64_t k_claim = K > 0 ? -1 : __atomic_load_n(c->last_avg_stamp, __ATOMIC_ACQUIRE);
     const int64_t u = __atomic_fetch_add(c->update_order, 1, __ATOMIC_ACQ_REL) + 1;
     if (c->rec_i64 && t < c->rec_cap) {
       int64_t* row = c->rec_i64 + 6 * t;
@@ -424,7 +430,10 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       CUDA_TRY(cudaStreamWaitEvent(stream, copied.ev[slot], 0));
     }
     if (!c->fused || t == 0) {
-      if (K > 0 && (rc = gather(slot)) != LPP_OK) return rc;
+      if (K > 0) {
+        if (!c->fused || !c->host_rng) draw_idx(slot);
+        if ((rc = gather(slot)) != LPP_OK) return rc;                               // K5
+      }
       if ((rc = lpp_snapshot(c->x, c->replica, c->n, stream)) != LPP_OK) return rc;   // K3
     }
     if ((rc = lpp_graph_launch(c->graph_exec[2 * b + buf], stream)) != LPP_OK) return rc;  // fwd+bwd
@@ -432,19 +441,35 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if (c->read_loss)
       CUDA_TRY(cudaMemcpyAsync(c->loss_pinned + slot, c->loss_dev[buf], sizeof(float),
                                cudaMemcpyDeviceToHost, stream));
-    if (c->fused && K > 0 && (rc = gather(next_slot)) != LPP_OK) return rc;          // K5 (next)
+    if (c->fused && K > 0) draw_idx(next_slot);         // read by this step's apply kernel
     if (side) {  // the apply on its own (high-priority) stream, after the graph
       CUDA_TRY(cudaEventRecord(order.ev[0], stream));
       CUDA_TRY(cudaStreamWaitEvent(astream, order.ev[0], 0));
     }
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t0.ev[k], astream));
-    if (c->fused) {
+    if (c->fused && K > 0) {
+      // K1+K3 + K5: classify this step, stamp, gather the next step's tags
+      const size_t o = (size_t)slot * K, on = (size_t)next_slot * K;
+      lpp_tag_plan plan{c->tag_idx_dev + on, c->tag_out_dev + on, c->tag_out_host_dev + on,
+                        c->tag_out_dev + o, c->claim_ring_dev + 2 * (size_t)slot, c->avg_cell_dev,
+                        c->done_ctr, K};
+      rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, c->tags, c->n, (size_t)lo,
+                                   (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u, &plan,
+                                   astream);
+      bytes_of[k] = c->apply_bytes_per_elem * (double)len + 4.0 * (double)(c->n - len) +
+                    4.0 * (double)c->n;
+    } else if (c->fused) {
       rc = lpp_apply_snapshot(c->x, c->g, c->m, c->replica, tagged ? c->tags : nullptr, c->n,
                               (size_t)lo, (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u,
                               astream);                                               // K1+K3
       bytes_of[k] = c->apply_bytes_per_elem * (double)len + 4.0 * (double)(c->n - len) +
                     4.0 * (double)c->n;
     } else if (tagged) {
+      if (K > 0) {  // k_claim after the gradient, on the apply's stream
+        rc = lpp_classify(c->tag_out_dev + (size_t)slot * K, (size_t)K, c->avg_cell_dev,
+                          c->claim_ring_dev + 2 * (size_t)slot, astream);
+        if (rc != LPP_OK) return rc;
+      }
       rc = lpp_apply_sgd_tagged(c->x + lo, c->g + lo, c->m ? c->m + lo : nullptr, (size_t)len,
                                 lr32, nullptr, c->mu, c->wd, c->apply_mode, c->tags + lo,
                                 (int32_t)u, astream);                                 // K1/K2+K5
@@ -493,14 +518,14 @@ inline double now_s() {
 }
 
 // RoundControl layout (rounds.py)
-constexpr int64_t kHeader = 16, kStamps = 8;
+constexpr int64_t kHeader = 16, kStamps = 8, kRing = 8;   // rounds.RoundControl.RING
 inline int64_t* cell(const lpp_averager_cfg* c, int64_t i) { return c->ctrl + i; }
-inline int64_t* vote_cell(const lpp_averager_cfg* c, int64_t r) { return cell(c, kHeader + r); }
+inline int64_t* vote_cell(const lpp_averager_cfg* c, int64_t r) { return cell(c, kHeader + r % kRing); }
 inline int64_t* final_cell(const lpp_averager_cfg* c, int64_t r) {
-  return cell(c, kHeader + c->max_rounds + 2 + r);
+  return cell(c, kHeader + kRing + r % kRing);
 }
 inline int64_t* fence_cell(const lpp_averager_cfg* c, int which, int64_t r) {
-  return cell(c, kHeader + (2 + which) * (c->max_rounds + 2) + r);
+  return cell(c, kHeader + (2 + which) * kRing + r % kRing);
 }
 inline int64_t ld(const int64_t* p) { return __atomic_load_n(p, __ATOMIC_ACQUIRE); }
 inline void st(int64_t* p, int64_t v) { __atomic_store_n(p, v, __ATOMIC_RELEASE); }
@@ -541,7 +566,11 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
     return set_err(LPP_E_VALUE, "averager_run: eval buffers missing");
   int64_t next_eval = c->eval_interval;
   if (evalm) *c->eval_count = 0;
-  const bool fenced = c->tagged || evalm;
+  // fence 0: every worker's stamp is published before owners write tags;
+  // fence 1: every owner is done with this worker's arena before the round
+  // counts as applied (last_avg_stamp: the updaters' k_claim and tag floor)
+  const bool fenced0 = c->tagged;
+  const bool fenced1 = c->tagged || evalm || c->stamp_floor;
   const bool timed = c->time_rounds && c->k4_ms && c->k4_rounds && Q > 1;
   cudaEvent_t k4a = nullptr, k4b = nullptr;
   struct EvPair {
@@ -587,17 +616,13 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
     backoff = 0.0;
     const int64_t r = round_no + 1;
     // vote (rounds.RoundControl.vote)
-    if (r > c->max_rounds) {
-      fail(LPP_E_INDEX);
-      return set_err(LPP_E_INDEX, "averaging round budget of the control block exceeded");
-    }
     if (drain) add(final_cell(c, r), 1);
     add(vote_cell(c, r), 1);
     // do_round: this worker's share of round r
     const int64_t u = add(c->update_order, 1) + 1;
     bool ok = true;
     int32_t stamps[LPP_MAX_WORKERS] = {0};
-    if (fenced) {
+    if (fenced0) {
       st(cell(c, kStamps + c->q), u);
       add(fence_cell(c, 0, r), 1);
       ok = wait_ge(fence_cell(c, 0, r), Q);
@@ -631,7 +656,7 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
           *c->k4_rounds += 1;
         }
       }
-      if (fenced) {
+      if (fenced1) {
         add(fence_cell(c, 1, r), 1);
         ok = wait_ge(fence_cell(c, 1, r), Q);
       }
@@ -643,6 +668,12 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
     // wait for every worker's vote (rounds.RoundControl.wait_votes)
     if (!wait_ge(vote_cell(c, r), Q)) break;
     const bool unanimous = ld(final_cell(c, r)) == Q;
+    if (r > 1) {  // rounds.RoundControl.release: round r - 1's cells are free
+      st(vote_cell(c, r - 1), 0);
+      st(final_cell(c, r - 1), 0);
+      st(fence_cell(c, 0, r - 1), 0);
+      st(fence_cell(c, 1, r - 1), 0);
+    }
     round_no = r;
     if (c->stop_after > 0 && round_no >= c->stop_after) st(stop, 1);
     if (c->rec && round_no <= c->max_records) {

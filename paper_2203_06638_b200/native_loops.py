@@ -109,10 +109,17 @@ class NativeLoops:
         c.time_apply = int(self.time_apply)
         c.tag_seed = (cfg.seed * 1_000_003 + w.q * 1009 + r + 1) & (2**64 - 1)
         if tracks:
-            c.tag_idx_pinned = w.tag_idx_pinned[r].data_ptr()
-            c.tag_idx_dev = w.tag_idx_dev[r].data_ptr()
+            # K5 rings in host-mapped memory (indices, effective tags, the
+            # apply kernels' (k_claim, clean) records) + the device tag ring
+            c.tag_idx_dev = w.idx_dev(r, 0)
+            c.tag_idx_pinned = w.host_addr(c.tag_idx_dev)
             c.tag_out_dev = w.tag_out_dev[r].data_ptr()
-            c.tag_out_pinned = w.tag_pinned[r].data_ptr()
+            c.tag_out_host_dev = w.tag_host_dev(r, 0)
+            c.tag_out_pinned = w.host_addr(c.tag_out_host_dev)
+            c.claim_ring_dev = w.claim_dev(r, 0)
+            c.claim_ring = w.host_addr(c.claim_ring_dev)
+            c.avg_cell_dev = w.avg_dev
+            c.done_ctr = w.done_ctr[r].data_ptr()
         c.classified = self.classified_count._a
         c.clean = self.clean_count._a
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
@@ -226,15 +233,20 @@ class NativeLoops:
         try:
             arenas = (ctypes.c_void_p * Q)(*self.arena_ptrs)
             tags = (ctypes.c_void_p * Q)(*self.tag_ptrs) if self.tag_ptrs is not None else None
-            cap = min(ctrl.max_rounds, 1 << 20)
+            # per-round records: at most one round per slot claimed (+ drain)
+            cap = Q * (self.budget + cfg.updaters) + 8
+            if cfg.round_budget is not None:
+                cap = min(cap, cfg.round_budget + 8)
+            cap = min(cap, 1 << 20)
             rec = np.zeros((cap, 5), dtype=np.int64)
             wall = np.zeros(cap, dtype=np.float64)
             lo, hi = self.shards[q]
             c = N.AveragerCfg()
             c.ctrl = ctrl.buf.ctypes.data
-            c.max_rounds = ctrl.max_rounds
+            c.max_rounds = 0
             c.workers, c.q, c.updaters = Q, q, cfg.updaters
             c.tagged = int(self.tag_ptrs is not None)
+            c.stamp_floor = int(cfg.tracks)
             c.sample_counter = w.store.sample_counter._a
             c.update_order = w.store.update_order_counter._a
             c.exited = w.exited._a

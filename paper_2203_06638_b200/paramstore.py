@@ -112,16 +112,19 @@ class ParamStore:
 
     # -- element access ---------------------------------------------------
 
-    def read(self, index: int) -> float:
+    def read(self, index: int, stream: torch.cuda.Stream | None = None) -> float:
+        """One element, acquire-loaded (``_atomics.load_f64``, _atomics.c:41-48)."""
         if not 0 <= index < self.dim:
             raise IndexError(f"index {index} out of range [0, {self.dim})")
-        return float(self.arena.tensor[index].item())
+        with torch.cuda.device(self.device):
+            return N.load_f32(self.arena.ptr, self.dim, int(index), stream_ptr(stream))
 
-    def write(self, index: int, value: float) -> None:
+    def write(self, index: int, value: float, stream: torch.cuda.Stream | None = None) -> None:
+        """One element, release-stored (``_atomics.store_f64``, _atomics.c:50-56)."""
         if not 0 <= index < self.dim:
             raise IndexError(f"index {index} out of range [0, {self.dim})")
-        self.arena.tensor[index] = value
-        torch.cuda.synchronize(self.device)
+        with torch.cuda.device(self.device):
+            N.store_f32(self.arena.ptr, self.dim, int(index), float(value), stream_ptr(stream))
 
     # -- counters -----------------------------------------------------------
 
@@ -178,6 +181,10 @@ class ParamStore:
     def _accum(self, start: int, delta, scale: float, stamp: int, stream) -> None:
         d = _as_device_f32(delta, self.device)
         n = d.numel()
+        if stream is not None:
+            # `d` was produced (uploaded / converted) on the current stream:
+            # the kernel on `stream` must not read it before that finished
+            stream.wait_stream(torch.cuda.current_stream(self.device))
         if start < 0 or start + n > self.dim:
             raise IndexError("update range out of bounds")
         mode = self.mode if self.mode != N.MODE_BULK else N.MODE_RED

@@ -60,17 +60,28 @@ class RoundControl:
     layout: [0] round_calls  [1] stop  [2] abort  [3] drained workers
             [8 : 16]  each worker's update-order stamp for the current round
                       (the owners write it into every arena's tags, K5)
-            then four per-round arrays of R+2 cells: vote count, final-vote
-            count, and the two fences (all published/paused; all shards done)
+            then four arrays of RING cells, indexed by round mod RING: vote
+            count, final-vote count, and the two fences (stamps published /
+            quiescent; every owner's shard done)
+
+    Rounds run in lock step (a worker votes in round r + 1 only after all Q
+    votes of round r are in), so round r's cells are free again once all
+    votes of round r + 1 are in: ``release(r + 1)`` zeroes them, and with
+    RING >= 3 they are zero before round r + RING can use them.  Any number
+    of rounds fits in a fixed-size block (no per-run round ceiling).
     """
 
     HEADER = 16
     STAMPS = 8
+    RING = 8
+    ARRAYS = 4
 
-    def __init__(self, workers: int, max_rounds: int, buf: np.ndarray | None = None):
+    def __init__(self, workers: int, max_rounds: int | None = None, buf: np.ndarray | None = None):
         self.workers = int(workers)
-        self.max_rounds = int(max_rounds)
-        n = self.cells(max_rounds)
+        # a capacity hint for per-round records only; the block is a ring
+        self.max_rounds = None if max_rounds is None else int(max_rounds)
+        self.ring = self.RING
+        n = self.cells()
         if buf is None:
             buf = np.zeros(n, dtype=np.int64)
         if buf.dtype != np.int64 or buf.shape[0] < n:
@@ -81,15 +92,13 @@ class RoundControl:
         self.abort = _Cell(buf, 2)
         self.drained = _Cell(buf, 3)
 
-    ARRAYS = 4
+    @staticmethod
+    def cells(max_rounds: int | None = None) -> int:
+        return RoundControl.HEADER + RoundControl.ARRAYS * RoundControl.RING
 
     @staticmethod
-    def cells(max_rounds: int) -> int:
-        return RoundControl.HEADER + RoundControl.ARRAYS * (int(max_rounds) + 2)
-
-    @staticmethod
-    def nbytes(max_rounds: int) -> int:
-        return 8 * RoundControl.cells(max_rounds)
+    def nbytes(max_rounds: int | None = None) -> int:
+        return 8 * RoundControl.cells()
 
     def publish_stamp(self, q: int, u: int) -> None:
         N.atomic_store(self.buf, self.STAMPS + q, u)
@@ -97,11 +106,14 @@ class RoundControl:
     def stamps(self) -> list[int]:
         return [N.atomic_load(self.buf, self.STAMPS + q) for q in range(self.workers)]
 
+    def _vote_cell(self, r: int) -> int:
+        return self.HEADER + r % self.RING
+
     def _final_cell(self, r: int) -> int:
-        return self.HEADER + self.max_rounds + 2 + r
+        return self.HEADER + self.RING + r % self.RING
 
     def _fence_cell(self, which: int, r: int) -> int:
-        return self.HEADER + (2 + which) * (self.max_rounds + 2) + r
+        return self.HEADER + (2 + which) * self.RING + r % self.RING
 
     def fence(self, which: int, r: int) -> bool:
         """Group-wide barrier number ``which`` (0/1) of round r; False on abort."""
@@ -110,21 +122,28 @@ class RoundControl:
         return N.atomic_wait_ge(self.buf, c, self.workers, self.buf, 2) is not None
 
     def vote(self, r: int, final: bool) -> None:
-        if r > self.max_rounds:
-            self.abort.store(1)
-            raise RuntimeError("averaging round budget of the control block exceeded")
         if final:
             N.atomic_fetch_add(self.buf, self._final_cell(r), 1)
-        N.atomic_fetch_add(self.buf, self.HEADER + r, 1)
+        N.atomic_fetch_add(self.buf, self._vote_cell(r), 1)
 
     def wait_votes(self, r: int) -> bool | None:
         """Block (GIL released) until all workers voted in round r.
 
         Returns whether the round was unanimously final; None on abort."""
-        got = N.atomic_wait_ge(self.buf, self.HEADER + r, self.workers, self.buf, 2)
+        got = N.atomic_wait_ge(self.buf, self._vote_cell(r), self.workers, self.buf, 2)
         if got is None:
             return None
-        return N.atomic_load(self.buf, self._final_cell(r)) == self.workers
+        unanimous = N.atomic_load(self.buf, self._final_cell(r)) == self.workers
+        self.release(r)
+        return unanimous
+
+    def release(self, r: int) -> None:
+        """All votes of round r are in, so nobody reads round r - 1's cells
+        any more: zero them for round r - 1 + RING (idempotent)."""
+        if r > 1:
+            for c in (self._vote_cell(r - 1), self._final_cell(r - 1), self._fence_cell(0, r - 1),
+                      self._fence_cell(1, r - 1)):
+                N.atomic_store(self.buf, c, 0)
 
 
 def averager_loop(ctrl: RoundControl, *, workers: int, read_counter, local_drained, sync_period,

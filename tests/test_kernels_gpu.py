@@ -498,3 +498,191 @@ def test_no_kernel_writes_outside_its_range(N, n):
             torch.cuda.synchronize()
             for b, f in ((x, S), (g, S), (m, S), (r, S), (t, T)):
                 assert _guards_intact(b, f), (n, "fused")
+
+
+# ---------------------------------------------------------------------------
+# K5 in the reference's order (lpp_tag_plan), the round floor, element access
+
+
+def _plan_setup(N, n, k, depth=3):
+    from paper_2203_06638_b200.arena import Arena
+
+    hb = N.HostBuffer(64 + 8 * depth * k + 4 * depth * k + 16 * depth)
+    avg = hb.view(np.int64, (1,))
+    idx = hb.view(np.int64, (depth, k), 64)
+    tag_host = hb.view(np.int32, (depth, k), 64 + 8 * depth * k)
+    claim = hb.view(np.int64, (depth, 2), 64 + 12 * depth * k)
+    dev = {"avg": hb.dev, "idx": hb.dev + 64, "tag_host": hb.dev + 64 + 8 * depth * k,
+           "claim": hb.dev + 64 + 12 * depth * k}
+    tag_dev = torch.zeros((depth, k), dtype=torch.int32, device="cuda")
+    done = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tags = Arena(n, 0)
+    return hb, avg, idx, tag_host, claim, dev, tag_dev, done, tags
+
+
+@pytest.mark.parametrize("n,lo,hi", [(4099, 0, 4099), (100_003, 1001, 77_777), (1_000_001, 3, 999_998)])
+def test_apply_snapshot_plan_values_tags_classification_and_next_gather(N, orc, n, lo, hi):
+    """The plan variant updates values exactly like the fused kernel, stamps
+    the block, classifies this step against the round-stamp cell read in the
+    kernel, and gathers the next step's sampled tags AFTER its own stamps
+    landed (elements inside the block come back with this step's stamp),
+    raised to the floor."""
+    from paper_2203_06638_b200.arena import Arena
+
+    k = 16
+    hb, avg, idx, tag_host, claim, dev, tag_dev, done, tags = _plan_setup(N, n, k)
+    gen = np.random.default_rng(n)
+    x = gen.normal(size=n).astype(np.float32)
+    g = (1e-2 * gen.normal(size=n)).astype(np.float32)
+    m = gen.normal(size=n).astype(np.float32)
+    ax, ag, am, ar = (Arena(n, 0) for _ in range(4))
+    ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g)), am.tensor.copy_(_cuda(m))
+    t0 = gen.integers(0, 50, size=n).astype(np.int32)
+    tags.tensor.view(torch.int32).copy_(_cuda(t0))
+    # this step's tags (slot 0): two cases of k_claim
+    tag_dev[0] = torch.tensor(np.arange(10, 10 + k), dtype=torch.int32)
+    avg[0] = 12                                  # k_claim 12 > 10 = min tag -> dirty
+    inside = np.sort(gen.choice(np.arange(lo, hi), size=k // 2, replace=False))
+    outside = np.sort(gen.choice(np.r_[0:lo, hi:n] if lo or hi < n else np.arange(n), size=k - k // 2,
+                                 replace=False))
+    idx[1] = np.sort(np.r_[inside, outside])
+    plan = N.TagPlan(dev["idx"] + 8 * k, tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
+                     tag_dev[0].data_ptr(), dev["claim"], dev["avg"], done.data_ptr(), k)
+    stamp = 40
+    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, tags.ptr, n, lo, hi, 0.05, None, 0.9,
+                          5e-4, stamp, plan, 0)
+    torch.cuda.synchronize()
+    xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
+    orc.apply_sgd(xv, g[lo:hi].copy(), mv, 0.05, 0.9, 5e-4)
+    want = x.copy()
+    want[lo:hi] = xv
+    assert np.array_equal(ax.tensor.cpu().numpy(), want)
+    assert np.array_equal(ar.tensor.cpu().numpy(), want)
+    t = tags.tensor.view(torch.int32).cpu().numpy()
+    assert (t[lo:hi] == stamp).all() and np.array_equal(t[:lo], t0[:lo]) and np.array_equal(t[hi:], t0[hi:])
+    assert list(claim[0]) == [12, 0]
+    want_next = np.maximum(t[idx[1]], 12)
+    assert np.array_equal(tag_host[1], want_next)
+    assert np.array_equal(tag_dev[1].cpu().numpy(), want_next)
+    assert int(done.item()) == 0                  # counter reset for the next launch
+    # second launch: clean (k_claim = 10 <= every tag), floor raises old tags
+    avg[0] = 10
+    plan2 = N.TagPlan(dev["idx"] + 16 * k, tag_dev[2].data_ptr(), dev["tag_host"] + 8 * k,
+                      tag_dev[0].data_ptr(), dev["claim"] + 16, dev["avg"], done.data_ptr(), k)
+    idx[2] = np.arange(k) * (n // k)
+    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, tags.ptr, n, lo, hi, 0.0, None, 0.0,
+                          0.0, stamp + 1, plan2, 0)
+    torch.cuda.synchronize()
+    assert list(claim[1]) == [10, 1]
+    t = tags.tensor.view(torch.int32).cpu().numpy()
+    assert np.array_equal(tag_host[2], np.maximum(t[idx[2]], 10))
+    for a in (ax, ag, am, ar, tags):
+        a.close()
+    hb.close()
+
+
+def test_apply_snapshot_plan_concurrent_streams_gather_sees_own_apply(N):
+    """4 streams x 30 fused steps, each gathering the next step's tags at
+    elements of its own block: a gathered tag is never older than the stamp
+    the same stream just wrote there (the gather follows the apply)."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, k, K, steps = 200_003, 8, 4, 30
+    x = Arena(n, 0)
+    g = torch.full((n,), -1.0, device="cuda")
+    tags = Arena(n, 0)
+    reps = [Arena(n, 0) for _ in range(K)]
+    streams = [torch.cuda.Stream() for _ in range(K)]
+    hb = N.HostBuffer(64 + K * (8 * k + 4 * k + 16) * steps)
+    avg = hb.view(np.int64, (1,))
+    avg[0] = 0
+    idx = hb.view(np.int64, (K, steps, k), 64)
+    o_tag = 64 + 8 * K * steps * k
+    tag_host = hb.view(np.int32, (K, steps, k), o_tag)
+    tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
+    done = torch.zeros(K, dtype=torch.int32, device="cuda")
+    bounds = np.linspace(0, n, K + 1).astype(np.int64)
+    gen = np.random.default_rng(5)
+    for s in range(K):
+        for t in range(steps):
+            idx[s, t] = np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k, replace=False))
+    torch.cuda.synchronize()
+    for t in range(steps):
+        for s, st in enumerate(streams):
+            stamp = 1000 * (s + 1) + t
+            plan = N.TagPlan(hb.dev + 64 + 8 * k * (s * steps + t), tag_dev[s, t].data_ptr(),
+                             hb.dev + o_tag + 4 * k * (s * steps + t), None, None, hb.dev,
+                             done[s].data_ptr(), k)
+            N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, tags.ptr, n,
+                                  int(bounds[s]), int(bounds[s + 1]), 1.0, None, 0.0, 0.0, stamp,
+                                  plan, st.cuda_stream)
+    torch.cuda.synchronize()
+    assert bool((x.tensor == float(steps)).all())
+    for s in range(K):
+        for t in range(steps):
+            assert (tag_host[s, t] == 1000 * (s + 1) + t).all(), (s, t)
+    for a in [x, tags] + reps:
+        a.close()
+    hb.close()
+
+
+def test_gather_floor_and_classify(N):
+    from paper_2203_06638_b200.arena import Arena
+
+    n, k = 5000, 16
+    tags = Arena(n, 0)
+    t = np.arange(n, dtype=np.int32) % 97
+    tags.tensor.view(torch.int32).copy_(_cuda(t))
+    hb = N.HostBuffer(64 + 8 * k + 4 * k + 16)
+    avg = hb.view(np.int64, (1,))
+    idx = hb.view(np.int64, (k,), 64)
+    out_host = hb.view(np.int32, (k,), 64 + 8 * k)
+    rec = hb.view(np.int64, (2,), 64 + 12 * k)
+    out_dev = torch.zeros(k, dtype=torch.int32, device="cuda")
+    idx[:] = np.arange(0, 300 * k, 300)
+    avg[0] = 40
+    N.gather_tags_floor(tags.ptr, hb.dev + 64, k, hb.dev, out_dev.data_ptr(), hb.dev + 64 + 8 * k, 0)
+    torch.cuda.synchronize()
+    want = np.maximum(t[idx], 40)
+    assert np.array_equal(out_host, want) and np.array_equal(out_dev.cpu().numpy(), want)
+    N.classify(out_dev.data_ptr(), k, hb.dev, hb.dev + 64 + 12 * k, 0)
+    torch.cuda.synchronize()
+    assert list(rec) == [40, 1]
+    avg[0] = 41
+    N.classify(out_dev.data_ptr(), k, hb.dev, hb.dev + 64 + 12 * k, 0)
+    torch.cuda.synchronize()
+    assert list(rec) == [41, int((want >= 41).all())]
+    # no floor: the raw tags
+    N.gather_tags_floor(tags.ptr, hb.dev + 64, k, None, out_dev.data_ptr(), None, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(out_dev.cpu().numpy(), t[idx])
+    with pytest.raises(ValueError):
+        N.gather_tags_floor(tags.ptr, hb.dev + 64, k, None, None, None, 0)
+    tags.close()
+    hb.close()
+
+
+def test_element_load_store_f32(N):
+    """lpp_load_f32 / lpp_store_f32 (_atomics.load_f64 / store_f64 counterparts)
+    and ParamStore.read / write through them."""
+    from paper_2203_06638_b200.arena import Arena
+    from paper_2203_06638_b200.paramstore import ParamStore
+
+    a = Arena(1000, 0)
+    a.tensor.copy_(torch.arange(1000, dtype=torch.float32))
+    assert N.load_f32(a.ptr, 1000, 7) == 7.0
+    N.store_f32(a.ptr, 1000, 999, -2.5)
+    assert float(a.tensor[999]) == -2.5
+    with pytest.raises(IndexError):
+        N.load_f32(a.ptr, 1000, 1000)
+    with pytest.raises(IndexError):
+        N.store_f32(a.ptr, 1000, 1000, 1.0)
+    a.close()
+    st = ParamStore(np.array([1.0, 2.0, 3.0, 4.0]))
+    st.write(2, 23.0)
+    assert st.read(2) == 23.0 and st.read(0) == 1.0
+    with pytest.raises(IndexError):
+        st.read(4)
+    s = torch.cuda.Stream()
+    st.write(1, 12.0, stream=s)
+    assert st.read(1, stream=s) == 12.0
