@@ -289,7 +289,8 @@ def ours(args) -> None:
     if tp.exists():
         launches_ = json.loads(tp.read_text())["launches"]
         name = "void k_apply_snapshot<" if fused else "void k_apply<1, 1, 1>"
-        cands = [e for e in launches_ if e["kernel"].startswith(name) and e.get("params", dim20) == dim20]
+        grid20 = min(-(-(dim20 // 4) // 256), 148 * 16)     # the launch's grid at d20
+        cands = [e for e in launches_ if e["kernel"].startswith(name) and e["grid"] == grid20]
         traffic = sum(e["dram_bytes"] for e in cands) / len(cands) if cands else None
         floor = [e["us"] for e in launches_ if e["kernel"] == "k_gather_tags"]
         if cands:

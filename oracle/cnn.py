@@ -26,12 +26,18 @@ SHAPES = ((16, 3, 3, 3), (16,), (32, 16, 3, 3), (32,), (10, 512), (10,))
 LAYER_COUNTS = tuple(int(np.prod(s)) for s in SHAPES)
 
 
-def make_images(n: int, seed: int, n_classes: int = 10):
+def make_images(n: int, seed: int, n_classes: int = 10, pattern_scale: float = 0.0):
     """Synthetic CIFAR-shaped data: labels, then N(0,1) images, one torch CPU
-    generator seeded ``seed`` (the product's host-data generator)."""
+    generator seeded ``seed`` (the product's host-data generator); with
+    ``pattern_scale`` > 0 every image also gets its class's fixed random
+    pattern (a second generator seeded ``seed + 7919``) times the scale —
+    make_blobs (data.py:34-52) in image space, a learnable task."""
     g = torch.Generator().manual_seed(seed)
     labels = torch.randint(0, n_classes, (n,), generator=g)
     images = torch.randn(n, 3, 32, 32, generator=g)
+    if pattern_scale:
+        pg = torch.Generator().manual_seed(seed + 7919)
+        images += (torch.randn(n_classes, 3, 32, 32, generator=pg) * pattern_scale)[labels]
     return images.double().numpy(), labels.numpy()
 
 

@@ -705,6 +705,42 @@ def test_async_loss_band_vs_reference_async_runs():
     assert all(lo <= f <= hi for f in finals), (finals, ref["final"])
 
 
+def test_async_cnn_band_vs_reference_async_runs():
+    """North star on BASELINE config 0 itself: the small CNN, LPP-SGD Q=2
+    workers x U=2 updaters, 2-block partial backprop, async.  The reference's
+    own engine driving the small CNN (tests/golden/async_band_cnn.json, made
+    by tests/golden/make_cnn_band.py: 5 seeds of live-thread runs) against
+    the GPU engine's default async path (native loops, fused K1+K3 with the
+    K5 plan, fp32) on the same data, x0 and seeds.  Band: every GPU final
+    loss inside the reference's [min, max] widened by 0.05 (~2 % of the
+    initial loss), the GPU mean inside [min, max]; initial losses (same x0,
+    fp32 vs fp64 forward) equal to 1e-4."""
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.objectives import ResNetObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    ref = json.loads((Path(__file__).parent / "golden" / "async_band_cnn.json").read_text())
+    obj = ResNetObjective("smallcnn", n_samples=ref["n_samples"], seed=ref["data_seed"],
+                          channels_last=False, autocast=None, data="host",
+                          pattern_scale=ref["pattern_scale"])
+    T, B, Q, U = ref["T"], ref["B"], ref["Q"], ref["U"]
+    finals = []
+    for seed, ref_init in zip(ref["seeds"], ref["initial"]):
+        cfg = RunConfig(algo="lpp_sgd", objective=obj, partition=make_partition(obj.dim, ref["bounds"]),
+                        lr=LrSchedule(kind="cosine", alpha0=0.05, total=T, warmup=T // 10, batch_local=B,
+                                      workers=Q, batch_base=B),
+                        sync=SyncScheme(total=T, period=16), budget=T, warm_start_budget=T // 10,
+                        workers=Q, updaters=U, batch_size=B, seed=seed, record_mode="light")
+        res = run_experiment(cfg)
+        assert abs(res.metrics[0].train_loss - ref_init) <= 1e-4
+        finals.append(res.metrics[-1].train_loss)
+    lo, hi = min(ref["final"]), max(ref["final"])
+    print(f"\ncnn async band: GPU finals {np.round(finals, 4)}  reference {np.round(ref['final'], 4)}")
+    assert all(lo - 0.05 <= f <= hi + 0.05 for f in finals), (finals, ref["final"])
+    assert lo <= float(np.mean(finals)) <= hi, (finals, ref["final"])
+
+
 def test_native_updater_failure_aborts_the_run():
     """The same contract with the native loops: one updater's failed
     lpp_updater_run sets abort / stop, the other native updaters and the

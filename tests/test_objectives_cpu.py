@@ -75,3 +75,16 @@ def test_smallcnn_objective_matches_oracle_layout_data_and_init():
     assert np.array_equal(obj.features.double().numpy(), X)
     assert np.array_equal(obj.labels.numpy(), y)
     assert np.array_equal(obj.init_params(5), SmallCnnOracle(X, y).init_params(5))
+
+
+def test_small_cnn_learnable_images_match_the_oracle_data():
+    """The config-0 band fixture's data (oracle.cnn.make_images with class
+    patterns) is the product's host dataset bit for bit."""
+    from oracle.cnn import make_images
+    from paper_2203_06638_b200.objectives import ResNetObjective
+
+    obj = ResNetObjective("smallcnn", n_samples=64, seed=3, channels_last=False, autocast=None,
+                          data="host", pattern_scale=0.3)
+    X, y = make_images(64, 3, pattern_scale=0.3)
+    assert np.array_equal(obj.labels.numpy(), y)
+    assert np.array_equal(obj.features.double().numpy(), X)

@@ -34,16 +34,24 @@ for d in (11_220_132, 25_557_032):
         N.apply_sgd_tagged(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, tg.ptr, 7, st)
     for a in (x, g, m, tg):
         a.close()
-# K1+K3 fused (the async default) at d20 and d50 with a partial block, + the K5 gather
+# K1+K3 fused (the async default) at d20 and d50 with a partial block: the
+# engine's launch, with the K5 plan (classify this step, stamp, gather the
+# next step's 16 tags in the last CTA) — and without tags for comparison
+hb = N.HostBuffer(4096)
+hb.view("int64", (16,), 64)[:] = range(0, 16 * 1000, 1000)
+dev_tags = torch.zeros(32, dtype=torch.int32, device="cuda")
+done = torch.zeros(1, dtype=torch.int32, device="cuda")
+plan = N.TagPlan(hb.dev + 64, dev_tags[16:].data_ptr(), hb.dev + 512, dev_tags[:16].data_ptr(),
+                 hb.dev + 1024, hb.dev, done.data_ptr(), 16)
 for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000)):
     x, g, m, rep, tg = (Arena(d, 0) for _ in range(5))
     x.tensor.normal_(), g.tensor.normal_()
-    idx = torch.randint(0, d, (16,), device="cuda")
-    out = torch.empty(16, dtype=torch.int32, device="cuda")
     for _ in range(2):
         flush()
-        N.gather_tags(tg.ptr, idx.data_ptr(), 16, out.data_ptr(), st)
-        N.apply_snapshot(x.ptr, g.ptr, m.ptr, rep.ptr, tg.ptr, d, lo, hi, 1e-3, None, 0.9, 5e-4, 3, st)
+        N.apply_snapshot_plan(x.ptr, g.ptr, m.ptr, rep.ptr, tg.ptr, d, lo, hi, 1e-3, None, 0.9, 5e-4,
+                              3, plan, st)
+        flush()
+        N.apply_snapshot(x.ptr, g.ptr, m.ptr, rep.ptr, None, d, lo, hi, 1e-3, None, 0.9, 5e-4, 3, st)
     for a in (x, g, m, rep, tg):
         a.close()
 d = 16_000_000
