@@ -543,8 +543,8 @@ def test_apply_snapshot_plan_values_tags_classification_and_next_gather(N, orc, 
     tag_dev[0] = torch.tensor(np.arange(10, 10 + k), dtype=torch.int32)
     avg[0] = 12                                  # k_claim 12 > 10 = min tag -> dirty
     inside = np.sort(gen.choice(np.arange(lo, hi), size=k // 2, replace=False))
-    outside = np.sort(gen.choice(np.r_[0:lo, hi:n] if lo or hi < n else np.arange(n), size=k - k // 2,
-                                 replace=False))
+    pool = np.r_[0:lo, hi:n] if lo or hi < n else np.arange(n)
+    outside = np.sort(gen.choice(pool, size=k - k // 2, replace=len(pool) < k - k // 2))
     idx[1] = np.sort(np.r_[inside, outside])
     plan = N.TagPlan(dev["idx"] + 8 * k, tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
                      tag_dev[0].data_ptr(), dev["claim"], dev["avg"], done.data_ptr(), k)
