@@ -143,8 +143,10 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
  *       stores, i.e. at the next step's snapshot; the floor *avg_cell is
  *       the worker's last completed round stamp, which a round writes
  *       into every element (engine.py:421)        (next_idx may be NULL)
- * avg_cell, next_idx, next_host, cur_claim may point into host memory from
- * lpp_host_alloc (the kernel reads / writes it directly).  done: a 4-byte
+ * avg_cell is the worker's DEVICE round-stamp cell (lpp_set_i64 by the
+ * averager once a round is applied; host memory would put a PCIe round trip
+ * on the kernel's tail); next_host / cur_claim may point into lpp_host_alloc
+ * memory (posted writes the host reads after the step's event).  done: a 4-byte
  * device counter, zero before the first launch, private to the stream (the
  * last CTA resets it).  Write tags: every thread issues all of its
  * reductions, one fence.acq_rel.gpu, then the tags of the same elements. */
@@ -230,6 +232,8 @@ int lpp_gather_tags(const int32_t* tags, const int64_t* idx, size_t k, int32_t* 
 int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
                           const int64_t* floor_cell, int32_t* out_dev, int32_t* out_host,
                           void* stream);
+/* *dev = v in stream order (the round-stamp cell the apply kernels read) */
+int lpp_set_i64(int64_t* dev, int64_t v, void* stream);
 /* classification at apply time (engine.py:353-362) for the unfused paths:
  * out[0] = *claim_cell read when the kernel runs, out[1] = all k tags >= it */
 int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_cell, int64_t* out,
@@ -454,15 +458,15 @@ typedef struct {
   int64_t epoch_seed;             /* < 0: i.i.d. draws */
   int64_t* idx_pinned;            /* [in_flight + 2][batch] */
   int64_t* idx_dev;               /* [batch] */
-  /* K5 in the reference's order (lpp_tag_plan): with claim_ring != NULL the
-   * sampled-tag indices live in host-mapped memory (tag_idx_pinned, device
-   * view tag_idx_dev, [in_flight + 2][tag_pick]) and the kernels read them
-   * there; the effective tags go to tag_out_dev and the host-mapped
-   * tag_out_pinned (device view tag_out_host_dev); each step's (k_claim,
-   * clean) is written by its apply kernel into claim_ring[slot] (device
-   * view claim_ring_dev), k_claim read from avg_cell_dev (the device view
-   * of last_avg_stamp, which then must be host-mapped); done_ctr: a 4-byte
-   * zeroed device counter private to this updater */
+  /* K5 in the reference's order (lpp_tag_plan): the sampled-tag indices are
+   * drawn into the pinned ring tag_idx_pinned and copied (stream-ordered,
+   * before the step's graph) into the device ring tag_idx_dev, both
+   * [in_flight + 2][tag_pick]; the effective tags go to tag_out_dev and the
+   * host-mapped tag_out_pinned (device view tag_out_host_dev); each step's
+   * (k_claim, clean) is written by its apply kernel into the host-mapped
+   * claim_ring[slot] (device view claim_ring_dev), k_claim read from the
+   * worker's device round-stamp cell avg_cell_dev; done_ctr: a 4-byte zeroed
+   * device counter private to this updater */
   int64_t* claim_ring;            /* [in_flight + 2][2] host view */
   int64_t* claim_ring_dev;
   int32_t* tag_out_host_dev;
@@ -545,6 +549,9 @@ typedef struct {
    * counts as applied (last_avg_stamp) only after every owner is done with
    * this worker's arena (fence 1), with no per-element tag writes */
   int32_t stamp_floor;
+  /* the worker's device round-stamp cell (lpp_set_i64 before last_avg_stamp
+   * moves; NULL: none) */
+  int64_t* round_cell;
 } lpp_averager_cfg;
 
 int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);

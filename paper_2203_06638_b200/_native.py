@@ -104,7 +104,7 @@ class AveragerCfg(ctypes.Structure):
         ("eval_cap", _c.c_int64), ("eval_rec", _vp), ("eval_wall_ms", _vp), ("eval_count", _vp),
         ("flops_cell", _vp), ("classified_cell", _vp), ("clean_cell", _vp),
         ("time_rounds", _c.c_int32), ("k4_ms", _vp), ("k4_rounds", _vp),
-        ("stamp_floor", _c.c_int32),
+        ("stamp_floor", _c.c_int32), ("round_cell", _vp),
     ]
 
 
@@ -151,6 +151,7 @@ _SIGS = {
     ),
     "lpp_gather_tags_floor": (_c.c_int, [_vp, _vp, _size, _vp, _vp, _vp, _vp]),
     "lpp_classify": (_c.c_int, [_vp, _size, _vp, _vp, _vp]),
+    "lpp_set_i64": (_c.c_int, [_vp, _c.c_int64, _vp]),
     "lpp_host_alloc": (_c.c_int, [_size, _c.POINTER(_vp), _c.POINTER(_vp)]),
     "lpp_host_free": (_c.c_int, [_vp]),
     "lpp_load_f32": (_c.c_int, [_vp, _size, _size, _c.POINTER(_c.c_float), _vp]),
@@ -326,6 +327,10 @@ def gather_tags_floor(tags_ptr, idx_ptr, k, floor_ptr, out_dev_ptr, out_host_ptr
 
 def classify(tags_ptr, k, claim_ptr, out_ptr, stream) -> None:
     check(lib.lpp_classify(tags_ptr, k, claim_ptr, out_ptr, stream), "classify")
+
+
+def set_i64(dev_ptr: int, v: int, stream: int) -> None:
+    check(lib.lpp_set_i64(dev_ptr, int(v), stream), "set_i64")
 
 
 def load_f32(arena_ptr: int, length: int, i: int, stream: int = 0) -> float:

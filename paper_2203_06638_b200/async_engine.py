@@ -127,19 +127,24 @@ class _Worker:
         self.tag_pick = min(cfg.tag_sample, d)
         k = max(self.tag_pick, 1)
         self.kk = k
-        # host-mapped memory the kernels read / write directly (lpp_host_alloc):
-        # [0] last_avg_stamp — the worker's last completed round stamp, read by
-        # the apply kernels as k_claim and as the tag floor — then, per updater
-        # and in-flight slot, the sampled-tag indices (int64), the gathered
-        # effective tags (int32) and the apply's (k_claim, clean) record
-        self._o_idx = 64
-        self._o_tag = self._o_idx + 8 * U * depth * k
-        self._o_claim = self._o_tag + 4 * U * depth * k
+        # the worker's round-stamp cell on the device: the stamp of the last
+        # round applied to this arena, written by the averager (lpp_set_i64)
+        # before the host cell last_avg_stamp moves; the apply kernels read it
+        # as k_claim and as the tag floor
+        self.last_avg_stamp = AtomicCounter(0)
+        self.round_cell = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.avg_dev = self.round_cell.data_ptr()
+        # host-mapped memory the kernels write directly (lpp_host_alloc): per
+        # updater and in-flight slot, the gathered effective tags (int32) and
+        # the apply's (k_claim, clean) record; the sampled-tag indices are
+        # drawn into a pinned ring and copied to a device ring in stream order
+        self._o_tag = 0
+        self._o_claim = 4 * U * depth * k
         self.hostmem = N.HostBuffer(self._o_claim + 16 * U * depth)
-        self.last_avg_stamp = AtomicCounter(0, cell=self.hostmem.view(np.int64, (1,)), index=0)
-        self.avg_dev = self.hostmem.dev
         if cfg.tracks:
-            self.tag_idx_np = self.hostmem.view(np.int64, (U, depth, k), self._o_idx)
+            self.tag_idx_pinned = torch.zeros((U, depth, k), dtype=torch.long, pin_memory=True)
+            self.tag_idx_np = self.tag_idx_pinned.numpy()
+            self.tag_idx_ring = torch.zeros((U, depth, k), dtype=torch.long, device=self.dev)
             self.tag_np = self.hostmem.view(np.int32, (U, depth, k), self._o_tag)
             self.claim_np = self.hostmem.view(np.int64, (U, depth, 2), self._o_claim)
             self.tag_out_dev = torch.zeros((U, depth, k), dtype=torch.int32, device=self.dev)
@@ -156,20 +161,32 @@ class _Worker:
         self.idx_pinned = None
         self.batch_pinned = None
 
-    def idx_dev(self, r: int, slot: int) -> int:
-        depth = self.tag_idx_np.shape[1]
-        return self.avg_dev + self._o_idx + 8 * self.kk * (r * depth + slot)
+    def stage_idx(self, r: int, slot: int, idx, stream_ptr: int) -> int:
+        """Sampled-tag indices of (updater r, slot): pinned ring -> device
+        ring on ``stream_ptr``; returns the device address."""
+        k = self.tag_pick
+        self.tag_idx_np[r, slot, :k] = idx
+        N.copy_async(self.tag_idx_ring[r, slot].data_ptr(), self.tag_idx_pinned[r, slot].data_ptr(),
+                     8 * k, stream_ptr)
+        return self.tag_idx_ring[r, slot].data_ptr()
 
     def tag_host_dev(self, r: int, slot: int) -> int:
-        depth = self.tag_idx_np.shape[1]
-        return self.avg_dev + self._o_tag + 4 * self.kk * (r * depth + slot)
+        depth = self.tag_np.shape[1]
+        return self.hostmem.dev + self._o_tag + 4 * self.kk * (r * depth + slot)
 
     def claim_dev(self, r: int, slot: int) -> int:
-        depth = self.tag_idx_np.shape[1]
-        return self.avg_dev + self._o_claim + 16 * (r * depth + slot)
+        depth = self.tag_np.shape[1]
+        return self.hostmem.dev + self._o_claim + 16 * (r * depth + slot)
 
     def host_addr(self, dev_addr: int) -> int:
-        return self.hostmem.ptr + (dev_addr - self.avg_dev)
+        return self.hostmem.ptr + (dev_addr - self.hostmem.dev)
+
+    def publish_round(self, u: int, stream: torch.cuda.Stream) -> None:
+        """The round with stamp u is applied to this arena: device cell first
+        (the apply kernels' k_claim / tag floor), then the host cell."""
+        N.set_i64(self.avg_dev, u, stream.cuda_stream)
+        stream.synchronize()
+        self.last_avg_stamp.store(u)
 
     def build_programs(self, engine: "_Engine", block_ids_per_rank: list[list[int]]) -> None:
         cfg = engine.cfg
@@ -343,6 +360,7 @@ class _Engine(NativeLoops):
         self.clean_count.store(0)
         self.classified_count.store(0)
         for w in self.workers.values():
+            w.round_cell.zero_()
             if w.tags is not None:
                 w.tags.zero_()
         torch.cuda.synchronize()
@@ -468,10 +486,10 @@ class _Engine(NativeLoops):
         snapshot values it describes (paramstore.py:108-112).  The indices are
         written into host-mapped memory and read there by the kernel."""
         k = w.tag_pick
-        w.tag_idx_np[r, slot, :k] = tag_idx
-        N.gather_tags_floor(w.tag_arena.ptr, w.idx_dev(r, slot), k, w.avg_dev,
-                            w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot),
-                            w.streams[r].cuda_stream)
+        sp = w.streams[r].cuda_stream
+        idx_dev = w.stage_idx(r, slot, tag_idx, sp)
+        N.gather_tags_floor(w.tag_arena.ptr, idx_dev, k, w.avg_dev,
+                            w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
 
     def classify_on_device(self, w: _Worker, r: int, slot: int, stream_ptr: int) -> None:
         """K5 classification at apply time (engine.py:353-362): k_claim is
@@ -505,6 +523,7 @@ class _Engine(NativeLoops):
                 if tracks:
                     self.gather_tags(w, r, slot, tag_idx)
                 N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)          # K3
+            next_idx_dev = w.stage_idx(r, next_slot, next_tag_idx, sp) if tracks else None
             prog.run(block_id, buf)                                                      # fwd+bwd
             if self.host_batches:
                 w.buf_free[r][buf].record(stream)
@@ -514,8 +533,7 @@ class _Engine(NativeLoops):
                 # its gradient), stamp, and gather the next step's tags after
                 # this apply landed (engine.py:343-362 order)
                 k = w.tag_pick
-                w.tag_idx_np[r, next_slot, :k] = next_tag_idx
-                plan = N.TagPlan(w.idx_dev(r, next_slot), w.tag_out_dev[r, next_slot].data_ptr(),
+                plan = N.TagPlan(next_idx_dev, w.tag_out_dev[r, next_slot].data_ptr(),
                                  w.tag_host_dev(r, next_slot), w.tag_out_dev[r, slot].data_ptr(),
                                  w.claim_dev(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(), k)
             mom = w.moms[r]
@@ -762,7 +780,7 @@ class _Engine(NativeLoops):
                 if self.nvls:
                     self.nvls_round(q, u_of[r], final or full or evalm,
                                     fence=lambda i: self.ctrl.fence(i, r))
-                    w.last_avg_stamp.store(u_of[r])
+                    w.publish_round(u_of[r], w.avg_stream)
                     w.synced_at.store(s_cur)
                     if full:
                         snaps[r] = (snap, self.nvls[q].mean_tensor.clone() if q == 0 else None)
@@ -785,7 +803,7 @@ class _Engine(NativeLoops):
                     # (engine.py:441 keeps it for worker 0 only)
                     mean = self.gather_round_mean() if q == 0 else None
                     snaps[r] = (snap, mean)
-                w.last_avg_stamp.store(u_of[r])
+                w.publish_round(u_of[r], w.avg_stream)
                 w.synced_at.store(s_cur)
             finally:
                 if quiet:
@@ -964,7 +982,7 @@ class _Engine(NativeLoops):
                 for q in range(cfg.workers):
                     w = self.workers[q]
                     u_avg = u_avgs[q]
-                    w.last_avg_stamp.store(u_avg)
+                    w.publish_round(u_avg, w.avg_stream)
                     self.stamps[q].append(AveragerStamp(
                         worker=q, round=rnd, u=u_avg, s_cur=counts[q], k_delta=counts[q] - s_pre[q],
                         wall_ms=(time.perf_counter() - self.t0) * 1e3, snapshot=snaps[q],

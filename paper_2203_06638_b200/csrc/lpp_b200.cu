@@ -469,12 +469,12 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 //     engine.py:421 add_assign(..., stamp=u_avg): the floor stands for it).
 
 struct TagPlanDev {
-  const int64_t* next_idx;  // k sampled indices of the next step (host-mapped)
+  const int64_t* next_idx;  // k sampled indices of the next step
   int* next_dev;            // -> the next step's effective tags (device ring slot)
   int* next_host;           // -> and a host-mapped copy for the records (may be null)
   const int* cur_dev;       // this step's effective tags (gathered at its snapshot)
   int64_t* cur_claim;       // -> this step's (k_claim, clean) (host-mapped; may be null)
-  const int64_t* avg_cell;  // the worker's last completed round stamp (host-mapped)
+  const int64_t* avg_cell;  // the worker's last completed round stamp (device cell)
   unsigned* done;           // CTA completion counter (device, 0 between launches)
   int k;
 };
@@ -620,6 +620,12 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
   }
   size_t nvec = n / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
+  // experiment hook: LPP_FUSED_CTAS caps the grid (tools/exp_insitu_grid.py)
+  static const long cap_env = [] {
+    const char* e = std::getenv("LPP_FUSED_CTAS");
+    return e ? std::atol(e) : 0L;
+  }();
+  if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
   cudaStream_t st = (cudaStream_t)stream;
   bool WD = wd != 0.f, MOM = mu != 0.f;
   // one vector per thread per grid stride: unrolling (2, 4 vectors with all
@@ -711,6 +717,19 @@ extern "C" int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_
   if (k > (1u << 20)) return set_err(LPP_E_VALUE, "classify: k too large");
   k_classify<<<1, 32, 0, (cudaStream_t)stream>>>(tags, (int)k, claim_cell, out);
   LAUNCH_CHECK("classify");
+  return LPP_OK;
+}
+
+// a device int64 cell set in stream order (the worker's round-stamp cell,
+// written by its averager once a round is applied to its arena)
+__global__ void k_set_i64(int64_t* p, int64_t v) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+extern "C" int lpp_set_i64(int64_t* dev, int64_t v, void* stream) {
+  if (!dev) return set_err(LPP_E_VALUE, "set_i64: null cell");
+  k_set_i64<<<1, 1, 0, (cudaStream_t)stream>>>(dev, v);
+  LAUNCH_CHECK("set_i64");
   return LPP_OK;
 }
 

@@ -317,8 +317,12 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   // one) gather them before their snapshot values are read
   // (paramstore.py:108-112); fused steps get them from the previous step's
   // apply kernel, after that apply landed (engine.py:343-362 order)
-  auto draw_idx = [&](int slot) {
-    if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, c->tag_idx_pinned + (size_t)slot * K);
+  // draw (device-sampling runs; host_rng runs drew them in step order)
+  // and copy one slot of indices to the device ring, on the updater stream
+  auto draw_idx = [&](int slot) -> int {
+    const size_t o = (size_t)slot * K;
+    if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, c->tag_idx_pinned + o);
+    return lpp_copy_async(c->tag_idx_dev + o, c->tag_idx_pinned + o, 8 * (size_t)K, stream);
   };
   auto gather = [&](int slot) -> int {
     const size_t o = (size_t)slot * K;
@@ -431,17 +435,18 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (!c->fused || t == 0) {
       if (K > 0) {
-        if (!c->fused || !c->host_rng) draw_idx(slot);
+        if ((rc = draw_idx(slot)) != LPP_OK) return rc;
         if ((rc = gather(slot)) != LPP_OK) return rc;                               // K5
       }
       if ((rc = lpp_snapshot(c->x, c->replica, c->n, stream)) != LPP_OK) return rc;   // K3
     }
+    // the next step's tag indices, for this step's apply kernel to gather
+    if (c->fused && K > 0 && (rc = draw_idx(next_slot)) != LPP_OK) return rc;
     if ((rc = lpp_graph_launch(c->graph_exec[2 * b + buf], stream)) != LPP_OK) return rc;  // fwd+bwd
     if (host) CUDA_TRY(cudaEventRecord(buf_free.ev[buf], stream));
     if (c->read_loss)
       CUDA_TRY(cudaMemcpyAsync(c->loss_pinned + slot, c->loss_dev[buf], sizeof(float),
                                cudaMemcpyDeviceToHost, stream));
-    if (c->fused && K > 0) draw_idx(next_slot);         // read by this step's apply kernel
     if (side) {  // the apply on its own (high-priority) stream, after the graph
       CUDA_TRY(cudaEventRecord(order.ev[0], stream));
       CUDA_TRY(cudaStreamWaitEvent(astream, order.ev[0], 0));
@@ -659,6 +664,17 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
       if (fenced1) {
         add(fence_cell(c, 1, r), 1);
         ok = wait_ge(fence_cell(c, 1, r), Q);
+      }
+      if (ok && c->round_cell) {
+        // the device round-stamp cell the updaters' apply kernels read as
+        // k_claim and tag floor, before the host cell moves
+        int rc2 = lpp_set_i64(c->round_cell, u, stream);
+        if (rc2 != LPP_OK) return fail(rc2);
+        cudaError_t e2 = cudaStreamSynchronize(stream);
+        if (e2 != cudaSuccess) {
+          fail(LPP_E_CUDA);
+          return set_err(LPP_E_CUDA, "averager: stream sync failed: %s", cudaGetErrorString(e2));
+        }
       }
       if (ok) {
         st(c->last_avg_stamp, u);

@@ -111,8 +111,8 @@ class NativeLoops:
         if tracks:
             # K5 rings in host-mapped memory (indices, effective tags, the
             # apply kernels' (k_claim, clean) records) + the device tag ring
-            c.tag_idx_dev = w.idx_dev(r, 0)
-            c.tag_idx_pinned = w.host_addr(c.tag_idx_dev)
+            c.tag_idx_dev = w.tag_idx_ring[r].data_ptr()
+            c.tag_idx_pinned = w.tag_idx_pinned[r].data_ptr()
             c.tag_out_dev = w.tag_out_dev[r].data_ptr()
             c.tag_out_host_dev = w.tag_host_dev(r, 0)
             c.tag_out_pinned = w.host_addr(c.tag_out_host_dev)
@@ -247,6 +247,7 @@ class NativeLoops:
             c.workers, c.q, c.updaters = Q, q, cfg.updaters
             c.tagged = int(self.tag_ptrs is not None)
             c.stamp_floor = int(cfg.tracks)
+            c.round_cell = w.avg_dev
             c.sample_counter = w.store.sample_counter._a
             c.update_order = w.store.update_order_counter._a
             c.exited = w.exited._a

@@ -37,12 +37,15 @@ for d in (11_220_132, 25_557_032):
 # K1+K3 fused (the async default) at d20 and d50 with a partial block: the
 # engine's launch, with the K5 plan (classify this step, stamp, gather the
 # next step's 16 tags in the last CTA) — and without tags for comparison
+# as the engine lays it out: indices and the round-stamp cell on the device,
+# the gathered tags and the (k_claim, clean) record written to mapped host memory
 hb = N.HostBuffer(4096)
-hb.view("int64", (16,), 64)[:] = range(0, 16 * 1000, 1000)
+idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long, device="cuda")
+cell = torch.zeros(1, dtype=torch.long, device="cuda")
 dev_tags = torch.zeros(32, dtype=torch.int32, device="cuda")
 done = torch.zeros(1, dtype=torch.int32, device="cuda")
-plan = N.TagPlan(hb.dev + 64, dev_tags[16:].data_ptr(), hb.dev + 512, dev_tags[:16].data_ptr(),
-                 hb.dev + 1024, hb.dev, done.data_ptr(), 16)
+plan = N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), hb.dev + 512, dev_tags[:16].data_ptr(),
+                 hb.dev + 1024, cell.data_ptr(), done.data_ptr(), 16)
 for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000)):
     x, g, m, rep, tg = (Arena(d, 0) for _ in range(5))
     x.tensor.normal_(), g.tensor.normal_()
