@@ -134,22 +134,24 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
 
 /* K5 inside the fused launch, in the reference updater's order
  * (engine.py:343-362: sampled tags at the snapshot, k_claim after the
- * gradient, then the apply):
+ * gradient, then the apply), with per-BLOCK write stamps: every update
+ * writes one whole block range, so an element's tag is the newest stamp of
+ * the blocks covering it (block 0 = all, and its partial block).
+ *   block_stamps[block_id] = max(., stamp), by the last CTA once every
+ *       element reduction of this launch is performed (a completion
+ *       counter `done`, zero before the first launch, private to the stream)
  *   cur_claim[0..1] = (k_claim, clean): k_claim = *avg_cell read when the
  *       kernel starts (after this step's gradient), clean = all of this
  *       step's k tags cur_dev[j] >= k_claim              (cur_claim may be NULL)
- *   next_dev[j] (and next_host[j]) = max(tags[next_idx[j]], *avg_cell) for
- *       j < k, read by the last CTA after every CTA's updates and tag
- *       stores, i.e. at the next step's snapshot; the floor *avg_cell is
- *       the worker's last completed round stamp, which a round writes
- *       into every element (engine.py:421)        (next_idx may be NULL)
- * avg_cell is the worker's DEVICE round-stamp cell (lpp_set_i64 by the
- * averager once a round is applied; host memory would put a PCIe round trip
- * on the kernel's tail); next_host / cur_claim may point into lpp_host_alloc
- * memory (posted writes the host reads after the step's event).  done: a 4-byte
- * device counter, zero before the first launch, private to the stream (the
- * last CTA resets it).  Write tags: every thread issues all of its
- * reductions, one fence.acq_rel.gpu, then the tags of the same elements. */
+ *   next_dev[j] (and next_host[j]) = the next step's sampled tag j, read by
+ *       the thread that refreshes the replica element next_idx[j] BEFORE it
+ *       reads the value and after this launch's own reduction there:
+ *       max(*avg_cell, block_stamps[0], block_stamps[b(e)], stamp if e is in
+ *       [lo, hi)); *avg_cell (the worker's last completed round stamp, a
+ *       device cell) is the floor a round writes into every element
+ *       (engine.py:421)                              (next_idx may be NULL)
+ * block_bounds: num_blocks + 1 boundaries (0 ... n); k <= 32; next_host and
+ * cur_claim may point into lpp_host_alloc memory. */
 typedef struct lpp_tag_plan {
   const int64_t* next_idx;
   int32_t* next_dev;
@@ -158,6 +160,10 @@ typedef struct lpp_tag_plan {
   int64_t* cur_claim;
   const int64_t* avg_cell;
   uint32_t* done;
+  int32_t* block_stamps;
+  const int64_t* block_bounds;
+  int32_t num_blocks;
+  int32_t block_id;
   int32_t k;
 } lpp_tag_plan;
 int lpp_apply_snapshot_plan(float* x, const float* g, float* m, float* replica,
@@ -232,6 +238,11 @@ int lpp_gather_tags(const int32_t* tags, const int64_t* idx, size_t k, int32_t* 
 int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
                           const int64_t* floor_cell, int32_t* out_dev, int32_t* out_host,
                           void* stream);
+/* the sampled tags of a fused run's first snapshot from the block stamps:
+ * out[j] = max(*floor_cell, stamps[0], stamps[b(idx[j])]) */
+int lpp_gather_block_stamps(const int32_t* stamps, const int64_t* bounds, int nb,
+                            const int64_t* idx, size_t k, const int64_t* floor_cell,
+                            int32_t* out_dev, int32_t* out_host, void* stream);
 /* *dev = v in stream order (the round-stamp cell the apply kernels read) */
 int lpp_set_i64(int64_t* dev, int64_t v, void* stream);
 /* classification at apply time (engine.py:353-362) for the unfused paths:
@@ -472,6 +483,10 @@ typedef struct {
   int32_t* tag_out_host_dev;
   const int64_t* avg_cell_dev;
   uint32_t* done_ctr;
+  /* fused runs: the worker's per-block write stamps [num_blocks + 1] and the
+   * block boundaries [num_blocks + 1] on the device (lpp_tag_plan) */
+  int32_t* block_stamps;
+  const int64_t* block_bounds_dev;
 } lpp_updater_cfg;
 
 typedef struct {

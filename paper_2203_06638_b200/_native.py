@@ -78,7 +78,7 @@ class UpdaterCfg(ctypes.Structure):
         ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
         ("claim_ring", _vp), ("claim_ring_dev", _vp), ("tag_out_host_dev", _vp),
-        ("avg_cell_dev", _vp), ("done_ctr", _vp),
+        ("avg_cell_dev", _vp), ("done_ctr", _vp), ("block_stamps", _vp), ("block_bounds_dev", _vp),
     ]
 
 
@@ -86,7 +86,9 @@ class TagPlan(ctypes.Structure):
     """``lpp_tag_plan`` (include/lpp_b200.h)."""
 
     _fields_ = [("next_idx", _vp), ("next_dev", _vp), ("next_host", _vp), ("cur_dev", _vp),
-                ("cur_claim", _vp), ("avg_cell", _vp), ("done", _vp), ("k", _c.c_int32)]
+                ("cur_claim", _vp), ("avg_cell", _vp), ("done", _vp), ("block_stamps", _vp),
+                ("block_bounds", _vp), ("num_blocks", _c.c_int32), ("block_id", _c.c_int32),
+                ("k", _c.c_int32)]
 
 
 class AveragerCfg(ctypes.Structure):
@@ -152,6 +154,7 @@ _SIGS = {
     "lpp_gather_tags_floor": (_c.c_int, [_vp, _vp, _size, _vp, _vp, _vp, _vp]),
     "lpp_classify": (_c.c_int, [_vp, _size, _vp, _vp, _vp]),
     "lpp_set_i64": (_c.c_int, [_vp, _c.c_int64, _vp]),
+    "lpp_gather_block_stamps": (_c.c_int, [_vp, _vp, _c.c_int, _vp, _size, _vp, _vp, _vp, _vp]),
     "lpp_host_alloc": (_c.c_int, [_size, _c.POINTER(_vp), _c.POINTER(_vp)]),
     "lpp_host_free": (_c.c_int, [_vp]),
     "lpp_load_f32": (_c.c_int, [_vp, _size, _size, _c.POINTER(_c.c_float), _vp]),
@@ -327,6 +330,12 @@ def gather_tags_floor(tags_ptr, idx_ptr, k, floor_ptr, out_dev_ptr, out_host_ptr
 
 def classify(tags_ptr, k, claim_ptr, out_ptr, stream) -> None:
     check(lib.lpp_classify(tags_ptr, k, claim_ptr, out_ptr, stream), "classify")
+
+
+def gather_block_stamps(stamps_ptr, bounds_ptr, nb, idx_ptr, k, floor_ptr, out_dev_ptr, out_host_ptr,
+                        stream) -> None:
+    check(lib.lpp_gather_block_stamps(stamps_ptr, bounds_ptr, nb, idx_ptr, k, floor_ptr, out_dev_ptr,
+                                      out_host_ptr, stream), "gather_block_stamps")
 
 
 def set_i64(dev_ptr: int, v: int, stream: int) -> None:

@@ -149,6 +149,12 @@ class _Worker:
             self.claim_np = self.hostmem.view(np.int64, (U, depth, 2), self._o_claim)
             self.tag_out_dev = torch.zeros((U, depth, k), dtype=torch.int32, device=self.dev)
             self.done_ctr = torch.zeros(U, dtype=torch.int32, device=self.dev)
+            # fused runs: per-block write stamps (an update writes one block
+            # range) and the block boundaries, on the device
+            nb = cfg.partition.num_blocks
+            self.block_stamps = torch.zeros(nb + 1, dtype=torch.int32, device=self.dev)
+            self.block_bounds = torch.tensor(cfg.partition.boundaries, dtype=torch.long,
+                                             device=self.dev)
             self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
             self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
         # full record mode keeps every update's whole tag snapshot (reference
@@ -337,7 +343,8 @@ class _Engine(NativeLoops):
         # algorithmic bytes per element of K1/K2: read g, read +
         # write x (the weight-decay read of x is that same read), + read and
         # write the per-stream momentum buffer, + the int32 write tag (K5)
-        self.apply_bytes_per_elem = 12 + (8 if mu else 0) + (4 if cfg.tracks else 0)
+        # (fused runs keep per-BLOCK stamps: no per-element tag bytes)
+        self.apply_bytes_per_elem = 12 + (8 if mu else 0) + (4 if cfg.tracks and not self.fused() else 0)
         fwd = obj.forward_cost()
         self._flops_of = {b: cfg.batch_size * (fwd + obj.backward_cost(cfg.partition.block(b)))
                           for b in range(cfg.partition.num_blocks + 1)}
@@ -363,6 +370,7 @@ class _Engine(NativeLoops):
             w.round_cell.zero_()
             if w.tags is not None:
                 w.tags.zero_()
+                w.block_stamps.zero_()
         torch.cuda.synchronize()
         self.updates = [[] for _ in range(self.cfg.workers * self.cfg.updaters)]
         self.stamps = [[] for _ in range(self.cfg.workers)]
@@ -488,8 +496,13 @@ class _Engine(NativeLoops):
         k = w.tag_pick
         sp = w.streams[r].cuda_stream
         idx_dev = w.stage_idx(r, slot, tag_idx, sp)
-        N.gather_tags_floor(w.tag_arena.ptr, idx_dev, k, w.avg_dev,
-                            w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
+        if self.fused():   # fused runs stamp blocks, not elements
+            N.gather_block_stamps(w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
+                                  self.cfg.partition.num_blocks, idx_dev, k, w.avg_dev,
+                                  w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
+        else:
+            N.gather_tags_floor(w.tag_arena.ptr, idx_dev, k, w.avg_dev,
+                                w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
 
     def classify_on_device(self, w: _Worker, r: int, slot: int, stream_ptr: int) -> None:
         """K5 classification at apply time (engine.py:353-362): k_claim is
@@ -535,7 +548,9 @@ class _Engine(NativeLoops):
                 k = w.tag_pick
                 plan = N.TagPlan(next_idx_dev, w.tag_out_dev[r, next_slot].data_ptr(),
                                  w.tag_host_dev(r, next_slot), w.tag_out_dev[r, slot].data_ptr(),
-                                 w.claim_dev(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(), k)
+                                 w.claim_dev(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(),
+                                 w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
+                                 cfg.partition.num_blocks, block_id, k)
             mom = w.moms[r]
             astream = stream
             if self.side_apply:
@@ -550,7 +565,7 @@ class _Engine(NativeLoops):
             if plan is not None:                                                         # K1+K3+K5
                 N.apply_snapshot_plan(w.store.arena.ptr, w.grads[r].ptr,
                                       mom.ptr if mom is not None else None, w.replicas[r].ptr,
-                                      w.tag_arena.ptr, self.dim, blk.start, blk.stop, float(lr), None,
+                                      None, self.dim, blk.start, blk.stop, float(lr), None,
                                       cfg.momentum, cfg.weight_decay, u, plan, sp)
             else:                                                                         # K1+K3
                 N.apply_snapshot(w.store.arena.ptr, w.grads[r].ptr,

@@ -455,28 +455,39 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 //
 // K5 inside the same launch (``lpp_tag_plan``), in the reference's order
 // (engine.py:343-362: snapshot tags -> gradient -> k_claim -> apply):
-//   * write tags: every thread issues ALL its reductions first, then one
-//     fence.acq_rel.gpu, then the tag stores of the same vectors (value
-//     before tag, _atomics.c:346-392) — one fence per thread instead of one
-//     per vector;
+//   * write stamps per BLOCK, not per element: every update writes one
+//     whole block range, so an element's tag is the newest stamp of the (at
+//     most two) blocks covering it — block 0 (full) and its partial block.
+//     The last CTA to finish (a completion counter: each CTA's thread 0
+//     fences after the CTA barrier, then counts) raises its block's stamp
+//     with atomicMax after a fence, so a stamp is visible only once every
+//     element reduction of its update is performed (value before tag,
+//     _atomics.c:346-392) — at no per-element cost;
 //   * classification of THIS step: block 0 reads k_claim from the worker's
-//     round-stamp cell (host-mapped) when the kernel starts, i.e. after the
-//     step's gradient, and compares the step's sampled tags with it;
-//   * the NEXT step's sampled tags: gathered by the last CTA to finish,
-//     after every CTA's reductions and tag stores (a completion counter),
-//     i.e. at the next snapshot's point in time; each tag is raised to the
-//     worker's last completed round stamp (rounds stamp every element,
-//     engine.py:421 add_assign(..., stamp=u_avg): the floor stands for it).
+//     device round-stamp cell when the kernel starts, i.e. after the step's
+//     gradient, and compares the step's sampled tags with it;
+//   * the NEXT step's sampled tags, element by element in snapshot order
+//     (paramstore.py:108-112: tag before value): the thread that refreshes
+//     the replica vector holding a sampled element acquire-reads the stamps
+//     and the round floor BEFORE it re-reads the value, after its own
+//     reduction of that vector; the effective tag is
+//     max(floor, stamp[0], stamp[b(e)], this update's stamp if e is in its
+//     block).  The floor is the worker's last completed round stamp (rounds
+//     stamp every element, engine.py:421 add_assign(..., stamp=u_avg)).
 
 struct TagPlanDev {
-  const int64_t* next_idx;  // k sampled indices of the next step
+  const int64_t* next_idx;  // k sampled indices of the next step (device)
   int* next_dev;            // -> the next step's effective tags (device ring slot)
   int* next_host;           // -> and a host-mapped copy for the records (may be null)
-  const int* cur_dev;       // this step's effective tags (gathered at its snapshot)
+  const int* cur_dev;       // this step's effective tags (read at its snapshot)
   int64_t* cur_claim;       // -> this step's (k_claim, clean) (host-mapped; may be null)
   const int64_t* avg_cell;  // the worker's last completed round stamp (device cell)
   unsigned* done;           // CTA completion counter (device, 0 between launches)
-  int k;
+  int* block_stamps;        // [nb + 1] newest stamp per block (device)
+  const int64_t* bounds;    // [nb + 1] block boundaries (bounds[0] = 0, bounds[nb] = n)
+  int nb;
+  int bid;                  // this update's block id
+  int k;                    // <= 32
 };
 
 __device__ __forceinline__ int64_t ld_sys_i64(const int64_t* p) {
@@ -484,27 +495,40 @@ __device__ __forceinline__ int64_t ld_sys_i64(const int64_t* p) {
   asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(r) : "l"(p));
   return r;
 }
+__device__ __forceinline__ int ld_acq_i32(const int* p) {
+  int r;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
 
-// gather the k sampled tags of the next snapshot (last CTA), tag >= floor
-__device__ __forceinline__ void plan_gather(const TagPlanDev& plan, const int* tags) {
+// effective tag of sampled element e, read before its value (see above)
+__device__ __forceinline__ int plan_tag_of(const TagPlanDev& plan, int64_t e, size_t lo, size_t hi,
+                                           int stamp) {
+  int b = 1;
+  while (b < plan.nb && e >= plan.bounds[b]) ++b;
+  int t = ld_acq_i32(plan.block_stamps);
+  int tb = ld_acq_i32(plan.block_stamps + b);
+  t = t > tb ? t : tb;
+  const int fl = (int)ld_sys_i64(plan.avg_cell);
+  t = t > fl ? t : fl;
+  if ((size_t)e >= lo && (size_t)e < hi && stamp > t) t = stamp;
+  return t;
+}
+
+// last CTA: publish this update's block stamp (after every CTA's reductions)
+__device__ __forceinline__ void plan_publish(const TagPlanDev& plan, int stamp) {
   __shared__ int is_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    fence_ar_gpu();  // this CTA's reductions and tag stores before the count
+    fence_ar_gpu();  // this CTA's reductions before the count
     unsigned old = atomicAdd(plan.done, 1u);
     is_last = (old == gridDim.x - 1);
-    if (is_last) fence_ar_gpu();
+    if (is_last) {
+      fence_ar_gpu();
+      atomicMax(plan.block_stamps + plan.bid, stamp);
+      *plan.done = 0u;
+    }
   }
-  __syncthreads();
-  if (!is_last) return;
-  const int floor_ = plan.avg_cell ? (int)ld_sys_i64(plan.avg_cell) : 0;
-  for (int j = threadIdx.x; j < plan.k; j += blockDim.x) {
-    int t = ld_tag(tags + ld_sys_i64(plan.next_idx + j));
-    t = t > floor_ ? t : floor_;
-    plan.next_dev[j] = t;
-    if (plan.next_host) plan.next_host[j] = t;
-  }
-  if (threadIdx.x == 0) *plan.done = 0u;
 }
 
 template <bool WD, bool MOM>
@@ -530,7 +554,7 @@ __global__ void __launch_bounds__(kThreads)
                      const float* __restrict__ lr_dev, float mu, float wd, int stamp,
                      TagPlanDev plan) {
   // k_claim of this step (engine.py:353: read after the gradient), issued
-  // first and consumed at the end so its host round trip overlaps the work
+  // first and consumed at the end
   const bool classifier = PLAN && blockIdx.x == 0 && threadIdx.x == 0 && plan.cur_claim != nullptr;
   int64_t k_claim = 0;
   if (classifier) k_claim = plan.avg_cell ? ld_sys_i64(plan.avg_cell) : 0;
@@ -538,10 +562,35 @@ __global__ void __launch_bounds__(kThreads)
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nvec = n / 4;
+  // which of the next step's sampled elements this thread refreshes: the
+  // owner of vector v is thread v mod stride (iteration v / stride); a tail
+  // element e >= 4 nvec belongs to block 0, thread (e - 4 nvec) mod blockDim
+  __shared__ int64_t sidx[32];
+  unsigned own = 0;
+  if (PLAN && plan.next_idx) {
+    if (threadIdx.x < plan.k) sidx[threadIdx.x] = plan.next_idx[threadIdx.x];
+    __syncthreads();
+    for (int j = 0; j < plan.k; ++j) {
+      const size_t e = (size_t)sidx[j], v = e / 4;
+      const bool mine = v < nvec ? (v % stride == tid)
+                                 : (blockIdx.x == 0 && (e - 4 * nvec) % blockDim.x == threadIdx.x);
+      if (mine) own |= 1u << j;
+    }
+  }
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element
   const size_t vlo = (lo + 3) / 4, vhi = hi / 4;
   for (size_t i = tid; i < nvec; i += stride) {
+    if (PLAN && own) {  // sampled elements of this vector: tags before values
+      for (unsigned bits = own; bits; bits &= bits - 1) {
+        const int j = __ffs(bits) - 1;
+        if ((size_t)sidx[j] / 4 == i) {
+          const int t = plan_tag_of(plan, sidx[j], lo, hi, stamp);
+          plan.next_dev[j] = t;
+          if (plan.next_host) plan.next_host[j] = t;
+        }
+      }
+    }
     if (i >= vlo && i < vhi) {
       float4 gr = __ldg(reinterpret_cast<const float4*>(g) + i);
       float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), mr = xr;
@@ -566,11 +615,21 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (blockIdx.x == 0)
-    for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x)
+    for (size_t e = 4 * nvec + threadIdx.x; e < n; e += blockDim.x) {
+      if (PLAN && own)
+        for (unsigned bits = own; bits; bits &= bits - 1) {
+          const int j = __ffs(bits) - 1;
+          if ((size_t)sidx[j] == e) {
+            const int t = plan_tag_of(plan, sidx[j], lo, hi, stamp);
+            plan.next_dev[j] = t;
+            if (plan.next_host) plan.next_host[j] = t;
+          }
+        }
       fused_elem<WD, MOM>(x, g, m, rep, e, lo, hi, lr, mu, wd);
+    }
   if (TAGS) {
-    // one fence: all of this thread's reductions are performed before any of
-    // its tag stores; then the tags of exactly the elements it updated
+    // per-element tags (ParamStore-level API): one fence per thread, then
+    // the tags of exactly the elements it updated
     fence_ar_gpu();
     for (size_t i = tid; i < nvec; i += stride) {
       if (i >= vlo && i < vhi) {
@@ -591,7 +650,7 @@ __global__ void __launch_bounds__(kThreads)
       plan.cur_claim[0] = k_claim;
       plan.cur_claim[1] = clean;
     }
-    if (plan.k > 0 && plan.next_idx) plan_gather(plan, tags);
+    plan_publish(plan, stamp);
   }
 }
 
@@ -609,14 +668,20 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     return set_err(LPP_E_VALUE, "apply_snapshot: arena bases must be 16-byte aligned");
   TagPlanDev pd{};
   if (plan) {
-    if (!tags) return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs the tag arena");
-    if (plan->k < 0) return set_err(LPP_E_VALUE, "apply_snapshot: negative tag count");
-    if (plan->k > 0 && plan->next_idx && (!plan->next_dev || !plan->done))
-      return set_err(LPP_E_VALUE, "apply_snapshot: next-step gather needs out and counter");
+    if (plan->k < 0 || plan->k > 32)
+      return set_err(LPP_E_VALUE, "apply_snapshot: tag count %d outside [0, 32]", plan->k);
+    if (!plan->done || !plan->block_stamps || !plan->block_bounds || !plan->avg_cell)
+      return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs stamps, bounds, round cell, counter");
+    if (plan->num_blocks < 1 || plan->block_id < 0 || plan->block_id > plan->num_blocks)
+      return set_err(LPP_E_VALUE, "apply_snapshot: block %d outside [0, %d]", plan->block_id,
+                     plan->num_blocks);
+    if (plan->k > 0 && plan->next_idx && !plan->next_dev)
+      return set_err(LPP_E_VALUE, "apply_snapshot: next-step tags need an output");
     if (plan->cur_claim && plan->k > 0 && !plan->cur_dev)
       return set_err(LPP_E_VALUE, "apply_snapshot: classification needs this step's tags");
-    pd = TagPlanDev{plan->next_idx, plan->next_dev, plan->next_host, plan->cur_dev,
-                    plan->cur_claim, plan->avg_cell, plan->done, plan->k};
+    pd = TagPlanDev{plan->next_idx,     plan->next_dev,  plan->next_host,   plan->cur_dev,
+                    plan->cur_claim,    plan->avg_cell,  plan->done,        plan->block_stamps,
+                    plan->block_bounds, plan->num_blocks, plan->block_id,   plan->k};
   }
   size_t nvec = n / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
@@ -635,7 +700,7 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
   // neither the in-situ d20 time nor images/s
 #define FUSED_LAUNCH(W, M)                                                                      \
   if (plan)                                                                                     \
-    k_apply_snapshot<W, M, true, true><<<grid, kThreads, 0, st>>>(                             \
+    k_apply_snapshot<W, M, false, true><<<grid, kThreads, 0, st>>>(                            \
         x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
   else if (tags)                                                                                \
     k_apply_snapshot<W, M, true, false><<<grid, kThreads, 0, st>>>(                            \
@@ -697,6 +762,37 @@ extern "C" int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, si
   k_gather_tags_floor<<<1, kThreads, 0, (cudaStream_t)stream>>>(tags, idx, (int)k, floor_cell,
                                                                  out_dev, out_host);
   LAUNCH_CHECK("gather_tags_floor");
+  return LPP_OK;
+}
+
+// the first step of a fused run: its sampled tags from the block stamps
+// (tag before value: the K3 snapshot that follows on the stream reads values)
+__global__ void k_gather_block_stamps(const int* stamps, const int64_t* bounds, int nb,
+                                      const int64_t* idx, int k, const int64_t* floor_cell,
+                                      int* out_dev, int* out_host) {
+  const int fl = floor_cell ? (int)ld_sys_i64(floor_cell) : 0;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const int64_t e = idx[j];
+    int b = 1;
+    while (b < nb && e >= bounds[b]) ++b;
+    int t = ld_acq_i32(stamps), tb = ld_acq_i32(stamps + b);
+    t = t > tb ? t : tb;
+    t = t > fl ? t : fl;
+    if (out_dev) out_dev[j] = t;
+    if (out_host) out_host[j] = t;
+  }
+}
+
+extern "C" int lpp_gather_block_stamps(const int32_t* stamps, const int64_t* bounds, int nb,
+                                       const int64_t* idx, size_t k, const int64_t* floor_cell,
+                                       int32_t* out_dev, int32_t* out_host, void* stream) {
+  if (k == 0) return LPP_OK;
+  if (!stamps || !bounds || !idx || nb < 1 || (!out_dev && !out_host))
+    return set_err(LPP_E_VALUE, "gather_block_stamps: null buffer or no blocks");
+  if (k > (1u << 20)) return set_err(LPP_E_VALUE, "gather_block_stamps: k too large");
+  k_gather_block_stamps<<<1, kThreads, 0, (cudaStream_t)stream>>>(stamps, bounds, nb, idx, (int)k,
+                                                                   floor_cell, out_dev, out_host);
+  LAUNCH_CHECK("gather_block_stamps");
   return LPP_OK;
 }
 

@@ -238,7 +238,8 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   const int K = tagged ? c->tag_pick : 0;
   if (K > 0 && (!c->tag_idx_pinned || !c->tag_idx_dev || !c->tag_out_dev || !c->tag_out_pinned ||
                 !c->tag_out_host_dev || !c->claim_ring || !c->claim_ring_dev ||
-                !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean))
+                !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean ||
+                (c->fused && (!c->block_stamps || !c->block_bounds_dev))))
     return set_err(LPP_E_VALUE, "updater_run: tag sampling buffers missing");
   const int F = c->in_flight < 1 ? 1 : c->in_flight;
   const int depth = F + 2;
@@ -326,6 +327,10 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   };
   auto gather = [&](int slot) -> int {
     const size_t o = (size_t)slot * K;
+    if (c->fused)  // fused runs stamp blocks, not elements
+      return lpp_gather_block_stamps(c->block_stamps, c->block_bounds_dev, c->num_blocks,
+                                     c->tag_idx_dev + o, (size_t)K, c->avg_cell_dev,
+                                     c->tag_out_dev + o, c->tag_out_host_dev + o, stream);
     return lpp_gather_tags_floor(c->tags, c->tag_idx_dev + o, (size_t)K, c->avg_cell_dev,
                                  c->tag_out_dev + o, c->tag_out_host_dev + o, stream);
   };
@@ -457,8 +462,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       const size_t o = (size_t)slot * K, on = (size_t)next_slot * K;
       lpp_tag_plan plan{c->tag_idx_dev + on, c->tag_out_dev + on, c->tag_out_host_dev + on,
                         c->tag_out_dev + o, c->claim_ring_dev + 2 * (size_t)slot, c->avg_cell_dev,
-                        c->done_ctr, K};
-      rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, c->tags, c->n, (size_t)lo,
+                        c->done_ctr, c->block_stamps, c->block_bounds_dev,
+                        c->num_blocks, b, K};
+      rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, nullptr, c->n, (size_t)lo,
                                    (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u, &plan,
                                    astream);
       bytes_of[k] = c->apply_bytes_per_elem * (double)len + 4.0 * (double)(c->n - len) +

@@ -120,6 +120,8 @@ class NativeLoops:
             c.claim_ring = w.host_addr(c.claim_ring_dev)
             c.avg_cell_dev = w.avg_dev
             c.done_ctr = w.done_ctr[r].data_ptr()
+            c.block_stamps = w.block_stamps.data_ptr()
+            c.block_bounds_dev = w.block_bounds.data_ptr()
         c.classified = self.classified_count._a
         c.clean = self.clean_count._a
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)

@@ -504,53 +504,53 @@ def test_no_kernel_writes_outside_its_range(N, n):
 # K5 in the reference's order (lpp_tag_plan), the round floor, element access
 
 
-def _plan_setup(N, n, k, depth=3):
-    from paper_2203_06638_b200.arena import Arena
-
-    hb = N.HostBuffer(64 + 8 * depth * k + 4 * depth * k + 16 * depth)
-    avg = hb.view(np.int64, (1,))
-    idx = hb.view(np.int64, (depth, k), 64)
-    tag_host = hb.view(np.int32, (depth, k), 64 + 8 * depth * k)
-    claim = hb.view(np.int64, (depth, 2), 64 + 12 * depth * k)
-    dev = {"avg": hb.dev, "idx": hb.dev + 64, "tag_host": hb.dev + 64 + 8 * depth * k,
-           "claim": hb.dev + 64 + 12 * depth * k}
+def _plan_bufs(N, k, nb, depth=3):
+    hb = N.HostBuffer(4 * depth * k + 16 * depth)
+    tag_host = hb.view(np.int32, (depth, k), 0)
+    claim = hb.view(np.int64, (depth, 2), 4 * depth * k)
+    dev = {"tag_host": hb.dev, "claim": hb.dev + 4 * depth * k}
     tag_dev = torch.zeros((depth, k), dtype=torch.int32, device="cuda")
+    idx = torch.zeros((depth, k), dtype=torch.long, device="cuda")
     done = torch.zeros(1, dtype=torch.int32, device="cuda")
-    tags = Arena(n, 0)
-    return hb, avg, idx, tag_host, claim, dev, tag_dev, done, tags
+    cell = torch.zeros(1, dtype=torch.long, device="cuda")
+    stamps = torch.zeros(nb + 1, dtype=torch.int32, device="cuda")
+    return hb, tag_host, claim, dev, tag_dev, idx, done, cell, stamps
 
 
-@pytest.mark.parametrize("n,lo,hi", [(4099, 0, 4099), (100_003, 1001, 77_777), (1_000_001, 3, 999_998)])
-def test_apply_snapshot_plan_values_tags_classification_and_next_gather(N, orc, n, lo, hi):
-    """The plan variant updates values exactly like the fused kernel, stamps
-    the block, classifies this step against the round-stamp cell read in the
-    kernel, and gathers the next step's sampled tags AFTER its own stamps
-    landed (elements inside the block come back with this step's stamp),
-    raised to the floor."""
+@pytest.mark.parametrize("n,bounds,bid", [(4099, (0, 1000, 4099), 2), (100_003, (0, 1001, 77_777, 100_003), 2),
+                                          (1_000_001, (0, 3, 999_998, 1_000_001), 0),
+                                          (1_000_001, (0, 3, 999_998, 1_000_001), 1)])
+def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, n, bounds, bid):
+    """The plan variant updates values exactly like the fused kernel, leaves
+    per-element tags alone, raises its block's stamp once done, classifies
+    this step against the round-stamp cell read in the kernel, and reads the
+    next step's sampled tags as max(floor, stamp[0], stamp[b(e)], own stamp
+    inside its block) — the own stamp even though it is published last."""
     from paper_2203_06638_b200.arena import Arena
 
-    k = 16
-    hb, avg, idx, tag_host, claim, dev, tag_dev, done, tags = _plan_setup(N, n, k)
-    gen = np.random.default_rng(n)
+    k, nb = 16, len(bounds) - 1
+    lo, hi = (0, n) if bid == 0 else (bounds[bid - 1], bounds[bid])
+    hb, tag_host, claim, dev, tag_dev, idx, done, cell, stamps = _plan_bufs(N, k, nb)
+    bnd = torch.tensor(bounds, dtype=torch.long, device="cuda")
+    gen = np.random.default_rng(n + bid)
     x = gen.normal(size=n).astype(np.float32)
     g = (1e-2 * gen.normal(size=n)).astype(np.float32)
     m = gen.normal(size=n).astype(np.float32)
     ax, ag, am, ar = (Arena(n, 0) for _ in range(4))
     ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g)), am.tensor.copy_(_cuda(m))
-    t0 = gen.integers(0, 50, size=n).astype(np.int32)
-    tags.tensor.view(torch.int32).copy_(_cuda(t0))
-    # this step's tags (slot 0): two cases of k_claim
-    tag_dev[0] = torch.tensor(np.arange(10, 10 + k), dtype=torch.int32)
-    avg[0] = 12                                  # k_claim 12 > 10 = min tag -> dirty
-    inside = np.sort(gen.choice(np.arange(lo, hi), size=k // 2, replace=False))
-    pool = np.r_[0:lo, hi:n] if lo or hi < n else np.arange(n)
-    outside = np.sort(gen.choice(pool, size=k - k // 2, replace=len(pool) < k - k // 2))
-    idx[1] = np.sort(np.r_[inside, outside])
-    plan = N.TagPlan(dev["idx"] + 8 * k, tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
-                     tag_dev[0].data_ptr(), dev["claim"], dev["avg"], done.data_ptr(), k)
+    old = gen.integers(5, 30, size=nb + 1).astype(np.int32)
+    stamps.copy_(_cuda(old))
+    tag_dev[0] = torch.tensor(np.arange(10, 10 + k), dtype=torch.int32)   # this step's tags
+    cell.fill_(12)                                 # k_claim 12 > 10 = min tag -> dirty
+    nxt = np.sort(gen.choice(n, size=k, replace=False))
+    nxt[0], nxt[-1] = 0, n - 1                     # first and last (tail) elements included
+    idx[1] = torch.tensor(nxt)
+    plan = N.TagPlan(idx[1].data_ptr(), tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
+                     tag_dev[0].data_ptr(), dev["claim"], cell.data_ptr(), done.data_ptr(),
+                     stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
     stamp = 40
-    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, tags.ptr, n, lo, hi, 0.05, None, 0.9,
-                          5e-4, stamp, plan, 0)
+    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.05, None, 0.9, 5e-4,
+                          stamp, plan, 0)
     torch.cuda.synchronize()
     xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
     orc.apply_sgd(xv, g[lo:hi].copy(), mv, 0.05, 0.9, 5e-4)
@@ -558,72 +558,77 @@ def test_apply_snapshot_plan_values_tags_classification_and_next_gather(N, orc, 
     want[lo:hi] = xv
     assert np.array_equal(ax.tensor.cpu().numpy(), want)
     assert np.array_equal(ar.tensor.cpu().numpy(), want)
-    t = tags.tensor.view(torch.int32).cpu().numpy()
-    assert (t[lo:hi] == stamp).all() and np.array_equal(t[:lo], t0[:lo]) and np.array_equal(t[hi:], t0[hi:])
+    got_stamps = stamps.cpu().numpy()
+    want_stamps = old.copy()
+    want_stamps[bid] = max(old[bid], stamp)
+    assert np.array_equal(got_stamps, want_stamps)
     assert list(claim[0]) == [12, 0]
-    want_next = np.maximum(t[idx[1]], 12)
+    b_of = np.searchsorted(np.array(bounds[1:-1]), nxt, side="right") + 1
+    want_next = np.maximum(np.maximum(old[0], old[b_of]), 12)
+    want_next = np.where((nxt >= lo) & (nxt < hi), np.maximum(want_next, stamp), want_next)
     assert np.array_equal(tag_host[1], want_next)
     assert np.array_equal(tag_dev[1].cpu().numpy(), want_next)
     assert int(done.item()) == 0                  # counter reset for the next launch
-    # second launch: clean (k_claim = 10 <= every tag), floor raises old tags
-    avg[0] = 10
-    plan2 = N.TagPlan(dev["idx"] + 16 * k, tag_dev[2].data_ptr(), dev["tag_host"] + 8 * k,
-                      tag_dev[0].data_ptr(), dev["claim"] + 16, dev["avg"], done.data_ptr(), k)
-    idx[2] = np.arange(k) * (n // k)
-    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, tags.ptr, n, lo, hi, 0.0, None, 0.0,
-                          0.0, stamp + 1, plan2, 0)
+    # second launch: clean (k_claim = 10 <= every tag)
+    cell.fill_(10)
+    plan2 = N.TagPlan(None, None, None, tag_dev[0].data_ptr(), dev["claim"] + 16, cell.data_ptr(),
+                      done.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
+    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.0, None, 0.0,
+                          0.0, stamp - 5, plan2, 0)
     torch.cuda.synchronize()
     assert list(claim[1]) == [10, 1]
-    t = tags.tensor.view(torch.int32).cpu().numpy()
-    assert np.array_equal(tag_host[2], np.maximum(t[idx[2]], 10))
-    for a in (ax, ag, am, ar, tags):
+    assert int(stamps[bid].item()) == max(old[bid], stamp)   # max: an older stamp never lowers it
+    first = torch.zeros(k, dtype=torch.int32, device="cuda")
+    N.gather_block_stamps(stamps.data_ptr(), bnd.data_ptr(), nb, idx[1].data_ptr(), k, cell.data_ptr(),
+                          first.data_ptr(), None, 0)
+    torch.cuda.synchronize()
+    st = stamps.cpu().numpy()
+    assert np.array_equal(first.cpu().numpy(), np.maximum(np.maximum(st[0], st[b_of]), 10))
+    for a in (ax, ag, am, ar):
         a.close()
     hb.close()
 
 
-def test_apply_snapshot_plan_concurrent_streams_gather_sees_own_apply(N):
-    """4 streams x 30 fused steps, each gathering the next step's tags at
-    elements of its own block: a gathered tag is never older than the stamp
-    the same stream just wrote there (the gather follows the apply)."""
+def test_apply_snapshot_plan_concurrent_streams(N):
+    """4 streams x 30 fused steps on disjoint blocks with momentum-free -1
+    gradients: every reduction lands; each step's next-step tags at elements
+    of its own block carry its own stamp (read after its own reduction); the
+    block stamps end at every stream's last stamp."""
+    n, k, K, steps = 200_003, 8, 4, 30
     from paper_2203_06638_b200.arena import Arena
 
-    n, k, K, steps = 200_003, 8, 4, 30
     x = Arena(n, 0)
     g = torch.full((n,), -1.0, device="cuda")
-    tags = Arena(n, 0)
     reps = [Arena(n, 0) for _ in range(K)]
     streams = [torch.cuda.Stream() for _ in range(K)]
-    hb = N.HostBuffer(64 + K * (8 * k + 4 * k + 16) * steps)
-    avg = hb.view(np.int64, (1,))
-    avg[0] = 0
-    idx = hb.view(np.int64, (K, steps, k), 64)
-    o_tag = 64 + 8 * K * steps * k
-    tag_host = hb.view(np.int32, (K, steps, k), o_tag)
-    tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
-    done = torch.zeros(K, dtype=torch.int32, device="cuda")
     bounds = np.linspace(0, n, K + 1).astype(np.int64)
+    bnd = torch.tensor(bounds, device="cuda")
+    stamps = torch.zeros(K + 1, dtype=torch.int32, device="cuda")
+    cell = torch.zeros(1, dtype=torch.long, device="cuda")
+    done = torch.zeros(K, dtype=torch.int32, device="cuda")
+    tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
     gen = np.random.default_rng(5)
-    for s in range(K):
-        for t in range(steps):
-            idx[s, t] = np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k, replace=False))
+    idx = torch.tensor(np.stack([[np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k,
+                                                     replace=False)) for _ in range(steps)]
+                                 for s in range(K)]), device="cuda")
     torch.cuda.synchronize()
     for t in range(steps):
         for s, st in enumerate(streams):
-            stamp = 1000 * (s + 1) + t
-            plan = N.TagPlan(hb.dev + 64 + 8 * k * (s * steps + t), tag_dev[s, t].data_ptr(),
-                             hb.dev + o_tag + 4 * k * (s * steps + t), None, None, hb.dev,
-                             done[s].data_ptr(), k)
-            N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, tags.ptr, n,
-                                  int(bounds[s]), int(bounds[s + 1]), 1.0, None, 0.0, 0.0, stamp,
-                                  plan, st.cuda_stream)
+            plan = N.TagPlan(idx[s, t].data_ptr(), tag_dev[s, t].data_ptr(), None, None, None,
+                             cell.data_ptr(), done[s].data_ptr(), stamps.data_ptr(), bnd.data_ptr(), K,
+                             s + 1, k)
+            N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, None, n, int(bounds[s]),
+                                  int(bounds[s + 1]), 1.0, None, 0.0, 0.0, 1000 * (s + 1) + t, plan,
+                                  st.cuda_stream)
     torch.cuda.synchronize()
     assert bool((x.tensor == float(steps)).all())
+    td = tag_dev.cpu().numpy()
     for s in range(K):
         for t in range(steps):
-            assert (tag_host[s, t] == 1000 * (s + 1) + t).all(), (s, t)
-    for a in [x, tags] + reps:
+            assert (td[s, t] == 1000 * (s + 1) + t).all(), (s, t)
+    assert stamps.cpu().tolist() == [0] + [1000 * (s + 1) + steps - 1 for s in range(K)]
+    for a in [x] + reps:
         a.close()
-    hb.close()
 
 
 def test_gather_floor_and_classify(N):

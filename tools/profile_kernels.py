@@ -35,23 +35,33 @@ for d in (11_220_132, 25_557_032):
     for a in (x, g, m, tg):
         a.close()
 # K1+K3 fused (the async default) at d20 and d50 with a partial block: the
-# engine's launch, with the K5 plan (classify this step, stamp, gather the
-# next step's 16 tags in the last CTA) — and without tags for comparison
-# as the engine lays it out: indices and the round-stamp cell on the device,
-# the gathered tags and the (k_claim, clean) record written to mapped host memory
+# engine's launch with the K5 plan (classify this step, read the next step's
+# 16 sampled tags before their values, publish the block stamp from the last
+# CTA) — and without K5 for comparison; laid out as the engine does it:
+# indices, stamps and the round-stamp cell on the device, the sampled tags
+# and the (k_claim, clean) record written to mapped host memory
 hb = N.HostBuffer(4096)
 idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long, device="cuda")
 cell = torch.zeros(1, dtype=torch.long, device="cuda")
 dev_tags = torch.zeros(32, dtype=torch.int32, device="cuda")
 done = torch.zeros(1, dtype=torch.int32, device="cuda")
-plan = N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), hb.dev + 512, dev_tags[:16].data_ptr(),
-                 hb.dev + 1024, cell.data_ptr(), done.data_ptr(), 16)
+stamps = torch.zeros(5, dtype=torch.int32, device="cuda")
+
+
+def make_plan(d, lo, hi):
+    bnd = torch.tensor([0, lo, hi, d], dtype=torch.long, device="cuda")
+    return bnd, N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), hb.dev + 512,
+                          dev_tags[:16].data_ptr(), hb.dev + 1024, cell.data_ptr(), done.data_ptr(),
+                          stamps.data_ptr(), bnd.data_ptr(), 3, 2, 16)
+
+
 for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000)):
     x, g, m, rep, tg = (Arena(d, 0) for _ in range(5))
     x.tensor.normal_(), g.tensor.normal_()
+    bnd, plan = make_plan(d, lo, hi)
     for _ in range(2):
         flush()
-        N.apply_snapshot_plan(x.ptr, g.ptr, m.ptr, rep.ptr, tg.ptr, d, lo, hi, 1e-3, None, 0.9, 5e-4,
+        N.apply_snapshot_plan(x.ptr, g.ptr, m.ptr, rep.ptr, None, d, lo, hi, 1e-3, None, 0.9, 5e-4,
                               3, plan, st)
         flush()
         N.apply_snapshot(x.ptr, g.ptr, m.ptr, rep.ptr, None, d, lo, hi, 1e-3, None, 0.9, 5e-4, 3, st)
