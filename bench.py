@@ -3,8 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (BASELINE.json configs[1]): ResNet-20 on synthetic CIFAR-10-shaped
-data (N(0,1) images, 50,000 x 32x32x3 stored in the bf16 compute dtype = 307 MB resident in HBM, larger
-than the 126 MB L2), LPP-SGD with U = 4 Hogwild CUDA streams per GPU,
+data (N(0,1) images, 50,000 x 3x32x32 fp32 = 614 MB resident in HBM, larger
+than the 126 MB L2), fp32 convolutions with TF32 off (the reference arm's
+precision; the bf16 variant is reported beside it as value_bf16 / e2e_bf16),
+LPP-SGD with U = 4 Hogwild CUDA streams per GPU,
 B = 128 per stream, 4-block PASSM+ partition (balanced_boundaries),
 momentum 0.9, wd 5e-4, cosine lr with warm-up, averaging every tick until
 T/2 then every 16 (SyncScheme defaults).  One *step* = one minibatch on
@@ -12,19 +14,22 @@ every updater stream (U x B images per GPU); K steps are timed with CUDA
 events (max over ranks), after W untimed warm-up steps.
 
 Extra keys beyond the base contract:
-  roofline      the fused apply kernel (K1+K3), timed live with CUDA events
-                around every launch in the timed region, algorithmic bytes
-                (block 12 B/elem + 8 momentum + 4 tag, replica refresh 4-8)
-                vs MEASURED_PEAKS.json hbm_gbs; + the ncu standalone time and
-                DRAM traffic of the same kernel (profiles/)
+  roofline      the fused apply kernel (K1+K3 with the K5 plan), timed live
+                with CUDA events around every launch in the timed region,
+                algorithmic bytes (block 12 B/elem + 8 momentum, replica
+                refresh 4 inside / 8 outside the block; K5 is per-block
+                stamps, O(1) bytes) vs MEASURED_PEAKS.json hbm_gbs; + the ncu
+                standalone time and DRAM traffic of the same kernel (profiles/)
   e2e           the same metric through Trainer(..., host_batches=True,
                 read_loss=True): each step's batch gathered from pinned host
                 memory and copied H2D inside the step (native updater loop,
                 copy stream), each step's loss copied D2H
   cpu_baseline  oracle/engine_port.py (threaded CPU LPP-SGD, the reference's
                 compiled _atomics) on this host, bounded sample, rank 0, N=1
-  baselines     the box's own synchronous MB-SGD (same per-GPU B, 1 stream)
-                and LAP-SGD (same engine, no partial backprop)
+  baselines     the box's own synchronous B1 MB-SGD (same per-GPU B, and
+                U x B per GPU) and B2 L-SGD / PL-SGD at the same N (NCCL
+                all-reduce for N > 1), and LAP-SGD (same engine, no partial
+                backprop), all fp32
   resnet18      config C2 (CIFAR-100-shaped, d = 11.2M): LPP vs MB-SGD images/s
                 and the apply kernel's in-situ HBM roofline
   resnet50      config C3 (ImageNet-shaped, d = 25.6M, B = 32 per stream,

@@ -566,16 +566,27 @@ __global__ void __launch_bounds__(kThreads)
   // owner of vector v is thread v mod stride (iteration v / stride); a tail
   // element e >= 4 nvec belongs to block 0, thread (e - 4 nvec) mod blockDim
   __shared__ int64_t sidx[32];
+  __shared__ unsigned sown[kThreads];
   unsigned own = 0;
   if (PLAN && plan.next_idx) {
-    if (threadIdx.x < plan.k) sidx[threadIdx.x] = plan.next_idx[threadIdx.x];
+    // threads j < k place sampled element j with its owning thread, if that
+    // thread is in this CTA (one division per element, not per thread)
+    sown[threadIdx.x] = 0u;
     __syncthreads();
-    for (int j = 0; j < plan.k; ++j) {
-      const size_t e = (size_t)sidx[j], v = e / 4;
-      const bool mine = v < nvec ? (v % stride == tid)
-                                 : (blockIdx.x == 0 && (e - 4 * nvec) % blockDim.x == threadIdx.x);
-      if (mine) own |= 1u << j;
+    if (threadIdx.x < plan.k) {
+      const int64_t e = plan.next_idx[threadIdx.x];
+      sidx[threadIdx.x] = e;
+      const size_t v = (size_t)e / 4;
+      size_t owner;
+      if (v < nvec) {
+        owner = v % stride;
+      } else {  // tail element: block 0, thread (e - 4 nvec) mod blockDim
+        owner = ((size_t)e - 4 * nvec) % blockDim.x;
+      }
+      if (owner / blockDim.x == blockIdx.x) atomicOr(&sown[owner % blockDim.x], 1u << threadIdx.x);
     }
+    __syncthreads();
+    own = sown[threadIdx.x];
   }
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element
