@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define LPP_ABI_VERSION 2
+#define LPP_ABI_VERSION 3
 
 /* error codes */
 #define LPP_OK 0
@@ -408,8 +408,6 @@ typedef struct {
   uint64_t tag_seed;
   int64_t* tag_idx_pinned;        /* [in_flight + 2][tag_pick] */
   int64_t* tag_idx_dev;           /* [tag_pick] */
-  int32_t* tag_out_dev;           /* [in_flight + 2][tag_pick] */
-  int32_t* tag_out_pinned;        /* [in_flight + 2][tag_pick] */
   int64_t* classified;            /* host counters (+= per classified step) */
   int64_t* clean;
   double apply_bytes_per_elem;    /* algorithmic bytes per block element */
@@ -472,15 +470,17 @@ typedef struct {
   /* K5 in the reference's order (lpp_tag_plan): the sampled-tag indices are
    * drawn into the pinned ring tag_idx_pinned and copied (stream-ordered,
    * before the step's graph) into the device ring tag_idx_dev, both
-   * [in_flight + 2][tag_pick]; the effective tags go to tag_out_dev and the
-   * host-mapped tag_out_pinned (device view tag_out_host_dev); each step's
-   * (k_claim, clean) is written by its apply kernel into the host-mapped
-   * claim_ring[slot] (device view claim_ring_dev), k_claim read from the
-   * worker's device round-stamp cell avg_cell_dev; done_ctr: a 4-byte zeroed
-   * device counter private to this updater */
-  int64_t* claim_ring;            /* [in_flight + 2][2] host view */
-  int64_t* claim_ring_dev;
-  int32_t* tag_out_host_dev;
+   * [in_flight + 2][tag_pick].  Step records, per in-flight slot s, in
+   * rec_cols int64 cells: {k_claim, clean, tags[tag_pick] as int32} — on the
+   * device (rec_dev, written by the kernels: the step's tags at its
+   * snapshot, its (k_claim, clean) by its apply), copied into rec_pinned[s]
+   * after the apply; k_claim is read from the worker's device round-stamp
+   * cell avg_cell_dev; done_ctr: a 4-byte zeroed device counter private to
+   * this updater.  (Host-mapped outputs measured +1.5 us each on the
+   * kernel: its completion waits for the system-scope write flush.) */
+  int64_t* rec_dev;
+  int64_t* rec_pinned;
+  int32_t rec_cols;
   const int64_t* avg_cell_dev;
   uint32_t* done_ctr;
   /* fused runs: the worker's per-block write stamps [num_blocks + 1] and the

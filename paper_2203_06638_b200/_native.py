@@ -64,8 +64,7 @@ class UpdaterCfg(ctypes.Structure):
         ("mu", _c.c_float), ("wd", _c.c_float), ("apply_mode", _c.c_int32),
         ("in_flight", _c.c_int32),
         ("tag_pick", _c.c_int32), ("time_apply", _c.c_int32), ("tag_seed", _c.c_uint64),
-        ("tag_idx_pinned", _vp), ("tag_idx_dev", _vp), ("tag_out_dev", _vp),
-        ("tag_out_pinned", _vp), ("classified", _vp), ("clean", _vp),
+        ("tag_idx_pinned", _vp), ("tag_idx_dev", _vp), ("classified", _vp), ("clean", _vp),
         ("apply_bytes_per_elem", _c.c_double), ("stream", _vp), ("apply_stream", _vp),
         ("host_feats", _vp), ("host_labels", _vp), ("n_rows", _c.c_int64), ("row_bytes", _c.c_int64),
         ("label_bytes", _c.c_int64), ("batch", _c.c_int32), ("read_loss", _c.c_int32),
@@ -77,8 +76,7 @@ class UpdaterCfg(ctypes.Structure):
         ("rec_tags", _vp), ("rec_cap", _c.c_int64), ("rec_count", _vp),
         ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
-        ("claim_ring", _vp), ("claim_ring_dev", _vp), ("tag_out_host_dev", _vp),
-        ("avg_cell_dev", _vp), ("done_ctr", _vp), ("block_stamps", _vp), ("block_bounds_dev", _vp),
+        ("rec_dev", _vp), ("rec_pinned", _vp), ("rec_cols", _c.c_int32), ("avg_cell_dev", _vp), ("done_ctr", _vp), ("block_stamps", _vp), ("block_bounds_dev", _vp),
     ]
 
 

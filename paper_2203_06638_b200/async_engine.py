@@ -134,20 +134,21 @@ class _Worker:
         self.last_avg_stamp = AtomicCounter(0)
         self.round_cell = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.avg_dev = self.round_cell.data_ptr()
-        # host-mapped memory the kernels write directly (lpp_host_alloc): per
-        # updater and in-flight slot, the gathered effective tags (int32) and
-        # the apply's (k_claim, clean) record; the sampled-tag indices are
-        # drawn into a pinned ring and copied to a device ring in stream order
-        self._o_tag = 0
-        self._o_claim = 4 * U * depth * k
-        self.hostmem = N.HostBuffer(self._o_claim + 16 * U * depth)
+        # K5 step records, per updater and in-flight slot: {k_claim, clean,
+        # tags[k] (int32)} — written on the device by the kernels (the tags at
+        # the step's snapshot, (k_claim, clean) by its apply), copied to the
+        # pinned ring after the apply; the sampled-tag indices go the other
+        # way (pinned ring -> device ring, before the step's graph)
+        self.rec_cols = 2 + (k + 1) // 2
         if cfg.tracks:
             self.tag_idx_pinned = torch.zeros((U, depth, k), dtype=torch.long, pin_memory=True)
             self.tag_idx_np = self.tag_idx_pinned.numpy()
             self.tag_idx_ring = torch.zeros((U, depth, k), dtype=torch.long, device=self.dev)
-            self.tag_np = self.hostmem.view(np.int32, (U, depth, k), self._o_tag)
-            self.claim_np = self.hostmem.view(np.int64, (U, depth, 2), self._o_claim)
-            self.tag_out_dev = torch.zeros((U, depth, k), dtype=torch.int32, device=self.dev)
+            self.rec_dev = torch.zeros((U, depth, self.rec_cols), dtype=torch.long, device=self.dev)
+            self.rec_pinned = torch.zeros((U, depth, self.rec_cols), dtype=torch.long, pin_memory=True)
+            rec_np = self.rec_pinned.numpy()
+            self.claim_np = rec_np[:, :, :2]
+            self.tag_np = rec_np[:, :, 2:].view(np.int32)
             self.done_ctr = torch.zeros(U, dtype=torch.int32, device=self.dev)
             # fused runs: per-block write stamps (an update writes one block
             # range) and the block boundaries, on the device
@@ -176,16 +177,17 @@ class _Worker:
                      8 * k, stream_ptr)
         return self.tag_idx_ring[r, slot].data_ptr()
 
-    def tag_host_dev(self, r: int, slot: int) -> int:
-        depth = self.tag_np.shape[1]
-        return self.hostmem.dev + self._o_tag + 4 * self.kk * (r * depth + slot)
+    def rec_claim(self, r: int, slot: int) -> int:
+        """Device address of step record (r, slot): (k_claim, clean)."""
+        return self.rec_dev[r, slot].data_ptr()
 
-    def claim_dev(self, r: int, slot: int) -> int:
-        depth = self.tag_np.shape[1]
-        return self.hostmem.dev + self._o_claim + 16 * (r * depth + slot)
+    def rec_tags(self, r: int, slot: int) -> int:
+        """Device address of step record (r, slot): its sampled tags (int32)."""
+        return self.rec_dev[r, slot].data_ptr() + 16
 
-    def host_addr(self, dev_addr: int) -> int:
-        return self.hostmem.ptr + (dev_addr - self.hostmem.dev)
+    def copy_rec(self, r: int, slot: int, stream_ptr: int) -> None:
+        N.copy_async(self.rec_pinned[r, slot].data_ptr(), self.rec_dev[r, slot].data_ptr(),
+                     8 * self.rec_cols, stream_ptr)
 
     def publish_round(self, u: int, stream: torch.cuda.Stream) -> None:
         """The round with stamp u is applied to this arena: device cell first
@@ -262,7 +264,6 @@ class _Worker:
         if self.store.tag_arena is not None:
             self.store.tag_arena.close()
         self.tags = None
-        self.hostmem.close()
 
 
 class _Engine(NativeLoops):
@@ -445,6 +446,8 @@ class _Engine(NativeLoops):
             if self.time_apply:
                 e1.record(astream)
                 self.apply_events.append((e0, e1, self.apply_bytes_per_elem * blk.length))
+            if tracks:
+                w.copy_rec(r, slot, sp)             # (k_claim, clean) + tags -> host
             if astream is not stream:
                 w.apply_done[r].record(astream)
                 stream.wait_event(w.apply_done[r])
@@ -499,19 +502,17 @@ class _Engine(NativeLoops):
         if self.fused():   # fused runs stamp blocks, not elements
             N.gather_block_stamps(w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
                                   self.cfg.partition.num_blocks, idx_dev, k, w.avg_dev,
-                                  w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
+                                  w.rec_tags(r, slot), None, sp)
         else:
-            N.gather_tags_floor(w.tag_arena.ptr, idx_dev, k, w.avg_dev,
-                                w.tag_out_dev[r, slot].data_ptr(), w.tag_host_dev(r, slot), sp)
+            N.gather_tags_floor(w.tag_arena.ptr, idx_dev, k, w.avg_dev, w.rec_tags(r, slot), None, sp)
 
     def classify_on_device(self, w: _Worker, r: int, slot: int, stream_ptr: int) -> None:
         """K5 classification at apply time (engine.py:353-362): k_claim is
         read by the kernel when it runs, i.e. after the step's gradient."""
         if self.cfg.record_mode == "full":
-            N.classify(w.min_dev[r, slot].data_ptr(), 1, w.avg_dev, w.claim_dev(r, slot), stream_ptr)
+            N.classify(w.min_dev[r, slot].data_ptr(), 1, w.avg_dev, w.rec_claim(r, slot), stream_ptr)
         else:
-            N.classify(w.tag_out_dev[r, slot].data_ptr(), w.tag_pick, w.avg_dev,
-                       w.claim_dev(r, slot), stream_ptr)
+            N.classify(w.rec_tags(r, slot), w.tag_pick, w.avg_dev, w.rec_claim(r, slot), stream_ptr)
 
     def step_fused(self, w: _Worker, r: int, block_id: int, lr: float, batch, slot: int,
                    next_slot: int, u: int, first: bool, tag_idx, next_tag_idx,
@@ -546,9 +547,8 @@ class _Engine(NativeLoops):
                 # its gradient), stamp, and gather the next step's tags after
                 # this apply landed (engine.py:343-362 order)
                 k = w.tag_pick
-                plan = N.TagPlan(next_idx_dev, w.tag_out_dev[r, next_slot].data_ptr(),
-                                 w.tag_host_dev(r, next_slot), w.tag_out_dev[r, slot].data_ptr(),
-                                 w.claim_dev(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(),
+                plan = N.TagPlan(next_idx_dev, w.rec_tags(r, next_slot), None, w.rec_tags(r, slot),
+                                 w.rec_claim(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(),
                                  w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
                                  cfg.partition.num_blocks, block_id, k)
             mom = w.moms[r]
@@ -579,6 +579,8 @@ class _Engine(NativeLoops):
                 nbytes = self.apply_bytes_per_elem * blk.length + 4 * (self.dim - blk.length) \
                     + 4 * self.dim
                 self.apply_events.append((e0, e1, nbytes))
+            if tracks:
+                w.copy_rec(r, slot, sp)             # (k_claim, clean) + tags -> host
             if astream is not stream:
                 w.apply_done[r].record(astream)
                 stream.wait_event(w.apply_done[r])

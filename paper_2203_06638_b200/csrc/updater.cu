@@ -236,9 +236,8 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     return set_err(LPP_E_VALUE, "updater_run: rank %d outside [1, %d]", c->rank, c->num_blocks);
   const bool tagged = c->tags != nullptr;
   const int K = tagged ? c->tag_pick : 0;
-  if (K > 0 && (!c->tag_idx_pinned || !c->tag_idx_dev || !c->tag_out_dev || !c->tag_out_pinned ||
-                !c->tag_out_host_dev || !c->claim_ring || !c->claim_ring_dev ||
-                !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean ||
+  if (K > 0 && (!c->tag_idx_pinned || !c->tag_idx_dev || !c->rec_dev || !c->rec_pinned ||
+                c->rec_cols < 2 + (K + 1) / 2 || !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean ||
                 (c->fused && (!c->block_stamps || !c->block_bounds_dev))))
     return set_err(LPP_E_VALUE, "updater_run: tag sampling buffers missing");
   const int F = c->in_flight < 1 ? 1 : c->in_flight;
@@ -325,14 +324,24 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if (!c->host_rng) draw_tags(&tag_state, (int64_t)c->n, K, c->tag_idx_pinned + o);
     return lpp_copy_async(c->tag_idx_dev + o, c->tag_idx_pinned + o, 8 * (size_t)K, stream);
   };
+  // step records: slot s = {k_claim, clean, tags[K] (int32)} in rec_cols cells
+  auto rec_tags = [&](int slot) -> int32_t* {
+    return reinterpret_cast<int32_t*>(c->rec_dev + (size_t)slot * c->rec_cols + 2);
+  };
+  auto rec_claim = [&](int slot) -> int64_t* { return c->rec_dev + (size_t)slot * c->rec_cols; };
   auto gather = [&](int slot) -> int {
     const size_t o = (size_t)slot * K;
     if (c->fused)  // fused runs stamp blocks, not elements
       return lpp_gather_block_stamps(c->block_stamps, c->block_bounds_dev, c->num_blocks,
                                      c->tag_idx_dev + o, (size_t)K, c->avg_cell_dev,
-                                     c->tag_out_dev + o, c->tag_out_host_dev + o, stream);
+                                     rec_tags(slot), nullptr, stream);
     return lpp_gather_tags_floor(c->tags, c->tag_idx_dev + o, (size_t)K, c->avg_cell_dev,
-                                 c->tag_out_dev + o, c->tag_out_host_dev + o, stream);
+                                 rec_tags(slot), nullptr, stream);
+  };
+  // the step's record to the host once its apply wrote (k_claim, clean)
+  auto copy_rec = [&](int slot, cudaStream_t st_) -> int {
+    const size_t o = (size_t)slot * c->rec_cols;
+    return lpp_copy_async(c->rec_pinned + o, c->rec_dev + o, 8 * (size_t)c->rec_cols, st_);
   };
   // once a step's event completed: classify its tags, collect its apply time
   auto retire = [&](int k) -> int {
@@ -343,10 +352,10 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (K > 0) {
       // (k_claim, clean) as the step's apply kernel saw them
-      const int32_t* tg = c->tag_out_pinned + (size_t)slot_of[k] * K;
-      const volatile int64_t* cr = c->claim_ring + 2 * (size_t)slot_of[k];
-      const int64_t kc = cr[0];
-      const bool clean = cr[1] != 0;
+      const int64_t* row = c->rec_pinned + (size_t)slot_of[k] * c->rec_cols;
+      const int32_t* tg = reinterpret_cast<const int32_t*>(row + 2);
+      const int64_t kc = row[0];
+      const bool clean = row[1] != 0;
       __atomic_fetch_add(c->classified, 1, __ATOMIC_ACQ_REL);
       if (clean) __atomic_fetch_add(c->clean, 1, __ATOMIC_ACQ_REL);
       const int64_t ts = step_of[k];
@@ -459,11 +468,10 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t0.ev[k], astream));
     if (c->fused && K > 0) {
       // K1+K3 + K5: classify this step, stamp, gather the next step's tags
-      const size_t o = (size_t)slot * K, on = (size_t)next_slot * K;
-      lpp_tag_plan plan{c->tag_idx_dev + on, c->tag_out_dev + on, c->tag_out_host_dev + on,
-                        c->tag_out_dev + o, c->claim_ring_dev + 2 * (size_t)slot, c->avg_cell_dev,
-                        c->done_ctr, c->block_stamps, c->block_bounds_dev,
-                        c->num_blocks, b, K};
+      const size_t on = (size_t)next_slot * K;
+      lpp_tag_plan plan{c->tag_idx_dev + on, rec_tags(next_slot), nullptr, rec_tags(slot),
+                        rec_claim(slot), c->avg_cell_dev, c->done_ctr, c->block_stamps,
+                        c->block_bounds_dev, c->num_blocks, b, K};
       rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, nullptr, c->n, (size_t)lo,
                                    (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u, &plan,
                                    astream);
@@ -477,8 +485,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
                     4.0 * (double)c->n;
     } else if (tagged) {
       if (K > 0) {  // k_claim after the gradient, on the apply's stream
-        rc = lpp_classify(c->tag_out_dev + (size_t)slot * K, (size_t)K, c->avg_cell_dev,
-                          c->claim_ring_dev + 2 * (size_t)slot, astream);
+        rc = lpp_classify(rec_tags(slot), (size_t)K, c->avg_cell_dev, rec_claim(slot), astream);
         if (rc != LPP_OK) return rc;
       }
       rc = lpp_apply_sgd_tagged(c->x + lo, c->g + lo, c->m ? c->m + lo : nullptr, (size_t)len,
@@ -492,6 +499,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (rc != LPP_OK) return rc;
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t1.ev[k], astream));
+    if (K > 0 && (rc = copy_rec(slot, astream)) != LPP_OK) return rc;
     if (side) {
       CUDA_TRY(cudaEventRecord(order.ev[1], astream));
       CUDA_TRY(cudaStreamWaitEvent(stream, order.ev[1], 0));

@@ -109,15 +109,13 @@ class NativeLoops:
         c.time_apply = int(self.time_apply)
         c.tag_seed = (cfg.seed * 1_000_003 + w.q * 1009 + r + 1) & (2**64 - 1)
         if tracks:
-            # K5 rings in host-mapped memory (indices, effective tags, the
-            # apply kernels' (k_claim, clean) records) + the device tag ring
+            # K5: sampled-index rings (pinned -> device), step records
+            # (device -> pinned after each apply), round cell, block stamps
             c.tag_idx_dev = w.tag_idx_ring[r].data_ptr()
             c.tag_idx_pinned = w.tag_idx_pinned[r].data_ptr()
-            c.tag_out_dev = w.tag_out_dev[r].data_ptr()
-            c.tag_out_host_dev = w.tag_host_dev(r, 0)
-            c.tag_out_pinned = w.host_addr(c.tag_out_host_dev)
-            c.claim_ring_dev = w.claim_dev(r, 0)
-            c.claim_ring = w.host_addr(c.claim_ring_dev)
+            c.rec_dev = w.rec_dev[r].data_ptr()
+            c.rec_pinned = w.rec_pinned[r].data_ptr()
+            c.rec_cols = w.rec_cols
             c.avg_cell_dev = w.avg_dev
             c.done_ctr = w.done_ctr[r].data_ptr()
             c.block_stamps = w.block_stamps.data_ptr()

@@ -38,9 +38,8 @@ for d in (11_220_132, 25_557_032):
 # engine's launch with the K5 plan (classify this step, read the next step's
 # 16 sampled tags before their values, publish the block stamp from the last
 # CTA) — and without K5 for comparison; laid out as the engine does it:
-# indices, stamps and the round-stamp cell on the device, the sampled tags
-# and the (k_claim, clean) record written to mapped host memory
-hb = N.HostBuffer(4096)
+# indices, stamps, the round-stamp cell and the step records on the device
+claim = torch.zeros(2, dtype=torch.long, device="cuda")
 idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long, device="cuda")
 cell = torch.zeros(1, dtype=torch.long, device="cuda")
 dev_tags = torch.zeros(32, dtype=torch.int32, device="cuda")
@@ -50,8 +49,8 @@ stamps = torch.zeros(5, dtype=torch.int32, device="cuda")
 
 def make_plan(d, lo, hi):
     bnd = torch.tensor([0, lo, hi, d], dtype=torch.long, device="cuda")
-    return bnd, N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), hb.dev + 512,
-                          dev_tags[:16].data_ptr(), hb.dev + 1024, cell.data_ptr(), done.data_ptr(),
+    return bnd, N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), None,
+                          dev_tags[:16].data_ptr(), claim.data_ptr(), cell.data_ptr(), done.data_ptr(),
                           stamps.data_ptr(), bnd.data_ptr(), 3, 2, 16)
 
 
