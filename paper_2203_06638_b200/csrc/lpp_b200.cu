@@ -515,15 +515,17 @@ __device__ __forceinline__ int plan_tag_of(const TagPlanDev& plan, int64_t e, si
   return t;
 }
 
-// last CTA: publish this update's block stamp (after every CTA's reductions)
+// last CTA: publish this update's block stamp (after every CTA's reductions).
+// No shared memory anywhere in the plan kernel: a CTA with static shared
+// memory cannot start on an SM whose carveout the running convolutions hold,
+// and in situ it then waits for whole convolution CTAs to drain (measured:
+// 172 us per launch inside the ResNet-20 step vs 26 us without)
 __device__ __forceinline__ void plan_publish(const TagPlanDev& plan, int stamp) {
-  __shared__ int is_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_ar_gpu();  // this CTA's reductions before the count
-    unsigned old = atomicAdd(plan.done, 1u);
-    is_last = (old == gridDim.x - 1);
-    if (is_last) {
+    const unsigned old = atomicAdd(plan.done, 1u);
+    if (old == gridDim.x - 1) {
       fence_ar_gpu();
       atomicMax(plan.block_stamps + plan.bid, stamp);
       *plan.done = 0u;
@@ -565,28 +567,19 @@ __global__ void __launch_bounds__(kThreads)
   // which of the next step's sampled elements this thread refreshes: the
   // owner of vector v is thread v mod stride (iteration v / stride); a tail
   // element e >= 4 nvec belongs to block 0, thread (e - 4 nvec) mod blockDim
-  __shared__ int64_t sidx[32];
-  __shared__ unsigned sown[kThreads];
+  // which of the next step's sampled elements this thread refreshes: the
+  // plan launch uses a power-of-two grid, so vector v belongs to thread
+  // v & (stride - 1); a tail element e >= 4 nvec to block 0, thread
+  // (e - 4 nvec) mod blockDim (the index loads are warp-uniform L1 hits)
   unsigned own = 0;
   if (PLAN && plan.next_idx) {
-    // threads j < k place sampled element j with its owning thread, if that
-    // thread is in this CTA (one division per element, not per thread)
-    sown[threadIdx.x] = 0u;
-    __syncthreads();
-    if (threadIdx.x < plan.k) {
-      const int64_t e = plan.next_idx[threadIdx.x];
-      sidx[threadIdx.x] = e;
-      const size_t v = (size_t)e / 4;
-      size_t owner;
-      if (v < nvec) {
-        owner = v % stride;
-      } else {  // tail element: block 0, thread (e - 4 nvec) mod blockDim
-        owner = ((size_t)e - 4 * nvec) % blockDim.x;
-      }
-      if (owner / blockDim.x == blockIdx.x) atomicOr(&sown[owner % blockDim.x], 1u << threadIdx.x);
+    const size_t mask = stride - 1;
+    for (int j = 0; j < plan.k; ++j) {
+      const size_t e = (size_t)__ldg(plan.next_idx + j), v = e >> 2;
+      const bool mine = v < nvec ? ((v & mask) == tid)
+                                 : (blockIdx.x == 0 && ((e - 4 * nvec) & (kThreads - 1)) == threadIdx.x);
+      if (mine) own |= 1u << j;
     }
-    __syncthreads();
-    own = sown[threadIdx.x];
   }
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element
@@ -595,8 +588,9 @@ __global__ void __launch_bounds__(kThreads)
     if (PLAN && own) {  // sampled elements of this vector: tags before values
       for (unsigned bits = own; bits; bits &= bits - 1) {
         const int j = __ffs(bits) - 1;
-        if ((size_t)sidx[j] / 4 == i) {
-          const int t = plan_tag_of(plan, sidx[j], lo, hi, stamp);
+        const int64_t e = __ldg(plan.next_idx + j);
+        if ((size_t)e / 4 == i) {
+          const int t = plan_tag_of(plan, e, lo, hi, stamp);
           plan.next_dev[j] = t;
           if (plan.next_host) plan.next_host[j] = t;
         }
@@ -630,8 +624,8 @@ __global__ void __launch_bounds__(kThreads)
       if (PLAN && own)
         for (unsigned bits = own; bits; bits &= bits - 1) {
           const int j = __ffs(bits) - 1;
-          if ((size_t)sidx[j] == e) {
-            const int t = plan_tag_of(plan, sidx[j], lo, hi, stamp);
+          if ((size_t)__ldg(plan.next_idx + j) == e) {
+            const int t = plan_tag_of(plan, (int64_t)e, lo, hi, stamp);
             plan.next_dev[j] = t;
             if (plan.next_host) plan.next_host[j] = t;
           }
@@ -702,6 +696,10 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     return e ? std::atol(e) : 0L;
   }();
   if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
+  // the plan kernel finds a sampled element's owner as v & (stride - 1):
+  // round its grid down to a power of two (267 -> 256 CTAs at d20)
+  if (plan)
+    while (grid & (grid - 1)) grid &= grid - 1;
   cudaStream_t st = (cudaStream_t)stream;
   bool WD = wd != 0.f, MOM = mu != 0.f;
   // one vector per thread per grid stride: unrolling (2, 4 vectors with all
