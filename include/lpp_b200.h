@@ -137,9 +137,8 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
  * gradient, then the apply), with per-BLOCK write stamps: every update
  * writes one whole block range, so an element's tag is the newest stamp of
  * the blocks covering it (block 0 = all, and its partial block).
- *   block_stamps[block_id] = max(., stamp), by the last CTA once every
- *       element reduction of this launch is performed (a completion
- *       counter `done`, zero before the first launch, private to the stream)
+ *   block_stamps[block_id] is NOT raised here: call lpp_publish_stamp next
+ *       on the same stream (after every element reduction is performed)
  *   cur_claim[0..1] = (k_claim, clean): k_claim = *avg_cell read when the
  *       kernel starts (after this step's gradient), clean = all of this
  *       step's k tags cur_dev[j] >= k_claim              (cur_claim may be NULL)
@@ -159,7 +158,6 @@ typedef struct lpp_tag_plan {
   const int32_t* cur_dev;
   int64_t* cur_claim;
   const int64_t* avg_cell;
-  uint32_t* done;
   int32_t* block_stamps;
   const int64_t* block_bounds;
   int32_t num_blocks;
@@ -243,6 +241,9 @@ int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
 int lpp_gather_block_stamps(const int32_t* stamps, const int64_t* bounds, int nb,
                             const int64_t* idx, size_t k, const int64_t* floor_cell,
                             int32_t* out_dev, int32_t* out_host, void* stream);
+/* stamps[block_id] = max(stamps[block_id], stamp), in stream order: launched
+ * right after an update's lpp_apply_snapshot_plan on the same stream */
+int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream);
 /* *dev = v in stream order (the round-stamp cell the apply kernels read) */
 int lpp_set_i64(int64_t* dev, int64_t v, void* stream);
 /* classification at apply time (engine.py:353-362) for the unfused paths:
@@ -475,14 +476,12 @@ typedef struct {
    * device (rec_dev, written by the kernels: the step's tags at its
    * snapshot, its (k_claim, clean) by its apply), copied into rec_pinned[s]
    * after the apply; k_claim is read from the worker's device round-stamp
-   * cell avg_cell_dev; done_ctr: a 4-byte zeroed device counter private to
-   * this updater.  (Host-mapped outputs measured +1.5 us each on the
+   * cell avg_cell_dev.  (Host-mapped outputs measured +1.5 us each on the
    * kernel: its completion waits for the system-scope write flush.) */
   int64_t* rec_dev;
   int64_t* rec_pinned;
   int32_t rec_cols;
   const int64_t* avg_cell_dev;
-  uint32_t* done_ctr;
   /* fused runs: the worker's per-block write stamps [num_blocks + 1] and the
    * block boundaries [num_blocks + 1] on the device (lpp_tag_plan) */
   int32_t* block_stamps;

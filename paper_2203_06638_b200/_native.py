@@ -76,7 +76,8 @@ class UpdaterCfg(ctypes.Structure):
         ("rec_tags", _vp), ("rec_cap", _c.c_int64), ("rec_count", _vp),
         ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
-        ("rec_dev", _vp), ("rec_pinned", _vp), ("rec_cols", _c.c_int32), ("avg_cell_dev", _vp), ("done_ctr", _vp), ("block_stamps", _vp), ("block_bounds_dev", _vp),
+        ("rec_dev", _vp), ("rec_pinned", _vp), ("rec_cols", _c.c_int32), ("avg_cell_dev", _vp),
+        ("block_stamps", _vp), ("block_bounds_dev", _vp),
     ]
 
 
@@ -84,7 +85,7 @@ class TagPlan(ctypes.Structure):
     """``lpp_tag_plan`` (include/lpp_b200.h)."""
 
     _fields_ = [("next_idx", _vp), ("next_dev", _vp), ("next_host", _vp), ("cur_dev", _vp),
-                ("cur_claim", _vp), ("avg_cell", _vp), ("done", _vp), ("block_stamps", _vp),
+                ("cur_claim", _vp), ("avg_cell", _vp), ("block_stamps", _vp),
                 ("block_bounds", _vp), ("num_blocks", _c.c_int32), ("block_id", _c.c_int32),
                 ("k", _c.c_int32)]
 
@@ -152,6 +153,7 @@ _SIGS = {
     "lpp_gather_tags_floor": (_c.c_int, [_vp, _vp, _size, _vp, _vp, _vp, _vp]),
     "lpp_classify": (_c.c_int, [_vp, _size, _vp, _vp, _vp]),
     "lpp_set_i64": (_c.c_int, [_vp, _c.c_int64, _vp]),
+    "lpp_publish_stamp": (_c.c_int, [_vp, _c.c_int, _c.c_int32, _vp]),
     "lpp_gather_block_stamps": (_c.c_int, [_vp, _vp, _c.c_int, _vp, _size, _vp, _vp, _vp, _vp]),
     "lpp_host_alloc": (_c.c_int, [_size, _c.POINTER(_vp), _c.POINTER(_vp)]),
     "lpp_host_free": (_c.c_int, [_vp]),
@@ -334,6 +336,10 @@ def gather_block_stamps(stamps_ptr, bounds_ptr, nb, idx_ptr, k, floor_ptr, out_d
                         stream) -> None:
     check(lib.lpp_gather_block_stamps(stamps_ptr, bounds_ptr, nb, idx_ptr, k, floor_ptr, out_dev_ptr,
                                       out_host_ptr, stream), "gather_block_stamps")
+
+
+def publish_stamp(stamps_ptr: int, block_id: int, stamp: int, stream: int) -> None:
+    check(lib.lpp_publish_stamp(stamps_ptr, block_id, stamp, stream), "publish_stamp")
 
 
 def set_i64(dev_ptr: int, v: int, stream: int) -> None:

@@ -149,7 +149,6 @@ class _Worker:
             rec_np = self.rec_pinned.numpy()
             self.claim_np = rec_np[:, :, :2]
             self.tag_np = rec_np[:, :, 2:].view(np.int32)
-            self.done_ctr = torch.zeros(U, dtype=torch.int32, device=self.dev)
             # fused runs: per-block write stamps (an update writes one block
             # range) and the block boundaries, on the device
             nb = cfg.partition.num_blocks
@@ -548,8 +547,7 @@ class _Engine(NativeLoops):
                 # this apply landed (engine.py:343-362 order)
                 k = w.tag_pick
                 plan = N.TagPlan(next_idx_dev, w.rec_tags(r, next_slot), None, w.rec_tags(r, slot),
-                                 w.rec_claim(r, slot), w.avg_dev, w.done_ctr[r].data_ptr(),
-                                 w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
+                                 w.rec_claim(r, slot), w.avg_dev, w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
                                  cfg.partition.num_blocks, block_id, k)
             mom = w.moms[r]
             astream = stream
@@ -579,6 +577,8 @@ class _Engine(NativeLoops):
                 nbytes = self.apply_bytes_per_elem * blk.length + 4 * (self.dim - blk.length) \
                     + 4 * self.dim
                 self.apply_events.append((e0, e1, nbytes))
+            if plan is not None:                    # K5: this update's block stamp
+                N.publish_stamp(w.block_stamps.data_ptr(), block_id, u, sp)
             if tracks:
                 w.copy_rec(r, slot, sp)             # (k_claim, clean) + tags -> host
             if astream is not stream:

@@ -458,11 +458,12 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 //   * write stamps per BLOCK, not per element: every update writes one
 //     whole block range, so an element's tag is the newest stamp of the (at
 //     most two) blocks covering it — block 0 (full) and its partial block.
-//     The last CTA to finish (a completion counter: each CTA's thread 0
-//     fences after the CTA barrier, then counts) raises its block's stamp
-//     with atomicMax after a fence, so a stamp is visible only once every
-//     element reduction of its update is performed (value before tag,
-//     _atomics.c:346-392) — at no per-element cost;
+//     The stamp is raised by lpp_publish_stamp, the next launch on the same
+//     stream, so it is visible only once every element reduction of its
+//     update is performed (value before tag, _atomics.c:346-392) — at no
+//     per-element cost and with no CTA barrier or fence in this kernel
+//     (in situ, among convolution CTAs, a completion counter + fence per
+//     CTA measured 4x the apply's latency: the CTAs run in many small waves);
 //   * classification of THIS step: block 0 reads k_claim from the worker's
 //     device round-stamp cell when the kernel starts, i.e. after the step's
 //     gradient, and compares the step's sampled tags with it;
@@ -482,7 +483,6 @@ struct TagPlanDev {
   const int* cur_dev;       // this step's effective tags (read at its snapshot)
   int64_t* cur_claim;       // -> this step's (k_claim, clean) (host-mapped; may be null)
   const int64_t* avg_cell;  // the worker's last completed round stamp (device cell)
-  unsigned* done;           // CTA completion counter (device, 0 between launches)
   int* block_stamps;        // [nb + 1] newest stamp per block (device)
   const int64_t* bounds;    // [nb + 1] block boundaries (bounds[0] = 0, bounds[nb] = n)
   int nb;
@@ -513,24 +513,6 @@ __device__ __forceinline__ int plan_tag_of(const TagPlanDev& plan, int64_t e, si
   t = t > fl ? t : fl;
   if ((size_t)e >= lo && (size_t)e < hi && stamp > t) t = stamp;
   return t;
-}
-
-// last CTA: publish this update's block stamp (after every CTA's reductions).
-// No shared memory anywhere in the plan kernel: a CTA with static shared
-// memory cannot start on an SM whose carveout the running convolutions hold,
-// and in situ it then waits for whole convolution CTAs to drain (measured:
-// 172 us per launch inside the ResNet-20 step vs 26 us without)
-__device__ __forceinline__ void plan_publish(const TagPlanDev& plan, int stamp) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_ar_gpu();  // this CTA's reductions before the count
-    const unsigned old = atomicAdd(plan.done, 1u);
-    if (old == gridDim.x - 1) {
-      fence_ar_gpu();
-      atomicMax(plan.block_stamps + plan.bid, stamp);
-      *plan.done = 0u;
-    }
-  }
 }
 
 template <bool WD, bool MOM>
@@ -655,7 +637,6 @@ __global__ void __launch_bounds__(kThreads)
       plan.cur_claim[0] = k_claim;
       plan.cur_claim[1] = clean;
     }
-    plan_publish(plan, stamp);
   }
 }
 
@@ -675,8 +656,8 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
   if (plan) {
     if (plan->k < 0 || plan->k > 32)
       return set_err(LPP_E_VALUE, "apply_snapshot: tag count %d outside [0, 32]", plan->k);
-    if (!plan->done || !plan->block_stamps || !plan->block_bounds || !plan->avg_cell)
-      return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs stamps, bounds, round cell, counter");
+    if (!plan->block_stamps || !plan->block_bounds || !plan->avg_cell)
+      return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs stamps, bounds, round cell");
     if (plan->num_blocks < 1 || plan->block_id < 0 || plan->block_id > plan->num_blocks)
       return set_err(LPP_E_VALUE, "apply_snapshot: block %d outside [0, %d]", plan->block_id,
                      plan->num_blocks);
@@ -684,9 +665,9 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
       return set_err(LPP_E_VALUE, "apply_snapshot: next-step tags need an output");
     if (plan->cur_claim && plan->k > 0 && !plan->cur_dev)
       return set_err(LPP_E_VALUE, "apply_snapshot: classification needs this step's tags");
-    pd = TagPlanDev{plan->next_idx,     plan->next_dev,  plan->next_host,   plan->cur_dev,
-                    plan->cur_claim,    plan->avg_cell,  plan->done,        plan->block_stamps,
-                    plan->block_bounds, plan->num_blocks, plan->block_id,   plan->k};
+    pd = TagPlanDev{plan->next_idx,    plan->next_dev,     plan->next_host, plan->cur_dev,
+                    plan->cur_claim,   plan->avg_cell,     plan->block_stamps, plan->block_bounds,
+                    plan->num_blocks,  plan->block_id,     plan->k};
   }
   size_t nvec = n / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
@@ -822,6 +803,20 @@ extern "C" int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_
   if (k > (1u << 20)) return set_err(LPP_E_VALUE, "classify: k too large");
   k_classify<<<1, 32, 0, (cudaStream_t)stream>>>(tags, (int)k, claim_cell, out);
   LAUNCH_CHECK("classify");
+  return LPP_OK;
+}
+
+// K5 block stamp of an update, raised after its apply kernel (same stream:
+// every element reduction of that launch is performed before this runs)
+__global__ void k_publish_stamp(int* stamps, int bid, int stamp) {
+  fence_ar_gpu();
+  atomicMax(stamps + bid, stamp);
+}
+
+extern "C" int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream) {
+  if (!stamps || block_id < 0) return set_err(LPP_E_VALUE, "publish_stamp: bad stamps / block");
+  k_publish_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(stamps, block_id, stamp);
+  LAUNCH_CHECK("publish_stamp");
   return LPP_OK;
 }
 

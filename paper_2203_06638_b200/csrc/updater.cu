@@ -237,7 +237,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   const bool tagged = c->tags != nullptr;
   const int K = tagged ? c->tag_pick : 0;
   if (K > 0 && (!c->tag_idx_pinned || !c->tag_idx_dev || !c->rec_dev || !c->rec_pinned ||
-                c->rec_cols < 2 + (K + 1) / 2 || !c->avg_cell_dev || !c->done_ctr || !c->classified || !c->clean ||
+                c->rec_cols < 2 + (K + 1) / 2 || !c->avg_cell_dev || !c->classified || !c->clean ||
                 (c->fused && (!c->block_stamps || !c->block_bounds_dev))))
     return set_err(LPP_E_VALUE, "updater_run: tag sampling buffers missing");
   const int F = c->in_flight < 1 ? 1 : c->in_flight;
@@ -469,9 +469,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if (c->fused && K > 0) {
       // K1+K3 + K5: classify this step, stamp, gather the next step's tags
       const size_t on = (size_t)next_slot * K;
-      lpp_tag_plan plan{c->tag_idx_dev + on, rec_tags(next_slot), nullptr, rec_tags(slot),
-                        rec_claim(slot), c->avg_cell_dev, c->done_ctr, c->block_stamps,
-                        c->block_bounds_dev, c->num_blocks, b, K};
+      lpp_tag_plan plan{c->tag_idx_dev + on, rec_tags(next_slot), nullptr,     rec_tags(slot),
+                        rec_claim(slot),       c->avg_cell_dev,      c->block_stamps,
+                        c->block_bounds_dev,   c->num_blocks,        b,           K};
       rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, nullptr, c->n, (size_t)lo,
                                    (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u, &plan,
                                    astream);
@@ -499,6 +499,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (rc != LPP_OK) return rc;
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t1.ev[k], astream));
+    if (c->fused && K > 0 &&
+        (rc = lpp_publish_stamp(c->block_stamps, b, (int32_t)u, astream)) != LPP_OK)
+      return rc;
     if (K > 0 && (rc = copy_rec(slot, astream)) != LPP_OK) return rc;
     if (side) {
       CUDA_TRY(cudaEventRecord(order.ev[1], astream));

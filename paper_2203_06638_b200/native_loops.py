@@ -117,7 +117,6 @@ class NativeLoops:
             c.rec_pinned = w.rec_pinned[r].data_ptr()
             c.rec_cols = w.rec_cols
             c.avg_cell_dev = w.avg_dev
-            c.done_ctr = w.done_ctr[r].data_ptr()
             c.block_stamps = w.block_stamps.data_ptr()
             c.block_bounds_dev = w.block_bounds.data_ptr()
         c.classified = self.classified_count._a

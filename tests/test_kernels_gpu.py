@@ -511,10 +511,9 @@ def _plan_bufs(N, k, nb, depth=3):
     dev = {"tag_host": hb.dev, "claim": hb.dev + 4 * depth * k}
     tag_dev = torch.zeros((depth, k), dtype=torch.int32, device="cuda")
     idx = torch.zeros((depth, k), dtype=torch.long, device="cuda")
-    done = torch.zeros(1, dtype=torch.int32, device="cuda")
     cell = torch.zeros(1, dtype=torch.long, device="cuda")
     stamps = torch.zeros(nb + 1, dtype=torch.int32, device="cuda")
-    return hb, tag_host, claim, dev, tag_dev, idx, done, cell, stamps
+    return hb, tag_host, claim, dev, tag_dev, idx, cell, stamps
 
 
 @pytest.mark.parametrize("n,bounds,bid", [(4099, (0, 1000, 4099), 2), (100_003, (0, 1001, 77_777, 100_003), 2),
@@ -522,7 +521,7 @@ def _plan_bufs(N, k, nb, depth=3):
                                           (1_000_001, (0, 3, 999_998, 1_000_001), 1)])
 def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, n, bounds, bid):
     """The plan variant updates values exactly like the fused kernel, leaves
-    per-element tags alone, raises its block's stamp once done, classifies
+    per-element tags alone (lpp_publish_stamp then raises its block's stamp), classifies
     this step against the round-stamp cell read in the kernel, and reads the
     next step's sampled tags as max(floor, stamp[0], stamp[b(e)], own stamp
     inside its block) — the own stamp even though it is published last."""
@@ -530,7 +529,7 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
 
     k, nb = 16, len(bounds) - 1
     lo, hi = (0, n) if bid == 0 else (bounds[bid - 1], bounds[bid])
-    hb, tag_host, claim, dev, tag_dev, idx, done, cell, stamps = _plan_bufs(N, k, nb)
+    hb, tag_host, claim, dev, tag_dev, idx, cell, stamps = _plan_bufs(N, k, nb)
     bnd = torch.tensor(bounds, dtype=torch.long, device="cuda")
     gen = np.random.default_rng(n + bid)
     x = gen.normal(size=n).astype(np.float32)
@@ -546,11 +545,14 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     nxt[0], nxt[-1] = 0, n - 1                     # first and last (tail) elements included
     idx[1] = torch.tensor(nxt)
     plan = N.TagPlan(idx[1].data_ptr(), tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
-                     tag_dev[0].data_ptr(), dev["claim"], cell.data_ptr(), done.data_ptr(),
+                     tag_dev[0].data_ptr(), dev["claim"], cell.data_ptr(),
                      stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
     stamp = 40
     N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.05, None, 0.9, 5e-4,
                           stamp, plan, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(stamps.cpu().numpy(), old)      # the kernel itself publishes nothing
+    N.publish_stamp(stamps.data_ptr(), bid, stamp, 0)
     torch.cuda.synchronize()
     xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
     orc.apply_sgd(xv, g[lo:hi].copy(), mv, 0.05, 0.9, 5e-4)
@@ -568,13 +570,13 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     want_next = np.where((nxt >= lo) & (nxt < hi), np.maximum(want_next, stamp), want_next)
     assert np.array_equal(tag_host[1], want_next)
     assert np.array_equal(tag_dev[1].cpu().numpy(), want_next)
-    assert int(done.item()) == 0                  # counter reset for the next launch
     # second launch: clean (k_claim = 10 <= every tag)
     cell.fill_(10)
     plan2 = N.TagPlan(None, None, None, tag_dev[0].data_ptr(), dev["claim"] + 16, cell.data_ptr(),
-                      done.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
+                      stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
     N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.0, None, 0.0,
                           0.0, stamp - 5, plan2, 0)
+    N.publish_stamp(stamps.data_ptr(), bid, stamp - 5, 0)
     torch.cuda.synchronize()
     assert list(claim[1]) == [10, 1]
     assert int(stamps[bid].item()) == max(old[bid], stamp)   # max: an older stamp never lowers it
@@ -605,7 +607,6 @@ def test_apply_snapshot_plan_concurrent_streams(N):
     bnd = torch.tensor(bounds, device="cuda")
     stamps = torch.zeros(K + 1, dtype=torch.int32, device="cuda")
     cell = torch.zeros(1, dtype=torch.long, device="cuda")
-    done = torch.zeros(K, dtype=torch.int32, device="cuda")
     tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
     gen = np.random.default_rng(5)
     idx = torch.tensor(np.stack([[np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k,
@@ -615,11 +616,11 @@ def test_apply_snapshot_plan_concurrent_streams(N):
     for t in range(steps):
         for s, st in enumerate(streams):
             plan = N.TagPlan(idx[s, t].data_ptr(), tag_dev[s, t].data_ptr(), None, None, None,
-                             cell.data_ptr(), done[s].data_ptr(), stamps.data_ptr(), bnd.data_ptr(), K,
-                             s + 1, k)
+                             cell.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), K, s + 1, k)
             N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, None, n, int(bounds[s]),
                                   int(bounds[s + 1]), 1.0, None, 0.0, 0.0, 1000 * (s + 1) + t, plan,
                                   st.cuda_stream)
+            N.publish_stamp(stamps.data_ptr(), s + 1, 1000 * (s + 1) + t, st.cuda_stream)
     torch.cuda.synchronize()
     assert bool((x.tensor == float(steps)).all())
     td = tag_dev.cpu().numpy()

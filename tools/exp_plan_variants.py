@@ -27,7 +27,7 @@ for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000
     def plan(next_idx=True, next_host=False, claim=None):
         return N.TagPlan(idx.data_ptr() if next_idx else None, tags_dev[16:32].data_ptr(),
                          hb.dev + 512 if next_host else None, tags_dev[:16].data_ptr(), claim,
-                         cell.data_ptr(), done.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), 3, 2, 16)
+                         cell.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), 3, 2, 16)
 
     variants = {
         "no plan": None,
