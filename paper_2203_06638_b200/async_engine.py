@@ -536,7 +536,8 @@ class _Engine(NativeLoops):
                 if tracks:
                     self.gather_tags(w, r, slot, tag_idx)
                 N.snapshot(w.store.arena.ptr, w.replicas[r].ptr, self.dim, sp)          # K3
-            next_idx_dev = w.stage_idx(r, next_slot, next_tag_idx, sp) if tracks else None
+            if tracks:   # the next step's indices: host ring, passed to the apply by value
+                w.tag_idx_np[r, next_slot, :w.tag_pick] = next_tag_idx
             prog.run(block_id, buf)                                                      # fwd+bwd
             if self.host_batches:
                 w.buf_free[r][buf].record(stream)
@@ -546,7 +547,8 @@ class _Engine(NativeLoops):
                 # its gradient), stamp, and gather the next step's tags after
                 # this apply landed (engine.py:343-362 order)
                 k = w.tag_pick
-                plan = N.TagPlan(next_idx_dev, w.rec_tags(r, next_slot), None, w.rec_tags(r, slot),
+                plan = N.TagPlan(w.tag_idx_pinned[r, next_slot].data_ptr(), w.rec_tags(r, next_slot),
+                                 None, w.rec_tags(r, slot),
                                  w.rec_claim(r, slot), w.avg_dev, w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
                                  cfg.partition.num_blocks, block_id, k)
             mom = w.moms[r]

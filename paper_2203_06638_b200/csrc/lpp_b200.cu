@@ -477,7 +477,8 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 //     stamp every element, engine.py:421 add_assign(..., stamp=u_avg)).
 
 struct TagPlanDev {
-  const int64_t* next_idx;  // k sampled indices of the next step (device)
+  int64_t idx[32];          // the next step's k sampled indices, by value (constant bank)
+  int has_next;
   int* next_dev;            // -> the next step's effective tags (device ring slot)
   int* next_host;           // -> and a host-mapped copy for the records (may be null)
   const int* cur_dev;       // this step's effective tags (read at its snapshot)
@@ -552,12 +553,15 @@ __global__ void __launch_bounds__(kThreads)
   // which of the next step's sampled elements this thread refreshes: the
   // plan launch uses a power-of-two grid, so vector v belongs to thread
   // v & (stride - 1); a tail element e >= 4 nvec to block 0, thread
-  // (e - 4 nvec) mod blockDim (the index loads are warp-uniform L1 hits)
+  // (e - 4 nvec) mod blockDim.  The indices are launch parameters (constant
+  // bank): a load from memory here, once per CTA, doubled the in-situ
+  // latency of the launch, whose CTAs run in many small waves among the
+  // convolutions' CTAs
   unsigned own = 0;
-  if (PLAN && plan.next_idx) {
+  if (PLAN && plan.has_next) {
     const size_t mask = stride - 1;
     for (int j = 0; j < plan.k; ++j) {
-      const size_t e = (size_t)__ldg(plan.next_idx + j), v = e >> 2;
+      const size_t e = (size_t)plan.idx[j], v = e >> 2;
       const bool mine = v < nvec ? ((v & mask) == tid)
                                  : (blockIdx.x == 0 && ((e - 4 * nvec) & (kThreads - 1)) == threadIdx.x);
       if (mine) own |= 1u << j;
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(kThreads)
     if (PLAN && own) {  // sampled elements of this vector: tags before values
       for (unsigned bits = own; bits; bits &= bits - 1) {
         const int j = __ffs(bits) - 1;
-        const int64_t e = __ldg(plan.next_idx + j);
+        const int64_t e = plan.idx[j];
         if ((size_t)e / 4 == i) {
           const int t = plan_tag_of(plan, e, lo, hi, stamp);
           plan.next_dev[j] = t;
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kThreads)
       if (PLAN && own)
         for (unsigned bits = own; bits; bits &= bits - 1) {
           const int j = __ffs(bits) - 1;
-          if ((size_t)__ldg(plan.next_idx + j) == e) {
+          if ((size_t)plan.idx[j] == e) {
             const int t = plan_tag_of(plan, (int64_t)e, lo, hi, stamp);
             plan.next_dev[j] = t;
             if (plan.next_host) plan.next_host[j] = t;
@@ -665,9 +669,23 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
       return set_err(LPP_E_VALUE, "apply_snapshot: next-step tags need an output");
     if (plan->cur_claim && plan->k > 0 && !plan->cur_dev)
       return set_err(LPP_E_VALUE, "apply_snapshot: classification needs this step's tags");
-    pd = TagPlanDev{plan->next_idx,    plan->next_dev,     plan->next_host, plan->cur_dev,
-                    plan->cur_claim,   plan->avg_cell,     plan->block_stamps, plan->block_bounds,
-                    plan->num_blocks,  plan->block_id,     plan->k};
+    pd.has_next = plan->next_idx != nullptr && plan->k > 0;
+    for (int j = 0; pd.has_next && j < plan->k; ++j) {  // host memory, copied into the launch
+      if (plan->next_idx[j] < 0 || (size_t)plan->next_idx[j] >= n)
+        return set_err(LPP_E_INDEX, "apply_snapshot: sampled index %lld outside [0, %zu)",
+                       (long long)plan->next_idx[j], n);
+      pd.idx[j] = plan->next_idx[j];
+    }
+    pd.next_dev = plan->next_dev;
+    pd.next_host = plan->next_host;
+    pd.cur_dev = plan->cur_dev;
+    pd.cur_claim = plan->cur_claim;
+    pd.avg_cell = plan->avg_cell;
+    pd.block_stamps = plan->block_stamps;
+    pd.bounds = plan->block_bounds;
+    pd.nb = plan->num_blocks;
+    pd.bid = plan->block_id;
+    pd.k = plan->k;
   }
   size_t nvec = n / 4;
   unsigned grid = grid_for(nvec ? nvec : 1, current_sms());

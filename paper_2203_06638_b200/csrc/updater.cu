@@ -454,8 +454,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       }
       if ((rc = lpp_snapshot(c->x, c->replica, c->n, stream)) != LPP_OK) return rc;   // K3
     }
-    // the next step's tag indices, for this step's apply kernel to gather
-    if (c->fused && K > 0 && (rc = draw_idx(next_slot)) != LPP_OK) return rc;
+    // the next step's tag indices (host ring; the apply launch takes them by value)
+    if (c->fused && K > 0 && !c->host_rng)
+      draw_tags(&tag_state, (int64_t)c->n, K, c->tag_idx_pinned + (size_t)next_slot * K);
     if ((rc = lpp_graph_launch(c->graph_exec[2 * b + buf], stream)) != LPP_OK) return rc;  // fwd+bwd
     if (host) CUDA_TRY(cudaEventRecord(buf_free.ev[buf], stream));
     if (c->read_loss)
@@ -469,7 +470,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     if (c->fused && K > 0) {
       // K1+K3 + K5: classify this step, stamp, gather the next step's tags
       const size_t on = (size_t)next_slot * K;
-      lpp_tag_plan plan{c->tag_idx_dev + on, rec_tags(next_slot), nullptr,     rec_tags(slot),
+      lpp_tag_plan plan{c->tag_idx_pinned + on, rec_tags(next_slot), nullptr, rec_tags(slot),
                         rec_claim(slot),       c->avg_cell_dev,      c->block_stamps,
                         c->block_bounds_dev,   c->num_blocks,        b,           K};
       rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, nullptr, c->n, (size_t)lo,

@@ -544,7 +544,8 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     nxt = np.sort(gen.choice(n, size=k, replace=False))
     nxt[0], nxt[-1] = 0, n - 1                     # first and last (tail) elements included
     idx[1] = torch.tensor(nxt)
-    plan = N.TagPlan(idx[1].data_ptr(), tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
+    nxt = np.ascontiguousarray(nxt, dtype=np.int64)   # the plan takes HOST indices by value
+    plan = N.TagPlan(nxt.ctypes.data, tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
                      tag_dev[0].data_ptr(), dev["claim"], cell.data_ptr(),
                      stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
     stamp = 40
@@ -591,6 +592,27 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     hb.close()
 
 
+def test_apply_snapshot_plan_rejects_out_of_range_indices(N):
+    from paper_2203_06638_b200.arena import Arena
+
+    n = 1000
+    x, g, r = Arena(n, 0), Arena(n, 0), Arena(n, 0)
+    stamps = torch.zeros(2, dtype=torch.int32, device="cuda")
+    bnd = torch.tensor([0, n], dtype=torch.long, device="cuda")
+    cell = torch.zeros(1, dtype=torch.long, device="cuda")
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    bad = np.array([0, 5, n, 7], dtype=np.int64)
+    plan = N.TagPlan(bad.ctypes.data, out.data_ptr(), None, None, None, cell.data_ptr(),
+                     stamps.data_ptr(), bnd.data_ptr(), 1, 1, 4)
+    with pytest.raises(IndexError):
+        N.apply_snapshot_plan(x.ptr, g.ptr, None, r.ptr, None, n, 0, n, 0.1, None, 0.0, 0.0, 1, plan, 0)
+    plan.k = 33
+    with pytest.raises(ValueError):
+        N.apply_snapshot_plan(x.ptr, g.ptr, None, r.ptr, None, n, 0, n, 0.1, None, 0.0, 0.0, 1, plan, 0)
+    for a in (x, g, r):
+        a.close()
+
+
 def test_apply_snapshot_plan_concurrent_streams(N):
     """4 streams x 30 fused steps on disjoint blocks with momentum-free -1
     gradients: every reduction lands; each step's next-step tags at elements
@@ -609,13 +631,13 @@ def test_apply_snapshot_plan_concurrent_streams(N):
     cell = torch.zeros(1, dtype=torch.long, device="cuda")
     tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
     gen = np.random.default_rng(5)
-    idx = torch.tensor(np.stack([[np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k,
-                                                     replace=False)) for _ in range(steps)]
-                                 for s in range(K)]), device="cuda")
+    idx = np.ascontiguousarray(np.stack([[np.sort(gen.choice(np.arange(bounds[s], bounds[s + 1]), size=k,
+                                                            replace=False)) for _ in range(steps)]
+                                        for s in range(K)]), dtype=np.int64)
     torch.cuda.synchronize()
     for t in range(steps):
         for s, st in enumerate(streams):
-            plan = N.TagPlan(idx[s, t].data_ptr(), tag_dev[s, t].data_ptr(), None, None, None,
+            plan = N.TagPlan(idx[s, t].ctypes.data, tag_dev[s, t].data_ptr(), None, None, None,
                              cell.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), K, s + 1, k)
             N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, None, n, int(bounds[s]),
                                   int(bounds[s + 1]), 1.0, None, 0.0, 0.0, 1000 * (s + 1) + t, plan,

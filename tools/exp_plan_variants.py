@@ -13,7 +13,7 @@ from paper_2203_06638_b200.arena import Arena  # noqa: E402
 
 st = torch.cuda.current_stream().cuda_stream
 hb = N.HostBuffer(4096)
-idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long, device="cuda")
+idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long)   # host: the plan takes indices by value
 cell = torch.zeros(1, dtype=torch.long, device="cuda")
 tags_dev = torch.zeros(64, dtype=torch.int32, device="cuda")
 claim_dev = torch.zeros(4, dtype=torch.long, device="cuda")

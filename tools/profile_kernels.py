@@ -40,7 +40,7 @@ for d in (11_220_132, 25_557_032):
 # CTA) — and without K5 for comparison; laid out as the engine does it:
 # indices, stamps, the round-stamp cell and the step records on the device
 claim = torch.zeros(2, dtype=torch.long, device="cuda")
-idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long, device="cuda")
+idx = torch.arange(0, 16 * 1000, 1000, dtype=torch.long)   # host: the plan takes indices by value
 cell = torch.zeros(1, dtype=torch.long, device="cuda")
 dev_tags = torch.zeros(32, dtype=torch.int32, device="cuda")
 done = torch.zeros(1, dtype=torch.int32, device="cuda")
