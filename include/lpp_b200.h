@@ -488,6 +488,9 @@ typedef struct {
    * block boundaries [num_blocks + 1] on the device (lpp_tag_plan) */
   int32_t* block_stamps;
   const int64_t* block_bounds_dev;
+  /* time_apply: each timed apply's CUDA-event ms, in step order (NULL: sum only) */
+  float* apply_ms_log;
+  int64_t apply_ms_cap;
 } lpp_updater_cfg;
 
 typedef struct {

@@ -77,7 +77,8 @@ class UpdaterCfg(ctypes.Structure):
         ("host_rng", _c.c_int32), ("n_entropy", _c.c_int32), ("rng_entropy", _c.c_uint64 * 4),
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
         ("rec_dev", _vp), ("rec_pinned", _vp), ("rec_cols", _c.c_int32), ("avg_cell_dev", _vp),
-        ("block_stamps", _vp), ("block_bounds_dev", _vp),
+        ("block_stamps", _vp), ("block_bounds_dev", _vp), ("apply_ms_log", _vp),
+        ("apply_ms_cap", _c.c_int64),
     ]
 
 

@@ -329,6 +329,8 @@ class _Engine(NativeLoops):
         self.err_lock = threading.Lock()
         self.apply_events: list = []
         self.native_apply = [0, 0.0, 0.0]   # launches, ms, bytes (native loop, time_apply)
+        self.apply_ms_samples: list = []    # per-launch ms (native loop, time_apply)
+        self._apply_logs: dict = {}
         self._records: dict = {}             # native loop record buffers per (worker, updater)
         self.side_apply = False             # applies on the high-priority stream (set per run)
         self.k4_timing = [0, 0.0]           # in-situ K4 rounds, summed ms (native averager, time_apply)
@@ -377,6 +379,7 @@ class _Engine(NativeLoops):
         self.errors = []
         self.apply_events = []
         self.native_apply = [0, 0.0, 0.0]
+        self.apply_ms_samples = []
         self.k4_timing = [0, 0.0]
         self.loss_log = []
         self.eval_points = []

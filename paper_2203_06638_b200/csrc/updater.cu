@@ -374,6 +374,8 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, t0.ev[k], t1.ev[k]));
       st->apply_ms += ms;
+      if (c->apply_ms_log && st->apply_launches < c->apply_ms_cap)
+        c->apply_ms_log[st->apply_launches] = ms;
       st->apply_bytes += bytes_of[k];
       st->apply_launches += 1;
     }

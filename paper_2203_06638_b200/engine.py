@@ -134,6 +134,7 @@ class Trainer:
         res.round_trace = getattr(eng, "round_trace", None)
         res.losses = list(eng.loss_log)
         res.k4_timing = tuple(getattr(eng, "k4_timing", (0, 0.0)))   # (rounds, summed ms), in situ
+        res.apply_ms_samples = list(getattr(eng, "apply_ms_samples", []))
         return res
 
     def close(self) -> None:

@@ -122,6 +122,11 @@ class NativeLoops:
         c.classified = self.classified_count._a
         c.clean = self.clean_count._a
         c.apply_bytes_per_elem = float(self.apply_bytes_per_elem)
+        if self.time_apply:
+            # per-launch apply times (distribution beside the bench's average)
+            alog = np.zeros(self.budget + 2, dtype=np.float32)
+            c.apply_ms_log, c.apply_ms_cap = alog.ctypes.data, len(alog)
+            self._apply_logs[(w.q, r)] = alog
         c.stream = w.streams[r].cuda_stream
         c.apply_stream = w.apply_streams[r].cuda_stream if self.side_apply else None
         keep = [lo, hi, execs, flops, ms]
@@ -201,7 +206,10 @@ class NativeLoops:
             del keep
             self.flops.add(int(st.flops))
             if self.time_apply:
+                alog = self._apply_logs.pop((q, r), None)
                 with self.native_lock:
+                    if alog is not None:
+                        self.apply_ms_samples.extend(alog[:int(st.apply_launches)].tolist())
                     self.native_apply[0] += int(st.apply_launches)
                     self.native_apply[1] += float(st.apply_ms)
                     self.native_apply[2] += float(st.apply_bytes)

@@ -9,6 +9,7 @@ import os
 import sys
 from pathlib import Path
 
+import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -32,11 +33,13 @@ for name, cfg in variants.items():
         continue
     tr = Trainer(cfg, time_apply=True)
     tr.run(5 * 4, evaluate=False)
-    for rep in range(2):
+    for rep in range(3):
         res = tr.run(60 * 4, evaluate=False)
         n_, ms, by = res.apply_timing
+        q = np.percentile(np.array(res.apply_ms_samples) * 1e3, [10, 50, 90, 99]) if res.apply_ms_samples else []
         print(json.dumps({"variant": name, "ctas_cap": os.environ.get("LPP_FUSED_CTAS", ""), "rep": rep,
                           "img_per_s": round(sum(res.counter_finals) * 128 / (res.device_ms / 1e3)),
                           "apply_avg_us": round(1e3 * ms / n_, 2),
+                          "p10_50_90_99_us": [round(float(v), 1) for v in q],
                           "frac": round(by / (ms / 1e3) / 1e9 / 6560.6, 4)}), flush=True)
     tr.close()
