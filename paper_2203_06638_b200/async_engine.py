@@ -13,6 +13,7 @@ deterministic interleaving used as the parity mode.
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 
@@ -131,9 +132,23 @@ class _Worker:
         # round applied to this arena, written by the averager (lpp_set_i64)
         # before the host cell last_avg_stamp moves; the apply kernels read it
         # as k_claim and as the tag floor
-        self.last_avg_stamp = AtomicCounter(0)
-        self.round_cell = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self.avg_dev = self.round_cell.data_ptr()
+        # Where the kernels read it: "host" (default) — the host cell itself,
+        # in mapped pinned memory: k_claim is exactly last_avg_stamp when the
+        # apply starts and a round costs no device work; "device" — a device
+        # mirror the averager sets with a one-thread launch per round (a
+        # launch on the averager's stream, which with 2U + 1 streams shares
+        # a hardware queue with a compute stream: in-situ apply p99 of ms)
+        self.round_cell_mode = os.environ.get("LPP_ROUND_CELL", "host")
+        if self.round_cell_mode == "host":
+            self.round_mem = N.HostBuffer(64)
+            self.last_avg_stamp = AtomicCounter(0, cell=self.round_mem.view(np.int64, (1,)), index=0)
+            self.round_cell = None
+            self.avg_dev = self.round_mem.dev
+        else:
+            self.round_mem = None
+            self.last_avg_stamp = AtomicCounter(0)
+            self.round_cell = torch.zeros(1, dtype=torch.int64, device=self.dev)
+            self.avg_dev = self.round_cell.data_ptr()
         # K5 step records, per updater and in-flight slot: {k_claim, clean,
         # tags[k] (int32)} — written on the device by the kernels (the tags at
         # the step's snapshot, (k_claim, clean) by its apply), copied to the
@@ -189,10 +204,11 @@ class _Worker:
                      8 * self.rec_cols, stream_ptr)
 
     def publish_round(self, u: int, stream: torch.cuda.Stream) -> None:
-        """The round with stamp u is applied to this arena: device cell first
-        (the apply kernels' k_claim / tag floor), then the host cell."""
-        N.set_i64(self.avg_dev, u, stream.cuda_stream)
-        stream.synchronize()
+        """The round with stamp u is applied to this arena: (device mirror
+        first,) then the host cell the kernels read as k_claim / tag floor."""
+        if self.round_cell is not None:
+            N.set_i64(self.avg_dev, u, stream.cuda_stream)
+            stream.synchronize()
         self.last_avg_stamp.store(u)
 
     def build_programs(self, engine: "_Engine", block_ids_per_rank: list[list[int]]) -> None:
@@ -263,6 +279,8 @@ class _Worker:
         if self.store.tag_arena is not None:
             self.store.tag_arena.close()
         self.tags = None
+        if self.round_mem is not None:
+            self.round_mem.close()
 
 
 class _Engine(NativeLoops):
@@ -369,7 +387,8 @@ class _Engine(NativeLoops):
         self.clean_count.store(0)
         self.classified_count.store(0)
         for w in self.workers.values():
-            w.round_cell.zero_()
+            if w.round_cell is not None:
+                w.round_cell.zero_()
             if w.tags is not None:
                 w.tags.zero_()
                 w.block_stamps.zero_()

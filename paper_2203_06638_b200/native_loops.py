@@ -254,7 +254,7 @@ class NativeLoops:
             c.workers, c.q, c.updaters = Q, q, cfg.updaters
             c.tagged = int(self.tag_ptrs is not None)
             c.stamp_floor = int(cfg.tracks)
-            c.round_cell = w.avg_dev
+            c.round_cell = w.avg_dev if w.round_cell is not None else None
             c.sample_counter = w.store.sample_counter._a
             c.update_order = w.store.update_order_counter._a
             c.exited = w.exited._a

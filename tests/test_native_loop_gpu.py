@@ -191,7 +191,9 @@ def test_native_averager_round_protocol(tags, workers):
             for q in range(workers):
                 w = tr.eng.workers[q]
                 last_u = max(st.u for st in res.stamps if st.worker == q)
-                assert int(w.round_cell.item()) == last_u == w.last_avg_stamp.read()
+                assert w.last_avg_stamp.read() == last_u
+                if w.round_cell is not None:
+                    assert int(w.round_cell.item()) == last_u
                 assert (w.block_stamps.cpu().numpy() > 0).all()
     finally:
         tr.close()
