@@ -52,6 +52,10 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# 4 updater + 4 apply + 1 averager (+ 4 copy, end to end) streams per GPU:
+# more than the default 8 hardware work queues, which would make unrelated
+# streams share a queue (in-situ apply p99 of ms, tools/exp_insitu_variants.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "16")
 
 B = 128
 U = 4

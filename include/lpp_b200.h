@@ -149,10 +149,10 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
  *       [lo, hi)); *avg_cell (the worker's last completed round stamp, a
  *       device cell) is the floor a round writes into every element
  *       (engine.py:421)                              (next_idx may be NULL)
- * next_idx is a HOST pointer: the k indices are copied into the launch
- * parameters; block_bounds: num_blocks + 1 boundaries (0 ... n) on the
- * device; k <= 32; next_host and cur_claim may point into lpp_host_alloc
- * memory. */
+ * next_idx and block_bounds (num_blocks + 1 boundaries, 0 ... n) are HOST
+ * pointers: the k indices and their partial blocks are computed into the
+ * launch parameters; k <= 32, num_blocks <= 127; next_host and cur_claim
+ * may point into lpp_host_alloc memory. */
 typedef struct lpp_tag_plan {
   const int64_t* next_idx;
   int32_t* next_dev;

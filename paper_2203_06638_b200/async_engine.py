@@ -132,13 +132,15 @@ class _Worker:
         # round applied to this arena, written by the averager (lpp_set_i64)
         # before the host cell last_avg_stamp moves; the apply kernels read it
         # as k_claim and as the tag floor
-        # Where the kernels read it: "host" (default) — the host cell itself,
-        # in mapped pinned memory: k_claim is exactly last_avg_stamp when the
-        # apply starts and a round costs no device work; "device" — a device
-        # mirror the averager sets with a one-thread launch per round (a
-        # launch on the averager's stream, which with 2U + 1 streams shares
-        # a hardware queue with a compute stream: in-situ apply p99 of ms)
-        self.round_cell_mode = os.environ.get("LPP_ROUND_CELL", "host")
+        # Where the kernels read it: "device" (default) — a device mirror the
+        # averager sets with a one-thread launch per round before the host
+        # cell moves; "host" — the host cell itself in mapped pinned memory
+        # (no device work per round, but every read is a PCIe round trip:
+        # in-situ apply median 33 vs 20 us on ResNet-20, tools/exp_insitu_variants.py).
+        # With more than 8 streams per device set CUDA_DEVICE_MAX_CONNECTIONS
+        # >= 16 (bench.py does): at 8 hardware queues the averager's stream
+        # shares one with a compute stream and the apply's p99 reaches ms
+        self.round_cell_mode = os.environ.get("LPP_ROUND_CELL", "device")
         if self.round_cell_mode == "host":
             self.round_mem = N.HostBuffer(64)
             self.last_avg_stamp = AtomicCounter(0, cell=self.round_mem.view(np.int64, (1,)), index=0)
@@ -170,6 +172,7 @@ class _Worker:
             self.block_stamps = torch.zeros(nb + 1, dtype=torch.int32, device=self.dev)
             self.block_bounds = torch.tensor(cfg.partition.boundaries, dtype=torch.long,
                                              device=self.dev)
+            self.block_bounds_host = np.ascontiguousarray(cfg.partition.boundaries, dtype=np.int64)
             self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
             self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
         # full record mode keeps every update's whole tag snapshot (reference
@@ -571,7 +574,8 @@ class _Engine(NativeLoops):
                 k = w.tag_pick
                 plan = N.TagPlan(w.tag_idx_pinned[r, next_slot].data_ptr(), w.rec_tags(r, next_slot),
                                  None, w.rec_tags(r, slot),
-                                 w.rec_claim(r, slot), w.avg_dev, w.block_stamps.data_ptr(), w.block_bounds.data_ptr(),
+                                 w.rec_claim(r, slot), w.avg_dev, w.block_stamps.data_ptr(),
+                                 w.block_bounds_host.ctypes.data,
                                  cfg.partition.num_blocks, block_id, k)
             mom = w.moms[r]
             astream = stream

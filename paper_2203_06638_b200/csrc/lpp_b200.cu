@@ -478,6 +478,7 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 
 struct TagPlanDev {
   int64_t idx[32];          // the next step's k sampled indices, by value (constant bank)
+  int8_t blk[32];           // ... and the partial block b(e) holding each (from host bounds)
   int has_next;
   int* next_dev;            // -> the next step's effective tags (device ring slot)
   int* next_host;           // -> and a host-mapped copy for the records (may be null)
@@ -485,7 +486,6 @@ struct TagPlanDev {
   int64_t* cur_claim;       // -> this step's (k_claim, clean) (host-mapped; may be null)
   const int64_t* avg_cell;  // the worker's last completed round stamp (device cell)
   int* block_stamps;        // [nb + 1] newest stamp per block (device)
-  const int64_t* bounds;    // [nb + 1] block boundaries (bounds[0] = 0, bounds[nb] = n)
   int nb;
   int bid;                  // this update's block id
   int k;                    // <= 32
@@ -502,15 +502,14 @@ __device__ __forceinline__ int ld_acq_i32(const int* p) {
   return r;
 }
 
-// effective tag of sampled element e, read before its value (see above)
-__device__ __forceinline__ int plan_tag_of(const TagPlanDev& plan, int64_t e, size_t lo, size_t hi,
-                                           int stamp) {
-  int b = 1;
-  while (b < plan.nb && e >= plan.bounds[b]) ++b;
+// effective tag of sampled element j (element e), read before its value:
+// three independent loads (one round trip), b(e) precomputed at launch
+__device__ __forceinline__ int plan_tag_of(const TagPlanDev& plan, int j, int64_t e, size_t lo,
+                                           size_t hi, int stamp) {
   int t = ld_acq_i32(plan.block_stamps);
-  int tb = ld_acq_i32(plan.block_stamps + b);
-  t = t > tb ? t : tb;
+  int tb = ld_acq_i32(plan.block_stamps + plan.blk[j]);
   const int fl = (int)ld_sys_i64(plan.avg_cell);
+  t = t > tb ? t : tb;
   t = t > fl ? t : fl;
   if ((size_t)e >= lo && (size_t)e < hi && stamp > t) t = stamp;
   return t;
@@ -576,7 +575,7 @@ __global__ void __launch_bounds__(kThreads)
         const int j = __ffs(bits) - 1;
         const int64_t e = plan.idx[j];
         if ((size_t)e / 4 == i) {
-          const int t = plan_tag_of(plan, e, lo, hi, stamp);
+          const int t = plan_tag_of(plan, j, e, lo, hi, stamp);
           plan.next_dev[j] = t;
           if (plan.next_host) plan.next_host[j] = t;
         }
@@ -611,7 +610,7 @@ __global__ void __launch_bounds__(kThreads)
         for (unsigned bits = own; bits; bits &= bits - 1) {
           const int j = __ffs(bits) - 1;
           if ((size_t)plan.idx[j] == e) {
-            const int t = plan_tag_of(plan, (int64_t)e, lo, hi, stamp);
+            const int t = plan_tag_of(plan, j, (int64_t)e, lo, hi, stamp);
             plan.next_dev[j] = t;
             if (plan.next_host) plan.next_host[j] = t;
           }
@@ -662,6 +661,8 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
       return set_err(LPP_E_VALUE, "apply_snapshot: tag count %d outside [0, 32]", plan->k);
     if (!plan->block_stamps || !plan->block_bounds || !plan->avg_cell)
       return set_err(LPP_E_VALUE, "apply_snapshot: a tag plan needs stamps, bounds, round cell");
+    if (plan->num_blocks > 127)
+      return set_err(LPP_E_VALUE, "apply_snapshot: at most 127 blocks with a tag plan");
     if (plan->num_blocks < 1 || plan->block_id < 0 || plan->block_id > plan->num_blocks)
       return set_err(LPP_E_VALUE, "apply_snapshot: block %d outside [0, %d]", plan->block_id,
                      plan->num_blocks);
@@ -675,6 +676,9 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
         return set_err(LPP_E_INDEX, "apply_snapshot: sampled index %lld outside [0, %zu)",
                        (long long)plan->next_idx[j], n);
       pd.idx[j] = plan->next_idx[j];
+      int b = 1;  // the partial block holding the element (host bounds)
+      while (b < plan->num_blocks && plan->next_idx[j] >= plan->block_bounds[b]) ++b;
+      pd.blk[j] = (int8_t)b;
     }
     pd.next_dev = plan->next_dev;
     pd.next_host = plan->next_host;
@@ -682,7 +686,6 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     pd.cur_claim = plan->cur_claim;
     pd.avg_cell = plan->avg_cell;
     pd.block_stamps = plan->block_stamps;
-    pd.bounds = plan->block_bounds;
     pd.nb = plan->num_blocks;
     pd.bid = plan->block_id;
     pd.k = plan->k;

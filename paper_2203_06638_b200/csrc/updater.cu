@@ -470,11 +470,12 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t0.ev[k], astream));
     if (c->fused && K > 0) {
-      // K1+K3 + K5: classify this step, stamp, gather the next step's tags
+      // K1+K3 + K5: classify this step, read the next step's tags (block_hi
+      // serves as the boundaries: block_hi[b] = end of partial block b)
       const size_t on = (size_t)next_slot * K;
       lpp_tag_plan plan{c->tag_idx_pinned + on, rec_tags(next_slot), nullptr, rec_tags(slot),
                         rec_claim(slot),       c->avg_cell_dev,      c->block_stamps,
-                        c->block_bounds_dev,   c->num_blocks,        b,           K};
+                        c->block_hi,           c->num_blocks,        b,           K};
       rc = lpp_apply_snapshot_plan(c->x, c->g, c->m, c->replica, nullptr, c->n, (size_t)lo,
                                    (size_t)hi, lr32, nullptr, c->mu, c->wd, (int32_t)u, &plan,
                                    astream);

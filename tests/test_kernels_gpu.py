@@ -545,9 +545,10 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     nxt[0], nxt[-1] = 0, n - 1                     # first and last (tail) elements included
     idx[1] = torch.tensor(nxt)
     nxt = np.ascontiguousarray(nxt, dtype=np.int64)   # the plan takes HOST indices by value
+    bnd_h = np.ascontiguousarray(bounds, dtype=np.int64)   # host boundaries for the plan
     plan = N.TagPlan(nxt.ctypes.data, tag_dev[1].data_ptr(), dev["tag_host"] + 4 * k,
                      tag_dev[0].data_ptr(), dev["claim"], cell.data_ptr(),
-                     stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
+                     stamps.data_ptr(), bnd_h.ctypes.data, nb, bid, k)
     stamp = 40
     N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.05, None, 0.9, 5e-4,
                           stamp, plan, 0)
@@ -574,7 +575,7 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     # second launch: clean (k_claim = 10 <= every tag)
     cell.fill_(10)
     plan2 = N.TagPlan(None, None, None, tag_dev[0].data_ptr(), dev["claim"] + 16, cell.data_ptr(),
-                      stamps.data_ptr(), bnd.data_ptr(), nb, bid, k)
+                      stamps.data_ptr(), bnd_h.ctypes.data, nb, bid, k)
     N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, ar.ptr, None, n, lo, hi, 0.0, None, 0.0,
                           0.0, stamp - 5, plan2, 0)
     N.publish_stamp(stamps.data_ptr(), bid, stamp - 5, 0)
@@ -598,12 +599,12 @@ def test_apply_snapshot_plan_rejects_out_of_range_indices(N):
     n = 1000
     x, g, r = Arena(n, 0), Arena(n, 0), Arena(n, 0)
     stamps = torch.zeros(2, dtype=torch.int32, device="cuda")
-    bnd = torch.tensor([0, n], dtype=torch.long, device="cuda")
+    bnd = np.array([0, n], dtype=np.int64)
     cell = torch.zeros(1, dtype=torch.long, device="cuda")
     out = torch.zeros(4, dtype=torch.int32, device="cuda")
     bad = np.array([0, 5, n, 7], dtype=np.int64)
     plan = N.TagPlan(bad.ctypes.data, out.data_ptr(), None, None, None, cell.data_ptr(),
-                     stamps.data_ptr(), bnd.data_ptr(), 1, 1, 4)
+                     stamps.data_ptr(), bnd.ctypes.data, 1, 1, 4)
     with pytest.raises(IndexError):
         N.apply_snapshot_plan(x.ptr, g.ptr, None, r.ptr, None, n, 0, n, 0.1, None, 0.0, 0.0, 1, plan, 0)
     plan.k = 33
@@ -626,7 +627,7 @@ def test_apply_snapshot_plan_concurrent_streams(N):
     reps = [Arena(n, 0) for _ in range(K)]
     streams = [torch.cuda.Stream() for _ in range(K)]
     bounds = np.linspace(0, n, K + 1).astype(np.int64)
-    bnd = torch.tensor(bounds, device="cuda")
+    bnd = np.ascontiguousarray(bounds, dtype=np.int64)
     stamps = torch.zeros(K + 1, dtype=torch.int32, device="cuda")
     cell = torch.zeros(1, dtype=torch.long, device="cuda")
     tag_dev = torch.zeros((K, steps, k), dtype=torch.int32, device="cuda")
@@ -638,7 +639,7 @@ def test_apply_snapshot_plan_concurrent_streams(N):
     for t in range(steps):
         for s, st in enumerate(streams):
             plan = N.TagPlan(idx[s, t].ctypes.data, tag_dev[s, t].data_ptr(), None, None, None,
-                             cell.data_ptr(), stamps.data_ptr(), bnd.data_ptr(), K, s + 1, k)
+                             cell.data_ptr(), stamps.data_ptr(), bnd.ctypes.data, K, s + 1, k)
             N.apply_snapshot_plan(x.ptr, g.data_ptr(), None, reps[s].ptr, None, n, int(bounds[s]),
                                   int(bounds[s + 1]), 1.0, None, 0.0, 0.0, 1000 * (s + 1) + t, plan,
                                   st.cuda_stream)

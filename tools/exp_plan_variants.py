@@ -22,7 +22,7 @@ stamps = torch.zeros(5, dtype=torch.int32, device="cuda")
 for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000)):
     x, g, m, rep = (Arena(d, 0) for _ in range(4))
     x.tensor.normal_(), g.tensor.normal_()
-    bnd = torch.tensor([0, lo, hi, d], dtype=torch.long, device="cuda")
+    bnd = torch.tensor([0, lo, hi, d], dtype=torch.long)   # host boundaries
 
     def plan(next_idx=True, next_host=False, claim=None):
         return N.TagPlan(idx.data_ptr() if next_idx else None, tags_dev[16:32].data_ptr(),

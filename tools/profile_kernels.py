@@ -48,7 +48,7 @@ stamps = torch.zeros(5, dtype=torch.int32, device="cuda")
 
 
 def make_plan(d, lo, hi):
-    bnd = torch.tensor([0, lo, hi, d], dtype=torch.long, device="cuda")
+    bnd = torch.tensor([0, lo, hi, d], dtype=torch.long)   # host boundaries
     return bnd, N.TagPlan(idx.data_ptr(), dev_tags[16:].data_ptr(), None,
                           dev_tags[:16].data_ptr(), claim.data_ptr(), cell.data_ptr(),
                           stamps.data_ptr(), bnd.data_ptr(), 3, 2, 16)
