@@ -479,6 +479,8 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 struct TagPlanDev {
   int64_t idx[32];          // the next step's k sampled indices, by value (constant bank)
   int8_t blk[32];           // ... and the partial block b(e) holding each (from host bounds)
+  uint32_t owner[32];       // owning thread of each, ascending (computed at launch)
+  int8_t owner_j[32];       // ... and which sampled element it is
   int has_next;
   int* next_dev;            // -> the next step's effective tags (device ring slot)
   int* next_host;           // -> and a host-mapped copy for the records (may be null)
@@ -549,22 +551,22 @@ __global__ void __launch_bounds__(kThreads)
   // which of the next step's sampled elements this thread refreshes: the
   // owner of vector v is thread v mod stride (iteration v / stride); a tail
   // element e >= 4 nvec belongs to block 0, thread (e - 4 nvec) mod blockDim
-  // which of the next step's sampled elements this thread refreshes: the
-  // plan launch uses a power-of-two grid, so vector v belongs to thread
-  // v & (stride - 1); a tail element e >= 4 nvec to block 0, thread
-  // (e - 4 nvec) mod blockDim.  The indices are launch parameters (constant
-  // bank): a load from memory here, once per CTA, doubled the in-situ
-  // latency of the launch, whose CTAs run in many small waves among the
-  // convolutions' CTAs
+  // which of the next step's sampled elements this thread refreshes: vector
+  // v belongs to thread v mod stride, a tail element e >= 4 nvec to block 0,
+  // thread (e - 4 nvec) mod blockDim.  The launcher computes the owners and
+  // passes them sorted in the launch parameters (constant bank): a load
+  // from memory here, once per CTA, doubled the in-situ latency of the
+  // launch, whose CTAs run in many small waves among the convolutions'
+  // CTAs, and 16 per-thread ownership tests cost ~8 us of it
   unsigned own = 0;
   if (PLAN && plan.has_next) {
-    const size_t mask = stride - 1;
-    for (int j = 0; j < plan.k; ++j) {
-      const size_t e = (size_t)plan.idx[j], v = e >> 2;
-      const bool mine = v < nvec ? ((v & mask) == tid)
-                                 : (blockIdx.x == 0 && ((e - 4 * nvec) & (kThreads - 1)) == threadIdx.x);
-      if (mine) own |= 1u << j;
+    // owners sorted at launch: a binary search over <= 32 (~5 compares)
+    int a = 0, b = plan.k;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (plan.owner[mid] < (uint32_t)tid) a = mid + 1; else b = mid;
     }
+    for (; a < plan.k && plan.owner[a] == (uint32_t)tid; ++a) own |= 1u << plan.owner_j[a];
   }
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element
@@ -698,10 +700,19 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     return e ? std::atol(e) : 0L;
   }();
   if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
-  // the plan kernel finds a sampled element's owner as v & (stride - 1):
-  // round its grid down to a power of two (267 -> 256 CTAs at d20)
-  if (plan)
-    while (grid & (grid - 1)) grid &= grid - 1;
+  if (plan && pd.has_next) {  // owning thread of each sampled element, sorted
+    const size_t stride = (size_t)grid * kThreads;
+    for (int j = 0; j < pd.k; ++j) {
+      const size_t e = (size_t)pd.idx[j], v = e / 4;
+      pd.owner[j] = (uint32_t)(v < nvec ? v % stride : (e - 4 * nvec) % kThreads);
+      pd.owner_j[j] = (int8_t)j;
+    }
+    for (int j = 1; j < pd.k; ++j)  // insertion sort of <= 32 (owner, j) pairs
+      for (int i = j; i > 0 && pd.owner[i - 1] > pd.owner[i]; --i) {
+        uint32_t t = pd.owner[i]; pd.owner[i] = pd.owner[i - 1]; pd.owner[i - 1] = t;
+        int8_t u = pd.owner_j[i]; pd.owner_j[i] = pd.owner_j[i - 1]; pd.owner_j[i - 1] = u;
+      }
+  }
   cudaStream_t st = (cudaStream_t)stream;
   bool WD = wd != 0.f, MOM = mu != 0.f;
   // one vector per thread per grid stride: unrolling (2, 4 vectors with all
