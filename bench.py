@@ -464,7 +464,7 @@ def ours(args) -> None:
                 return steps * batch * ws / (ms / 1e3)
 
             base = {}
-            coll = "NCCL all-reduce" if ws > 1 else "none (one worker)"
+            coll = f"{dist.get_backend()} all-reduce" if ws > 1 else "none (one worker)"
             mb = sync_rate("mb_sgd", B, K * U, W * U)
             base["mb_sgd"] = {"value": mb, "unit": "images/s", "batch_per_gpu": B, "streams": 1,
                               "collective": coll, "note": "B1: synchronous SGD, same per-GPU batch"}
