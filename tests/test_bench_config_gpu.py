@@ -193,3 +193,44 @@ def test_bench_pipeline_matches_oracle_resnet20_fp32():
     # parameter differences above
     np.testing.assert_allclose(res.losses[0], want[0], rtol=1e-6)
     np.testing.assert_allclose(res.losses, want, rtol=1e-4)
+
+
+@pytest.mark.parametrize("record_mode", ["full", "light"])
+def test_serialized_momentum_q2u2_matches_oracle(record_mode):
+    """Momentum 0.9 / weight decay 5e-4 (one momentum buffer per updater
+    stream) with averaging across Q = 2 workers x U = 2 updaters: the
+    serialized schedule (the parity mode, unfused K3 / K1) against the
+    oracle; "light" records also draw the 16 sampled tag indices from each
+    updater's rng before its batch (engine.py:343-351), which shifts the
+    batch stream."""
+    import dataclasses
+
+    from oracle import data as odata
+    from oracle import schedule as osched
+    from oracle.mlp import MlpOracle
+    from paper_2203_06638_b200.engine import RunConfig, run_experiment
+    from paper_2203_06638_b200.objectives import MlpObjective
+    from paper_2203_06638_b200.partition import make_partition
+    from paper_2203_06638_b200.schedules import LrSchedule, SyncScheme
+
+    X, y = odata.make_blobs(48, 6, 6, 2.0, 0.5, 13)
+    obj = MlpObjective(X, y, (6, 6, 6), 6)
+    bounds = (0, obj.edges[2], obj.dim)
+    T = 80
+    sched = LrSchedule(kind="cosine", alpha0=0.05, total=T, warmup=8, batch_local=8, workers=2,
+                       batch_base=8, boost=True)
+    cfg = RunConfig(algo="lpp_sgd", objective=obj, partition=make_partition(obj.dim, bounds), lr=sched,
+                    sync=SyncScheme(total=T, period=4), budget=T, warm_start_budget=8, workers=2,
+                    updaters=2, batch_size=8, seed=3, schedule="serialized", record_mode=record_mode,
+                    record_tensors=False, evaluate=False, momentum=MU, weight_decay=WD)
+    res = run_experiment(cfg)
+    o = MlpOracle(X, y, (6, 6, 6), 6)
+    tr = osched.run_serialized(
+        o, algo="lpp_sgd", workers=2, updaters=2, boundaries=bounds,
+        lr=osched.Lr(kind="cosine", alpha0=0.05, total=T, warmup=8, peak=sched.peak),
+        switch_point=cfg.sync.switch_point, period=4, budget=T, warm_start=8, batch_size=8, seed=3,
+        mu=MU, wd=WD, tag_draw=16 if record_mode == "light" else 0)
+    assert sorted((u.worker, u.rank, u.s, u.block_id) for u in res.updates) == sorted(tr.block_ids)
+    assert [tuple(r) for r in res.round_trace] == [(a, b, *c) for a, b, c in tr.rounds]
+    np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-5, rtol=1e-4)
+    assert np.max(np.abs(tr.final_values - res.x0)) > 1e-2
