@@ -13,9 +13,13 @@ from paper_2203_06638_b200.engine import Trainer
 from paper_2203_06638_b200.objectives import ResNetObjective
 
 torch.backends.cudnn.benchmark = True
+torch.backends.cudnn.allow_tf32 = False        # the bench's fp32 headline
+torch.backends.cuda.matmul.allow_tf32 = False
 K, W, U = 20, 5, 4
-out_dir = Path(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out")
-obj = ResNetObjective("resnet20", n_samples=50_000, seed=0, data="device")
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+out_dir = Path(args[0] if args else "gpurun_out")
+obj = ResNetObjective("resnet20", n_samples=50_000, seed=0, data="device",
+                      autocast=None if "--bf16" not in sys.argv else "bf16")
 cfg = bench.build_cfg(obj, (K + W) * U)
 tr = Trainer(cfg)
 tr.run(W * U, evaluate=False)
@@ -41,11 +45,13 @@ for n, _, d in rows:
     tot[k] += d
     cnt[k] += 1
 T = sum(tot.values())
-ours = ("k_apply", "void k_apply", "k_snapshot", "void k_average", "k_accum", "k_gather", "(anonymous namespace)::k_sample")
+ours = ("k_apply", "void k_apply", "k_snapshot", "void k_average", "k_accum", "k_gather", "k_publish",
+        "k_set_i64", "k_classify", "(anonymous namespace)::k_sample")
 mine = sum(v for k, v in tot.items() if k.startswith(ours))
 span = (rows[-1][1] + rows[-1][2] - rows[0][1]) if rows else 0
 lines = [f"# {len(rows)} kernels in the timed region of {K * U + U} minibatches "
-         f"(ResNet-20 LPP-SGD U=4 B=128, native loop); summed kernel time {T / 1e3:.1f} ms "
+         f"(ResNet-20 LPP-SGD U=4 B=128, {'bf16' if '--bf16' in sys.argv else 'fp32'} convolutions, "
+         f"native loop); summed kernel time {T / 1e3:.1f} ms "
          f"over a {span / 1e3:.1f} ms span (4 streams overlap)",
          f"# our kernels (K1-K5 + in-graph sampler): {100 * mine / T:.2f}% of summed kernel time",
          "share%   total_us   n   kernel"]
