@@ -715,3 +715,60 @@ def test_element_load_store_f32(N):
     s = torch.cuda.Stream()
     st.write(1, 12.0, stream=s)
     assert st.read(1, stream=s) == 12.0
+
+
+@pytest.mark.parametrize("round_lands", [False, True])
+def test_fused_and_unfused_k5_classify_alike(N, round_lands):
+    """The reference's classification (engine.py:343-362): a step is clean
+    iff its sampled tags, read at its snapshot, are all >= k_claim, the
+    round stamp read after its gradient.  Scripted on one stream, the
+    unfused path (per-element tags, lpp_gather_tags_floor at the snapshot,
+    lpp_classify before the apply) and the fused path (block stamps; step
+    t's apply reads step t+1's tags after its own reduction, step t+1's
+    apply classifies) must agree, with and without a round landing
+    between step t+1's snapshot and its apply."""
+    from paper_2203_06638_b200.arena import Arena
+
+    n, k = 4096, 8
+    bounds = np.array([0, 2048, n], dtype=np.int64)
+    bnd_dev = torch.tensor(bounds, device="cuda")
+    x, g, rep, tags = (Arena(n, 0) for _ in range(4))
+    g.tensor.fill_(1e-3)
+    cell = torch.zeros(1, dtype=torch.long, device="cuda")
+    stamps = torch.zeros(3, dtype=torch.int32, device="cuda")
+    rec = torch.zeros((2, 2 + k), dtype=torch.long, device="cuda")      # claim + tags (as int32 pairs)
+    rt = lambda s: rec[s].data_ptr() + 16                                # noqa: E731
+    idx = np.ascontiguousarray(np.arange(100, 100 + 8 * 250, 250)[:k], dtype=np.int64)  # inside block 1
+    idx_dev = torch.tensor(idx, device="cuda")
+    # a round with stamp 5 was applied before the run (floor 5); step t
+    # (stamp 7) writes block 1; step t+1 samples tags inside block 1
+    cell.fill_(5)
+    # --- unfused: t applies (per-element tags), t+1 snapshot gathers, [round 9], classify
+    N.apply_sgd_tagged(x.ptr, g.ptr, None, 2048, 0.1, None, 0.0, 0.0, N.MODE_RED, tags.ptr, 7, 0)
+    N.gather_tags_floor(tags.ptr, idx_dev.data_ptr(), k, cell.data_ptr(), rt(0), None, 0)
+    if round_lands:
+        N.set_i64(cell.data_ptr(), 9, 0)
+    N.classify(rt(0), k, cell.data_ptr(), rec[0].data_ptr(), 0)
+    torch.cuda.synchronize()
+    unfused = (int(rec[0, 0]), int(rec[0, 1]))
+    # --- fused: t's apply reads t+1's tags; [round 9]; t+1's apply classifies
+    cell.fill_(5)
+    plan_t = N.TagPlan(idx.ctypes.data, rt(1), None, None, None, cell.data_ptr(), stamps.data_ptr(),
+                       bounds.ctypes.data, 2, 1, k)
+    N.apply_snapshot_plan(x.ptr, g.ptr, None, rep.ptr, None, n, 0, 2048, 0.1, None, 0.0, 0.0, 7, plan_t, 0)
+    N.publish_stamp(stamps.data_ptr(), 1, 7, 0)
+    if round_lands:
+        N.set_i64(cell.data_ptr(), 9, 0)
+    plan_t1 = N.TagPlan(None, None, None, rt(1), rec[1].data_ptr(), cell.data_ptr(), stamps.data_ptr(),
+                        bounds.ctypes.data, 2, 2, k)
+    N.apply_snapshot_plan(x.ptr, g.ptr, None, rep.ptr, None, n, 2048, n, 0.1, None, 0.0, 0.0, 8, plan_t1, 0)
+    torch.cuda.synchronize()
+    fused = (int(rec[1, 0]), int(rec[1, 1]))
+    tags_u = rec[0, 2:].cpu().numpy().view(np.int32)[:k]
+    tags_f = rec[1, 2:].cpu().numpy().view(np.int32)[:k]
+    assert np.array_equal(tags_u, tags_f) and (tags_f == 7).all()   # step t's stamp, seen at t+1's snapshot
+    want = (9, 0) if round_lands else (5, 1)                          # reference: 7 >= 9 false / 7 >= 5 true
+    assert unfused == fused == want
+    for a in (x, g, rep, tags):
+        a.close()
+    del bnd_dev
