@@ -554,19 +554,17 @@ __global__ void __launch_bounds__(kThreads)
   // which of the next step's sampled elements this thread refreshes: vector
   // v belongs to thread v mod stride, a tail element e >= 4 nvec to block 0,
   // thread (e - 4 nvec) mod blockDim.  The launcher computes the owners and
-  // passes them sorted in the launch parameters (constant bank): a load
-  // from memory here, once per CTA, doubled the in-situ latency of the
-  // launch, whose CTAs run in many small waves among the convolutions'
-  // CTAs, and 16 per-thread ownership tests cost ~8 us of it
+  // passes them in the launch parameters (constant bank): a load from
+  // memory here, once per CTA, doubled the in-situ latency of the launch,
+  // whose CTAs run in many small waves among the convolutions' CTAs, and
+  // per-thread modulo arithmetic cost ~8 us of it
   unsigned own = 0;
   if (PLAN && plan.has_next) {
-    // owners sorted at launch: a binary search over <= 32 (~5 compares)
-    int a = 0, b = plan.k;
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (plan.owner[mid] < (uint32_t)tid) a = mid + 1; else b = mid;
-    }
-    for (; a < plan.k && plan.owner[a] == (uint32_t)tid; ++a) own |= 1u << plan.owner_j[a];
+    // fully unrolled: each compare takes its operand straight from the
+    // constant bank (no load, no divergence)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < plan.k && plan.owner[j] == (uint32_t)tid) own |= 1u << plan.owner_j[j];
   }
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element

@@ -13,9 +13,11 @@ from paper_2203_06638_b200.objectives import ResNetObjective  # noqa: E402
 torch.backends.cudnn.benchmark = True
 torch.backends.cudnn.allow_tf32 = False
 torch.backends.cuda.matmul.allow_tf32 = False
-for tf32 in (False, True):
+limits = [int(a) for a in sys.argv[1:]] or [10]
+for tf32, cl, lim in [(False, True, l) for l in limits] + ([(False, False, 10), (True, True, 10)] if len(sys.argv) == 1 else []):
     torch.backends.cudnn.allow_tf32 = tf32
-    for cl in (True, False):
+    torch.backends.cudnn.benchmark_limit = lim
+    if True:
         obj = ResNetObjective("resnet20", n_samples=4096, seed=0, autocast=None, channels_last=cl)
         arena = torch.from_numpy(obj.init_params(0)).float().cuda()
         grads = torch.zeros_like(arena)
@@ -46,4 +48,4 @@ for tf32 in (False, True):
             g.replay()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        print(f"tf32={tf32} channels_last={cl}: {n * 512 / dt:,.0f} images/s")
+        print(f"tf32={tf32} channels_last={cl} benchmark_limit={lim}: {n * 512 / dt:,.0f} images/s")
