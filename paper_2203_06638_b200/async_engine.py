@@ -470,11 +470,11 @@ class _Engine(NativeLoops):
             if self.time_apply:
                 e1.record(astream)
                 self.apply_events.append((e0, e1, self.apply_bytes_per_elem * blk.length))
-            if tracks:
-                w.copy_rec(r, slot, sp)             # (k_claim, clean) + tags -> host
             if astream is not stream:
                 w.apply_done[r].record(astream)
                 stream.wait_event(w.apply_done[r])
+            if tracks:   # (k_claim, clean) + tags -> host, on the updater stream
+                w.copy_rec(r, slot, stream.cuda_stream)
             if self.read_loss:
                 self.read_back_loss(w, r, slot, buf)
 
@@ -605,13 +605,15 @@ class _Engine(NativeLoops):
                 nbytes = self.apply_bytes_per_elem * blk.length + 4 * (self.dim - blk.length) \
                     + 4 * self.dim
                 self.apply_events.append((e0, e1, nbytes))
-            if plan is not None:                    # K5: this update's block stamp
-                N.publish_stamp(w.block_stamps.data_ptr(), block_id, u, sp)
-            if tracks:
-                w.copy_rec(r, slot, sp)             # (k_claim, clean) + tags -> host
             if astream is not stream:
                 w.apply_done[r].record(astream)
                 stream.wait_event(w.apply_done[r])
+            # K5 bookkeeping on the updater stream, after the apply: this
+            # update's block stamp, then (k_claim, clean) + tags -> host
+            if plan is not None:
+                N.publish_stamp(w.block_stamps.data_ptr(), block_id, u, stream.cuda_stream)
+            if tracks:
+                w.copy_rec(r, slot, stream.cuda_stream)
             if self.read_loss:
                 self.read_back_loss(w, r, slot, buf)
 

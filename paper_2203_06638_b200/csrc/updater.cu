@@ -503,14 +503,19 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     }
     if (rc != LPP_OK) return rc;
     if (c->time_apply) CUDA_TRY(cudaEventRecord(t1.ev[k], astream));
-    if (c->fused && K > 0 &&
-        (rc = lpp_publish_stamp(c->block_stamps, b, (int32_t)u, astream)) != LPP_OK)
-      return rc;
-    if (K > 0 && (rc = copy_rec(slot, astream)) != LPP_OK) return rc;
+
     if (side) {
       CUDA_TRY(cudaEventRecord(order.ev[1], astream));
       CUDA_TRY(cudaStreamWaitEvent(stream, order.ev[1], 0));
     }
+    // K5 bookkeeping on the updater stream, ordered after the apply: this
+    // update's block stamp, then the step's record to the host (queued
+    // behind the apply on the high-priority apply stream, the copy measured
+    // +5 us on the apply's in-situ time, tools/exp_insitu_variants.py)
+    if (c->fused && K > 0 &&
+        (rc = lpp_publish_stamp(c->block_stamps, b, (int32_t)u, stream)) != LPP_OK)
+      return rc;
+    if (K > 0 && (rc = copy_rec(slot, stream)) != LPP_OK) return rc;
     CUDA_TRY(cudaEventRecord(done.ev[k], stream));
     used[k] = 1;
     claim_of[k] = k_claim;
