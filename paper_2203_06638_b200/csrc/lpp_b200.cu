@@ -533,7 +533,7 @@ __device__ __forceinline__ void fused_elem(float* x, const float* g, float* m, f
   }
 }
 
-template <bool WD, bool MOM, bool TAGS, bool PLAN>
+template <bool WD, bool MOM, bool TAGS, bool PLAN, int UNR = 1>
 __global__ void __launch_bounds__(kThreads)
     k_apply_snapshot(float* x, const float* __restrict__ g, float* m, float* __restrict__ rep,
                      int* tags, size_t n, size_t lo, size_t hi, float lr,
@@ -548,9 +548,6 @@ __global__ void __launch_bounds__(kThreads)
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nvec = n / 4;
-  // which of the next step's sampled elements this thread refreshes: the
-  // owner of vector v is thread v mod stride (iteration v / stride); a tail
-  // element e >= 4 nvec belongs to block 0, thread (e - 4 nvec) mod blockDim
   // which of the next step's sampled elements this thread refreshes: vector
   // v belongs to thread v mod stride, a tail element e >= 4 nvec to block 0,
   // thread (e - 4 nvec) mod blockDim.  The launcher computes the owners and
@@ -569,39 +566,70 @@ __global__ void __launch_bounds__(kThreads)
   // vectors fully inside [lo, hi) take the apply path, vectors fully outside
   // the copy path; the (at most two) straddling vectors go per element
   const size_t vlo = (lo + 3) / 4, vhi = hi / 4;
-  for (size_t i = tid; i < nvec; i += stride) {
-    if (PLAN && own) {  // sampled elements of this vector: tags before values
-      for (unsigned bits = own; bits; bits &= bits - 1) {
-        const int j = __ffs(bits) - 1;
-        const int64_t e = plan.idx[j];
-        if ((size_t)e / 4 == i) {
-          const int t = plan_tag_of(plan, j, e, lo, hi, stamp);
-          plan.next_dev[j] = t;
-          if (plan.next_host) plan.next_host[j] = t;
+  // UNR vectors per thread per round (v = i0 + u * stride keeps the owner
+  // rule): every load of the round is issued before the first reduction,
+  // then the reductions, then the re-reads — more bytes in flight per
+  // resident thread, which is what matters when the launch only gets the
+  // SM slots the convolutions leave (in situ)
+  for (size_t i0 = tid; i0 < nvec; i0 += stride * UNR) {
+    float4 gr[UNR], xr[UNR], mr[UNR];
+    int kind[UNR];  // 0 none, 1 inside the block, 2 outside, 3 straddling
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const size_t i = i0 + (size_t)u * stride;
+      kind[u] = 0;
+      gr[u] = xr[u] = mr[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i >= nvec) continue;
+      if (PLAN && own) {  // sampled elements of this vector: tags before values
+        for (unsigned bits = own; bits; bits &= bits - 1) {
+          const int j = __ffs(bits) - 1;
+          const int64_t e = plan.idx[j];
+          if ((size_t)e / 4 == i) {
+            const int t = plan_tag_of(plan, j, e, lo, hi, stamp);
+            plan.next_dev[j] = t;
+            if (plan.next_host) plan.next_host[j] = t;
+          }
         }
       }
+      if (i >= vlo && i < vhi) {
+        kind[u] = 1;
+        gr[u] = __ldg(reinterpret_cast<const float4*>(g) + i);
+        if (WD) xr[u] = ld_cg4(x + 4 * i);
+        if (MOM) mr[u] = reinterpret_cast<const float4*>(m)[i];
+      } else if (4 * i + 4 <= lo || 4 * i >= hi) {
+        kind[u] = 2;
+        xr[u] = ld_cg4(x + 4 * i);
+      } else {
+        kind[u] = 3;
+      }
     }
-    if (i >= vlo && i < vhi) {
-      float4 gr = __ldg(reinterpret_cast<const float4*>(g) + i);
-      float4 xr = make_float4(0.f, 0.f, 0.f, 0.f), mr = xr;
-      if (WD) xr = ld_cg4(x + 4 * i);
-      if (MOM) mr = reinterpret_cast<const float4*>(m)[i];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (kind[u] != 1) continue;
+      const size_t i = i0 + (size_t)u * stride;
       float4 dr;
-      dr.x = sgd_delta<WD, MOM>(gr.x, xr.x, mr.x, lr, mu, wd);
-      dr.y = sgd_delta<WD, MOM>(gr.y, xr.y, mr.y, lr, mu, wd);
-      dr.z = sgd_delta<WD, MOM>(gr.z, xr.z, mr.z, lr, mu, wd);
-      dr.w = sgd_delta<WD, MOM>(gr.w, xr.w, mr.w, lr, mu, wd);
-      // vector reduction, then re-read: the replica gets the arena value
-      // after this step's add (plus any concurrent adds that landed first),
-      // i.e. what a K3 snapshot right after the apply would copy
+      dr.x = sgd_delta<WD, MOM>(gr[u].x, xr[u].x, mr[u].x, lr, mu, wd);
+      dr.y = sgd_delta<WD, MOM>(gr[u].y, xr[u].y, mr[u].y, lr, mu, wd);
+      dr.z = sgd_delta<WD, MOM>(gr[u].z, xr[u].z, mr[u].z, lr, mu, wd);
+      dr.w = sgd_delta<WD, MOM>(gr[u].w, xr[u].w, mr[u].w, lr, mu, wd);
+      // vector reduction, then (below) the re-read: the replica gets the
+      // arena value after this step's add (plus any concurrent adds that
+      // landed first), i.e. what a K3 snapshot right after the apply copies
       red_add_v4(x + 4 * i, dr);
-      float4 nv = ld_cg4(x + 4 * i);
-      if (MOM) reinterpret_cast<float4*>(m)[i] = mr;
-      reinterpret_cast<float4*>(rep)[i] = nv;
-    } else if (4 * i + 4 <= lo || 4 * i >= hi) {
-      reinterpret_cast<float4*>(rep)[i] = ld_cg4(x + 4 * i);
-    } else {
-      for (size_t e = 4 * i; e < 4 * i + 4; ++e) fused_elem<WD, MOM>(x, g, m, rep, e, lo, hi, lr, mu, wd);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const size_t i = i0 + (size_t)u * stride;
+      if (kind[u] == 1) {
+        const float4 nv = ld_cg4(x + 4 * i);
+        if (MOM) reinterpret_cast<float4*>(m)[i] = mr[u];
+        reinterpret_cast<float4*>(rep)[i] = nv;
+      } else if (kind[u] == 2) {
+        reinterpret_cast<float4*>(rep)[i] = xr[u];
+      } else if (kind[u] == 3) {
+        for (size_t e = 4 * i; e < 4 * i + 4; ++e)
+          fused_elem<WD, MOM>(x, g, m, rep, e, lo, hi, lr, mu, wd);
+      }
     }
   }
   if (blockIdx.x == 0)
@@ -698,6 +726,13 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     return e ? std::atol(e) : 0L;
   }();
   if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
+  // experiment hook: LPP_FUSED_UNR = 2 / 4 vectors per thread per round
+  // for the plan kernel (tools/exp_insitu_variants.py)
+  static const int unr = [] {
+    const char* e = std::getenv("LPP_FUSED_UNR");
+    const int v = e ? std::atoi(e) : 1;
+    return (v == 2 || v == 4) ? v : 1;
+  }();
   if (plan && pd.has_next) {  // owning thread of each sampled element, sorted
     const size_t stride = (size_t)grid * kThreads;
     for (int j = 0; j < pd.k; ++j) {
@@ -719,7 +754,13 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
   // or 128-thread CTAs (easier to fit between other streams' CTAs) changed
   // neither the in-situ d20 time nor images/s
 #define FUSED_LAUNCH(W, M)                                                                      \
-  if (plan)                                                                                     \
+  if (plan && unr == 4)                                                                         \
+    k_apply_snapshot<W, M, false, true, 4><<<grid, kThreads, 0, st>>>(                         \
+        x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
+  else if (plan && unr == 2)                                                                    \
+    k_apply_snapshot<W, M, false, true, 2><<<grid, kThreads, 0, st>>>(                         \
+        x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
+  else if (plan)                                                                                \
     k_apply_snapshot<W, M, false, true><<<grid, kThreads, 0, st>>>(                            \
         x, g, m, replica, tags, n, lo, hi, lr, lr_dev, mu, wd, stamp, pd);                     \
   else if (tags)                                                                                \
