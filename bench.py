@@ -301,13 +301,13 @@ def ours(args) -> None:
         grid20 = min(-(-(dim20 // 4) // 256), 148 * 16)     # the launch's grid at d20
         cands = [e for e in launches_ if e["kernel"].startswith(name) and e["grid"] == grid20]
         traffic = sum(e["dram_bytes"] for e in cands) / len(cands) if cands else None
-        floor = [e["us"] for e in launches_ if e["kernel"] == "k_gather_tags"]
+        floor = [e["us"] for e in launches_ if e["kernel"].startswith(("k_gather", "void k_gather"))]
         if cands:
             us = sum(e["us"] for e in cands) / len(cands)
             standalone = {"us": us, "latency_floor_us": min(floor) if floor else None,
                           "src": f"{tp.relative_to(ROOT)}: ncu gpu__time_duration of the same kernel "
                                  "at d20 launched alone (cold L2); latency_floor_us = a 16-element "
-                                 "gather kernel"}
+                                 "gather kernel (a launch + dependent loads)"}
     line = {
         "metric": "train_images_per_sec", "value": value, "unit": "images/s", "n_gpus": ws,
         "steps": K, "warmup": W, "ms_per_step": dev_ms / K, "higher_is_better": True,

@@ -66,6 +66,12 @@ for d, lo, hi in ((272_474, 68_000, 204_000), (25_557_032, 2_000_000, 12_000_000
         N.apply_snapshot(x.ptr, g.ptr, m.ptr, rep.ptr, None, d, lo, hi, 1e-3, None, 0.9, 5e-4, 3, st)
     for a in (x, g, m, rep, tg):
         a.close()
+# the latency floor: a 16-element sampled-tag gather (one launch, dependent loads)
+idx_dev = idx.cuda()
+for _ in range(2):
+    flush()
+    N.gather_block_stamps(stamps.data_ptr(), torch.tensor([0, 5000, 272_474], device="cuda").data_ptr(), 2,
+                          idx_dev.data_ptr(), 16, cell.data_ptr(), dev_tags.data_ptr(), None, st)
 d = 16_000_000
 ars = [Arena(d, 0) for _ in range(4)]
 for _ in range(2):
