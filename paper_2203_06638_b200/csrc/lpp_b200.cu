@@ -726,12 +726,15 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     return e ? std::atol(e) : 0L;
   }();
   if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
-  // experiment hook: LPP_FUSED_UNR = 2 / 4 vectors per thread per round
-  // for the plan kernel (tools/exp_insitu_variants.py)
+  // vectors per thread per round of the plan kernel: 2 (LPP_FUSED_UNR
+  // overrides: 1, 2, 4).  In situ (bf16 ResNet-18 / ResNet-50 steps,
+  // tools/exp_fused_insitu.py) 2 reaches 0.72 / 0.79-0.81 of HBM vs 0.70 /
+  // 0.75-0.76 with 1 and 0.63 / 0.73-0.75 with 4 (84 registers); standalone
+  // and at d20 in situ the three are within noise
   static const int unr = [] {
     const char* e = std::getenv("LPP_FUSED_UNR");
-    const int v = e ? std::atoi(e) : 1;
-    return (v == 2 || v == 4) ? v : 1;
+    const int v = e ? std::atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
   if (plan && pd.has_next) {  // owning thread of each sampled element, sorted
     const size_t stride = (size_t)grid * kThreads;
