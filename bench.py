@@ -510,69 +510,59 @@ def ours(args) -> None:
             t6.close()
             del t6
 
-    # ---------------- ResNet-18 / CIFAR-100 shape (config C2) ----------------
-    if not args.no_rn18 and ws == 1:
+    def phase(cfg_, steps, warm, images_per_slot, time_apply=False):
+        """warm-up + timed phase of cfg_ over the group; returns (whole-job
+        images/s, result); the timed region is max over ranks."""
+        t = Trainer(cfg_, group=group, time_apply=time_apply)
+        t.run(warm, evaluate=False)
+        barrier()
+        r = t.run(steps, evaluate=False)
+        ms = max_over_ranks(r.device_ms)
+        slots = sum(r.counter_finals) if cfg_.algo in ("lap_sgd", "lpp_sgd") else steps
+        t.close()
+        return slots * images_per_slot * ws / (ms / 1e3), r
+
+    def apply_roofline(r):
+        na, msa, bya = r.apply_timing
+        a_ = bya / (msa / 1e3) / 1e9
+        return {"achieved": a_, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": a_ / peaks["hbm_gbs"],
+                "launches": na, "avg_us": 1e3 * msa / max(na, 1), "bytes_per_launch": bya / max(na, 1)}
+
+    # ---------------- ResNet-18 / CIFAR-100 shape (config C2), at every N ----------------
+    if not args.no_rn18:
         with _Optional(line, "resnet18"):
             obj18 = ResNetObjective("resnet18", n_samples=N_SAMPLES, seed=0, data="device")
             out18 = {"workload": "resnet18_cifar100_u4_b128", "params": obj18.dim, "unit": "images/s",
-                     "conv_compute": "bf16 shadow weights (all three rows)"}
+                     "workers": ws, "conv_compute": "bf16 shadow weights (all three rows)",
+                     "collective": f"{dist.get_backend()} all-reduce (B1/B2)" if ws > 1 else "none"}
             for algo in ("lpp_sgd", "mb_sgd", "pl_sgd"):
-                c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=1)
-                t18 = Trainer(c18, time_apply=(algo == "lpp_sgd"))
-                t18.run(3 * U, evaluate=False)
-                torch.cuda.synchronize()
-                r18 = t18.run(args.rn18_steps * U, evaluate=False)
-                n18 = sum(r18.counter_finals) if algo == "lpp_sgd" else args.rn18_steps * U
-                if algo != "lpp_sgd":
-                    t18.close()
-                out18[algo] = n18 * B / (r18.device_ms / 1e3)
-                if algo == "lpp_sgd":
-                    na, msa, bya = r18.apply_timing
-                    a18 = bya / (msa / 1e3) / 1e9
-                    out18["apply_roofline"] = {"achieved": a18, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                               "frac": a18 / peaks["hbm_gbs"], "launches": na,
-                                               "avg_us": 1e3 * msa / max(na, 1),
-                                               "bytes_per_launch": bya / max(na, 1)}
-                    t18.close()
-                del t18
+                c18 = build_cfg(obj18, (args.rn18_steps + 3) * U, algo=algo, workers=ws)
+                lpp = algo == "lpp_sgd"
+                v18, r18 = phase(c18, args.rn18_steps * U, 3 * U, B, time_apply=lpp)
+                out18[algo] = v18
+                if lpp:
+                    out18["apply_roofline"] = apply_roofline(r18)
             out18["lpp_over_mb"] = out18["lpp_sgd"] / out18["mb_sgd"]
             out18["lpp_over_pl"] = out18["lpp_sgd"] / out18["pl_sgd"]
             line["resnet18"] = out18
 
-    # ---------------- ResNet-50 / ImageNet shape (config C3): in-situ HBM apply ----------------
-    if not args.no_rn50 and ws == 1:
+    # ---------------- ResNet-50 / ImageNet shape (config C3), at every N ----------------
+    if not args.no_rn50:
         with _Optional(line, "resnet50"):
             obj50 = ResNetObjective("resnet50", n_samples=2048, seed=0, data="device")
-            c50 = build_cfg(obj50, 64, workers=1)
+            c50 = build_cfg(obj50, 64, workers=ws)
             # C3: B = 32 per stream, non-blocking averaging every H = 16 local
             # steps from the start (switch_point 0, SURVEY §8d)
             c50 = dataclasses.replace(c50, batch_size=32,
                                       sync=SyncScheme(total=c50.sync.total, period=16, switch_point=0))
-            t50 = Trainer(c50, time_apply=True)
-            t50.run(3 * U, evaluate=False)
-            torch.cuda.synchronize()
-            r50 = t50.run(args.rn50_steps * U, evaluate=False)
-            n50, ms50, by50 = r50.apply_timing
-            a50 = by50 / (ms50 / 1e3) / 1e9
+            v50, r50 = phase(c50, args.rn50_steps * U, 3 * U, 32, time_apply=True)
             line["resnet50"] = {
-                "workload": "resnet50_imagenet224_lpp_sgd_u4_b32_h16", "params": obj50.dim,
-                "conv_compute": "bf16 shadow weights (both rows)",
-                "value": sum(r50.counter_finals) * 32 / (r50.device_ms / 1e3), "unit": "images/s",
-                "apply_roofline": {"achieved": a50, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                                   "frac": a50 / peaks["hbm_gbs"], "launches": n50,
-                                   "avg_us": 1e3 * ms50 / max(n50, 1),
-                                   "bytes_per_launch": by50 / max(n50, 1)}}
-            t50.close()
-            del t50
-            m50 = build_cfg(obj50, 64, algo="mb_sgd", workers=1)
-            m50 = dataclasses.replace(m50, batch_size=32)
-            tm50 = Trainer(m50)
-            tm50.run(3 * U, evaluate=False)
-            torch.cuda.synchronize()
-            rm50 = tm50.run(args.rn50_steps * U, evaluate=False)
-            line["resnet50"]["mb_sgd"] = args.rn50_steps * U * 32 / (rm50.device_ms / 1e3)
+                "workload": "resnet50_imagenet224_lpp_sgd_u4_b32_h16", "params": obj50.dim, "workers": ws,
+                "conv_compute": "bf16 shadow weights (both rows)", "value": v50, "unit": "images/s",
+                "apply_roofline": apply_roofline(r50)}
+            m50 = dataclasses.replace(build_cfg(obj50, 64, algo="mb_sgd", workers=ws), batch_size=32)
+            line["resnet50"]["mb_sgd"], _ = phase(m50, args.rn50_steps * U, 3 * U, 32)
             line["resnet50"]["lpp_over_mb"] = line["resnet50"]["value"] / line["resnet50"]["mb_sgd"]
-            del tm50
 
     # ---------------- kernel sweep (HBM roofline evidence) ----------------
     if not args.no_sweep and rank == 0:
