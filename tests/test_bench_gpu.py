@@ -38,3 +38,6 @@ def test_bench_line_contract():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] > 0
     assert d["config"]["workload"] == "resnet20_cifar10_lpp_sgd"
+    # the headline is at the reference arm's precision; bf16 is a labelled extra
+    assert d["dtype"] == "f32" and d["config"]["conv_compute"].startswith("fp32")
+    assert d["value_bf16"] > 0 and d["e2e_bf16"]["value"] > 0
