@@ -7,13 +7,19 @@
 //   K3     k_snapshot             : replica refresh,
 //          replaces ParamStore.snapshot -> snapshot_f64 (_atomics.c:186-215)
 //   K1+K3  k_apply_snapshot       : the async default — one step's apply
-//          fused with the next step's replica refresh (engine.py:343-355)
+//          fused with the next step's replica refresh (engine.py:343-355);
+//          with a lpp_tag_plan also the updater's K5 bookkeeping in the
+//          reference's order (this step's classification, the next step's
+//          sampled tags before their values), per-block write stamps
+//          published by k_publish_stamp after it (engine.py:343-362)
 //   K4     k_average              : owner-computes in-place model averaging,
 //          replaces _averager_body + _MeanAllReduce + add_assign(mean - snap)
 //          (engine.py:199-229, 418-421); k_average_bulk: the TMA-staged
 //          variant (bulk loads on an mbarrier, bulk reductions)
-//   K5     tagged variants / k_gather_tags : write stamps and the sampled
-//          tag gather (_atomics.c:217-310, 346-392)
+//   K5     tagged variants / k_gather_tags / k_gather_tags_floor /
+//          k_gather_block_stamps / k_classify / k_publish_stamp : write
+//          stamps, the sampled-tag gather, the clean classification
+//          (_atomics.c:217-310, 346-392; engine.py:353-362)
 //   K6     host atomics           : _atomics.{load,store,fetch_add}_i64
 //          (_atomics.c:125-183)
 //   NVLS   k_nvls_mean / k_nvls_apply : the averaging round in the switch
