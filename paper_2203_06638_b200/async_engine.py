@@ -512,8 +512,13 @@ class _Engine(NativeLoops):
     def fused(self) -> bool:
         """Whether async steps use the fused apply+next-snapshot kernel."""
         cfg = self.cfg
+        # the fused K5 plan carries at most 32 sampled tags (and block ids
+        # < 128) in its launch parameters; larger ones take the unfused
+        # per-element path
         return (cfg.fuse_snapshot and cfg.schedule == "async" and not cfg.quiescent
-                and cfg.record_mode != "full" and cfg.apply_mode != "plain")
+                and cfg.record_mode != "full" and cfg.apply_mode != "plain"
+                and (not cfg.tracks or (min(cfg.tag_sample, self.dim) <= 32
+                                        and cfg.partition.num_blocks <= 127)))
 
     def gather_tags(self, w: _Worker, r: int, slot: int, tag_idx) -> None:
         """K5: the step's sampled tags, raised to the round floor, into slot
