@@ -234,3 +234,23 @@ def test_serialized_momentum_q2u2_matches_oracle(record_mode):
     assert [tuple(r) for r in res.round_trace] == [(a, b, *c) for a, b, c in tr.rounds]
     np.testing.assert_allclose(res.final_values, tr.final_values, atol=1e-5, rtol=1e-4)
     assert np.max(np.abs(tr.final_values - res.x0)) > 1e-2
+
+
+def test_more_than_32_sampled_tags_take_the_unfused_path():
+    """The fused K5 plan carries <= 32 sampled tags in its launch; a larger
+    tag_sample runs the unfused per-element path and still classifies
+    every update (engine.py:343-362)."""
+    obj, orc, bounds = _c0()
+    cfg = _cfg(obj, bounds, budget=40, B=32, record_mode="light", tag_sample=40)
+    from paper_2203_06638_b200.engine import Trainer
+
+    tr = Trainer(cfg)
+    try:
+        assert not tr.eng.fused() and tr.eng.native_loop()
+        res = tr.run()
+    finally:
+        tr.close()
+    assert all(u.clean is not None and len(u.tags) == 40 for u in res.updates)
+    assert all(u.clean == bool((u.tags >= u.k_claim).all()) for u in res.updates)
+    tr2 = _oracle(orc, cfg, bounds)
+    np.testing.assert_allclose(res.final_values, tr2.final_values, atol=1e-5, rtol=1e-4)
