@@ -35,7 +35,8 @@ Extra keys beyond the base contract:
   resnet50      config C3 (ImageNet-shaped, d = 25.6M, B = 32 per stream,
                 averaging every H = 16 local steps from the start): images/s,
                 the apply kernel's in-situ HBM roofline, vs MB-SGD
-  kernel_sweep  K1/K3 alone at 16M/64M params (HBM roofline evidence)
+  kernel_sweep  K1/K3 and the fused apply with its K5 plan alone at 16M/64M
+                params, L2 flushed (HBM roofline evidence)
 """
 
 from __future__ import annotations
@@ -572,14 +573,40 @@ def ours(args) -> None:
             st = torch.cuda.current_stream().cuda_stream
             scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
             sweep = []
+            import numpy as np
+
+            # the shipped fused apply with its K5 plan (16 sampled tags,
+            # classification, block stamps), as the engine launches it
+            kstamps = torch.zeros(5, dtype=torch.int32, device="cuda")
+            kcell = torch.zeros(1, dtype=torch.long, device="cuda")
+            krec = torch.zeros(64, dtype=torch.long, device="cuda")
+
+            def plan_for(d_, lo_, hi_):
+                bnd = np.array([0, lo_, hi_, d_], dtype=np.int64)
+                idx = np.sort(np.random.default_rng(0).choice(d_, 16, replace=False)).astype(np.int64)
+                return (bnd, idx), N.TagPlan(idx.ctypes.data, krec[32:].data_ptr(), None, krec[4:].data_ptr(),
+                                             krec.data_ptr(), kcell.data_ptr(), kstamps.data_ptr(),
+                                             bnd.ctypes.data, 3, 2, 16)
+
             for d in (16_000_000, 64_000_000):
                 x, g, m = Arena(d, dev), Arena(d, dev), Arena(d, dev)
                 r_ = Arena(d, dev)
+                part = (d // 5, d // 5 + 2 * d // 5)      # a partial block of 40 %
+                keep_full, plan_full = plan_for(d, 0, d)
+                keep_part, plan_part = plan_for(d, *part)
+                blen = part[1] - part[0]
                 for name, fn, bpe in (
                     ("apply_red", lambda: N.apply_sgd(x.ptr, g.ptr, None, d, 1e-3, None, 0.0, 0.0, N.MODE_RED, st), 12),
                     ("apply_red_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_RED, st), 20),
                     ("apply_bulk_mom_wd", lambda: N.apply_sgd(x.ptr, g.ptr, m.ptr, d, 1e-3, None, 0.9, 5e-4, N.MODE_BULK, st), 20),
                     ("snapshot", lambda: N.snapshot(x.ptr, r_.ptr, d, st), 8),
+                    ("fused_apply_k5_full_block_mom_wd",
+                     lambda: N.apply_snapshot_plan(x.ptr, g.ptr, m.ptr, r_.ptr, None, d, 0, d, 1e-3, None, 0.9,
+                                                   5e-4, 3, plan_full, st), 24),
+                    ("fused_apply_k5_block40pct_mom_wd",
+                     lambda: N.apply_snapshot_plan(x.ptr, g.ptr, m.ptr, r_.ptr, None, d, part[0], part[1], 1e-3,
+                                                   None, 0.9, 5e-4, 3, plan_part, st),
+                     (24 * blen + 8 * (d - blen)) / d),
                 ):
                     for _ in range(5):
                         fn()
