@@ -137,8 +137,9 @@ int lpp_apply_snapshot(float* x, const float* g, float* m, float* replica,
  * gradient, then the apply), with per-BLOCK write stamps: every update
  * writes one whole block range, so an element's tag is the newest stamp of
  * the blocks covering it (block 0 = all, and its partial block).
- *   block_stamps[block_id] is NOT raised here: call lpp_publish_stamp next
- *       on the same stream (after every element reduction is performed)
+ *   block_stamps[block_id] is NOT written here: call lpp_publish_stamp
+ *       after it, ordered on a stream (once every element reduction is
+ *       performed)
  *   cur_claim[0..1] = (k_claim, clean): k_claim = *avg_cell read when the
  *       kernel starts (after this step's gradient), clean = all of this
  *       step's k tags cur_dev[j] >= k_claim              (cur_claim may be NULL)
@@ -243,8 +244,10 @@ int lpp_gather_tags_floor(const int32_t* tags, const int64_t* idx, size_t k,
 int lpp_gather_block_stamps(const int32_t* stamps, const int64_t* bounds, int nb,
                             const int64_t* idx, size_t k, const int64_t* floor_cell,
                             int32_t* out_dev, int32_t* out_host, void* stream);
-/* stamps[block_id] = max(stamps[block_id], stamp), in stream order: launched
- * right after an update's lpp_apply_snapshot_plan on the same stream */
+/* stamps[block_id] = stamp, in stream order after all prior work on the
+ * stream and a system-wide memory barrier (a stream memory operation, no
+ * kernel): issued after an update's lpp_apply_snapshot_plan, ordered after
+ * it.  The last write wins, like the reference's per-element tags. */
 int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream);
 /* *dev = v in stream order (the round-stamp cell the apply kernels read) */
 int lpp_set_i64(int64_t* dev, int64_t v, void* stream);

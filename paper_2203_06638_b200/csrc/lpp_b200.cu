@@ -11,13 +11,13 @@
 //          with a lpp_tag_plan also the updater's K5 bookkeeping in the
 //          reference's order (this step's classification, the next step's
 //          sampled tags before their values), per-block write stamps
-//          published by k_publish_stamp after it (engine.py:343-362)
+//          published by a stream write after it (engine.py:343-362)
 //   K4     k_average              : owner-computes in-place model averaging,
 //          replaces _averager_body + _MeanAllReduce + add_assign(mean - snap)
 //          (engine.py:199-229, 418-421); k_average_bulk: the TMA-staged
 //          variant (bulk loads on an mbarrier, bulk reductions)
 //   K5     tagged variants / k_gather_tags / k_gather_tags_floor /
-//          k_gather_block_stamps / k_classify / k_publish_stamp : write
+//          k_gather_block_stamps / k_classify / lpp_publish_stamp : write
 //          stamps, the sampled-tag gather, the clean classification
 //          (_atomics.c:217-310, 346-392; engine.py:353-362)
 //   K6     host atomics           : _atomics.{load,store,fetch_add}_i64
@@ -464,9 +464,9 @@ static int apply_impl(float* x, const float* g, float* m, size_t n, float lr, co
 //   * write stamps per BLOCK, not per element: every update writes one
 //     whole block range, so an element's tag is the newest stamp of the (at
 //     most two) blocks covering it — block 0 (full) and its partial block.
-//     The stamp is raised by lpp_publish_stamp, the next launch on the same
-//     stream, so it is visible only once every element reduction of its
-//     update is performed (value before tag, _atomics.c:346-392) — at no
+//     The stamp is written by lpp_publish_stamp, a stream memory operation
+//     after the apply, so it is visible only once every element reduction
+//     of its update is performed (value before tag, _atomics.c:346-392) — at no
 //     per-element cost and with no CTA barrier or fence in this kernel
 //     (in situ, among convolution CTAs, a completion counter + fence per
 //     CTA measured 4x the apply's latency: the CTAs run in many small waves);
@@ -883,20 +883,6 @@ extern "C" int lpp_classify(const int32_t* tags, size_t k, const int64_t* claim_
   if (k > (1u << 20)) return set_err(LPP_E_VALUE, "classify: k too large");
   k_classify<<<1, 32, 0, (cudaStream_t)stream>>>(tags, (int)k, claim_cell, out);
   LAUNCH_CHECK("classify");
-  return LPP_OK;
-}
-
-// K5 block stamp of an update, raised after its apply kernel (same stream:
-// every element reduction of that launch is performed before this runs)
-__global__ void k_publish_stamp(int* stamps, int bid, int stamp) {
-  fence_ar_gpu();
-  atomicMax(stamps + bid, stamp);
-}
-
-extern "C" int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream) {
-  if (!stamps || block_id < 0) return set_err(LPP_E_VALUE, "publish_stamp: bad stamps / block");
-  k_publish_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(stamps, block_id, stamp);
-  LAUNCH_CHECK("publish_stamp");
   return LPP_OK;
 }
 
@@ -1794,6 +1780,7 @@ LPP_DRV_FN(cuMemExportToShareableHandle, CUresult,
            (void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long))
 LPP_DRV_FN(cuMemImportFromShareableHandle, CUresult,
            (CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType))
+LPP_DRV_FN(cuStreamWriteValue32, CUresult, (CUstream, CUdeviceptr, cuuint32_t, unsigned int))
 #undef LPP_DRV_FN
 
 template <typename T>
@@ -1830,6 +1817,28 @@ static int init() {
   return ok ? LPP_OK : set_err(LPP_E_CUDA, "CUDA driver entry points unavailable");
 }
 }  // namespace drv
+
+// K5: an update's block stamp, written by the stream's front end once the
+// apply before it on the stream has completed, after a system-wide memory
+// barrier (CU_STREAM_WRITE_VALUE_DEFAULT): every element reduction of the
+// update is visible before the stamp.  The last write wins, as the
+// reference's per-element tags (the CAS that lands last stamps last,
+// _atomics.c:346-392).  A stream memory operation, not a kernel: the step's
+// only launch of ours stays the fused apply.
+extern "C" int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream) {
+  if (!stamps || block_id < 0) return set_err(LPP_E_VALUE, "publish_stamp: bad stamps / block");
+  if (!drv::load(drv::cuStreamWriteValue32, "cuStreamWriteValue32") ||
+      !drv::load(drv::cuGetErrorString, "cuGetErrorString"))
+    return set_err(LPP_E_CUDA, "publish_stamp: cuStreamWriteValue32 unavailable");
+  CUresult r = drv::cuStreamWriteValue32((CUstream)stream, (CUdeviceptr)(stamps + block_id),
+                                         (cuuint32_t)stamp, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) {
+    const char* e = nullptr;
+    drv::cuGetErrorString(r, &e);
+    return set_err(LPP_E_CUDA, "publish_stamp: cuStreamWriteValue32 failed: %s", e ? e : "?");
+  }
+  return LPP_OK;
+}
 
 #define CU_TRY(expr)                                                        \
   do {                                                                      \

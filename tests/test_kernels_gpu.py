@@ -581,7 +581,7 @@ def test_apply_snapshot_plan_values_stamps_classification_and_next_tags(N, orc, 
     N.publish_stamp(stamps.data_ptr(), bid, stamp - 5, 0)
     torch.cuda.synchronize()
     assert list(claim[1]) == [10, 1]
-    assert int(stamps[bid].item()) == max(old[bid], stamp)   # max: an older stamp never lowers it
+    assert int(stamps[bid].item()) == stamp - 5     # the last publication wins (last writer)
     first = torch.zeros(k, dtype=torch.int32, device="cuda")
     N.gather_block_stamps(stamps.data_ptr(), bnd.data_ptr(), nb, idx[1].data_ptr(), k, cell.data_ptr(),
                           first.data_ptr(), None, 0)
