@@ -326,9 +326,12 @@ class _Engine(NativeLoops):
             self.ctrl = RoundControl(cfg.workers)
         else:
             group.reset_control()
+            n_peers = len(group.peers)
             self.arena_ptrs = group.attach_arenas(self.workers[group.rank].store.arena)
             self.tag_ptrs = (group.attach_arenas(self.workers[group.rank].tag_arena)
                              if self.round_tags else None)
+            # this engine's IPC mappings of the peers' arenas (closed with it)
+            self._peer_maps = group.peers[n_peers:]
             self.ctrl = group.control
         self.shards = shard_bounds(self.dim, cfg.workers)
         self.nvls = {}
@@ -1089,6 +1092,14 @@ class _Engine(NativeLoops):
         for nv in self.nvls.values():
             nv.close()
         self.nvls = {}
+        if self.group is not None:
+            # every rank is past its run (run_async ends on a group barrier):
+            # drop this engine's peer mappings before the arenas go
+            for pm in getattr(self, "_peer_maps", []):
+                pm.close()
+                if pm in self.group.peers:
+                    self.group.peers.remove(pm)
+            self._peer_maps = []
         for w in self.workers.values():
             w.close()
         self.errors = []
