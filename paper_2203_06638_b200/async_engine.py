@@ -127,7 +127,6 @@ class _Worker:
         depth = cfg.in_flight + 2
         self.tag_pick = min(cfg.tag_sample, d)
         k = max(self.tag_pick, 1)
-        self.kk = k
         # the worker's round-stamp cell on the device: the stamp of the last
         # round applied to this arena, written by the averager (lpp_set_i64)
         # before the host cell last_avg_stamp moves; the apply kernels read it
@@ -174,7 +173,6 @@ class _Worker:
                                              device=self.dev)
             self.block_bounds_host = np.ascontiguousarray(cfg.partition.boundaries, dtype=np.int64)
             self.min_dev = torch.zeros((U, depth), dtype=torch.int32, device=self.dev)
-            self.min_pinned = torch.zeros((U, depth), dtype=torch.int32, pin_memory=True)
         # full record mode keeps every update's whole tag snapshot (reference
         # full mode, engine.py:343-344); one buffer per in-flight slot
         self.snap_tags = None
@@ -253,7 +251,6 @@ class _Worker:
             # writes/reads skip the framework's dispatch
             self.idx_np = self.idx_pinned.numpy()
             if cfg.tracks:
-                self.min_np = self.min_pinned.numpy()
             # the warm-up passes touched the replica/grad arenas and BN stats
             # only; re-snapshot so every replica starts at x0
             for r in range(cfg.updaters):
@@ -437,7 +434,6 @@ class _Engine(NativeLoops):
                     out_tags = w.snap_tags[r][slot].data_ptr()
                 N.snapshot_tagged(w.store.arena.ptr, w.tag_arena.ptr, w.replicas[r].ptr, out_tags,
                                   self.dim, w.min_dev[r, slot].data_ptr(), sp)
-                w.min_pinned[r, slot].copy_(w.min_dev[r, slot], non_blocking=True)
             else:
                 # K5: sampled tags are gathered BEFORE the value copy (paramstore.py:108-112)
                 self.gather_tags(w, r, slot, tag_idx)
