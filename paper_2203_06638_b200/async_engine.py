@@ -250,7 +250,6 @@ class _Worker:
             # numpy views of the pinned staging rings: the per-step host
             # writes/reads skip the framework's dispatch
             self.idx_np = self.idx_pinned.numpy()
-            if cfg.tracks:
             # the warm-up passes touched the replica/grad arenas and BN stats
             # only; re-snapshot so every replica starts at x0
             for r in range(cfg.updaters):
