@@ -520,9 +520,9 @@ class _Engine(NativeLoops):
 
     def gather_tags(self, w: _Worker, r: int, slot: int, tag_idx) -> None:
         """K5: the step's sampled tags, raised to the round floor, into slot
-        (device ring + host-mapped copy); on the updater stream before the
+        (the step's device record); on the updater stream before the
         snapshot values it describes (paramstore.py:108-112).  The indices are
-        written into host-mapped memory and read there by the kernel."""
+        copied to a device ring first, in stream order."""
         k = w.tag_pick
         sp = w.streams[r].cuda_stream
         idx_dev = w.stage_idx(r, slot, tag_idx, sp)

@@ -312,8 +312,9 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
   uint64_t tag_state = c->tag_seed;
   *st = lpp_updater_stats{};
 
-  // a step's sampled tags live in slot t % depth (indices in host-mapped
-  // memory, read there by the kernels).  Unfused steps (and the first fused
+  // a step's sampled tags live in slot t % depth (indices drawn into the
+  // pinned ring; unfused gathers read them from the device ring, the fused
+  // apply takes them by value).  Unfused steps (and the first fused
   // one) gather them before their snapshot values are read
   // (paramstore.py:108-112); fused steps get them from the previous step's
   // apply kernel, after that apply landed (engine.py:343-362 order)
