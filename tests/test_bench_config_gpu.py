@@ -254,3 +254,28 @@ def test_more_than_32_sampled_tags_take_the_unfused_path():
     assert all(u.clean == bool((u.tags >= u.k_claim).all()) for u in res.updates)
     tr2 = _oracle(orc, cfg, bounds)
     np.testing.assert_allclose(res.final_values, tr2.final_values, atol=1e-5, rtol=1e-4)
+
+
+def test_repeated_phases_reset_k5_state_and_keep_parity():
+    """Trainer phases (bench: warm-up, then the timed phase) on the same
+    arenas: every phase restarts counters, the round cell and the block
+    stamps; the records of the second phase satisfy the classification rule
+    and its stamps start from 1 again."""
+    from paper_2203_06638_b200.engine import Trainer
+
+    obj, orc, bounds = _c0()
+    cfg = _cfg(obj, bounds, budget=200, B=32, record_mode="light")
+    tr = Trainer(cfg)
+    try:
+        r1 = tr.run(30)
+        w = tr.eng.workers[0]
+        assert int(w.block_stamps.max().item()) > 0
+        r2 = tr.run(30)
+        us = sorted(u.u for u in r2.updates)
+        assert us[0] == 1 or min(st.u for st in r2.stamps) == 1     # stamps restart each phase
+        assert r2.counter_finals == [31]
+        assert all(u.clean == bool((u.tags >= u.k_claim).all()) for u in r2.updates)
+        assert int(w.block_stamps.max().item()) <= max(us)          # no stamp from phase 1 left
+    finally:
+        tr.close()
+    assert r1.counter_finals == [31]
