@@ -324,11 +324,14 @@ def ours(args) -> None:
                    "momentum": 0.9, "weight_decay": 5e-4,
                    "write_tags": facts["tracks"], "averaging_rounds": rounds},
         "gpu_launches": launches,
-        "gpu_launches_note": "lpp_b200 kernels launched in the timed region on this rank "
-                             "(fused K1+K3 apply + K5 tag gather + in-graph sampler per minibatch, "
-                             "+ K4 per round)",
+        "gpu_launches_note": "lpp_b200 kernels launched through the C ABI in the timed region on "
+                             "this rank: the fused K1+K3+K5 apply per minibatch (its block-stamp "
+                             "publication is a stream write, its record a memcpy), the round-stamp "
+                             "cell write (and K4 for Q > 1) per averaging round; the in-graph "
+                             "sampler runs inside the captured step graph",
         "roofline": {"bound": "hbm",
-                     "kernel": ("lpp_apply_snapshot (K1+K3 fused, red.add.v4.f32 + re-read)" if fused else
+                     "kernel": ("lpp_apply_snapshot_plan (K1+K3 fused + K5 plan, red.add.v4.f32 + "
+                                "re-read)" if fused else
                                 "lpp_apply_sgd (K1/K2, red.global.add.v4.f32)"),
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "peak_src": peaks["src"],
