@@ -1827,9 +1827,10 @@ static int init() {
 // only launch of ours stays the fused apply.
 extern "C" int lpp_publish_stamp(int32_t* stamps, int block_id, int32_t stamp, void* stream) {
   if (!stamps || block_id < 0) return set_err(LPP_E_VALUE, "publish_stamp: bad stamps / block");
-  if (!drv::load(drv::cuStreamWriteValue32, "cuStreamWriteValue32") ||
-      !drv::load(drv::cuGetErrorString, "cuGetErrorString"))
-    return set_err(LPP_E_CUDA, "publish_stamp: cuStreamWriteValue32 unavailable");
+  // resolved once, thread-safely (function-local static initialisation)
+  static const bool have = drv::load(drv::cuStreamWriteValue32, "cuStreamWriteValue32") &&
+                           drv::load(drv::cuGetErrorString, "cuGetErrorString");
+  if (!have) return set_err(LPP_E_CUDA, "publish_stamp: cuStreamWriteValue32 unavailable");
   CUresult r = drv::cuStreamWriteValue32((CUstream)stream, (CUdeviceptr)(stamps + block_id),
                                          (cuuint32_t)stamp, CU_STREAM_WRITE_VALUE_DEFAULT);
   if (r != CUDA_SUCCESS) {
