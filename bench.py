@@ -298,9 +298,10 @@ def ours(args) -> None:
         tp = ROOT / "profiles" / "r1_kernel_traffic.json"
     if tp.exists():
         launches_ = json.loads(tp.read_text())["launches"]
-        name = "void k_apply_snapshot<" if fused else "void k_apply<1, 1, 1>"
-        grid20 = min(-(-(dim20 // 4) // 256), 148 * 16)     # the launch's grid at d20
-        cands = [e for e in launches_ if e["kernel"].startswith(name) and e["grid"] == grid20]
+        # the plan variant (momentum + wd, K5 plan) at the d20 size: the
+        # capture's small-grid launches (the d50 ones run the full grid)
+        name = "void k_apply_snapshot<1, 1, 0, 1" if fused else "void k_apply<1, 1, 1>"
+        cands = [e for e in launches_ if e["kernel"].startswith(name) and e["grid"] < 148 * 16]
         traffic = sum(e["dram_bytes"] for e in cands) / len(cands) if cands else None
         floor = [e["us"] for e in launches_ if e["kernel"].startswith(("k_gather", "void k_gather"))]
         if cands:

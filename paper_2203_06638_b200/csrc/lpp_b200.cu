@@ -725,13 +725,6 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     pd.k = plan->k;
   }
   size_t nvec = n / 4;
-  unsigned grid = grid_for(nvec ? nvec : 1, current_sms());
-  // experiment hook: LPP_FUSED_CTAS caps the grid (tools/exp_insitu_grid.py)
-  static const long cap_env = [] {
-    const char* e = std::getenv("LPP_FUSED_CTAS");
-    return e ? std::atol(e) : 0L;
-  }();
-  if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
   // vectors per thread per round of the plan kernel: 2 (LPP_FUSED_UNR
   // overrides: 1, 2, 4).  In situ (bf16 ResNet-18 / ResNet-50 steps,
   // tools/exp_fused_insitu.py) 2 reaches 0.72 / 0.79-0.81 of HBM vs 0.70 /
@@ -742,6 +735,17 @@ static int apply_snapshot_launch(float* x, const float* g, float* m, float* repl
     const int v = e ? std::atoi(e) : 2;
     return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
+  // grid: one round of `unr` vectors per thread (the plain kernels: one vector);
+  // at d20 the plan launch then needs 134 CTAs instead of 267 — fewer SM slots
+  // to wait for among the convolutions' CTAs
+  const size_t per_thread = plan ? (size_t)unr : 1;
+  unsigned grid = grid_for(nvec ? (nvec + per_thread - 1) / per_thread : 1, current_sms());
+  // experiment hook: LPP_FUSED_CTAS caps the grid (tools/exp_insitu_grid.py)
+  static const long cap_env = [] {
+    const char* e = std::getenv("LPP_FUSED_CTAS");
+    return e ? std::atol(e) : 0L;
+  }();
+  if (cap_env > 0 && grid > (unsigned)cap_env) grid = (unsigned)cap_env;
   if (plan && pd.has_next) {  // owning thread of each sampled element, sorted
     const size_t stride = (size_t)grid * kThreads;
     for (int j = 0; j < pd.k; ++j) {
