@@ -19,7 +19,7 @@ for arch, B, K, n in (("resnet18", 128, 40, 8192), ("resnet50", 32, 30, 2048)):
     for rep in range(3):
         res = tr.run(K * 4, evaluate=False)
         nn_, ms, by = res.apply_timing
-        print(json.dumps({"variant": tag or os.environ.get("LPP_FUSED_UNR", "1"), "arch": arch, "rep": rep,
+        print(json.dumps({"variant": tag or os.environ.get("LPP_FUSED_UNR", "2 (default)"), "arch": arch, "rep": rep,
                           "img_per_s": round(sum(res.counter_finals) * B / (res.device_ms / 1e3)),
                           "apply_avg_us": round(1e3 * ms / nn_, 1), "frac": round(by / (ms / 1e3) / 1e9 / 6560.6, 3)}),
               flush=True)
