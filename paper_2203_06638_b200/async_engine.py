@@ -545,7 +545,8 @@ class _Engine(NativeLoops):
                    next_slot: int, u: int, first: bool, tag_idx, next_tag_idx,
                    buf: int = 0) -> None:
         """One async step with K1+K3 fused: [first: gather + K3] -> graph ->
-        gather(next) -> apply(this) fused with snapshot(next)."""
+        apply(this) fused with snapshot(next) and the K5 plan (classify this
+        step, read the next step's sampled tags) -> block stamp + record."""
         cfg = self.cfg
         stream = w.streams[r]
         prog = w.programs[r]
@@ -572,8 +573,9 @@ class _Engine(NativeLoops):
             plan = None
             if tracks:
                 # K5 inside the apply: classify this step (k_claim read after
-                # its gradient), stamp, and gather the next step's tags after
-                # this apply landed (engine.py:343-362 order)
+                # its gradient) and read the next step's sampled tags before
+                # their values, after this apply's own reductions
+                # (engine.py:343-362 order)
                 k = w.tag_pick
                 plan = N.TagPlan(w.tag_idx_pinned[r, next_slot].data_ptr(), w.rec_tags(r, next_slot),
                                  None, w.rec_tags(r, slot),

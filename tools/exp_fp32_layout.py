@@ -13,7 +13,9 @@ from paper_2203_06638_b200.objectives import ResNetObjective  # noqa: E402
 torch.backends.cudnn.benchmark = True
 torch.backends.cudnn.allow_tf32 = False
 torch.backends.cuda.matmul.allow_tf32 = False
-limits = [int(a) for a in sys.argv[1:]] or [10]
+bench_mode = "--no-benchmark" not in sys.argv
+torch.backends.cudnn.benchmark = bench_mode
+limits = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [10]
 for tf32, cl, lim in [(False, True, l) for l in limits] + ([(False, False, 10), (True, True, 10)] if len(sys.argv) == 1 else []):
     torch.backends.cudnn.allow_tf32 = tf32
     torch.backends.cudnn.benchmark_limit = lim
@@ -48,4 +50,5 @@ for tf32, cl, lim in [(False, True, l) for l in limits] + ([(False, False, 10), 
             g.replay()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        print(f"tf32={tf32} channels_last={cl} benchmark_limit={lim}: {n * 512 / dt:,.0f} images/s")
+        print(f"tf32={tf32} channels_last={cl} benchmark={bench_mode} limit={lim}: "
+              f"{n * 512 / dt:,.0f} images/s")
