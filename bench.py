@@ -288,6 +288,11 @@ def ours(args) -> None:
     k4_rounds, k4_ms = getattr(res, "k4_timing", (0, 0.0))
     achieved = app_bytes / (app_ms / 1e3) / 1e9
     rounds = max((st.round for st in res.stamps), default=0)
+    # the per-launch distribution (the native loop's log): the mean above is
+    # the contract's number; the median shows the tail's weight
+    samples = sorted(1e3 * v for v in getattr(res, "apply_ms_samples", []))
+    in_situ_pct = ([round(samples[min(len(samples) - 1, int(q * len(samples)))], 2)
+                    for q in (0.10, 0.50, 0.90, 0.99)] if samples else None)
 
     # traffic: DRAM bytes per launch of the same kernel at the ResNet-20 arena
     # size from the committed ncu --set full capture (profiles/)
@@ -339,6 +344,7 @@ def ours(args) -> None:
                      "traffic": traffic,
                      "traffic_src": "ncu --set full, d20, cold L2 (profiles/)",
                      "launches": n_app, "avg_us": 1e3 * app_ms / max(n_app, 1),
+                     "in_situ_us_p10_50_90_99": in_situ_pct,
                      "bytes_per_launch": app_bytes / max(n_app, 1),
                      "standalone": standalone,
                      "note": "d20 arena (1.09 MB) is L2-resident: latency-bound; see kernel_sweep, "
