@@ -205,10 +205,14 @@ class _Worker:
                      8 * self.rec_cols, stream_ptr)
 
     def publish_round(self, u: int, stream: torch.cuda.Stream) -> None:
-        """The round with stamp u is applied to this arena: (device mirror
-        first,) then the host cell the kernels read as k_claim / tag floor."""
+        """The round with stamp u is applied to this arena: the device cell
+        the kernels read as k_claim / tag floor (enqueued on the averager's
+        stream) and the host cell."""
         if self.round_cell is not None:
             N.set_i64(self.avg_dev, u, stream.cuda_stream)
+            # the Python averager serves the serialized / quiescent / record
+            # modes, where the next steps must see the new stamp: wait (the
+            # native averager, the throughput path, does not)
             stream.synchronize()
         self.last_avg_stamp.store(u)
 

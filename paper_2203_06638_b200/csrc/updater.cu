@@ -694,14 +694,10 @@ extern "C" int lpp_averager_run(const lpp_averager_cfg* c, int64_t* rounds_out) 
       }
       if (ok && c->round_cell) {
         // the device round-stamp cell the updaters' apply kernels read as
-        // k_claim and tag floor, before the host cell moves
+        // k_claim and tag floor (stream-ordered; no wait: the host cell
+        // below serves host readers, the kernels read the device one)
         int rc2 = lpp_set_i64(c->round_cell, u, stream);
         if (rc2 != LPP_OK) return fail(rc2);
-        cudaError_t e2 = cudaStreamSynchronize(stream);
-        if (e2 != cudaSuccess) {
-          fail(LPP_E_CUDA);
-          return set_err(LPP_E_CUDA, "averager: stream sync failed: %s", cudaGetErrorString(e2));
-        }
       }
       if (ok) {
         st(c->last_avg_stamp, u);
