@@ -180,6 +180,7 @@ def reference_arm(args) -> None:
                    "batch_per_updater": B, "updaters_per_gpu": U, "workers": 1, "blocks": U,
                    "parallelism": f"lpp_sgd_q1_u{U}", "device": "host CPU (reference arm)"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": r["cores"], "kind": "port",
+                         "cpu_count": os.cpu_count(),
                          "sample": f"{r['minibatches']} minibatches x {B} images, one minibatch per "
                                    f"reference-arm step (LPP-SGD, U={U}, "
                                    f"threaded port of engine.py:289-523 incl. the averager and "
@@ -713,7 +714,7 @@ def ours(args) -> None:
             run_lpp_cpu(slots=U, updaters=U, batch_size=B)
             r = run_lpp_cpu(slots=25 * U, updaters=U, batch_size=B)
             line["cpu_baseline"] = {"value": r["images"] / r["seconds"], "unit": "images/s",
-                                    "cores": r["cores"], "kind": "port",
+                                    "cores": r["cores"], "kind": "port", "cpu_count": os.cpu_count(),
                                     "sample": f"{r['minibatches']} minibatches x {B} images, LPP-SGD U={U} "
                                               f"(port of engine.py:289-523 incl. averager + tags), "
                                               f"torch-CPU ResNet-20 grads, store ops via the "
