@@ -772,3 +772,59 @@ def test_fused_and_unfused_k5_classify_alike(N, round_lands):
     for a in (x, g, rep, tags):
         a.close()
     del bnd_dev
+
+
+def test_apply_snapshot_plan_randomized(N, orc):
+    """Random sizes (tails 0-3), blocks (straddling vector boundaries),
+    sampled indices (incl. the tail and block edges), stamps and floors:
+    values bit-exact with the oracle apply, replica = arena, next-step tags
+    = max(floor, stamp[0], stamp[b(e)], own stamp inside the block),
+    classification = (all current tags >= the cell)."""
+    from paper_2203_06638_b200.arena import Arena
+
+    gen = np.random.default_rng(2026)
+    for case in range(12):
+        n = int(gen.integers(5, 300_000))
+        nb = int(gen.integers(1, 6))
+        cuts = np.sort(gen.choice(np.arange(1, n), size=nb - 1, replace=False)) if nb > 1 else np.array([], int)
+        bounds = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+        bid = int(gen.integers(0, nb + 1))
+        lo, hi = (0, n) if bid == 0 else (int(bounds[bid - 1]), int(bounds[bid]))
+        k = int(gen.integers(1, 33))
+        idx = gen.choice(n, size=k, replace=k > n)
+        idx[0] = n - 1
+        idx[-1] = lo if bid else 0
+        idx = np.ascontiguousarray(np.sort(idx), dtype=np.int64)
+        x = gen.normal(size=n).astype(np.float32)
+        g = (1e-2 * gen.normal(size=n)).astype(np.float32)
+        m = gen.normal(size=n).astype(np.float32)
+        mu, wd = (0.9, 5e-4) if case % 2 else (0.0, 0.0)
+        ax, ag, am, ar = (Arena(n, 0) for _ in range(4))
+        ax.tensor.copy_(_cuda(x)), ag.tensor.copy_(_cuda(g)), am.tensor.copy_(_cuda(m))
+        stamps_h = gen.integers(1, 50, size=nb + 1).astype(np.int32)
+        stamps = _cuda(stamps_h)
+        floor = int(gen.integers(0, 60))
+        cell = torch.tensor([floor], dtype=torch.long, device="cuda")
+        cur = _cuda(gen.integers(0, 80, size=k).astype(np.int32))
+        nxt = torch.zeros(k, dtype=torch.int32, device="cuda")
+        claim = torch.zeros(2, dtype=torch.long, device="cuda")
+        stamp = 100 + case
+        plan = N.TagPlan(idx.ctypes.data, nxt.data_ptr(), None, cur.data_ptr(), claim.data_ptr(),
+                         cell.data_ptr(), stamps.data_ptr(), bounds.ctypes.data, nb, bid, k)
+        N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr if mu else None, ar.ptr, None, n, lo, hi, 0.05,
+                              None, mu, wd, stamp, plan, 0)
+        torch.cuda.synchronize()
+        xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
+        orc.apply_sgd(xv, g[lo:hi].copy(), mv if mu else None, 0.05, mu, wd)
+        want = x.copy()
+        want[lo:hi] = xv
+        got = ax.tensor.cpu().numpy()
+        assert np.array_equal(got, want), case
+        assert np.array_equal(ar.tensor.cpu().numpy(), want), case
+        b_of = np.searchsorted(bounds[1:-1], idx, side="right") + 1
+        t = np.maximum(np.maximum(stamps_h[0], stamps_h[b_of]), floor)
+        t = np.where((idx >= lo) & (idx < hi), np.maximum(t, stamp), t)
+        assert np.array_equal(nxt.cpu().numpy(), t), case
+        assert claim.cpu().tolist() == [floor, int((cur.cpu().numpy() >= floor).all())], case
+        for a in (ax, ag, am, ar):
+            a.close()
