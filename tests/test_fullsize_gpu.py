@@ -138,3 +138,45 @@ def test_snapshot_and_sampler_at_sweep_size(N):
         N.sample_indices(idx.data_ptr(), step.data_ptr(), b, n, 99, 0)
         torch.cuda.synchronize()
         assert np.array_equal(idx.cpu().numpy(), N.sample_indices_host(b, n, 99, 12345))
+
+
+@pytest.mark.parametrize("d", [D20, D18, D50])
+def test_fused_apply_with_k5_plan_at_full_size(N, orc, d):
+    """The async default at the C1 / C2 / C3 arena sizes (full grid, two
+    vectors per thread per round): values bit-exact with the oracle, the
+    replica equal to the arena, 32 sampled next-step tags (spread over the
+    arena, incl. the tail) by the block-stamp rule, the classification."""
+    x, g, m = _inputs(d, 9)
+    ax, ag, am = _arena(x), _arena(g), _arena(m)
+    rep = _arena(np.full(d, -3.0, np.float32))
+    bounds = np.array([0, d // 4, d // 2 + 1, 3 * d // 4, d], dtype=np.int64)
+    bid, lo, hi = 2, d // 4, d // 2 + 1
+    gen = np.random.default_rng(d)
+    idx = np.sort(gen.choice(d, size=32, replace=False)).astype(np.int64)
+    idx[-1] = d - 1
+    idx = np.unique(idx)
+    k = len(idx)
+    stamps_h = np.array([11, 5, 30, 7, 9], dtype=np.int32)
+    stamps = torch.from_numpy(stamps_h).cuda()
+    cell = torch.tensor([8], dtype=torch.long, device="cuda")
+    cur = torch.full((k,), 8, dtype=torch.int32, device="cuda")
+    nxt = torch.zeros(k, dtype=torch.int32, device="cuda")
+    claim = torch.zeros(2, dtype=torch.long, device="cuda")
+    plan = N.TagPlan(idx.ctypes.data, nxt.data_ptr(), None, cur.data_ptr(), claim.data_ptr(),
+                     cell.data_ptr(), stamps.data_ptr(), bounds.ctypes.data, 4, bid, k)
+    N.apply_snapshot_plan(ax.ptr, ag.ptr, am.ptr, rep.ptr, None, d, lo, hi, 0.05, None, 0.9, 5e-4, 77,
+                          plan, 0)
+    torch.cuda.synchronize()
+    xv, mv = x[lo:hi].copy(), m[lo:hi].copy()
+    orc.apply_sgd(xv, g[lo:hi].copy(), mv, 0.05, 0.9, 5e-4)
+    want = x.copy()
+    want[lo:hi] = xv
+    assert np.array_equal(ax.tensor.cpu().numpy(), want)
+    assert np.array_equal(rep.tensor.cpu().numpy(), want)
+    b_of = np.searchsorted(bounds[1:-1], idx, side="right") + 1
+    t = np.maximum(np.maximum(stamps_h[0], stamps_h[b_of]), 8)
+    t = np.where((idx >= lo) & (idx < hi), np.maximum(t, 77), t)
+    assert np.array_equal(nxt.cpu().numpy(), t)
+    assert claim.cpu().tolist() == [8, 1]
+    for a in (ax, ag, am, rep):
+        a.close()
