@@ -368,8 +368,17 @@ def ours(args) -> None:
     # ---------------- the same two measurements with bf16 convolutions ----------------
     if not args.no_bf16:
         with _Optional(line, "bf16"):
-            vb, _, fb, _, _ = lpp_phase("bf16")
+            vb, rb, fb, _, _ = lpp_phase("bf16", time_apply=True)
             line["value_bf16"] = vb
+            # the same apply kernel timed inside the bf16 step (shorter
+            # convolution CTAs: fewer waves to wait through) — round 1's
+            # headline condition
+            nb_, msb_, byb_ = rb.apply_timing
+            if nb_:
+                ab_ = byb_ / (msb_ / 1e3) / 1e9
+                line["roofline"]["in_situ_bf16_step"] = {
+                    "avg_us": 1e3 * msb_ / nb_, "achieved": ab_, "frac": ab_ / peaks["hbm_gbs"],
+                    "launches": nb_}
             line["bf16"] = {"conv_compute": "bf16 shadow weights (one cast per step from the fp32 "
                                             "replica), dataset stored NHWC bf16; arena, grads, apply, "
                                             "averaging fp32", "clocks": fb["clocks"]}
