@@ -234,6 +234,7 @@ def ours(args) -> None:
     from paper_2203_06638_b200.engine import Trainer
     from paper_2203_06638_b200.objectives import ResNetObjective
     from paper_2203_06638_b200.schedules import SyncScheme
+    from paper_2203_06638_b200.step import graph_kernel_count
 
     peaks = _peaks()
     K, W = args.steps, args.warmup
@@ -270,17 +271,19 @@ def ours(args) -> None:
             t.eng.nvtx = "lpp_timed"   # ncu --nvtx --nvtx-include lpp_timed/ profiles this phase only
         with Clocks(dev) as clk:
             barrier()
-            l0 = N.launch_count()
+            l0, g0 = N.launch_count(), graph_kernel_count()
             r = t.run(K * U, evaluate=False)
             n_l = N.launch_count() - l0
+            n_g = graph_kernel_count() - g0
             barrier()
+        facts["launches_c_abi"], facts["launches_in_graph"] = n_l, n_g
         t.eng.nvtx = None
         ms = max_over_ranks(r.device_ms)
         v = sum(r.counter_finals) * B * ws / (ms / 1e3)   # claim-then-process: K*U + U per rank
         facts["clocks"] = clk.summary()
         t.close()
         del t
-        return v, r, facts, n_l, ms
+        return v, r, facts, n_l + n_g, ms
 
     # ---------------- device-resident throughput (value), fp32 ----------------
     value, res, facts, launches, dev_ms = lpp_phase(None, time_apply=True)
@@ -326,16 +329,23 @@ def ours(args) -> None:
                    "parallelism": f"lpp_sgd_q{ws}_u{U}", "params": dim20,
                    "conv_compute": "fp32 (TF32 off), the reference arm's precision; arena, grads, "
                                    "apply and averaging fp32",
+                   "conv_kernels": ("lpp_conv3x3_f32 / lpp_conv3x3_wgrad_f32 (FFMA, NHWC) for the 16 "
+                                    "3x3 stride-1 C->C convolutions; cuDNN for the stem, stride-2 and "
+                                    "1x1 ones" if os.environ.get("LPP_CONV", "native") != "cudnn"
+                                    else "cuDNN (LPP_CONV=cudnn)"),
                    "l2": "inputs larger than L2 (50,000-image dataset, 614 MB fp32, gathered per step)",
                    "sampling": "in-graph device RNG", "host_loop": "native" if tr_native else "python",
                    "momentum": 0.9, "weight_decay": 5e-4,
                    "write_tags": facts["tracks"], "averaging_rounds": rounds},
         "gpu_launches": launches,
-        "gpu_launches_note": "lpp_b200 kernels launched through the C ABI in the timed region on "
-                             "this rank: the fused K1+K3+K5 apply per minibatch (its block-stamp "
-                             "publication is a stream write, its record a memcpy), the round-stamp "
-                             "cell write (and K4 for Q > 1) per averaging round; the in-graph "
-                             "sampler runs inside the captured step graph",
+        "gpu_launches_note": "lpp_b200 kernels in the timed region on this rank: launched through "
+                             "the C ABI (the fused K1+K3+K5 apply per minibatch — its block-stamp "
+                             "publication is a stream write, its record a memcpy — the round-stamp "
+                             "cell write, and K4 for Q > 1, per averaging round) plus those inside "
+                             "the replayed step graphs (the device sampler and the fp32 3x3 "
+                             "convolutions: forward, dgrad, wgrad + its reduction), counted per "
+                             "graph at capture and summed per replay",
+        "gpu_launches_split": {"c_abi": facts["launches_c_abi"], "in_graph": facts["launches_in_graph"]},
         "roofline": {"bound": "hbm",
                      "kernel": ("lpp_apply_snapshot_plan (K1+K3 fused + K5 plan, red.add.v4.f32 + "
                                 "re-read)" if fused else

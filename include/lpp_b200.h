@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define LPP_ABI_VERSION 3
+#define LPP_ABI_VERSION 4
 
 /* error codes */
 #define LPP_OK 0
@@ -494,6 +494,10 @@ typedef struct {
   /* time_apply: each timed apply's CUDA-event ms, in step order (NULL: sum only) */
   float* apply_ms_log;
   int64_t apply_ms_cap;
+  /* per block id: kernels of this library inside the step graph
+   * (csrc/conv_f32.cu's convolutions), summed into stats->graph_kernels per
+   * launch (NULL: not counted) */
+  const int64_t* graph_kernels_of;
 } lpp_updater_cfg;
 
 typedef struct {
@@ -502,6 +506,7 @@ typedef struct {
   int64_t apply_launches;         /* timed applies (time_apply) */
   double apply_ms;                /* summed CUDA-event time of the applies */
   double apply_bytes;             /* summed algorithmic bytes of the applies */
+  int64_t graph_kernels;          /* sum of graph_kernels_of over the steps */
 } lpp_updater_stats;
 
 int lpp_updater_run(const lpp_updater_cfg* cfg, lpp_updater_stats* stats);
@@ -580,6 +585,25 @@ int lpp_averager_run(const lpp_averager_cfg* cfg, int64_t* rounds_out);
 
 /* p[i] = v for i in [0, n) (int32, stream-ordered) */
 int lpp_fill_i32(int32_t* p, size_t n, int32_t v, void* stream);
+
+/* ---- fp32 3x3 / stride-1 / pad-1 C->C convolutions (csrc/conv_f32.cu) ----
+ * The gradient step of SURVEY §8 a6 on the GPU: the CNN forward/backward.
+ * Replaces, for CIFAR ResNet-20's 3x3 stride-1 C->C convolutions in fp32
+ * (TF32 off), the cuDNN calls torch's F.conv2d / convolution_backward make
+ * (the reference computes these in fp64 numpy/torch-CPU on its objectives'
+ * grad_block, objectives.py:33-63).  Activations NHWC [n][hw][hw][c]
+ * (torch channels_last), weights and their gradient OHWI [c][3][3][c] (the
+ * arena's channels_last view).  Shapes with a kernel: (c, hw) in
+ * {(16, 32), (32, 16), (64, 8)}. */
+int lpp_conv3x3_supported(int c, int hw);
+/* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x */
+int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
+                    void* stream);
+/* bytes of workspace lpp_conv3x3_wgrad_f32 needs (per-tile partial sums) */
+size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
+/* dw = sum over pixels of x (*) dy, deterministic (fixed-order reduction) */
+int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
+                          int n, int c, int hw, void* stream);
 
 #ifdef __cplusplus
 }

@@ -78,7 +78,7 @@ class UpdaterCfg(ctypes.Structure):
         ("epoch_seed", _c.c_int64), ("idx_pinned", _vp), ("idx_dev", _vp),
         ("rec_dev", _vp), ("rec_pinned", _vp), ("rec_cols", _c.c_int32), ("avg_cell_dev", _vp),
         ("block_stamps", _vp), ("block_bounds_dev", _vp), ("apply_ms_log", _vp),
-        ("apply_ms_cap", _c.c_int64),
+        ("apply_ms_cap", _c.c_int64), ("graph_kernels_of", _vp),
     ]
 
 
@@ -114,7 +114,8 @@ class UpdaterStats(ctypes.Structure):
     """``lpp_updater_stats``."""
 
     _fields_ = [("steps", _c.c_int64), ("flops", _c.c_int64), ("apply_launches", _c.c_int64),
-                ("apply_ms", _c.c_double), ("apply_bytes", _c.c_double)]
+                ("apply_ms", _c.c_double), ("apply_bytes", _c.c_double),
+                ("graph_kernels", _c.c_int64)]
 
 
 _SIGS = {
@@ -216,6 +217,10 @@ _SIGS = {
     "lpp_nprng_permutation": (_c.c_int, [_vp, _c.c_int64, _vp]),
     "lpp_averager_run": (_c.c_int, [_c.POINTER(AveragerCfg), _c.POINTER(_c.c_int64)]),
     "lpp_fill_i32": (_c.c_int, [_vp, _size, _c.c_int32, _vp]),
+    "lpp_conv3x3_supported": (_c.c_int, [_c.c_int, _c.c_int]),
+    "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp]),
+    "lpp_conv3x3_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
+    "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _c.c_int, _c.c_int, _c.c_int, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -15,7 +15,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRCS = [PKG / "csrc" / "lpp_b200.cu", PKG / "csrc" / "updater.cu", PKG / "csrc" / "nprng.cu"]
+SRCS = [PKG / "csrc" / "lpp_b200.cu", PKG / "csrc" / "updater.cu", PKG / "csrc" / "nprng.cu",
+        PKG / "csrc" / "conv_f32.cu"]
 OUT = PKG / "lib" / "liblpp_b200.so"
 
 NVCC_FLAGS = [

@@ -1,0 +1,446 @@
+// conv_f32.cu — fp32 3x3 stride-1 pad-1 C->C convolutions over NHWC
+// activations, the 16 of CIFAR ResNet-20's 19 convolutions that dominate the
+// fp32 step (the gradient of the mean batch loss; on the GPU
+// the CNN forward/backward).  cuDNN runs these at 6-16 TFLOP/s on B200 with
+// TF32 off (profiles/r2_conv_cudnn_f32.txt); this is plain FFMA arithmetic in
+// fp32 (no TF32, no split-precision tricks), so results agree with cuDNN's
+// fp32 algorithms to summation order.
+//
+// Forward and data-gradient share one kernel: dgrad of a 3x3 / pad-1 /
+// stride-1 convolution is the same convolution of dY with the weights
+// flipped in both taps and transposed in (ci, co); the weight tile is
+// re-laid out while it is staged into shared memory.
+//
+//   k_conv3x3: a CTA owns TH output rows (of one image, or TH/H whole images)
+//   x COT output channels.  The input rows it needs (+1 halo row each side,
+//   zero columns either side) are staged once into shared memory with a
+//   pixel stride of C+4 floats (bank-conflict-free float4 reads along x);
+//   the weight slice [tap][ci][co] (co contiguous) beside them.  A thread
+//   holds PX vertically adjacent pixels x CO channels of accumulators; per
+//   (tap column s, 4 input channels) it loads the PX+2 input float4s its
+//   three tap rows share, and per tap row the 4 x CO weights (a warp-wide
+//   broadcast: every lane of a warp owns the same CO channels), then does
+//   3 x 4 x PX x CO FFMAs — 8 FFMAs per shared-memory wavefront at PX=4,
+//   CO=8, enough to keep the FFMA pipes the limit.
+//
+//   k_wgrad3x3: dW[co][r][s][ci] = sum_p dY[p][co] X[p + (r-1, s-1)][ci], a
+//   (C x 9C) product with a reduction over all B*H*W pixels.  A CTA takes a
+//   pixel tile (same tiling as the forward) and a COT channel slice; a
+//   thread owns one tap row r, 4 ci and 4 co for all three tap columns (48
+//   accumulators) and walks the tile's rows with a sliding window of three
+//   input float4s along x: 2 shared loads per 48 FFMAs.  Each CTA writes its
+//   partial dW into a workspace; k_wgrad_reduce sums the partials in a fixed
+//   order (deterministic) straight into the OHWI weight-gradient layout.
+//
+// Layouts: x, y, dy: [N][H][W][C] fp32 (torch channels_last); weights and
+// their gradient: [Cout][3][3][Cin] (OHWI, the arena's channels_last view,
+// objectives.py _view).
+
+#include "common.cuh"
+
+#include <cstdint>
+
+namespace {
+
+constexpr int kPad = 4;  // floats of padding per staged pixel
+
+// 16-byte global -> shared copy that does not hold a register or stall the
+// issuing thread (LDGSTS); pred == false zero-fills the destination
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// stage NIMG x SROWS x SCOLS pixels of C channels (image rows y0-1 ..,
+// columns -1 .. W; zero outside the image) at pixel stride CP
+template <int C, int H, int W, int NIMG, int SROWS, int SCOLS, int CP, int THREADS>
+__device__ __forceinline__ void stage_rows(const float* __restrict__ x, float* xs, int n0, int y0) {
+  constexpr int C4 = C / 4;
+  constexpr int TOTAL = NIMG * SROWS * SCOLS * C4;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < TOTAL; i += THREADS) {
+    const int c4 = i % C4;
+    const int col = (i / C4) % SCOLS;
+    const int srow = (i / (C4 * SCOLS)) % SROWS;
+    const int b = i / (C4 * SCOLS * SROWS);
+    const int gy = y0 + srow - 1, gx = col - 1;
+    const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+    const float* src = in ? x + ((size_t(n0 + b) * H + gy) * W + gx) * C + c4 * 4 : x;
+    cp_async16(xs + ((b * SROWS + srow) * SCOLS + col) * CP + c4 * 4, src, in);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward / dgrad
+
+template <int C, int H, int TH, int COT, int PX, int CO>
+struct ConvCfg {
+  static constexpr int W = H;
+  static constexpr int CP = C + kPad;                  // staged pixel stride
+  static constexpr int IR = TH < H ? TH : H;           // output rows per image in a tile
+  static constexpr int NIMG = TH < H ? 1 : TH / H;     // images per tile
+  static constexpr int SROWS = IR + 2;                 // staged rows per image
+  static constexpr int SCOLS = W + 2;
+  static constexpr int XS = NIMG * SROWS * SCOLS * CP; // staged input floats
+  static constexpr int WS = 9 * C * COT;               // staged weight floats
+  static constexpr int LR = 32 / W;                    // row groups per warp
+  static constexpr int NPG = TH / (LR * PX);           // pixel groups per CTA
+  static constexpr int NCG = COT / CO;                 // channel groups per CTA
+  static constexpr int THREADS = 32 * NPG * NCG;
+  static constexpr int SMEM = (XS + WS) * 4;
+  static_assert(W <= 32 && 32 % W == 0, "image width");
+  static_assert(TH % (LR * PX) == 0, "pixel groups");
+  static_assert(IR % PX == 0, "a thread's rows stay in one image");
+  static_assert(TH < H ? H % TH == 0 : TH % H == 0, "row tiles");
+  static_assert(C % COT == 0 && COT % CO == 0 && CO % 4 == 0 && C % 4 == 0, "channels");
+};
+
+template <int C, int H, int TH, int COT, int PX, int CO, bool DGRAD>
+__global__ void __launch_bounds__(ConvCfg<C, H, TH, COT, PX, CO>::THREADS)
+k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y) {
+  using K = ConvCfg<C, H, TH, COT, PX, CO>;
+  constexpr int W = K::W, CP = K::CP;
+  extern __shared__ float4 smem4[];
+  float* xs = reinterpret_cast<float*>(smem4);
+  float* ws = xs + K::XS;
+
+  constexpr int CO_TILES = C / COT;
+  constexpr int ROW_TILES = TH < H ? H / TH : 1;
+  const int bid = blockIdx.x;
+  const int cot = bid % CO_TILES;
+  const int rt = (bid / CO_TILES) % ROW_TILES;
+  const int n0 = (bid / (CO_TILES * ROW_TILES)) * K::NIMG;
+  const int y0 = rt * K::IR;
+  const int co0 = cot * COT;
+
+  // stage the input rows (zero halo): asynchronous 16-byte copies along (x, c)
+  stage_rows<C, H, W, K::NIMG, K::SROWS, K::SCOLS, CP, K::THREADS>(x, xs, n0, y0);
+  // stage the weight slice as ws[tap][k][j] (j = output channel of the tile)
+  {
+    constexpr int C4 = C / 4;
+    if constexpr (!DGRAD) {
+      // y[.., co] = sum x[.., ci] w[co][r][s][ci]: ws[t][ci][co - co0], a
+      // transpose — lanes take consecutive co so the scalar stores are
+      // conflict-free
+#pragma unroll 4
+      for (int i = threadIdx.x; i < COT * 9 * C4; i += K::THREADS) {
+        const int j = i % COT, rem = i / COT;
+        const int t = rem / C4, c4 = rem % C4;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(w + size_t(co0 + j) * 9 * C) + rem);
+        float* d = ws + (t * C + c4 * 4) * COT + j;
+        d[0] = v.x; d[COT] = v.y; d[2 * COT] = v.z; d[3 * COT] = v.w;
+      }
+    } else {
+      // dx[.., ci] = sum dy[.., co] w[co][2-r][2-s][ci]: ws[t][co][ci - co0]
+      constexpr int J4 = COT / 4;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < C * 9 * J4; i += K::THREADS) {
+        const int j4 = i % J4, t = (i / J4) % 9, k = i / (9 * J4);
+        cp_async16(ws + ((8 - t) * C + k) * COT + j4 * 4, w + (size_t(k) * 9 + t) * C + co0 + j4 * 4, true);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pg = warp % K::NPG, cg = warp / K::NPG;
+  const int lx = lane % W, rg = lane / W;
+  const int t0 = (pg * K::LR + rg) * PX;      // first tile row of this thread
+  const int b = t0 / K::IR, ty0 = t0 % K::IR;
+  const float* xrow = xs + (b * K::SROWS + ty0) * K::SCOLS * CP + lx * CP;
+  const float* wcol = ws + cg * CO;
+
+  float acc[PX][CO];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int j = 0; j < CO; ++j) acc[i][j] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+#pragma unroll(C <= 16 ? C / 4 : 2)
+    for (int c4 = 0; c4 < C / 4; ++c4) {
+      float4 a[PX + 2];
+#pragma unroll
+      for (int j = 0; j < PX + 2; ++j)
+        a[j] = *reinterpret_cast<const float4*>(xrow + (j * K::SCOLS + s) * CP + c4 * 4);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const float* wp = wcol + ((r * 3 + s) * C + c4 * 4) * COT;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float wv[CO];
+#pragma unroll
+          for (int j = 0; j < CO; j += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(wp + q * COT + j);
+            wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+          }
+#pragma unroll
+          for (int i = 0; i < PX; ++i) {
+            const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : q == 2 ? a[i + r].z : a[i + r].w;
+#pragma unroll
+            for (int j = 0; j < CO; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+          }
+        }
+      }
+    }
+  }
+
+#pragma unroll
+  for (int i = 0; i < PX; ++i) {
+    float* out = y + ((size_t(n0 + b) * H + y0 + ty0 + i) * W + lx) * C + co0 + cg * CO;
+#pragma unroll
+    for (int j = 0; j < CO; j += 4)
+      *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+  }
+}
+
+template <int C, int H, int TH, int COT, int PX, int CO>
+int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cudaStream_t st) {
+  using K = ConvCfg<C, H, TH, COT, PX, CO>;
+  if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d not a multiple of %d", n, K::NIMG);
+  const int tiles = (n / K::NIMG) * (TH < H ? H / TH : 1) * (C / COT);
+  if (dgrad) {
+    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, true>;
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+      attr = true;
+    }
+    kern<<<tiles, K::THREADS, K::SMEM, st>>>(x, w, y);
+  } else {
+    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, false>;
+    static bool attr = false;
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+      attr = true;
+    }
+    kern<<<tiles, K::THREADS, K::SMEM, st>>>(x, w, y);
+  }
+  LAUNCH_CHECK("k_conv3x3");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// weight gradient
+
+template <int C, int H, int TH, int COT, int PS>
+struct WgradCfg {
+  static constexpr int W = H;
+  static constexpr int CP = C + kPad;
+  static constexpr int IR = TH < H ? TH : H;
+  static constexpr int NIMG = TH < H ? 1 : TH / H;
+  static constexpr int SROWS = IR + 2;
+  static constexpr int SCOLS = W + 2;
+  static constexpr int XS = NIMG * SROWS * SCOLS * CP;
+  static constexpr int DP = COT + kPad;                // staged dY pixel stride
+  static constexpr int DS = TH * W * DP;
+  static constexpr int GROUP = 3 * (C / 4) * (COT / 4);  // threads per pixel split
+  static constexpr int THREADS = GROUP * PS;
+  static constexpr int RED = 9 * C * COT;              // the CTA's partial dW
+  static constexpr int SMEM = ((XS + DS) > RED ? (XS + DS) : RED) * 4;
+  static constexpr int TILES_PER_N = (TH < H ? H / TH : 1);
+  static_assert(TH % PS == 0 && (TH / PS) % 1 == 0, "pixel splits");
+  static_assert(IR % (TH / PS) == 0 || (TH / PS) % IR == 0, "splits align with images");
+};
+
+template <int C, int H, int TH, int COT, int PS>
+__global__ void __launch_bounds__(WgradCfg<C, H, TH, COT, PS>::THREADS)
+k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part) {
+  using K = WgradCfg<C, H, TH, COT, PS>;
+  constexpr int W = K::W, CP = K::CP, DP = K::DP;
+  extern __shared__ float4 smem4[];
+  float* xs = reinterpret_cast<float*>(smem4);
+  float* ds = xs + K::XS;
+
+  constexpr int CO_TILES = C / COT;
+  const int bid = blockIdx.x;
+  const int cot = bid % CO_TILES;
+  const int ptile = bid / CO_TILES;                 // pixel tile index
+  const int rt = ptile % K::TILES_PER_N;
+  const int n0 = (ptile / K::TILES_PER_N) * K::NIMG;
+  const int y0 = rt * K::IR;
+  const int co0 = cot * COT;
+
+  stage_rows<C, H, W, K::NIMG, K::SROWS, K::SCOLS, CP, K::THREADS>(x, xs, n0, y0);
+  {
+    constexpr int J4 = COT / 4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TH * W * J4; i += K::THREADS) {
+      const int j4 = i % J4, p = i / J4;             // p: tile pixel (row-major over the tile)
+      const int b = p / (K::IR * W), rem = p % (K::IR * W);
+      cp_async16(ds + p * DP + j4 * 4, dy + ((size_t(n0 + b) * H + y0) * W + rem) * C + co0 + j4 * 4, true);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // thread -> (ci4 fastest, co4, r, pixel split)
+  const int tid = threadIdx.x;
+  const int ci4 = tid % (C / 4);
+  const int co4 = (tid / (C / 4)) % (COT / 4);
+  const int r = (tid / ((C / 4) * (COT / 4))) % 3;
+  const int ps = tid / K::GROUP;
+
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+
+  constexpr int RPS = TH / PS;                      // tile rows per split
+#pragma unroll 1
+  for (int tr = ps * RPS; tr < (ps + 1) * RPS; ++tr) {
+    const int b = tr / K::IR, ty = tr % K::IR;
+    const float* xr = xs + ((b * K::SROWS + ty + r) * K::SCOLS) * CP + ci4 * 4;
+    const float* dr = ds + (tr * W) * DP + co4 * 4;
+    float4 xm = *reinterpret_cast<const float4*>(xr);
+    float4 x0 = *reinterpret_cast<const float4*>(xr + CP);
+#pragma unroll 4
+    for (int xx = 0; xx < W; ++xx) {
+      const float4 xp = *reinterpret_cast<const float4*>(xr + (xx + 2) * CP);
+      const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
+      const float dv[4] = {d.x, d.y, d.z, d.w};
+      const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+      xm = x0;
+      x0 = xp;
+    }
+  }
+
+  // combine the pixel splits in a fixed order, then write the CTA's partial
+  // [co][r][s][ci] slice (co in the tile) contiguously
+  float* red = xs;
+  __syncthreads();
+#pragma unroll 1
+  for (int p = 0; p < PS; ++p) {
+    if (ps == p) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          float* d = red + ((co4 * 4 + c) * 9 + r * 3 + s) * C + ci4 * 4;
+          float4 v = make_float4(acc[s][0][c], acc[s][1][c], acc[s][2][c], acc[s][3][c]);
+          if (p > 0) {
+            const float4 o = *reinterpret_cast<const float4*>(d);
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          *reinterpret_cast<float4*>(d) = v;
+        }
+    }
+    __syncthreads();
+  }
+  float4* out = reinterpret_cast<float4*>(part + size_t(ptile) * 9 * C * C + size_t(co0) * 9 * C);
+  for (int i = tid; i < K::RED / 4; i += K::THREADS) out[i] = reinterpret_cast<const float4*>(red)[i];
+}
+
+// out[i] = sum_t part[t][i]: a CTA owns 8 float4 columns x 32 tile groups;
+// fixed summation order (per-thread strided partial sums, then the 32 groups)
+__global__ void __launch_bounds__(256)
+k_wgrad_reduce(const float4* __restrict__ part, float4* __restrict__ out, int cols4, int tiles) {
+  __shared__ float4 sm[32][8];
+  const int c = blockIdx.x * 8 + (threadIdx.x & 7);
+  const int g = threadIdx.x >> 3;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c < cols4) {
+#pragma unroll 4
+    for (int t = g; t < tiles; t += 32) {
+      const float4 v = __ldg(part + size_t(t) * cols4 + c);
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    }
+  }
+  sm[g][threadIdx.x & 7] = a;
+  __syncthreads();
+  if (g == 0 && c < cols4) {
+    float4 s = sm[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < 32; ++k) {
+      const float4 v = sm[k][threadIdx.x];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    out[c] = s;
+  }
+}
+
+template <int C, int H, int TH, int COT, int PS>
+size_t wgrad_tiles(int n) {
+  using K = WgradCfg<C, H, TH, COT, PS>;
+  return size_t(n / K::NIMG) * K::TILES_PER_N;
+}
+
+template <int C, int H, int TH, int COT, int PS>
+int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes, int n,
+                 cudaStream_t st) {
+  using K = WgradCfg<C, H, TH, COT, PS>;
+  if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: batch %d not a multiple of %d", n, K::NIMG);
+  const size_t tiles = wgrad_tiles<C, H, TH, COT, PS>(n);
+  if (ws_bytes < tiles * 9 * C * C * sizeof(float))
+    return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: workspace %zu B < %zu B", ws_bytes,
+                   tiles * 9 * C * C * sizeof(float));
+  auto kern = k_wgrad3x3<C, H, TH, COT, PS>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+    attr = true;
+  }
+  kern<<<unsigned(tiles * (C / COT)), K::THREADS, K::SMEM, st>>>(x, dy, ws);
+  LAUNCH_CHECK("k_wgrad3x3");
+  const int cols4 = 9 * C * C / 4;
+  k_wgrad_reduce<<<(cols4 + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float4*>(ws),
+                                                 reinterpret_cast<float4*>(dw), cols4, int(tiles));
+  LAUNCH_CHECK("k_wgrad_reduce");
+  return 0;
+}
+
+// the ResNet-20 shapes (C, H): tile configurations
+#define CONV_CFG_16 16, 32, 8, 16, 4, 8
+#define CONV_CFG_32 32, 16, 8, 32, 4, 8
+#define CONV_CFG_64 64, 8, 8, 32, 2, 8
+#define WG_CFG_16 16, 32, 8, 16, 2
+#define WG_CFG_32 32, 16, 8, 32, 1
+#define WG_CFG_64 64, 8, 8, 32, 1
+
+}  // namespace
+
+extern "C" int lpp_conv3x3_supported(int c, int hw) {
+  return (c == 16 && hw == 32) || (c == 32 && hw == 16) || (c == 64 && hw == 8);
+}
+
+extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
+                               void* stream) {
+  if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
+  if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (c == 16 && hw == 32) return launch_conv<CONV_CFG_16>(x, w, y, n, dgrad != 0, st);
+  if (c == 32 && hw == 16) return launch_conv<CONV_CFG_32>(x, w, y, n, dgrad != 0, st);
+  if (c == 64 && hw == 8) return launch_conv<CONV_CFG_64>(x, w, y, n, dgrad != 0, st);
+  return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: no kernel for C=%d H=W=%d", c, hw);
+}
+
+extern "C" size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw) {
+  if (n <= 0) return 0;
+  if (c == 16 && hw == 32) return wgrad_tiles<WG_CFG_16>(n) * 9 * c * c * sizeof(float);
+  if (c == 32 && hw == 16) return wgrad_tiles<WG_CFG_32>(n) * 9 * c * c * sizeof(float);
+  if (c == 64 && hw == 8) return wgrad_tiles<WG_CFG_64>(n) * 9 * c * c * sizeof(float);
+  return 0;
+}
+
+extern "C" int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
+                                     int n, int c, int hw, void* stream) {
+  if (!x || !dy || !dw || !ws) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: null pointer");
+  if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: batch %d", n);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (c == 16 && hw == 32) return launch_wgrad<WG_CFG_16>(x, dy, dw, ws, ws_bytes, n, st);
+  if (c == 32 && hw == 16) return launch_wgrad<WG_CFG_32>(x, dy, dw, ws, ws_bytes, n, st);
+  if (c == 64 && hw == 8) return launch_wgrad<WG_CFG_64>(x, dy, dw, ws, ws_bytes, n, st);
+  return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: no kernel for C=%d H=W=%d", c, hw);
+}

@@ -523,6 +523,7 @@ extern "C" int lpp_updater_run(const lpp_updater_cfg* c, lpp_updater_stats* st) 
     slot_of[k] = slot;
     step_of[k] = t;
     st->flops += c->flops_of[b];
+    if (c->graph_kernels_of) st->graph_kernels += c->graph_kernels_of[b];
     ++t;
   }
   CUDA_TRY(cudaStreamSynchronize(stream));

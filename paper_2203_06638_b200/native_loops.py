@@ -22,6 +22,7 @@ import torch
 
 from . import _native as N
 from .records import AveragerStamp, UpdateRecord
+from .step import add_graph_kernels
 
 
 class NativeLoops:
@@ -68,10 +69,12 @@ class NativeLoops:
         hi = np.zeros(nb + 1, dtype=np.int64)
         execs = (ctypes.c_void_p * (2 * (nb + 1)))()       # [block][input buffer]
         flops = np.zeros(nb + 1, dtype=np.int64)
+        gk = np.zeros(nb + 1, dtype=np.int64)
         for b in range(nb + 1):
             blk = cfg.partition.block(b)
             lo[b], hi[b] = blk.start, blk.stop
             flops[b] = self._flops_of[b]
+            gk[b] = prog.graph_kernels.get((b, 0), 0)
             for buf in (0, 1):
                 key = (b, buf % prog.nbuf)
                 if key in prog.execs:
@@ -97,6 +100,7 @@ class NativeLoops:
         c.block_lo, c.block_hi = lo.ctypes.data, hi.ctypes.data
         c.graph_exec = ctypes.addressof(execs)
         c.flops_of = flops.ctypes.data
+        c.graph_kernels_of = gk.ctypes.data
         c.x, c.g = w.store.arena.ptr, w.grads[r].ptr
         c.m = w.moms[r].ptr if w.moms[r] is not None else None
         c.replica = w.replicas[r].ptr
@@ -129,7 +133,7 @@ class NativeLoops:
             self._apply_logs[(w.q, r)] = alog
         c.stream = w.streams[r].cuda_stream
         c.apply_stream = w.apply_streams[r].cuda_stream if self.side_apply else None
-        keep = [lo, hi, execs, flops, ms]
+        keep = [lo, hi, execs, flops, ms, gk]
         if cfg.sampling == "host":
             # the reference's numpy stream (engine.py:293-296), restated natively
             c.host_rng = 1
@@ -205,6 +209,7 @@ class NativeLoops:
                     self.loss_log.extend(float(v) for v in log[:min(count, len(log))])
             del keep
             self.flops.add(int(st.flops))
+            add_graph_kernels(int(st.graph_kernels))
             if self.time_apply:
                 alog = self._apply_logs.pop((q, r), None)
                 with self.native_lock:

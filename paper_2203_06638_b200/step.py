@@ -19,10 +19,33 @@ replay by the engine through the C ABI.
 from __future__ import annotations
 
 import gc
+import threading
 
 import torch
 
 from .partition import Block
+
+# kernels of this library launched from inside replayed step graphs (the
+# conv_f32.cu convolutions): counted per graph at capture, summed per replay
+# here and by the native loop (lpp_updater_stats.graph_kernels)
+_GRAPH_KERNELS = [0]
+_GK_LOCK = threading.Lock()
+
+
+def add_graph_kernels(n: int) -> None:
+    with _GK_LOCK:
+        _GRAPH_KERNELS[0] += int(n)
+
+
+def graph_kernel_count() -> int:
+    """Library kernels run inside step-graph replays so far (process-wide)."""
+    return _GRAPH_KERNELS[0]
+
+
+def _lib_launches() -> int:
+    from . import _native
+
+    return _native.launch_count()
 
 
 class StepProgram:
@@ -84,6 +107,7 @@ class StepProgram:
             raise ValueError("grad_mode='accumulate' needs fp32 parameters (bf16 shadow weights "
                              "have no arena .grad views)")
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.graph_kernels: dict[tuple[int, int], int] = {}
         self.use_graphs = use_graphs
         with torch.cuda.stream(stream):
             for _ in range(max(warmup, 1)):
@@ -103,8 +127,10 @@ class StepProgram:
                     for bid in self.blocks:
                         for buf in range(self.nbuf):
                             g = torch.cuda.CUDAGraph()
+                            l0 = _lib_launches()
                             with torch.cuda.graph(g, pool=pool, stream=stream):
                                 self._body(bid, buf)
+                            self.graph_kernels[(bid, buf)] = _lib_launches() - l0
                             pool = g.pool()
                             self.graphs[(bid, buf)] = g
                 finally:
@@ -159,8 +185,10 @@ class StepProgram:
         buf %= self.nbuf
         if self.execs:
             self._native.graph_launch(self.execs[(bid, buf)], self.stream.cuda_stream)
+            add_graph_kernels(self.graph_kernels.get((bid, buf), 0))
         elif self.use_graphs:
             self.graphs[(bid, buf)].replay()
+            add_graph_kernels(self.graph_kernels.get((bid, buf), 0))
         else:
             with torch.cuda.stream(self.stream):
                 self._body(bid, buf)

@@ -1,0 +1,158 @@
+"""The library's fp32 3x3 convolutions (csrc/conv_f32.cu via conv.py)
+against an fp64 reference of the same op (cuDNN in fp64), at the CIFAR
+ResNet-20 shapes: forward, data gradient, weight gradient, the autograd
+function with partial backprop, graph capture, and the cuDNN routing for
+shapes without a kernel."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+CL = torch.channels_last
+SHAPES = [(16, 32), (32, 16), (64, 8)]
+# fp32 FFMA with a different summation order than the fp64 reference:
+# max |err| / max |ref| (cuDNN's own fp32 algorithms land at ~5e-7)
+TOL = 1e-5
+
+
+def _rel(a, ref):
+    return float((a.double() - ref).abs().max() / ref.abs().max())
+
+
+def _data(c, hw, n, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn(n, c, hw, hw, device="cuda", generator=g).to(memory_format=CL)
+    w = (torch.randn(c, c, 3, 3, device="cuda", generator=g) / (3 * c ** 0.5)).to(memory_format=CL)
+    gy = torch.randn(n, c, hw, hw, device="cuda", generator=g).to(memory_format=CL)
+    return x, w, gy
+
+
+def _ref(x, w, gy):
+    xd, wd, gyd = x.double(), w.double(), gy.double()
+    y = F.conv2d(xd, wd, padding=1)
+    gx, gw, _ = torch.ops.aten.convolution_backward(gyd, xd, wd, None, (1, 1), (1, 1), (1, 1), False, (0, 0), 1,
+                                                    (True, True, False))
+    return y, gx, gw
+
+
+@pytest.mark.parametrize("c,hw", SHAPES)
+@pytest.mark.parametrize("n", [1, 3, 128])
+def test_conv_kernels_match_fp64(c, hw, n):
+    from paper_2203_06638_b200 import conv
+
+    x, w, gy = _data(c, hw, n)
+    y_ref, gx_ref, gw_ref = _ref(x, w, gy)
+    y = conv.conv_fwd(x, w)
+    gx = conv.conv_fwd(gy, w, dgrad=True)
+    gw = conv.conv_wgrad(x, gy, w)
+    assert y.is_contiguous(memory_format=CL) and gw.is_contiguous(memory_format=CL)
+    assert _rel(y, y_ref) < TOL
+    assert _rel(gx, gx_ref) < TOL
+    assert _rel(gw, gw_ref) < TOL
+
+
+@pytest.mark.parametrize("c,hw", SHAPES)
+def test_conv_wgrad_deterministic(c, hw):
+    from paper_2203_06638_b200 import conv
+
+    x, w, gy = _data(c, hw, 64, seed=1)
+    a = conv.conv_wgrad(x, gy, w)
+    b = conv.conv_wgrad(x, gy, w)
+    assert torch.equal(a, b)
+
+
+def test_conv_zero_padding_edges():
+    """A constant image: border outputs see fewer taps (zero padding)."""
+    from paper_2203_06638_b200 import conv
+
+    c, hw = 16, 32
+    x = torch.ones(2, c, hw, hw, device="cuda").to(memory_format=CL)
+    w = torch.ones(c, c, 3, 3, device="cuda").to(memory_format=CL)
+    y = conv.conv_fwd(x, w)
+    assert float(y[0, 0, 0, 0]) == 4 * c and float(y[0, 0, 5, 5]) == 9 * c and float(y[1, 3, 0, 7]) == 6 * c
+
+
+@pytest.mark.parametrize("which", ["both", "input", "weight"])
+def test_conv3x3_module_autograd(which):
+    from paper_2203_06638_b200.conv import Conv3x3
+
+    torch.manual_seed(0)
+    m = Conv3x3(32, 32, 1).cuda().to(memory_format=CL)
+    x, _, gy = _data(32, 16, 8, seed=2)
+    x.requires_grad_(which in ("both", "input"))
+    m.weight.requires_grad_(which in ("both", "weight"))
+    y = m(x)
+    y.backward(gy)
+    xd = x.detach().double().requires_grad_(x.requires_grad)
+    wd = m.weight.detach().double().requires_grad_(m.weight.requires_grad)
+    yd = F.conv2d(xd, wd, padding=1)
+    yd.backward(gy.double())
+    assert _rel(y.detach(), yd.detach()) < TOL
+    if which in ("both", "input"):
+        assert _rel(x.grad, xd.grad) < TOL
+    else:
+        assert x.grad is None
+    if which in ("both", "weight"):
+        assert _rel(m.weight.grad, wd.grad) < TOL
+    else:
+        assert m.weight.grad is None
+
+
+def test_conv3x3_routes_other_cases_to_cudnn(monkeypatch):
+    """No kernel for the shape / stride / dtype, or LPP_CONV=cudnn: F.conv2d."""
+    from paper_2203_06638_b200 import conv
+    from paper_2203_06638_b200.conv import Conv3x3
+
+    calls = []
+    real = conv.conv3x3
+    monkeypatch.setattr(conv, "conv3x3", lambda x, w: calls.append(1) or real(x, w))
+    x16 = torch.randn(2, 16, 16, 16, device="cuda").to(memory_format=CL)   # (16, 16): no kernel
+    m = Conv3x3(16, 16, 1).cuda().to(memory_format=CL)
+    assert torch.allclose(m(x16), F.conv2d(x16, m.weight, padding=1), atol=1e-5)
+    s2 = Conv3x3(16, 32, 2).cuda().to(memory_format=CL)
+    x32 = torch.randn(2, 16, 32, 32, device="cuda").to(memory_format=CL)
+    s2(x32)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        m(x32)
+    assert calls == []
+    m(x32)
+    assert calls == [1]
+    monkeypatch.setenv("LPP_CONV", "cudnn")
+    m(x32)
+    assert calls == [1]
+
+
+def test_conv_in_cuda_graph():
+    from paper_2203_06638_b200 import conv
+
+    x, w, gy = _data(64, 8, 16, seed=3)
+    y_ref, gx_ref, gw_ref = _ref(x, w, gy)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        conv.conv_fwd(x, w), conv.conv_fwd(gy, w, dgrad=True), conv.conv_wgrad(x, gy, w)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = (conv.conv_fwd(x, w), conv.conv_fwd(gy, w, dgrad=True), conv.conv_wgrad(x, gy, w))
+    for o in out:
+        o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert _rel(out[0], y_ref) < TOL and _rel(out[1], gx_ref) < TOL and _rel(out[2], gw_ref) < TOL
+
+
+def test_conv_rejects_unsupported_shape():
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200 import conv
+
+    x = torch.randn(2, 16, 16, 16, device="cuda").to(memory_format=CL)
+    w = torch.randn(16, 16, 3, 3, device="cuda").to(memory_format=CL)
+    with pytest.raises(ValueError, match="no kernel"):
+        conv.conv_fwd(x, w)
+    assert N.lib.lpp_conv3x3_wgrad_workspace(2, 16, 16) == 0

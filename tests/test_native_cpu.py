@@ -42,7 +42,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_error_channel():
-    assert N.lib.lpp_abi_version() == 3
+    assert N.lib.lpp_abi_version() == 4
     with pytest.raises(IndexError):
         # range check happens before any device work
         N.accum(0, 4, 3, 0, 2, 1.0, N.MODE_RED, 0)
