@@ -39,6 +39,7 @@
 #include "common.cuh"
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace {
 
@@ -96,7 +97,7 @@ struct ConvCfg {
   static_assert(C % COT == 0 && COT % CO == 0 && CO % 4 == 0 && C % 4 == 0, "channels");
 };
 
-template <int C, int H, int TH, int COT, int PX, int CO, bool DGRAD>
+template <int C, int H, int TH, int COT, int PX, int CO, int U, bool DGRAD>
 __global__ void __launch_bounds__(ConvCfg<C, H, TH, COT, PX, CO>::THREADS)
 k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y) {
   using K = ConvCfg<C, H, TH, COT, PX, CO>;
@@ -158,9 +159,12 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
 #pragma unroll
     for (int j = 0; j < CO; ++j) acc[i][j] = 0.f;
 
-#pragma unroll
+  // rolled over (s, c4): the 384-FFMA body stays resident in the
+  // instruction cache (fully unrolled, instruction fetch was a third of the
+  // stalls)
+#pragma unroll 1
   for (int s = 0; s < 3; ++s) {
-#pragma unroll(C <= 16 ? C / 4 : 2)
+#pragma unroll(U)
     for (int c4 = 0; c4 < C / 4; ++c4) {
       float4 a[PX + 2];
 #pragma unroll
@@ -197,13 +201,13 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
   }
 }
 
-template <int C, int H, int TH, int COT, int PX, int CO>
+template <int C, int H, int TH, int COT, int PX, int CO, int U>
 int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cudaStream_t st) {
   using K = ConvCfg<C, H, TH, COT, PX, CO>;
   if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d not a multiple of %d", n, K::NIMG);
   const int tiles = (n / K::NIMG) * (TH < H ? H / TH : 1) * (C / COT);
   if (dgrad) {
-    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, true>;
+    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, true>;
     static bool attr = false;
     if (!attr) {
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
@@ -211,7 +215,7 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cud
     }
     kern<<<tiles, K::THREADS, K::SMEM, st>>>(x, w, y);
   } else {
-    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, false>;
+    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, false>;
     static bool attr = false;
     if (!attr) {
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
@@ -343,28 +347,29 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* __r
   for (int i = tid; i < K::RED / 4; i += K::THREADS) out[i] = reinterpret_cast<const float4*>(red)[i];
 }
 
-// out[i] = sum_t part[t][i]: a CTA owns 8 float4 columns x 32 tile groups;
-// fixed summation order (per-thread strided partial sums, then the 32 groups)
-__global__ void __launch_bounds__(256)
+// out[i] = sum_t part[t][i]: a CTA owns 4 float4 columns x 64 tile groups;
+// fixed summation order (per-thread strided partial sums, then the 64 groups)
+constexpr int kRedCols = 4, kRedGroups = 64;
+__global__ void __launch_bounds__(kRedCols * kRedGroups)
 k_wgrad_reduce(const float4* __restrict__ part, float4* __restrict__ out, int cols4, int tiles) {
-  __shared__ float4 sm[32][8];
-  const int c = blockIdx.x * 8 + (threadIdx.x & 7);
-  const int g = threadIdx.x >> 3;
+  __shared__ float4 sm[kRedGroups][kRedCols];
+  const int lc = threadIdx.x % kRedCols, g = threadIdx.x / kRedCols;
+  const int c = blockIdx.x * kRedCols + lc;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   if (c < cols4) {
-#pragma unroll 4
-    for (int t = g; t < tiles; t += 32) {
+#pragma unroll 8
+    for (int t = g; t < tiles; t += kRedGroups) {
       const float4 v = __ldg(part + size_t(t) * cols4 + c);
       a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
     }
   }
-  sm[g][threadIdx.x & 7] = a;
+  sm[g][lc] = a;
   __syncthreads();
   if (g == 0 && c < cols4) {
-    float4 s = sm[0][threadIdx.x];
-#pragma unroll
-    for (int k = 1; k < 32; ++k) {
-      const float4 v = sm[k][threadIdx.x];
+    float4 s = sm[0][lc];
+#pragma unroll 8
+    for (int k = 1; k < kRedGroups; ++k) {
+      const float4 v = sm[k][lc];
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
     out[c] = s;
@@ -395,19 +400,53 @@ int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t w
   kern<<<unsigned(tiles * (C / COT)), K::THREADS, K::SMEM, st>>>(x, dy, ws);
   LAUNCH_CHECK("k_wgrad3x3");
   const int cols4 = 9 * C * C / 4;
-  k_wgrad_reduce<<<(cols4 + 7) / 8, 256, 0, st>>>(reinterpret_cast<const float4*>(ws),
+  k_wgrad_reduce<<<(cols4 + kRedCols - 1) / kRedCols, kRedCols * kRedGroups, 0, st>>>(reinterpret_cast<const float4*>(ws),
                                                  reinterpret_cast<float4*>(dw), cols4, int(tiles));
   LAUNCH_CHECK("k_wgrad_reduce");
   return 0;
 }
 
-// the ResNet-20 shapes (C, H): tile configurations
-#define CONV_CFG_16 16, 32, 8, 16, 4, 8
-#define CONV_CFG_32 32, 16, 8, 32, 4, 8
-#define CONV_CFG_64 64, 8, 8, 32, 2, 8
-#define WG_CFG_16 16, 32, 8, 16, 2
-#define WG_CFG_32 32, 16, 8, 32, 1
-#define WG_CFG_64 64, 8, 8, 32, 1
+// the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
+// default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
+// tools/exp_conv_native.py).
+using ConvFn = int (*)(const float*, const float*, float*, int, bool, cudaStream_t);
+using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, int, cudaStream_t);
+using TilesFn = size_t (*)(int);
+
+//                     C   H  TH COT PX CO U
+const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 4, 16, 4, 8, 1>,
+                          launch_conv<16, 32, 8, 16, 4, 8, 2>, launch_conv<16, 32, 4, 16, 4, 8, 2>};
+const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 16, 4, 8, 1>,
+                          launch_conv<32, 16, 4, 32, 2, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
+const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 8, 16, 2, 8, 1>,
+                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 8, 32, 2, 8, 2>};
+//                        C   H  TH COT PS
+const WgradFn kWg16[] = {launch_wgrad<16, 32, 8, 16, 2>, launch_wgrad<16, 32, 8, 16, 4>,
+                         launch_wgrad<16, 32, 16, 16, 4>, launch_wgrad<16, 32, 4, 16, 2>};
+const TilesFn kWt16[] = {wgrad_tiles<16, 32, 8, 16, 2>, wgrad_tiles<16, 32, 8, 16, 4>,
+                         wgrad_tiles<16, 32, 16, 16, 4>, wgrad_tiles<16, 32, 4, 16, 2>};
+const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1>, launch_wgrad<32, 16, 8, 16, 2>,
+                         launch_wgrad<32, 16, 4, 32, 1>, launch_wgrad<32, 16, 16, 32, 2>};
+const TilesFn kWt32[] = {wgrad_tiles<32, 16, 8, 32, 1>, wgrad_tiles<32, 16, 8, 16, 2>,
+                         wgrad_tiles<32, 16, 4, 32, 1>, wgrad_tiles<32, 16, 16, 32, 2>};
+const WgradFn kWg64[] = {launch_wgrad<64, 8, 8, 32, 1>, launch_wgrad<64, 8, 8, 16, 1>,
+                         launch_wgrad<64, 8, 8, 16, 2>, launch_wgrad<64, 8, 8, 8, 1>};
+const TilesFn kWt64[] = {wgrad_tiles<64, 8, 8, 32, 1>, wgrad_tiles<64, 8, 8, 16, 1>,
+                         wgrad_tiles<64, 8, 8, 16, 2>, wgrad_tiles<64, 8, 8, 8, 1>};
+
+int env_variant(const char* name) {
+  const char* v = std::getenv(name);
+  const int i = v ? std::atoi(v) : 0;
+  return i < 0 || i > 3 ? 0 : i;
+}
+int conv_variant() {
+  static const int v = env_variant("LPP_CONV_VARIANT");
+  return v;
+}
+int wgrad_variant() {
+  static const int v = env_variant("LPP_WGRAD_VARIANT");
+  return v;
+}
 
 }  // namespace
 
@@ -420,17 +459,19 @@ extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, 
   if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
   auto st = static_cast<cudaStream_t>(stream);
-  if (c == 16 && hw == 32) return launch_conv<CONV_CFG_16>(x, w, y, n, dgrad != 0, st);
-  if (c == 32 && hw == 16) return launch_conv<CONV_CFG_32>(x, w, y, n, dgrad != 0, st);
-  if (c == 64 && hw == 8) return launch_conv<CONV_CFG_64>(x, w, y, n, dgrad != 0, st);
+  const int v = conv_variant();
+  if (c == 16 && hw == 32) return kConv16[v](x, w, y, n, dgrad != 0, st);
+  if (c == 32 && hw == 16) return kConv32[v](x, w, y, n, dgrad != 0, st);
+  if (c == 64 && hw == 8) return kConv64[v](x, w, y, n, dgrad != 0, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: no kernel for C=%d H=W=%d", c, hw);
 }
 
 extern "C" size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw) {
   if (n <= 0) return 0;
-  if (c == 16 && hw == 32) return wgrad_tiles<WG_CFG_16>(n) * 9 * c * c * sizeof(float);
-  if (c == 32 && hw == 16) return wgrad_tiles<WG_CFG_32>(n) * 9 * c * c * sizeof(float);
-  if (c == 64 && hw == 8) return wgrad_tiles<WG_CFG_64>(n) * 9 * c * c * sizeof(float);
+  const int v = wgrad_variant();
+  if (c == 16 && hw == 32) return kWt16[v](n) * 9 * c * c * sizeof(float);
+  if (c == 32 && hw == 16) return kWt32[v](n) * 9 * c * c * sizeof(float);
+  if (c == 64 && hw == 8) return kWt64[v](n) * 9 * c * c * sizeof(float);
   return 0;
 }
 
@@ -439,8 +480,9 @@ extern "C" int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw,
   if (!x || !dy || !dw || !ws) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: batch %d", n);
   auto st = static_cast<cudaStream_t>(stream);
-  if (c == 16 && hw == 32) return launch_wgrad<WG_CFG_16>(x, dy, dw, ws, ws_bytes, n, st);
-  if (c == 32 && hw == 16) return launch_wgrad<WG_CFG_32>(x, dy, dw, ws, ws_bytes, n, st);
-  if (c == 64 && hw == 8) return launch_wgrad<WG_CFG_64>(x, dy, dw, ws, ws_bytes, n, st);
+  const int v = wgrad_variant();
+  if (c == 16 && hw == 32) return kWg16[v](x, dy, dw, ws, ws_bytes, n, st);
+  if (c == 32 && hw == 16) return kWg32[v](x, dy, dw, ws, ws_bytes, n, st);
+  if (c == 64 && hw == 8) return kWg64[v](x, dy, dw, ws, ws_bytes, n, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: no kernel for C=%d H=W=%d", c, hw);
 }

@@ -41,22 +41,31 @@ with open(out_dir / "trace_launches.csv", "w", newline="") as f:
         w.writerow([n, s - t0, d])
 tot, cnt = collections.Counter(), collections.Counter()
 for n, _, d in rows:
-    k = n.split("(")[0][:110]
+    k = n.replace("(anonymous namespace)::", "").split("(")[0][:110]
     tot[k] += d
     cnt[k] += 1
 T = sum(tot.values())
-ours = ("k_apply", "void k_apply", "k_snapshot", "void k_average", "k_accum", "k_gather", "k_publish",
-        "k_set_i64", "k_classify", "(anonymous namespace)::k_sample")
-mine = sum(v for k, v in tot.items() if k.startswith(ours))
+OURS = ("k_apply", "k_snapshot", "k_average", "k_accum", "k_gather", "k_publish", "k_set_i64",
+        "k_classify", "k_sample", "k_conv3x3", "k_wgrad3x3", "k_wgrad_reduce")
+
+
+def is_ours(k):
+    base = k[5:] if k.startswith("void ") else k
+    base = base.replace("(anonymous namespace)::", "")
+    return base.startswith(OURS)
+
+
+mine = sum(v for k, v in tot.items() if is_ours(k))
 span = (rows[-1][1] + rows[-1][2] - rows[0][1]) if rows else 0
 lines = [f"# {len(rows)} kernels in the timed region of {K * U + U} minibatches "
          f"(ResNet-20 LPP-SGD U=4 B=128, {'bf16' if '--bf16' in sys.argv else 'fp32'} convolutions, "
          f"native loop); summed kernel time {T / 1e3:.1f} ms "
          f"over a {span / 1e3:.1f} ms span (4 streams overlap)",
-         f"# our kernels (K1-K5 + in-graph sampler): {100 * mine / T:.2f}% of summed kernel time",
+         f"# our kernels (K1-K5, in-graph sampler, fp32 3x3 convolutions): {100 * mine / T:.2f}% of "
+         f"summed kernel time",
          "share%   total_us   n   kernel"]
 for k, v in tot.most_common():
-    tag = "[ours] " if k.startswith(ours) else ""
+    tag = "[ours] " if is_ours(k) else ""
     lines.append(f"{100 * v / T:6.2f} {v:10.1f} {cnt[k]:5d}  {tag}{k}")
 (out_dir / "trace_share.txt").write_text("\n".join(lines) + "\n")
 print("\n".join(lines[:30]))
