@@ -599,11 +599,17 @@ int lpp_conv3x3_supported(int c, int hw);
 /* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x */
 int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
                     void* stream);
-/* bytes of workspace lpp_conv3x3_wgrad_f32 needs (per-tile partial sums) */
+/* bytes of workspace lpp_conv3x3_wgrad_f32 needs (per-cluster partial sums) */
 size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
-/* dw = sum over pixels of x (*) dy, deterministic (fixed-order reduction) */
+/* dw = sum over pixels of x (*) dy in ONE launch, deterministic: CTA
+ * partials summed over thread-block-cluster DSMEM in rank order, cluster
+ * partials summed in cluster order by the last cluster to arrive.
+ * arrivals: LPP_CONV_ARRIVALS uint32 device cells, zero before the first
+ * call and left zero by every call; one set per stream (launches sharing a
+ * set must be stream-ordered). */
+#define LPP_CONV_ARRIVALS 8
 int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
-                          int n, int c, int hw, void* stream);
+                          uint32_t* arrivals, int n, int c, int hw, void* stream);
 
 #ifdef __cplusplus
 }

@@ -220,7 +220,7 @@ _SIGS = {
     "lpp_conv3x3_supported": (_c.c_int, [_c.c_int, _c.c_int]),
     "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp]),
     "lpp_conv3x3_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
-    "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _c.c_int, _c.c_int, _c.c_int, _vp]),
+    "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _vp, _c.c_int, _c.c_int, _c.c_int, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

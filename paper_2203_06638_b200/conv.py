@@ -57,7 +57,17 @@ def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False) -> torch.Ten
     return y
 
 
-def conv_wgrad(x: torch.Tensor, dy: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+ARRIVALS = 8   # LPP_CONV_ARRIVALS
+
+
+def arrival_cells(device) -> torch.Tensor:
+    """Zeroed counters for lpp_conv3x3_wgrad_f32 (every call leaves them
+    zero; calls sharing a set must be stream-ordered)."""
+    return torch.zeros(ARRIVALS, dtype=torch.int32, device=device)
+
+
+def conv_wgrad(x: torch.Tensor, dy: torch.Tensor, like: torch.Tensor,
+               arrivals: torch.Tensor | None = None) -> torch.Tensor:
     N = _lib()
     n, c, h, _ = x.shape
     x = x.contiguous(memory_format=_CL)
@@ -65,29 +75,62 @@ def conv_wgrad(x: torch.Tensor, dy: torch.Tensor, like: torch.Tensor) -> torch.T
     dw = torch.empty_like(like, memory_format=_CL)
     nbytes = int(N.lib.lpp_conv3x3_wgrad_workspace(n, c, h))
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
+    if arrivals is None:
+        arrivals = arrival_cells(x.device)
     N.check(N.lib.lpp_conv3x3_wgrad_f32(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(), nbytes,
-                                        n, c, h, torch.cuda.current_stream(x.device).cuda_stream),
+                                        arrivals.data_ptr(), n, c, h,
+                                        torch.cuda.current_stream(x.device).cuda_stream),
             "conv3x3_wgrad_f32")
     return dw
 
 
+def _will_run(node) -> bool:
+    """Whether the current backward pass executes ``node`` (a non-leaf
+    autograd node): the input gradient of a block's input-most layer is not
+    needed under partial backprop."""
+    if node is None:
+        return False
+    try:
+        return bool(torch._C._will_engine_execute_node(node))
+    except RuntimeError:
+        return True
+
+
 class _Conv3x3Fn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w):
+    def forward(ctx, x, w, arrivals, want_w):
         ctx.save_for_backward(x, w)
+        ctx.arrivals, ctx.want_w = arrivals, want_w
         return conv_fwd(x, w)
 
     @staticmethod
     def backward(ctx, gy):
         x, w = ctx.saved_tensors
-        gx = conv_fwd(gy, w, dgrad=True) if ctx.needs_input_grad[0] else None
-        gw = conv_wgrad(x, gy, w) if ctx.needs_input_grad[1] else None
-        return gx, gw
+        gx = gw = None
+        if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
+            gx = conv_fwd(gy, w, dgrad=True)
+        if ctx.needs_input_grad[1] and ctx.want_w:
+            gw = conv_wgrad(x, gy, w, ctx.arrivals)
+        return gx, gw, None, None
 
 
-def conv3x3(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-    """y = conv2d(x, w, stride 1, padding 1) on the library's kernels."""
-    return _Conv3x3Fn.apply(x, w)
+def conv3x3(x: torch.Tensor, w: torch.Tensor, arrivals: torch.Tensor | None = None,
+            want_w: bool = True) -> torch.Tensor:
+    """y = conv2d(x, w, stride 1, padding 1) on the library's kernels.
+    ``want_w=False``: the weight gradient is not wanted (a layer above the
+    partial-backprop block; autograd.grad cannot tell a custom function)."""
+    if arrivals is None:
+        arrivals = arrival_cells(x.device)
+    return _Conv3x3Fn.apply(x, w, arrivals, want_w)
+
+
+def mark_weight_grads(module: nn.Module, leaves) -> None:
+    """Set which ``Conv3x3`` weights the next backward differentiates (the
+    block's leaves): the others skip their weight-gradient kernels."""
+    ids = {id(p) for p in leaves}
+    for m in module.modules():
+        if isinstance(m, Conv3x3):
+            m.want_w = id(m.weight) in ids
 
 
 class Conv3x3(nn.Conv2d):
@@ -96,10 +139,14 @@ class Conv3x3(nn.Conv2d):
 
     def __init__(self, cin: int, cout: int, stride: int = 1):
         super().__init__(cin, cout, 3, stride, 1, bias=False)
+        self.want_w = True
+        self._arrivals = None   # wgrad arrival counters; this module's launches are stream-ordered
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if (x.dtype == torch.float32 and x.is_cuda and self.weight.dtype == torch.float32
                 and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled()
                 and supported(self.in_channels, self.out_channels, x.shape[2], self.stride[0], 3)):
-            return conv3x3(x, self.weight)
+            if self._arrivals is None or self._arrivals.device != x.device:
+                self._arrivals = arrival_cells(x.device)
+            return conv3x3(x, self.weight, self._arrivals, self.want_w)
         return F.conv2d(x, self.weight, None, self.stride, self.padding)

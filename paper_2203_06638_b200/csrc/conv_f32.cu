@@ -38,8 +38,13 @@
 
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -230,7 +235,7 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cud
 // ---------------------------------------------------------------------------
 // weight gradient
 
-template <int C, int H, int TH, int COT, int PS>
+template <int C, int H, int TH, int COT, int PS, int CLMAX>
 struct WgradCfg {
   static constexpr int W = H;
   static constexpr int CP = C + kPad;
@@ -246,23 +251,33 @@ struct WgradCfg {
   static constexpr int RED = 9 * C * COT;              // the CTA's partial dW
   static constexpr int SMEM = ((XS + DS) > RED ? (XS + DS) : RED) * 4;
   static constexpr int TILES_PER_N = (TH < H ? H / TH : 1);
-  static_assert(TH % PS == 0 && (TH / PS) % 1 == 0, "pixel splits");
+  static_assert(TH % PS == 0, "pixel splits");
   static_assert(IR % (TH / PS) == 0 || (TH / PS) % IR == 0, "splits align with images");
+  static_assert(RED % (4 * CLMAX) == 0, "cluster slices");
 };
 
-template <int C, int H, int TH, int COT, int PS>
-__global__ void __launch_bounds__(WgradCfg<C, H, TH, COT, PS>::THREADS)
-k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part) {
-  using K = WgradCfg<C, H, TH, COT, PS>;
+// Weight gradient, reduced without a second launch and in a fixed order:
+//   1. each CTA: its tile's partial dW slice (co in the tile) in shared memory
+//      (pixel splits combined in order);
+//   2. cluster rank k sums slice k of the CL CTAs' partials over DSMEM (rank
+//      order) into the cluster's partial in the workspace;
+//   3. the last cluster to finish (a per-co-tile arrival counter, left at 0
+//      for the next launch) sums the clusters' partials in cluster order
+//      into dW.  Any arrival order gives the same bits.
+template <int C, int H, int TH, int COT, int PS, int CLMAX>
+__global__ void __launch_bounds__(WgradCfg<C, H, TH, COT, PS, CLMAX>::THREADS)
+k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* part, float* __restrict__ dw,
+           unsigned* __restrict__ arrivals) {
+  using K = WgradCfg<C, H, TH, COT, PS, CLMAX>;
   constexpr int W = K::W, CP = K::CP, DP = K::DP;
   extern __shared__ float4 smem4[];
+  __shared__ int s_last;
   float* xs = reinterpret_cast<float*>(smem4);
   float* ds = xs + K::XS;
+  cg::cluster_group cluster = cg::this_cluster();
 
-  constexpr int CO_TILES = C / COT;
-  const int bid = blockIdx.x;
-  const int cot = bid % CO_TILES;
-  const int ptile = bid / CO_TILES;                 // pixel tile index
+  const int ptile = blockIdx.x;                     // pixel tile index
+  const int cot = blockIdx.y;
   const int rt = ptile % K::TILES_PER_N;
   const int n0 = (ptile / K::TILES_PER_N) * K::NIMG;
   const int y0 = rt * K::IR;
@@ -321,8 +336,7 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* __r
     }
   }
 
-  // combine the pixel splits in a fixed order, then write the CTA's partial
-  // [co][r][s][ci] slice (co in the tile) contiguously
+  // 1. the CTA's partial [co][r][s][ci] (co in the tile), pixel splits in order
   float* red = xs;
   __syncthreads();
 #pragma unroll 1
@@ -343,66 +357,101 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* __r
     }
     __syncthreads();
   }
-  float4* out = reinterpret_cast<float4*>(part + size_t(ptile) * 9 * C * C + size_t(co0) * 9 * C);
-  for (int i = tid; i < K::RED / 4; i += K::THREADS) out[i] = reinterpret_cast<const float4*>(red)[i];
-}
 
-// out[i] = sum_t part[t][i]: a CTA owns 4 float4 columns x 64 tile groups;
-// fixed summation order (per-thread strided partial sums, then the 64 groups)
-constexpr int kRedCols = 4, kRedGroups = 64;
-__global__ void __launch_bounds__(kRedCols * kRedGroups)
-k_wgrad_reduce(const float4* __restrict__ part, float4* __restrict__ out, int cols4, int tiles) {
-  __shared__ float4 sm[kRedGroups][kRedCols];
-  const int lc = threadIdx.x % kRedCols, g = threadIdx.x / kRedCols;
-  const int c = blockIdx.x * kRedCols + lc;
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (c < cols4) {
+  // 2. cluster rank k: slice k summed over the cluster's CTAs (DSMEM, rank order)
+  cluster.sync();
+  const int cl = int(cluster.num_blocks());         // 1, 2, 4 or 8 (launch_wgrad)
+  const int slice4 = K::RED / 4 / cl;               // float4s of the partial per cluster rank
+  const int k = int(cluster.block_rank());
+  const int cid = ptile / cl, nclusters = gridDim.x / cl;
+  float4* cpart = reinterpret_cast<float4*>(part + size_t(cid) * 9 * C * C + size_t(co0) * 9 * C) + k * slice4;
+  for (int i = tid; i < slice4; i += K::THREADS) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-    for (int t = g; t < tiles; t += kRedGroups) {
-      const float4 v = __ldg(part + size_t(t) * cols4 + c);
+    for (int q = 0; q < cl; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(cluster.map_shared_rank(red, q))[k * slice4 + i];
       a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
     }
+    __stcg(cpart + i, a);
   }
-  sm[g][lc] = a;
-  __syncthreads();
-  if (g == 0 && c < cols4) {
-    float4 s = sm[0][lc];
+  __threadfence();
+  cluster.sync();                                   // every slice written (and every DSMEM read done)
+  if (k == 0 && tid == 0) {
+    const unsigned old = atomicAdd(arrivals + cot, 1u);
+    s_last = old == unsigned(nclusters - 1);
+  }
+  cluster.sync();
+  const int last = *cluster.map_shared_rank(&s_last, 0);
+  cluster.sync();                                   // rank 0's s_last read by all before it may exit
+  if (!last) return;
+
+  // 3. the last cluster: dW slice k = sum over clusters in order
+  __threadfence();
+  const float4* all = reinterpret_cast<const float4*>(part + size_t(co0) * 9 * C) + k * slice4;
+  float4* out = reinterpret_cast<float4*>(dw + size_t(co0) * 9 * C) + k * slice4;
+  constexpr int CC4 = 9 * C * C / 4;                 // float4 stride between cluster partials
+  for (int i = tid; i < slice4; i += K::THREADS) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-    for (int k = 1; k < kRedGroups; ++k) {
-      const float4 v = sm[k][lc];
-      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    for (int c = 0; c < nclusters; ++c) {
+      const float4 v = __ldcg(all + size_t(c) * CC4 + i);
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
     }
-    out[c] = s;
+    out[i] = a;
   }
+  if (k == 0 && tid == 0) arrivals[cot] = 0u;       // ready for the next launch on this stream
 }
 
-template <int C, int H, int TH, int COT, int PS>
+template <int C, int H, int TH, int COT, int PS, int CLMAX>
 size_t wgrad_tiles(int n) {
-  using K = WgradCfg<C, H, TH, COT, PS>;
+  using K = WgradCfg<C, H, TH, COT, PS, CLMAX>;
   return size_t(n / K::NIMG) * K::TILES_PER_N;
 }
 
-template <int C, int H, int TH, int COT, int PS>
-int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes, int n,
-                 cudaStream_t st) {
-  using K = WgradCfg<C, H, TH, COT, PS>;
+// CTAs per cluster: the largest power of two <= clmax dividing the tile count
+inline int wgrad_cluster(size_t tiles, int clmax) {
+  int cl = clmax;
+  while (cl > 1 && tiles % cl) cl /= 2;
+  return cl;
+}
+
+template <int C, int H, int TH, int COT, int PS, int CLMAX>
+size_t wgrad_partials(int n) {
+  const size_t tiles = wgrad_tiles<C, H, TH, COT, PS, CLMAX>(n);
+  return tiles / wgrad_cluster(tiles, CLMAX);
+}
+
+template <int C, int H, int TH, int COT, int PS, int CLMAX>
+int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes, unsigned* arrivals,
+                 int n, cudaStream_t st) {
+  using K = WgradCfg<C, H, TH, COT, PS, CLMAX>;
+  const size_t tiles = wgrad_tiles<C, H, TH, COT, PS, CLMAX>(n);
   if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: batch %d not a multiple of %d", n, K::NIMG);
-  const size_t tiles = wgrad_tiles<C, H, TH, COT, PS>(n);
-  if (ws_bytes < tiles * 9 * C * C * sizeof(float))
-    return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: workspace %zu B < %zu B", ws_bytes,
-                   tiles * 9 * C * C * sizeof(float));
-  auto kern = k_wgrad3x3<C, H, TH, COT, PS>;
+  if (!arrivals) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: null arrival counters");
+  const size_t need = wgrad_partials<C, H, TH, COT, PS, CLMAX>(n) * 9 * C * C * sizeof(float);
+  if (ws_bytes < need)
+    return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: workspace %zu B < %zu B", ws_bytes, need);
+  auto kern = k_wgrad3x3<C, H, TH, COT, PS, CLMAX>;
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+    if (CLMAX > 8) CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
-  kern<<<unsigned(tiles * (C / COT)), K::THREADS, K::SMEM, st>>>(x, dy, ws);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(tiles), C / COT, 1);
+  cfg.blockDim = dim3(K::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = K::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(wgrad_cluster(tiles, CLMAX));
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, x, dy, ws, dw, arrivals));
   LAUNCH_CHECK("k_wgrad3x3");
-  const int cols4 = 9 * C * C / 4;
-  k_wgrad_reduce<<<(cols4 + kRedCols - 1) / kRedCols, kRedCols * kRedGroups, 0, st>>>(reinterpret_cast<const float4*>(ws),
-                                                 reinterpret_cast<float4*>(dw), cols4, int(tiles));
-  LAUNCH_CHECK("k_wgrad_reduce");
   return 0;
 }
 
@@ -410,7 +459,7 @@ int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t w
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
 using ConvFn = int (*)(const float*, const float*, float*, int, bool, cudaStream_t);
-using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, int, cudaStream_t);
+using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsigned*, int, cudaStream_t);
 using TilesFn = size_t (*)(int);
 
 //                     C   H  TH COT PX CO U
@@ -420,32 +469,43 @@ const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 1
                           launch_conv<32, 16, 4, 32, 2, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
 const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 8, 16, 2, 8, 1>,
                           launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 8, 32, 2, 8, 2>};
-//                        C   H  TH COT PS
-const WgradFn kWg16[] = {launch_wgrad<16, 32, 8, 16, 2>, launch_wgrad<16, 32, 8, 16, 4>,
-                         launch_wgrad<16, 32, 16, 16, 4>, launch_wgrad<16, 32, 4, 16, 2>};
-const TilesFn kWt16[] = {wgrad_tiles<16, 32, 8, 16, 2>, wgrad_tiles<16, 32, 8, 16, 4>,
-                         wgrad_tiles<16, 32, 16, 16, 4>, wgrad_tiles<16, 32, 4, 16, 2>};
-const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1>, launch_wgrad<32, 16, 8, 16, 2>,
-                         launch_wgrad<32, 16, 4, 32, 1>, launch_wgrad<32, 16, 16, 32, 2>};
-const TilesFn kWt32[] = {wgrad_tiles<32, 16, 8, 32, 1>, wgrad_tiles<32, 16, 8, 16, 2>,
-                         wgrad_tiles<32, 16, 4, 32, 1>, wgrad_tiles<32, 16, 16, 32, 2>};
-const WgradFn kWg64[] = {launch_wgrad<64, 8, 8, 32, 1>, launch_wgrad<64, 8, 8, 16, 1>,
-                         launch_wgrad<64, 8, 8, 16, 2>, launch_wgrad<64, 8, 8, 8, 1>};
-const TilesFn kWt64[] = {wgrad_tiles<64, 8, 8, 32, 1>, wgrad_tiles<64, 8, 8, 16, 1>,
-                         wgrad_tiles<64, 8, 8, 16, 2>, wgrad_tiles<64, 8, 8, 8, 1>};
+//                        C   H  TH COT PS CL
+const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32, 16, 16, 4, 16>,
+                         launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
+const TilesFn kWt16[] = {wgrad_partials<16, 32, 16, 16, 4, 8>, wgrad_partials<16, 32, 16, 16, 4, 16>,
+                         wgrad_partials<16, 32, 8, 16, 2, 16>, wgrad_partials<16, 32, 8, 16, 2, 8>};
+const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1, 8>, launch_wgrad<32, 16, 8, 32, 1, 16>,
+                         launch_wgrad<32, 16, 16, 32, 2, 8>, launch_wgrad<32, 16, 16, 32, 2, 16>};
+const TilesFn kWt32[] = {wgrad_partials<32, 16, 8, 32, 1, 8>, wgrad_partials<32, 16, 8, 32, 1, 16>,
+                         wgrad_partials<32, 16, 16, 32, 2, 8>, wgrad_partials<32, 16, 16, 32, 2, 16>};
+const WgradFn kWg64[] = {launch_wgrad<64, 8, 8, 8, 1, 8>, launch_wgrad<64, 8, 8, 8, 1, 16>,
+                         launch_wgrad<64, 8, 8, 32, 1, 8>, launch_wgrad<64, 8, 8, 16, 1, 16>};
+const TilesFn kWt64[] = {wgrad_partials<64, 8, 8, 8, 1, 8>, wgrad_partials<64, 8, 8, 8, 1, 16>,
+                         wgrad_partials<64, 8, 8, 32, 1, 8>, wgrad_partials<64, 8, 8, 16, 1, 16>};
 
-int env_variant(const char* name) {
+// "i" (every shape) or "i,j,k" (C = 16, 32, 64)
+int env_variant(const char* name, int which) {
   const char* v = std::getenv(name);
-  const int i = v ? std::atoi(v) : 0;
+  if (!v) return 0;
+  int i = std::atoi(v);
+  for (int k = 0; k < which; ++k) {
+    const char* comma = std::strchr(v, ',');
+    if (!comma) break;
+    v = comma + 1;
+    i = std::atoi(v);
+  }
   return i < 0 || i > 3 ? 0 : i;
 }
-int conv_variant() {
-  static const int v = env_variant("LPP_CONV_VARIANT");
-  return v;
+int shape_index(int c) { return c == 16 ? 0 : c == 32 ? 1 : 2; }
+int conv_variant(int c) {
+  static const int v[3] = {env_variant("LPP_CONV_VARIANT", 0), env_variant("LPP_CONV_VARIANT", 1),
+                           env_variant("LPP_CONV_VARIANT", 2)};
+  return v[shape_index(c)];
 }
-int wgrad_variant() {
-  static const int v = env_variant("LPP_WGRAD_VARIANT");
-  return v;
+int wgrad_variant(int c) {
+  static const int v[3] = {env_variant("LPP_WGRAD_VARIANT", 0), env_variant("LPP_WGRAD_VARIANT", 1),
+                           env_variant("LPP_WGRAD_VARIANT", 2)};
+  return v[shape_index(c)];
 }
 
 }  // namespace
@@ -459,7 +519,7 @@ extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, 
   if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
   auto st = static_cast<cudaStream_t>(stream);
-  const int v = conv_variant();
+  const int v = conv_variant(c);
   if (c == 16 && hw == 32) return kConv16[v](x, w, y, n, dgrad != 0, st);
   if (c == 32 && hw == 16) return kConv32[v](x, w, y, n, dgrad != 0, st);
   if (c == 64 && hw == 8) return kConv64[v](x, w, y, n, dgrad != 0, st);
@@ -468,7 +528,7 @@ extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, 
 
 extern "C" size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw) {
   if (n <= 0) return 0;
-  const int v = wgrad_variant();
+  const int v = wgrad_variant(c);
   if (c == 16 && hw == 32) return kWt16[v](n) * 9 * c * c * sizeof(float);
   if (c == 32 && hw == 16) return kWt32[v](n) * 9 * c * c * sizeof(float);
   if (c == 64 && hw == 8) return kWt64[v](n) * 9 * c * c * sizeof(float);
@@ -476,13 +536,13 @@ extern "C" size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw) {
 }
 
 extern "C" int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
-                                     int n, int c, int hw, void* stream) {
+                                     uint32_t* arrivals, int n, int c, int hw, void* stream) {
   if (!x || !dy || !dw || !ws) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: batch %d", n);
   auto st = static_cast<cudaStream_t>(stream);
-  const int v = wgrad_variant();
-  if (c == 16 && hw == 32) return kWg16[v](x, dy, dw, ws, ws_bytes, n, st);
-  if (c == 32 && hw == 16) return kWg32[v](x, dy, dw, ws, ws_bytes, n, st);
-  if (c == 64 && hw == 8) return kWg64[v](x, dy, dw, ws, ws_bytes, n, st);
+  const int v = wgrad_variant(c);
+  if (c == 16 && hw == 32) return kWg16[v](x, dy, dw, ws, ws_bytes, arrivals, n, st);
+  if (c == 32 && hw == 16) return kWg32[v](x, dy, dw, ws, ws_bytes, arrivals, n, st);
+  if (c == 64 && hw == 8) return kWg64[v](x, dy, dw, ws, ws_bytes, arrivals, n, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: no kernel for C=%d H=W=%d", c, hw);
 }

@@ -30,7 +30,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
-from .conv import Conv3x3
+from .conv import Conv3x3, mark_weight_grads
 from .partition import Block
 
 
@@ -134,6 +134,8 @@ class ArenaObjective:
         g = torch.zeros_like(xp)
         bound = self.bind(xp, g)
         idx = torch.as_tensor(np.asarray(batch), device=device, dtype=torch.long)
+        if getattr(bound, "module", None) is not None:
+            mark_weight_grads(bound.module, bound.params[first:last + 1])
         loss = self.loss_on(bound, self.features_on(device)[idx], self.labels_on(device)[idx])
         grads = torch.autograd.grad(loss, bound.params[first:last + 1])
         torch._foreach_copy_(bound.grad_views[first:last + 1], list(grads))

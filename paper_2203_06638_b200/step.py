@@ -23,6 +23,7 @@ import threading
 
 import torch
 
+from .conv import mark_weight_grads
 from .partition import Block
 
 # kernels of this library launched from inside replayed step graphs (the
@@ -168,6 +169,9 @@ class StepProgram:
         else:
             xb = self.feats.index_select(0, self.idx)
             yb = self.labels.index_select(0, self.idx)
+        module = getattr(self.bound, "module", None)
+        if module is not None:
+            mark_weight_grads(module, self.leaves[bid])
         loss = self.obj.loss_on(self.bound, xb, yb)
         if self.grad_mode == "copy":
             grads = torch.autograd.grad(loss, self.leaves[bid])

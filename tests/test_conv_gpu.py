@@ -109,7 +109,7 @@ def test_conv3x3_routes_other_cases_to_cudnn(monkeypatch):
 
     calls = []
     real = conv.conv3x3
-    monkeypatch.setattr(conv, "conv3x3", lambda x, w: calls.append(1) or real(x, w))
+    monkeypatch.setattr(conv, "conv3x3", lambda *a: calls.append(1) or real(*a))
     x16 = torch.randn(2, 16, 16, 16, device="cuda").to(memory_format=CL)   # (16, 16): no kernel
     m = Conv3x3(16, 16, 1).cuda().to(memory_format=CL)
     assert torch.allclose(m(x16), F.conv2d(x16, m.weight, padding=1), atol=1e-5)
@@ -156,3 +156,55 @@ def test_conv_rejects_unsupported_shape():
     with pytest.raises(ValueError, match="no kernel"):
         conv.conv_fwd(x, w)
     assert N.lib.lpp_conv3x3_wgrad_workspace(2, 16, 16) == 0
+
+
+def test_wgrad_arrival_cells_reused_stay_zero():
+    """One launch per weight gradient: the last cluster resets the arrival
+    counters, so a set reused by stream-ordered calls gives the same bits."""
+    from paper_2203_06638_b200 import conv
+
+    for c, hw in SHAPES:
+        x, w, gy = _data(c, hw, 32, seed=4)
+        cells = conv.arrival_cells("cuda")
+        outs = [conv.conv_wgrad(x, gy, w, cells) for _ in range(4)]
+        assert all(torch.equal(outs[0], o) for o in outs[1:])
+        assert int(cells.abs().sum()) == 0
+        _, _, gw_ref = _ref(x, w, gy)
+        assert _rel(outs[0], gw_ref) < TOL
+
+
+def test_partial_backprop_skips_unneeded_kernels():
+    """autograd.grad over a subset of weights (a PASSM+ block): layers above
+    the block run dgrad only, the block's input-most layer no dgrad."""
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200 import conv
+    from paper_2203_06638_b200.conv import Conv3x3
+
+    torch.manual_seed(1)
+    seq = torch.nn.Sequential(Conv3x3(16, 16), torch.nn.ReLU(), Conv3x3(16, 16)).cuda().to(memory_format=CL)
+    x = torch.randn(4, 16, 32, 32, device="cuda").to(memory_format=CL)
+    c1, c2 = seq[0], seq[2]
+
+    def grads(targets):
+        conv.mark_weight_grads(seq, targets)
+        y = seq(x)
+        torch.cuda.synchronize()
+        l0 = N.launch_count()
+        g = torch.autograd.grad((y * y).sum(), targets)
+        torch.cuda.synchronize()
+        return g, N.launch_count() - l0
+
+    (g2,), n2 = grads([c2.weight])
+    assert n2 == 1                         # conv2 wgrad only
+    (g1,), n1 = grads([c1.weight])
+    assert n1 == 2                         # conv2 dgrad + conv1 wgrad
+    (a1, a2), n12 = grads([c1.weight, c2.weight])
+    assert n12 == 3
+    xd = x.double()
+    w1 = c1.weight.detach().double().requires_grad_()
+    w2 = c2.weight.detach().double().requires_grad_()
+    yd = F.conv2d(F.relu(F.conv2d(xd, w1, padding=1)), w2, padding=1)
+    r1, r2 = torch.autograd.grad((yd * yd).sum(), [w1, w2])
+    for got, ref in ((g1, r1), (g2, r2), (a1, r1), (a2, r2)):
+        assert _rel(got, ref) < TOL
+    conv.mark_weight_grads(seq, list(seq.parameters()))
