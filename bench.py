@@ -210,6 +210,58 @@ def build_cfg(obj, steps_slots: int, algo: str = "lpp_sgd", workers: int = 1, sa
         momentum=0.9, weight_decay=5e-4, sampling=sampling, evaluate=False, record_mode="off")
 
 
+def conv_roofline(N) -> dict:
+    """The fp32 3x3 convolution kernels (csrc/conv_f32.cu) — most of the
+    fp32 step's kernel time — against the FFMA peak measured here
+    (lpp_fma_probe): each kernel launched standalone at B = 128 on the
+    ResNet-20 shapes, CUDA events, weighted by its launches per minibatch
+    (6 / 5 / 5 convolutions x forward, dgrad, wgrad).  Algorithmic flops:
+    2 x B x H x W x C x C x 9 per launch."""
+    import torch
+
+    from paper_2203_06638_b200 import conv
+
+    def timed(fn, n=30):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    sink = torch.empty(148 * 8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    iters = 2000
+    ms = timed(lambda: N.check(N.lib.lpp_fma_probe(sink.data_ptr(), 148 * 8, iters, stream), "fma_probe"), 5)
+    peak = 148 * 8 * 256 * iters * 128 * 2 / (ms / 1e3) / 1e12
+    B, rows, tot_f, tot_ms = 128, [], 0.0, 0.0
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for c, hw, cnt in ((16, 32, 6), (32, 16, 5), (64, 8, 5)):
+        x = torch.randn(B, c, hw, hw, device="cuda", generator=g).to(memory_format=torch.channels_last)
+        w = torch.randn(c, c, 3, 3, device="cuda", generator=g).to(memory_format=torch.channels_last)
+        cells = conv.arrival_cells("cuda")
+        flop = 2.0 * B * hw * hw * c * c * 9
+        for kind, fn in (("fwd", lambda: conv.conv_fwd(x, w)), ("dgrad", lambda: conv.conv_fwd(x, w, dgrad=True)),
+                         ("wgrad", lambda: conv.conv_wgrad(x, x, w, cells))):
+            t = timed(fn)
+            rows.append({"c": c, "hw": hw, "pass": kind, "us": round(1e3 * t, 2),
+                         "tflops": round(flop / (t / 1e3) / 1e12, 2)})
+            tot_f += cnt * flop
+            tot_ms += cnt * t
+    ach = tot_f / (tot_ms / 1e3) / 1e12
+    return {"bound": "fp32 FFMA (no tensor cores: TF32 is below the reference arm's precision)",
+            "kernel": "k_conv3x3 (forward / dgrad) + k_wgrad3x3, 16 stride-1 3x3 convolutions",
+            "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "peak_src": "measured: lpp_fma_probe (148 x 8 CTAs x 256 threads of dependent-chain FFMA)",
+            "flops_per_launch": "2 x 128 x H x W x C x C x 9", "per_kernel": rows,
+            "note": "standalone, B = 128, weighted by launches per full-backprop minibatch; in the step "
+                    "these kernels are ~49 % of the kernel time (profiles/r2_bench_trace_share.txt)"}
+
+
 def ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -362,6 +414,8 @@ def ours(args) -> None:
                              "resnet18 / resnet50 apply_roofline for the HBM-sized arenas"},
     }
     line["clocks"] = facts["clocks"]
+    if os.environ.get("LPP_CONV", "native") != "cudnn":
+        line["roofline_conv"] = conv_roofline(N)
 
     # ---------------- end to end (host buffers), fp32 ----------------
     if not args.no_e2e:

@@ -596,6 +596,10 @@ int lpp_fill_i32(int32_t* p, size_t n, int32_t v, void* stream);
  * arena's channels_last view).  Shapes with a kernel: (c, hw) in
  * {(16, 32), (32, 16), (64, 8)}. */
 int lpp_conv3x3_supported(int c, int hw);
+/* measurement utility: blocks x 256 threads x iters x 128 dependent-chain
+ * FFMAs (8 chains per thread), no memory traffic — the fp32 FMA peak the
+ * convolutions' roofline divides by (2 flops per FFMA) */
+int lpp_fma_probe(float* out, int blocks, int iters, void* stream);
 /* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x */
 int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
                     void* stream);

@@ -218,6 +218,7 @@ _SIGS = {
     "lpp_averager_run": (_c.c_int, [_c.POINTER(AveragerCfg), _c.POINTER(_c.c_int64)]),
     "lpp_fill_i32": (_c.c_int, [_vp, _size, _c.c_int32, _vp]),
     "lpp_conv3x3_supported": (_c.c_int, [_c.c_int, _c.c_int]),
+    "lpp_fma_probe": (_c.c_int, [_vp, _c.c_int, _c.c_int, _vp]),
     "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp]),
     "lpp_conv3x3_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _vp, _c.c_int, _c.c_int, _c.c_int, _vp]),

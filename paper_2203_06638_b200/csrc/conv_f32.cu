@@ -508,7 +508,32 @@ int wgrad_variant(int c) {
   return v[shape_index(c)];
 }
 
+// FFMA peak probe: 8 independent fma chains per thread, no memory traffic
+// in the loop (the denominator of the convolutions' roofline)
+__global__ void __launch_bounds__(256) k_fma_probe(float* out, int iters, float a, float b) {
+  float v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = threadIdx.x * 1e-7f + k;
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = fmaf(v[k], a, b);
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += v[k];
+  if (s == 1234.5f) out[blockIdx.x] = s;       // keeps the chains live
+}
+
 }  // namespace
+
+extern "C" int lpp_fma_probe(float* out, int blocks, int iters, void* stream) {
+  if (!out || blocks <= 0 || iters <= 0) return set_err(LPP_E_VALUE, "lpp_fma_probe: bad argument");
+  k_fma_probe<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(out, iters, 0.999999f, 1e-6f);
+  LAUNCH_CHECK("k_fma_probe");
+  return 0;
+}
 
 extern "C" int lpp_conv3x3_supported(int c, int hw) {
   return (c == 16 && hw == 32) || (c == 32 && hw == 16) || (c == 64 && hw == 8);

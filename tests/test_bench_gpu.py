@@ -41,3 +41,7 @@ def test_bench_line_contract():
     # the headline is at the reference arm's precision; bf16 is a labelled extra
     assert d["dtype"] == "f32" and d["config"]["conv_compute"].startswith("fp32")
     assert d["value_bf16"] > 0 and d["e2e_bf16"]["value"] > 0
+    # the step's dominant kernels: the fp32 convolutions vs the measured FFMA peak
+    rc = d["roofline_conv"]
+    assert rc["unit"] == "TFLOP/s" and 50 < rc["peak"] < 100 and 0.1 < rc["frac"] < 1.0
+    assert d["gpu_launches_split"]["in_graph"] > 0
