@@ -612,6 +612,17 @@ size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
  * call and left zero by every call; one set per stream (launches sharing a
  * set must be stream-ordered). */
 #define LPP_CONV_ARRIVALS 8
+
+/* 1x1 stride-2 projection shortcuts (ci -> co, hw_in -> hw_in / 2) at
+ * CIFAR ResNet-20's shapes {(16, 32, 32), (32, 64, 16)}.
+ * mode 0: out = y  of (a = x [n][hw][hw][ci], b = w [co][ci]);
+ * mode 1: out = dX of (a = dY [n][hw/2][hw/2][co], b = w);
+ * mode 2: out = dW of (a = x, b = dY), one launch, deterministic (as
+ *         lpp_conv3x3_wgrad_f32; ws / arrivals used only here). */
+int lpp_conv1x1s2_supported(int ci, int co, int hw_in);
+size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in);
+int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
+                      float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream);
 int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
                           uint32_t* arrivals, int n, int c, int hw, void* stream);
 

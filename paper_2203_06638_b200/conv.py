@@ -96,6 +96,56 @@ def _will_run(node) -> bool:
         return True
 
 
+def conv1x1s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
+              arrivals: torch.Tensor | None = None) -> torch.Tensor:
+    """The projection shortcut's kernels: mode 0 y = conv(x, w); 1 dX of
+    dY = x; 2 dW of (x, dY = other)."""
+    N = _lib()
+    co, ci = w.shape[0], w.shape[1]
+    x = x.contiguous(memory_format=_CL)
+    w = _ohwi(w)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    if mode == 0:
+        n, _, hw, _ = x.shape
+        out = torch.empty((n, co, hw // 2, hw // 2), device=x.device, memory_format=_CL)
+        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, None, 0,
+                                        None, stream), "conv1x1s2_f32")
+    elif mode == 1:
+        n, _, ho, _ = x.shape
+        out = torch.empty((n, ci, 2 * ho, 2 * ho), device=x.device, memory_format=_CL)
+        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, 2 * ho, 1, None, 0,
+                                        None, stream), "conv1x1s2_f32")
+    else:
+        n, _, hw, _ = x.shape
+        dy = other.contiguous(memory_format=_CL)
+        out = torch.empty_like(w, memory_format=_CL)
+        nbytes = int(N.lib.lpp_conv1x1s2_wgrad_workspace(n, ci, co, hw))
+        ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
+        if arrivals is None:
+            arrivals = arrival_cells(x.device)
+        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), dy.data_ptr(), out.data_ptr(), n, ci, co, hw, 2,
+                                        ws.data_ptr(), nbytes, arrivals.data_ptr(), stream), "conv1x1s2_f32")
+    return out
+
+
+class _Conv1x1s2Fn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, arrivals, want_w):
+        ctx.save_for_backward(x, w)
+        ctx.arrivals, ctx.want_w = arrivals, want_w
+        return conv1x1s2(x, w, 0)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        gx = gw = None
+        if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
+            gx = conv1x1s2(gy, w, 1)
+        if ctx.needs_input_grad[1] and ctx.want_w:
+            gw = conv1x1s2(x, w, 2, gy, ctx.arrivals)
+        return gx, gw, None, None
+
+
 class _Conv3x3Fn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, arrivals, want_w):
@@ -129,7 +179,7 @@ def mark_weight_grads(module: nn.Module, leaves) -> None:
     block's leaves): the others skip their weight-gradient kernels."""
     ids = {id(p) for p in leaves}
     for m in module.modules():
-        if isinstance(m, Conv3x3):
+        if isinstance(m, (Conv3x3, Conv1x1)):
             m.want_w = id(m.weight) in ids
 
 
@@ -149,4 +199,24 @@ class Conv3x3(nn.Conv2d):
             if self._arrivals is None or self._arrivals.device != x.device:
                 self._arrivals = arrival_cells(x.device)
             return conv3x3(x, self.weight, self._arrivals, self.want_w)
+        return F.conv2d(x, self.weight, None, self.stride, self.padding)
+
+
+class Conv1x1(nn.Conv2d):
+    """nn.Conv2d(cin, cout, 1, stride, bias=False) — the projection shortcut —
+    with the native fp32 path for stride 2 at the shapes with a kernel."""
+
+    def __init__(self, cin: int, cout: int, stride: int = 1):
+        super().__init__(cin, cout, 1, stride, 0, bias=False)
+        self.want_w = True
+        self._arrivals = None
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if (x.dtype == torch.float32 and x.is_cuda and self.weight.dtype == torch.float32
+                and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled()
+                and self.stride[0] == 2 and self.stride[1] == 2
+                and _lib().lib.lpp_conv1x1s2_supported(self.in_channels, self.out_channels, x.shape[2])):
+            if self._arrivals is None or self._arrivals.device != x.device:
+                self._arrivals = arrival_cells(x.device)
+            return _Conv1x1s2Fn.apply(x, self.weight, self._arrivals, self.want_w)
         return F.conv2d(x, self.weight, None, self.stride, self.padding)

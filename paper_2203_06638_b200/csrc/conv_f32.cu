@@ -77,6 +77,60 @@ __device__ __forceinline__ void stage_rows(const float* __restrict__ x, float* x
   }
 }
 
+// Cross-CTA reduction of weight-gradient partials in one launch, in a fixed
+// order (deterministic):
+//   cluster rank k sums slice k of its cluster's CTA partials over DSMEM (rank
+//   order) into the cluster's partial in the workspace; the last cluster to
+//   arrive (per arrival counter, left at 0 for the next launch) sums the
+//   cluster partials in cluster order into dw.
+// red: this CTA's partial in shared memory (red4 float4s) covering float4s
+// [off4, off4 + red4) of a gradient of total4 float4s; part: [clusters][total4].
+template <int THREADS>
+__device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, const float* red, int red4,
+                                                    size_t off4, int total4, float* part, float* dw,
+                                                    unsigned* arrival, int tile) {
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  cluster.sync();
+  const int cl = int(cluster.num_blocks());
+  const int slice4 = red4 / cl;
+  const int k = int(cluster.block_rank());
+  const int cid = tile / cl, nclusters = gridDim.x / cl;
+  float4* cpart = reinterpret_cast<float4*>(part) + size_t(cid) * total4 + off4 + k * slice4;
+  for (int i = tid; i < slice4; i += THREADS) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int q = 0; q < cl; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(cluster.map_shared_rank(red, q))[k * slice4 + i];
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    }
+    __stcg(cpart + i, a);
+  }
+  __threadfence();
+  cluster.sync();                                   // every slice written (and every DSMEM read done)
+  if (k == 0 && tid == 0) {
+    const unsigned old = atomicAdd(arrival, 1u);
+    s_last = old == unsigned(nclusters - 1);
+  }
+  cluster.sync();
+  const int last = *cluster.map_shared_rank(&s_last, 0);
+  cluster.sync();                                   // rank 0's s_last read by all before it may exit
+  if (!last) return;
+  __threadfence();
+  const float4* all = reinterpret_cast<const float4*>(part) + off4 + k * slice4;
+  float4* out = reinterpret_cast<float4*>(dw) + off4 + k * slice4;
+  for (int i = tid; i < slice4; i += THREADS) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int c = 0; c < nclusters; ++c) {
+      const float4 v = __ldcg(all + size_t(c) * total4 + i);
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    }
+    out[i] = a;
+  }
+  if (k == 0 && tid == 0) *arrival = 0u;            // ready for the next launch on this stream
+}
+
 // ---------------------------------------------------------------------------
 // forward / dgrad
 
@@ -271,7 +325,6 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* par
   using K = WgradCfg<C, H, TH, COT, PS, CLMAX>;
   constexpr int W = K::W, CP = K::CP, DP = K::DP;
   extern __shared__ float4 smem4[];
-  __shared__ int s_last;
   float* xs = reinterpret_cast<float*>(smem4);
   float* ds = xs + K::XS;
   cg::cluster_group cluster = cg::this_cluster();
@@ -358,48 +411,8 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* par
     __syncthreads();
   }
 
-  // 2. cluster rank k: slice k summed over the cluster's CTAs (DSMEM, rank order)
-  cluster.sync();
-  const int cl = int(cluster.num_blocks());         // 1, 2, 4 or 8 (launch_wgrad)
-  const int slice4 = K::RED / 4 / cl;               // float4s of the partial per cluster rank
-  const int k = int(cluster.block_rank());
-  const int cid = ptile / cl, nclusters = gridDim.x / cl;
-  float4* cpart = reinterpret_cast<float4*>(part + size_t(cid) * 9 * C * C + size_t(co0) * 9 * C) + k * slice4;
-  for (int i = tid; i < slice4; i += K::THREADS) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int q = 0; q < cl; ++q) {
-      const float4 v = reinterpret_cast<const float4*>(cluster.map_shared_rank(red, q))[k * slice4 + i];
-      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-    }
-    __stcg(cpart + i, a);
-  }
-  __threadfence();
-  cluster.sync();                                   // every slice written (and every DSMEM read done)
-  if (k == 0 && tid == 0) {
-    const unsigned old = atomicAdd(arrivals + cot, 1u);
-    s_last = old == unsigned(nclusters - 1);
-  }
-  cluster.sync();
-  const int last = *cluster.map_shared_rank(&s_last, 0);
-  cluster.sync();                                   // rank 0's s_last read by all before it may exit
-  if (!last) return;
-
-  // 3. the last cluster: dW slice k = sum over clusters in order
-  __threadfence();
-  const float4* all = reinterpret_cast<const float4*>(part + size_t(co0) * 9 * C) + k * slice4;
-  float4* out = reinterpret_cast<float4*>(dw + size_t(co0) * 9 * C) + k * slice4;
-  constexpr int CC4 = 9 * C * C / 4;                 // float4 stride between cluster partials
-  for (int i = tid; i < slice4; i += K::THREADS) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int c = 0; c < nclusters; ++c) {
-      const float4 v = __ldcg(all + size_t(c) * CC4 + i);
-      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-    }
-    out[i] = a;
-  }
-  if (k == 0 && tid == 0) arrivals[cot] = 0u;       // ready for the next launch on this stream
+  cluster_tail_reduce<K::THREADS>(cluster, red, K::RED / 4, size_t(co0) * 9 * C / 4, 9 * C * C / 4, part, dw,
+                                  arrivals + cot, ptile);
 }
 
 template <int C, int H, int TH, int COT, int PS, int CLMAX>
@@ -453,6 +466,187 @@ int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t w
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, x, dy, ws, dw, arrivals));
   LAUNCH_CHECK("k_wgrad3x3");
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// 1x1 stride-2 projection shortcut: CI -> CO channels, input 2HO x 2HO,
+// output HO x HO (the ResNet-20 shortcuts 16->32 @32x32 and 32->64 @16x16).
+// Memory-bound: a thread owns one pixel x 8 channels, the weights sit in
+// shared memory and every lane of a warp reads the same ones (broadcast).
+
+template <int CI, int CO, int HO>
+__global__ void __launch_bounds__(256)
+k_conv1x1s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, int npix) {
+  __shared__ __align__(16) float ws[CI * CO];       // [ci][co]
+  for (int i = threadIdx.x; i < CI * CO; i += 256) {
+    const int co = i % CO, ci = i / CO;
+    ws[i] = __ldg(w + co * CI + ci);
+  }
+  __syncthreads();
+  constexpr int G = CO / 8, PPB = 32 * (8 / G);     // channel groups, pixels per CTA
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp % G;
+  const int p = blockIdx.x * PPB + (warp / G) * 32 + lane;
+  if (p >= npix) return;
+  const int xo = p % HO, yo = (p / HO) % HO, n = p / (HO * HO);
+  const float4* xin = reinterpret_cast<const float4*>(x + ((size_t(n) * 2 * HO + 2 * yo) * 2 * HO + 2 * xo) * CI);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c4 = 0; c4 < CI / 4; ++c4) {
+    const float4 v = __ldg(xin + c4);
+    const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 w0 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8);
+      const float4 w1 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8 + 4);
+      acc[0] = fmaf(xv[q], w0.x, acc[0]); acc[1] = fmaf(xv[q], w0.y, acc[1]);
+      acc[2] = fmaf(xv[q], w0.z, acc[2]); acc[3] = fmaf(xv[q], w0.w, acc[3]);
+      acc[4] = fmaf(xv[q], w1.x, acc[4]); acc[5] = fmaf(xv[q], w1.y, acc[5]);
+      acc[6] = fmaf(xv[q], w1.z, acc[6]); acc[7] = fmaf(xv[q], w1.w, acc[7]);
+    }
+  }
+  float4* out = reinterpret_cast<float4*>(y + size_t(p) * CO + g * 8);
+  out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// dX of the projection: dY (x) W at the even pixels, zero at the others
+template <int CI, int CO, int HO>
+__global__ void __launch_bounds__(256)
+k_conv1x1s2_dgrad(const float* __restrict__ dy, const float* __restrict__ w, float* __restrict__ dx, int npix_in) {
+  __shared__ __align__(16) float ws[CO * CI];       // [co][ci] (the OHWI layout)
+  for (int i = threadIdx.x; i < CO * CI / 4; i += 256)
+    reinterpret_cast<float4*>(ws)[i] = __ldg(reinterpret_cast<const float4*>(w) + i);
+  __syncthreads();
+  constexpr int G = CI / 8, PPB = 32 * (8 / G), HI = 2 * HO;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp % G;
+  const int p = blockIdx.x * PPB + (warp / G) * 32 + lane;
+  if (p >= npix_in) return;
+  const int xi = p % HI, yi = (p / HI) % HI, n = p / (HI * HI);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (((xi | yi) & 1) == 0) {
+    const float4* d = reinterpret_cast<const float4*>(dy + ((size_t(n) * HO + yi / 2) * HO + xi / 2) * CO);
+#pragma unroll 4
+    for (int c4 = 0; c4 < CO / 4; ++c4) {
+      const float4 v = __ldg(d + c4);
+      const float dv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 w0 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CI + g * 8);
+        const float4 w1 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CI + g * 8 + 4);
+        acc[0] = fmaf(dv[q], w0.x, acc[0]); acc[1] = fmaf(dv[q], w0.y, acc[1]);
+        acc[2] = fmaf(dv[q], w0.z, acc[2]); acc[3] = fmaf(dv[q], w0.w, acc[3]);
+        acc[4] = fmaf(dv[q], w1.x, acc[4]); acc[5] = fmaf(dv[q], w1.y, acc[5]);
+        acc[6] = fmaf(dv[q], w1.z, acc[6]); acc[7] = fmaf(dv[q], w1.w, acc[7]);
+      }
+    }
+  }
+  float4* out = reinterpret_cast<float4*>(dx + size_t(p) * CI + g * 8);
+  out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+// dW[co][ci] = sum_p dY[p][co] X[2p][ci]: a thread owns 4 co x 4 ci over a
+// strided subset of the CTA's pixels; splits combined in order in shared
+// memory, then the cluster reduction (cluster_tail_reduce)
+template <int CI, int CO, int HO, int PPC>
+__global__ void __launch_bounds__(256)
+k_conv1x1s2_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* part, float* __restrict__ dw,
+                  unsigned* __restrict__ arrivals) {
+  constexpr int T = (CO / 4) * (CI / 4), PS = 256 / T;
+  static_assert(256 % T == 0, "tile");
+  __shared__ __align__(16) float red[CO * CI];      // [co][ci]
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tid = threadIdx.x;
+  const int ci4 = tid % (CI / 4), co4 = (tid / (CI / 4)) % (CO / 4), ps = tid / T;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+  const int p0 = blockIdx.x * PPC;
+#pragma unroll 4
+  for (int pp = ps; pp < PPC; pp += PS) {
+    const int p = p0 + pp;
+    const int xo = p % HO, yo = (p / HO) % HO, n = p / (HO * HO);
+    const float4 d = __ldg(reinterpret_cast<const float4*>(dy + size_t(p) * CO) + co4);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(
+                             x + ((size_t(n) * 2 * HO + 2 * yo) * 2 * HO + 2 * xo) * CI) + ci4);
+    const float dv[4] = {d.x, d.y, d.z, d.w}, xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(dv[a], xv[c], acc[a][c]);
+  }
+#pragma unroll 1
+  for (int q = 0; q < PS; ++q) {
+    if (ps == q) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        float4* d = reinterpret_cast<float4*>(red + (co4 * 4 + a) * CI + ci4 * 4);
+        float4 v = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+        if (q > 0) {
+          const float4 o = *d;
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        *d = v;
+      }
+    }
+    __syncthreads();
+  }
+  cluster_tail_reduce<256>(cluster, red, CO * CI / 4, 0, CO * CI / 4, part, dw, arrivals, blockIdx.x);
+}
+
+template <int CI, int CO, int HO>
+constexpr int wg1x1_ppc() { return HO >= 16 ? 256 : 64; }
+
+template <int CI, int CO, int HO>
+int launch_conv1x1s2(const float* x, const float* w, float* y, int n, int mode, float* dw, float* ws,
+                     size_t ws_bytes, unsigned* arrivals, cudaStream_t st) {
+  if (mode == 0) {
+    const int npix = n * HO * HO;
+    constexpr int PPB = 32 * (8 / (CO / 8));
+    k_conv1x1s2<CI, CO, HO><<<(npix + PPB - 1) / PPB, 256, 0, st>>>(x, w, y, npix);
+    LAUNCH_CHECK("k_conv1x1s2");
+  } else if (mode == 1) {
+    const int npix = n * 4 * HO * HO;
+    constexpr int PPB = 32 * (8 / (CI / 8));
+    k_conv1x1s2_dgrad<CI, CO, HO><<<(npix + PPB - 1) / PPB, 256, 0, st>>>(x, w, y, npix);
+    LAUNCH_CHECK("k_conv1x1s2_dgrad");
+  } else {
+    constexpr int PPC = wg1x1_ppc<CI, CO, HO>();
+    const int npix = n * HO * HO;
+    if (npix % PPC) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: %d output pixels not a multiple of %d", npix, PPC);
+    if (!arrivals) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: null arrival counters");
+    const size_t ctas = size_t(npix / PPC);
+    const int cl = wgrad_cluster(ctas, 8);
+    const size_t need = ctas / cl * CO * CI * sizeof(float);
+    if (ws_bytes < need) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: workspace %zu B < %zu B", ws_bytes, need);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(ctas), 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(cl);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // mode 2: x = the forward input, y = dY
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_conv1x1s2_wgrad<CI, CO, HO, PPC>, x, static_cast<const float*>(y), ws, dw,
+                                arrivals));
+    LAUNCH_CHECK("k_conv1x1s2_wgrad");
+  }
+  return 0;
+}
+
+template <int CI, int CO, int HO>
+size_t conv1x1s2_workspace(int n) {
+  constexpr int PPC = wg1x1_ppc<CI, CO, HO>();
+  const size_t ctas = size_t(n) * HO * HO / PPC;
+  return ctas / wgrad_cluster(ctas, 8) * CO * CI * sizeof(float);
 }
 
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
@@ -570,4 +764,32 @@ extern "C" int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw,
   if (c == 32 && hw == 16) return kWg32[v](x, dy, dw, ws, ws_bytes, arrivals, n, st);
   if (c == 64 && hw == 8) return kWg64[v](x, dy, dw, ws, ws_bytes, arrivals, n, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_wgrad_f32: no kernel for C=%d H=W=%d", c, hw);
+}
+
+extern "C" int lpp_conv1x1s2_supported(int ci, int co, int hw_in) {
+  return (ci == 16 && co == 32 && hw_in == 32) || (ci == 32 && co == 64 && hw_in == 16);
+}
+
+extern "C" size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in) {
+  if (n <= 0) return 0;
+  if (ci == 16 && co == 32 && hw_in == 32) return conv1x1s2_workspace<16, 32, 16>(n);
+  if (ci == 32 && co == 64 && hw_in == 16) return conv1x1s2_workspace<32, 64, 8>(n);
+  return 0;
+}
+
+extern "C" int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in,
+                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream) {
+  if (!a || !b || !out) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: null pointer");
+  if (n <= 0 || mode < 0 || mode > 2) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: batch %d mode %d", n, mode);
+  auto st = static_cast<cudaStream_t>(stream);
+  // mode 0: out = y of (a = x, b = w); 1: out = dX of (a = dY, b = w); 2: out = dW of (a = x, b = dY)
+  if (ci == 16 && co == 32 && hw_in == 32)
+    return mode == 2 ? launch_conv1x1s2<16, 32, 16>(a, nullptr, const_cast<float*>(b), n, 2, out, ws, ws_bytes,
+                                                    arrivals, st)
+                     : launch_conv1x1s2<16, 32, 16>(a, b, out, n, mode, nullptr, nullptr, 0, nullptr, st);
+  if (ci == 32 && co == 64 && hw_in == 16)
+    return mode == 2 ? launch_conv1x1s2<32, 64, 8>(a, nullptr, const_cast<float*>(b), n, 2, out, ws, ws_bytes,
+                                                   arrivals, st)
+                     : launch_conv1x1s2<32, 64, 8>(a, b, out, n, mode, nullptr, nullptr, 0, nullptr, st);
+  return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: no kernel for %d->%d at %dx%d", ci, co, hw_in, hw_in);
 }

@@ -30,7 +30,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
-from .conv import Conv3x3, mark_weight_grads
+from .conv import Conv1x1, Conv3x3, mark_weight_grads
 from .partition import Block
 
 
@@ -344,8 +344,7 @@ class _Basic(nn.Module):
         self.bn2 = nn.BatchNorm2d(cout)
         self.shortcut = None
         if stride != 1 or cin != cout:
-            self.shortcut = nn.Sequential(nn.Conv2d(cin, cout, 1, stride, bias=False),
-                                          nn.BatchNorm2d(cout))
+            self.shortcut = nn.Sequential(Conv1x1(cin, cout, stride), nn.BatchNorm2d(cout))
 
     def forward(self, x):
         out = F.relu(self.bn1(self.conv1(x)))

@@ -208,3 +208,50 @@ def test_partial_backprop_skips_unneeded_kernels():
     for got, ref in ((g1, r1), (g2, r2), (a1, r1), (a2, r2)):
         assert _rel(got, ref) < TOL
     conv.mark_weight_grads(seq, list(seq.parameters()))
+
+
+SHAPES_1X1 = [(16, 32, 32), (32, 64, 16)]
+
+
+@pytest.mark.parametrize("ci,co,hw", SHAPES_1X1)
+@pytest.mark.parametrize("n", [1, 3, 128])
+def test_conv1x1s2_kernels_match_fp64(ci, co, hw, n):
+    """The projection shortcut (1x1, stride 2): forward, dX (zero at the
+    odd pixels), dW — against fp64."""
+    from paper_2203_06638_b200 import conv
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n, ci, hw, hw, device="cuda", generator=g).to(memory_format=CL)
+    w = (torch.randn(co, ci, 1, 1, device="cuda", generator=g) / ci ** 0.5).to(memory_format=CL)
+    gy = torch.randn(n, co, hw // 2, hw // 2, device="cuda", generator=g).to(memory_format=CL)
+    xd, wd, gyd = x.double(), w.double(), gy.double()
+    y_ref = F.conv2d(xd, wd, stride=2)
+    gx_ref, gw_ref, _ = torch.ops.aten.convolution_backward(gyd, xd, wd, None, (2, 2), (0, 0), (1, 1), False,
+                                                            (0, 0), 1, (True, True, False))
+    y = conv.conv1x1s2(x, w, 0)
+    gx = conv.conv1x1s2(gy, w, 1)
+    cells = conv.arrival_cells("cuda")
+    gw = conv.conv1x1s2(x, w, 2, gy, cells)
+    gw2 = conv.conv1x1s2(x, w, 2, gy, cells)
+    assert y.shape == y_ref.shape and gx.shape == gx_ref.shape and gw.shape == gw_ref.shape
+    assert _rel(y, y_ref) < TOL and _rel(gx, gx_ref) < TOL and _rel(gw, gw_ref) < TOL
+    assert torch.equal(gw, gw2) and int(cells.abs().sum()) == 0
+    assert float(gx[:, :, 1::2, :].abs().max()) == 0.0
+
+
+def test_conv1x1_module_routes_and_grads():
+    from paper_2203_06638_b200.conv import Conv1x1
+
+    torch.manual_seed(2)
+    m = Conv1x1(16, 32, 2).cuda().to(memory_format=CL)
+    x = torch.randn(8, 16, 32, 32, device="cuda").to(memory_format=CL).requires_grad_()
+    y = m(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xd = x.detach().double().requires_grad_()
+    wd = m.weight.detach().double().requires_grad_()
+    F.conv2d(xd, wd, stride=2).backward(gy.double())
+    assert _rel(x.grad, xd.grad) < TOL and _rel(m.weight.grad, wd.grad) < TOL
+    s1 = Conv1x1(16, 32, 1).cuda().to(memory_format=CL)      # stride 1: cuDNN
+    x1 = torch.randn(2, 16, 8, 8, device="cuda").to(memory_format=CL)
+    assert torch.allclose(s1(x1), F.conv2d(x1, s1.weight), atol=1e-5)

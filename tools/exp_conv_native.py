@@ -18,17 +18,29 @@ torch.backends.cudnn.allow_tf32 = False
 CL = torch.channels_last
 
 
-def timeit(fn, n=50):
-    for _ in range(5):
-        fn()
+def timeit(fn, n=20):
+    """Device time per call: n calls captured in one CUDA graph, replayed
+    (no host launch overhead in the number — these kernels are µs-scale)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(n):
-        fn()
+    for _ in range(5):
+        g.replay()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / n * 1e3
+    return a.elapsed_time(b) / (5 * n) * 1e3
 
 
 def rel(a, ref):
@@ -71,6 +83,19 @@ def main(B=128):
             tot_c += cnt * tc
             tot_n += cnt * tn
     print(f"16 stride-1 3x3 convs per minibatch (fwd+dgrad+wgrad): cudnn {tot_c:.0f} us, native {tot_n:.0f} us")
+    for ci, co, hw in ((16, 32, 32), (32, 64, 16)):
+        x = torch.randn(B, ci, hw, hw, device="cuda", generator=g).to(memory_format=CL)
+        w = torch.randn(co, ci, 1, 1, device="cuda", generator=g).to(memory_format=CL)
+        gy = torch.randn(B, co, hw // 2, hw // 2, device="cuda", generator=g).to(memory_format=CL)
+        cells = conv.arrival_cells("cuda")
+        cb = torch.ops.aten.convolution_backward
+        t = {"fwd": (timeit(lambda: F.conv2d(x, w, stride=2)), timeit(lambda: conv.conv1x1s2(x, w, 0))),
+             "dgrad": (timeit(lambda: cb(gy, x, w, None, (2, 2), (0, 0), (1, 1), False, (0, 0), 1, (True, False, False))),
+                       timeit(lambda: conv.conv1x1s2(gy, w, 1))),
+             "wgrad": (timeit(lambda: cb(gy, x, w, None, (2, 2), (0, 0), (1, 1), False, (0, 0), 1, (False, True, False))),
+                       timeit(lambda: conv.conv1x1s2(x, w, 2, gy, cells)))}
+        print(f"1x1 stride 2 {ci}->{co} at {hw}x{hw}: " + "; ".join(
+            f"{k} cudnn {tc:.1f} us native {tn:.1f} us" for k, (tc, tn) in t.items()))
 
 
 if __name__ == "__main__":
