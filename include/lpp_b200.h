@@ -620,6 +620,13 @@ size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
  * mode 2: out = dW of (a = x, b = dY), one launch, deterministic (as
  *         lpp_conv3x3_wgrad_f32; ws / arrivals used only here). */
 int lpp_conv1x1s2_supported(int ci, int co, int hw_in);
+/* 3x3 stride-2 pad-1 convolutions (ci -> co, hw_in -> hw_in / 2) at the
+ * same shapes, same modes and arguments (w [co][3][3][ci]); dgrad per 2x2
+ * quad of dX pixels (no products with inserted zeros) */
+int lpp_conv3x3s2_supported(int ci, int co, int hw_in);
+size_t lpp_conv3x3s2_wgrad_workspace(int n, int ci, int co, int hw_in);
+int lpp_conv3x3s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
+                      float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream);
 size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in);
 int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
                       float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream);

@@ -96,54 +96,67 @@ def _will_run(node) -> bool:
         return True
 
 
-def conv1x1s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
-              arrivals: torch.Tensor | None = None) -> torch.Tensor:
-    """The projection shortcut's kernels: mode 0 y = conv(x, w); 1 dX of
-    dY = x; 2 dW of (x, dY = other)."""
+def _strided(kind: str, x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None,
+             arrivals: torch.Tensor | None) -> torch.Tensor:
+    """The stride-2 kernels (kind "1x1" or "3x3s2"): mode 0 y = conv(x, w);
+    1 dX of dY = x; 2 dW of (x, dY = other)."""
     N = _lib()
+    fn = N.lib.lpp_conv1x1s2_f32 if kind == "1x1" else N.lib.lpp_conv3x3s2_f32
+    wsq = N.lib.lpp_conv1x1s2_wgrad_workspace if kind == "1x1" else N.lib.lpp_conv3x3s2_wgrad_workspace
     co, ci = w.shape[0], w.shape[1]
     x = x.contiguous(memory_format=_CL)
     w = _ohwi(w)
     stream = torch.cuda.current_stream(x.device).cuda_stream
+    what = f"conv{kind}_f32"
     if mode == 0:
         n, _, hw, _ = x.shape
         out = torch.empty((n, co, hw // 2, hw // 2), device=x.device, memory_format=_CL)
-        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, None, 0,
-                                        None, stream), "conv1x1s2_f32")
+        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, None, 0, None, stream), what)
     elif mode == 1:
         n, _, ho, _ = x.shape
         out = torch.empty((n, ci, 2 * ho, 2 * ho), device=x.device, memory_format=_CL)
-        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, 2 * ho, 1, None, 0,
-                                        None, stream), "conv1x1s2_f32")
+        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, 2 * ho, 1, None, 0, None, stream), what)
     else:
         n, _, hw, _ = x.shape
         dy = other.contiguous(memory_format=_CL)
         out = torch.empty_like(w, memory_format=_CL)
-        nbytes = int(N.lib.lpp_conv1x1s2_wgrad_workspace(n, ci, co, hw))
+        nbytes = int(wsq(n, ci, co, hw))
         ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
         if arrivals is None:
             arrivals = arrival_cells(x.device)
-        N.check(N.lib.lpp_conv1x1s2_f32(x.data_ptr(), dy.data_ptr(), out.data_ptr(), n, ci, co, hw, 2,
-                                        ws.data_ptr(), nbytes, arrivals.data_ptr(), stream), "conv1x1s2_f32")
+        N.check(fn(x.data_ptr(), dy.data_ptr(), out.data_ptr(), n, ci, co, hw, 2, ws.data_ptr(), nbytes,
+                   arrivals.data_ptr(), stream), what)
     return out
 
 
-class _Conv1x1s2Fn(torch.autograd.Function):
+def conv1x1s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
+              arrivals: torch.Tensor | None = None) -> torch.Tensor:
+    """The projection shortcut's kernels (1x1, stride 2)."""
+    return _strided("1x1", x, w, mode, other, arrivals)
+
+
+def conv3x3s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
+              arrivals: torch.Tensor | None = None) -> torch.Tensor:
+    """The stage-opening 3x3 stride-2 convolution's kernels."""
+    return _strided("3x3s2", x, w, mode, other, arrivals)
+
+
+class _StridedFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, arrivals, want_w):
+    def forward(ctx, x, w, arrivals, want_w, kind):
         ctx.save_for_backward(x, w)
-        ctx.arrivals, ctx.want_w = arrivals, want_w
-        return conv1x1s2(x, w, 0)
+        ctx.arrivals, ctx.want_w, ctx.kind = arrivals, want_w, kind
+        return _strided(kind, x, w, 0, None, None)
 
     @staticmethod
     def backward(ctx, gy):
         x, w = ctx.saved_tensors
         gx = gw = None
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
-            gx = conv1x1s2(gy, w, 1)
+            gx = _strided(ctx.kind, gy, w, 1, None, None)
         if ctx.needs_input_grad[1] and ctx.want_w:
-            gw = conv1x1s2(x, w, 2, gy, ctx.arrivals)
-        return gx, gw, None, None
+            gw = _strided(ctx.kind, x, w, 2, gy, ctx.arrivals)
+        return gx, gw, None, None, None
 
 
 class _Conv3x3Fn(torch.autograd.Function):
@@ -192,13 +205,19 @@ class Conv3x3(nn.Conv2d):
         self.want_w = True
         self._arrivals = None   # wgrad arrival counters; this module's launches are stream-ordered
 
+    def _arrival_cells(self, device) -> torch.Tensor:
+        if self._arrivals is None or self._arrivals.device != device:
+            self._arrivals = arrival_cells(device)
+        return self._arrivals
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        if (x.dtype == torch.float32 and x.is_cuda and self.weight.dtype == torch.float32
-                and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled()
-                and supported(self.in_channels, self.out_channels, x.shape[2], self.stride[0], 3)):
-            if self._arrivals is None or self._arrivals.device != x.device:
-                self._arrivals = arrival_cells(x.device)
-            return conv3x3(x, self.weight, self._arrivals, self.want_w)
+        native = (x.dtype == torch.float32 and x.is_cuda and self.weight.dtype == torch.float32
+                  and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled())
+        if native and supported(self.in_channels, self.out_channels, x.shape[2], self.stride[0], 3):
+            return conv3x3(x, self.weight, self._arrival_cells(x.device), self.want_w)
+        if (native and self.stride == (2, 2)
+                and _lib().lib.lpp_conv3x3s2_supported(self.in_channels, self.out_channels, x.shape[2])):
+            return _StridedFn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, "3x3s2")
         return F.conv2d(x, self.weight, None, self.stride, self.padding)
 
 
@@ -218,5 +237,5 @@ class Conv1x1(nn.Conv2d):
                 and _lib().lib.lpp_conv1x1s2_supported(self.in_channels, self.out_channels, x.shape[2])):
             if self._arrivals is None or self._arrivals.device != x.device:
                 self._arrivals = arrival_cells(x.device)
-            return _Conv1x1s2Fn.apply(x, self.weight, self._arrivals, self.want_w)
+            return _StridedFn.apply(x, self.weight, self._arrivals, self.want_w, "1x1")
         return F.conv2d(x, self.weight, None, self.stride, self.padding)

@@ -649,6 +649,417 @@ size_t conv1x1s2_workspace(int n) {
   return ctas / wgrad_cluster(ctas, 8) * CO * CI * sizeof(float);
 }
 
+// ---------------------------------------------------------------------------
+// 3x3 stride-2 pad-1 convolutions CI -> CO at input 2HO x 2HO, output HO x HO
+// (ResNet-20's stage-opening convolutions 16->32 @32x32, 32->64 @16x16).
+//
+// Forward: like k_conv3x3, with the staged input columns de-interleaved
+// (even columns, then odd) so that lanes at consecutive output x read
+// consecutive staged pixels; a thread's PX output rows read 2 PX + 1 input
+// rows for its 3 PX (row, tap row) pairs.
+
+template <int CI, int CO, int HO, int TH, int COT, int PX, int CW>
+struct S2Cfg {
+  static constexpr int CP = CI + kPad;
+  static constexpr int SROWS = 2 * TH + 1, SCOLS = 2 * HO + 1;
+  static constexpr int XS = SROWS * SCOLS * CP;
+  static constexpr int WS = 9 * CI * COT;
+  static constexpr int LR = 32 / HO;
+  static constexpr int NPG = TH / (LR * PX), NCG = COT / CW;
+  static constexpr int THREADS = 32 * NPG * NCG;
+  static constexpr int SMEM = (XS + WS) * 4;
+  static_assert(HO <= 32 && 32 % HO == 0 && TH % (LR * PX) == 0 && HO % TH == 0, "tiles");
+  static_assert(CO % COT == 0 && COT % CW == 0 && CW % 4 == 0 && CI % 4 == 0, "channels");
+};
+
+__device__ __forceinline__ int s2_col(int t, int ho) { return (t & 1) ? ho + 1 + (t >> 1) : (t >> 1); }
+
+template <int CI, int CO, int HO, int TH, int COT, int PX, int CW>
+__global__ void __launch_bounds__(S2Cfg<CI, CO, HO, TH, COT, PX, CW>::THREADS)
+k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y) {
+  using K = S2Cfg<CI, CO, HO, TH, COT, PX, CW>;
+  constexpr int CP = K::CP, HI = 2 * HO;
+  extern __shared__ float4 smem4[];
+  float* xs = reinterpret_cast<float*>(smem4);
+  float* ws = xs + K::XS;
+  constexpr int CO_TILES = CO / COT, ROW_TILES = HO / TH;
+  const int bid = blockIdx.x;
+  const int cot = bid % CO_TILES, rt = (bid / CO_TILES) % ROW_TILES, n = bid / (CO_TILES * ROW_TILES);
+  const int y0 = rt * TH, co0 = cot * COT;
+  {
+    constexpr int C4 = CI / 4, TOTAL = K::SROWS * K::SCOLS * C4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TOTAL; i += K::THREADS) {
+      const int c4 = i % C4, t = (i / C4) % K::SCOLS, srow = i / (C4 * K::SCOLS);
+      const int gy = 2 * y0 - 1 + srow, gx = t - 1;
+      const bool in = gy >= 0 && gy < HI && gx >= 0 && gx < HI;
+      const float* src = in ? x + ((size_t(n) * HI + gy) * HI + gx) * CI + c4 * 4 : x;
+      cp_async16(xs + (srow * K::SCOLS + s2_col(t, HO)) * CP + c4 * 4, src, in);
+    }
+    // ws[t][ci][co - co0] (a transpose of OHWI; lanes take consecutive co)
+#pragma unroll 4
+    for (int i = threadIdx.x; i < COT * 9 * C4; i += K::THREADS) {
+      const int j = i % COT, rem = i / COT;
+      const int tap = rem / C4, c4 = rem % C4;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(w + size_t(co0 + j) * 9 * CI) + rem);
+      float* d = ws + (tap * CI + c4 * 4) * COT + j;
+      d[0] = v.x; d[COT] = v.y; d[2 * COT] = v.z; d[3 * COT] = v.w;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pg = warp % K::NPG, cg = warp / K::NPG;
+  const int lx = lane % HO, rg = lane / HO;
+  const int ty0 = (pg * K::LR + rg) * PX;            // first output row of the thread (tile-relative)
+  const float* wcol = ws + cg * CW;
+  float acc[PX][CW];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
+
+#pragma unroll 1
+  for (int s = 0; s < 3; ++s) {
+    const int col = s == 0 ? lx : s == 1 ? HO + 1 + lx : lx + 1;
+    const float* xcol = xs + (2 * ty0 * K::SCOLS + col) * CP;
+#pragma unroll 1
+    for (int c4 = 0; c4 < CI / 4; ++c4) {
+      float4 a[2 * PX + 1];
+#pragma unroll
+      for (int j = 0; j < 2 * PX + 1; ++j)
+        a[j] = *reinterpret_cast<const float4*>(xcol + j * K::SCOLS * CP + c4 * 4);
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const float* wp = wcol + ((r * 3 + s) * CI + c4 * 4) * COT;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float wv[CW];
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(wp + q * COT + j);
+            wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+          }
+#pragma unroll
+          for (int i = 0; i < PX; ++i) {
+            const float4 av4 = a[2 * i + r];
+            const float av = q == 0 ? av4.x : q == 1 ? av4.y : q == 2 ? av4.z : av4.w;
+#pragma unroll
+            for (int j = 0; j < CW; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PX; ++i) {
+    float* out = y + ((size_t(n) * HO + y0 + ty0 + i) * HO + lx) * CO + co0 + cg * CW;
+#pragma unroll
+    for (int j = 0; j < CW; j += 4)
+      *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+  }
+}
+
+// dgrad of the stride-2 convolution, per 2x2 quad of dX pixels (2yq + a,
+// 2xq + b): the even/odd row and column classes take 1, 2, 2, 4 taps from
+// the dY pixels (yq, xq), (yq, xq+1), (yq+1, xq), (yq+1, xq+1) — the 9 taps
+// once per quad, no multiplications by inserted zeros.  A thread owns PQ
+// vertically adjacent quads x CIW input channels.
+template <int CI, int CO, int HO, int TQ, int CIT, int PQ, int CIW>
+struct S2dCfg {
+  static constexpr int DP = CO + kPad;
+  static constexpr int DROWS = TQ + 1, DCOLS = HO + 1;  // + the zero row / column past the edge
+  static constexpr int DS = DROWS * DCOLS * DP;
+  static constexpr int WS = 9 * CO * CIT;
+  static constexpr int LR = 32 / HO;
+  static constexpr int NPG = TQ / (LR * PQ), NCG = CIT / CIW;
+  static constexpr int THREADS = 32 * NPG * NCG;
+  static constexpr int SMEM = (DS + WS) * 4;
+  static_assert(HO <= 32 && 32 % HO == 0 && TQ % (LR * PQ) == 0 && HO % TQ == 0, "tiles");
+  static_assert(CI % CIT == 0 && CIT % CIW == 0 && CIW % 4 == 0 && CO % 4 == 0, "channels");
+};
+
+template <int CI, int CO, int HO, int TQ, int CIT, int PQ, int CIW>
+__global__ void __launch_bounds__(S2dCfg<CI, CO, HO, TQ, CIT, PQ, CIW>::THREADS)
+k_conv3x3s2_dgrad(const float* __restrict__ dy, const float* __restrict__ w, float* __restrict__ dx) {
+  using K = S2dCfg<CI, CO, HO, TQ, CIT, PQ, CIW>;
+  constexpr int DP = K::DP, HI = 2 * HO;
+  extern __shared__ float4 smem4[];
+  float* ds = reinterpret_cast<float*>(smem4);
+  float* ws = ds + K::DS;
+  constexpr int CI_TILES = CI / CIT, ROW_TILES = HO / TQ;
+  const int bid = blockIdx.x;
+  const int cit = bid % CI_TILES, rt = (bid / CI_TILES) % ROW_TILES, n = bid / (CI_TILES * ROW_TILES);
+  const int q0 = rt * TQ, ci0 = cit * CIT;
+  {
+    constexpr int C4 = CO / 4, TOTAL = K::DROWS * K::DCOLS * C4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TOTAL; i += K::THREADS) {
+      const int c4 = i % C4, col = (i / C4) % K::DCOLS, row = i / (C4 * K::DCOLS);
+      const int gy = q0 + row;
+      const bool in = gy < HO && col < HO;
+      const float* src = in ? dy + ((size_t(n) * HO + gy) * HO + col) * CO + c4 * 4 : dy;
+      cp_async16(ds + (row * K::DCOLS + col) * DP + c4 * 4, src, in);
+    }
+    // ws[tap][co][ci - ci0]: contiguous in ci, a straight copy
+    constexpr int J4 = CIT / 4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < CO * 9 * J4; i += K::THREADS) {
+      const int j4 = i % J4, tap = (i / J4) % 9, co = i / (9 * J4);
+      cp_async16(ws + (tap * CO + co) * CIT + j4 * 4, w + (size_t(co) * 9 + tap) * CI + ci0 + j4 * 4, true);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pg = warp % K::NPG, cg = warp / K::NPG;
+  const int lx = lane % HO, rg = lane / HO;
+  const int tq0 = (pg * K::LR + rg) * PQ;            // first quad row (tile-relative)
+  const float* wcol = ws + cg * CIW;
+  // acc[quad][class ee, eo, oe, oo][ci]
+  float acc[PQ][4][CIW];
+#pragma unroll
+  for (int i = 0; i < PQ; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < CIW; ++j) acc[i][c][j] = 0.f;
+
+#pragma unroll 1
+  for (int c4 = 0; c4 < CO / 4; ++c4) {
+    float4 dl[PQ + 1], dr[PQ + 1];                   // dY at (row, xq) and (row, xq + 1)
+#pragma unroll
+    for (int j = 0; j < PQ + 1; ++j) {
+      const float* p = ds + ((tq0 + j) * K::DCOLS + lx) * DP + c4 * 4;
+      dl[j] = *reinterpret_cast<const float4*>(p);
+      dr[j] = *reinterpret_cast<const float4*>(p + DP);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int r = tap / 3, s = tap % 3;
+        float wv[CIW];
+#pragma unroll
+        for (int j = 0; j < CIW; j += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(wcol + (tap * CO + c4 * 4 + q) * CIT + j);
+          wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+        }
+        // class of the tap: rows r = 1 -> even (dY row yq), r = 0 -> odd from yq + 1, r = 2 -> odd from yq;
+        // columns likewise
+        const int cls = (r == 1 ? 0 : 2) + (s == 1 ? 0 : 1);
+        const int dyr = r == 0 ? 1 : 0;              // dY row offset
+        const bool right = s == 0;                   // dY column xq + 1
+#pragma unroll
+        for (int i = 0; i < PQ; ++i) {
+          const float4 v4 = right ? dr[i + dyr] : dl[i + dyr];
+          const float v = q == 0 ? v4.x : q == 1 ? v4.y : q == 2 ? v4.z : v4.w;
+#pragma unroll
+          for (int j = 0; j < CIW; ++j) acc[i][cls][j] = fmaf(v, wv[j], acc[i][cls][j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PQ; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int yi = 2 * (q0 + tq0 + i) + (c >> 1), xi = 2 * lx + (c & 1);
+      float* out = dx + ((size_t(n) * HI + yi) * HI + xi) * CI + ci0 + cg * CIW;
+#pragma unroll
+      for (int j = 0; j < CIW; j += 4)
+        *reinterpret_cast<float4*>(out + j) =
+            make_float4(acc[i][c][j], acc[i][c][j + 1], acc[i][c][j + 2], acc[i][c][j + 3]);
+    }
+}
+
+// wgrad of the stride-2 convolution: k_wgrad3x3's thread tile with the
+// input window sliding by two columns per output pixel (2 input float4s +
+// 1 dY float4 per 48 FFMAs)
+template <int CI, int CO, int HO, int TH, int COT, int PS>
+struct S2wCfg {
+  static constexpr int CP = CI + kPad, DP = COT + kPad;
+  static constexpr int SROWS = 2 * TH + 1, SCOLS = 2 * HO + 1;
+  static constexpr int XS = SROWS * SCOLS * CP, DS = TH * HO * DP;
+  static constexpr int GROUP = 3 * (CI / 4) * (COT / 4), THREADS = GROUP * PS;
+  static constexpr int RED = 9 * CI * COT;
+  static constexpr int SMEM = ((XS + DS) > RED ? (XS + DS) : RED) * 4;
+  static_assert(TH % PS == 0 && HO % TH == 0 && RED % (4 * 8) == 0, "tiles");
+};
+
+template <int CI, int CO, int HO, int TH, int COT, int PS>
+__global__ void __launch_bounds__(S2wCfg<CI, CO, HO, TH, COT, PS>::THREADS)
+k_wgrad3x3s2(const float* __restrict__ x, const float* __restrict__ dy, float* part, float* __restrict__ dw,
+             unsigned* __restrict__ arrivals) {
+  using K = S2wCfg<CI, CO, HO, TH, COT, PS>;
+  constexpr int CP = K::CP, DP = K::DP, HI = 2 * HO;
+  extern __shared__ float4 smem4[];
+  float* xs = reinterpret_cast<float*>(smem4);
+  float* ds = xs + K::XS;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int ROW_TILES = HO / TH;
+  const int tile = blockIdx.x, cot = blockIdx.y;
+  const int rt = tile % ROW_TILES, n = tile / ROW_TILES;
+  const int y0 = rt * TH, co0 = cot * COT;
+  {
+    constexpr int C4 = CI / 4, TOTAL = K::SROWS * K::SCOLS * C4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TOTAL; i += K::THREADS) {
+      const int c4 = i % C4, t = (i / C4) % K::SCOLS, srow = i / (C4 * K::SCOLS);
+      const int gy = 2 * y0 - 1 + srow, gx = t - 1;
+      const bool in = gy >= 0 && gy < HI && gx >= 0 && gx < HI;
+      const float* src = in ? x + ((size_t(n) * HI + gy) * HI + gx) * CI + c4 * 4 : x;
+      cp_async16(xs + (srow * K::SCOLS + t) * CP + c4 * 4, src, in);
+    }
+    constexpr int J4 = COT / 4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TH * HO * J4; i += K::THREADS) {
+      const int j4 = i % J4, p = i / J4;
+      cp_async16(ds + p * DP + j4 * 4, dy + ((size_t(n) * HO + y0) * HO + p) * CO + co0 + j4 * 4, true);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int tid = threadIdx.x;
+  const int ci4 = tid % (CI / 4), co4 = (tid / (CI / 4)) % (COT / 4);
+  const int r = (tid / ((CI / 4) * (COT / 4))) % 3, ps = tid / K::GROUP;
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+  constexpr int RPS = TH / PS;
+#pragma unroll 1
+  for (int ty = ps * RPS; ty < (ps + 1) * RPS; ++ty) {
+    const float* xr = xs + ((2 * ty + r) * K::SCOLS) * CP + ci4 * 4;
+    const float* dr = ds + (ty * HO) * DP + co4 * 4;
+    float4 xm = *reinterpret_cast<const float4*>(xr);
+#pragma unroll 4
+    for (int xx = 0; xx < HO; ++xx) {
+      const float4 x0 = *reinterpret_cast<const float4*>(xr + (2 * xx + 1) * CP);
+      const float4 xp = *reinterpret_cast<const float4*>(xr + (2 * xx + 2) * CP);
+      const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
+      const float dv[4] = {d.x, d.y, d.z, d.w};
+      const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+      xm = xp;
+    }
+  }
+  float* red = xs;
+  __syncthreads();
+#pragma unroll 1
+  for (int p = 0; p < PS; ++p) {
+    if (ps == p) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          float* d = red + ((co4 * 4 + c) * 9 + r * 3 + s) * CI + ci4 * 4;
+          float4 v = make_float4(acc[s][0][c], acc[s][1][c], acc[s][2][c], acc[s][3][c]);
+          if (p > 0) {
+            const float4 o = *reinterpret_cast<const float4*>(d);
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          *reinterpret_cast<float4*>(d) = v;
+        }
+    }
+    __syncthreads();
+  }
+  cluster_tail_reduce<K::THREADS>(cluster, red, K::RED / 4, size_t(co0) * 9 * CI / 4, 9 * CI * CO / 4, part, dw,
+                                  arrivals + cot, tile);
+}
+
+template <typename Kern>
+int set_smem(Kern kern, int bytes, bool& done) {
+  if (!done) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
+  }
+  return 0;
+}
+
+// configurations per shape: (CI, CO, HO) -> forward / dgrad / wgrad tiles
+template <int CI, int CO, int HO>
+struct S2Shape;
+template <>
+struct S2Shape<16, 32, 16> {
+  using F = S2Cfg<16, 32, 16, 8, 32, 4, 8>;
+  using D = S2dCfg<16, 32, 16, 8, 16, 2, 8>;
+  using Wg = S2wCfg<16, 32, 16, 8, 32, 2>;
+  static constexpr auto fwd = k_conv3x3s2<16, 32, 16, 8, 32, 4, 8>;
+  static constexpr auto dgrad = k_conv3x3s2_dgrad<16, 32, 16, 8, 16, 2, 8>;
+  static constexpr auto wgrad = k_wgrad3x3s2<16, 32, 16, 8, 32, 2>;
+  static constexpr int F_TILES = (16 / 8) * (32 / 32), D_TILES = (16 / 8) * (16 / 16), W_TILES = 16 / 8, W_CO = 32 / 32;
+};
+template <>
+struct S2Shape<32, 64, 8> {
+  using F = S2Cfg<32, 64, 8, 8, 32, 2, 8>;
+  using D = S2dCfg<32, 64, 8, 8, 16, 2, 8>;
+  using Wg = S2wCfg<32, 64, 8, 8, 32, 1>;
+  static constexpr auto fwd = k_conv3x3s2<32, 64, 8, 8, 32, 2, 8>;
+  static constexpr auto dgrad = k_conv3x3s2_dgrad<32, 64, 8, 8, 16, 2, 8>;
+  static constexpr auto wgrad = k_wgrad3x3s2<32, 64, 8, 8, 32, 1>;
+  static constexpr int F_TILES = (8 / 8) * (64 / 32), D_TILES = (8 / 8) * (32 / 16), W_TILES = 8 / 8, W_CO = 64 / 32;
+};
+
+template <int CI, int CO, int HO>
+size_t conv3x3s2_workspace(int n) {
+  using S = S2Shape<CI, CO, HO>;
+  const size_t tiles = size_t(n) * S::W_TILES;
+  return tiles / wgrad_cluster(tiles, 8) * 9 * CI * CO * sizeof(float);
+}
+
+template <int CI, int CO, int HO>
+int launch_conv3x3s2(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
+                     unsigned* arrivals, cudaStream_t st) {
+  using S = S2Shape<CI, CO, HO>;
+  int rc;
+  if (mode == 0) {
+    static bool done = false;
+    if ((rc = set_smem(S::fwd, S::F::SMEM, done))) return rc;
+    S::fwd<<<n * S::F_TILES, S::F::THREADS, S::F::SMEM, st>>>(a, b, out);
+    LAUNCH_CHECK("k_conv3x3s2");
+  } else if (mode == 1) {
+    static bool done = false;
+    if ((rc = set_smem(S::dgrad, S::D::SMEM, done))) return rc;
+    S::dgrad<<<n * S::D_TILES, S::D::THREADS, S::D::SMEM, st>>>(a, b, out);
+    LAUNCH_CHECK("k_conv3x3s2_dgrad");
+  } else {
+    if (!arrivals) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: null arrival counters");
+    const size_t need = conv3x3s2_workspace<CI, CO, HO>(n);
+    if (ws_bytes < need) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: workspace %zu B < %zu B", ws_bytes, need);
+    static bool done = false;
+    if ((rc = set_smem(S::wgrad, S::Wg::SMEM, done))) return rc;
+    const size_t tiles = size_t(n) * S::W_TILES;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(tiles), S::W_CO, 1);
+    cfg.blockDim = dim3(S::Wg::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = S::Wg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(wgrad_cluster(tiles, 8));
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // mode 2: a = x (forward input), b = dY
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, S::wgrad, a, b, ws, out, arrivals));
+    LAUNCH_CHECK("k_wgrad3x3s2");
+  }
+  return 0;
+}
+
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
@@ -792,4 +1203,27 @@ extern "C" int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int
                                                    arrivals, st)
                      : launch_conv1x1s2<32, 64, 8>(a, b, out, n, mode, nullptr, nullptr, 0, nullptr, st);
   return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: no kernel for %d->%d at %dx%d", ci, co, hw_in, hw_in);
+}
+
+extern "C" int lpp_conv3x3s2_supported(int ci, int co, int hw_in) {
+  return (ci == 16 && co == 32 && hw_in == 32) || (ci == 32 && co == 64 && hw_in == 16);
+}
+
+extern "C" size_t lpp_conv3x3s2_wgrad_workspace(int n, int ci, int co, int hw_in) {
+  if (n <= 0) return 0;
+  if (ci == 16 && co == 32 && hw_in == 32) return conv3x3s2_workspace<16, 32, 16>(n);
+  if (ci == 32 && co == 64 && hw_in == 16) return conv3x3s2_workspace<32, 64, 8>(n);
+  return 0;
+}
+
+extern "C" int lpp_conv3x3s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in,
+                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream) {
+  if (!a || !b || !out) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: null pointer");
+  if (n <= 0 || mode < 0 || mode > 2) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: batch %d mode %d", n, mode);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (ci == 16 && co == 32 && hw_in == 32)
+    return launch_conv3x3s2<16, 32, 16>(a, b, out, n, mode, ws, ws_bytes, arrivals, st);
+  if (ci == 32 && co == 64 && hw_in == 16)
+    return launch_conv3x3s2<32, 64, 8>(a, b, out, n, mode, ws, ws_bytes, arrivals, st);
+  return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: no kernel for %d->%d at %dx%d", ci, co, hw_in, hw_in);
 }

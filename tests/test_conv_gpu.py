@@ -255,3 +255,43 @@ def test_conv1x1_module_routes_and_grads():
     s1 = Conv1x1(16, 32, 1).cuda().to(memory_format=CL)      # stride 1: cuDNN
     x1 = torch.randn(2, 16, 8, 8, device="cuda").to(memory_format=CL)
     assert torch.allclose(s1(x1), F.conv2d(x1, s1.weight), atol=1e-5)
+
+
+@pytest.mark.parametrize("ci,co,hw", SHAPES_1X1)
+@pytest.mark.parametrize("n", [1, 3, 128])
+def test_conv3x3s2_kernels_match_fp64(ci, co, hw, n):
+    """The stage-opening 3x3 stride-2 convolution: forward, quad dgrad, wgrad."""
+    from paper_2203_06638_b200 import conv
+
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(n, ci, hw, hw, device="cuda", generator=g).to(memory_format=CL)
+    w = (torch.randn(co, ci, 3, 3, device="cuda", generator=g) / (3 * ci ** 0.5)).to(memory_format=CL)
+    gy = torch.randn(n, co, hw // 2, hw // 2, device="cuda", generator=g).to(memory_format=CL)
+    xd, wd, gyd = x.double(), w.double(), gy.double()
+    y_ref = F.conv2d(xd, wd, stride=2, padding=1)
+    gx_ref, gw_ref, _ = torch.ops.aten.convolution_backward(gyd, xd, wd, None, (2, 2), (1, 1), (1, 1), False,
+                                                            (0, 0), 1, (True, True, False))
+    cells = conv.arrival_cells("cuda")
+    y = conv.conv3x3s2(x, w, 0)
+    gx = conv.conv3x3s2(gy, w, 1)
+    gw = conv.conv3x3s2(x, w, 2, gy, cells)
+    assert y.shape == y_ref.shape and gx.shape == gx_ref.shape and gw.shape == gw_ref.shape
+    assert _rel(y, y_ref) < TOL and _rel(gx, gx_ref) < TOL and _rel(gw, gw_ref) < TOL
+    assert torch.equal(gw, conv.conv3x3s2(x, w, 2, gy, cells)) and int(cells.abs().sum()) == 0
+
+
+def test_conv3x3_stride2_module_grads():
+    from paper_2203_06638_b200.conv import Conv3x3
+
+    torch.manual_seed(3)
+    m = Conv3x3(32, 64, 2).cuda().to(memory_format=CL)
+    x = torch.randn(8, 32, 16, 16, device="cuda").to(memory_format=CL).requires_grad_()
+    y = m(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xd = x.detach().double().requires_grad_()
+    wd = m.weight.detach().double().requires_grad_()
+    yd = F.conv2d(xd, wd, stride=2, padding=1)
+    yd.backward(gy.double())
+    assert _rel(y.detach(), yd.detach()) < TOL
+    assert _rel(x.grad, xd.grad) < TOL and _rel(m.weight.grad, wd.grad) < TOL

@@ -96,6 +96,14 @@ def main(B=128):
                        timeit(lambda: conv.conv1x1s2(x, w, 2, gy, cells)))}
         print(f"1x1 stride 2 {ci}->{co} at {hw}x{hw}: " + "; ".join(
             f"{k} cudnn {tc:.1f} us native {tn:.1f} us" for k, (tc, tn) in t.items()))
+        w3 = torch.randn(co, ci, 3, 3, device="cuda", generator=g).to(memory_format=CL)
+        t = {"fwd": (timeit(lambda: F.conv2d(x, w3, stride=2, padding=1)), timeit(lambda: conv.conv3x3s2(x, w3, 0))),
+             "dgrad": (timeit(lambda: cb(gy, x, w3, None, (2, 2), (1, 1), (1, 1), False, (0, 0), 1, (True, False, False))),
+                       timeit(lambda: conv.conv3x3s2(gy, w3, 1))),
+             "wgrad": (timeit(lambda: cb(gy, x, w3, None, (2, 2), (1, 1), (1, 1), False, (0, 0), 1, (False, True, False))),
+                       timeit(lambda: conv.conv3x3s2(x, w3, 2, gy, cells)))}
+        print(f"3x3 stride 2 {ci}->{co} at {hw}x{hw}: " + "; ".join(
+            f"{k} cudnn {tc:.1f} us native {tn:.1f} us" for k, (tc, tn) in t.items()))
 
 
 if __name__ == "__main__":
