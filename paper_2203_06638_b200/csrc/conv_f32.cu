@@ -1068,12 +1068,12 @@ using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsi
 using TilesFn = size_t (*)(int);
 
 //                     C   H  TH COT PX CO U
-const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 4, 16, 4, 8, 1>,
+const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 8, 16, 4, 16, 1>,
                           launch_conv<16, 32, 8, 16, 4, 8, 2>, launch_conv<16, 32, 4, 16, 4, 8, 2>};
-const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 16, 4, 8, 1>,
-                          launch_conv<32, 16, 4, 32, 2, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
-const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 8, 16, 2, 8, 1>,
-                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 8, 32, 2, 8, 2>};
+const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 16, 1>,
+                          launch_conv<32, 16, 16, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
+const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 16, 16, 4, 8, 1>,
+                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 16, 32, 4, 8, 1>};
 //                        C   H  TH COT PS CL
 const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32, 16, 16, 4, 16>,
                          launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
