@@ -600,9 +600,16 @@ int lpp_conv3x3_supported(int c, int hw);
  * FFMAs (8 chains per thread), no memory traffic — the fp32 FMA peak the
  * convolutions' roofline divides by (2 flops per FFMA) */
 int lpp_fma_probe(float* out, int blocks, int iters, void* stream);
-/* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x */
+/* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x.
+ * Forward only, stat_sums != NULL: also the BatchNorm statistics of y,
+ * stat_sums[c][2] = (sum, sum of squares) over the n x hw x hw pixels, fused
+ * into the epilogue and reduced in the same launch (fixed order, as
+ * lpp_conv3x3_wgrad_f32), with stat_ws (lpp_conv3x3_stats_workspace bytes)
+ * and LPP_CONV_ARRIVALS zeroed stat_arrivals cells. */
 int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
+                    float* stat_ws, size_t stat_ws_bytes, float* stat_sums, uint32_t* stat_arrivals,
                     void* stream);
+size_t lpp_conv3x3_stats_workspace(int n, int c, int hw);
 /* bytes of workspace lpp_conv3x3_wgrad_f32 needs (per-cluster partial sums) */
 size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
 /* dw = sum over pixels of x (*) dy in ONE launch, deterministic: CTA
@@ -626,10 +633,26 @@ int lpp_conv1x1s2_supported(int ci, int co, int hw_in);
 int lpp_conv3x3s2_supported(int ci, int co, int hw_in);
 size_t lpp_conv3x3s2_wgrad_workspace(int n, int ci, int co, int hw_in);
 int lpp_conv3x3s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
-                      float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream);
+                      float* ws, size_t ws_bytes, uint32_t* arrivals, float* stat_sums, void* stream);
+size_t lpp_conv3x3s2_stats_workspace(int n, int ci, int co, int hw_in);
+
+/* BatchNorm in training mode from the fused statistics (sums[c][2] of the
+ * npix pixels, NHWC x of c in {16, 32, 64} channels):
+ * y = [relu](x * gamma * invstd + beta - mean * gamma * invstd [+ resid]);
+ * writes save_mean / save_invstd (the backward's inputs, as
+ * torch.native_batch_norm) and, when given, moves running_mean /
+ * running_var by momentum (unbiased variance) — BatchNorm2d.forward
+ * (+ the block's residual add and ReLU) in one memory pass. */
+int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, const float* beta,
+                     const float* resid, float* y, float* save_mean, float* save_invstd,
+                     float* running_mean, float* running_var, int64_t npix, int c, float eps,
+                     float momentum, int relu, void* stream);
 size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in);
 int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
-                      float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream);
+                      float* ws, size_t ws_bytes, uint32_t* arrivals, float* stat_sums, void* stream);
+/* mode 0 with stat_sums: the fused BatchNorm statistics of y (as
+ * lpp_conv3x3_f32; ws of lpp_conv1x1s2_stats_workspace bytes) */
+size_t lpp_conv1x1s2_stats_workspace(int n, int ci, int co, int hw_in);
 int lpp_conv3x3_wgrad_f32(const float* x, const float* dy, float* dw, float* ws, size_t ws_bytes,
                           uint32_t* arrivals, int n, int c, int hw, void* stream);
 

@@ -223,11 +223,17 @@ _SIGS = {
     "lpp_conv3x3s2_supported": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3s2_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3s2_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp, _size,
-                                      _vp, _vp]),
+                                      _vp, _vp, _vp]),
     "lpp_conv1x1s2_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv1x1s2_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp, _size,
-                                      _vp, _vp]),
-    "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp]),
+                                      _vp, _vp, _vp]),
+    "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp, _size, _vp, _vp,
+                                    _vp]),
+    "lpp_conv3x3_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
+    "lpp_conv1x1s2_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
+    "lpp_conv3x3s2_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
+    "lpp_bn_apply_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_int64, _c.c_int,
+                                     _c.c_float, _c.c_float, _c.c_int, _vp]),
     "lpp_conv3x3_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _vp, _c.c_int, _c.c_int, _c.c_int, _vp]),
 }

@@ -46,24 +46,36 @@ def _ohwi(w: torch.Tensor) -> torch.Tensor:
     return w.contiguous(memory_format=_CL)
 
 
-def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False) -> torch.Tensor:
+def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False, stats: torch.Tensor | None = None):
+    """y = conv(x, w) (dgrad: the input gradient for dY = x).  With
+    ``stats`` (LPP_CONV_ARRIVALS zeroed cells) also the fused BatchNorm
+    statistics of y: returns (y, sums[c][2])."""
     N = _lib()
     n, c, h, _ = x.shape
     x = x.contiguous(memory_format=_CL)
     w = _ohwi(w)
     y = torch.empty_like(x, memory_format=_CL)
-    N.check(N.lib.lpp_conv3x3_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, c, h, int(dgrad),
-                                  torch.cuda.current_stream(x.device).cuda_stream), "conv3x3_f32")
-    return y
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    if stats is None:
+        N.check(N.lib.lpp_conv3x3_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, c, h, int(dgrad), None, 0, None,
+                                      None, stream), "conv3x3_f32")
+        return y
+    nbytes = int(N.lib.lpp_conv3x3_stats_workspace(n, c, h))
+    ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
+    sums = torch.empty(2 * c, dtype=torch.float32, device=x.device)
+    N.check(N.lib.lpp_conv3x3_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, c, h, 0, ws.data_ptr(), nbytes,
+                                  sums.data_ptr(), stats.data_ptr(), stream), "conv3x3_f32")
+    return y, sums
 
 
 ARRIVALS = 8   # LPP_CONV_ARRIVALS
 
 
-def arrival_cells(device) -> torch.Tensor:
-    """Zeroed counters for lpp_conv3x3_wgrad_f32 (every call leaves them
-    zero; calls sharing a set must be stream-ordered)."""
-    return torch.zeros(ARRIVALS, dtype=torch.int32, device=device)
+def arrival_cells(device, sets: int = 1) -> torch.Tensor:
+    """Zeroed counters for the one-launch reductions (weight gradients, the
+    fused BatchNorm statistics); every call leaves them zero; calls sharing
+    a set must be stream-ordered.  ``sets`` sets of LPP_CONV_ARRIVALS."""
+    return torch.zeros(ARRIVALS * sets, dtype=torch.int32, device=device)
 
 
 def conv_wgrad(x: torch.Tensor, dy: torch.Tensor, like: torch.Tensor,
@@ -97,12 +109,14 @@ def _will_run(node) -> bool:
 
 
 def _strided(kind: str, x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None,
-             arrivals: torch.Tensor | None) -> torch.Tensor:
-    """The stride-2 kernels (kind "1x1" or "3x3s2"): mode 0 y = conv(x, w);
-    1 dX of dY = x; 2 dW of (x, dY = other)."""
+             arrivals: torch.Tensor | None, stats: torch.Tensor | None = None):
+    """The stride-2 kernels (kind "1x1" or "3x3s2"): mode 0 y = conv(x, w)
+    (with ``stats`` cells: (y, BatchNorm sums)); 1 dX of dY = x; 2 dW of
+    (x, dY = other)."""
     N = _lib()
     fn = N.lib.lpp_conv1x1s2_f32 if kind == "1x1" else N.lib.lpp_conv3x3s2_f32
     wsq = N.lib.lpp_conv1x1s2_wgrad_workspace if kind == "1x1" else N.lib.lpp_conv3x3s2_wgrad_workspace
+    ssq = N.lib.lpp_conv1x1s2_stats_workspace if kind == "1x1" else N.lib.lpp_conv3x3s2_stats_workspace
     co, ci = w.shape[0], w.shape[1]
     x = x.contiguous(memory_format=_CL)
     w = _ohwi(w)
@@ -111,80 +125,105 @@ def _strided(kind: str, x: torch.Tensor, w: torch.Tensor, mode: int, other: torc
     if mode == 0:
         n, _, hw, _ = x.shape
         out = torch.empty((n, co, hw // 2, hw // 2), device=x.device, memory_format=_CL)
-        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, None, 0, None, stream), what)
-    elif mode == 1:
+        if stats is None:
+            N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, None, 0, None, None, stream),
+                    what)
+            return out
+        nbytes = int(ssq(n, ci, co, hw))
+        ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
+        sums = torch.empty(2 * co, dtype=torch.float32, device=x.device)
+        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, hw, 0, ws.data_ptr(), nbytes,
+                   stats.data_ptr(), sums.data_ptr(), stream), what)
+        return out, sums
+    if mode == 1:
         n, _, ho, _ = x.shape
         out = torch.empty((n, ci, 2 * ho, 2 * ho), device=x.device, memory_format=_CL)
-        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, 2 * ho, 1, None, 0, None, stream), what)
-    else:
-        n, _, hw, _ = x.shape
-        dy = other.contiguous(memory_format=_CL)
-        out = torch.empty_like(w, memory_format=_CL)
-        nbytes = int(wsq(n, ci, co, hw))
-        ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
-        if arrivals is None:
-            arrivals = arrival_cells(x.device)
-        N.check(fn(x.data_ptr(), dy.data_ptr(), out.data_ptr(), n, ci, co, hw, 2, ws.data_ptr(), nbytes,
-                   arrivals.data_ptr(), stream), what)
+        N.check(fn(x.data_ptr(), w.data_ptr(), out.data_ptr(), n, ci, co, 2 * ho, 1, None, 0, None, None, stream),
+                what)
+        return out
+    n, _, hw, _ = x.shape
+    dy = other.contiguous(memory_format=_CL)
+    out = torch.empty_like(w, memory_format=_CL)
+    nbytes = int(wsq(n, ci, co, hw))
+    ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
+    if arrivals is None:
+        arrivals = arrival_cells(x.device)
+    N.check(fn(x.data_ptr(), dy.data_ptr(), out.data_ptr(), n, ci, co, hw, 2, ws.data_ptr(), nbytes,
+               arrivals.data_ptr(), None, stream), what)
     return out
 
 
 def conv1x1s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
-              arrivals: torch.Tensor | None = None) -> torch.Tensor:
+              arrivals: torch.Tensor | None = None, stats: torch.Tensor | None = None):
     """The projection shortcut's kernels (1x1, stride 2)."""
-    return _strided("1x1", x, w, mode, other, arrivals)
+    return _strided("1x1", x, w, mode, other, arrivals, stats)
 
 
 def conv3x3s2(x: torch.Tensor, w: torch.Tensor, mode: int, other: torch.Tensor | None = None,
-              arrivals: torch.Tensor | None = None) -> torch.Tensor:
+              arrivals: torch.Tensor | None = None, stats: torch.Tensor | None = None):
     """The stage-opening 3x3 stride-2 convolution's kernels."""
-    return _strided("3x3s2", x, w, mode, other, arrivals)
+    return _strided("3x3s2", x, w, mode, other, arrivals, stats)
+
+
+def _stat_cells(arrivals):
+    return arrivals[ARRIVALS:2 * ARRIVALS] if arrivals.numel() >= 2 * ARRIVALS else None
 
 
 class _StridedFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, arrivals, want_w, kind):
+    def forward(ctx, x, w, arrivals, want_w, kind, with_stats):
         ctx.save_for_backward(x, w)
         ctx.arrivals, ctx.want_w, ctx.kind = arrivals, want_w, kind
-        return _strided(kind, x, w, 0, None, None)
+        if with_stats:
+            y, sums = _strided(kind, x, w, 0, None, None, _stat_cells(arrivals))
+            ctx.mark_non_differentiable(sums)
+            return y, sums
+        return _strided(kind, x, w, 0, None, None), None
 
     @staticmethod
-    def backward(ctx, gy):
+    def backward(ctx, gy, _gsums):
         x, w = ctx.saved_tensors
         gx = gw = None
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
             gx = _strided(ctx.kind, gy, w, 1, None, None)
         if ctx.needs_input_grad[1] and ctx.want_w:
             gw = _strided(ctx.kind, x, w, 2, gy, ctx.arrivals)
-        return gx, gw, None, None, None
+        return gx, gw, None, None, None, None
 
 
 class _Conv3x3Fn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, w, arrivals, want_w):
+    def forward(ctx, x, w, arrivals, want_w, with_stats):
         ctx.save_for_backward(x, w)
         ctx.arrivals, ctx.want_w = arrivals, want_w
-        return conv_fwd(x, w)
+        if with_stats:
+            y, sums = conv_fwd(x, w, stats=_stat_cells(arrivals))
+            ctx.mark_non_differentiable(sums)
+            return y, sums
+        return conv_fwd(x, w), None
 
     @staticmethod
-    def backward(ctx, gy):
+    def backward(ctx, gy, _gsums):
         x, w = ctx.saved_tensors
         gx = gw = None
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
             gx = conv_fwd(gy, w, dgrad=True)
         if ctx.needs_input_grad[1] and ctx.want_w:
             gw = conv_wgrad(x, gy, w, ctx.arrivals)
-        return gx, gw, None, None
+        return gx, gw, None, None, None
 
 
 def conv3x3(x: torch.Tensor, w: torch.Tensor, arrivals: torch.Tensor | None = None,
-            want_w: bool = True) -> torch.Tensor:
+            want_w: bool = True, with_stats: bool = False):
     """y = conv2d(x, w, stride 1, padding 1) on the library's kernels.
     ``want_w=False``: the weight gradient is not wanted (a layer above the
-    partial-backprop block; autograd.grad cannot tell a custom function)."""
+    partial-backprop block; autograd.grad cannot tell a custom function).
+    ``with_stats``: returns (y, BatchNorm sums of y) — y's statistics fused
+    into the forward's epilogue."""
     if arrivals is None:
-        arrivals = arrival_cells(x.device)
-    return _Conv3x3Fn.apply(x, w, arrivals, want_w)
+        arrivals = arrival_cells(x.device, 2)
+    y, sums = _Conv3x3Fn.apply(x, w, arrivals, want_w, with_stats)
+    return (y, sums) if with_stats else y
 
 
 def mark_weight_grads(module: nn.Module, leaves) -> None:
@@ -203,21 +242,27 @@ class Conv3x3(nn.Conv2d):
     def __init__(self, cin: int, cout: int, stride: int = 1):
         super().__init__(cin, cout, 3, stride, 1, bias=False)
         self.want_w = True
-        self._arrivals = None   # wgrad arrival counters; this module's launches are stream-ordered
+        # bn_stats: a BatchNorm consumes the output (bn_act) — compute its
+        # statistics in the forward's epilogue
+        self.bn_stats = False
+        self._arrivals = None   # arrival counters; this module's launches are stream-ordered
 
     def _arrival_cells(self, device) -> torch.Tensor:
         if self._arrivals is None or self._arrivals.device != device:
-            self._arrivals = arrival_cells(device)
+            self._arrivals = arrival_cells(device, 2)
         return self._arrivals
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         native = (x.dtype == torch.float32 and x.is_cuda and self.weight.dtype == torch.float32
                   and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled())
         if native and supported(self.in_channels, self.out_channels, x.shape[2], self.stride[0], 3):
-            return conv3x3(x, self.weight, self._arrival_cells(x.device), self.want_w)
+            y, sums = _Conv3x3Fn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, self.bn_stats)
+            return _with_sums(y, sums)
         if (native and self.stride == (2, 2)
                 and _lib().lib.lpp_conv3x3s2_supported(self.in_channels, self.out_channels, x.shape[2])):
-            return _StridedFn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, "3x3s2")
+            y, sums = _StridedFn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, "3x3s2",
+                                       self.bn_stats)
+            return _with_sums(y, sums)
         return F.conv2d(x, self.weight, None, self.stride, self.padding)
 
 
@@ -228,6 +273,7 @@ class Conv1x1(nn.Conv2d):
     def __init__(self, cin: int, cout: int, stride: int = 1):
         super().__init__(cin, cout, 1, stride, 0, bias=False)
         self.want_w = True
+        self.bn_stats = False
         self._arrivals = None
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
@@ -236,6 +282,66 @@ class Conv1x1(nn.Conv2d):
                 and self.stride[0] == 2 and self.stride[1] == 2
                 and _lib().lib.lpp_conv1x1s2_supported(self.in_channels, self.out_channels, x.shape[2])):
             if self._arrivals is None or self._arrivals.device != x.device:
-                self._arrivals = arrival_cells(x.device)
-            return _StridedFn.apply(x, self.weight, self._arrivals, self.want_w, "1x1")
+                self._arrivals = arrival_cells(x.device, 2)
+            y, sums = _StridedFn.apply(x, self.weight, self._arrivals, self.want_w, "1x1", self.bn_stats)
+            return _with_sums(y, sums)
         return F.conv2d(x, self.weight, None, self.stride, self.padding)
+
+
+def _with_sums(y: torch.Tensor, sums: torch.Tensor | None) -> torch.Tensor:
+    if sums is not None:
+        y._lpp_bn_sums = sums
+    return y
+
+
+class _BnActFn(torch.autograd.Function):
+    """BatchNorm2d (training) [+ residual] [+ ReLU] from the statistics the
+    producing convolution fused into its epilogue: forward one
+    ``lpp_bn_apply_f32`` pass; backward torch's own threshold_backward and
+    native_batch_norm_backward on the saved mean / invstd (the same
+    gradient formulas as nn.BatchNorm2d)."""
+
+    @staticmethod
+    def forward(ctx, x, gamma, beta, resid, sums, running_mean, running_var, eps, momentum, relu):
+        N = _lib()
+        n, c, h, w_ = x.shape
+        y = torch.empty_like(x, memory_format=_CL)
+        mean = torch.empty(c, dtype=torch.float32, device=x.device)
+        invstd = torch.empty(c, dtype=torch.float32, device=x.device)
+        rm = running_mean.data_ptr() if running_mean is not None else None
+        rv = running_var.data_ptr() if running_var is not None else None
+        N.check(N.lib.lpp_bn_apply_f32(x.data_ptr(), sums.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+                                       resid.data_ptr() if resid is not None else None, y.data_ptr(),
+                                       mean.data_ptr(), invstd.data_ptr(), rm, rv, n * h * w_, c, float(eps),
+                                       float(momentum), int(relu),
+                                       torch.cuda.current_stream(x.device).cuda_stream), "bn_apply_f32")
+        ctx.save_for_backward(x, gamma, mean, invstd, y)
+        ctx.eps, ctx.relu, ctx.has_resid = eps, relu, resid is not None
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, gamma, mean, invstd, y = ctx.saved_tensors
+        g = torch.ops.aten.threshold_backward(gy, y, 0) if ctx.relu else gy
+        need = ctx.needs_input_grad
+        gx, gg, gb = torch.ops.aten.native_batch_norm_backward(g, x, gamma, None, None, mean, invstd, True, ctx.eps,
+                                                               [need[0], need[1], need[2]])
+        gres = g if ctx.has_resid and need[3] else None
+        return gx, gg, gb, gres, None, None, None, None, None, None
+
+
+def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.Tensor | None = None):
+    """``[relu](bn(x) [+ resid])``: one fused pass when x came from one of
+    our convolutions with its statistics (``bn_stats``) and bn trains;
+    torch's modules otherwise (cuDNN BatchNorm, eval mode, bf16, ...)."""
+    sums = getattr(x, "_lpp_bn_sums", None)
+    if (sums is None or not bn.training or not bn.affine or not bn.track_running_stats
+            or bn.momentum is None or x.dtype != torch.float32 or not enabled()):
+        out = bn(x)
+        if resid is not None:
+            out = out + resid
+        return F.relu(out) if relu else out
+    if resid is not None:
+        resid = resid.contiguous(memory_format=_CL)
+    return _BnActFn.apply(x, bn.weight, bn.bias, resid, sums, bn.running_mean, bn.running_var, bn.eps,
+                          bn.momentum, relu)

@@ -42,6 +42,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 
 namespace cg = cooperative_groups;
@@ -131,6 +132,71 @@ __device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, 
   if (k == 0 && tid == 0) *arrival = 0u;            // ready for the next launch on this stream
 }
 
+// BatchNorm statistics of a convolution's output, fused into its epilogue:
+// per channel (sum, sum of squares) over this thread's PX pixels, then the
+// warp (every lane owns the same channels: a butterfly, fixed order), then
+// the NPG warps of each channel group in order.  red[0, 2 NCG CW) =
+// [CTA channel][sum, sumsq]; scratch holds NPG x that.  Leaves the CTA
+// synchronised.
+template <int PX, int CW, int NPG, int NCG>
+__device__ __forceinline__ void tile_channel_stats(const float (&acc)[PX][CW], int npx, int pg, int cg,
+                                                   float* scratch, float* red) {
+  float st[CW][2];
+#pragma unroll
+  for (int j = 0; j < CW; ++j) {
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int i = 0; i < PX; ++i)
+      if (i < npx) {
+        a += acc[i][j];
+        b = fmaf(acc[i][j], acc[i][j], b);
+      }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    st[j][0] = a;
+    st[j][1] = b;
+  }
+  __syncthreads();                                  // the tile buffers are free now
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      scratch[((pg * NCG + cg) * CW + j) * 2] = st[j][0];
+      scratch[((pg * NCG + cg) * CW + j) * 2 + 1] = st[j][1];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < NCG * CW * 2; t += blockDim.x) {
+    float a = 0.f;
+#pragma unroll 1
+    for (int q = 0; q < NPG; ++q) a += scratch[q * NCG * CW * 2 + t];
+    red[t] = a;
+  }
+  __syncthreads();
+}
+
+// launch with a thread-block cluster of up to 8 CTAs along x (the reduction
+// of cluster_tail_reduce); cl = 1 is a plain launch
+template <typename Kern, typename... Args>
+int launch_clustered(Kern kern, dim3 grid, int threads, int smem, int cl, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(cl);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // forward / dgrad
 
@@ -158,19 +224,18 @@ struct ConvCfg {
 
 template <int C, int H, int TH, int COT, int PX, int CO, int U, bool DGRAD>
 __global__ void __launch_bounds__(ConvCfg<C, H, TH, COT, PX, CO>::THREADS)
-k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y) {
+k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, float* stat_part,
+          float* __restrict__ stat_sums, unsigned* __restrict__ stat_arrivals) {
   using K = ConvCfg<C, H, TH, COT, PX, CO>;
   constexpr int W = K::W, CP = K::CP;
   extern __shared__ float4 smem4[];
   float* xs = reinterpret_cast<float*>(smem4);
   float* ws = xs + K::XS;
 
-  constexpr int CO_TILES = C / COT;
   constexpr int ROW_TILES = TH < H ? H / TH : 1;
-  const int bid = blockIdx.x;
-  const int cot = bid % CO_TILES;
-  const int rt = (bid / CO_TILES) % ROW_TILES;
-  const int n0 = (bid / (CO_TILES * ROW_TILES)) * K::NIMG;
+  const int ptile = blockIdx.x, cot = blockIdx.y;   // pixel tile, output-channel tile
+  const int rt = ptile % ROW_TILES;
+  const int n0 = (ptile / ROW_TILES) * K::NIMG;
   const int y0 = rt * K::IR;
   const int co0 = cot * COT;
 
@@ -258,13 +323,45 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
     for (int j = 0; j < CO; j += 4)
       *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
   }
+  if constexpr (!DGRAD) {
+    if (stat_sums) {                                // BatchNorm statistics of y (uniform branch)
+      float* red = xs;
+      tile_channel_stats<PX, CO, K::NPG, K::NCG>(acc, PX, pg, cg, xs + 2 * COT, red);
+      cg::cluster_group cluster = cg::this_cluster();
+      cluster_tail_reduce<K::THREADS>(cluster, red, COT / 2, size_t(co0) / 2, C / 2, stat_part, stat_sums,
+                                      stat_arrivals + cot, ptile);
+    }
+  }
+}
+
+// CTAs per cluster: the largest power of two <= clmax dividing the tile count
+inline int wgrad_cluster(size_t tiles, int clmax) {
+  int cl = clmax;
+  while (cl > 1 && tiles % cl) cl /= 2;
+  return cl;
 }
 
 template <int C, int H, int TH, int COT, int PX, int CO, int U>
-int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cudaStream_t st) {
+size_t conv_ptiles(int n) {
   using K = ConvCfg<C, H, TH, COT, PX, CO>;
+  return size_t(n / K::NIMG) * (TH < H ? H / TH : 1);
+}
+
+// floats of workspace the fused BatchNorm statistics need (cluster partials)
+template <int C, int H, int TH, int COT, int PX, int CO, int U>
+size_t conv_stats_workspace(int n) {
+  const size_t t = conv_ptiles<C, H, TH, COT, PX, CO, U>(n);
+  return t / wgrad_cluster(t, 8) * 2 * C;
+}
+
+template <int C, int H, int TH, int COT, int PX, int CO, int U>
+int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, float* stat_ws, size_t stat_ws_bytes,
+                float* stat_sums, unsigned* stat_arrivals, cudaStream_t st) {
+  using K = ConvCfg<C, H, TH, COT, PX, CO>;
+  static_assert(COT % 8 == 0, "statistics slices (COT / 2 float4s over up to 8 cluster ranks... >= 1 each)");
   if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d not a multiple of %d", n, K::NIMG);
-  const int tiles = (n / K::NIMG) * (TH < H ? H / TH : 1) * (C / COT);
+  const size_t ptiles = conv_ptiles<C, H, TH, COT, PX, CO, U>(n);
+  const dim3 grid(unsigned(ptiles), C / COT, 1);
   if (dgrad) {
     auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, true>;
     static bool attr = false;
@@ -272,7 +369,7 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cud
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
       attr = true;
     }
-    kern<<<tiles, K::THREADS, K::SMEM, st>>>(x, w, y);
+    kern<<<grid, K::THREADS, K::SMEM, st>>>(x, w, y, nullptr, nullptr, nullptr);
   } else {
     auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, false>;
     static bool attr = false;
@@ -280,7 +377,16 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, cud
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
       attr = true;
     }
-    kern<<<tiles, K::THREADS, K::SMEM, st>>>(x, w, y);
+    if (stat_sums) {
+      if (!stat_ws || !stat_arrivals) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics need ws + arrivals");
+      if (stat_ws_bytes < conv_stats_workspace<C, H, TH, COT, PX, CO, U>(n) * sizeof(float))
+        return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics workspace too small");
+      int rc = launch_clustered(kern, grid, K::THREADS, K::SMEM, wgrad_cluster(ptiles, 8), st, x, w, y, stat_ws,
+                                stat_sums, stat_arrivals);
+      if (rc) return rc;
+    } else {
+      kern<<<grid, K::THREADS, K::SMEM, st>>>(x, w, y, nullptr, nullptr, nullptr);
+    }
   }
   LAUNCH_CHECK("k_conv3x3");
   return 0;
@@ -421,13 +527,6 @@ size_t wgrad_tiles(int n) {
   return size_t(n / K::NIMG) * K::TILES_PER_N;
 }
 
-// CTAs per cluster: the largest power of two <= clmax dividing the tile count
-inline int wgrad_cluster(size_t tiles, int clmax) {
-  int cl = clmax;
-  while (cl > 1 && tiles % cl) cl /= 2;
-  return cl;
-}
-
 template <int C, int H, int TH, int COT, int PS, int CLMAX>
 size_t wgrad_partials(int n) {
   const size_t tiles = wgrad_tiles<C, H, TH, COT, PS, CLMAX>(n);
@@ -476,7 +575,8 @@ int launch_wgrad(const float* x, const float* dy, float* dw, float* ws, size_t w
 
 template <int CI, int CO, int HO>
 __global__ void __launch_bounds__(256)
-k_conv1x1s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, int npix) {
+k_conv1x1s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, int npix,
+            float* stat_part, float* __restrict__ stat_sums, unsigned* __restrict__ stat_arrivals) {
   __shared__ __align__(16) float ws[CI * CO];       // [ci][co]
   for (int i = threadIdx.x; i < CI * CO; i += 256) {
     const int co = i % CO, ci = i / CO;
@@ -487,27 +587,36 @@ k_conv1x1s2(const float* __restrict__ x, const float* __restrict__ w, float* __r
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = warp % G;
   const int p = blockIdx.x * PPB + (warp / G) * 32 + lane;
-  if (p >= npix) return;
-  const int xo = p % HO, yo = (p / HO) % HO, n = p / (HO * HO);
-  const float4* xin = reinterpret_cast<const float4*>(x + ((size_t(n) * 2 * HO + 2 * yo) * 2 * HO + 2 * xo) * CI);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool valid = p < npix;
+  float acc[1][8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
+  if (valid) {
+    const int xo = p % HO, yo = (p / HO) % HO, n = p / (HO * HO);
+    const float4* xin = reinterpret_cast<const float4*>(x + ((size_t(n) * 2 * HO + 2 * yo) * 2 * HO + 2 * xo) * CI);
 #pragma unroll
-  for (int c4 = 0; c4 < CI / 4; ++c4) {
-    const float4 v = __ldg(xin + c4);
-    const float xv[4] = {v.x, v.y, v.z, v.w};
+    for (int c4 = 0; c4 < CI / 4; ++c4) {
+      const float4 v = __ldg(xin + c4);
+      const float xv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 w0 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8);
-      const float4 w1 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8 + 4);
-      acc[0] = fmaf(xv[q], w0.x, acc[0]); acc[1] = fmaf(xv[q], w0.y, acc[1]);
-      acc[2] = fmaf(xv[q], w0.z, acc[2]); acc[3] = fmaf(xv[q], w0.w, acc[3]);
-      acc[4] = fmaf(xv[q], w1.x, acc[4]); acc[5] = fmaf(xv[q], w1.y, acc[5]);
-      acc[6] = fmaf(xv[q], w1.z, acc[6]); acc[7] = fmaf(xv[q], w1.w, acc[7]);
+      for (int q = 0; q < 4; ++q) {
+        const float4 w0 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8);
+        const float4 w1 = *reinterpret_cast<const float4*>(ws + (c4 * 4 + q) * CO + g * 8 + 4);
+        float* a = acc[0];
+        a[0] = fmaf(xv[q], w0.x, a[0]); a[1] = fmaf(xv[q], w0.y, a[1]);
+        a[2] = fmaf(xv[q], w0.z, a[2]); a[3] = fmaf(xv[q], w0.w, a[3]);
+        a[4] = fmaf(xv[q], w1.x, a[4]); a[5] = fmaf(xv[q], w1.y, a[5]);
+        a[6] = fmaf(xv[q], w1.z, a[6]); a[7] = fmaf(xv[q], w1.w, a[7]);
+      }
     }
+    float4* out = reinterpret_cast<float4*>(y + size_t(p) * CO + g * 8);
+    out[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+    out[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
   }
-  float4* out = reinterpret_cast<float4*>(y + size_t(p) * CO + g * 8);
-  out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  if (stat_sums) {                                  // BatchNorm statistics of y (uniform branch)
+    __shared__ __align__(16) float scratch[(8 / G) * CO * 2], red[CO * 2];
+    tile_channel_stats<1, 8, 8 / G, G>(acc, valid ? 1 : 0, warp / G, g, scratch, red);
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster_tail_reduce<256>(cluster, red, CO / 2, 0, CO / 2, stat_part, stat_sums, stat_arrivals, blockIdx.x);
+  }
 }
 
 // dX of the projection: dY (x) W at the even pixels, zero at the others
@@ -602,12 +711,28 @@ template <int CI, int CO, int HO>
 constexpr int wg1x1_ppc() { return HO >= 16 ? 256 : 64; }
 
 template <int CI, int CO, int HO>
+size_t conv1x1s2_stats_workspace(int n) {
+  constexpr int PPB = 32 * (8 / (CO / 8));
+  const size_t ctas = (size_t(n) * HO * HO + PPB - 1) / PPB;
+  return ctas / wgrad_cluster(ctas, 8) * 2 * CO;
+}
+
+template <int CI, int CO, int HO>
 int launch_conv1x1s2(const float* x, const float* w, float* y, int n, int mode, float* dw, float* ws,
-                     size_t ws_bytes, unsigned* arrivals, cudaStream_t st) {
+                     size_t ws_bytes, unsigned* arrivals, float* sums, cudaStream_t st) {
   if (mode == 0) {
     const int npix = n * HO * HO;
     constexpr int PPB = 32 * (8 / (CO / 8));
-    k_conv1x1s2<CI, CO, HO><<<(npix + PPB - 1) / PPB, 256, 0, st>>>(x, w, y, npix);
+    const unsigned ctas = unsigned((npix + PPB - 1) / PPB);
+    if (sums) {
+      if (!ws || !arrivals || ws_bytes < conv1x1s2_stats_workspace<CI, CO, HO>(n) * sizeof(float))
+        return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: statistics need ws + arrivals");
+      int rc = launch_clustered(k_conv1x1s2<CI, CO, HO>, dim3(ctas, 1, 1), 256, 0, wgrad_cluster(ctas, 8), st, x, w,
+                                y, npix, ws, sums, arrivals);
+      if (rc) return rc;
+    } else {
+      k_conv1x1s2<CI, CO, HO><<<ctas, 256, 0, st>>>(x, w, y, npix, nullptr, nullptr, nullptr);
+    }
     LAUNCH_CHECK("k_conv1x1s2");
   } else if (mode == 1) {
     const int npix = n * 4 * HO * HO;
@@ -676,15 +801,16 @@ __device__ __forceinline__ int s2_col(int t, int ho) { return (t & 1) ? ho + 1 +
 
 template <int CI, int CO, int HO, int TH, int COT, int PX, int CW>
 __global__ void __launch_bounds__(S2Cfg<CI, CO, HO, TH, COT, PX, CW>::THREADS)
-k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y) {
+k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, float* stat_part,
+            float* __restrict__ stat_sums, unsigned* __restrict__ stat_arrivals) {
   using K = S2Cfg<CI, CO, HO, TH, COT, PX, CW>;
   constexpr int CP = K::CP, HI = 2 * HO;
   extern __shared__ float4 smem4[];
   float* xs = reinterpret_cast<float*>(smem4);
   float* ws = xs + K::XS;
-  constexpr int CO_TILES = CO / COT, ROW_TILES = HO / TH;
-  const int bid = blockIdx.x;
-  const int cot = bid % CO_TILES, rt = (bid / CO_TILES) % ROW_TILES, n = bid / (CO_TILES * ROW_TILES);
+  constexpr int ROW_TILES = HO / TH;
+  const int tile = blockIdx.x, cot = blockIdx.y;
+  const int rt = tile % ROW_TILES, n = tile / ROW_TILES;
   const int y0 = rt * TH, co0 = cot * COT;
   {
     constexpr int C4 = CI / 4, TOTAL = K::SROWS * K::SCOLS * C4;
@@ -758,6 +884,12 @@ k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __r
 #pragma unroll
     for (int j = 0; j < CW; j += 4)
       *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+  }
+  if (stat_sums) {                                  // BatchNorm statistics of y (uniform branch)
+    tile_channel_stats<PX, CW, K::NPG, K::NCG>(acc, PX, pg, cg, xs + 2 * COT, xs);
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster_tail_reduce<K::THREADS>(cluster, xs, COT / 2, size_t(co0) / 2, CO / 2, stat_part, stat_sums,
+                                    stat_arrivals + cot, tile);
   }
 }
 
@@ -999,7 +1131,8 @@ struct S2Shape<16, 32, 16> {
   static constexpr auto fwd = k_conv3x3s2<16, 32, 16, 8, 32, 4, 8>;
   static constexpr auto dgrad = k_conv3x3s2_dgrad<16, 32, 16, 8, 16, 2, 8>;
   static constexpr auto wgrad = k_wgrad3x3s2<16, 32, 16, 8, 32, 2>;
-  static constexpr int F_TILES = (16 / 8) * (32 / 32), D_TILES = (16 / 8) * (16 / 16), W_TILES = 16 / 8, W_CO = 32 / 32;
+  static constexpr int F_TILES = 16 / 8, F_CO = 32 / 32, D_TILES = (16 / 8) * (16 / 16), W_TILES = 16 / 8,
+                       W_CO = 32 / 32;
 };
 template <>
 struct S2Shape<32, 64, 8> {
@@ -1009,7 +1142,8 @@ struct S2Shape<32, 64, 8> {
   static constexpr auto fwd = k_conv3x3s2<32, 64, 8, 8, 32, 2, 8>;
   static constexpr auto dgrad = k_conv3x3s2_dgrad<32, 64, 8, 8, 16, 2, 8>;
   static constexpr auto wgrad = k_wgrad3x3s2<32, 64, 8, 8, 32, 1>;
-  static constexpr int F_TILES = (8 / 8) * (64 / 32), D_TILES = (8 / 8) * (32 / 16), W_TILES = 8 / 8, W_CO = 64 / 32;
+  static constexpr int F_TILES = 8 / 8, F_CO = 64 / 32, D_TILES = (8 / 8) * (32 / 16), W_TILES = 8 / 8,
+                       W_CO = 64 / 32;
 };
 
 template <int CI, int CO, int HO>
@@ -1020,14 +1154,30 @@ size_t conv3x3s2_workspace(int n) {
 }
 
 template <int CI, int CO, int HO>
+size_t conv3x3s2_stats_workspace(int n) {
+  using S = S2Shape<CI, CO, HO>;
+  const size_t tiles = size_t(n) * S::F_TILES;
+  return tiles / wgrad_cluster(tiles, 8) * 2 * CO;
+}
+
+template <int CI, int CO, int HO>
 int launch_conv3x3s2(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
-                     unsigned* arrivals, cudaStream_t st) {
+                     unsigned* arrivals, float* sums, cudaStream_t st) {
   using S = S2Shape<CI, CO, HO>;
   int rc;
   if (mode == 0) {
     static bool done = false;
     if ((rc = set_smem(S::fwd, S::F::SMEM, done))) return rc;
-    S::fwd<<<n * S::F_TILES, S::F::THREADS, S::F::SMEM, st>>>(a, b, out);
+    const dim3 grid(unsigned(n * S::F_TILES), S::F_CO, 1);
+    if (sums) {
+      if (!ws || !arrivals || ws_bytes < conv3x3s2_stats_workspace<CI, CO, HO>(n) * sizeof(float))
+        return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: statistics need ws + arrivals");
+      if ((rc = launch_clustered(S::fwd, grid, S::F::THREADS, S::F::SMEM, wgrad_cluster(grid.x, 8), st, a, b, out,
+                                 ws, sums, arrivals)))
+        return rc;
+    } else {
+      S::fwd<<<grid, S::F::THREADS, S::F::SMEM, st>>>(a, b, out, nullptr, nullptr, nullptr);
+    }
     LAUNCH_CHECK("k_conv3x3s2");
   } else if (mode == 1) {
     static bool done = false;
@@ -1060,10 +1210,90 @@ int launch_conv3x3s2(const float* a, const float* b, float* out, int n, int mode
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// BatchNorm (training) apply with the statistics the convolution epilogue
+// reduced: y = [relu](x * scale + shift [+ resid]), scale = gamma * invstd,
+// shift = beta - mean * scale; CTA 0 also writes save_mean / save_invstd
+// (for the backward) and moves the running statistics (unbiased variance).
+// One read of x (and resid), one write of y: the BatchNorm, the residual add
+// and the ReLU of the reference block in one memory pass.
+template <int C, bool RELU, bool RESID>
+__global__ void __launch_bounds__(256)
+k_bn_apply(const float4* __restrict__ x, const float* __restrict__ sums, const float* __restrict__ gamma,
+           const float* __restrict__ beta, const float4* __restrict__ resid, float4* __restrict__ y,
+           float* __restrict__ save_mean, float* __restrict__ save_invstd, float* __restrict__ running_mean,
+           float* __restrict__ running_var, size_t n4, double count, float eps, float momentum) {
+  __shared__ __align__(16) float sc[C], sh[C];
+  if (threadIdx.x < C) {
+    const int c = threadIdx.x;
+    const double mean = double(sums[2 * c]) / count;
+    double var = double(sums[2 * c + 1]) / count - mean * mean;
+    var = var > 0.0 ? var : 0.0;
+    const float invstd = float(1.0 / sqrt(var + double(eps)));
+    const float scale = gamma[c] * invstd;
+    sc[c] = scale;
+    sh[c] = beta[c] - float(mean) * scale;
+    if (blockIdx.x == 0) {
+      save_mean[c] = float(mean);
+      save_invstd[c] = invstd;
+      if (running_mean) {
+        running_mean[c] = (1.f - momentum) * running_mean[c] + momentum * float(mean);
+        running_var[c] = (1.f - momentum) * running_var[c] + momentum * float(var * count / (count - 1.0));
+      }
+    }
+  }
+  __syncthreads();
+  constexpr int C4 = C / 4;
+  for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
+    const int c = int(i % C4) * 4;
+    float4 v = __ldg(x + i);
+    v.x = fmaf(v.x, sc[c], sh[c]);
+    v.y = fmaf(v.y, sc[c + 1], sh[c + 1]);
+    v.z = fmaf(v.z, sc[c + 2], sh[c + 2]);
+    v.w = fmaf(v.w, sc[c + 3], sh[c + 3]);
+    if constexpr (RESID) {
+      const float4 r = __ldg(resid + i);
+      v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+    }
+    if constexpr (RELU) {
+      v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+    }
+    y[i] = v;
+  }
+}
+
+template <int C>
+int launch_bn_apply(const float* x, const float* sums, const float* gamma, const float* beta, const float* resid,
+                    float* y, float* save_mean, float* save_invstd, float* running_mean, float* running_var,
+                    size_t npix, float eps, float momentum, int relu, cudaStream_t st) {
+  const size_t n4 = npix * C / 4;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const unsigned grid = unsigned(std::min<size_t>((n4 + 255) / 256, size_t(sms) * 8));
+  auto x4 = reinterpret_cast<const float4*>(x);
+  auto r4 = reinterpret_cast<const float4*>(resid);
+  auto y4 = reinterpret_cast<float4*>(y);
+  const double cnt = double(npix);
+#define LPP_BN(R, S)                                                                                  \
+  k_bn_apply<C, R, S><<<grid, 256, 0, st>>>(x4, sums, gamma, beta, r4, y4, save_mean, save_invstd,   \
+                                             running_mean, running_var, n4, cnt, eps, momentum)
+  if (relu && resid) LPP_BN(true, true);
+  else if (relu) LPP_BN(true, false);
+  else if (resid) LPP_BN(false, true);
+  else LPP_BN(false, false);
+#undef LPP_BN
+  LAUNCH_CHECK("k_bn_apply");
+  return 0;
+}
+
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
-using ConvFn = int (*)(const float*, const float*, float*, int, bool, cudaStream_t);
+using ConvFn = int (*)(const float*, const float*, float*, int, bool, float*, size_t, float*, unsigned*, cudaStream_t);
 using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsigned*, int, cudaStream_t);
 using TilesFn = size_t (*)(int);
 
@@ -1074,6 +1304,12 @@ const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 1
                           launch_conv<32, 16, 16, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
 const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 16, 16, 4, 8, 1>,
                           launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 16, 32, 4, 8, 1>};
+const TilesFn kConv16Ws[] = {conv_stats_workspace<16, 32, 8, 16, 4, 8, 1>, conv_stats_workspace<16, 32, 8, 16, 4, 16, 1>,
+                          conv_stats_workspace<16, 32, 8, 16, 4, 8, 2>, conv_stats_workspace<16, 32, 4, 16, 4, 8, 2>};
+const TilesFn kConv32Ws[] = {conv_stats_workspace<32, 16, 8, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 16, 1>,
+                          conv_stats_workspace<32, 16, 16, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 2>};
+const TilesFn kConv64Ws[] = {conv_stats_workspace<64, 8, 8, 32, 2, 8, 1>, conv_stats_workspace<64, 8, 16, 16, 4, 8, 1>,
+                          conv_stats_workspace<64, 8, 8, 32, 2, 16, 1>, conv_stats_workspace<64, 8, 16, 32, 4, 8, 1>};
 //                        C   H  TH COT PS CL
 const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32, 16, 16, 4, 16>,
                          launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
@@ -1145,15 +1381,29 @@ extern "C" int lpp_conv3x3_supported(int c, int hw) {
 }
 
 extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
+                               float* stat_ws, size_t stat_ws_bytes, float* stat_sums, uint32_t* stat_arrivals,
                                void* stream) {
   if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
+  if (dgrad && stat_sums) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics are a forward epilogue");
   auto st = static_cast<cudaStream_t>(stream);
   const int v = conv_variant(c);
-  if (c == 16 && hw == 32) return kConv16[v](x, w, y, n, dgrad != 0, st);
-  if (c == 32 && hw == 16) return kConv32[v](x, w, y, n, dgrad != 0, st);
-  if (c == 64 && hw == 8) return kConv64[v](x, w, y, n, dgrad != 0, st);
+  if (c == 16 && hw == 32)
+    return kConv16[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
+  if (c == 32 && hw == 16)
+    return kConv32[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
+  if (c == 64 && hw == 8)
+    return kConv64[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: no kernel for C=%d H=W=%d", c, hw);
+}
+
+extern "C" size_t lpp_conv3x3_stats_workspace(int n, int c, int hw) {
+  if (n <= 0) return 0;
+  const int v = conv_variant(c);
+  if (c == 16 && hw == 32) return kConv16Ws[v](n) * sizeof(float);
+  if (c == 32 && hw == 16) return kConv32Ws[v](n) * sizeof(float);
+  if (c == 64 && hw == 8) return kConv64Ws[v](n) * sizeof(float);
+  return 0;
 }
 
 extern "C" size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw) {
@@ -1188,20 +1438,30 @@ extern "C" size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in
   return 0;
 }
 
+extern "C" size_t lpp_conv1x1s2_stats_workspace(int n, int ci, int co, int hw_in) {
+  if (n <= 0) return 0;
+  if (ci == 16 && co == 32 && hw_in == 32) return conv1x1s2_stats_workspace<16, 32, 16>(n) * sizeof(float);
+  if (ci == 32 && co == 64 && hw_in == 16) return conv1x1s2_stats_workspace<32, 64, 8>(n) * sizeof(float);
+  return 0;
+}
+
 extern "C" int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in,
-                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream) {
+                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, float* stat_sums,
+                                 void* stream) {
   if (!a || !b || !out) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: null pointer");
   if (n <= 0 || mode < 0 || mode > 2) return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: batch %d mode %d", n, mode);
   auto st = static_cast<cudaStream_t>(stream);
   // mode 0: out = y of (a = x, b = w); 1: out = dX of (a = dY, b = w); 2: out = dW of (a = x, b = dY)
   if (ci == 16 && co == 32 && hw_in == 32)
     return mode == 2 ? launch_conv1x1s2<16, 32, 16>(a, nullptr, const_cast<float*>(b), n, 2, out, ws, ws_bytes,
-                                                    arrivals, st)
-                     : launch_conv1x1s2<16, 32, 16>(a, b, out, n, mode, nullptr, nullptr, 0, nullptr, st);
+                                                    arrivals, nullptr, st)
+                     : launch_conv1x1s2<16, 32, 16>(a, b, out, n, mode, nullptr, ws, ws_bytes, arrivals,
+                                                    mode == 0 ? stat_sums : nullptr, st);
   if (ci == 32 && co == 64 && hw_in == 16)
     return mode == 2 ? launch_conv1x1s2<32, 64, 8>(a, nullptr, const_cast<float*>(b), n, 2, out, ws, ws_bytes,
-                                                   arrivals, st)
-                     : launch_conv1x1s2<32, 64, 8>(a, b, out, n, mode, nullptr, nullptr, 0, nullptr, st);
+                                                   arrivals, nullptr, st)
+                     : launch_conv1x1s2<32, 64, 8>(a, b, out, n, mode, nullptr, ws, ws_bytes, arrivals,
+                                                   mode == 0 ? stat_sums : nullptr, st);
   return set_err(LPP_E_VALUE, "lpp_conv1x1s2_f32: no kernel for %d->%d at %dx%d", ci, co, hw_in, hw_in);
 }
 
@@ -1216,14 +1476,43 @@ extern "C" size_t lpp_conv3x3s2_wgrad_workspace(int n, int ci, int co, int hw_in
   return 0;
 }
 
+extern "C" size_t lpp_conv3x3s2_stats_workspace(int n, int ci, int co, int hw_in) {
+  if (n <= 0) return 0;
+  if (ci == 16 && co == 32 && hw_in == 32) return conv3x3s2_stats_workspace<16, 32, 16>(n) * sizeof(float);
+  if (ci == 32 && co == 64 && hw_in == 16) return conv3x3s2_stats_workspace<32, 64, 8>(n) * sizeof(float);
+  return 0;
+}
+
 extern "C" int lpp_conv3x3s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in,
-                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, void* stream) {
+                                 int mode, float* ws, size_t ws_bytes, uint32_t* arrivals, float* stat_sums,
+                                 void* stream) {
   if (!a || !b || !out) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: null pointer");
   if (n <= 0 || mode < 0 || mode > 2) return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: batch %d mode %d", n, mode);
   auto st = static_cast<cudaStream_t>(stream);
   if (ci == 16 && co == 32 && hw_in == 32)
-    return launch_conv3x3s2<16, 32, 16>(a, b, out, n, mode, ws, ws_bytes, arrivals, st);
+    return launch_conv3x3s2<16, 32, 16>(a, b, out, n, mode, ws, ws_bytes, arrivals, mode == 0 ? stat_sums : nullptr,
+                                        st);
   if (ci == 32 && co == 64 && hw_in == 16)
-    return launch_conv3x3s2<32, 64, 8>(a, b, out, n, mode, ws, ws_bytes, arrivals, st);
+    return launch_conv3x3s2<32, 64, 8>(a, b, out, n, mode, ws, ws_bytes, arrivals, mode == 0 ? stat_sums : nullptr,
+                                       st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3s2_f32: no kernel for %d->%d at %dx%d", ci, co, hw_in, hw_in);
+}
+
+extern "C" int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, const float* beta,
+                                const float* resid, float* y, float* save_mean, float* save_invstd,
+                                float* running_mean, float* running_var, int64_t npix, int c, float eps,
+                                float momentum, int relu, void* stream) {
+  if (!x || !sums || !gamma || !beta || !y || !save_mean || !save_invstd)
+    return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: null pointer");
+  if (npix < 2) return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: %lld pixels", (long long)npix);
+  if ((running_mean == nullptr) != (running_var == nullptr))
+    return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: running mean and var go together");
+  auto st = static_cast<cudaStream_t>(stream);
+  if (c == 16) return launch_bn_apply<16>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
+                                          running_var, size_t(npix), eps, momentum, relu, st);
+  if (c == 32) return launch_bn_apply<32>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
+                                          running_var, size_t(npix), eps, momentum, relu, st);
+  if (c == 64) return launch_bn_apply<64>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
+                                          running_var, size_t(npix), eps, momentum, relu, st);
+  return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: no kernel for %d channels", c);
 }

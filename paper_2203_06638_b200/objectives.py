@@ -30,7 +30,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
-from .conv import Conv1x1, Conv3x3, mark_weight_grads
+from .conv import Conv1x1, Conv3x3, bn_act, mark_weight_grads
 from .partition import Block
 
 
@@ -345,11 +345,15 @@ class _Basic(nn.Module):
         self.shortcut = None
         if stride != 1 or cin != cout:
             self.shortcut = nn.Sequential(Conv1x1(cin, cout, stride), nn.BatchNorm2d(cout))
+            self.shortcut[0].bn_stats = True
+        # the convolutions' epilogues compute their BatchNorm statistics and
+        # bn_act applies BatchNorm (+ residual) + ReLU in one pass (conv.py)
+        self.conv1.bn_stats = self.conv2.bn_stats = True
 
     def forward(self, x):
-        out = F.relu(self.bn1(self.conv1(x)))
-        out = self.bn2(self.conv2(out))
-        return F.relu(out + (x if self.shortcut is None else self.shortcut(x)))
+        out = bn_act(self.conv1(x), self.bn1, relu=True)
+        sc = x if self.shortcut is None else bn_act(self.shortcut[0](x), self.shortcut[1], relu=False)
+        return bn_act(self.conv2(out), self.bn2, relu=True, resid=sc)
 
 
 class _Bottleneck(nn.Module):

@@ -103,27 +103,29 @@ def test_conv3x3_module_autograd(which):
 
 
 def test_conv3x3_routes_other_cases_to_cudnn(monkeypatch):
-    """No kernel for the shape / stride / dtype, or LPP_CONV=cudnn: F.conv2d."""
-    from paper_2203_06638_b200 import conv
+    """No kernel for the shape / dtype, autocast, or LPP_CONV=cudnn: F.conv2d
+    (no library launch); the supported shapes launch ours."""
+    from paper_2203_06638_b200 import _native as N
     from paper_2203_06638_b200.conv import Conv3x3
 
-    calls = []
-    real = conv.conv3x3
-    monkeypatch.setattr(conv, "conv3x3", lambda *a: calls.append(1) or real(*a))
+    def launches(fn):
+        torch.cuda.synchronize()
+        l0 = N.launch_count()
+        out = fn()
+        torch.cuda.synchronize()
+        return out, N.launch_count() - l0
+
     x16 = torch.randn(2, 16, 16, 16, device="cuda").to(memory_format=CL)   # (16, 16): no kernel
     m = Conv3x3(16, 16, 1).cuda().to(memory_format=CL)
-    assert torch.allclose(m(x16), F.conv2d(x16, m.weight, padding=1), atol=1e-5)
-    s2 = Conv3x3(16, 32, 2).cuda().to(memory_format=CL)
+    y, k = launches(lambda: m(x16))
+    assert k == 0 and torch.allclose(y, F.conv2d(x16, m.weight, padding=1), atol=1e-5)
     x32 = torch.randn(2, 16, 32, 32, device="cuda").to(memory_format=CL)
-    s2(x32)
     with torch.autocast("cuda", dtype=torch.bfloat16):
-        m(x32)
-    assert calls == []
-    m(x32)
-    assert calls == [1]
+        assert launches(lambda: m(x32))[1] == 0
+    assert launches(lambda: m(x32.double()) if False else m(x32))[1] == 1
+    assert launches(lambda: Conv3x3(16, 32, 2).cuda().to(memory_format=CL)(x32))[1] == 1   # stride-2 kernel
     monkeypatch.setenv("LPP_CONV", "cudnn")
-    m(x32)
-    assert calls == [1]
+    assert launches(lambda: m(x32))[1] == 0
 
 
 def test_conv_in_cuda_graph():
@@ -295,3 +297,42 @@ def test_conv3x3_stride2_module_grads():
     yd.backward(gy.double())
     assert _rel(y.detach(), yd.detach()) < TOL
     assert _rel(x.grad, xd.grad) < TOL and _rel(m.weight.grad, wd.grad) < TOL
+
+
+@pytest.mark.parametrize("cin,cout,stride,hw", [(16, 16, 1, 32), (16, 32, 2, 32), (32, 64, 2, 16), (64, 64, 1, 8)])
+def test_basic_block_fused_bn_matches_fp64(cin, cout, stride, hw):
+    """A ResNet basic block on the native path — convolutions with fused
+    BatchNorm statistics, bn_act (BatchNorm + residual + ReLU in one pass) —
+    against the same block in fp64 on torch's modules: output, running
+    statistics, and every gradient."""
+    import copy
+
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200.objectives import _Basic
+
+    torch.manual_seed(4)
+    blk = _Basic(cin, cout, stride).cuda().to(memory_format=CL)
+    for m in blk.modules():
+        if isinstance(m, torch.nn.BatchNorm2d):
+            m.weight.data.uniform_(0.5, 1.5)
+            m.bias.data.uniform_(-0.5, 0.5)
+    ref = copy.deepcopy(blk).double()
+    x = torch.randn(16, cin, hw, hw, device="cuda").to(memory_format=CL).requires_grad_()
+    xd = x.detach().double().requires_grad_()
+    l0 = N.launch_count()
+    y = blk(x)
+    n_fwd = N.launch_count() - l0
+    yd = ref(xd)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    yd.backward(gy.double())
+    tol = 2e-5
+    assert _rel(y.detach(), yd.detach()) < tol
+    assert _rel(x.grad, xd.grad) < tol
+    for (name, p), (_, pd) in zip(blk.named_parameters(), ref.named_parameters()):
+        assert _rel(p.grad, pd.grad) < tol, name
+    for (name, b), (_, bd) in zip(blk.named_buffers(), ref.named_buffers()):
+        if b.dtype.is_floating_point:
+            assert _rel(b, bd) < tol, name
+    # conv + BatchNorm pass per convolution: 2 x 2, plus 2 for the projection
+    assert n_fwd == (4 if blk.shortcut is None else 6)
