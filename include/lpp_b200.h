@@ -647,6 +647,16 @@ int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, cons
                      const float* resid, float* y, float* save_mean, float* save_invstd,
                      float* running_mean, float* running_var, int64_t npix, int c, float eps,
                      float momentum, int relu, void* stream);
+/* its backward in two launches (a cluster-reduced per-channel sum, then
+ * the elementwise pass): g = gy [* (y > 0)]; dx = gamma * invstd * (g -
+ * mean(g) - xhat * mean(g xhat)); gres = g (the residual branch, NULL:
+ * none); ggamma / gbeta = sum g xhat / sum g (NULL: not wanted); dx NULL:
+ * not wanted.  ws: lpp_bn_backward_workspace bytes; arrivals as
+ * lpp_conv3x3_wgrad_f32. */
+size_t lpp_bn_backward_workspace(int64_t npix, int c);
+int lpp_bn_backward_f32(const float* gy, const float* y, const float* x, const float* mean, const float* invstd,
+                        const float* gamma, float* dx, float* gres, float* ggamma, float* gbeta, float* ws,
+                        size_t ws_bytes, uint32_t* arrivals, int64_t npix, int c, int relu, void* stream);
 size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in);
 int lpp_conv1x1s2_f32(const float* a, const float* b, float* out, int n, int ci, int co, int hw_in, int mode,
                       float* ws, size_t ws_bytes, uint32_t* arrivals, float* stat_sums, void* stream);

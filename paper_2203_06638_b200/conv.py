@@ -172,6 +172,7 @@ def _stat_cells(arrivals):
 class _StridedFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, arrivals, want_w, kind, with_stats):
+        ctx.set_materialize_grads(False)    # no zero-filled gradient for the statistics output
         ctx.save_for_backward(x, w)
         ctx.arrivals, ctx.want_w, ctx.kind = arrivals, want_w, kind
         if with_stats:
@@ -184,6 +185,8 @@ class _StridedFn(torch.autograd.Function):
     def backward(ctx, gy, _gsums):
         x, w = ctx.saved_tensors
         gx = gw = None
+        if gy is None:
+            return (None,) * len(ctx.needs_input_grad)
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
             gx = _strided(ctx.kind, gy, w, 1, None, None)
         if ctx.needs_input_grad[1] and ctx.want_w:
@@ -194,6 +197,7 @@ class _StridedFn(torch.autograd.Function):
 class _Conv3x3Fn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, arrivals, want_w, with_stats):
+        ctx.set_materialize_grads(False)    # no zero-filled gradient for the statistics output
         ctx.save_for_backward(x, w)
         ctx.arrivals, ctx.want_w = arrivals, want_w
         if with_stats:
@@ -206,6 +210,8 @@ class _Conv3x3Fn(torch.autograd.Function):
     def backward(ctx, gy, _gsums):
         x, w = ctx.saved_tensors
         gx = gw = None
+        if gy is None:
+            return (None,) * len(ctx.needs_input_grad)
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
             gx = conv_fwd(gy, w, dgrad=True)
         if ctx.needs_input_grad[1] and ctx.want_w:
@@ -297,12 +303,12 @@ def _with_sums(y: torch.Tensor, sums: torch.Tensor | None) -> torch.Tensor:
 class _BnActFn(torch.autograd.Function):
     """BatchNorm2d (training) [+ residual] [+ ReLU] from the statistics the
     producing convolution fused into its epilogue: forward one
-    ``lpp_bn_apply_f32`` pass; backward torch's own threshold_backward and
-    native_batch_norm_backward on the saved mean / invstd (the same
-    gradient formulas as nn.BatchNorm2d)."""
+    ``lpp_bn_apply_f32`` pass; backward ``lpp_bn_backward_f32`` (ReLU mask,
+    per-channel sums, dx / residual gradient / dgamma / dbeta: the formulas
+    of torch.native_batch_norm_backward in train mode)."""
 
     @staticmethod
-    def forward(ctx, x, gamma, beta, resid, sums, running_mean, running_var, eps, momentum, relu):
+    def forward(ctx, x, gamma, beta, resid, sums, running_mean, running_var, eps, momentum, relu, cells):
         N = _lib()
         n, c, h, w_ = x.shape
         y = torch.empty_like(x, memory_format=_CL)
@@ -316,18 +322,28 @@ class _BnActFn(torch.autograd.Function):
                                        float(momentum), int(relu),
                                        torch.cuda.current_stream(x.device).cuda_stream), "bn_apply_f32")
         ctx.save_for_backward(x, gamma, mean, invstd, y)
-        ctx.eps, ctx.relu, ctx.has_resid = eps, relu, resid is not None
+        ctx.relu, ctx.has_resid, ctx.cells = relu, resid is not None, cells
         return y
 
     @staticmethod
     def backward(ctx, gy):
+        N = _lib()
         x, gamma, mean, invstd, y = ctx.saved_tensors
-        g = torch.ops.aten.threshold_backward(gy, y, 0) if ctx.relu else gy
+        n, c, h, w_ = x.shape
         need = ctx.needs_input_grad
-        gx, gg, gb = torch.ops.aten.native_batch_norm_backward(g, x, gamma, None, None, mean, invstd, True, ctx.eps,
-                                                               [need[0], need[1], need[2]])
-        gres = g if ctx.has_resid and need[3] else None
-        return gx, gg, gb, gres, None, None, None, None, None, None
+        gy = gy.contiguous(memory_format=_CL)
+        gx = torch.empty_like(x, memory_format=_CL) if need[0] and _will_run(ctx.next_functions[0][0]) else None
+        gres = torch.empty_like(x, memory_format=_CL) if ctx.has_resid and need[3] else None
+        gg = torch.empty_like(gamma) if need[1] else None
+        gb = torch.empty_like(gamma) if need[2] else None
+        nbytes = int(N.lib.lpp_bn_backward_workspace(n * h * w_, c))
+        ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        N.check(N.lib.lpp_bn_backward_f32(gy.data_ptr(), y.data_ptr(), x.data_ptr(), mean.data_ptr(),
+                                          invstd.data_ptr(), gamma.data_ptr(), ptr(gx), ptr(gres), ptr(gg), ptr(gb),
+                                          ws.data_ptr(), nbytes, ctx.cells.data_ptr(), n * h * w_, c, int(ctx.relu),
+                                          torch.cuda.current_stream(x.device).cuda_stream), "bn_backward_f32")
+        return gx, gg, gb, gres, None, None, None, None, None, None, None
 
 
 def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.Tensor | None = None):
@@ -343,5 +359,9 @@ def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.
         return F.relu(out) if relu else out
     if resid is not None:
         resid = resid.contiguous(memory_format=_CL)
+    cells = getattr(bn, "_lpp_arrivals", None)
+    if cells is None or cells.device != x.device:
+        # the backward's one-launch reduction; this module's launches are stream-ordered
+        cells = bn._lpp_arrivals = arrival_cells(x.device)
     return _BnActFn.apply(x, bn.weight, bn.bias, resid, sums, bn.running_mean, bn.running_var, bn.eps,
-                          bn.momentum, relu)
+                          bn.momentum, relu, cells)

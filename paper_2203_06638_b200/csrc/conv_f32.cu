@@ -1290,6 +1290,160 @@ int launch_bn_apply(const float* x, const float* sums, const float* gamma, const
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// BatchNorm (training) backward with the ReLU mask and the residual branch
+// fused: g = gy [* (y > 0)];  sums = (sum g, sum g * xhat) per channel (one
+// launch, cluster-reduced, fixed order);  dx = gamma * invstd * (g -
+// mean(g) - xhat * mean(g * xhat));  gres = g;  dgamma / dbeta = the sums.
+// The same formulas as torch.native_batch_norm_backward (train mode).
+
+// reduce grid: a multiple of 8 CTAs (clusters of 8), at most 4 per SM
+inline unsigned bn_reduce_ctas(size_t n4) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess)
+      sms = 148;
+  }
+  size_t want = (n4 + 255) / 256;
+  want = std::min<size_t>(want, size_t(sms) * 4);
+  want = (want + 7) / 8 * 8;
+  return unsigned(want);
+}
+
+template <int C, bool RELU>
+__global__ void __launch_bounds__(256)
+k_bn_bwd_reduce(const float4* __restrict__ gy, const float4* __restrict__ y, const float4* __restrict__ x,
+                const float* __restrict__ mean, const float* __restrict__ invstd, float* part,
+                float* __restrict__ sums, unsigned* __restrict__ arrival, size_t n4) {
+  constexpr int C4 = C / 4;
+  static_assert(256 % C4 == 0, "a thread keeps one channel quad");
+  __shared__ __align__(16) float sm[256 * 8];
+  __shared__ __align__(16) float red[2 * C];
+  const int q = threadIdx.x % C4;
+  const float4 mu = *reinterpret_cast<const float4*>(mean + 4 * q);
+  const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
+  float sg[4] = {0.f, 0.f, 0.f, 0.f}, sgx[4] = {0.f, 0.f, 0.f, 0.f};
+  for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
+    float4 g = __ldg(gy + i);
+    if constexpr (RELU) {
+      const float4 o = __ldg(y + i);
+      g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
+      g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+    }
+    const float4 v = __ldg(x + i);
+    sg[0] += g.x; sg[1] += g.y; sg[2] += g.z; sg[3] += g.w;
+    sgx[0] = fmaf(g.x, (v.x - mu.x) * is.x, sgx[0]);
+    sgx[1] = fmaf(g.y, (v.y - mu.y) * is.y, sgx[1]);
+    sgx[2] = fmaf(g.z, (v.z - mu.z) * is.z, sgx[2]);
+    sgx[3] = fmaf(g.w, (v.w - mu.w) * is.w, sgx[3]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    sm[threadIdx.x * 8 + k] = sg[k];
+    sm[threadIdx.x * 8 + 4 + k] = sgx[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * C) {                       // channel c, (sum g | sum g xhat), threads of its quad in order
+    const int c = threadIdx.x >> 1, which = threadIdx.x & 1;
+    const int cq = c / 4, ck = c % 4;
+    float a = 0.f;
+#pragma unroll 4
+    for (int t = cq; t < 256; t += C4) a += sm[t * 8 + which * 4 + ck];
+    red[threadIdx.x] = a;
+  }
+  __syncthreads();
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster_tail_reduce<256>(cluster, red, C / 2, 0, C / 2, part, sums, arrival, blockIdx.x);
+}
+
+template <int C, bool RELU, bool DX, bool RESID>
+__global__ void __launch_bounds__(256)
+k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, const float4* __restrict__ x,
+               const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ gamma,
+               const float* __restrict__ sums, float4* __restrict__ dx, float4* __restrict__ gres,
+               float* __restrict__ ggamma, float* __restrict__ gbeta, size_t n4, float inv_count) {
+  constexpr int C4 = C / 4;
+  __shared__ __align__(16) float ka[C], kb[C], kc[C], mu[C], is[C];
+  if (threadIdx.x < C) {
+    const int c = threadIdx.x;
+    const float sg = sums[2 * c], sgx = sums[2 * c + 1];
+    ka[c] = gamma[c] * invstd[c];
+    kb[c] = sg * inv_count;
+    kc[c] = sgx * inv_count;
+    mu[c] = mean[c];
+    is[c] = invstd[c];
+    if (blockIdx.x == 0) {
+      if (ggamma) ggamma[c] = sgx;
+      if (gbeta) gbeta[c] = sg;
+    }
+  }
+  __syncthreads();
+  if constexpr (!DX && !RESID) return;
+  for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
+    const int c = int(i % C4) * 4;
+    float4 g = __ldg(gy + i);
+    if constexpr (RELU) {
+      const float4 o = __ldg(y + i);
+      g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
+      g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+    }
+    if constexpr (RESID) gres[i] = g;
+    if constexpr (DX) {
+      const float4 v = __ldg(x + i);
+      float4 d;
+      d.x = ka[c] * (g.x - kb[c] - (v.x - mu[c]) * is[c] * kc[c]);
+      d.y = ka[c + 1] * (g.y - kb[c + 1] - (v.y - mu[c + 1]) * is[c + 1] * kc[c + 1]);
+      d.z = ka[c + 2] * (g.z - kb[c + 2] - (v.z - mu[c + 2]) * is[c + 2] * kc[c + 2]);
+      d.w = ka[c + 3] * (g.w - kb[c + 3] - (v.w - mu[c + 3]) * is[c + 3] * kc[c + 3]);
+      dx[i] = d;
+    }
+  }
+}
+
+template <int C>
+int launch_bn_backward(const float* gy, const float* y, const float* x, const float* mean, const float* invstd,
+                       const float* gamma, float* dx, float* gres, float* ggamma, float* gbeta, float* ws,
+                       size_t ws_bytes, unsigned* arrivals, size_t npix, int relu, cudaStream_t st) {
+  const size_t n4 = npix * C / 4;
+  const unsigned rctas = bn_reduce_ctas(n4);
+  if (ws_bytes < size_t(rctas / 8 + 1) * 2 * C * sizeof(float) + 2 * C * sizeof(float))
+    return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: workspace too small");
+  float* sums = ws;                                 // [C][2]
+  float* part = ws + 2 * C;
+  auto gy4 = reinterpret_cast<const float4*>(gy);
+  auto y4 = reinterpret_cast<const float4*>(y);
+  auto x4 = reinterpret_cast<const float4*>(x);
+  int rc = relu ? launch_clustered(k_bn_bwd_reduce<C, true>, dim3(rctas), 256, 0, 8, st, gy4, y4, x4, mean, invstd,
+                                   part, sums, arrivals, n4)
+                : launch_clustered(k_bn_bwd_reduce<C, false>, dim3(rctas), 256, 0, 8, st, gy4, y4, x4, mean, invstd,
+                                   part, sums, arrivals, n4);
+  if (rc) return rc;
+  LAUNCH_CHECK("k_bn_bwd_reduce");
+  const unsigned actas = dx || gres ? unsigned(std::min<size_t>((n4 + 255) / 256, size_t(rctas) * 2)) : 1u;
+  const float inv = float(1.0 / double(npix));
+  auto dx4 = reinterpret_cast<float4*>(dx);
+  auto gr4 = reinterpret_cast<float4*>(gres);
+#define LPP_BNB(R, D, S)                                                                               \
+  k_bn_bwd_apply<C, R, D, S><<<actas, 256, 0, st>>>(gy4, y4, x4, mean, invstd, gamma, sums, dx4, gr4,  \
+                                                    ggamma, gbeta, n4, inv)
+#define LPP_BNB_R(R)                    \
+  if (dx && gres) LPP_BNB(R, true, true);     \
+  else if (dx) LPP_BNB(R, true, false);       \
+  else if (gres) LPP_BNB(R, false, true);     \
+  else LPP_BNB(R, false, false)
+  if (relu) {
+    LPP_BNB_R(true);
+  } else {
+    LPP_BNB_R(false);
+  }
+#undef LPP_BNB_R
+#undef LPP_BNB
+  LAUNCH_CHECK("k_bn_bwd_apply");
+  return 0;
+}
+
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
@@ -1515,4 +1669,27 @@ extern "C" int lpp_bn_apply_f32(const float* x, const float* sums, const float* 
   if (c == 64) return launch_bn_apply<64>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
                                           running_var, size_t(npix), eps, momentum, relu, st);
   return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: no kernel for %d channels", c);
+}
+
+extern "C" size_t lpp_bn_backward_workspace(int64_t npix, int c) {
+  if (npix <= 0 || (c != 16 && c != 32 && c != 64)) return 0;
+  const unsigned r = bn_reduce_ctas(size_t(npix) * c / 4);
+  return (size_t(r / 8 + 1) * 2 * c + 2 * c) * sizeof(float);
+}
+
+extern "C" int lpp_bn_backward_f32(const float* gy, const float* y, const float* x, const float* mean,
+                                   const float* invstd, const float* gamma, float* dx, float* gres, float* ggamma,
+                                   float* gbeta, float* ws, size_t ws_bytes, uint32_t* arrivals, int64_t npix, int c,
+                                   int relu, void* stream) {
+  if (!gy || !x || !mean || !invstd || !gamma || !ws || !arrivals || (relu && !y))
+    return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: null pointer");
+  if (npix < 2) return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: %lld pixels", (long long)npix);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (c == 16) return launch_bn_backward<16>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+                                             arrivals, size_t(npix), relu, st);
+  if (c == 32) return launch_bn_backward<32>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+                                             arrivals, size_t(npix), relu, st);
+  if (c == 64) return launch_bn_backward<64>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+                                             arrivals, size_t(npix), relu, st);
+  return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: no kernel for %d channels", c);
 }

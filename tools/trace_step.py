@@ -47,7 +47,7 @@ for n, _, d in rows:
 T = sum(tot.values())
 OURS = ("k_apply", "k_snapshot", "k_average", "k_accum", "k_gather", "k_publish", "k_set_i64",
         "k_classify", "k_sample", "k_conv3x3", "k_wgrad3x3", "k_wgrad_reduce", "k_conv1x1s2",
-        "k_fma_probe")
+        "k_fma_probe", "k_bn_apply", "k_bn_bwd")
 
 
 def is_ours(k):
@@ -62,7 +62,7 @@ lines = [f"# {len(rows)} kernels in the timed region of {K * U + U} minibatches 
          f"(ResNet-20 LPP-SGD U=4 B=128, {'bf16' if '--bf16' in sys.argv else 'fp32'} convolutions, "
          f"native loop); summed kernel time {T / 1e3:.1f} ms "
          f"over a {span / 1e3:.1f} ms span (4 streams overlap)",
-         f"# our kernels (K1-K5, in-graph sampler, fp32 3x3 convolutions): {100 * mine / T:.2f}% of "
+         f"# our kernels (K1-K5, in-graph sampler, fp32 convolutions, fused BatchNorm): {100 * mine / T:.2f}% of "
          f"summed kernel time",
          "share%   total_us   n   kernel"]
 for k, v in tot.most_common():
