@@ -120,14 +120,35 @@ __device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, 
   __threadfence();
   const float4* all = reinterpret_cast<const float4*>(part) + off4 + k * slice4;
   float4* out = reinterpret_cast<float4*>(dw) + off4 + k * slice4;
-  for (int i = tid; i < slice4; i += THREADS) {
+  // G thread groups split the cluster partials (group g: c = g, g + G, ...),
+  // then the G sums are added in group order: fixed order, and short
+  // dependent-load chains when the slice is narrow
+  constexpr int GMAX = 16;
+  __shared__ float4 gsum[THREADS];
+  const int G = slice4 >= THREADS ? 1 : (THREADS / slice4 < GMAX ? THREADS / slice4 : GMAX);
+  const int lanes = slice4 >= THREADS ? THREADS : slice4;
+  for (int i0 = 0; i0 < slice4; i0 += lanes) {
+    const int i = i0 + tid % lanes, g = tid / lanes;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int c = 0; c < nclusters; ++c) {
-      const float4 v = __ldcg(all + size_t(c) * total4 + i);
-      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    if (g < G && i < slice4) {
+#pragma unroll 4
+      for (int c = g; c < nclusters; c += G) {
+        const float4 v = __ldcg(all + size_t(c) * total4 + i);
+        a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+      }
     }
-    out[i] = a;
+    if (G > 1) {
+      if (g < G) gsum[g * lanes + tid % lanes] = a;
+      __syncthreads();
+      if (g == 0 && i < slice4) {
+        for (int q = 1; q < G; ++q) {
+          const float4 v = gsum[q * lanes + tid];
+          a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+      }
+      __syncthreads();
+    }
+    if (g == 0 && i < slice4) out[i] = a;
   }
   if (k == 0 && tid == 0) *arrival = 0u;            // ready for the next launch on this stream
 }
@@ -288,7 +309,7 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
   // stalls)
 #pragma unroll 1
   for (int s = 0; s < 3; ++s) {
-#pragma unroll(U)
+#pragma unroll(U % 10)
     for (int c4 = 0; c4 < C / 4; ++c4) {
       float4 a[PX + 2];
 #pragma unroll
@@ -305,11 +326,22 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
             const float4 t = *reinterpret_cast<const float4*>(wp + q * COT + j);
             wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
           }
+          if constexpr (U / 10 == 0) {
 #pragma unroll
-          for (int i = 0; i < PX; ++i) {
-            const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : q == 2 ? a[i + r].z : a[i + r].w;
+            for (int i = 0; i < PX; ++i) {
+              const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : q == 2 ? a[i + r].z : a[i + r].w;
 #pragma unroll
-            for (int j = 0; j < CO; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+              for (int j = 0; j < CO; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+            }
+          } else {
+            float av[PX];
+#pragma unroll
+            for (int i = 0; i < PX; ++i)
+              av[i] = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : q == 2 ? a[i + r].z : a[i + r].w;
+#pragma unroll
+            for (int j = 0; j < CO; ++j)
+#pragma unroll
+              for (int i = 0; i < PX; ++i) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
           }
         }
       }
@@ -708,7 +740,7 @@ k_conv1x1s2_wgrad(const float* __restrict__ x, const float* __restrict__ dy, flo
 }
 
 template <int CI, int CO, int HO>
-constexpr int wg1x1_ppc() { return HO >= 16 ? 256 : 64; }
+constexpr int wg1x1_ppc() { return 64; }
 
 template <int CI, int CO, int HO>
 size_t conv1x1s2_stats_workspace(int n) {
@@ -1339,18 +1371,29 @@ k_bn_bwd_reduce(const float4* __restrict__ gy, const float4* __restrict__ y, con
     sgx[2] = fmaf(g.z, (v.z - mu.z) * is.z, sgx[2]);
     sgx[3] = fmaf(g.w, (v.w - mu.w) * is.w, sgx[3]);
   }
+  // lanes of a warp that share a channel quad (lane % C4): butterfly over
+  // the offsets >= C4, then the 8 warps in order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    sm[threadIdx.x * 8 + k] = sg[k];
-    sm[threadIdx.x * 8 + 4 + k] = sgx[k];
-  }
+  for (int off = 16; off >= C4; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sg[k] += __shfl_xor_sync(0xffffffffu, sg[k], off);
+      sgx[k] += __shfl_xor_sync(0xffffffffu, sgx[k], off);
+    }
+  if (lane < C4)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sm[(warp * C4 + lane) * 8 + k] = sg[k];
+      sm[(warp * C4 + lane) * 8 + 4 + k] = sgx[k];
+    }
   __syncthreads();
-  if (threadIdx.x < 2 * C) {                       // channel c, (sum g | sum g xhat), threads of its quad in order
+  if (threadIdx.x < 2 * C) {                       // channel c, (sum g | sum g xhat)
     const int c = threadIdx.x >> 1, which = threadIdx.x & 1;
     const int cq = c / 4, ck = c % 4;
     float a = 0.f;
-#pragma unroll 4
-    for (int t = cq; t < 256; t += C4) a += sm[t * 8 + which * 4 + ck];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) a += sm[(w * C4 + cq) * 8 + which * 4 + ck];
     red[threadIdx.x] = a;
   }
   __syncthreads();
@@ -1380,7 +1423,7 @@ k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, cons
     }
   }
   __syncthreads();
-  if constexpr (!DX && !RESID) return;
+  if constexpr (DX || RESID) {
   for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
     const int c = int(i % C4) * 4;
     float4 g = __ldg(gy + i);
@@ -1399,6 +1442,7 @@ k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, cons
       d.w = ka[c + 3] * (g.w - kb[c + 3] - (v.w - mu[c + 3]) * is[c + 3] * kc[c + 3]);
       dx[i] = d;
     }
+  }
   }
 }
 
@@ -1452,18 +1496,18 @@ using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsi
 using TilesFn = size_t (*)(int);
 
 //                     C   H  TH COT PX CO U
-const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 8, 16, 4, 16, 1>,
-                          launch_conv<16, 32, 8, 16, 4, 8, 2>, launch_conv<16, 32, 4, 16, 4, 8, 2>};
-const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 16, 1>,
-                          launch_conv<32, 16, 16, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 2>};
-const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 16, 16, 4, 8, 1>,
-                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 16, 32, 4, 8, 1>};
-const TilesFn kConv16Ws[] = {conv_stats_workspace<16, 32, 8, 16, 4, 8, 1>, conv_stats_workspace<16, 32, 8, 16, 4, 16, 1>,
-                          conv_stats_workspace<16, 32, 8, 16, 4, 8, 2>, conv_stats_workspace<16, 32, 4, 16, 4, 8, 2>};
-const TilesFn kConv32Ws[] = {conv_stats_workspace<32, 16, 8, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 16, 1>,
-                          conv_stats_workspace<32, 16, 16, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 2>};
-const TilesFn kConv64Ws[] = {conv_stats_workspace<64, 8, 8, 32, 2, 8, 1>, conv_stats_workspace<64, 8, 16, 16, 4, 8, 1>,
-                          conv_stats_workspace<64, 8, 8, 32, 2, 16, 1>, conv_stats_workspace<64, 8, 16, 32, 4, 8, 1>};
+const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 8, 16, 4, 8, 11>,
+                          launch_conv<16, 32, 8, 16, 4, 8, 2>, launch_conv<16, 32, 8, 16, 4, 8, 12>};
+const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 11>,
+                          launch_conv<32, 16, 16, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 12>};
+const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 8, 32, 2, 8, 11>,
+                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 8, 32, 2, 16, 11>};
+const TilesFn kConv16Ws[] = {conv_stats_workspace<16, 32, 8, 16, 4, 8, 1>, conv_stats_workspace<16, 32, 8, 16, 4, 8, 11>,
+                          conv_stats_workspace<16, 32, 8, 16, 4, 8, 2>, conv_stats_workspace<16, 32, 8, 16, 4, 8, 12>};
+const TilesFn kConv32Ws[] = {conv_stats_workspace<32, 16, 8, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 11>,
+                          conv_stats_workspace<32, 16, 16, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 12>};
+const TilesFn kConv64Ws[] = {conv_stats_workspace<64, 8, 8, 32, 2, 8, 1>, conv_stats_workspace<64, 8, 8, 32, 2, 8, 11>,
+                          conv_stats_workspace<64, 8, 8, 32, 2, 16, 1>, conv_stats_workspace<64, 8, 8, 32, 2, 16, 11>};
 //                        C   H  TH COT PS CL
 const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32, 16, 16, 4, 16>,
                          launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
