@@ -654,6 +654,13 @@ int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, cons
  * not wanted.  ws: lpp_bn_backward_workspace bytes; arrivals as
  * lpp_conv3x3_wgrad_f32. */
 size_t lpp_bn_backward_workspace(int64_t npix, int c);
+/* The CIFAR stem (3 -> 16, 3x3, 32 x 32) reading the input batch in NCHW:
+ * mode 0 y = conv(a = x, b = w) (+ BatchNorm statistics into stat_sums);
+ * mode 2 dW [16][3][3][4] (ci padded) of (a = x, b = dY); ws of
+ * lpp_stem_workspace bytes, arrivals as lpp_conv3x3_wgrad_f32. */
+size_t lpp_stem_workspace(int n);
+int lpp_stem_f32(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
+                 uint32_t* arrivals, float* stat_sums, void* stream);
 int lpp_bn_backward_f32(const float* gy, const float* y, const float* x, const float* mean, const float* invstd,
                         const float* gamma, float* dx, float* gres, float* ggamma, float* gbeta, float* ws,
                         size_t ws_bytes, uint32_t* arrivals, int64_t npix, int c, int relu, void* stream);

@@ -194,6 +194,57 @@ class _StridedFn(torch.autograd.Function):
         return gx, gw, None, None, None, None
 
 
+def stem(x: torch.Tensor, w: torch.Tensor, mode: int, dy: torch.Tensor | None = None,
+         arrivals: torch.Tensor | None = None, stats: torch.Tensor | None = None):
+    """The CIFAR stem (3 -> 16, 3x3, 32 x 32) on NCHW input: mode 0 y
+    (channels-last; with ``stats`` cells: (y, BatchNorm sums)); mode 2 dW."""
+    N = _lib()
+    n = x.shape[0]
+    x = x.contiguous()                                  # NCHW, as gathered
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    nbytes = int(N.lib.lpp_stem_workspace(n))
+    if mode == 0:
+        y = torch.empty((n, 16, 32, 32), device=x.device, memory_format=_CL)
+        if stats is None:
+            N.check(N.lib.lpp_stem_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, 0, None, 0, None, None, stream),
+                    "stem_f32")
+            return y
+        ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
+        sums = torch.empty(32, dtype=torch.float32, device=x.device)
+        N.check(N.lib.lpp_stem_f32(x.data_ptr(), _ohwi(w).data_ptr(), y.data_ptr(), n, 0, ws.data_ptr(), nbytes,
+                                   stats.data_ptr(), sums.data_ptr(), stream), "stem_f32")
+        return y, sums
+    dy = dy.contiguous(memory_format=_CL)
+    ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
+    padded = torch.empty((16, 3, 3, 4), dtype=torch.float32, device=x.device)
+    if arrivals is None:
+        arrivals = arrival_cells(x.device)
+    N.check(N.lib.lpp_stem_f32(x.data_ptr(), dy.data_ptr(), padded.data_ptr(), n, 2, ws.data_ptr(), nbytes,
+                               arrivals.data_ptr(), None, stream), "stem_f32")
+    return padded[..., :3].permute(0, 3, 1, 2)          # [co, ci, kh, kw] over the OHWI(4) buffer
+
+
+class _StemFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, arrivals, want_w, with_stats):
+        ctx.set_materialize_grads(False)
+        ctx.save_for_backward(x)
+        ctx.arrivals, ctx.want_w = arrivals, want_w
+        w = _ohwi(w)
+        if with_stats:
+            y, sums = stem(x, w, 0, stats=_stat_cells(arrivals))
+            ctx.mark_non_differentiable(sums)
+            return y, sums
+        return stem(x, w, 0), None
+
+    @staticmethod
+    def backward(ctx, gy, _gsums):
+        (x,) = ctx.saved_tensors
+        if gy is None or not (ctx.needs_input_grad[1] and ctx.want_w):
+            return None, None, None, None, None
+        return None, stem(x, None, 2, gy, ctx.arrivals), None, None, None
+
+
 class _Conv3x3Fn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, arrivals, want_w, with_stats):
@@ -269,6 +320,12 @@ class Conv3x3(nn.Conv2d):
             y, sums = _StridedFn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, "3x3s2",
                                        self.bn_stats)
             return _with_sums(y, sums)
+        if (native and self.stride == (1, 1) and (self.in_channels, self.out_channels) == (3, 16)
+                and x.shape[2] == 32 and not x.requires_grad):
+            y, sums = _StemFn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, self.bn_stats)
+            return _with_sums(y, sums)
+        if self.weight.is_contiguous(memory_format=_CL) and not x.is_contiguous(memory_format=_CL):
+            x = x.contiguous(memory_format=_CL)
         return F.conv2d(x, self.weight, None, self.stride, self.padding)
 
 

@@ -1488,6 +1488,168 @@ int launch_bn_backward(const float* gy, const float* y, const float* x, const fl
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// The stem: 3 -> 16 channels, 3x3 stride 1 pad 1, 32 x 32, reading the
+// input batch in its gathered NCHW layout (no channels-last copy): a CTA
+// stages 10 input rows x 3 planes into [row][col][4] (channel 3 zero) and
+// computes 8 output rows x 16 channels, with the output's BatchNorm
+// statistics; its weight gradient has no input gradient beside it.
+constexpr int kStemTH = 8;
+
+__global__ void __launch_bounds__(128)
+k_stem_conv(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, float* stat_part,
+            float* __restrict__ stat_sums, unsigned* __restrict__ stat_arrivals) {
+  constexpr int H = 32, W = 32, CO = 16, CW = 8, PX = 4, SCOLS = W + 2, SROWS = kStemTH + 2;
+  __shared__ __align__(16) float xs[SROWS * SCOLS * 4];
+  __shared__ __align__(16) float ws[9 * 4 * CO];    // [tap][ci (3 + zero)][co]
+  const int tile = blockIdx.x;
+  const int n = tile / (H / kStemTH), y0 = (tile % (H / kStemTH)) * kStemTH;
+  for (int i = threadIdx.x; i < SROWS * SCOLS * 4; i += 128) xs[i] = 0.f;
+  for (int i = threadIdx.x; i < 9 * 4 * CO; i += 128) {
+    const int co = i % CO, ci = (i / CO) % 4, t = i / (4 * CO);
+    ws[i] = ci < 3 ? __ldg(w + (co * 9 + t) * 3 + ci) : 0.f;
+  }
+  __syncthreads();
+  // rows y0-1 .. y0+8 of the 3 planes: float4 along x, scattered into pixels
+  for (int i = threadIdx.x; i < SROWS * 3 * (W / 4); i += 128) {
+    const int x4 = i % (W / 4), c = (i / (W / 4)) % 3, srow = i / (3 * (W / 4));
+    const int gy = y0 - 1 + srow;
+    if (gy < 0 || gy >= H) continue;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + ((size_t(n) * 3 + c) * H + gy) * W) + x4);
+    float* d = xs + (srow * SCOLS + 1 + 4 * x4) * 4 + c;
+    d[0] = v.x; d[4] = v.y; d[8] = v.z; d[12] = v.w;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pg = warp % 2, cg = warp / 2;              // 2 pixel groups (4 rows each) x 2 channel groups
+  const int ty0 = pg * PX;
+  float acc[PX][CW];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    float4 a[PX + 2];
+#pragma unroll
+    for (int j = 0; j < PX + 2; ++j) a[j] = *reinterpret_cast<const float4*>(xs + ((ty0 + j) * SCOLS + lane + s) * 4);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        float wv[CW];
+#pragma unroll
+        for (int j = 0; j < CW; j += 4) {
+          const float4 t = *reinterpret_cast<const float4*>(ws + ((r * 3 + s) * 4 + q) * CO + cg * CW + j);
+          wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+        }
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+          const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : a[i + r].z;
+#pragma unroll
+          for (int j = 0; j < CW; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+        }
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < PX; ++i) {
+    float* out = y + ((size_t(n) * H + y0 + ty0 + i) * W + lane) * CO + cg * CW;
+#pragma unroll
+    for (int j = 0; j < CW; j += 4)
+      *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+  }
+  if (stat_sums) {
+    __shared__ __align__(16) float scratch[2 * 2 * CW * 2], red[2 * CO];
+    tile_channel_stats<PX, CW, 2, 2>(acc, PX, pg, cg, scratch, red);
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster_tail_reduce<128>(cluster, red, CO / 2, 0, CO / 2, stat_part, stat_sums, stat_arrivals, tile);
+  }
+}
+
+// dW[co][r][s][ci] (ci padded to 4 in the output: [16][3][3][4]) of the stem
+__global__ void __launch_bounds__(96)
+k_stem_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* part, float* __restrict__ dw,
+             unsigned* __restrict__ arrivals) {
+  constexpr int H = 32, W = 32, CO = 16, SCOLS = W + 2, SROWS = kStemTH + 2, DP = CO + 4;
+  __shared__ __align__(16) float xs[SROWS * SCOLS * 4];
+  __shared__ __align__(16) float ds[kStemTH * W * DP];
+  const int tile = blockIdx.x;
+  const int n = tile / (H / kStemTH), y0 = (tile % (H / kStemTH)) * kStemTH;
+  for (int i = threadIdx.x; i < SROWS * SCOLS * 4; i += 96) xs[i] = 0.f;
+  __syncthreads();
+  for (int i = threadIdx.x; i < SROWS * 3 * (W / 4); i += 96) {
+    const int x4 = i % (W / 4), c = (i / (W / 4)) % 3, srow = i / (3 * (W / 4));
+    const int gy = y0 - 1 + srow;
+    if (gy < 0 || gy >= H) continue;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(x + ((size_t(n) * 3 + c) * H + gy) * W) + x4);
+    float* d = xs + (srow * SCOLS + 1 + 4 * x4) * 4 + c;
+    d[0] = v.x; d[4] = v.y; d[8] = v.z; d[12] = v.w;
+  }
+  for (int i = threadIdx.x; i < kStemTH * W * (CO / 4); i += 96) {
+    const int j4 = i % (CO / 4), p = i / (CO / 4);
+    cp_async16(ds + p * DP + j4 * 4, dy + ((size_t(n) * H + y0) * W + p) * CO + j4 * 4, true);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // thread -> (co4, r, row): 4 x 3 x 8
+  const int tid = threadIdx.x;
+  const int co4 = tid % 4, r = (tid / 4) % 3, ty = tid / 12;
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+  const float* xr = xs + ((ty + r) * SCOLS) * 4;
+  const float* dr = ds + (ty * W) * DP + co4 * 4;
+  float4 xm = *reinterpret_cast<const float4*>(xr);
+  float4 x0 = *reinterpret_cast<const float4*>(xr + 4);
+#pragma unroll 4
+  for (int xx = 0; xx < W; ++xx) {
+    const float4 xp = *reinterpret_cast<const float4*>(xr + (xx + 2) * 4);
+    const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
+    const float dv[4] = {d.x, d.y, d.z, d.w};
+    const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+    xm = x0;
+    x0 = xp;
+  }
+  // rows in order: red[co][r][s][ci4] (576 floats) accumulated over the 8 row groups
+  __shared__ __align__(16) float red[CO * 9 * 4];
+  __syncthreads();
+#pragma unroll 1
+  for (int q = 0; q < kStemTH; ++q) {
+    if (ty == q) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          float4* d = reinterpret_cast<float4*>(red + ((co4 * 4 + c) * 9 + r * 3 + s) * 4);
+          float4 v = make_float4(acc[s][0][c], acc[s][1][c], acc[s][2][c], acc[s][3][c]);
+          if (q > 0) {
+            const float4 o = *d;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          *d = v;
+        }
+    }
+    __syncthreads();
+  }
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster_tail_reduce<96>(cluster, red, CO * 9, 0, CO * 9, part, dw, arrivals, tile);
+}
+
+size_t stem_partials(int n) {
+  const size_t tiles = size_t(n) * (32 / kStemTH);
+  return tiles / wgrad_cluster(tiles, 8);
+}
+
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
@@ -1736,4 +1898,36 @@ extern "C" int lpp_bn_backward_f32(const float* gy, const float* y, const float*
   if (c == 64) return launch_bn_backward<64>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
                                              arrivals, size_t(npix), relu, st);
   return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: no kernel for %d channels", c);
+}
+
+extern "C" size_t lpp_stem_workspace(int n) {
+  return n <= 0 ? 0 : stem_partials(n) * 16 * 9 * 4 * sizeof(float);
+}
+
+extern "C" int lpp_stem_f32(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
+                            uint32_t* arrivals, float* stat_sums, void* stream) {
+  // mode 0: out = y [n][32][32][16] of (a = x NCHW [n][3][32][32], b = w [16][3][3][3]), with the
+  //         BatchNorm statistics when stat_sums; mode 2: out = dW [16][3][3][4] of (a = x, b = dY)
+  if (!a || !b || !out || n <= 0) return set_err(LPP_E_VALUE, "lpp_stem_f32: bad argument");
+  auto st = static_cast<cudaStream_t>(stream);
+  const unsigned tiles = unsigned(n * (32 / kStemTH));
+  const int cl = wgrad_cluster(tiles, 8);
+  if (mode == 0) {
+    if (stat_sums) {
+      if (!ws || !arrivals || ws_bytes < lpp_stem_workspace(n))
+        return set_err(LPP_E_VALUE, "lpp_stem_f32: statistics need ws + arrivals");
+      int rc = launch_clustered(k_stem_conv, dim3(tiles), 128, 0, cl, st, a, b, out, ws, stat_sums, arrivals);
+      if (rc) return rc;
+    } else {
+      k_stem_conv<<<tiles, 128, 0, st>>>(a, b, out, nullptr, nullptr, nullptr);
+    }
+    LAUNCH_CHECK("k_stem_conv");
+    return 0;
+  }
+  if (mode != 2) return set_err(LPP_E_VALUE, "lpp_stem_f32: mode %d (the stem has no input gradient)", mode);
+  if (!ws || !arrivals || ws_bytes < lpp_stem_workspace(n)) return set_err(LPP_E_VALUE, "lpp_stem_f32: workspace");
+  int rc = launch_clustered(k_stem_wgrad, dim3(tiles), 96, 0, cl, st, a, b, ws, out, arrivals);
+  if (rc) return rc;
+  LAUNCH_CHECK("k_stem_wgrad");
+  return 0;
 }

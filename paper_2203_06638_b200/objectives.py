@@ -31,6 +31,7 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from .conv import Conv1x1, Conv3x3, bn_act, mark_weight_grads
+from .conv import enabled as conv_enabled
 from .partition import Block
 
 
@@ -386,7 +387,8 @@ class CifarResNet20(nn.Module):
 
     def __init__(self, num_classes=10):
         super().__init__()
-        self.conv1 = nn.Conv2d(3, 16, 3, 1, 1, bias=False)
+        self.conv1 = Conv3x3(3, 16, 1)        # the stem: native on NCHW input in fp32 (conv.py)
+        self.conv1.bn_stats = True
         self.bn1 = nn.BatchNorm2d(16)
         layers, cin = [], 16
         for cout, stride in ((16, 1), (32, 2), (64, 2)):
@@ -397,7 +399,7 @@ class CifarResNet20(nn.Module):
         self.fc = nn.Linear(64, num_classes)
 
     def forward(self, x):
-        out = F.relu(self.bn1(self.conv1(x)))
+        out = bn_act(self.conv1(x), self.bn1, relu=True)
         out = self.layers(out)
         out = F.adaptive_avg_pool2d(out, 1).flatten(1)
         return self.fc(out)
@@ -640,6 +642,7 @@ class ResNetObjective(ArenaObjective):
         cl = self.channels_last
 
         image_shape = tuple(self.image_shape)
+        stem_nchw = self.arch == "resnet20"
 
         def forward(xb):
             if shadow is not None:
@@ -648,7 +651,8 @@ class ResNetObjective(ArenaObjective):
                 xb = xb.permute(0, 3, 1, 2)
             if shadow is not None:
                 xb = xb.to(shadow_dtype)
-            if cl:
+            if cl and not (stem_nchw and xb.dtype == torch.float32 and conv_enabled()):
+                # (the fp32 ResNet-20 stem reads the gathered NCHW batch itself)
                 xb = xb.contiguous(memory_format=torch.channels_last)
             return module(xb)
 

@@ -336,3 +336,69 @@ def test_basic_block_fused_bn_matches_fp64(cin, cout, stride, hw):
             assert _rel(b, bd) < tol, name
     # conv + BatchNorm pass per convolution: 2 x 2, plus 2 for the projection
     assert n_fwd == (4 if blk.shortcut is None else 6)
+
+
+@pytest.mark.parametrize("n", [1, 3, 128])
+def test_stem_kernels_match_fp64(n):
+    """The stem (3 -> 16 on the NCHW batch): forward, fused statistics, dW."""
+    from paper_2203_06638_b200 import conv
+
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(n, 3, 32, 32, device="cuda", generator=g)                  # NCHW, as gathered
+    w = (torch.randn(16, 3, 3, 3, device="cuda", generator=g) / 5).to(memory_format=CL)
+    gy = torch.randn(n, 16, 32, 32, device="cuda", generator=g).to(memory_format=CL)
+    xd, wd = x.double(), w.double()
+    y_ref = F.conv2d(xd, wd, padding=1)
+    _, gw_ref, _ = torch.ops.aten.convolution_backward(gy.double(), xd, wd, None, (1, 1), (1, 1), (1, 1), False,
+                                                       (0, 0), 1, (False, True, False))
+    cells = conv.arrival_cells("cuda", 2)
+    y, sums = conv.stem(x, w, 0, stats=cells[8:])
+    assert y.is_contiguous(memory_format=CL) and _rel(y, y_ref) < TOL
+    ref_sums = torch.stack([y_ref.sum((0, 2, 3)), (y_ref * y_ref).sum((0, 2, 3))], 1).reshape(-1)
+    assert _rel(sums, ref_sums) < TOL
+    gw = conv.stem(x, None, 2, gy, cells)
+    assert gw.shape == (16, 3, 3, 3) and _rel(gw, gw_ref) < TOL
+    assert int(cells.abs().sum()) == 0
+
+
+def test_resnet20_native_matches_fp64(monkeypatch):
+    """The whole fp32 ResNet-20 on the native path (stem, 20 convolutions,
+    fused BatchNorm / residual / ReLU) against an fp64 copy on torch's
+    modules: logits, every parameter gradient, the running statistics —
+    each within 3x the error torch's own fp32 path (cuDNN, TF32 off) makes
+    against the same fp64 copy (20 BatchNorm layers amplify fp32 rounding),
+    and never above 2e-3."""
+    import copy
+
+    from paper_2203_06638_b200 import _native as N
+    from paper_2203_06638_b200.objectives import CifarResNet20
+
+    torch.backends.cudnn.allow_tf32 = False
+    torch.manual_seed(8)
+    model = CifarResNet20().cuda().to(memory_format=CL)
+    torch_fp32 = copy.deepcopy(model)
+    ref = copy.deepcopy(model).double()
+    x = torch.randn(64, 3, 32, 32, device="cuda")
+    gy = torch.randn(64, 10, device="cuda")
+    l0 = N.launch_count()
+    y = model(x)
+    assert N.launch_count() - l0 == 21 + 21          # stem + 18 + 2 projections, one BatchNorm pass each
+    y.backward(gy)
+    yd = ref(x.double())
+    yd.backward(gy.double())
+    monkeypatch.setenv("LPP_CONV", "cudnn")
+    yt = torch_fp32(x.contiguous(memory_format=CL))
+    yt.backward(gy)
+    monkeypatch.delenv("LPP_CONV")
+
+    def ok(ours, theirs, exact, what):
+        e_ours, e_torch = _rel(ours, exact), _rel(theirs, exact)
+        assert e_ours < max(1e-5, 3 * e_torch) and e_ours < 2e-3, (what, e_ours, e_torch)
+
+    ok(y.detach(), yt.detach(), yd.detach(), "logits")
+    for (name, p), (_, pt), (_, pd) in zip(model.named_parameters(), torch_fp32.named_parameters(),
+                                           ref.named_parameters()):
+        ok(p.grad, pt.grad, pd.grad, name)
+    for (name, b), (_, bt), (_, bd) in zip(model.named_buffers(), torch_fp32.named_buffers(), ref.named_buffers()):
+        if b.dtype.is_floating_point:
+            ok(b, bt, bd, name)
