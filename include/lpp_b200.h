@@ -656,7 +656,7 @@ int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, cons
 size_t lpp_bn_backward_workspace(int64_t npix, int c);
 /* The CIFAR stem (3 -> 16, 3x3, 32 x 32) reading the input batch in NCHW:
  * mode 0 y = conv(a = x, b = w) (+ BatchNorm statistics into stat_sums);
- * mode 2 dW [16][3][3][4] (ci padded) of (a = x, b = dY); ws of
+ * mode 2 dW [16][3][3][3] (OHWI) of (a = x, b = dY); ws of
  * lpp_stem_workspace bytes, arrivals as lpp_conv3x3_wgrad_f32. */
 size_t lpp_stem_workspace(int n);
 int lpp_stem_f32(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,

@@ -216,12 +216,14 @@ def stem(x: torch.Tensor, w: torch.Tensor, mode: int, dy: torch.Tensor | None = 
         return y, sums
     dy = dy.contiguous(memory_format=_CL)
     ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
-    padded = torch.empty((16, 3, 3, 4), dtype=torch.float32, device=x.device)
+    # OHWI, like the weight's arena view: the step's one multi-tensor gradient
+    # copy keeps its fast path only when every gradient is dense
+    dw = torch.empty((16, 3, 3, 3), dtype=torch.float32, device=x.device, memory_format=_CL)
     if arrivals is None:
         arrivals = arrival_cells(x.device)
-    N.check(N.lib.lpp_stem_f32(x.data_ptr(), dy.data_ptr(), padded.data_ptr(), n, 2, ws.data_ptr(), nbytes,
+    N.check(N.lib.lpp_stem_f32(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), n, 2, ws.data_ptr(), nbytes,
                                arrivals.data_ptr(), None, stream), "stem_f32")
-    return padded[..., :3].permute(0, 3, 1, 2)          # [co, ci, kh, kw] over the OHWI(4) buffer
+    return dw
 
 
 class _StemFn(torch.autograd.Function):

@@ -86,7 +86,7 @@ __device__ __forceinline__ void stage_rows(const float* __restrict__ x, float* x
 //   cluster partials in cluster order into dw.
 // red: this CTA's partial in shared memory (red4 float4s) covering float4s
 // [off4, off4 + red4) of a gradient of total4 float4s; part: [clusters][total4].
-template <int THREADS>
+template <int THREADS, bool COMPACT3 = false>
 __device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, const float* red, int red4,
                                                     size_t off4, int total4, float* part, float* dw,
                                                     unsigned* arrival, int tile) {
@@ -148,7 +148,14 @@ __device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, 
       }
       __syncthreads();
     }
-    if (g == 0 && i < slice4) out[i] = a;
+    if (g == 0 && i < slice4) {
+      if constexpr (COMPACT3) {                     // [..][4] partials -> [..][3] output (the stem's ci)
+        float* o = dw + (off4 + size_t(k) * slice4 + i) * 3;
+        o[0] = a.x; o[1] = a.y; o[2] = a.z;
+      } else {
+        out[i] = a;
+      }
+    }
   }
   if (k == 0 && tid == 0) *arrival = 0u;            // ready for the next launch on this stream
 }
@@ -1566,7 +1573,8 @@ k_stem_conv(const float* __restrict__ x, const float* __restrict__ w, float* __r
   }
 }
 
-// dW[co][r][s][ci] (ci padded to 4 in the output: [16][3][3][4]) of the stem
+// dW[co][r][s][ci] of the stem ([16][3][3][3], the OHWI weight layout;
+// the cluster partials keep ci padded to 4)
 __global__ void __launch_bounds__(96)
 k_stem_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* part, float* __restrict__ dw,
              unsigned* __restrict__ arrivals) {
@@ -1642,7 +1650,7 @@ k_stem_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* p
     __syncthreads();
   }
   cg::cluster_group cluster = cg::this_cluster();
-  cluster_tail_reduce<96>(cluster, red, CO * 9, 0, CO * 9, part, dw, arrivals, tile);
+  cluster_tail_reduce<96, true>(cluster, red, CO * 9, 0, CO * 9, part, dw, arrivals, tile);
 }
 
 size_t stem_partials(int n) {
@@ -1907,7 +1915,7 @@ extern "C" size_t lpp_stem_workspace(int n) {
 extern "C" int lpp_stem_f32(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
                             uint32_t* arrivals, float* stat_sums, void* stream) {
   // mode 0: out = y [n][32][32][16] of (a = x NCHW [n][3][32][32], b = w [16][3][3][3]), with the
-  //         BatchNorm statistics when stat_sums; mode 2: out = dW [16][3][3][4] of (a = x, b = dY)
+  //         BatchNorm statistics when stat_sums; mode 2: out = dW [16][3][3][3] of (a = x, b = dY)
   if (!a || !b || !out || n <= 0) return set_err(LPP_E_VALUE, "lpp_stem_f32: bad argument");
   auto st = static_cast<cudaStream_t>(stream);
   const unsigned tiles = unsigned(n * (32 / kStemTH));
