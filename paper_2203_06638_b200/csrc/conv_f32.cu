@@ -59,6 +59,23 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// Packed fp32 FMA (sm_100a FFMA2): two IEEE fp32 fmas per lane in one
+// instruction — the same results as two fmaf, half the issue slots.  A
+// (v, v) pair of one scalar compiles to FFMA2's scalar-broadcast operand.
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
 // stage NIMG x SROWS x SCOLS pixels of C channels (image rows y0-1 ..,
 // columns -1 .. W; zero outside the image) at pixel stride CP
 template <int C, int H, int W, int NIMG, int SROWS, int SCOLS, int CP, int THREADS>
@@ -306,6 +323,54 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
   const float* wcol = ws + cg * CO;
 
   float acc[PX][CO];
+  if constexpr (U / 10 == 2) {
+    // FFMA2: channel pairs (j, j+1) share one packed accumulator; the weight
+    // pairs come straight from the float4 broadcast loads
+    unsigned long long acc2[PX][CO / 2];
+#pragma unroll
+    for (int i = 0; i < PX; ++i)
+#pragma unroll
+      for (int j = 0; j < CO / 2; ++j) acc2[i][j] = 0ull;
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+#pragma unroll(U % 10)
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        float4 a[PX + 2];
+#pragma unroll
+        for (int j = 0; j < PX + 2; ++j)
+          a[j] = *reinterpret_cast<const float4*>(xrow + (j * K::SCOLS + s) * CP + c4 * 4);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const float* wp = wcol + ((r * 3 + s) * C + c4 * 4) * COT;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            unsigned long long wv2[CO / 2];
+#pragma unroll
+            for (int j = 0; j < CO; j += 4) {
+              const float4 t = *reinterpret_cast<const float4*>(wp + q * COT + j);
+              wv2[j / 2] = f2pack(t.x, t.y);
+              wv2[j / 2 + 1] = f2pack(t.z, t.w);
+            }
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+              const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : q == 2 ? a[i + r].z : a[i + r].w;
+              const unsigned long long av2 = f2pack(av, av);
+#pragma unroll
+              for (int j = 0; j < CO / 2; ++j) ffma2(acc2[i][j], av2, wv2[j]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PX; ++i)
+#pragma unroll
+      for (int j = 0; j < CO / 2; ++j) {
+        const float2 v = f2unpack(acc2[i][j]);
+        acc[i][2 * j] = v.x;
+        acc[i][2 * j + 1] = v.y;
+      }
+  } else {
 #pragma unroll
   for (int i = 0; i < PX; ++i)
 #pragma unroll
@@ -353,6 +418,7 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
         }
       }
     }
+  }
   }
 
 #pragma unroll
@@ -501,13 +567,11 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* par
   const int r = (tid / ((C / 4) * (COT / 4))) % 3;
   const int ps = tid / K::GROUP;
 
-  float acc[3][4][4];
+  unsigned long long acc2[3][4][2];              // FFMA2 accumulators: output-channel pairs
 #pragma unroll
   for (int s = 0; s < 3; ++s)
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+    for (int a = 0; a < 4; ++a) acc2[s][a][0] = acc2[s][a][1] = 0ull;
 
   constexpr int RPS = TH / PS;                      // tile rows per split
 #pragma unroll 1
@@ -521,20 +585,30 @@ k_wgrad3x3(const float* __restrict__ x, const float* __restrict__ dy, float* par
     for (int xx = 0; xx < W; ++xx) {
       const float4 xp = *reinterpret_cast<const float4*>(xr + (xx + 2) * CP);
       const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
-      const float dv[4] = {d.x, d.y, d.z, d.w};
+      const unsigned long long d01 = f2pack(d.x, d.y), d23 = f2pack(d.z, d.w);
       const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
 #pragma unroll
       for (int s = 0; s < 3; ++s)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+        for (int a = 0; a < 4; ++a) {                // FFMA2 over output-channel pairs
+          const unsigned long long x2 = f2pack(xv[s][a], xv[s][a]);
+          ffma2(acc2[s][a][0], x2, d01);
+          ffma2(acc2[s][a][1], x2, d23);
+        }
       xm = x0;
       x0 = xp;
     }
   }
 
   // 1. the CTA's partial [co][r][s][ci] (co in the tile), pixel splits in order
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const float2 lo = f2unpack(acc2[s][a][0]), hi = f2unpack(acc2[s][a][1]);
+      acc[s][a][0] = lo.x; acc[s][a][1] = lo.y; acc[s][a][2] = hi.x; acc[s][a][3] = hi.y;
+    }
   float* red = xs;
   __syncthreads();
 #pragma unroll 1
@@ -1097,13 +1171,11 @@ k_wgrad3x3s2(const float* __restrict__ x, const float* __restrict__ dy, float* p
   const int tid = threadIdx.x;
   const int ci4 = tid % (CI / 4), co4 = (tid / (CI / 4)) % (COT / 4);
   const int r = (tid / ((CI / 4) * (COT / 4))) % 3, ps = tid / K::GROUP;
-  float acc[3][4][4];
+  unsigned long long acc2[3][4][2];              // FFMA2 accumulators: output-channel pairs
 #pragma unroll
   for (int s = 0; s < 3; ++s)
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+    for (int a = 0; a < 4; ++a) acc2[s][a][0] = acc2[s][a][1] = 0ull;
   constexpr int RPS = TH / PS;
 #pragma unroll 1
   for (int ty = ps * RPS; ty < (ps + 1) * RPS; ++ty) {
@@ -1115,17 +1187,27 @@ k_wgrad3x3s2(const float* __restrict__ x, const float* __restrict__ dy, float* p
       const float4 x0 = *reinterpret_cast<const float4*>(xr + (2 * xx + 1) * CP);
       const float4 xp = *reinterpret_cast<const float4*>(xr + (2 * xx + 2) * CP);
       const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
-      const float dv[4] = {d.x, d.y, d.z, d.w};
+      const unsigned long long d01 = f2pack(d.x, d.y), d23 = f2pack(d.z, d.w);
       const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
 #pragma unroll
       for (int s = 0; s < 3; ++s)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+        for (int a = 0; a < 4; ++a) {                // FFMA2 over output-channel pairs
+          const unsigned long long x2 = f2pack(xv[s][a], xv[s][a]);
+          ffma2(acc2[s][a][0], x2, d01);
+          ffma2(acc2[s][a][1], x2, d23);
+        }
       xm = xp;
     }
   }
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const float2 lo = f2unpack(acc2[s][a][0]), hi = f2unpack(acc2[s][a][1]);
+      acc[s][a][0] = lo.x; acc[s][a][1] = lo.y; acc[s][a][2] = hi.x; acc[s][a][3] = hi.y;
+    }
   float* red = xs;
   __syncthreads();
 #pragma unroll 1
@@ -1602,13 +1684,11 @@ k_stem_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* p
   // thread -> (co4, r, row): 4 x 3 x 8
   const int tid = threadIdx.x;
   const int co4 = tid % 4, r = (tid / 4) % 3, ty = tid / 12;
-  float acc[3][4][4];
+  unsigned long long acc2[3][4][2];              // FFMA2 accumulators: output-channel pairs
 #pragma unroll
   for (int s = 0; s < 3; ++s)
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][a][c] = 0.f;
+    for (int a = 0; a < 4; ++a) acc2[s][a][0] = acc2[s][a][1] = 0ull;
   const float* xr = xs + ((ty + r) * SCOLS) * 4;
   const float* dr = ds + (ty * W) * DP + co4 * 4;
   float4 xm = *reinterpret_cast<const float4*>(xr);
@@ -1617,17 +1697,27 @@ k_stem_wgrad(const float* __restrict__ x, const float* __restrict__ dy, float* p
   for (int xx = 0; xx < W; ++xx) {
     const float4 xp = *reinterpret_cast<const float4*>(xr + (xx + 2) * 4);
     const float4 d = *reinterpret_cast<const float4*>(dr + xx * DP);
-    const float dv[4] = {d.x, d.y, d.z, d.w};
+    const unsigned long long d01 = f2pack(d.x, d.y), d23 = f2pack(d.z, d.w);
     const float xv[3][4] = {{xm.x, xm.y, xm.z, xm.w}, {x0.x, x0.y, x0.z, x0.w}, {xp.x, xp.y, xp.z, xp.w}};
 #pragma unroll
     for (int s = 0; s < 3; ++s)
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[s][a][c] = fmaf(xv[s][a], dv[c], acc[s][a][c]);
+      for (int a = 0; a < 4; ++a) {
+        const unsigned long long x2 = f2pack(xv[s][a], xv[s][a]);
+        ffma2(acc2[s][a][0], x2, d01);
+        ffma2(acc2[s][a][1], x2, d23);
+      }
     xm = x0;
     x0 = xp;
   }
+  float acc[3][4][4];
+#pragma unroll
+  for (int s = 0; s < 3; ++s)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const float2 lo = f2unpack(acc2[s][a][0]), hi = f2unpack(acc2[s][a][1]);
+      acc[s][a][0] = lo.x; acc[s][a][1] = lo.y; acc[s][a][2] = hi.x; acc[s][a][3] = hi.y;
+    }
   // rows in order: red[co][r][s][ci4] (576 floats) accumulated over the 8 row groups
   __shared__ __align__(16) float red[CO * 9 * 4];
   __syncthreads();
@@ -1666,18 +1756,19 @@ using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsi
 using TilesFn = size_t (*)(int);
 
 //                     C   H  TH COT PX CO U
-const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 1>, launch_conv<16, 32, 8, 16, 4, 8, 11>,
-                          launch_conv<16, 32, 8, 16, 4, 8, 2>, launch_conv<16, 32, 8, 16, 4, 8, 12>};
-const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 11>,
-                          launch_conv<32, 16, 16, 32, 4, 8, 1>, launch_conv<32, 16, 8, 32, 4, 8, 12>};
-const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 1>, launch_conv<64, 8, 8, 32, 2, 8, 11>,
-                          launch_conv<64, 8, 8, 32, 2, 16, 1>, launch_conv<64, 8, 8, 32, 2, 16, 11>};
-const TilesFn kConv16Ws[] = {conv_stats_workspace<16, 32, 8, 16, 4, 8, 1>, conv_stats_workspace<16, 32, 8, 16, 4, 8, 11>,
-                          conv_stats_workspace<16, 32, 8, 16, 4, 8, 2>, conv_stats_workspace<16, 32, 8, 16, 4, 8, 12>};
-const TilesFn kConv32Ws[] = {conv_stats_workspace<32, 16, 8, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 11>,
-                          conv_stats_workspace<32, 16, 16, 32, 4, 8, 1>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 12>};
-const TilesFn kConv64Ws[] = {conv_stats_workspace<64, 8, 8, 32, 2, 8, 1>, conv_stats_workspace<64, 8, 8, 32, 2, 8, 11>,
-                          conv_stats_workspace<64, 8, 8, 32, 2, 16, 1>, conv_stats_workspace<64, 8, 8, 32, 2, 16, 11>};
+// index 0 (the default): FFMA2, (s, c4) loop unrolled by 2; 1: plain FFMA
+const ConvFn kConv16[] = {launch_conv<16, 32, 8, 16, 4, 8, 22>, launch_conv<16, 32, 8, 16, 4, 8, 1>,
+                          launch_conv<16, 32, 8, 16, 4, 8, 21>, launch_conv<16, 32, 8, 16, 4, 16, 21>};
+const ConvFn kConv32[] = {launch_conv<32, 16, 8, 32, 4, 8, 22>, launch_conv<32, 16, 8, 32, 4, 8, 1>,
+                          launch_conv<32, 16, 8, 32, 4, 8, 21>, launch_conv<32, 16, 8, 32, 4, 16, 21>};
+const ConvFn kConv64[] = {launch_conv<64, 8, 8, 32, 2, 8, 22>, launch_conv<64, 8, 8, 32, 2, 8, 1>,
+                          launch_conv<64, 8, 8, 32, 2, 8, 21>, launch_conv<64, 8, 8, 32, 2, 16, 21>};
+const TilesFn kConv16Ws[] = {conv_stats_workspace<16, 32, 8, 16, 4, 8, 22>, conv_stats_workspace<16, 32, 8, 16, 4, 8, 1>,
+                          conv_stats_workspace<16, 32, 8, 16, 4, 8, 21>, conv_stats_workspace<16, 32, 8, 16, 4, 16, 21>};
+const TilesFn kConv32Ws[] = {conv_stats_workspace<32, 16, 8, 32, 4, 8, 22>, conv_stats_workspace<32, 16, 8, 32, 4, 8, 1>,
+                          conv_stats_workspace<32, 16, 8, 32, 4, 8, 21>, conv_stats_workspace<32, 16, 8, 32, 4, 16, 21>};
+const TilesFn kConv64Ws[] = {conv_stats_workspace<64, 8, 8, 32, 2, 8, 22>, conv_stats_workspace<64, 8, 8, 32, 2, 8, 1>,
+                          conv_stats_workspace<64, 8, 8, 32, 2, 8, 21>, conv_stats_workspace<64, 8, 8, 32, 2, 16, 21>};
 //                        C   H  TH COT PS CL
 const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32, 16, 16, 4, 16>,
                          launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
