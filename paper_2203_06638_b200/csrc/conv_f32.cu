@@ -953,11 +953,11 @@ k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __r
   const int lx = lane % HO, rg = lane / HO;
   const int ty0 = (pg * K::LR + rg) * PX;            // first output row of the thread (tile-relative)
   const float* wcol = ws + cg * CW;
-  float acc[PX][CW];
+  unsigned long long acc2[PX][CW / 2];                // FFMA2 over output-channel pairs
 #pragma unroll
   for (int i = 0; i < PX; ++i)
 #pragma unroll
-    for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < CW / 2; ++j) acc2[i][j] = 0ull;
 
 #pragma unroll 1
   for (int s = 0; s < 3; ++s) {
@@ -974,23 +974,34 @@ k_conv3x3s2(const float* __restrict__ x, const float* __restrict__ w, float* __r
         const float* wp = wcol + ((r * 3 + s) * CI + c4 * 4) * COT;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float wv[CW];
+          unsigned long long wv2[CW / 2];
 #pragma unroll
           for (int j = 0; j < CW; j += 4) {
             const float4 t = *reinterpret_cast<const float4*>(wp + q * COT + j);
-            wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+            wv2[j / 2] = f2pack(t.x, t.y);
+            wv2[j / 2 + 1] = f2pack(t.z, t.w);
           }
 #pragma unroll
           for (int i = 0; i < PX; ++i) {
             const float4 av4 = a[2 * i + r];
             const float av = q == 0 ? av4.x : q == 1 ? av4.y : q == 2 ? av4.z : av4.w;
+            const unsigned long long av2 = f2pack(av, av);
 #pragma unroll
-            for (int j = 0; j < CW; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+            for (int j = 0; j < CW / 2; ++j) ffma2(acc2[i][j], av2, wv2[j]);
           }
         }
       }
     }
   }
+  float acc[PX][CW];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int j = 0; j < CW / 2; ++j) {
+      const float2 v = f2unpack(acc2[i][j]);
+      acc[i][2 * j] = v.x;
+      acc[i][2 * j + 1] = v.y;
+    }
 #pragma unroll
   for (int i = 0; i < PX; ++i) {
     float* out = y + ((size_t(n) * HO + y0 + ty0 + i) * HO + lx) * CO + co0 + cg * CW;
@@ -1064,13 +1075,13 @@ k_conv3x3s2_dgrad(const float* __restrict__ dy, const float* __restrict__ w, flo
   const int tq0 = (pg * K::LR + rg) * PQ;            // first quad row (tile-relative)
   const float* wcol = ws + cg * CIW;
   // acc[quad][class ee, eo, oe, oo][ci]
-  float acc[PQ][4][CIW];
+  unsigned long long acc2[PQ][4][CIW / 2];            // FFMA2 over input-channel pairs
 #pragma unroll
   for (int i = 0; i < PQ; ++i)
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int j = 0; j < CIW; ++j) acc[i][c][j] = 0.f;
+      for (int j = 0; j < CIW / 2; ++j) acc2[i][c][j] = 0ull;
 
 #pragma unroll 1
   for (int c4 = 0; c4 < CO / 4; ++c4) {
@@ -1086,11 +1097,12 @@ k_conv3x3s2_dgrad(const float* __restrict__ dy, const float* __restrict__ w, flo
 #pragma unroll
       for (int tap = 0; tap < 9; ++tap) {
         const int r = tap / 3, s = tap % 3;
-        float wv[CIW];
+        unsigned long long wv2[CIW / 2];
 #pragma unroll
         for (int j = 0; j < CIW; j += 4) {
           const float4 t = *reinterpret_cast<const float4*>(wcol + (tap * CO + c4 * 4 + q) * CIT + j);
-          wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+          wv2[j / 2] = f2pack(t.x, t.y);
+          wv2[j / 2 + 1] = f2pack(t.z, t.w);
         }
         // class of the tap: rows r = 1 -> even (dY row yq), r = 0 -> odd from yq + 1, r = 2 -> odd from yq;
         // columns likewise
@@ -1101,12 +1113,24 @@ k_conv3x3s2_dgrad(const float* __restrict__ dy, const float* __restrict__ w, flo
         for (int i = 0; i < PQ; ++i) {
           const float4 v4 = right ? dr[i + dyr] : dl[i + dyr];
           const float v = q == 0 ? v4.x : q == 1 ? v4.y : q == 2 ? v4.z : v4.w;
+          const unsigned long long v2 = f2pack(v, v);
 #pragma unroll
-          for (int j = 0; j < CIW; ++j) acc[i][cls][j] = fmaf(v, wv[j], acc[i][cls][j]);
+          for (int j = 0; j < CIW / 2; ++j) ffma2(acc2[i][cls][j], v2, wv2[j]);
         }
       }
     }
   }
+  float acc[PQ][4][CIW];
+#pragma unroll
+  for (int i = 0; i < PQ; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < CIW / 2; ++j) {
+        const float2 v = f2unpack(acc2[i][c][j]);
+        acc[i][c][2 * j] = v.x;
+        acc[i][c][2 * j + 1] = v.y;
+      }
 #pragma unroll
   for (int i = 0; i < PQ; ++i)
 #pragma unroll
@@ -1612,11 +1636,11 @@ k_stem_conv(const float* __restrict__ x, const float* __restrict__ w, float* __r
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pg = warp % 2, cg = warp / 2;              // 2 pixel groups (4 rows each) x 2 channel groups
   const int ty0 = pg * PX;
-  float acc[PX][CW];
+  unsigned long long acc2[PX][CW / 2];                // FFMA2 over output-channel pairs
 #pragma unroll
   for (int i = 0; i < PX; ++i)
 #pragma unroll
-    for (int j = 0; j < CW; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < CW / 2; ++j) acc2[i][j] = 0ull;
 #pragma unroll
   for (int s = 0; s < 3; ++s) {
     float4 a[PX + 2];
@@ -1626,20 +1650,31 @@ k_stem_conv(const float* __restrict__ x, const float* __restrict__ w, float* __r
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        float wv[CW];
+        unsigned long long wv2[CW / 2];
 #pragma unroll
         for (int j = 0; j < CW; j += 4) {
           const float4 t = *reinterpret_cast<const float4*>(ws + ((r * 3 + s) * 4 + q) * CO + cg * CW + j);
-          wv[j] = t.x; wv[j + 1] = t.y; wv[j + 2] = t.z; wv[j + 3] = t.w;
+          wv2[j / 2] = f2pack(t.x, t.y);
+          wv2[j / 2 + 1] = f2pack(t.z, t.w);
         }
 #pragma unroll
         for (int i = 0; i < PX; ++i) {
           const float av = q == 0 ? a[i + r].x : q == 1 ? a[i + r].y : a[i + r].z;
+          const unsigned long long av2 = f2pack(av, av);
 #pragma unroll
-          for (int j = 0; j < CW; ++j) acc[i][j] = fmaf(av, wv[j], acc[i][j]);
+          for (int j = 0; j < CW / 2; ++j) ffma2(acc2[i][j], av2, wv2[j]);
         }
       }
   }
+  float acc[PX][CW];
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+#pragma unroll
+    for (int j = 0; j < CW / 2; ++j) {
+      const float2 v = f2unpack(acc2[i][j]);
+      acc[i][2 * j] = v.x;
+      acc[i][2 * j + 1] = v.y;
+    }
 #pragma unroll
   for (int i = 0; i < PX; ++i) {
     float* out = y + ((size_t(n) * H + y0 + ty0 + i) * W + lane) * CO + cg * CW;
