@@ -642,13 +642,14 @@ size_t lpp_conv3x3s2_stats_workspace(int n, int ci, int co, int hw_in);
  * writes save_mean / save_invstd (the backward's inputs, as
  * torch.native_batch_norm) and, when given, moves running_mean /
  * running_var by momentum (unbiased variance) — BatchNorm2d.forward
- * (+ the block's residual add and ReLU) in one memory pass. */
+ * (+ the block's residual add and ReLU) in one memory pass.  relu: also
+ * relu_mask, 1 bit per element (npix * c / 32 words), for the backward. */
 int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, const float* beta,
                      const float* resid, float* y, float* save_mean, float* save_invstd,
-                     float* running_mean, float* running_var, int64_t npix, int c, float eps,
-                     float momentum, int relu, void* stream);
+                     float* running_mean, float* running_var, uint32_t* relu_mask, int64_t npix, int c,
+                     float eps, float momentum, int relu, void* stream);
 /* its backward in two launches (a cluster-reduced per-channel sum, then
- * the elementwise pass): g = gy [* (y > 0)]; dx = gamma * invstd * (g -
+ * the elementwise pass): g = gy [* relu_mask]; dx = gamma * invstd * (g -
  * mean(g) - xhat * mean(g xhat)); gres = g (the residual branch, NULL:
  * none); ggamma / gbeta = sum g xhat / sum g (NULL: not wanted); dx NULL:
  * not wanted.  ws: lpp_bn_backward_workspace bytes; arrivals as
@@ -661,7 +662,8 @@ size_t lpp_bn_backward_workspace(int64_t npix, int c);
 size_t lpp_stem_workspace(int n);
 int lpp_stem_f32(const float* a, const float* b, float* out, int n, int mode, float* ws, size_t ws_bytes,
                  uint32_t* arrivals, float* stat_sums, void* stream);
-int lpp_bn_backward_f32(const float* gy, const float* y, const float* x, const float* mean, const float* invstd,
+int lpp_bn_backward_f32(const float* gy, const uint32_t* relu_mask, const float* x, const float* mean,
+                        const float* invstd,
                         const float* gamma, float* dx, float* gres, float* ggamma, float* gbeta, float* ws,
                         size_t ws_bytes, uint32_t* arrivals, int64_t npix, int c, int relu, void* stream);
 size_t lpp_conv1x1s2_wgrad_workspace(int n, int ci, int co, int hw_in);

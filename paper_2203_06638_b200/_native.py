@@ -237,7 +237,7 @@ _SIGS = {
                                         _c.c_int, _c.c_int, _vp]),
     "lpp_stem_workspace": (_size, [_c.c_int]),
     "lpp_stem_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _vp, _size, _vp, _vp, _vp]),
-    "lpp_bn_apply_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_int64, _c.c_int,
+    "lpp_bn_apply_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c.c_int64, _c.c_int,
                                      _c.c_float, _c.c_float, _c.c_int, _vp]),
     "lpp_conv3x3_wgrad_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3_wgrad_f32": (_c.c_int, [_vp, _vp, _vp, _vp, _size, _vp, _c.c_int, _c.c_int, _c.c_int, _vp]),

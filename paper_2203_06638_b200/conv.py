@@ -375,19 +375,22 @@ class _BnActFn(torch.autograd.Function):
         invstd = torch.empty(c, dtype=torch.float32, device=x.device)
         rm = running_mean.data_ptr() if running_mean is not None else None
         rv = running_var.data_ptr() if running_var is not None else None
+        # the ReLU mask (1 bit per element) is what the backward reads instead of y
+        mask = torch.empty(n * c * h * w_ // 32 if relu else 1, dtype=torch.int32, device=x.device)
         N.check(N.lib.lpp_bn_apply_f32(x.data_ptr(), sums.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
                                        resid.data_ptr() if resid is not None else None, y.data_ptr(),
-                                       mean.data_ptr(), invstd.data_ptr(), rm, rv, n * h * w_, c, float(eps),
+                                       mean.data_ptr(), invstd.data_ptr(), rm, rv,
+                                       mask.data_ptr() if relu else None, n * h * w_, c, float(eps),
                                        float(momentum), int(relu),
                                        torch.cuda.current_stream(x.device).cuda_stream), "bn_apply_f32")
-        ctx.save_for_backward(x, gamma, mean, invstd, y)
+        ctx.save_for_backward(x, gamma, mean, invstd, mask)
         ctx.relu, ctx.has_resid, ctx.cells = relu, resid is not None, cells
         return y
 
     @staticmethod
     def backward(ctx, gy):
         N = _lib()
-        x, gamma, mean, invstd, y = ctx.saved_tensors
+        x, gamma, mean, invstd, mask = ctx.saved_tensors
         n, c, h, w_ = x.shape
         need = ctx.needs_input_grad
         gy = gy.contiguous(memory_format=_CL)
@@ -398,7 +401,8 @@ class _BnActFn(torch.autograd.Function):
         nbytes = int(N.lib.lpp_bn_backward_workspace(n * h * w_, c))
         ws = torch.empty(nbytes // 4, dtype=torch.float32, device=x.device)
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        N.check(N.lib.lpp_bn_backward_f32(gy.data_ptr(), y.data_ptr(), x.data_ptr(), mean.data_ptr(),
+        N.check(N.lib.lpp_bn_backward_f32(gy.data_ptr(), mask.data_ptr() if ctx.relu else None, x.data_ptr(),
+                                          mean.data_ptr(),
                                           invstd.data_ptr(), gamma.data_ptr(), ptr(gx), ptr(gres), ptr(gg), ptr(gb),
                                           ws.data_ptr(), nbytes, ctx.cells.data_ptr(), n * h * w_, c, int(ctx.relu),
                                           torch.cuda.current_stream(x.device).cuda_stream), "bn_backward_f32")

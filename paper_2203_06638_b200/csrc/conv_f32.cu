@@ -1367,7 +1367,8 @@ __global__ void __launch_bounds__(256)
 k_bn_apply(const float4* __restrict__ x, const float* __restrict__ sums, const float* __restrict__ gamma,
            const float* __restrict__ beta, const float4* __restrict__ resid, float4* __restrict__ y,
            float* __restrict__ save_mean, float* __restrict__ save_invstd, float* __restrict__ running_mean,
-           float* __restrict__ running_var, size_t n4, double count, float eps, float momentum) {
+           float* __restrict__ running_var, unsigned* __restrict__ relu_mask, size_t n4, double count, float eps,
+           float momentum) {
   __shared__ __align__(16) float sc[C], sh[C];
   if (threadIdx.x < C) {
     const int c = threadIdx.x;
@@ -1389,29 +1390,45 @@ k_bn_apply(const float4* __restrict__ x, const float* __restrict__ sums, const f
   }
   __syncthreads();
   constexpr int C4 = C / 4;
-  for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
-    const int c = int(i % C4) * 4;
-    float4 v = __ldg(x + i);
-    v.x = fmaf(v.x, sc[c], sh[c]);
-    v.y = fmaf(v.y, sc[c + 1], sh[c + 1]);
-    v.z = fmaf(v.z, sc[c + 2], sh[c + 2]);
-    v.w = fmaf(v.w, sc[c + 3], sh[c + 3]);
-    if constexpr (RESID) {
-      const float4 r = __ldg(resid + i);
-      v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+  // warp-uniform trip count (the mask words are assembled with shuffles):
+  // lane l of a warp owns float4 i = base + l, 8 lanes form one 32-bit word
+  const int lane = threadIdx.x & 31;
+  for (size_t base = blockIdx.x * size_t(256) + (threadIdx.x & ~31u); base < n4; base += size_t(gridDim.x) * 256) {
+    const size_t i = base + lane;
+    unsigned nib = 0;
+    if (i < n4) {
+      const int c = int(i % C4) * 4;
+      float4 v = __ldg(x + i);
+      v.x = fmaf(v.x, sc[c], sh[c]);
+      v.y = fmaf(v.y, sc[c + 1], sh[c + 1]);
+      v.z = fmaf(v.z, sc[c + 2], sh[c + 2]);
+      v.w = fmaf(v.w, sc[c + 3], sh[c + 3]);
+      if constexpr (RESID) {
+        const float4 r = __ldg(resid + i);
+        v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+      }
+      if constexpr (RELU) {
+        nib = unsigned(v.x > 0.f) | unsigned(v.y > 0.f) << 1 | unsigned(v.z > 0.f) << 2 | unsigned(v.w > 0.f) << 3;
+        v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+      }
+      y[i] = v;
     }
-    if constexpr (RELU) {
-      v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+    if constexpr (RELU) {                           // the ReLU mask, 1 bit per element, for the backward
+      unsigned word = nib << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      if ((lane & 7) == 0 && i < n4) relu_mask[i >> 3] = word;
     }
-    y[i] = v;
   }
 }
 
 template <int C>
 int launch_bn_apply(const float* x, const float* sums, const float* gamma, const float* beta, const float* resid,
                     float* y, float* save_mean, float* save_invstd, float* running_mean, float* running_var,
-                    size_t npix, float eps, float momentum, int relu, cudaStream_t st) {
+                    unsigned* relu_mask, size_t npix, float eps, float momentum, int relu, cudaStream_t st) {
   const size_t n4 = npix * C / 4;
+  if (relu && (!relu_mask || n4 % 8)) return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: ReLU mask (n*c %% 32 == 0)");
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1425,7 +1442,7 @@ int launch_bn_apply(const float* x, const float* sums, const float* gamma, const
   const double cnt = double(npix);
 #define LPP_BN(R, S)                                                                                  \
   k_bn_apply<C, R, S><<<grid, 256, 0, st>>>(x4, sums, gamma, beta, r4, y4, save_mean, save_invstd,   \
-                                             running_mean, running_var, n4, cnt, eps, momentum)
+                                             running_mean, running_var, relu_mask, n4, cnt, eps, momentum)
   if (relu && resid) LPP_BN(true, true);
   else if (relu) LPP_BN(true, false);
   else if (resid) LPP_BN(false, true);
@@ -1459,7 +1476,7 @@ inline unsigned bn_reduce_ctas(size_t n4) {
 
 template <int C, bool RELU>
 __global__ void __launch_bounds__(256)
-k_bn_bwd_reduce(const float4* __restrict__ gy, const float4* __restrict__ y, const float4* __restrict__ x,
+k_bn_bwd_reduce(const float4* __restrict__ gy, const unsigned* __restrict__ relu_mask, const float4* __restrict__ x,
                 const float* __restrict__ mean, const float* __restrict__ invstd, float* part,
                 float* __restrict__ sums, unsigned* __restrict__ arrival, size_t n4) {
   constexpr int C4 = C / 4;
@@ -1473,9 +1490,9 @@ k_bn_bwd_reduce(const float4* __restrict__ gy, const float4* __restrict__ y, con
   for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
     float4 g = __ldg(gy + i);
     if constexpr (RELU) {
-      const float4 o = __ldg(y + i);
-      g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
-      g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+      const unsigned bits = __ldg(relu_mask + (i >> 3)) >> (4 * (i & 7));
+      g.x = bits & 1u ? g.x : 0.f; g.y = bits & 2u ? g.y : 0.f;
+      g.z = bits & 4u ? g.z : 0.f; g.w = bits & 8u ? g.w : 0.f;
     }
     const float4 v = __ldg(x + i);
     sg[0] += g.x; sg[1] += g.y; sg[2] += g.z; sg[3] += g.w;
@@ -1516,7 +1533,7 @@ k_bn_bwd_reduce(const float4* __restrict__ gy, const float4* __restrict__ y, con
 
 template <int C, bool RELU, bool DX, bool RESID>
 __global__ void __launch_bounds__(256)
-k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, const float4* __restrict__ x,
+k_bn_bwd_apply(const float4* __restrict__ gy, const unsigned* __restrict__ relu_mask, const float4* __restrict__ x,
                const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ gamma,
                const float* __restrict__ sums, float4* __restrict__ dx, float4* __restrict__ gres,
                float* __restrict__ ggamma, float* __restrict__ gbeta, size_t n4, float inv_count) {
@@ -1541,9 +1558,9 @@ k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, cons
     const int c = int(i % C4) * 4;
     float4 g = __ldg(gy + i);
     if constexpr (RELU) {
-      const float4 o = __ldg(y + i);
-      g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
-      g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+      const unsigned bits = __ldg(relu_mask + (i >> 3)) >> (4 * (i & 7));
+      g.x = bits & 1u ? g.x : 0.f; g.y = bits & 2u ? g.y : 0.f;
+      g.z = bits & 4u ? g.z : 0.f; g.w = bits & 8u ? g.w : 0.f;
     }
     if constexpr (RESID) gres[i] = g;
     if constexpr (DX) {
@@ -1560,7 +1577,8 @@ k_bn_bwd_apply(const float4* __restrict__ gy, const float4* __restrict__ y, cons
 }
 
 template <int C>
-int launch_bn_backward(const float* gy, const float* y, const float* x, const float* mean, const float* invstd,
+int launch_bn_backward(const float* gy, const unsigned* relu_mask, const float* x, const float* mean,
+                       const float* invstd,
                        const float* gamma, float* dx, float* gres, float* ggamma, float* gbeta, float* ws,
                        size_t ws_bytes, unsigned* arrivals, size_t npix, int relu, cudaStream_t st) {
   const size_t n4 = npix * C / 4;
@@ -1570,7 +1588,7 @@ int launch_bn_backward(const float* gy, const float* y, const float* x, const fl
   float* sums = ws;                                 // [C][2]
   float* part = ws + 2 * C;
   auto gy4 = reinterpret_cast<const float4*>(gy);
-  auto y4 = reinterpret_cast<const float4*>(y);
+  auto y4 = relu_mask;                              // the ReLU mask words (RELU only)
   auto x4 = reinterpret_cast<const float4*>(x);
   int rc = relu ? launch_clustered(k_bn_bwd_reduce<C, true>, dim3(rctas), 256, 0, 8, st, gy4, y4, x4, mean, invstd,
                                    part, sums, arrivals, n4)
@@ -1809,9 +1827,9 @@ const WgradFn kWg16[] = {launch_wgrad<16, 32, 16, 16, 4, 8>, launch_wgrad<16, 32
                          launch_wgrad<16, 32, 8, 16, 2, 16>, launch_wgrad<16, 32, 8, 16, 2, 8>};
 const TilesFn kWt16[] = {wgrad_partials<16, 32, 16, 16, 4, 8>, wgrad_partials<16, 32, 16, 16, 4, 16>,
                          wgrad_partials<16, 32, 8, 16, 2, 16>, wgrad_partials<16, 32, 8, 16, 2, 8>};
-const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1, 8>, launch_wgrad<32, 16, 8, 32, 1, 16>,
+const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1, 16>, launch_wgrad<32, 16, 8, 32, 1, 8>,
                          launch_wgrad<32, 16, 16, 32, 2, 8>, launch_wgrad<32, 16, 16, 32, 2, 16>};
-const TilesFn kWt32[] = {wgrad_partials<32, 16, 8, 32, 1, 8>, wgrad_partials<32, 16, 8, 32, 1, 16>,
+const TilesFn kWt32[] = {wgrad_partials<32, 16, 8, 32, 1, 16>, wgrad_partials<32, 16, 8, 32, 1, 8>,
                          wgrad_partials<32, 16, 16, 32, 2, 8>, wgrad_partials<32, 16, 16, 32, 2, 16>};
 const WgradFn kWg64[] = {launch_wgrad<64, 8, 8, 8, 1, 8>, launch_wgrad<64, 8, 8, 8, 1, 16>,
                          launch_wgrad<64, 8, 8, 32, 1, 8>, launch_wgrad<64, 8, 8, 16, 1, 16>};
@@ -1994,8 +2012,8 @@ extern "C" int lpp_conv3x3s2_f32(const float* a, const float* b, float* out, int
 
 extern "C" int lpp_bn_apply_f32(const float* x, const float* sums, const float* gamma, const float* beta,
                                 const float* resid, float* y, float* save_mean, float* save_invstd,
-                                float* running_mean, float* running_var, int64_t npix, int c, float eps,
-                                float momentum, int relu, void* stream) {
+                                float* running_mean, float* running_var, uint32_t* relu_mask, int64_t npix, int c,
+                                float eps, float momentum, int relu, void* stream) {
   if (!x || !sums || !gamma || !beta || !y || !save_mean || !save_invstd)
     return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: null pointer");
   if (npix < 2) return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: %lld pixels", (long long)npix);
@@ -2003,11 +2021,11 @@ extern "C" int lpp_bn_apply_f32(const float* x, const float* sums, const float* 
     return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: running mean and var go together");
   auto st = static_cast<cudaStream_t>(stream);
   if (c == 16) return launch_bn_apply<16>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
-                                          running_var, size_t(npix), eps, momentum, relu, st);
+                                          running_var, relu_mask, size_t(npix), eps, momentum, relu, st);
   if (c == 32) return launch_bn_apply<32>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
-                                          running_var, size_t(npix), eps, momentum, relu, st);
+                                          running_var, relu_mask, size_t(npix), eps, momentum, relu, st);
   if (c == 64) return launch_bn_apply<64>(x, sums, gamma, beta, resid, y, save_mean, save_invstd, running_mean,
-                                          running_var, size_t(npix), eps, momentum, relu, st);
+                                          running_var, relu_mask, size_t(npix), eps, momentum, relu, st);
   return set_err(LPP_E_VALUE, "lpp_bn_apply_f32: no kernel for %d channels", c);
 }
 
@@ -2017,19 +2035,19 @@ extern "C" size_t lpp_bn_backward_workspace(int64_t npix, int c) {
   return (size_t(r / 8 + 1) * 2 * c + 2 * c) * sizeof(float);
 }
 
-extern "C" int lpp_bn_backward_f32(const float* gy, const float* y, const float* x, const float* mean,
+extern "C" int lpp_bn_backward_f32(const float* gy, const uint32_t* relu_mask, const float* x, const float* mean,
                                    const float* invstd, const float* gamma, float* dx, float* gres, float* ggamma,
                                    float* gbeta, float* ws, size_t ws_bytes, uint32_t* arrivals, int64_t npix, int c,
                                    int relu, void* stream) {
-  if (!gy || !x || !mean || !invstd || !gamma || !ws || !arrivals || (relu && !y))
+  if (!gy || !x || !mean || !invstd || !gamma || !ws || !arrivals || (relu && !relu_mask))
     return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: null pointer");
   if (npix < 2) return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: %lld pixels", (long long)npix);
   auto st = static_cast<cudaStream_t>(stream);
-  if (c == 16) return launch_bn_backward<16>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+  if (c == 16) return launch_bn_backward<16>(gy, relu_mask, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
                                              arrivals, size_t(npix), relu, st);
-  if (c == 32) return launch_bn_backward<32>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+  if (c == 32) return launch_bn_backward<32>(gy, relu_mask, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
                                              arrivals, size_t(npix), relu, st);
-  if (c == 64) return launch_bn_backward<64>(gy, y, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
+  if (c == 64) return launch_bn_backward<64>(gy, relu_mask, x, mean, invstd, gamma, dx, gres, ggamma, gbeta, ws, ws_bytes,
                                              arrivals, size_t(npix), relu, st);
   return set_err(LPP_E_VALUE, "lpp_bn_backward_f32: no kernel for %d channels", c);
 }
