@@ -124,17 +124,21 @@ __device__ __forceinline__ void cluster_tail_reduce(cg::cluster_group& cluster, 
     }
     __stcg(cpart + i, a);
   }
-  __threadfence();
   cluster.sync();                                   // every slice written (and every DSMEM read done)
   if (k == 0 && tid == 0) {
+    // one thread fences for the cluster: cumulative over the barrier above
+    // (release of every CTA's slice) and, after the arrival, an acquire of
+    // the other clusters' partials for the barrier below to pass on.  The
+    // verdict goes into every CTA's own shared memory, so no CTA reads
+    // another's after the next barrier (which would need a fourth one).
+    __threadfence();
     const unsigned old = atomicAdd(arrival, 1u);
-    s_last = old == unsigned(nclusters - 1);
+    __threadfence();
+    const int v = old == unsigned(nclusters - 1);
+    for (int q = 0; q < cl; ++q) *cluster.map_shared_rank(&s_last, q) = v;
   }
   cluster.sync();
-  const int last = *cluster.map_shared_rank(&s_last, 0);
-  cluster.sync();                                   // rank 0's s_last read by all before it may exit
-  if (!last) return;
-  __threadfence();
+  if (!s_last) return;
   const float4* all = reinterpret_cast<const float4*>(part) + off4 + k * slice4;
   float4* out = reinterpret_cast<float4*>(dw) + off4 + k * slice4;
   // G thread groups split the cluster partials (group g: c = g, g + G, ...),
