@@ -1397,6 +1397,7 @@ k_bn_apply(const float4* __restrict__ x, const float* __restrict__ sums, const f
   // warp-uniform trip count (the mask words are assembled with shuffles):
   // lane l of a warp owns float4 i = base + l, 8 lanes form one 32-bit word
   const int lane = threadIdx.x & 31;
+#pragma unroll 4
   for (size_t base = blockIdx.x * size_t(256) + (threadIdx.x & ~31u); base < n4; base += size_t(gridDim.x) * 256) {
     const size_t i = base + lane;
     unsigned nib = 0;
@@ -1439,7 +1440,8 @@ int launch_bn_apply(const float* x, const float* sums, const float* gamma, const
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const unsigned grid = unsigned(std::min<size_t>((n4 + 255) / 256, size_t(sms) * 8));
+  // 4 float4 per thread (unrolled: their loads in flight together)
+  const unsigned grid = unsigned(std::min<size_t>((n4 + 1023) / 1024, size_t(sms) * 4));
   auto x4 = reinterpret_cast<const float4*>(x);
   auto r4 = reinterpret_cast<const float4*>(resid);
   auto y4 = reinterpret_cast<float4*>(y);
@@ -1472,7 +1474,7 @@ inline unsigned bn_reduce_ctas(size_t n4) {
                                                   cudaSuccess)
       sms = 148;
   }
-  size_t want = (n4 + 255) / 256;
+  size_t want = (n4 + 1023) / 1024;                 // 4 float4 per thread
   want = std::min<size_t>(want, size_t(sms) * 4);
   want = (want + 7) / 8 * 8;
   return unsigned(want);
@@ -1491,6 +1493,7 @@ k_bn_bwd_reduce(const float4* __restrict__ gy, const unsigned* __restrict__ relu
   const float4 mu = *reinterpret_cast<const float4*>(mean + 4 * q);
   const float4 is = *reinterpret_cast<const float4*>(invstd + 4 * q);
   float sg[4] = {0.f, 0.f, 0.f, 0.f}, sgx[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
   for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
     float4 g = __ldg(gy + i);
     if constexpr (RELU) {
@@ -1558,6 +1561,7 @@ k_bn_bwd_apply(const float4* __restrict__ gy, const unsigned* __restrict__ relu_
   }
   __syncthreads();
   if constexpr (DX || RESID) {
+#pragma unroll 4
   for (size_t i = blockIdx.x * size_t(256) + threadIdx.x; i < n4; i += size_t(gridDim.x) * 256) {
     const int c = int(i % C4) * 4;
     float4 g = __ldg(gy + i);
@@ -1600,7 +1604,7 @@ int launch_bn_backward(const float* gy, const unsigned* relu_mask, const float* 
                                    part, sums, arrivals, n4);
   if (rc) return rc;
   LAUNCH_CHECK("k_bn_bwd_reduce");
-  const unsigned actas = dx || gres ? unsigned(std::min<size_t>((n4 + 255) / 256, size_t(rctas) * 2)) : 1u;
+  const unsigned actas = dx || gres ? unsigned(std::min<size_t>((n4 + 1023) / 1024, size_t(rctas))) : 1u;
   const float inv = float(1.0 / double(npix));
   auto dx4 = reinterpret_cast<float4*>(dx);
   auto gr4 = reinterpret_cast<float4*>(gres);
