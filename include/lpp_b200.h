@@ -605,7 +605,9 @@ int lpp_fma_probe(float* out, int blocks, int iters, void* stream);
  * stat_sums[c][2] = (sum, sum of squares) over the n x hw x hw pixels, fused
  * into the epilogue and reduced in the same launch (fixed order, as
  * lpp_conv3x3_wgrad_f32), with stat_ws (lpp_conv3x3_stats_workspace bytes)
- * and LPP_CONV_ARRIVALS zeroed stat_arrivals cells. */
+ * and LPP_CONV_ARRIVALS zeroed stat_arrivals cells.  dgrad = 1 with
+ * stat_ws != NULL: y = dX + stat_ws (an NHWC addend of stat_ws_bytes >= the
+ * output's: the residual branch's gradient of the same activation). */
 int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int hw, int dgrad,
                     float* stat_ws, size_t stat_ws_bytes, float* stat_sums, uint32_t* stat_arrivals,
                     void* stream);

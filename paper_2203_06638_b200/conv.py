@@ -46,10 +46,11 @@ def _ohwi(w: torch.Tensor) -> torch.Tensor:
     return w.contiguous(memory_format=_CL)
 
 
-def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False, stats: torch.Tensor | None = None):
-    """y = conv(x, w) (dgrad: the input gradient for dY = x).  With
-    ``stats`` (LPP_CONV_ARRIVALS zeroed cells) also the fused BatchNorm
-    statistics of y: returns (y, sums[c][2])."""
+def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False, stats: torch.Tensor | None = None,
+             addend: torch.Tensor | None = None):
+    """y = conv(x, w) (dgrad: the input gradient for dY = x, plus
+    ``addend`` when given).  With ``stats`` (LPP_CONV_ARRIVALS zeroed
+    cells) also the fused BatchNorm statistics of y: returns (y, sums)."""
     N = _lib()
     n, c, h, _ = x.shape
     x = x.contiguous(memory_format=_CL)
@@ -57,8 +58,13 @@ def conv_fwd(x: torch.Tensor, w: torch.Tensor, dgrad: bool = False, stats: torch
     y = torch.empty_like(x, memory_format=_CL)
     stream = torch.cuda.current_stream(x.device).cuda_stream
     if stats is None:
-        N.check(N.lib.lpp_conv3x3_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, c, h, int(dgrad), None, 0, None,
-                                      None, stream), "conv3x3_f32")
+        add = None
+        if addend is not None:
+            add = addend.contiguous(memory_format=_CL)
+        N.check(N.lib.lpp_conv3x3_f32(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, c, h, int(dgrad),
+                                      add.data_ptr() if add is not None else None,
+                                      add.numel() * 4 if add is not None else 0, None, None, stream),
+                "conv3x3_f32")
         return y
     nbytes = int(N.lib.lpp_conv3x3_stats_workspace(n, c, h))
     ws = torch.empty(max(nbytes // 4, 1), dtype=torch.float32, device=x.device)
@@ -94,6 +100,13 @@ def conv_wgrad(x: torch.Tensor, dy: torch.Tensor, like: torch.Tensor,
                                         torch.cuda.current_stream(x.device).cuda_stream),
             "conv3x3_wgrad_f32")
     return dw
+
+
+# residual-branch gradients waiting for the dgrad of the block's first
+# convolution to add them in its epilogue (instead of an autograd add
+# kernel): {data_ptr of the block input: gradient}; set by _BnActFn's
+# backward, consumed by _Conv3x3Fn's, always within one backward pass
+_PENDING_RESID: dict[int, torch.Tensor] = {}
 
 
 def _will_run(node) -> bool:
@@ -263,10 +276,13 @@ class _Conv3x3Fn(torch.autograd.Function):
     def backward(ctx, gy, _gsums):
         x, w = ctx.saved_tensors
         gx = gw = None
+        pending = _PENDING_RESID.pop(x.data_ptr(), None)
         if gy is None:
-            return (None,) * len(ctx.needs_input_grad)
+            return (pending,) + (None,) * (len(ctx.needs_input_grad) - 1)
         if ctx.needs_input_grad[0] and _will_run(ctx.next_functions[0][0]):
-            gx = conv_fwd(gy, w, dgrad=True)
+            gx = conv_fwd(gy, w, dgrad=True, addend=pending)
+        elif pending is not None:
+            gx = pending
         if ctx.needs_input_grad[1] and ctx.want_w:
             gw = conv_wgrad(x, gy, w, ctx.arrivals)
         return gx, gw, None, None, None
@@ -316,6 +332,7 @@ class Conv3x3(nn.Conv2d):
                   and not torch.is_autocast_enabled("cuda") and x.shape[2] == x.shape[3] and enabled())
         if native and supported(self.in_channels, self.out_channels, x.shape[2], self.stride[0], 3):
             y, sums = _Conv3x3Fn.apply(x, self.weight, self._arrival_cells(x.device), self.want_w, self.bn_stats)
+            y._lpp_input_ptr = x.data_ptr()
             return _with_sums(y, sums)
         if (native and self.stride == (2, 2)
                 and _lib().lib.lpp_conv3x3s2_supported(self.in_channels, self.out_channels, x.shape[2])):
@@ -367,7 +384,8 @@ class _BnActFn(torch.autograd.Function):
     of torch.native_batch_norm_backward in train mode)."""
 
     @staticmethod
-    def forward(ctx, x, gamma, beta, resid, sums, running_mean, running_var, eps, momentum, relu, cells):
+    def forward(ctx, x, gamma, beta, resid, sums, running_mean, running_var, eps, momentum, relu, cells,
+                resid_consumer=None):
         N = _lib()
         n, c, h, w_ = x.shape
         y = torch.empty_like(x, memory_format=_CL)
@@ -385,6 +403,8 @@ class _BnActFn(torch.autograd.Function):
                                        torch.cuda.current_stream(x.device).cuda_stream), "bn_apply_f32")
         ctx.save_for_backward(x, gamma, mean, invstd, mask)
         ctx.relu, ctx.has_resid, ctx.cells = relu, resid is not None, cells
+        ctx.resid_ptr = resid.data_ptr() if resid is not None else None
+        ctx.resid_consumer = resid_consumer
         return y
 
     @staticmethod
@@ -406,10 +426,17 @@ class _BnActFn(torch.autograd.Function):
                                           invstd.data_ptr(), gamma.data_ptr(), ptr(gx), ptr(gres), ptr(gg), ptr(gb),
                                           ws.data_ptr(), nbytes, ctx.cells.data_ptr(), n * h * w_, c, int(ctx.relu),
                                           torch.cuda.current_stream(x.device).cuda_stream), "bn_backward_f32")
-        return gx, gg, gb, gres, None, None, None, None, None, None, None
+        consumer = ctx.resid_consumer
+        if (gres is not None and consumer is not None and _will_run(consumer)
+                and _will_run(consumer.next_functions[0][0])):
+            # the block's first convolution adds it in its dgrad epilogue
+            _PENDING_RESID[ctx.resid_ptr] = gres
+            gres = None
+        return gx, gg, gb, gres, None, None, None, None, None, None, None, None
 
 
-def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.Tensor | None = None):
+def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.Tensor | None = None,
+           resid_consumer: torch.Tensor | None = None):
     """``[relu](bn(x) [+ resid])``: one fused pass when x came from one of
     our convolutions with its statistics (``bn_stats``) and bn trains;
     torch's modules otherwise (cuDNN BatchNorm, eval mode, bf16, ...)."""
@@ -426,5 +453,13 @@ def bn_act(x: torch.Tensor, bn: nn.BatchNorm2d, relu: bool = True, resid: torch.
     if cells is None or cells.device != x.device:
         # the backward's one-launch reduction; this module's launches are stream-ordered
         cells = bn._lpp_arrivals = arrival_cells(x.device)
+    node = None
+    if resid_consumer is not None and resid is not None:
+        # resid_consumer: the output of the block's first convolution, whose
+        # input is resid — on our kernel its dgrad adds the residual gradient
+        fn = resid_consumer.grad_fn
+        if fn is not None and type(fn).__name__ == "_Conv3x3FnBackward" and \
+                resid.data_ptr() == resid_consumer._lpp_input_ptr:
+            node = fn
     return _BnActFn.apply(x, bn.weight, bn.bias, resid, sums, bn.running_mean, bn.running_var, bn.eps,
-                          bn.momentum, relu, cells)
+                          bn.momentum, relu, cells, node)

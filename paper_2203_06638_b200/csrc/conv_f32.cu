@@ -425,12 +425,22 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
   }
   }
 
+  // dgrad: stat_part is an optional addend (the residual branch's gradient
+  // of the same activation, summed here instead of by autograd)
+  const float* addend = DGRAD ? stat_part : nullptr;
 #pragma unroll
   for (int i = 0; i < PX; ++i) {
-    float* out = y + ((size_t(n0 + b) * H + y0 + ty0 + i) * W + lx) * C + co0 + cg * CO;
+    const size_t o = ((size_t(n0 + b) * H + y0 + ty0 + i) * W + lx) * C + co0 + cg * CO;
+    float* out = y + o;
 #pragma unroll
-    for (int j = 0; j < CO; j += 4)
-      *reinterpret_cast<float4*>(out + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+    for (int j = 0; j < CO; j += 4) {
+      float4 v = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+      if (addend) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(addend + o + j));
+        v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      }
+      *reinterpret_cast<float4*>(out + j) = v;
+    }
   }
   if constexpr (!DGRAD) {
     if (stat_sums) {                                // BatchNorm statistics of y (uniform branch)
@@ -478,7 +488,7 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, flo
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
       attr = true;
     }
-    kern<<<grid, K::THREADS, K::SMEM, st>>>(x, w, y, nullptr, nullptr, nullptr);
+    kern<<<grid, K::THREADS, K::SMEM, st>>>(x, w, y, stat_ws, nullptr, nullptr);   // stat_ws: addend
   } else {
     auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, false>;
     static bool attr = false;
@@ -1906,6 +1916,8 @@ extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, 
   if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
   if (dgrad && stat_sums) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics are a forward epilogue");
+  if (dgrad && stat_ws && stat_ws_bytes < size_t(n) * hw * hw * c * sizeof(float))
+    return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: dgrad addend too small");
   auto st = static_cast<cudaStream_t>(stream);
   const int v = conv_variant(c);
   if (c == 16 && hw == 32)

@@ -352,9 +352,12 @@ class _Basic(nn.Module):
         self.conv1.bn_stats = self.conv2.bn_stats = True
 
     def forward(self, x):
-        out = bn_act(self.conv1(x), self.bn1, relu=True)
+        c1 = self.conv1(x)
+        out = bn_act(c1, self.bn1, relu=True)
         sc = x if self.shortcut is None else bn_act(self.shortcut[0](x), self.shortcut[1], relu=False)
-        return bn_act(self.conv2(out), self.bn2, relu=True, resid=sc)
+        # identity blocks: conv1's dgrad adds the residual gradient of x
+        return bn_act(self.conv2(out), self.bn2, relu=True, resid=sc,
+                      resid_consumer=c1 if self.shortcut is None else None)
 
 
 class _Bottleneck(nn.Module):
