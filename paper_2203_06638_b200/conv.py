@@ -1,15 +1,22 @@
-"""fp32 3x3 stride-1 C->C convolutions on the library's own kernels
-(``csrc/conv_f32.cu``) — the CNN forward/backward of SURVEY §8 a6 in fp32.
+"""The fp32 CNN forward/backward on the library's own kernels
+(``csrc/conv_f32.cu``) — the gradient step of SURVEY §8 a6 in fp32.
 
-``Conv3x3`` is an ``nn.Conv2d`` (same parameters, init and state-dict
-names) whose forward runs ``lpp_conv3x3_f32`` / ``lpp_conv3x3_wgrad_f32``
-when the activation is fp32 on a CUDA device and the (channels, size) pair
-has a kernel — CIFAR ResNet-20's 16 stride-1 3x3 convolutions — and is
-cuDNN's ``F.conv2d`` otherwise (bf16 compute or autocast, other shapes).  The kernels
-take NHWC activations (torch channels_last) and OHWI weights (the arena's
-channels_last view, ``objectives.py`` ``_view``), so no layout change runs
-around them.  Launches go to torch's current stream: they are captured into
-the step graphs like cuDNN's.
+* ``Conv3x3`` / ``Conv1x1`` are ``nn.Conv2d``s (same parameters, init and
+  state-dict names) whose forward runs our kernels when the activation is
+  fp32 on a CUDA device and the shape has one — every convolution of CIFAR
+  ResNet-20: the stem (on the gathered NCHW batch), the 3x3 stride-1 and
+  stride-2 convolutions and the 1x1 stride-2 projections — and cuDNN's
+  ``F.conv2d`` otherwise (bf16 compute or autocast, other shapes,
+  ``LPP_CONV=cudnn``).  Forward (optionally with the output's BatchNorm
+  statistics in the epilogue), input gradient (optionally adding the
+  residual branch's gradient), weight gradient (one deterministic launch).
+* ``bn_act`` is BatchNorm2d (train) [+ residual] [+ ReLU] in one pass each
+  way from those statistics, torch's modules when they are absent.
+
+NHWC activations (torch channels_last) and OHWI weights (the arena's
+channels_last view, ``objectives.py`` ``_view``): no layout change runs
+around the kernels.  Launches go to torch's current stream, so they are
+captured into the step graphs like cuDNN's.
 """
 
 from __future__ import annotations
