@@ -1,10 +1,16 @@
-// conv_f32.cu — fp32 3x3 stride-1 pad-1 C->C convolutions over NHWC
-// activations, the 16 of CIFAR ResNet-20's 19 convolutions that dominate the
-// fp32 step (the gradient of the mean batch loss; on the GPU
-// the CNN forward/backward).  cuDNN runs these at 6-16 TFLOP/s on B200 with
-// TF32 off (profiles/r2_conv_cudnn_f32.txt); this is plain FFMA arithmetic in
-// fp32 (no TF32, no split-precision tricks), so results agree with cuDNN's
-// fp32 algorithms to summation order.
+// conv_f32.cu — the fp32 CNN of the headline step on our own kernels: every
+// convolution of CIFAR ResNet-20 over NHWC activations (3x3 stride 1 and 2,
+// the 1x1 stride-2 projections, the 3->16 stem), forward / input gradient /
+// weight gradient, with the BatchNorm statistics fused into the forward
+// epilogues and BatchNorm + residual + ReLU in one pass each way (SURVEY §8
+// a6: the gradient of the mean batch loss; on the GPU the CNN
+// forward/backward).  cuDNN runs these convolutions at 6-16 TFLOP/s on B200
+// with TF32 off (profiles/r2_conv_cudnn_f32.txt); this is plain fp32 FMA
+// arithmetic (no TF32, no split-precision tricks), issued as FFMA2 (two
+// IEEE fmas per instruction), so results agree with cuDNN's fp32 algorithms
+// to summation order.  Cross-CTA reductions (weight gradients, BatchNorm
+// statistics) run inside the producing launch over thread-block-cluster
+// DSMEM and a last-cluster pass, in a fixed order (cluster_tail_reduce).
 //
 // Forward and data-gradient share one kernel: dgrad of a 3x3 / pad-1 /
 // stride-1 convolution is the same convolution of dY with the weights
