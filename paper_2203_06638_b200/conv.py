@@ -273,6 +273,9 @@ class _Conv3x3Fn(torch.autograd.Function):
         ctx.set_materialize_grads(False)    # no zero-filled gradient for the statistics output
         ctx.save_for_backward(x, w)
         ctx.arrivals, ctx.want_w = arrivals, want_w
+        # a residual gradient left for an earlier tensor at this address (a
+        # backward that raised between the hand-off and this dgrad) is stale
+        _PENDING_RESID.pop(x.data_ptr(), None)
         if with_stats:
             y, sums = conv_fwd(x, w, stats=_stat_cells(arrivals))
             ctx.mark_non_differentiable(sums)
