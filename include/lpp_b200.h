@@ -600,7 +600,8 @@ int lpp_conv3x3_supported(int c, int hw);
  * FFMAs (8 chains per thread), no memory traffic — the fp32 FMA peak the
  * convolutions' roofline divides by (2 flops per FFMA) */
 int lpp_fma_probe(float* out, int blocks, int iters, void* stream);
-/* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x.
+/* dgrad = 0: y = conv(x, w); dgrad = 1: y = dX of conv for dY = x;
+ * dgrad = 2: y = conv(x, w) with w tap-major (lpp_conv3x3_tapmajor).
  * Forward only, stat_sums != NULL: also the BatchNorm statistics of y,
  * stat_sums[c][2] = (sum, sum of squares) over the n x hw x hw pixels, fused
  * into the epilogue and reduced in the same launch (fixed order, as
@@ -612,6 +613,9 @@ int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, int c, int 
                     float* stat_ws, size_t stat_ws_bytes, float* stat_sums, uint32_t* stat_arrivals,
                     void* stream);
 size_t lpp_conv3x3_stats_workspace(int n, int c, int hw);
+/* wt[t][ci][co] = w[co][t][ci]: tap-major weights for lpp_conv3x3_f32's
+ * dgrad = 2 (a forward whose weights need no per-CTA transpose) */
+int lpp_conv3x3_tapmajor(const float* w, float* wt, int c, void* stream);
 /* bytes of workspace lpp_conv3x3_wgrad_f32 needs (per-cluster partial sums) */
 size_t lpp_conv3x3_wgrad_workspace(int n, int c, int hw);
 /* dw = sum over pixels of x (*) dy in ONE launch, deterministic: CTA

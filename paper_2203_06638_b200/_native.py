@@ -230,6 +230,7 @@ _SIGS = {
     "lpp_conv3x3_f32": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp, _size, _vp, _vp,
                                     _vp]),
     "lpp_conv3x3_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int]),
+    "lpp_conv3x3_tapmajor": (_c.c_int, [_vp, _vp, _c.c_int, _vp]),
     "lpp_conv1x1s2_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
     "lpp_conv3x3s2_stats_workspace": (_size, [_c.c_int, _c.c_int, _c.c_int, _c.c_int]),
     "lpp_bn_backward_workspace": (_size, [_c.c_int64, _c.c_int]),

@@ -277,7 +277,10 @@ struct ConvCfg {
   static_assert(C % COT == 0 && COT % CO == 0 && CO % 4 == 0 && C % 4 == 0, "channels");
 };
 
-template <int C, int H, int TH, int COT, int PX, int CO, int U, bool DGRAD>
+// MODE 0: forward, weights OHWI (transposed while staged); 1: dgrad; 2:
+// forward, weights already tap-major [t][ci][co] (k_w_tapmajor), staged
+// with 16-byte copies like dgrad's
+template <int C, int H, int TH, int COT, int PX, int CO, int U, int MODE>
 __global__ void __launch_bounds__(ConvCfg<C, H, TH, COT, PX, CO>::THREADS)
 k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, float* stat_part,
           float* __restrict__ stat_sums, unsigned* __restrict__ stat_arrivals) {
@@ -299,7 +302,15 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
   // stage the weight slice as ws[tap][k][j] (j = output channel of the tile)
   {
     constexpr int C4 = C / 4;
-    if constexpr (!DGRAD) {
+    if constexpr (MODE == 2) {
+      // ws[t][ci][co - co0] rows straight from the tap-major weights
+      constexpr int J4 = COT / 4;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < 9 * C * J4; i += K::THREADS) {
+        const int j4 = i % J4, k = i / J4;          // k = t * C + ci
+        cp_async16(ws + k * COT + j4 * 4, w + size_t(k) * C + co0 + j4 * 4, true);
+      }
+    } else if constexpr (MODE == 0) {
       // y[.., co] = sum x[.., ci] w[co][r][s][ci]: ws[t][ci][co - co0], a
       // transpose — lanes take consecutive co so the scalar stores are
       // conflict-free
@@ -433,7 +444,7 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
 
   // dgrad: stat_part is an optional addend (the residual branch's gradient
   // of the same activation, summed here instead of by autograd)
-  const float* addend = DGRAD ? stat_part : nullptr;
+  const float* addend = MODE == 1 ? stat_part : nullptr;
 #pragma unroll
   for (int i = 0; i < PX; ++i) {
     const size_t o = ((size_t(n0 + b) * H + y0 + ty0 + i) * W + lx) * C + co0 + cg * CO;
@@ -448,7 +459,7 @@ k_conv3x3(const float* __restrict__ x, const float* __restrict__ w, float* __res
       *reinterpret_cast<float4*>(out + j) = v;
     }
   }
-  if constexpr (!DGRAD) {
+  if constexpr (MODE != 1) {
     if (stat_sums) {                                // BatchNorm statistics of y (uniform branch)
       float* red = xs;
       tile_channel_stats<PX, CO, K::NPG, K::NCG>(acc, PX, pg, cg, xs + 2 * COT, red);
@@ -480,15 +491,15 @@ size_t conv_stats_workspace(int n) {
 }
 
 template <int C, int H, int TH, int COT, int PX, int CO, int U>
-int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, float* stat_ws, size_t stat_ws_bytes,
+int launch_conv(const float* x, const float* w, float* y, int n, int mode, float* stat_ws, size_t stat_ws_bytes,
                 float* stat_sums, unsigned* stat_arrivals, cudaStream_t st) {
   using K = ConvCfg<C, H, TH, COT, PX, CO>;
   static_assert(COT % 8 == 0, "statistics slices (COT / 2 float4s over up to 8 cluster ranks... >= 1 each)");
   if (n % K::NIMG) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d not a multiple of %d", n, K::NIMG);
   const size_t ptiles = conv_ptiles<C, H, TH, COT, PX, CO, U>(n);
   const dim3 grid(unsigned(ptiles), C / COT, 1);
-  if (dgrad) {
-    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, true>;
+  if (mode == 1) {
+    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, 1>;
     static bool attr = false;
     if (!attr) {
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
@@ -496,11 +507,11 @@ int launch_conv(const float* x, const float* w, float* y, int n, bool dgrad, flo
     }
     kern<<<grid, K::THREADS, K::SMEM, st>>>(x, w, y, stat_ws, nullptr, nullptr);   // stat_ws: addend
   } else {
-    auto kern = k_conv3x3<C, H, TH, COT, PX, CO, U, false>;
-    static bool attr = false;
-    if (!attr) {
+    auto kern = mode == 2 ? k_conv3x3<C, H, TH, COT, PX, CO, U, 2> : k_conv3x3<C, H, TH, COT, PX, CO, U, 0>;
+    static bool attr[2] = {false, false};
+    if (!attr[mode == 2]) {
       CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
-      attr = true;
+      attr[mode == 2] = true;
     }
     if (stat_sums) {
       if (!stat_ws || !stat_arrivals) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics need ws + arrivals");
@@ -1825,10 +1836,20 @@ size_t stem_partials(int n) {
   return tiles / wgrad_cluster(tiles, 8);
 }
 
+// wt[t][ci][co] = w[co][t][ci] (OHWI -> tap-major): once per forward call,
+// instead of every CTA transposing its slice while staging (k_conv3x3 MODE 2)
+__global__ void __launch_bounds__(256) k_w_tapmajor(const float* __restrict__ w, float* __restrict__ wt, int c) {
+  const int total = 9 * c * c;
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    const int co = i % c, ci = (i / c) % c, t = i / (c * c);
+    wt[i] = __ldg(w + (size_t(co) * 9 + t) * c + ci);
+  }
+}
+
 // the ResNet-20 shapes (C, H): tile configurations.  Index 0 is the
 // default; LPP_CONV_VARIANT / LPP_WGRAD_VARIANT pick another (tuning runs,
 // tools/exp_conv_native.py).
-using ConvFn = int (*)(const float*, const float*, float*, int, bool, float*, size_t, float*, unsigned*, cudaStream_t);
+using ConvFn = int (*)(const float*, const float*, float*, int, int, float*, size_t, float*, unsigned*, cudaStream_t);
 using WgradFn = int (*)(const float*, const float*, float*, float*, size_t, unsigned*, int, cudaStream_t);
 using TilesFn = size_t (*)(int);
 
@@ -1921,17 +1942,18 @@ extern "C" int lpp_conv3x3_f32(const float* x, const float* w, float* y, int n, 
                                void* stream) {
   if (!x || !w || !y) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: null pointer");
   if (n <= 0) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: batch %d", n);
-  if (dgrad && stat_sums) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics are a forward epilogue");
-  if (dgrad && stat_ws && stat_ws_bytes < size_t(n) * hw * hw * c * sizeof(float))
+  if (dgrad < 0 || dgrad > 2) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: mode %d", dgrad);
+  if (dgrad == 1 && stat_sums) return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: statistics are a forward epilogue");
+  if (dgrad == 1 && stat_ws && stat_ws_bytes < size_t(n) * hw * hw * c * sizeof(float))
     return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: dgrad addend too small");
   auto st = static_cast<cudaStream_t>(stream);
   const int v = conv_variant(c);
   if (c == 16 && hw == 32)
-    return kConv16[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
+    return kConv16[v](x, w, y, n, dgrad, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
   if (c == 32 && hw == 16)
-    return kConv32[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
+    return kConv32[v](x, w, y, n, dgrad, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
   if (c == 64 && hw == 8)
-    return kConv64[v](x, w, y, n, dgrad != 0, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
+    return kConv64[v](x, w, y, n, dgrad, stat_ws, stat_ws_bytes, stat_sums, stat_arrivals, st);
   return set_err(LPP_E_VALUE, "lpp_conv3x3_f32: no kernel for C=%d H=W=%d", c, hw);
 }
 
@@ -2107,5 +2129,13 @@ extern "C" int lpp_stem_f32(const float* a, const float* b, float* out, int n, i
   int rc = launch_clustered(k_stem_wgrad, dim3(tiles), 96, 0, cl, st, a, b, ws, out, arrivals);
   if (rc) return rc;
   LAUNCH_CHECK("k_stem_wgrad");
+  return 0;
+}
+
+extern "C" int lpp_conv3x3_tapmajor(const float* w, float* wt, int c, void* stream) {
+  if (!w || !wt || c <= 0 || c % 4) return set_err(LPP_E_VALUE, "lpp_conv3x3_tapmajor: bad argument");
+  const int total = 9 * c * c;
+  k_w_tapmajor<<<(total + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(w, wt, c);
+  LAUNCH_CHECK("k_w_tapmajor");
   return 0;
 }

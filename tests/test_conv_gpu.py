@@ -334,8 +334,10 @@ def test_basic_block_fused_bn_matches_fp64(cin, cout, stride, hw):
     for (name, b), (_, bd) in zip(blk.named_buffers(), ref.named_buffers()):
         if b.dtype.is_floating_point:
             assert _rel(b, bd) < tol, name
-    # conv + BatchNorm pass per convolution: 2 x 2, plus 2 for the projection
-    assert n_fwd == (4 if blk.shortcut is None else 6)
+    # conv + BatchNorm pass per convolution: 2 x 2, plus 2 for the projection,
+    # plus the tap-major weight copy of each stride-1 forward with C >= 32
+    tapmajor = sum(1 for m in (blk.conv1, blk.conv2) if m.stride == (1, 1) and m.out_channels >= 32)
+    assert n_fwd == (4 if blk.shortcut is None else 6) + tapmajor
 
 
 @pytest.mark.parametrize("n", [1, 3, 128])
@@ -382,7 +384,9 @@ def test_resnet20_native_matches_fp64(monkeypatch):
     gy = torch.randn(64, 10, device="cuda")
     l0 = N.launch_count()
     y = model(x)
-    assert N.launch_count() - l0 == 21 + 21          # stem + 18 + 2 projections, one BatchNorm pass each
+    # stem + 18 + 2 projections, one BatchNorm pass each, and the tap-major
+    # weight copy of the 10 stride-1 forwards with C >= 32
+    assert N.launch_count() - l0 == 21 + 21 + 10
     y.backward(gy)
     yd = ref(x.double())
     yd.backward(gy.double())
