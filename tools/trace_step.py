@@ -47,7 +47,7 @@ for n, _, d in rows:
 T = sum(tot.values())
 OURS = ("k_apply", "k_snapshot", "k_average", "k_accum", "k_gather", "k_publish", "k_set_i64",
         "k_classify", "k_sample", "k_conv3x3", "k_wgrad3x3", "k_wgrad_reduce", "k_conv1x1s2",
-        "k_fma_probe", "k_bn_apply", "k_bn_bwd", "k_stem")
+        "k_fma_probe", "k_bn_apply", "k_bn_bwd", "k_stem", "k_w_tapmajor")
 
 
 def is_ours(k):
