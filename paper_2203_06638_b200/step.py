@@ -129,7 +129,11 @@ class StepProgram:
                         for buf in range(self.nbuf):
                             g = torch.cuda.CUDAGraph()
                             l0 = _lib_launches()
-                            with torch.cuda.graph(g, pool=pool, stream=stream):
+                            # thread_local: a CUDA call on another thread (NCCL's
+                            # watchdog polling its events on multi-GPU jobs)
+                            # must not invalidate this capture
+                            with torch.cuda.graph(g, pool=pool, stream=stream,
+                                                  capture_error_mode="thread_local"):
                                 self._body(bid, buf)
                             self.graph_kernels[(bid, buf)] = _lib_launches() - l0
                             pool = g.pool()
