@@ -1877,9 +1877,9 @@ const WgradFn kWg32[] = {launch_wgrad<32, 16, 8, 32, 1, 16>, launch_wgrad<32, 16
 const TilesFn kWt32[] = {wgrad_partials<32, 16, 8, 32, 1, 16>, wgrad_partials<32, 16, 8, 32, 1, 8>,
                          wgrad_partials<32, 16, 16, 32, 2, 8>, wgrad_partials<32, 16, 16, 32, 2, 16>};
 const WgradFn kWg64[] = {launch_wgrad<64, 8, 8, 8, 1, 8>, launch_wgrad<64, 8, 8, 8, 1, 16>,
-                         launch_wgrad<64, 8, 8, 32, 1, 8>, launch_wgrad<64, 8, 8, 16, 1, 16>};
+                         launch_wgrad<64, 8, 16, 8, 2, 8>, launch_wgrad<64, 8, 16, 8, 2, 16>};
 const TilesFn kWt64[] = {wgrad_partials<64, 8, 8, 8, 1, 8>, wgrad_partials<64, 8, 8, 8, 1, 16>,
-                         wgrad_partials<64, 8, 8, 32, 1, 8>, wgrad_partials<64, 8, 8, 16, 1, 16>};
+                         wgrad_partials<64, 8, 16, 8, 2, 8>, wgrad_partials<64, 8, 16, 8, 2, 16>};
 
 // "i" (every shape) or "i,j,k" (C = 16, 32, 64)
 int env_variant(const char* name, int which) {
